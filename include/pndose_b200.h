@@ -1,0 +1,126 @@
+/* Drop-in C-ABI of the B200 collided-flux DLRA stepper (libpndose_b200.so).
+ *
+ * The reference (`pndose`, pure Python) has no FFI; its boundary for this hot
+ * path is the Python API of pkg/src/pndose/dlra.py, spatial.py, raytracer.py
+ * and the energy loop of driver.py. Each entry point below replaces one of
+ * those reference interfaces (cited per function); the Python shim
+ * paper_2508_04484_b200/{dlra,spatial,raytracer,driver}.py binds them with
+ * ctypes and keeps the reference's names, argument meanings and exceptions.
+ *
+ * Conventions
+ *   - every function returns 0 on success or the reference's exit category:
+ *     2 ConfigError, 3 PhysicsDataError, 4 NumericalError, 5 OutputIOError
+ *     (pkg/src/pndose/errors.py:13-31), 6 for a CUDA runtime failure;
+ *     pnd_last_error() copies the message (the shim raises the matching
+ *     Python class with it, so message fragments such as "column" or
+ *     "rank_max" match the reference's);
+ *   - host arrays are C-contiguous float64 (int32 for indices), read or
+ *     written only during the call; n = nx*ny*nz cells in the flat order
+ *     k*nx*ny + j*nx + i (spatial.py:62-63), m = (N+1)^2 moments;
+ *   - all device memory is owned by the handle; calls on one handle are
+ *     stream-ordered and not thread-safe.
+ */
+#ifndef PNDOSE_B200_H
+#define PNDOSE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pnd_handle pnd_handle;
+
+/* ---- lifecycle ------------------------------------------------------- */
+/* Grid3D + n_moments of an assembled problem (spatial.py:32-78). Raises
+ * ConfigError for a 2-cell axis (spatial.py:84-88, "3-point"). */
+int pnd_create(pnd_handle** h, int nx, int ny, int nz, double dx, double dy, double dz, int m,
+               int device);
+int pnd_destroy(pnd_handle* h);
+int pnd_last_error(pnd_handle* h, char* buf, size_t len);
+int pnd_synchronize(pnd_handle* h);
+/* bytes of device memory held by the handle */
+int pnd_device_bytes(pnd_handle* h, double* bytes);
+
+/* ---- frozen operators / per-step coefficients (driver.py:523-538) --- */
+/* A_d^+- = V_d diag(lambda_d^+-) V_d^T, 3 x m x m each (replaces
+ * PNOperators.eig_v/lam_plus/lam_minus as used by dlra.py:155-194). */
+int pnd_set_angular(pnd_handle* h, const double* a_plus, const double* a_minus);
+/* Material classes: cell_class (n) indexes class_atomic (n_class x 12)
+ * atomic densities N_i (ScatteringContext.element_weights, dlra.py:240). */
+int pnd_set_materials(pnd_handle* h, const int32_t* cell_class, int n_class,
+                      const double* class_atomic);
+/* 1/S per cell (StreamingContext.inv_s / ScatteringContext.inv_s). */
+int pnd_set_inv_s(pnd_handle* h, const double* inv_s);
+/* S(E_mid) per class -> inv_s and the S field on device (Problem.stopping_field,
+ * driver.py:331-335, gathered per cell on the GPU). */
+int pnd_set_class_stopping(pnd_handle* h, const double* class_s);
+/* g_diags (12 x m) and sigma_t (12) of Problem.scattering_tables (driver.py:337-362). */
+int pnd_set_scattering(pnd_handle* h, const double* g_diags, const double* sigma_t);
+/* Uncollided sources [(psi_u (n), T_M (m))] (ScatteringContext.sources). */
+int pnd_set_sources(pnd_handle* h, int n_beams, const double* psi, const double* t_m);
+/* Device-resident group table of one beam's uncollided flux (UncollidedFlux.values,
+ * n x G row-major) and its T_M; pnd_select_flux then forms at_energy() on the GPU
+ * (raytracer.py:440-449): which = 0 -> source slice (E_mid), 1 -> tally slice (E_lo). */
+int pnd_set_flux_table(pnd_handle* h, int beam, int n_beams, int n_groups, const double* values,
+                       const double* t_m);
+int pnd_select_flux(pnd_handle* h, int which, const int32_t* j0, const double* w0,
+                    const int32_t* j1, const double* w1);
+
+/* ---- low-rank state (LowRankState, dlra.py:46-72) --------------------- */
+int pnd_state_set(pnd_handle* h, int ru, int rv, const double* u, const double* s, const double* v);
+int pnd_state_shape(pnd_handle* h, int* ru, int* rv);
+int pnd_state_get(pnd_handle* h, double* u, double* s, double* v);
+
+/* ---- the hot path ----------------------------------------------------- */
+/* streaming_step(state, dt, ctx) (dlra.py:213-225): state -> augmented state. */
+int pnd_streaming_step(pnd_handle* h, double dt);
+/* scattering_step(state, dt, ctx) (dlra.py:270-322). */
+int pnd_scattering_step(pnd_handle* h, double dt);
+/* truncate(state, TruncationPolicy(theta, rank_min, rank_max)) (dlra.py:90-115). */
+int pnd_truncate(pnd_handle* h, double theta, int rank_min, int rank_max, double* tail,
+                 int* rank);
+/* one step of the energy loop (driver.py:578-622): streaming, truncate
+ * (truncate_after & 1), scattering, truncate (truncate_after & 2), dose
+ * trapezoid; tally_steps adds S * sum_b psi_b(E_lo) to the integrand.
+ * out[0..3] = tail after streaming, tail after scattering, rank, defect
+ * (defect only when want_defect != 0). */
+int pnd_step(pnd_handle* h, double dt, double theta, int rank_min, int rank_max,
+             int truncate_after, int tally_steps, int want_defect, double* out);
+int pnd_dose_reset(pnd_handle* h);
+int pnd_dose_accumulate(pnd_handle* h, double dt, int tally_steps);
+int pnd_get_dose(pnd_handle* h, double* deposited);
+/* LowRankState.orthonormality_defect() (dlra.py:67-70) on the device state. */
+int pnd_orth_defect(pnd_handle* h, double* defect);
+
+/* ---- unit-parity entry points (host in / host out) -------------------- */
+/* apply_streaming(u, inv_s, stencils, ops) (spatial.py:148-167), m <= 64. */
+int pnd_apply_streaming(pnd_handle* h, const double* u, double* out);
+/* [X^T D_s S^-1 Y] for every stencil s (the L/S-phase factors of
+ * dlra.py:183-184, 199-209); out is ns x a x b. */
+int pnd_stencil_grams(pnd_handle* h, const double* x, int a, const double* y, int b,
+                      double* out);
+/* k_rhs(K, F) = -sum_s (D_s S^-1 K) F_s (dlra.py:168-174); f is ns x r x r. */
+int pnd_k_rhs(pnd_handle* h, const double* k, int r, const double* f, double* out);
+/* orthonormal_columns(a) (dlra.py:26-43) via device TSQR; q is rows x min(rows, cols),
+ * r is min(rows, cols) x cols. Independent of the handle's grid. */
+int pnd_orthonormalize(pnd_handle* h, const double* a, int rows, int cols, double* q, double* r);
+/* np.linalg.svd(s, full_matrices=False) of a p x q matrix (dlra.py:99). */
+int pnd_svd_small(pnd_handle* h, const double* s, int p, int q, double* pm, double* sig,
+                  double* qt);
+
+/* ---- uncollided ray traversal (raytracer.py:353-403) ------------------ */
+/* Amanatides-Woo walk of n_rays rays through the handle's grid (origin given),
+ * bit-exact with the reference. Pass cells == NULL to get only counts
+ * (counts[i] = segments of ray i); otherwise offsets (n_rays + 1, exclusive
+ * scan of counts) place ray i's segments at [offsets[i], offsets[i+1]). */
+int pnd_traverse(pnd_handle* h, const double* origin3, int n_rays, const double* starts,
+                 const double* dirs, int32_t* counts, const int64_t* offsets, int64_t* cells,
+                 double* t0, double* t1);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PNDOSE_B200_H */

@@ -1,0 +1,572 @@
+// extern "C" boundary (include/pndose_b200.h): argument checks, host<->device
+// staging, error mapping. Every exception raised inside the library becomes
+// a status code plus a message stored in the handle.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+
+#include "../../include/pndose_b200.h"
+#include "handle.h"
+
+namespace pnd {
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    fail(PND_EDEVICE, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+double* DBuf::get(size_t count) {
+  if (count > cap) {
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, count * sizeof(double)));
+    cap = count;
+  }
+  return p;
+}
+void DBuf::free_() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+int* IBuf::get(size_t count) {
+  if (count > cap) {
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, count * sizeof(int)));
+    cap = count;
+  }
+  return p;
+}
+void IBuf::free_() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+void traverse(const Geom& g, const double* origin, int n_rays, const double* starts,
+              const double* dirs, int* counts, const long long* offsets, long long* cells,
+              double* t0, double* t1, cudaStream_t st);
+
+}  // namespace pnd
+
+struct pnd_handle {
+  pnd::Handle h;
+};
+
+using pnd::Handle;
+
+namespace {
+
+template <class F>
+int guard(pnd_handle* hh, F&& f) {
+  if (!hh) return PND_ECONFIG;
+  try {
+    CK(cudaSetDevice(hh->h.device));
+    f(hh->h);
+    return PND_OK;
+  } catch (const pnd::Error& e) {
+    hh->h.err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    hh->h.err = e.what();
+    return PND_EDEVICE;
+  }
+}
+
+void up(double* dst, const double* src, size_t count, cudaStream_t st) {
+  if (!count) return;
+  CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyHostToDevice, st));
+}
+void down(double* dst, const double* src, size_t count, cudaStream_t st) {
+  if (!count) return;
+  CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, double dz, int m,
+               int device) {
+  if (!out) return PND_ECONFIG;
+  *out = nullptr;
+  auto* hh = new pnd_handle();
+  Handle& h = hh->h;
+  h.device = device;
+  try {
+    const int dims[3] = {nx, ny, nz};
+    const char* names[3] = {"nx", "ny", "nz"};
+    for (int a = 0; a < 3; ++a) {
+      if (dims[a] < 1) pnd::fail(PND_ECONFIG, "grid needs at least one cell per dimension");
+      if (dims[a] == 2 && h.stencil_error.empty()) {
+        // Grid3D allows it; only the stencil cannot be built (spatial.py:84-88)
+        h.stencil_error = std::string("grid.") + names[a] +
+                          "=2: grids with 2 cells along a used axis cannot host the 3-point "
+                          "one-sided stencil; use 1 (inactive) or >= 3";
+      }
+    }
+    if (!(dx > 0 && dy > 0 && dz > 0)) pnd::fail(PND_ECONFIG, "grid spacings must be positive");
+    if (m < 1) pnd::fail(PND_ECONFIG, "need at least one moment");
+    const long long n = (long long)nx * ny * nz;
+    if (n >= (1LL << 31) - 1024) pnd::fail(PND_ECONFIG, "grid exceeds 2^31 cells per device");
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&h.pinned, 64 * sizeof(double)));
+    pnd::Geom& g = h.g;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = nz;
+    g.n = (int)n;
+    g.ld = (int)((n + 31) / 32 * 32);
+    g.h[0] = dx;
+    g.h[1] = dy;
+    g.h[2] = dz;
+    g.na = 0;
+    for (int a = 0; a < 3; ++a)
+      if (dims[a] > 1) g.axis[g.na++] = a;
+    for (int a = g.na; a < 3; ++a) g.axis[a] = 0;
+    g.ns = 2 * g.na;
+    h.m = m;
+    *out = hh;
+    return PND_OK;
+  } catch (const pnd::Error& e) {
+    h.err = e.msg;
+    *out = hh;  // caller reads the message, then destroys
+    return e.code;
+  }
+}
+
+int pnd_destroy(pnd_handle* hh) {
+  if (!hh) return PND_OK;
+  Handle& h = hh->h;
+  cudaSetDevice(h.device);
+  if (h.st) cudaStreamSynchronize(h.st);
+  pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.s_field, &h.cls_atomic, &h.cls_val, &h.gdiag,
+                       &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.U, &h.S, &h.V, &h.A,
+                       &h.Uhat, &h.W1, &h.W2, &h.part, &h.dep, &h.prev, &h.host_stage,
+                       &h.tq_n.tau, &h.tq_n.tree, &h.tq_n.rbuf, &h.tq_n.cbuf, &h.tq_m.tau,
+                       &h.tq_m.tree, &h.tq_m.rbuf, &h.tq_m.cbuf};
+  for (auto* b : bufs) b->free_();
+  for (auto& b : h.sm) b.free_();
+  h.cls.free_();
+  h.iflag.free_();
+  if (h.pinned) cudaFreeHost(h.pinned);
+  if (h.st) cudaStreamDestroy(h.st);
+  delete hh;
+  return PND_OK;
+}
+
+int pnd_last_error(pnd_handle* hh, char* buf, size_t len) {
+  if (!hh || !buf || !len) return PND_ECONFIG;
+  std::snprintf(buf, len, "%s", hh->h.err.c_str());
+  return PND_OK;
+}
+
+int pnd_synchronize(pnd_handle* hh) {
+  return guard(hh, [&](Handle& h) { CK(cudaStreamSynchronize(h.st)); });
+}
+
+int pnd_device_bytes(pnd_handle* hh, double* bytes) {
+  return guard(hh, [&](Handle& h) {
+    double total = 0;
+    const pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.s_field, &h.cls_atomic, &h.gdiag, &h.psi,
+                               &h.psi_lo, &h.tm, &h.flux, &h.U, &h.S, &h.V, &h.A, &h.Uhat,
+                               &h.W1, &h.W2, &h.part, &h.dep, &h.prev, &h.tq_n.tau,
+                               &h.tq_n.tree, &h.tq_n.cbuf, &h.tq_m.tau, &h.tq_m.tree,
+                               &h.tq_m.cbuf};
+    for (auto* b : bufs) total += 8.0 * b->cap;
+    for (auto& b : h.sm) total += 8.0 * b.cap;
+    *bytes = total;
+  });
+}
+
+int pnd_set_angular(pnd_handle* hh, const double* a_plus, const double* a_minus) {
+  return guard(hh, [&](Handle& h) {
+    const size_t mm = (size_t)h.m * h.m;
+    double* d = h.amat.get(h.g.ns * mm + 1);
+    for (int ai = 0; ai < h.g.na; ++ai) {
+      const int axis = h.g.axis[ai];
+      up(d + (2 * ai) * mm, a_plus + axis * mm, mm, h.st);
+      up(d + (2 * ai + 1) * mm, a_minus + axis * mm, mm, h.st);
+    }
+    CK(cudaStreamSynchronize(h.st));
+    h.have_angular = true;
+  });
+}
+
+int pnd_set_materials(pnd_handle* hh, const int32_t* cell_class, int n_class,
+                      const double* class_atomic) {
+  return guard(hh, [&](Handle& h) {
+    if (n_class < 1) pnd::fail(PND_ECONFIG, "need at least one material class");
+    int* c = h.cls.get(h.g.n);
+    CK(cudaMemcpyAsync(c, cell_class, sizeof(int) * h.g.n, cudaMemcpyHostToDevice, h.st));
+    up(h.cls_atomic.get((size_t)n_class * 12), class_atomic, (size_t)n_class * 12, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    h.n_cls = n_class;
+    h.have_mat = true;
+  });
+}
+
+int pnd_set_inv_s(pnd_handle* hh, const double* inv_s) {
+  return guard(hh, [&](Handle& h) {
+    double* d = h.inv_s.get(h.g.ld);
+    pnd::fill_zero(d, h.g.ld, h.st);
+    up(d, inv_s, h.g.n, h.st);
+    double* sf = h.s_field.get(h.g.ld);
+    pnd::fill_zero(sf, h.g.ld, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    h.have_inv_s = true;
+  });
+}
+
+int pnd_set_class_stopping(pnd_handle* hh, const double* class_s) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.have_mat) pnd::fail(PND_ECONFIG, "set materials before class stopping powers");
+    double* v = h.cls_val.get(h.n_cls);
+    up(v, class_s, h.n_cls, h.st);
+    double* d = h.inv_s.get(h.g.ld);
+    double* sf = h.s_field.get(h.g.ld);
+    pnd::class_gather_inv(h.cls.p, v, h.g.n, d, sf, h.st);
+    h.have_inv_s = true;
+  });
+}
+
+int pnd_set_scattering(pnd_handle* hh, const double* g_diags, const double* sigma_t) {
+  return guard(hh, [&](Handle& h) {
+    up(h.gdiag.get((size_t)12 * h.m), g_diags, (size_t)12 * h.m, h.st);
+    up(h.sigt.get(12), sigma_t, 12, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    h.have_scat = true;
+  });
+}
+
+int pnd_set_sources(pnd_handle* hh, int n_beams, const double* psi, const double* t_m) {
+  return guard(hh, [&](Handle& h) {
+    if (n_beams < 0 || n_beams > 4) pnd::fail(PND_ECONFIG, "0..4 uncollided sources supported");
+    h.n_beams = n_beams;
+    if (!n_beams) return;
+    double* d = h.psi.get((size_t)n_beams * h.g.ld);
+    for (int b = 0; b < n_beams; ++b) up(d + (size_t)b * h.g.ld, psi + (size_t)b * h.g.n, h.g.n, h.st);
+    up(h.tm.get((size_t)n_beams * h.m), t_m, (size_t)n_beams * h.m, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, const double* values,
+                       const double* t_m) {
+  return guard(hh, [&](Handle& h) {
+    if (n_beams < 1 || n_beams > 4) pnd::fail(PND_ECONFIG, "1..4 beams supported");
+    if (beam < 0 || beam >= n_beams) pnd::fail(PND_ECONFIG, "beam index out of range");
+    if (beam == 0) {
+      h.n_groups = n_groups;
+      h.n_beams = n_beams;
+      h.flux.get((size_t)n_beams * n_groups * h.g.ld);
+      h.psi.get((size_t)n_beams * h.g.ld);
+      h.psi_lo.get((size_t)n_beams * h.g.ld);
+      h.tm.get((size_t)n_beams * h.m);
+    } else if (n_groups != h.n_groups || n_beams != h.n_beams) {
+      pnd::fail(PND_ECONFIG, "all beams must share the group grid");
+    }
+    // values (n x G row-major) -> G columns of length ld
+    double* stage = h.sm[47].get((size_t)h.g.n * n_groups);
+    up(stage, values, (size_t)h.g.n * n_groups, h.st);
+    pnd::transpose_in(stage, h.g.n, n_groups, h.flux.p + (size_t)beam * n_groups * h.g.ld,
+                      h.g.ld, h.st);
+    up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_select_flux(pnd_handle* hh, int which, const int32_t* j0, const double* w0,
+                    const int32_t* j1, const double* w1) {
+  return guard(hh, [&](Handle& h) {
+    double* dst = which == 0 ? h.psi.p : h.psi_lo.p;
+    for (int b = 0; b < h.n_beams; ++b) {
+      const double* tab = h.flux.p + (size_t)b * h.n_groups * h.g.ld;
+      pnd::psi_lerp(tab, h.g.ld, h.g.n, j0[b], w0[b], j1[b], w1[b], dst + (size_t)b * h.g.ld,
+                    h.st);
+    }
+  });
+}
+
+int pnd_state_set(pnd_handle* hh, int ru, int rv, const double* u, const double* s,
+                  const double* v) {
+  return guard(hh, [&](Handle& h) {
+    if (ru < 1 || rv < 1) pnd::fail(PND_ECONFIG, "rank must be positive");
+    if (ru > 64 || rv > 64) pnd::fail(PND_ECONFIG, "rank above 64 is not supported");
+    double* stage = h.sm[46].get((size_t)h.g.n * ru);
+    up(stage, u, (size_t)h.g.n * ru, h.st);
+    double* U = h.U.get((size_t)h.g.ld * ru);
+    pnd::fill_zero(U, (size_t)h.g.ld * ru, h.st);
+    pnd::transpose_in(stage, h.g.n, ru, U, h.g.ld, h.st);
+    up(h.S.get((size_t)ru * rv), s, (size_t)ru * rv, h.st);
+    up(h.V.get((size_t)h.m * rv), v, (size_t)h.m * rv, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    h.ru = ru;
+    h.rv = rv;
+  });
+}
+
+int pnd_state_shape(pnd_handle* hh, int* ru, int* rv) {
+  return guard(hh, [&](Handle& h) {
+    *ru = h.ru;
+    *rv = h.rv;
+  });
+}
+
+int pnd_state_get(pnd_handle* hh, double* u, double* s, double* v) {
+  return guard(hh, [&](Handle& h) {
+    if (u) {
+      double* stage = h.sm[46].get((size_t)h.g.n * h.ru);
+      pnd::transpose_out(h.U.p, h.g.ld, h.g.n, h.ru, stage, h.st);
+      down(u, stage, (size_t)h.g.n * h.ru, h.st);
+    }
+    if (s) down(s, h.S.p, (size_t)h.ru * h.rv, h.st);
+    if (v) down(v, h.V.p, (size_t)h.m * h.rv, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_streaming_step(pnd_handle* hh, double dt) {
+  return guard(hh, [&](Handle& h) { pnd::streaming_step(h, dt); });
+}
+
+int pnd_scattering_step(pnd_handle* hh, double dt) {
+  return guard(hh, [&](Handle& h) { pnd::scattering_step(h, dt); });
+}
+
+int pnd_truncate(pnd_handle* hh, double theta, int rank_min, int rank_max, double* tail,
+                 int* rank) {
+  return guard(hh, [&](Handle& h) {
+    if (theta < 0) pnd::fail(PND_ECONFIG, "truncation threshold must be nonnegative");
+    if (!(1 <= rank_min && rank_min <= rank_max))
+      pnd::fail(PND_ECONFIG, "need 1 <= rank_min <= rank_max");
+    pnd::truncate(h, theta, rank_min, rank_max, tail, rank);
+  });
+}
+
+int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max,
+             int truncate_after, int tally_steps, int want_defect, double* out) {
+  return guard(hh, [&](Handle& h) {
+    double t1 = 0.0, t2 = 0.0;
+    int rank = 0;
+    pnd::streaming_step(h, dt);
+    if (truncate_after & 1) pnd::truncate(h, theta, rank_min, rank_max, &t1, &rank);
+    pnd::scattering_step(h, dt);
+    if (truncate_after & 2) pnd::truncate(h, theta, rank_min, rank_max, &t2, &rank);
+    pnd::dose_accumulate_step(h, dt, tally_steps != 0);
+    double defect = 0.0;
+    if (want_defect) defect = pnd::orth_defect(h);
+    if (out) {
+      out[0] = t1;
+      out[1] = t2;
+      out[2] = (double)(h.ru < h.rv ? h.ru : h.rv);
+      out[3] = defect;
+    }
+  });
+}
+
+int pnd_dose_reset(pnd_handle* hh) {
+  return guard(hh, [&](Handle& h) {
+    pnd::fill_zero(h.dep.get(h.g.ld), h.g.ld, h.st);
+    pnd::fill_zero(h.prev.get(h.g.ld), h.g.ld, h.st);
+    if (!h.s_field.p) pnd::fill_zero(h.s_field.get(h.g.ld), h.g.ld, h.st);
+  });
+}
+
+int pnd_dose_accumulate(pnd_handle* hh, double dt, int tally_steps) {
+  return guard(hh, [&](Handle& h) { pnd::dose_accumulate_step(h, dt, tally_steps != 0); });
+}
+
+int pnd_get_dose(pnd_handle* hh, double* deposited) {
+  return guard(hh, [&](Handle& h) {
+    down(deposited, h.dep.get(h.g.ld), h.g.n, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_orth_defect(pnd_handle* hh, double* defect) {
+  return guard(hh, [&](Handle& h) { *defect = pnd::orth_defect(h); });
+}
+
+// ------------------------------------------------------------ unit parity
+int pnd_apply_streaming(pnd_handle* hh, const double* u, double* out) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
+    if (!h.have_angular || !h.have_inv_s) pnd::fail(PND_ECONFIG, "set angular and inv_s first");
+    if (h.m > 64) pnd::fail(PND_ECONFIG, "apply_streaming supports m <= 64");
+    const int n = h.g.n, m = h.m, ld = h.g.ld, ns = h.g.ns;
+    for (size_t i = 0; i < (size_t)n * m; ++i)
+      if (!std::isfinite(u[i])) pnd::fail(PND_ENUMERICAL, "non-finite streaming input");
+    pnd::DBuf su, du, dout, stage, mneg;
+    try {
+      double* s = stage.get((size_t)n * m);
+      up(s, u, (size_t)n * m, h.st);
+      double* U = du.get((size_t)ld * m);
+      pnd::transpose_in(s, n, m, U, ld, h.st);
+      double* M = mneg.get((size_t)ns * m * m + 1);
+      pnd::axpby(ns * m * m, -1.0, h.amat.p, 0.0, M, h.st);
+      double* O = dout.get((size_t)ld * m);
+      pnd::apply_streaming_full(h.g, U, ld, m, h.inv_s.p, M, nullptr, O, ld, h.st);
+      pnd::transpose_out(O, ld, n, m, s, h.st);
+      down(out, s, (size_t)n * m, h.st);
+      CK(cudaStreamSynchronize(h.st));
+    } catch (...) {
+      su.free_(); du.free_(); dout.free_(); stage.free_(); mneg.free_();
+      throw;
+    }
+    su.free_(); du.free_(); dout.free_(); stage.free_(); mneg.free_();
+  });
+}
+
+int pnd_stencil_grams(pnd_handle* hh, const double* x, int a, const double* y, int b,
+                      double* out) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
+    if (!h.have_inv_s) pnd::fail(PND_ECONFIG, "set inv_s first");
+    const int n = h.g.n, ld = h.g.ld, ns = h.g.ns;
+    pnd::DBuf sx, sy, dx, dy, dout;
+    double* s1 = sx.get((size_t)n * a);
+    double* s2 = sy.get((size_t)n * b);
+    up(s1, x, (size_t)n * a, h.st);
+    up(s2, y, (size_t)n * b, h.st);
+    double* X = dx.get((size_t)ld * a);
+    double* Y = dy.get((size_t)ld * b);
+    pnd::fill_zero(X, (size_t)ld * a, h.st);
+    pnd::fill_zero(Y, (size_t)ld * b, h.st);
+    pnd::transpose_in(s1, n, a, X, ld, h.st);
+    pnd::transpose_in(s2, n, b, Y, ld, h.st);
+    double* O = dout.get((size_t)ns * a * b + 1);
+    pnd::GramArgs ga{};
+    ga.geo = h.g;
+    ga.X = X; ga.ldx = ld; ga.na = a;
+    ga.Y = Y; ga.ldy = ld; ga.nb = b;
+    ga.nphase = ns;
+    ga.gen = pnd::GEN_STENCIL;
+    ga.inv_s = h.inv_s.p;
+    ga.out = O;
+    pnd::gram(ga, h.part, h.st);
+    down(out, O, (size_t)ns * a * b, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    sx.free_(); sy.free_(); dx.free_(); dy.free_(); dout.free_();
+  });
+}
+
+int pnd_k_rhs(pnd_handle* hh, const double* k, int r, const double* f, double* out) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
+    if (!h.have_inv_s) pnd::fail(PND_ECONFIG, "set inv_s first");
+    const int n = h.g.n, ld = h.g.ld, ns = h.g.ns;
+    pnd::DBuf st, dk, dm, dout;
+    double* s = st.get((size_t)n * r);
+    up(s, k, (size_t)n * r, h.st);
+    double* K = dk.get((size_t)ld * r);
+    pnd::transpose_in(s, n, r, K, ld, h.st);
+    double* M = dm.get((size_t)ns * r * r + 1);
+    up(M, f, (size_t)ns * r * r, h.st);
+    pnd::axpby(ns * r * r, -1.0, M, 0.0, M, h.st);
+    double* O = dout.get((size_t)ld * r);
+    pnd::KStageArgs ka{};
+    ka.geo = h.g;
+    ka.X = K; ka.ldx = ld; ka.xc = r;
+    ka.U0 = nullptr; ka.ra = 0;
+    ka.M = M;
+    ka.inv_s = h.inv_s.p;
+    ka.r = r;
+    ka.out = O; ka.ldo = ld;
+    pnd::kstage(ka, h.st);
+    pnd::transpose_out(O, ld, n, r, s, h.st);
+    down(out, s, (size_t)n * r, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    st.free_(); dk.free_(); dm.free_(); dout.free_();
+  });
+}
+
+int pnd_orthonormalize(pnd_handle* hh, const double* a, int rows, int cols, double* q,
+                       double* r) {
+  return guard(hh, [&](Handle& h) {
+    if (rows < 1 || cols < 1) pnd::fail(PND_ECONFIG, "empty matrix");
+    const int kc = rows < cols ? rows : cols;
+    pnd::DBuf st, da, dq, dr;
+    double* s = st.get((size_t)rows * cols);
+    up(s, a, (size_t)rows * cols, h.st);
+    double* A = da.get((size_t)rows * cols);
+    pnd::transpose_in(s, rows, cols, A, rows, h.st);
+    double* Q = dq.get((size_t)rows * kc);
+    double* R = dr.get((size_t)kc * cols);
+    pnd::TsqrWork w;
+    pnd::tsqr(A, rows, cols, rows, Q, rows, R, w, h.st);
+    pnd::transpose_out(Q, rows, rows, kc, s, h.st);
+    down(q, s, (size_t)rows * kc, h.st);
+    if (r) down(r, R, (size_t)kc * cols, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    w.tau.free_(); w.tree.free_(); w.rbuf.free_(); w.cbuf.free_();
+    st.free_(); da.free_(); dq.free_(); dr.free_();
+  });
+}
+
+int pnd_svd_small(pnd_handle* hh, const double* s, int p, int q, double* pm, double* sig,
+                  double* qt) {
+  return guard(hh, [&](Handle& h) {
+    const int k = p < q ? p : q;
+    pnd::DBuf ds, dp, dsig, dq;
+    double* S = ds.get((size_t)p * q);
+    up(S, s, (size_t)p * q, h.st);
+    double* P = dp.get((size_t)p * k);
+    double* G = dsig.get(k);
+    double* Q = dq.get((size_t)k * q);
+    pnd::svd_small(S, p, q, P, G, Q, nullptr, h.st);
+    down(pm, P, (size_t)p * k, h.st);
+    down(sig, G, k, h.st);
+    down(qt, Q, (size_t)k * q, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    ds.free_(); dp.free_(); dsig.free_(); dq.free_();
+  });
+}
+
+int pnd_traverse(pnd_handle* hh, const double* origin3, int n_rays, const double* starts,
+                 const double* dirs, int32_t* counts, const int64_t* offsets, int64_t* cells,
+                 double* t0, double* t1) {
+  return guard(hh, [&](Handle& h) {
+    if (n_rays <= 0) return;
+    pnd::DBuf ds, dd, dt0, dt1;
+    pnd::IBuf dc;
+    double* S = ds.get((size_t)n_rays * 3);
+    double* D = dd.get((size_t)n_rays * 3);
+    up(S, starts, (size_t)n_rays * 3, h.st);
+    up(D, dirs, (size_t)n_rays * 3, h.st);
+    if (!cells) {
+      int* C = dc.get(n_rays);
+      pnd::traverse(h.g, origin3, n_rays, S, D, C, nullptr, nullptr, nullptr, nullptr, h.st);
+      CK(cudaMemcpyAsync(counts, C, sizeof(int) * n_rays, cudaMemcpyDeviceToHost, h.st));
+      CK(cudaStreamSynchronize(h.st));
+    } else {
+      const long long total = offsets[n_rays];
+      long long* O = nullptr;
+      long long* CE = nullptr;
+      CK(cudaMalloc(&O, sizeof(long long) * (n_rays + 1)));
+      CK(cudaMalloc(&CE, sizeof(long long) * (total > 0 ? total : 1)));
+      double* T0 = dt0.get(total > 0 ? total : 1);
+      double* T1 = dt1.get(total > 0 ? total : 1);
+      CK(cudaMemcpyAsync(O, offsets, sizeof(long long) * (n_rays + 1), cudaMemcpyHostToDevice,
+                         h.st));
+      pnd::traverse(h.g, origin3, n_rays, S, D, nullptr, O, CE, T0, T1, h.st);
+      CK(cudaMemcpyAsync(cells, CE, sizeof(long long) * total, cudaMemcpyDeviceToHost, h.st));
+      down(t0, T0, total, h.st);
+      down(t1, T1, total, h.st);
+      CK(cudaStreamSynchronize(h.st));
+      cudaFree(O);
+      cudaFree(CE);
+    }
+    ds.free_(); dd.free_(); dt0.free_(); dt1.free_(); dc.free_();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,679 @@
+// Dense small / m-side linear algebra on the device, so no step leaves the GPU.
+//
+//   gemm        strided batched FP64 GEMM for the m-side factors
+//               (dlra.py:155-166, 176-194) and all R x R products;
+//   tsqr        communication-avoiding Householder QR (TSQR) used for every
+//               orthonormal_columns call (dlra.py:26-43) and the moment-side
+//               qr(L1^T) (dlra.py:299): Householder leaves of 128 rows in
+//               shared memory (LAPACK dlarfg conventions, so an exactly zero
+//               column yields tau = 0 and the unit vector, reproducing the
+//               reference's canonical step-0 basis),
+//               a tree of stacked R factors, then top-down formation of the
+//               explicit Q;
+//   svd_small   one-CTA one-sided (Hestenes) Jacobi SVD of the augmented
+//               coefficient matrix (dlra.py:99), with exact zero singular
+//               values completed by canonical unit vectors (svd(0) = I, I);
+//   tail_rule   the truncation rank rule (dlra.py:100-109), same summation
+//               order as numpy's reversed cumsum;
+//   scat_solves the m independent r x r implicit solves of scattering
+//               substep 1 (dlra.py:286-298), partial-pivoting LU per column;
+//   s_rk4       Horner-form RK4 of the precontracted Galerkin S-phase.
+#include <float.h>
+
+#include "pnd.h"
+
+namespace pnd {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// all threads of the block get the sum; red must hold >= 32 doubles
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  __syncthreads();
+  return s;
+}
+
+// ----------------------------------------------------------------- gemm
+__global__ void gemm_kernel(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB,
+                            double beta, Mat C, long sC) {
+  __shared__ double As[16][17];
+  __shared__ double Bs[16][17];
+  const int b = blockIdx.z;
+  const double* a = A.p + (size_t)b * sA;
+  const double* bb = B.p + (size_t)b * sB;
+  double* c = C.p + (size_t)b * sC;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double acc = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    // A tile: (row block, k0..k0+15); load with tx running along k
+    const int ar = blockIdx.y * 16 + ty, ak = k0 + tx;
+    As[ty][tx] = (ar < M && ak < K) ? a[ar * A.rs + ak * A.cs] : 0.0;
+    const int bk = k0 + ty, bc = blockIdx.x * 16 + tx;
+    Bs[ty][tx] = (bk < K && bc < N) ? bb[bk * B.rs + bc * B.cs] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
+    __syncthreads();
+  }
+  if (row < M && col < N) {
+    double* dst = c + row * C.rs + col * C.cs;
+    *dst = beta == 0.0 ? alpha * acc : alpha * acc + beta * (*dst);
+  }
+}
+
+__global__ void axpby_kernel(int n, double a, const double* x, double b, double* y) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    y[i] = b == 0.0 ? a * x[i] : a * x[i] + b * y[i];
+}
+
+// ----------------------------------------------------------------- TSQR
+struct Part {
+  int rows, cols, br, nblk;
+  __host__ __device__ int start(int b) const { return b * br; }
+  __host__ __device__ int count(int b) const { return b == nblk - 1 ? rows - b * br : br; }
+};
+
+__global__ void hh_qr_kernel(double* A, int lda, Part pt, int first, double* tau, double* Rn,
+                             int ldn) {
+  extern __shared__ double sm[];
+  const int b = first + blockIdx.x;
+  const int r0 = pt.start(b), rb = pt.count(b), cols = pt.cols;
+  const int LDS = cols + 1;
+  double* S = sm;                      // rb x LDS
+  double* red = sm + rb * LDS;         // 32
+  double* wk = red + 32;               // cols
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  for (int idx = tid; idx < rb * cols; idx += nthr) {
+    const int i = idx % rb, j = idx / rb;
+    S[i * LDS + j] = A[(size_t)(r0 + i) + (size_t)j * lda];
+  }
+  __syncthreads();
+  const int kk = rb < cols ? rb : cols;
+  for (int j = 0; j < kk; ++j) {
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < rb; i += nthr) part += S[i * LDS + j] * S[i * LDS + j];
+    const double xnorm2 = block_sum(part, red);
+    double tj = 0.0;
+    if (xnorm2 > 0.0) {
+      const double alpha = S[j * LDS + j];
+      const double beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+      tj = (beta - alpha) / beta;
+      const double scl = 1.0 / (alpha - beta);
+      for (int i = j + 1 + tid; i < rb; i += nthr) S[i * LDS + j] *= scl;
+      __syncthreads();
+      for (int k = j + 1 + warp; k < cols; k += nw) {
+        double s = 0.0;
+        for (int i = j + 1 + lane; i < rb; i += 32) s += S[i * LDS + j] * S[i * LDS + k];
+        s = warp_sum(s);
+        if (lane == 0) wk[k] = S[j * LDS + k] + s;
+      }
+      __syncthreads();
+      const int w = cols - j - 1;
+      if (w > 0) {
+        for (int idx = tid; idx < (rb - j) * w; idx += nthr) {
+          const int i = j + idx / w, k = j + 1 + idx % w;
+          const double v = (i == j) ? 1.0 : S[i * LDS + j];
+          S[i * LDS + k] -= tj * v * wk[k];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) S[j * LDS + j] = beta;
+      __syncthreads();
+    }
+    if (tid == 0) tau[(size_t)b * cols + j] = tj;
+  }
+  for (int j = kk + tid; j < cols; j += nthr) tau[(size_t)b * cols + j] = 0.0;
+  for (int idx = tid; idx < rb * cols; idx += nthr) {
+    const int i = idx % rb, j = idx / rb;
+    A[(size_t)(r0 + i) + (size_t)j * lda] = S[i * LDS + j];
+  }
+  if (Rn) {
+    for (int idx = tid; idx < cols * cols; idx += nthr) {
+      const int i = idx % cols, j = idx / cols;
+      const double v = (i < kk && i <= j) ? S[i * LDS + j] : 0.0;
+      Rn[(size_t)(b * cols + i) + (size_t)j * ldn] = v;
+    }
+  }
+}
+
+// X = H_0 ... H_{kk-1} [C_b; 0] for every block b of the partition
+__global__ void hh_applyq_kernel(const double* V, int ldv, Part pt, int first, const double* tau,
+                                 const double* C, int ldc, int kc, double* Q, int ldq) {
+  extern __shared__ double sm[];
+  const int b = first + blockIdx.x;
+  const int r0 = pt.start(b), rb = pt.count(b), cols = pt.cols;
+  const int LDV = cols + 1, LDX = kc + 1;
+  double* Vs = sm;                // rb x LDV
+  double* X = Vs + rb * LDV;      // rb x LDX
+  double* wk = X + rb * LDX;      // kc
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  const int kk = rb < cols ? rb : cols;
+  for (int idx = tid; idx < rb * cols; idx += nthr) {
+    const int i = idx % rb, j = idx / rb;
+    Vs[i * LDV + j] = V[(size_t)(r0 + i) + (size_t)j * ldv];
+  }
+  for (int idx = tid; idx < rb * kc; idx += nthr) {
+    const int i = idx % rb, c = idx / rb;
+    double v = 0.0;
+    if (i < cols) {
+      if (C) v = C[(size_t)(b * cols + i) + (size_t)c * ldc];
+      else v = (i == c) ? 1.0 : 0.0;
+    }
+    X[i * LDX + c] = v;
+  }
+  __syncthreads();
+  for (int j = kk - 1; j >= 0; --j) {
+    const double tj = tau[(size_t)b * cols + j];
+    if (tj == 0.0) continue;
+    for (int c = warp; c < kc; c += nw) {
+      double s = 0.0;
+      for (int i = j + 1 + lane; i < rb; i += 32) s += Vs[i * LDV + j] * X[i * LDX + c];
+      s = warp_sum(s);
+      if (lane == 0) wk[c] = X[j * LDX + c] + s;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (rb - j) * kc; idx += nthr) {
+      const int i = j + idx / kc, c = idx % kc;
+      const double v = (i == j) ? 1.0 : Vs[i * LDV + j];
+      X[i * LDX + c] -= tj * v * wk[c];
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < rb * kc; idx += nthr) {
+    const int i = idx % rb, c = idx / rb;
+    Q[(size_t)(r0 + i) + (size_t)c * ldq] = X[i * LDX + c];
+  }
+}
+
+__global__ void copy_rfac_kernel(const double* Rn, int ldn, int kc, int cols, double* rfac) {
+  for (int idx = threadIdx.x + blockIdx.x * blockDim.x; idx < kc * cols;
+       idx += blockDim.x * gridDim.x) {
+    const int i = idx / cols, j = idx % cols;
+    rfac[idx] = Rn[(size_t)i + (size_t)j * ldn];
+  }
+}
+
+// ----------------------------------------------------------------- SVD
+__global__ void svd_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
+  extern __shared__ double sm[];
+  const bool tall = p >= q;
+  const int M = tall ? p : q, N = tall ? q : p;
+  const int N2 = N + (N & 1);
+  double* A = sm;                  // column-major M x N2
+  double* Vm = A + M * N2;         // column-major N2 x N2
+  double* U = Vm + N2 * N2;        // column-major M x N (sorted, completed)
+  double* sg = U + M * N;          // N2
+  int* perm = (int*)(sg + N2);     // N
+  __shared__ int rotated;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  for (int idx = tid; idx < M * N2; idx += nthr) {
+    const int i = idx % M, j = idx / M;
+    double v = 0.0;
+    if (j < N) v = tall ? s[i * q + j] : s[j * q + i];
+    A[idx] = v;
+  }
+  for (int idx = tid; idx < N2 * N2; idx += nthr) Vm[idx] = (idx % N2 == idx / N2) ? 1.0 : 0.0;
+  __syncthreads();
+  const int npair = N2 / 2;
+  for (int sweep = 0; sweep < 60 && N2 > 1; ++sweep) {
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < N2 - 1; ++round) {
+      for (int k = warp; k < npair; k += nw) {
+        int a, b;
+        if (k == 0) {
+          a = round;
+          b = N2 - 1;
+        } else {
+          a = (round + k) % (N2 - 1);
+          b = (round + N2 - 1 - k) % (N2 - 1);
+        }
+        if (a > b) { const int t = a; a = b; b = t; }
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < M; i += 32) {
+          const double x = A[a * M + i], y = A[b * M + i];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+          for (int i = lane; i < M; i += 32) {
+            const double x = A[a * M + i], y = A[b * M + i];
+            A[a * M + i] = c * x - sn * y;
+            A[b * M + i] = sn * x + c * y;
+          }
+          for (int i = lane; i < N2; i += 32) {
+            const double x = Vm[a * N2 + i], y = Vm[b * N2 + i];
+            Vm[a * N2 + i] = c * x - sn * y;
+            Vm[b * N2 + i] = sn * x + c * y;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  // singular values
+  for (int j = warp; j < N; j += nw) {
+    double x = 0.0;
+    for (int i = lane; i < M; i += 32) x += A[j * M + i] * A[j * M + i];
+    x = warp_sum(x);
+    if (lane == 0) sg[j] = sqrt(x);
+  }
+  __syncthreads();
+  if (tid == 0) {  // stable selection sort, descending
+    for (int j = 0; j < N; ++j) perm[j] = j;
+    for (int j = 0; j < N; ++j) {
+      int best = j;
+      for (int k = j + 1; k < N; ++k)
+        if (sg[perm[k]] > sg[perm[best]]) best = k;
+      const int t = perm[j];
+      perm[j] = perm[best];
+      perm[best] = t;
+    }
+  }
+  __syncthreads();
+  // left vectors for nonzero singular values
+  for (int idx = tid; idx < M * N; idx += nthr) {
+    const int i = idx % M, j = idx / M;
+    const double sv = sg[perm[j]];
+    U[idx] = sv > 0.0 ? A[perm[j] * M + i] / sv : 0.0;
+  }
+  __syncthreads();
+  // complete the zero ones with canonical unit vectors (Gram-Schmidt x2)
+  if (warp == 0) {
+    int cand = 0;
+    for (int j = 0; j < N; ++j) {
+      if (sg[perm[j]] > 0.0) continue;
+      for (; cand < M; ++cand) {
+        double vloc[8];
+        // v = e_cand - sum_k U_k U_k[cand] over filled columns, twice
+        for (int t = 0; t < 8; ++t) vloc[t] = 0.0;
+        for (int i = lane, t = 0; i < M; i += 32, ++t) vloc[t] = (i == cand) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int k = 0; k < N; ++k) {
+            if (k == j || (sg[perm[k]] == 0.0 && k > j)) continue;
+            double d = 0.0;
+            for (int i = lane, t = 0; i < M; i += 32, ++t) d += U[k * M + i] * vloc[t];
+            d = warp_sum(d);
+            for (int i = lane, t = 0; i < M; i += 32, ++t) vloc[t] -= d * U[k * M + i];
+          }
+        }
+        double nn = 0.0;
+        for (int i = lane, t = 0; i < M; i += 32, ++t) nn += vloc[t] * vloc[t];
+        nn = warp_sum(nn);
+        if (nn > 0.25) {
+          const double inv = 1.0 / sqrt(nn);
+          for (int i = lane, t = 0; i < M; i += 32, ++t) U[j * M + i] = vloc[t] * inv;
+          __syncwarp();
+          ++cand;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // outputs: s = P diag(sig) Qt
+  for (int j = tid; j < N; j += nthr) sig[j] = sg[perm[j]];
+  if (tall) {
+    for (int idx = tid; idx < p * N; idx += nthr) {
+      const int i = idx / N, j = idx % N;
+      P[idx] = U[j * M + i];
+    }
+    for (int idx = tid; idx < N * q; idx += nthr) {
+      const int j = idx / q, c = idx % q;
+      Qt[idx] = Vm[perm[j] * N2 + c];
+    }
+  } else {
+    for (int idx = tid; idx < p * N; idx += nthr) {
+      const int i = idx / N, j = idx % N;
+      P[idx] = Vm[perm[j] * N2 + i];
+    }
+    for (int idx = tid; idx < N * q; idx += nthr) {
+      const int j = idx / q, c = idx % q;
+      Qt[idx] = U[j * M + c];
+    }
+  }
+}
+
+__global__ void tail_kernel(const double* sig, int k, double theta, int rmin, int rmax, int* info,
+                            double* tail) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // tails[j] = sum_{i >= j} sigma_i accumulated from the smallest (np.cumsum of sigma[::-1])
+  double tails[129];
+  tails[k] = 0.0;
+  double acc = 0.0;
+  for (int j = k - 1; j >= 0; --j) {
+    acc = (j == k - 1) ? sig[j] : acc + sig[j];
+    tails[j] = acc;
+  }
+  int r1 = k;
+  for (int j = 0; j <= k; ++j)
+    if (tails[j] <= theta) { r1 = j; break; }
+  if (r1 > rmax) {
+    info[0] = -r1 - 1;
+    tail[0] = 0.0;
+    return;
+  }
+  int r = r1 < rmin ? rmin : r1;
+  if (r > rmax) r = rmax;
+  if (r > k) r = k;
+  info[0] = r;
+  tail[0] = tails[r];
+}
+
+__global__ void scat_solve_kernel(const double* B, const double* coeffs, const double* lcols,
+                                  int r, int m, double dt, double* lnew, int* singular) {
+  extern __shared__ double sm[];
+  const int q = blockIdx.x;
+  const int LD = r + 1;
+  double* Mx = sm;           // r x LD
+  double* x = sm + r * LD;   // r
+  __shared__ int piv;
+  __shared__ int bad;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int idx = tid; idx < r * r; idx += nthr) {
+    const int a = idx / r, b = idx % r;
+    double s = 0.0;
+    for (int i = 0; i < 12; ++i) s += coeffs[i * m + q] * B[(size_t)i * r * r + idx];
+    Mx[a * LD + b] = (a == b ? 1.0 : 0.0) + dt * s;
+  }
+  for (int a = tid; a < r; a += nthr) x[a] = lcols[a * m + q];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    if (tid == 0) {
+      int p = j;
+      double best = fabs(Mx[j * LD + j]);
+      for (int i = j + 1; i < r; ++i) {
+        const double v = fabs(Mx[i * LD + j]);
+        if (v > best) { best = v; p = i; }
+      }
+      piv = p;
+      if (best == 0.0) bad = 1;
+    }
+    __syncthreads();
+    if (bad) break;
+    const int p = piv;
+    if (p != j) {
+      for (int k = tid; k < r; k += nthr) {
+        const double t = Mx[j * LD + k];
+        Mx[j * LD + k] = Mx[p * LD + k];
+        Mx[p * LD + k] = t;
+      }
+      if (tid == 0) { const double t = x[j]; x[j] = x[p]; x[p] = t; }
+    }
+    __syncthreads();
+    const double inv = 1.0 / Mx[j * LD + j];
+    for (int i = j + 1 + tid; i < r; i += nthr) {
+      const double l = Mx[i * LD + j] * inv;
+      Mx[i * LD + j] = l;
+      for (int k = j + 1; k < r; ++k) Mx[i * LD + k] -= l * Mx[j * LD + k];
+      x[i] -= l * x[j];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) atomicMin(singular, q);
+    return;
+  }
+  if (tid == 0) {
+    for (int i = r - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int k = i + 1; k < r; ++k) s -= Mx[i * LD + k] * x[k];
+      x[i] = s / Mx[i * LD + i];
+    }
+  }
+  __syncthreads();
+  for (int a = tid; a < r; a += nthr) lnew[a * m + q] = x[a];
+}
+
+__global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const double* F, int ns,
+                             double dt) {
+  extern __shared__ double sm[];
+  const int pq = p * q;
+  double* S0 = sm;
+  double* W = S0 + pq;
+  double* T = W + pq;
+  double* Acc = T + pq;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < pq; i += nthr) S0[i] = W[i] = S[i];
+  __syncthreads();
+  const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+  for (int st = 0; st < 4; ++st) {
+    for (int i = tid; i < pq; i += nthr) Acc[i] = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const double* Gs = G + (size_t)s * p * p;
+      const double* Fs = F + (size_t)s * q * q;
+      __syncthreads();
+      for (int i = tid; i < pq; i += nthr) {
+        const int a = i / q, b = i % q;
+        double t = 0.0;
+        for (int k = 0; k < p; ++k) t = fma(Gs[a * p + k], W[k * q + b], t);
+        T[i] = t;
+      }
+      __syncthreads();
+      for (int i = tid; i < pq; i += nthr) {
+        const int a = i / q, b = i % q;
+        double t = 0.0;
+        for (int k = 0; k < q; ++k) t = fma(T[a * q + k], Fs[k * q + b], t);
+        Acc[i] -= t;
+      }
+    }
+    __syncthreads();
+    const double c = coef[st] * dt;
+    for (int i = tid; i < pq; i += nthr) W[i] = S0[i] + c * Acc[i];
+    __syncthreads();
+  }
+  for (int i = tid; i < pq; i += nthr) S[i] = W[i];
+}
+
+void set_smem(const void* fn, size_t bytes) {
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// partition of a level: leaves of `br` rows, a short tail merged into the
+// previous block so every block but a lone one has >= cols rows
+Part make_part(int rows, int cols, int br) {
+  Part p{rows, cols, br, 0};
+  if (rows <= br) {
+    p.nblk = 1;
+    p.br = rows;
+    return p;
+  }
+  int nb = rows / br;
+  const int tail = rows - nb * br;
+  if (tail >= cols) nb += 1;  // tail is its own block (count = tail)
+  p.nblk = nb;                // else the tail is merged into the last block
+  return p;
+}
+
+}  // namespace
+
+void gemm(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB, double beta, Mat C,
+          long sC, int batch, cudaStream_t st) {
+  if (M <= 0 || N <= 0 || batch <= 0) return;
+  dim3 grid((N + 15) / 16, (M + 15) / 16, batch), block(16, 16);
+  gemm_kernel<<<grid, block, 0, st>>>(M, N, K, alpha, A, sA, B, sB, beta, C, sC);
+  CK(cudaGetLastError());
+}
+
+void axpby(int count, double a, const double* x, double b, double* y, cudaStream_t st) {
+  if (count <= 0) return;
+  int blocks = (count + 255) / 256;
+  if (blocks > 1024) blocks = 1024;
+  axpby_kernel<<<blocks, 256, 0, st>>>(count, a, x, b, y);
+  CK(cudaGetLastError());
+}
+
+int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfac, TsqrWork& w,
+         cudaStream_t st) {
+  if (cols > 64) fail(PND_ECONFIG, "orthonormalisation supports at most 64 columns");
+  const int kc = rows < cols ? rows : cols;
+  // level matrices: level 0 is `a`; level l+1 holds the stacked R's of level l
+  struct Level {
+    double* mat;
+    int ld;
+    Part part;
+    double* tau;
+    double* qexp;  // explicit Q of this level (non-leaf levels)
+  };
+  std::vector<Level> lv;
+  const int br0 = 128;
+  const int grp = cols > 32 ? 2 : (cols > 16 ? 4 : 8);
+  // sizes
+  size_t tree_need = 0, tau_need = 0, q_need = 0;
+  {
+    int r = rows;
+    Part p = make_part(r, cols, br0);
+    for (;;) {
+      tau_need += (size_t)p.nblk * cols;
+      const int next_rows = p.nblk * cols;
+      tree_need += (size_t)next_rows * cols;
+      if (p.nblk == 1) break;
+      q_need += (size_t)next_rows * cols;
+      p = make_part(next_rows, cols, grp * cols);
+    }
+  }
+  double* tree = w.tree.get(tree_need);
+  double* taus = w.tau.get(tau_need);
+  double* qbuf = w.cbuf.get(q_need > 0 ? q_need : 1);
+  {
+    double* mat = a;
+    int ld = lda;
+    Part p = make_part(rows, cols, br0);
+    size_t toff = 0, taoff = 0, qoff = 0;
+    for (;;) {
+      Level L{mat, ld, p, taus + taoff, nullptr};
+      taoff += (size_t)p.nblk * cols;
+      double* Rn = tree + toff;
+      const int ldn = p.nblk * cols;
+      toff += (size_t)ldn * cols;
+      // QR of every block of this level
+      const int tail_b = p.nblk - 1;
+      const int nreg = p.nblk - 1;
+      if (nreg > 0) {
+        const size_t sm = ((size_t)p.br * (cols + 1) + 32 + cols) * sizeof(double);
+        set_smem((const void*)hh_qr_kernel, sm);
+        hh_qr_kernel<<<nreg, 128, sm, st>>>(mat, ld, p, 0, L.tau, Rn, ldn);
+        CK(cudaGetLastError());
+      }
+      {
+        const size_t sm = ((size_t)p.count(tail_b) * (cols + 1) + 32 + cols) * sizeof(double);
+        set_smem((const void*)hh_qr_kernel, sm);
+        hh_qr_kernel<<<1, 128, sm, st>>>(mat, ld, p, tail_b, L.tau, Rn, ldn);
+        CK(cudaGetLastError());
+      }
+      lv.push_back(L);
+      if (p.nblk == 1) {
+        // root: its R block (kc x cols) is the triangular factor
+        copy_rfac_kernel<<<1, 256, 0, st>>>(Rn, ldn, p.rows < cols ? p.rows : cols, cols, rfac);
+        CK(cudaGetLastError());
+        break;
+      }
+      lv.back().qexp = qbuf + qoff;  // explicit Q of the NEXT level is stored per level below
+      qoff += (size_t)ldn * cols;
+      mat = Rn;
+      ld = ldn;
+      p = make_part(ldn, cols, grp * cols);
+    }
+  }
+  // top-down explicit Q: level L-1 (root) down to 0
+  const double* C = nullptr;
+  int ldc = 0;
+  for (int l = (int)lv.size() - 1; l >= 0; --l) {
+    Level& L = lv[l];
+    const Part& p = L.part;
+    const int kcl = (l == (int)lv.size() - 1) ? (p.rows < cols ? p.rows : cols) : cols;
+    double* out;
+    int ldo;
+    if (l == 0) {
+      out = q;
+      ldo = ldq;
+    } else {
+      out = lv[l - 1].qexp;
+      ldo = p.rows;
+    }
+    const int nreg = p.nblk - 1;
+    if (nreg > 0) {
+      const size_t sm = ((size_t)p.br * (cols + 1 + kcl + 1) + kcl) * sizeof(double);
+      set_smem((const void*)hh_applyq_kernel, sm);
+      hh_applyq_kernel<<<nreg, 128, sm, st>>>(L.mat, L.ld, p, 0, L.tau, C, ldc, kcl, out, ldo);
+      CK(cudaGetLastError());
+    }
+    {
+      const size_t sm =
+          ((size_t)p.count(p.nblk - 1) * (cols + 1 + kcl + 1) + kcl) * sizeof(double);
+      set_smem((const void*)hh_applyq_kernel, sm);
+      hh_applyq_kernel<<<1, 128, sm, st>>>(L.mat, L.ld, p, p.nblk - 1, L.tau, C, ldc, kcl, out,
+                                           ldo);
+      CK(cudaGetLastError());
+    }
+    C = out;
+    ldc = ldo;
+  }
+  return kc;
+}
+
+void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt, double*,
+               cudaStream_t st) {
+  const int M = p >= q ? p : q, N = p >= q ? q : p;
+  if (M > 256 || N > 64) fail(PND_ECONFIG, "truncation SVD supports at most 256 x 64");
+  const int N2 = N + (N & 1);
+  const size_t sm =
+      ((size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N + N2) * sizeof(double) + N * sizeof(int);
+  set_smem((const void*)svd_kernel, sm);
+  svd_kernel<<<1, 256, sm, st>>>(s, p, q, P, sig, Qt);
+  CK(cudaGetLastError());
+}
+
+void tail_rule(const double* sig, int k, double theta, int rmin, int rmax, int* info,
+               double* tail, cudaStream_t st) {
+  if (k > 128) fail(PND_ECONFIG, "tail rule supports at most 128 singular values");
+  tail_kernel<<<1, 32, 0, st>>>(sig, k, theta, rmin, rmax, info, tail);
+  CK(cudaGetLastError());
+}
+
+void scat_solves(const double* B, const double* coeffs, const double* lcols, int r, int m,
+                 double dt, double* lnew, int* singular, cudaStream_t st) {
+  const size_t sm = ((size_t)r * (r + 1) + r) * sizeof(double);
+  set_smem((const void*)scat_solve_kernel, sm);
+  scat_solve_kernel<<<m, 64, sm, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular);
+  CK(cudaGetLastError());
+}
+
+void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt, double*,
+           cudaStream_t st) {
+  const size_t sm = 4 * (size_t)p * q * sizeof(double);
+  set_smem((const void*)s_rk4_kernel, sm);
+  s_rk4_kernel<<<1, 1024, sm, st>>>(S, p, q, G, F, ns, dt);
+  CK(cudaGetLastError());
+}
+
+}  // namespace pnd

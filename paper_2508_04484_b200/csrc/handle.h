@@ -1,0 +1,55 @@
+// Device-resident problem + state of one DLRA solve (behind pnd_handle).
+#pragma once
+
+#include "pnd.h"
+
+namespace pnd {
+
+struct Handle {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  Geom g{};
+  int m = 0;
+  std::string err;
+  std::string stencil_error;  // non-empty for a 2-cell axis
+
+  // operators and coefficients
+  DBuf amat;        // ns x m x m, A_s in stencil order
+  DBuf inv_s;       // n
+  DBuf s_field;     // n (S at E_mid, for the "steps" tally)
+  IBuf cls;         // n
+  DBuf cls_atomic;  // n_cls x 12
+  DBuf cls_val;     // n_cls (staging)
+  int n_cls = 0;
+  DBuf gdiag;       // 12 x m
+  DBuf sigt;        // 12
+  int n_beams = 0;
+  DBuf psi;         // n_beams x ld (source slice, E_mid)
+  DBuf psi_lo;      // n_beams x ld (tally slice, E_lo)
+  DBuf tm;          // n_beams x m
+  DBuf flux;        // n_beams x G x ld (group tables)
+  int n_groups = 0;
+  bool have_angular = false, have_inv_s = false, have_mat = false, have_scat = false;
+
+  // state: U (ld x ru col-major), S (ru x rv row-major), V (m x rv row-major)
+  DBuf U, S, V;
+  int ru = 0, rv = 0;
+
+  // workspaces
+  DBuf A, Uhat, W1, W2;       // n-side (ld x cols)
+  DBuf part;                  // gram partials
+  TsqrWork tq_n, tq_m;
+  DBuf sm[48];                // small / m-side scratch (see step.cu Slot)
+  IBuf iflag;
+  DBuf dep, prev;             // dose tally
+  DBuf host_stage;            // unused placeholder
+  double* pinned = nullptr;   // small pinned readback buffer
+};
+
+void streaming_step(Handle& h, double dt);
+void scattering_step(Handle& h, double dt);
+void truncate(Handle& h, double theta, int rmin, int rmax, double* tail, int* rank);
+void dose_accumulate_step(Handle& h, double dt, bool tally_steps);
+double orth_defect(Handle& h);
+
+}  // namespace pnd

@@ -1,0 +1,447 @@
+// Orchestration of one pseudo-time (energy) step on the device.
+//
+// Shapes follow the reference: U0 (n x a), S0 (a x b), V0 (m x b); R-sized
+// augmented factors after each substep. The n-side work (O(n r^2) flops,
+// O(n r) bytes) runs in nside.cu / gram.cu / dense.cu TSQR kernels; the
+// m-side and R x R work is replicated small kernels. Horner's form is used for
+// every RK4 of a linear autonomous right-hand side (K, L and S phases): for
+// y' = L y, classic RK4 (dlra.py:118-123) equals
+//   y1 = y0 + h L (y0 + h/2 L (y0 + h/3 L (y0 + h/4 L y0)))
+// exactly in exact arithmetic, which takes 4 passes over n-side data instead
+// of the classic scheme's 4 stage evaluations plus 3 combination passes.
+#include <cmath>
+#include <cstring>
+
+#include "handle.h"
+
+namespace pnd {
+
+namespace {
+
+enum Slot {
+  S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RU, S_RV, S_ST1, S_SHAT, S_G,
+  S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
+  S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_UNEW, S_VNEW, S_SNEW, S_M2,
+  S_COUNT
+};
+
+double* slot(Handle& h, int s, size_t count) { return h.sm[s].get(count > 0 ? count : 1); }
+
+void need(bool ok, const char* what) {
+  if (!ok) fail(PND_ECONFIG, std::string("handle is missing ") + what);
+}
+
+// F_s(W) = W^T A_s W for every stencil s; W row-major (m x c) -> out ns x c x c
+void moment_factors(Handle& h, double* W, int c, double* out) {
+  const int m = h.m, ns = h.g.ns;
+  double* Y = slot(h, S_YST, (size_t)ns * m * c);
+  gemm(ns * m, c, m, 1.0, rowm(h.amat.p, m), 0, rowm(W, c), 0, 0.0, rowm(Y, c), 0, 1, h.st);
+  gemm(c, c, m, 1.0, tr(rowm(W, c)), 0, rowm(Y, c), (long)m * c, 0.0, rowm(out, c), (long)c * c,
+       ns, h.st);
+}
+
+// col-major (rows x c, ld) <- row-major (rows x c)
+void to_colmajor(Handle& h, const double* src, int rows, int c, double* dst, int ld) {
+  transpose_in(src, rows, c, dst, ld, h.st);
+}
+
+}  // namespace
+
+void streaming_step(Handle& h, double dt) {
+  if (!h.stencil_error.empty()) fail(PND_ECONFIG, h.stencil_error);
+  need(h.have_angular, "angular operators (pnd_set_angular)");
+  need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
+  const Geom& g = h.g;
+  const int m = h.m, ns = g.ns, ld = g.ld;
+  const int a = h.ru, b = h.rv;
+  if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
+  cudaStream_t st = h.st;
+
+  // --- K phase: K1 = RK4 of K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
+  double* F = slot(h, S_FV, (size_t)ns * b * b);
+  moment_factors(h, h.V.p, b, F);
+  const int xmax = a > b ? a : b;
+  double* M = slot(h, S_MST, (size_t)ns * xmax * b);
+  double* W1 = h.W1.get((size_t)ld * b);
+  double* W2 = h.W2.get((size_t)ld * b);
+  const int cols = a + b;
+  double* A = h.A.get((size_t)ld * cols);
+  const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+  for (int stage = 0; stage < 4; ++stage) {
+    KStageArgs ka{};
+    ka.geo = g;
+    ka.inv_s = h.inv_s.p;
+    ka.U0 = h.U.p;
+    ka.ldu = ld;
+    ka.ra = a;
+    ka.S0 = h.S.p;
+    ka.r = b;
+    ka.M = M;
+    const double c = -coef[stage] * dt;
+    if (stage == 0) {
+      // L(U0 S0) = -sum_s (D_s U0)(S0 F_s): X = U0, M_s = -(h/4) S0 F_s
+      gemm(a, b, b, c, rowm(h.S.p, b), 0, rowm(F, b), (long)b * b, 0.0, rowm(M, b),
+           (long)a * b, ns, st);
+      ka.X = h.U.p;
+      ka.ldx = ld;
+      ka.xc = a;
+      ka.out = W1;
+    } else {
+      axpby(ns * b * b, c, F, 0.0, M, st);
+      ka.X = stage == 2 ? W2 : W1;
+      ka.ldx = ld;
+      ka.xc = b;
+      ka.out = stage == 3 ? A : (stage == 1 ? W2 : W1);
+      if (stage == 3) {
+        ka.copy_u = A + (size_t)b * ld;  // [K1 | U0] for the augmentation
+        ka.ldc = ld;
+      }
+    }
+    ka.ldo = ld;
+    kstage(ka, st);
+  }
+
+  // --- L phase: L' = -sum_s A_s L Q_s, Q_s = (D_s S^-1 U0)^T U0, L0 = V0 S0^T
+  double* QT = slot(h, S_QT, (size_t)ns * a * a);
+  {
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
+    ga.Y = h.U.p; ga.ldy = ld; ga.nb = a;
+    ga.nphase = ns;
+    ga.gen = GEN_STENCIL;
+    ga.inv_s = h.inv_s.p;
+    ga.out = QT;  // QT_s = U0^T D_s U0 = Q_s^T
+    gram(ga, h.part, st);
+  }
+  double* L0 = slot(h, S_L0, (size_t)m * a);
+  double* LW = slot(h, S_LW, (size_t)m * a);
+  double* Z = slot(h, S_ZST, (size_t)ns * m * a);
+  gemm(m, a, b, 1.0, rowm(h.V.p, b), 0, tr(rowm(h.S.p, b)), 0, 0.0, rowm(L0, a), 0, 1, st);
+  CK(cudaMemcpyAsync(LW, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
+  double* BV = slot(h, S_BV, (size_t)m * cols);
+  for (int stage = 0; stage < 4; ++stage) {
+    // Z_s = LW Q_s  (Q_s = QT_s^T)
+    gemm(m, a, a, 1.0, rowm(LW, a), 0, tr(rowm(QT, a)), (long)a * a, 0.0, rowm(Z, a),
+         (long)m * a, ns, st);
+    double* dst = stage == 3 ? slot(h, S_M2, (size_t)m * a) : LW;
+    CK(cudaMemcpyAsync(dst, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
+    // dst = L0 - c h sum_s A_s Z_s  (A_s symmetric: [A_0..A_ns-1] = (stacked A)^T)
+    gemm(m, a, ns * m, -coef[stage] * dt, tr(rowm(h.amat.p, m)), 0, rowm(Z, a), 0, 1.0,
+         rowm(dst, a), 0, 1, st);
+    if (stage == 3) to_colmajor(h, dst, m, a, BV, m);
+  }
+  to_colmajor(h, h.V.p, m, b, BV + (size_t)a * m, m);
+
+  // --- augmentation: U^ = orth([K1, U0]), V^ = orth([L1, V0])  (dlra.py:220-221)
+  double* Uh = h.Uhat.get((size_t)ld * cols);
+  double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
+  double* Vhc = slot(h, S_VHC, (size_t)m * cols);
+  double* Rv = slot(h, S_RV, (size_t)cols * cols);
+  const int rv = tsqr(BV, m, cols, m, Vhc, m, Rv, h.tq_m, st);
+
+  // --- S^0 = (U^T U0) S0 (V0^T V^) = Ru[:, b:] S0 Rv[:, a:]^T
+  double* T1 = slot(h, S_ST1, (size_t)ru * b);
+  double* Sh = slot(h, S_SHAT, (size_t)ru * rv);
+  gemm(ru, b, a, 1.0, Mat{Ru + b, cols, 1}, 0, rowm(h.S.p, b), 0, 0.0, rowm(T1, b), 0, 1, st);
+  gemm(ru, rv, b, 1.0, rowm(T1, b), 0, Mat{Rv + a, 1, cols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
+
+  // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
+  double* G = slot(h, S_G, (size_t)ns * ru * ru);
+  {
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = Uh; ga.ldx = ld; ga.na = ru;
+    ga.Y = Uh; ga.ldy = ld; ga.nb = ru;
+    ga.nphase = ns;
+    ga.gen = GEN_STENCIL;
+    ga.inv_s = h.inv_s.p;
+    ga.out = G;
+    gram(ga, h.part, st);
+  }
+  double* Vhr = slot(h, S_VHR, (size_t)m * rv);
+  transpose_out(Vhc, m, m, rv, Vhr, st);
+  double* Fh = slot(h, S_FH, (size_t)ns * rv * rv);
+  moment_factors(h, Vhr, rv, Fh);
+  s_rk4(Sh, ru, rv, G, Fh, ns, dt, nullptr, st);
+
+  // --- new (augmented) state
+  std::swap(h.U, h.Uhat);
+  double* Snew = h.S.get((size_t)ru * rv);
+  CK(cudaMemcpyAsync(Snew, Sh, sizeof(double) * ru * rv, cudaMemcpyDeviceToDevice, st));
+  double* Vnew = h.V.get((size_t)m * rv);
+  CK(cudaMemcpyAsync(Vnew, Vhr, sizeof(double) * m * rv, cudaMemcpyDeviceToDevice, st));
+  h.ru = ru;
+  h.rv = rv;
+}
+
+namespace {
+
+__global__ void gt_kernel(const double* g, const double* tm, int m, int nb, double* gt) {
+  const int total = nb * 12 * m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int b = i / (12 * m), rem = i - b * 12 * m, q = rem % m;
+    gt[i] = g[rem] * tm[b * m + q];
+  }
+}
+
+__global__ void coeff_kernel(const double* g, const double* sig, int m, double* c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 12 * m; i += gridDim.x * blockDim.x)
+    c[i] = sig[i / m] - g[i];
+}
+
+__global__ void init_int(int* p, int v) { *p = v; }
+
+}  // namespace
+
+void scattering_step(Handle& h, double dt) {
+  need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
+  need(h.have_mat, "materials (pnd_set_materials)");
+  need(h.have_scat, "scattering tables (pnd_set_scattering)");
+  const Geom& g = h.g;
+  const int m = h.m, ld = g.ld;
+  const int a = h.ru, b = h.rv;
+  const int B = h.n_beams;
+  cudaStream_t st = h.st;
+  if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
+  if (a > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
+
+  // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
+  double* gt = slot(h, S_GT, (size_t)(B > 0 ? B : 1) * 12 * m);
+  double* rows = slot(h, S_ROWS, (size_t)(B > 0 ? B : 1) * 12 * b);
+  if (B > 0) {
+    gt_kernel<<<64, 256, 0, st>>>(h.gdiag.p, h.tm.p, m, B, gt);
+    CK(cudaGetLastError());
+    gemm(12 * B, b, m, 1.0, rowm(gt, m), 0, rowm(h.V.p, b), 0, 0.0, rowm(rows, b), 0, 1, st);
+  }
+
+  // substep 2 input: A = [K1 | U0], K1 = U0 S0 + dt src_rows(V0)  (dlra.py:303)
+  const int cols = b + a;
+  double* A = h.A.get((size_t)ld * cols);
+  scat_k1(g, h.U.p, ld, a, h.S.p, b, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p,
+          B > 0 ? h.psi.p : nullptr, ld, B, rows, A, ld, st);
+
+  // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
+  const int nw = h.n_cls <= 12 ? h.n_cls : 12;
+  double* H = slot(h, S_H, (size_t)nw * a * a);
+  {
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
+    ga.Y = h.U.p; ga.ldy = ld; ga.nb = a;
+    ga.nphase = nw;
+    ga.gen = GEN_WEIGHT;
+    ga.inv_s = h.inv_s.p;
+    ga.cls = h.cls.p;
+    ga.wtab = h.cls_atomic.p;
+    ga.n_cls = h.n_cls;
+    ga.wmode = h.n_cls <= 12 ? 0 : 1;
+    ga.out = H;
+    gram(ga, h.part, st);
+  }
+  double* Bi = slot(h, S_BI, (size_t)12 * a * a);
+  if (h.n_cls <= 12) {
+    // B_i = sum_k N_{k,i} H_k
+    gemm(12, a * a, h.n_cls, 1.0, tr(rowm(h.cls_atomic.p, 12)), 0, rowm(H, a * a), 0, 0.0,
+         rowm(Bi, a * a), 0, 1, st);
+  } else {
+    CK(cudaMemcpyAsync(Bi, H, sizeof(double) * 12 * a * a, cudaMemcpyDeviceToDevice, st));
+  }
+  // source projections U0^T (N psi_b / S)  (a x 12B)
+  double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
+  if (B > 0) {
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
+    ga.nb = 12 * B;
+    ga.nphase = 1;
+    ga.gen = GEN_SOURCE;
+    ga.inv_s = h.inv_s.p;
+    ga.cls = h.cls.p;
+    ga.wtab = h.cls_atomic.p;
+    ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
+    ga.out = left;
+    gram(ga, h.part, st);
+  }
+  double* coeffs = slot(h, S_COEF, (size_t)12 * m);
+  coeff_kernel<<<16, 256, 0, st>>>(h.gdiag.p, h.sigt.p, m, coeffs);
+  CK(cudaGetLastError());
+  double* lcols = slot(h, S_LCOL, (size_t)a * m);
+  gemm(a, m, b, 1.0, rowm(h.S.p, b), 0, tr(rowm(h.V.p, b)), 0, 0.0, rowm(lcols, m), 0, 1, st);
+  double* lnew = slot(h, S_LNEW, (size_t)a * m);
+  int* flag = h.iflag.get(4);
+  init_int<<<1, 1, 0, st>>>(flag, 1 << 30);
+  scat_solves(Bi, coeffs, lcols, a, m, dt, lnew, flag, st);
+  int singular = 0;
+  CK(cudaMemcpyAsync(&singular, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (singular != (1 << 30)) {
+    fail(PND_ENUMERICAL, "implicit scattering solve singular at moment column " +
+                             std::to_string(singular) +
+                             "; the step size is too large for the scattering stiffness");
+  }
+  // V~, R~ = qr(L1^T): lnew row-major (a x m) is L1^T column-major (m x a)
+  const int kt = m < a ? m : a;
+  double* Vtc = slot(h, S_VTC, (size_t)m * kt);
+  double* Rt = slot(h, S_RT, (size_t)kt * a);
+  tsqr(lnew, m, a, m, Vtc, m, Rt, h.tq_m, st);  // S~ = R~^T  (a x kt)
+
+  // substep 2: U^ = orth([K1, U0])
+  double* Uh = h.Uhat.get((size_t)ld * cols);
+  double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
+
+  // substep 3: l3 = V~ S~^T + dt proj^T, V^ = orth([l3, V~])  (dlra.py:306-312)
+  const int vcols = a + kt;
+  double* BV = slot(h, S_BV, (size_t)m * vcols);
+  double* proj = slot(h, S_PROJ, (size_t)a * m);
+  gemm(m, a, kt, 1.0, colm(Vtc, m), 0, rowm(Rt, a), 0, 0.0, colm(BV, m), 0, 1, st);
+  if (B > 0) {
+    for (int beam = 0; beam < B; ++beam) {
+      gemm(a, m, 12, 1.0, Mat{left + beam * 12, 12 * B, 1}, 0, rowm(gt + (size_t)beam * 12 * m, m),
+           0, beam == 0 ? 0.0 : 1.0, rowm(proj, m), 0, 1, st);
+    }
+    axpby(a * m, dt, proj, 1.0, BV, st);  // col-major (m x a) == row-major (a x m) layout
+  }
+  CK(cudaMemcpyAsync(BV + (size_t)a * m, Vtc, sizeof(double) * m * kt, cudaMemcpyDeviceToDevice,
+                     st));
+  double* Vhc = slot(h, S_VHC, (size_t)m * vcols);
+  double* Rv = slot(h, S_RV, (size_t)vcols * vcols);
+  const int rv = tsqr(BV, m, vcols, m, Vhc, m, Rv, h.tq_m, st);
+
+  // substep 4: S1 = (U^T U0) S~ (V~^T V^) + dt U^T (N psi / S)(g o T_M) V^
+  double* T1 = slot(h, S_ST1, (size_t)ru * kt);
+  double* Sh = slot(h, S_SHAT, (size_t)ru * rv);
+  gemm(ru, kt, a, 1.0, Mat{Ru + b, cols, 1}, 0, tr(rowm(Rt, a)), 0, 0.0, rowm(T1, kt), 0, 1, st);
+  gemm(ru, rv, kt, 1.0, rowm(T1, kt), 0, Mat{Rv + a, 1, vcols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
+  if (B > 0) {
+    double* proj2 = slot(h, S_PROJ2, (size_t)ru * 12 * B);
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = Uh; ga.ldx = ld; ga.na = ru;
+    ga.nb = 12 * B;
+    ga.nphase = 1;
+    ga.gen = GEN_SOURCE;
+    ga.inv_s = h.inv_s.p;
+    ga.cls = h.cls.p;
+    ga.wtab = h.cls_atomic.p;
+    ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
+    ga.out = proj2;
+    gram(ga, h.part, st);
+    double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
+    gemm(12 * B, rv, m, 1.0, rowm(gt, m), 0, colm(Vhc, m), 0, 0.0, rowm(gtv, rv), 0, 1, st);
+    for (int beam = 0; beam < B; ++beam) {
+      gemm(ru, rv, 12, dt, Mat{proj2 + beam * 12, 12 * B, 1}, 0,
+           rowm(gtv + (size_t)beam * 12 * rv, rv), 0, 1.0, rowm(Sh, rv), 0, 1, st);
+    }
+  }
+
+  std::swap(h.U, h.Uhat);
+  double* Snew = h.S.get((size_t)ru * rv);
+  CK(cudaMemcpyAsync(Snew, Sh, sizeof(double) * ru * rv, cudaMemcpyDeviceToDevice, st));
+  double* Vnew = h.V.get((size_t)m * rv);
+  transpose_out(Vhc, m, m, rv, Vnew, st);
+  h.ru = ru;
+  h.rv = rv;
+}
+
+namespace {
+__global__ void diag_kernel(const double* sig, int r, double* S) {
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) S[i] = (i / r == i % r) ? sig[i / r] : 0.0;
+}
+
+__global__ void defect_kernel(const double* G, int r, double* out) {
+  __shared__ double red[256];
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    const double v = fabs(G[i] - ((i / r == i % r) ? 1.0 : 0.0));
+    mx = v > mx ? v : mx;
+  }
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int i = 0; i < blockDim.x; ++i) m = red[i] > m ? red[i] : m;
+    out[0] = out[0] > m ? out[0] : m;
+  }
+}
+}  // namespace
+
+void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int* rank_out) {
+  const int p = h.ru, q = h.rv, k = p < q ? p : q;
+  cudaStream_t st = h.st;
+  double* P = slot(h, S_P, (size_t)p * k);
+  double* sig = slot(h, S_SIG, (size_t)k);
+  double* Qt = slot(h, S_QTM, (size_t)k * q);
+  svd_small(h.S.p, p, q, P, sig, Qt, nullptr, st);
+  double* dtail = slot(h, S_TAIL, 2);
+  int* info = h.iflag.get(4);
+  tail_rule(sig, k, theta, rmin, rmax, info + 1, dtail, st);
+  CK(cudaMemcpyAsync(h.pinned, dtail, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync((int*)(h.pinned + 1), info + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int r1 = *(int*)(h.pinned + 1);
+  const double tail = h.pinned[0];
+  if (r1 < 0) {
+    fail(PND_ENUMERICAL, "adaptive rank " + std::to_string(-r1 - 1) + " exceeds rank_max=" +
+                             std::to_string(rmax) + "; increase the truncation threshold");
+  }
+  const Geom& g = h.g;
+  const int m = h.m;
+  double* Unew = h.Uhat.get((size_t)g.ld * (r1 > 0 ? r1 : 1));
+  rotate_ld(g, h.U.p, g.ld, p, P, k, r1, Unew, g.ld, st);
+  double* Vn = slot(h, S_VNEW, (size_t)m * r1);
+  gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);
+  std::swap(h.U, h.Uhat);
+  double* V = h.V.get((size_t)m * r1);
+  CK(cudaMemcpyAsync(V, Vn, sizeof(double) * m * r1, cudaMemcpyDeviceToDevice, st));
+  double* S = h.S.get((size_t)r1 * r1);
+  diag_kernel<<<1, 256, 0, st>>>(sig, r1, S);
+  CK(cudaGetLastError());
+  h.ru = h.rv = r1;
+  if (tail_out) *tail_out = tail;
+  if (rank_out) *rank_out = r1;
+}
+
+void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
+  const Geom& g = h.g;
+  cudaStream_t st = h.st;
+  double* coef = slot(h, S_COEFD, (size_t)h.ru);
+  // integrand = sqrt(4 pi) U (S V[0, :]) (+ S psi_u(E_lo))  (driver.py:606, 613-621)
+  gemm(h.ru, 1, h.rv, 1.0, rowm(h.S.p, h.rv), 0, Mat{h.V.p, 1, 0}, 0, 0.0, Mat{coef, 1, 0}, 0, 1,
+       st);
+  double* dep = h.dep.get((size_t)g.ld);
+  double* prev = h.prev.get((size_t)g.ld);
+  pnd::dose_accumulate(g, h.U.p, g.ld, coef, h.ru, 0.5 * dt, h.s_field.p,
+                       tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr, g.ld, h.n_beams, dep,
+                       prev, st);
+}
+
+double orth_defect(Handle& h) {
+  const Geom& g = h.g;
+  cudaStream_t st = h.st;
+  double* G = slot(h, S_DEF, (size_t)h.ru * h.ru + (size_t)h.rv * h.rv + 2);
+  double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
+  GramArgs ga{};
+  ga.geo = g;
+  ga.X = h.U.p; ga.ldx = g.ld; ga.na = h.ru;
+  ga.Y = h.U.p; ga.ldy = g.ld; ga.nb = h.ru;
+  ga.nphase = 1;
+  ga.gen = GEN_PLAIN;
+  ga.inv_s = h.inv_s.p;
+  ga.out = G;
+  gram(ga, h.part, st);
+  double* GV = G + (size_t)h.ru * h.ru;
+  gemm(h.rv, h.rv, h.m, 1.0, tr(rowm(h.V.p, h.rv)), 0, rowm(h.V.p, h.rv), 0, 0.0,
+       rowm(GV, h.rv), 0, 1, st);
+  fill_zero(out, 1, st);
+  defect_kernel<<<1, 256, 0, st>>>(G, h.ru, out);
+  defect_kernel<<<1, 256, 0, st>>>(GV, h.rv, out);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(h.pinned + 2, out, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h.pinned[2];
+}
+
+}  // namespace pnd

@@ -1,0 +1,210 @@
+"""Device-resident energy loop: the hot path of pndose.driver.run_simulation.
+
+`run_bundle(bundle)` is the loop of driver.py:541-666 with the state kept on
+the GPU for the whole run: per step the host computes only the frozen
+coefficients of driver.step_contexts (a few hundred doubles: S per material
+class, the 12 x m scattering diagonals, the at_energy interpolation weights)
+and one `pnd_step` call does streaming -> truncate -> scattering ->
+truncate -> dose trapezoid on the device. The per-cell 1/S and S fields and
+the psi_u slices are formed on the device from those scalars.
+
+`run_simulation(config, solver="dlra")` is the drop-in entry point for a
+reference `ProblemConfig`: it assembles and ray-traces with the reference's
+own host code (which stays unchanged) and hands the energy
+loop to the device. It needs the reference package importable; on the GPU
+box the tests and the benchmark drive `run_bundle` with committed bundles.
+"""
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .dlra import LowRankState, orthonormal_columns
+from .errors import ConfigError
+from .problem import SQRT_4PI, ProblemBundle, export_problem
+
+TRUNCATE_FLAGS = {"streaming": 1, "scattering": 2, "both": 3}
+
+
+@dataclass
+class DoseGrid:
+    deposited: np.ndarray
+    dose: np.ndarray
+
+    @property
+    def negativity(self):
+        neg = self.deposited < 0.0
+        return {
+            "min_value": float(self.deposited.min(initial=0.0)),
+            "negative_cells": int(np.count_nonzero(neg)),
+        }
+
+
+@dataclass
+class SimulationResult:
+    bundle: ProblemBundle
+    dose: DoseGrid
+    rank_history: list
+    diagnostics: dict
+    uncollided: np.ndarray = field(default=None, repr=False)
+
+
+class DeviceSolver:
+    """One bundle's device state: operators, flux tables, low-rank factors."""
+
+    def __init__(self, bundle: ProblemBundle, device: int = 0):
+        self.bundle = bundle
+        b = bundle
+        self.h = _lib.Handle(b.shape, b.spacing, b.n_moments, device)
+        self.h.set_angular(*b.a_split())
+        self.h.set_materials(b.cell_class, b.class_atomic)
+        nb = len(b.fluxes)
+        for i, (f, tm) in enumerate(zip(b.fluxes, b.t_ms)):
+            vals = _lib.f64(f.values)
+            t = _lib.f64(tm)
+            self.h.call("pnd_set_flux_table", i, nb, int(vals.shape[1]), _lib.ptr(vals),
+                        _lib.ptr(t))
+        self.h.call("pnd_dose_reset")
+
+    def init_state(self, rank=None, seed=None):
+        """LowRankState.zero (dlra.py:54-60): seeded Gaussian bases, S = 0."""
+        b = self.bundle
+        n, m = b.n_cells, b.n_moments
+        r0 = min(b.rank_min if rank is None else rank, n, m)
+        st = LowRankState.zero(n, m, r0, seed=b.seed if seed is None else seed)
+        self.h.set_state(st.u, st.s, st.v)
+
+    def select_flux(self, which: int, e_mev: float):
+        fl = self.bundle.fluxes
+        if not fl:
+            return
+        w = [f.lerp_weights(e_mev) for f in fl]
+        j0 = np.array([x[0] for x in w], dtype=np.int32)
+        w0 = np.array([x[1] for x in w])
+        j1 = np.array([x[2] for x in w], dtype=np.int32)
+        w1 = np.array([x[3] for x in w])
+        self.h.call("pnd_select_flux", which, _lib.ptr(j0), _lib.ptr(w0), _lib.ptr(j1),
+                    _lib.ptr(w1))
+
+    def set_coefficients(self, e_hi: float, e_lo: float):
+        """driver.step_contexts (driver.py:523-538), coefficients only."""
+        b = self.bundle
+        e_mid = 0.5 * (e_hi + e_lo)
+        self.h.set_class_stopping(b.class_stopping(e_mid))
+        g, s = b.scattering_tables(e_mid)
+        self.h.set_scattering(g, s)
+        self.select_flux(0, e_mid)
+        if b.uncollided_tally == "steps":
+            self.select_flux(1, e_lo)
+
+    def step(self, dt: float, want_defect: bool = True):
+        b = self.bundle
+        out = np.zeros(4)
+        self.h.call(
+            "pnd_step", float(dt), float(b.truncation_tolerance), int(b.rank_min),
+            int(b.rank_max), TRUNCATE_FLAGS[b.truncate_after],
+            1 if b.uncollided_tally == "steps" else 0, 1 if want_defect else 0, _lib.ptr(out),
+        )
+        return out
+
+    def dose(self) -> np.ndarray:
+        out = np.empty(self.bundle.n_cells)
+        self.h.call("pnd_get_dose", _lib.ptr(out))
+        return out
+
+    def state(self):
+        return self.h.get_state()
+
+    def close(self):
+        self.h.close()
+
+
+def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0,
+               solver="dlra") -> SimulationResult:
+    """The pseudo-time loop of run_simulation (driver.py:541-666) on the device."""
+    if solver != "dlra":
+        raise ConfigError(f"unknown solver '{solver}'")
+    t_start = time.perf_counter()
+    b = bundle
+    n, m = b.n_cells, b.n_moments
+    solver_ = DeviceSolver(b, device)
+    solver_.init_state()
+    edges = b.pseudo_time_edges()
+    n_steps = len(edges) - 1
+    if max_steps is not None:
+        n_steps = min(n_steps, int(max_steps))
+    de = float(edges[0] - edges[1])
+    ranks, max_tail, violations, max_defect = [], 0.0, 0, 0.0
+    peak_state = 0
+    peak_transient = 0
+    for k in range(n_steps):
+        e_hi, e_lo = edges[k], edges[k + 1]
+        solver_.set_coefficients(e_hi, e_lo)
+        out = solver_.step(e_hi - e_lo, want_defect)
+        r = int(out[2])
+        for idx, flag in ((0, 1), (1, 2)):
+            if TRUNCATE_FLAGS[b.truncate_after] & flag:
+                tail = float(out[idx])
+                max_tail = max(max_tail, tail)
+                violations += tail > b.truncation_tolerance + 1e-15
+        max_defect = max(max_defect, float(out[3]))
+        ranks.append((k, float(e_lo), r))
+        peak_state = max(peak_state, n * r + r * r + m * r)
+        peak_transient = max(peak_transient, n * 2 * r + 4 * r * r + m * 2 * r)
+    deposited = solver_.dose()
+    unc = None
+    if b.uncollided_tally == "groups":
+        unc = b.uncollided_dose()
+        deposited = deposited + unc
+    solver_.close()
+    density = b.density
+    dose = DoseGrid(deposited=deposited, dose=deposited / density)
+    full = n * m
+    diagnostics = {
+        "solver": "dlra-b200",
+        "n_cells": n,
+        "n_moments": m,
+        "n_steps": n_steps,
+        "energy_step_mev": de,
+        "max_orthonormality_defect": max_defect,
+        "max_truncation_tail": max_tail,
+        "tail_violations": int(violations),
+        "mean_rank": float(np.mean([r for _, _, r in ranks])) if ranks else 0.0,
+        "max_rank": int(max((r for _, _, r in ranks), default=0)),
+        "peak_state_numbers": int(peak_state),
+        "peak_transient_numbers": int(peak_transient),
+        "fullrank_numbers": int(full),
+        "state_memory_fraction": float(peak_state / full),
+        "negativity": dose.negativity,
+        "runtime_s": time.perf_counter() - t_start,
+    }
+    return SimulationResult(bundle=b, dose=dose, rank_history=ranks, diagnostics=diagnostics,
+                            uncollided=unc)
+
+
+def run_simulation(config, solver: str = "dlra"):
+    """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541).
+
+    `config` is a reference ProblemConfig. Problem assembly and ray tracing
+    are the reference's unchanged host code; the energy loop runs on the GPU.
+    solver="dlra-cpu" / "fullrank" hand the whole run back to the reference.
+    """
+    from pndose import driver as ref_driver  # the reference package
+    from pndose.angular import beam_projection
+
+    if solver in ("dlra-cpu", "fullrank"):
+        return ref_driver.run_simulation(config, solver="dlra" if solver == "dlra-cpu" else solver)
+    if solver != "dlra":
+        raise ConfigError(f"unknown solver '{solver}'")
+    problem = ref_driver.assemble_problem(config)
+    fluxes = ref_driver.trace_all_beams(problem)
+    t_ms = [beam_projection(config.pn_order, bm.direction) for bm in config.beams]
+    bundle = ProblemBundle.from_arrays(export_problem(problem, fluxes, t_ms))
+    return run_bundle(bundle)
+
+
+__all__ = ["DeviceSolver", "run_bundle", "run_simulation", "SimulationResult", "DoseGrid",
+           "SQRT_4PI", "math", "orthonormal_columns"]

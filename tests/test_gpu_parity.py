@@ -1,0 +1,310 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the reference.
+
+Tiers follow SURVEY.md §8(c):
+  T0 bit-exact voxel lists and t-intervals (traversal);
+  T1 kernel level on identical inputs, <= 1e-12 relative (FP64 reordering);
+  T2 single-step reconstruction U S V^T after streaming / scattering /
+     truncation, <= 1e-11 relative;
+  T3 maximal-rank lockstep DLRA vs full rank, <= 1e-8;
+  T4/T5 end-to-end dose vs the reference: dev <= 10 x the gauge floor of
+     tests/golden/floors.json (written by tools/measure_floors.py) with equal
+     rank histories; T6 the rank-1 regime.
+Every expected value comes from the reference (tests/golden/*.npz) or the
+numpy oracle pinned to it (tests/test_oracle.py).
+"""
+
+import json
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / nb) if nb > 0 else float(
+        np.linalg.norm(a))
+
+
+def relmax(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+def grid_ns(arr):
+    nx, ny, nz = (int(v) for v in arr[:3])
+    return SimpleNamespace(nx=nx, ny=ny, nz=nz, dx=float(arr[3]), dy=float(arr[4]),
+                           dz=float(arr[5]))
+
+
+def ops_ns(npz, p):
+    return SimpleNamespace(eig_v=list(npz[p + "eig_v"]), lam_plus=list(npz[p + "lam_plus"]),
+                           lam_minus=list(npz[p + "lam_minus"]))
+
+
+KCASES = ["g3d", "g3d_b", "gz", "gyz", "gx3"]
+
+
+@pytest.fixture(scope="module")
+def dl():
+    from paper_2508_04484_b200 import dlra
+
+    return dlra
+
+
+# ------------------------------------------------------------------ T1
+@pytest.mark.parametrize("case", KCASES)
+def test_apply_streaming(dl, kernels_npz, case):
+    p = case + "_"
+    K = kernels_npz
+    ctx = dl.StreamingContext(K[p + "inv_s"], SimpleNamespace(grid=grid_ns(K[p + "grid"])),
+                              ops_ns(K, p))
+    got = ctx.full_rhs(K[p + "u_full"])
+    assert relmax(got, K[p + "apply_streaming"]) < 1e-12
+
+
+@pytest.mark.parametrize("case", KCASES)
+def test_k_rhs_and_l_grams(dl, kernels_npz, case):
+    p = case + "_"
+    K = kernels_npz
+    ctx = dl.StreamingContext(K[p + "inv_s"], SimpleNamespace(grid=grid_ns(K[p + "grid"])),
+                              ops_ns(K, p))
+    got = ctx.k_rhs(K[p + "k"], ctx._moment_factors(K[p + "v0"]))
+    assert relmax(got, K[p + "k_rhs"]) < 1e-12
+    lf = ctx.l_step_factors(K[p + "u0"])
+    q = np.array([[f[2], f[3]] for f in lf])
+    assert relmax(q, K[p + "q_grams"]) < 1e-12
+    got_l = ctx.l_rhs(K[p + "l"], lf)
+    assert relmax(got_l, K[p + "l_rhs"]) < 1e-12
+    sf = ctx.s_step_factors(K[p + "u0"], K[p + "v0"])
+    assert relmax(ctx.s_rhs(K[p + "s"], K[p + "u0"], sf), K[p + "s_rhs"]) < 1e-11
+
+
+def test_non_finite_streaming_input(dl, kernels_npz):
+    from paper_2508_04484_b200.errors import NumericalError
+
+    p = "gz_"
+    K = kernels_npz
+    ctx = dl.StreamingContext(K[p + "inv_s"], SimpleNamespace(grid=grid_ns(K[p + "grid"])),
+                              ops_ns(K, p))
+    u = K[p + "u_full"].copy()
+    u[0, 0] = np.nan
+    with pytest.raises(NumericalError, match="non-finite"):
+        ctx.full_rhs(u)
+
+
+def test_two_cell_axis_rejected(dl, kernels_npz):
+    from paper_2508_04484_b200.errors import ConfigError
+
+    K = kernels_npz
+    p = "g3d_"
+    grid = SimpleNamespace(nx=2, ny=3, nz=3, dx=0.1, dy=0.1, dz=0.1)
+    ctx = dl.StreamingContext(np.ones(18), SimpleNamespace(grid=grid), ops_ns(K, p))
+    with pytest.raises(ConfigError, match="3-point"):
+        ctx.full_rhs(np.zeros((18, K[p + "eig_v"].shape[1])))
+
+
+@pytest.mark.parametrize("shape", [(7, 3), (40, 6), (300, 12), (1000, 40), (5, 9), (129, 64),
+                                   (4000, 2)])
+def test_orthonormalize_tsqr(dl, shape):
+    rng = np.random.default_rng(sum(shape))
+    a = rng.standard_normal(shape)
+    if shape[1] >= 4:
+        a[:, 1] = 0.0                      # exactly zero column
+        a[:, 3] = 2.0 * a[:, 2]            # rank deficiency
+    q = dl.orthonormal_columns(a)
+    k = min(shape)
+    assert q.shape == (shape[0], k)
+    assert np.abs(q.T @ q - np.eye(k)).max() < 1e-13
+    # the span of a is contained in span(q)
+    assert np.abs(q @ (q.T @ a) - a).max() < 1e-12 * max(1.0, np.abs(a).max())
+
+
+def test_orthonormalize_zero_block_is_canonical(dl):
+    # [0 | U0] -> first columns are +e_0.. (reference step-0 behaviour, Appendix C.4)
+    rng = np.random.default_rng(5)
+    u0 = np.linalg.qr(rng.standard_normal((700, 5)))[0]
+    q = dl.orthonormal_columns(np.hstack([np.zeros((700, 5)), u0]))
+    np.testing.assert_array_equal(q[:, :5], np.eye(700)[:, :5])
+
+
+@pytest.mark.parametrize("pq", [(6, 6), (10, 4), (4, 10), (40, 40), (32, 16)])
+def test_svd_small(pq):
+    from paper_2508_04484_b200 import _lib
+    from paper_2508_04484_b200.dlra import _generic_handle
+
+    p, q = pq
+    rng = np.random.default_rng(p * 100 + q)
+    s = rng.standard_normal((p, q)) * np.exp(-0.3 * np.arange(q))
+    k = min(p, q)
+    pm, sig, qt = np.empty((p, k)), np.empty(k), np.empty((k, q))
+    _generic_handle().call("pnd_svd_small", _lib.ptr(s), p, q, _lib.ptr(pm), _lib.ptr(sig),
+                           _lib.ptr(qt))
+    ref = np.linalg.svd(s, compute_uv=False)
+    assert relmax(sig, ref) < 1e-13
+    assert np.abs(pm.T @ pm - np.eye(k)).max() < 1e-13
+    assert np.abs(qt @ qt.T - np.eye(k)).max() < 1e-13
+    assert relmax(pm @ np.diag(sig) @ qt, s) < 1e-13
+    # zero matrix -> identity factors (np.linalg.svd(0) convention)
+    z = np.zeros((p, q))
+    _generic_handle().call("pnd_svd_small", _lib.ptr(z), p, q, _lib.ptr(pm), _lib.ptr(sig),
+                           _lib.ptr(qt))
+    np.testing.assert_array_equal(pm, np.eye(p, k))
+    np.testing.assert_array_equal(qt, np.eye(k, q))
+
+
+# ------------------------------------------------------------------ T2
+@pytest.mark.parametrize("case", ["str3d", "str2d", "strz"])
+def test_streaming_step_and_truncate(dl, steps_npz, case):
+    S = steps_npz
+    p = case + "_"
+    ctx = dl.StreamingContext(S[p + "inv_s"], SimpleNamespace(grid=grid_ns(S[p + "grid"])),
+                              ops_ns(S, p))
+    st = dl.LowRankState(S[p + "u0"], S[p + "s0"], S[p + "v0"])
+    aug = dl.streaming_step(st, float(S[p + "dt"]), ctx)
+    assert aug.orthonormality_defect() < 1e-13
+    assert rel(aug.matrix(), S[p + "aug_matrix"]) < 1e-11
+    sig = np.linalg.svd(aug.s, compute_uv=False)
+    assert relmax(sig[: len(S[p + "aug_sigma"])], S[p + "aug_sigma"]) < 1e-9
+    r = st.s.shape[0]
+    tr0, tail0 = dl.truncate(aug, dl.TruncationPolicy(0.0, 1, 2 * r))
+    assert tr0.rank == int(S[p + "trunc0_rank"])
+    assert rel(tr0.matrix(), S[p + "trunc0_matrix"]) < 1e-11
+    trr, tailr = dl.truncate(aug, dl.TruncationPolicy(1e300, r, r))
+    assert rel(trr.matrix(), S[p + "truncr_matrix"]) < 1e-10
+    assert tailr == pytest.approx(float(S[p + "truncr_tail"]), rel=1e-9)
+
+
+@pytest.mark.parametrize("case", ["scat_h", "scat_x", "scat_max"])
+def test_scattering_step_and_truncate(dl, steps_npz, case):
+    S = steps_npz
+    p = case + "_"
+    ctx = dl.ScatteringContext(S[p + "weights"], S[p + "inv_s"], S[p + "g_diags"],
+                               S[p + "sigma_t"], list(zip(S[p + "psi"], S[p + "tm"])))
+    st = dl.LowRankState(S[p + "u0"], S[p + "s0"], S[p + "v0"])
+    aug = dl.scattering_step(st, float(S[p + "dt"]), ctx)
+    assert tuple(aug.s.shape) == tuple(S[p + "aug_shape"])
+    assert aug.orthonormality_defect() < 1e-12
+    assert rel(aug.matrix(), S[p + "aug_matrix"]) < 1e-11
+    r = st.s.shape[0]
+    tr0, _ = dl.truncate(aug, dl.TruncationPolicy(0.0, 1, 2 * r))
+    assert tr0.rank == int(S[p + "trunc0_rank"])
+    assert rel(tr0.matrix(), S[p + "trunc0_matrix"]) < 1e-10
+
+
+def test_truncation_rule_cases(dl, steps_npz):
+    for row in steps_npz["trunc_cases"]:
+        theta, rmin, rmax, rank, tail = row[:5]
+        sig = row[5:]
+        q = sig.size
+        st = dl.LowRankState(np.eye(q), np.diag(sig), np.eye(q))
+        out, t = dl.truncate(st, dl.TruncationPolicy(theta, int(rmin), int(rmax)))
+        assert out.rank == int(rank)
+        assert t == pytest.approx(tail, rel=1e-12, abs=1e-300)
+
+
+def test_truncation_rank_max_error(dl):
+    from paper_2508_04484_b200.errors import NumericalError
+
+    rng = np.random.default_rng(29)
+    u = np.linalg.qr(rng.standard_normal((20, 6)))[0]
+    v = np.linalg.qr(rng.standard_normal((10, 6)))[0]
+    st = dl.LowRankState(u, np.diag([4.0, 2.0, 1.0, 0.5, 0.1, 0.01]), v)
+    out, _ = dl.truncate(st, dl.TruncationPolicy(100.0, rank_min=3, rank_max=5))
+    assert out.rank == 3
+    with pytest.raises(NumericalError, match="rank_max"):
+        dl.truncate(st, dl.TruncationPolicy(1e-9, rank_min=1, rank_max=2))
+
+
+def test_singular_implicit_solve_reports_column(dl):
+    from paper_2508_04484_b200.errors import NumericalError
+
+    n, m, r = 4, 3, 2
+    state = dl.LowRankState(u=np.eye(n)[:, :r], s=np.eye(r), v=np.eye(m)[:, :r])
+    ctx = dl.ScatteringContext(np.ones((n, 12)) / 12.0, np.ones(n), np.zeros((12, m)),
+                               -np.ones(12), [])
+    with pytest.raises(NumericalError, match="column 0"):
+        dl.scattering_step(state, 1.0, ctx)
+
+
+# ------------------------------------------------------------------ T0
+def test_traverse_bit_exact(traverse_npz):
+    from paper_2508_04484_b200.raytracer import traverse_rays
+
+    T = traverse_npz
+    for gname in T["grids"]:
+        p = str(gname) + "_"
+        gr = T[p + "grid"]
+        cells, t0, t1, offs = traverse_rays(tuple(int(v) for v in gr[:3]), tuple(gr[3:6]),
+                                            tuple(gr[6:9]), T[p + "origins"], T[p + "dirs"])
+        np.testing.assert_array_equal(offs, T[p + "offsets"])
+        np.testing.assert_array_equal(cells, T[p + "cells"])
+        # bit-exact float64 intervals
+        np.testing.assert_array_equal(t0.view(np.int64), T[p + "t0"].view(np.int64))
+        np.testing.assert_array_equal(t1.view(np.int64), T[p + "t1"].view(np.int64))
+
+
+# ------------------------------------------------------------------ T3
+def test_lockstep_maximal_rank_vs_fullrank():
+    """Acceptance criterion 2 (test_acceptance.py:101-152) on the device:
+    DLRA at maximal rank r = m = 16 vs the full-rank oracle, <= 1e-8."""
+    from oracle import dlra_np
+    from paper_2508_04484_b200.driver import DeviceSolver
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_lockstep.npz")
+    grid = dlra_np.Grid(*b.shape, *b.spacing)
+    ops = dlra_np.Ops(b.eig_v, b.lam_plus, b.lam_minus)
+    solver = dlra_np.Grid  # noqa: F841
+    dev = DeviceSolver(b)
+    dev.init_state(rank=16)
+    edges = b.pseudo_time_edges()
+    n, m = b.n_cells, b.n_moments
+    u = np.zeros((n, m))
+    weights = b.atomic_densities
+    worst = 0.0
+    for k in range(len(edges) - 1):
+        dt = edges[k] - edges[k + 1]
+        dev.set_coefficients(edges[k], edges[k + 1])
+        dev.step(dt, want_defect=False)
+        e_mid = 0.5 * (edges[k] + edges[k + 1])
+        inv_s = 1.0 / b.stopping_field(e_mid)
+        g, s = b.scattering_tables(e_mid)
+        u = dlra_np.fullrank_streaming_step(u, dt, inv_s, grid, ops)
+        u = dlra_np.fullrank_scattering_step(u, dt, weights, inv_s, g, s,
+                                             list(zip(b.psi_at(e_mid), b.t_ms)))
+        if k % 20 == 0 or k == len(edges) - 2:
+            uu, ss, vv = dev.state()
+            norm = np.linalg.norm(u)
+            if norm > 0:
+                worst = max(worst, np.linalg.norm(uu @ ss @ vv.T - u) / norm)
+    dev.close()
+    assert worst <= 1e-8, worst
+
+
+# ------------------------------------------------------------------ T4/T5/T6
+FLOORS = json.loads((GOLDEN / "floors.json").read_text())
+
+
+@pytest.mark.parametrize("tag", ["rank1", "hetero", "smoke", "fp", "config1"])
+def test_end_to_end_dose(tag):
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / f"bundle_{tag}.npz")
+    g = golden(f"e2e_{tag}.npz")
+    res = run_bundle(b)
+    dep = res.dose.deposited
+    unc = g["uncollided"]
+    ranks = np.array([r for _, _, r in res.rank_history])
+    np.testing.assert_array_equal(ranks, g["rank_history"][:, 2].astype(int))
+    assert res.diagnostics["max_orthonormality_defect"] < 1e-10
+    assert res.diagnostics["tail_violations"] == 0
+    floor = FLOORS[tag]
+    dev_total = rel(dep, g["deposited"])
+    dev_coll = rel(dep - unc, g["deposited"] - unc)
+    assert dev_total <= max(10.0 * floor["total"], 1e-12), (dev_total, floor)
+    assert dev_coll <= max(10.0 * floor["collided"], 1e-10), (dev_coll, floor)

@@ -1,0 +1,492 @@
+"""Generate the golden fixtures under tests/golden/ from the reference.
+
+Runs HERE only (the reference tree exists in this container, not on the GPU
+box). It imports the unmodified reference package from
+/root/reference/pkg/src, runs it on small seeded inputs and writes the
+inputs and outputs as .npz fixtures. The fixtures travel with the repo; the
+tests, smoke() and bench.py read only the fixtures, never the reference.
+
+    PYTHONDONTWRITEBYTECODE=1 OPENBLAS_NUM_THREADS=1 python tools/make_golden.py
+
+OPENBLAS_NUM_THREADS is pinned because the reference's collided output
+depends on the BLAS thread count; the versions used are
+recorded in every fixture under the key `provenance`.
+"""
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF_SRC = Path("/root/reference/pkg/src")
+OUT = Path(__file__).resolve().parents[1] / "tests" / "golden"
+
+sys.path.insert(0, str(REF_SRC))
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import scipy  # noqa: E402
+
+from pndose import angular, dlra, driver, raytracer, spatial  # noqa: E402
+from pndose.angular import PNOperators  # noqa: E402
+from pndose.fullrank import fullrank_scattering_step, fullrank_streaming_step  # noqa: E402
+
+from paper_2508_04484_b200.problem import export_problem  # noqa: E402
+
+
+def provenance():
+    return json.dumps(
+        {
+            "numpy": np.__version__,
+            "scipy": scipy.__version__,
+            "openblas_threads": os.environ.get("OPENBLAS_NUM_THREADS"),
+            "reference": str(REF_SRC),
+            "generated": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
+        }
+    )
+
+
+def save(name, **arrays):
+    arrays["provenance"] = np.array(provenance())
+    path = OUT / name
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {path} ({path.stat().st_size / 1024:.1f} KiB)")
+
+
+def ops_arrays(ops, prefix=""):
+    return {
+        prefix + "eig_v": np.stack(ops.eig_v),
+        prefix + "lam_plus": np.stack(ops.lam_plus),
+        prefix + "lam_minus": np.stack(ops.lam_minus),
+    }
+
+
+# --------------------------------------------------------------- angular
+def make_angular():
+    out = {}
+    for n_max in (1, 2, 3, 5, 7):
+        ops = PNOperators.build(n_max)
+        out[f"a_{n_max}"] = np.stack(ops.matrices)
+        out[f"spectral_radius_{n_max}"] = np.array(ops.spectral_radius)
+        for d in range(3):
+            v = ops.eig_v[d]
+            out[f"aplus_{n_max}_{d}"] = (v * ops.lam_plus[d]) @ v.T
+            out[f"aminus_{n_max}_{d}"] = (v * ops.lam_minus[d]) @ v.T
+        out[f"tm_{n_max}"] = angular.beam_projection(n_max, (0.0, 0.6, 0.8))
+        out[f"fp_{n_max}"] = angular.scattering_matrix_fp(2.5e-3, n_max)
+    save("angular.npz", **out)
+
+
+# --------------------------------------------------------------- kernels
+KERNEL_CASES = [
+    # name, grid, n_max, r
+    ("g3d", spatial.Grid3D(5, 4, 6, 0.2, 0.25, 0.2), 2, 3),
+    ("g3d_b", spatial.Grid3D(7, 6, 5, 0.1, 0.15, 0.3), 3, 5),
+    ("gz", spatial.Grid3D(1, 1, 12, 1.0, 1.0, 0.1), 2, 2),
+    ("gyz", spatial.Grid3D(1, 6, 7, 2.0, 0.1, 0.1), 3, 4),
+    ("gx3", spatial.Grid3D(3, 1, 1, 0.3, 1.0, 1.0), 1, 1),
+]
+
+
+def make_kernels():
+    out = {}
+    for name, grid, n_max, r in KERNEL_CASES:
+        rng = np.random.default_rng(sum(name.encode()) * 31 + r)
+        ops = PNOperators.build(n_max)
+        stencils = spatial.build_stencils(grid)
+        n, m = grid.n_cells, ops.basis.size
+        inv_s = 1.0 / rng.uniform(8.0, 20.0, n)
+        ctx = dlra.StreamingContext(inv_s, stencils, ops)
+        u_full = rng.standard_normal((n, m))
+        u0 = dlra.orthonormal_columns(rng.standard_normal((n, r)))
+        v0 = dlra.orthonormal_columns(rng.standard_normal((m, r)))
+        k = rng.standard_normal((n, r))
+        l = rng.standard_normal((m, r))
+        s = rng.standard_normal((r, r))
+        kf = ctx._moment_factors(v0)
+        lf = ctx.l_step_factors(u0)
+        sf = ctx.s_step_factors(u0, v0)
+        p = name + "_"
+        out.update(
+            {
+                p + "grid": np.array([grid.nx, grid.ny, grid.nz, grid.dx, grid.dy, grid.dz]),
+                p + "n_max": np.array(n_max),
+                p + "inv_s": inv_s,
+                p + "u_full": u_full,
+                p + "apply_streaming": spatial.apply_streaming(u_full, inv_s, stencils, ops),
+                p + "u0": u0,
+                p + "v0": v0,
+                p + "k": k,
+                p + "l": l,
+                p + "s": s,
+                p + "k_rhs": ctx.k_rhs(k, kf),
+                p + "l_rhs": ctx.l_rhs(l, lf),
+                p + "s_rhs": ctx.s_rhs(s, u0, sf),
+                # (Ds+- U0)^T U0 per active axis, stacked [axis][+/-]
+                p + "q_grams": np.array([[f[2], f[3]] for f in lf]),
+                p + "active": np.array(ctx.active_axes),
+            }
+        )
+        out.update(ops_arrays(ops, p))
+    save("kernels.npz", **out)
+
+
+# --------------------------------------------------------------- steps
+def make_steps():
+    out = {}
+    # streaming: full-rank-ish well-conditioned state on a small 3-D grid
+    for name, grid, n_max, r, dt in (
+        ("str3d", spatial.Grid3D(6, 5, 7, 0.2, 0.2, 0.25), 2, 3, 0.02),
+        ("str2d", spatial.Grid3D(1, 8, 9, 2.0, 0.1, 0.1), 3, 4, 0.01),
+        ("strz", spatial.Grid3D(1, 1, 64, 1.0, 1.0, 0.1), 3, 2, 0.05),
+    ):
+        rng = np.random.default_rng(len(name) * 1000 + r)
+        ops = PNOperators.build(n_max)
+        stencils = spatial.build_stencils(grid)
+        n, m = grid.n_cells, ops.basis.size
+        inv_s = 1.0 / rng.uniform(8.0, 20.0, n)
+        ctx = dlra.StreamingContext(inv_s, stencils, ops)
+        u0 = dlra.orthonormal_columns(rng.standard_normal((n, r)))
+        v0 = dlra.orthonormal_columns(rng.standard_normal((m, r)))
+        s0 = np.diag(np.logspace(0, -2, r)) + 0.01 * rng.standard_normal((r, r))
+        st = dlra.LowRankState(u0, s0, v0)
+        aug = dlra.streaming_step(st, dt, ctx)
+        tr, tail = dlra.truncate(aug, dlra.TruncationPolicy(0.0, rank_min=1, rank_max=2 * r))
+        trr, tailr = dlra.truncate(aug, dlra.TruncationPolicy(1e300, rank_min=r, rank_max=r))
+        full = fullrank_streaming_step(st.matrix(), dt, ctx)
+        p = name + "_"
+        out.update(
+            {
+                p + "grid": np.array([grid.nx, grid.ny, grid.nz, grid.dx, grid.dy, grid.dz]),
+                p + "n_max": np.array(n_max),
+                p + "dt": np.array(dt),
+                p + "inv_s": inv_s,
+                p + "u0": u0,
+                p + "s0": s0,
+                p + "v0": v0,
+                p + "aug_matrix": aug.matrix(),
+                p + "aug_sigma": np.linalg.svd(aug.s, compute_uv=False),
+                p + "trunc0_matrix": tr.matrix(),
+                p + "trunc0_rank": np.array(tr.rank),
+                p + "trunc0_tail": np.array(tail),
+                p + "truncr_matrix": trr.matrix(),
+                p + "truncr_tail": np.array(tailr),
+                p + "full_matrix": full,
+            }
+        )
+        out.update(ops_arrays(ops, p))
+
+    # scattering: random contexts (homogeneous / heterogeneous, with sources)
+    for name, n, n_max, r, homog, n_src in (
+        ("scat_h", 60, 2, 3, True, 1),
+        ("scat_x", 80, 3, 5, False, 2),
+        ("scat_max", 200, 3, 16, True, 1),
+    ):
+        rng = np.random.default_rng(n * 7 + r)
+        m = (n_max + 1) ** 2
+        if homog:
+            weights = np.tile(np.abs(rng.standard_normal(12)), (n, 1)) * 1e22
+        else:
+            weights = np.abs(rng.standard_normal((n, 12))) * 1e22
+        g_diags = np.abs(rng.standard_normal((12, m))) * 1e-28
+        sigma_t = g_diags[:, 0] + np.abs(rng.standard_normal(12)) * 1e-28
+        inv_s = 1.0 / rng.uniform(8.0, 20.0, n)
+        sources = [
+            (np.abs(rng.standard_normal(n)), rng.standard_normal(m)) for _ in range(n_src)
+        ]
+        ctx = dlra.ScatteringContext(weights, inv_s, g_diags, sigma_t, sources)
+        if r == m:
+            uu, ss, vvt = np.linalg.svd(rng.standard_normal((n, m)), full_matrices=False)
+            u0, s0, v0 = uu, np.diag(ss), vvt.T
+        else:
+            u0 = dlra.orthonormal_columns(rng.standard_normal((n, r)))
+            v0 = dlra.orthonormal_columns(rng.standard_normal((m, r)))
+            s0 = np.diag(np.logspace(0, -1, r)) + 0.05 * rng.standard_normal((r, r))
+        st = dlra.LowRankState(u0, s0, v0)
+        dt = 0.3
+        aug = dlra.scattering_step(st, dt, ctx)
+        tr, tail = dlra.truncate(aug, dlra.TruncationPolicy(0.0, rank_min=1, rank_max=2 * r))
+        full = fullrank_scattering_step(st.matrix(), dt, ctx)
+        p = name + "_"
+        out.update(
+            {
+                p + "n_max": np.array(n_max),
+                p + "dt": np.array(dt),
+                p + "weights": weights,
+                p + "inv_s": inv_s,
+                p + "g_diags": g_diags,
+                p + "sigma_t": sigma_t,
+                p + "psi": np.array([s[0] for s in sources]),
+                p + "tm": np.array([s[1] for s in sources]),
+                p + "u0": u0,
+                p + "s0": s0,
+                p + "v0": v0,
+                p + "aug_matrix": aug.matrix(),
+                p + "aug_shape": np.array([aug.u.shape[1], aug.v.shape[1]]),
+                p + "trunc0_matrix": tr.matrix(),
+                p + "trunc0_rank": np.array(tr.rank),
+                p + "full_matrix": full,
+            }
+        )
+
+    # truncation rule cases (dlra.py:90-115)
+    cases = []
+    rng = np.random.default_rng(23)
+    for i in range(12):
+        q = 8
+        sig = np.sort(np.abs(rng.standard_normal(q)) * np.exp(-np.arange(q)))[::-1]
+        theta = 10.0 ** rng.uniform(-4, 0)
+        rmin, rmax = 1 + i % 3, q
+        s = np.diag(sig)
+        st = dlra.LowRankState(np.eye(q), s, np.eye(q))
+        tr, tail = dlra.truncate(st, dlra.TruncationPolicy(theta, rmin, rmax))
+        cases.append([theta, rmin, rmax, tr.rank, tail] + list(sig))
+    out["trunc_cases"] = np.array(cases)
+    save("steps.npz", **out)
+
+
+# --------------------------------------------------------------- traversal
+def make_traverse():
+    rays = []
+    grids = {
+        "a": spatial.Grid3D(4, 4, 10, 0.1, 0.1, 0.1),
+        "b": spatial.Grid3D(5, 5, 5, 0.2, 0.2, 0.2),
+        "c": spatial.Grid3D(20, 20, 70, 0.1, 0.1, 0.1),
+        "d": spatial.Grid3D(7, 9, 11, 0.13, 0.07, 0.21, origin=(-0.3, 0.2, -0.1)),
+        "e": spatial.Grid3D(1, 20, 70, 2.0, 0.1, 0.1),
+    }
+    rng = np.random.default_rng(99)
+    out = {}
+    for gname, g in grids.items():
+        (x0, x1), (y0, y1), (z0, z1) = g.extent()
+        origins, dirs = [], []
+        # axis-aligned, diagonal and random rays, plus beam-like bundles
+        for _ in range(60):
+            o = np.array([rng.uniform(x0 - 0.2, x1 + 0.2), rng.uniform(y0 - 0.2, y1 + 0.2),
+                          z0 - rng.uniform(0.01, 0.5)])
+            d = rng.standard_normal(3)
+            d[2] = abs(d[2]) + 0.1
+            d /= np.linalg.norm(d)
+            origins.append(o)
+            dirs.append(d)
+        for axis in range(3):
+            for sgn in (1.0, -1.0):
+                d = np.zeros(3)
+                d[axis] = sgn
+                for _ in range(6):
+                    o = np.array([rng.uniform(x0, x1), rng.uniform(y0, y1), rng.uniform(z0, z1)])
+                    o[axis] = (x0, y0, z0)[axis] - 0.3 if sgn > 0 else (x1, y1, z1)[axis] + 0.3
+                    origins.append(o)
+                    dirs.append(d.copy())
+        d = np.array([1.0, 1.0, 1.0]) / np.sqrt(3.0)
+        origins.append(np.array([x0, y0, z0]) - 0.1 * d)
+        dirs.append(d)
+        # a stratified pencil beam bundle (the reference's own start points)
+        beam = raytracer.BeamSource((0.0, 0.6, 0.8), 50.0, (0.5 * (x0 + x1), y0, z0), sigma_xy_cm=0.2)
+        e1, e2 = beam.transverse_frame()
+        offsets, _ = raytracer.stratified_ray_offsets(beam.sigma_xy_cm, 7, 3.0)
+        for off in offsets:
+            origins.append(np.asarray(beam.position_cm) + off[0] * e1 + off[1] * e2)
+            dirs.append(np.asarray(beam.direction))
+        cells, t0, t1, offs = [], [], [], [0]
+        for o, d in zip(origins, dirs):
+            path = raytracer.traverse_grid(g, o, d)
+            for c, a, b in path:
+                cells.append(c)
+                t0.append(a)
+                t1.append(b)
+            offs.append(len(cells))
+        p = gname + "_"
+        out.update(
+            {
+                p + "grid": np.array([g.nx, g.ny, g.nz, g.dx, g.dy, g.dz] + list(g.origin)),
+                p + "origins": np.array(origins),
+                p + "dirs": np.array(dirs),
+                p + "cells": np.array(cells, dtype=np.int64),
+                p + "t0": np.array(t0),
+                p + "t1": np.array(t1),
+                p + "offsets": np.array(offs, dtype=np.int64),
+            }
+        )
+    out["grids"] = np.array(list(grids))
+    save("traverse.npz", **out)
+
+
+# --------------------------------------------------------------- end to end
+def smoke_raw(**over):
+    raw = {
+        "name": "smoke",
+        "grid": {"nx": 8, "ny": 8, "nz": 12,
+                 "delta_x_cm": 0.25, "delta_y_cm": 0.25, "delta_z_cm": 0.25},
+        "phantom": {"background_hu": 0.0},
+        "beams": [{"direction": [0, 0, 1], "energy_mev": 20.0, "position_cm": [1.0, 1.0, 0.0]}],
+        "pn_order": 3,
+        "transport": {"cfl_number": 0.2},
+        "energy": {"groups": 64},
+        "rays": {"n_side": 5},
+    }
+    raw.update(over)
+    return raw
+
+
+def config1_raw():
+    import yaml
+
+    with open("/root/reference/pkg/configs/homogeneous_90MeV.yaml") as fh:
+        raw = yaml.safe_load(fh)
+    raw["grid"]["nx"] = 1
+    raw["grid"]["delta_x_cm"] = 2.0
+    raw["transport"].update({"truncation_tolerance": 1e300, "rank_min": 20, "rank_max": 20})
+    raw.pop("output", None)
+    return raw
+
+
+def lockstep_raw():
+    return {
+        "grid": {"nx": 8, "ny": 8, "nz": 8,
+                 "delta_x_cm": 0.25, "delta_y_cm": 0.25, "delta_z_cm": 0.25},
+        "phantom": {"background_hu": 0.0},
+        "beams": [{"direction": [0, 0, 1], "energy_mev": 20.0, "position_cm": [1.0, 1.0, 0.0]}],
+        "pn_order": 3,
+        "transport": {"cfl_number": 0.0003, "truncation_tolerance": 0.0,
+                      "rank_min": 16, "rank_max": 16},
+        "energy": {"e_min_mev": 19.0, "e_max_mev": 21.0, "groups": 64},
+        "rays": {"n_side": 5},
+    }
+
+
+def hetero_raw():
+    raw = smoke_raw(name="hetero")
+    raw["grid"] = {"nx": 8, "ny": 8, "nz": 16,
+                   "delta_x_cm": 0.25, "delta_y_cm": 0.25, "delta_z_cm": 0.25}
+    raw["phantom"] = {
+        "background_hu": 0.0,
+        "boxes": [
+            {"origin_cm": [0, 0, 1.0], "size_cm": [2, 2, 0.75], "hu": 1200.0},
+            {"origin_cm": [1.0, 0, 2.0], "size_cm": [1, 2, 1.0], "hu": -700.0},
+        ],
+    }
+    raw["beams"] = [
+        {"direction": [0, 0, 1], "energy_mev": 25.0, "position_cm": [1.0, 1.0, 0.0]},
+        {"direction": [0, 0.6, 0.8], "energy_mev": 22.0, "position_cm": [1.0, 0.3, 0.0],
+         "weight": 0.5},
+    ]
+    raw["transport"] = {"cfl_number": 0.2, "truncation_tolerance": 1e300,
+                        "rank_min": 6, "rank_max": 6}
+    return raw
+
+
+def fp_raw():
+    raw = smoke_raw(name="fp", model="fokker-planck")
+    raw["physics"] = {"fp_correction_scale": 0.5}
+    raw["transport"] = {"cfl_number": 0.2, "truncation_tolerance": 1e300,
+                        "rank_min": 4, "rank_max": 4}
+    return raw
+
+
+def rank1_raw():
+    raw = smoke_raw(name="rank1")
+    raw["transport"] = {"cfl_number": 0.2, "truncation_tolerance": 1e-6,
+                        "rank_min": 1, "rank_max": 40}
+    return raw
+
+
+def run_e2e(tag, raw, with_contexts=True):
+    t0 = time.perf_counter()
+    config = driver.ProblemConfig.from_dict(raw)
+    problem = driver.assemble_problem(config)
+    fluxes = driver.trace_all_beams(problem)
+    t_ms = [angular.beam_projection(config.pn_order, b.direction) for b in config.beams]
+    bundle = export_problem(problem, fluxes, t_ms)
+    save(f"bundle_{tag}.npz", **bundle)
+
+    res = driver.run_simulation(config, solver="dlra")
+    unc = driver.uncollided_dose(problem, fluxes)
+    edges = driver.pseudo_time_edges(problem)
+    out = {
+        "deposited": res.dose.deposited,
+        "dose": res.dose.dose,
+        "uncollided": unc,
+        "rank_history": np.array([[k, e, r] for k, e, r in res.rank_history]),
+        "edges": edges,
+        "diagnostics": np.array(json.dumps(driver._jsonable(res.diagnostics))),
+        "runtime_s": np.array(time.perf_counter() - t0),
+    }
+    if with_contexts:
+        # per-step contexts at a few steps: pins the host coefficient path
+        steps = sorted({0, 1, len(edges) // 3, len(edges) - 2})
+        out["ctx_steps"] = np.array(steps)
+        for k in steps:
+            sc, cc, s_field = driver.step_contexts(problem, fluxes, t_ms, edges[k], edges[k + 1])
+            out[f"ctx{k}_inv_s"] = sc.inv_s
+            out[f"ctx{k}_g_diags"] = cc.g_diags
+            out[f"ctx{k}_sigma_t"] = cc.sigma_t
+            out[f"ctx{k}_psi"] = np.array([s[0] for s in cc.sources])
+            out[f"ctx{k}_s_field"] = s_field
+    save(f"e2e_{tag}.npz", **out)
+    print(f"  {tag}: {res.diagnostics['n_steps']} steps in {time.perf_counter() - t0:.1f}s")
+
+
+def make_e2e(which):
+    cases = {
+        "smoke": smoke_raw(),
+        "config1": config1_raw(),
+        "lockstep": lockstep_raw(),
+        "hetero": hetero_raw(),
+        "fp": fp_raw(),
+        "rank1": rank1_raw(),
+    }
+    for tag, raw in cases.items():
+        if which and tag not in which:
+            continue
+        run_e2e(tag, raw, with_contexts=(tag != "lockstep"))
+
+
+def make_march():
+    """One Crank-Nicolson march (raytracer.py:285-350) for the tracer tests."""
+    space = raytracer.EnergyDGSpace(1.0, 31.5, 32, 2)
+
+    def const(v):
+        return lambda e: np.full_like(np.asarray(e, dtype=float), v)
+
+    coeff = {0: (lambda e: 2.0 + 0.05 * np.asarray(e, dtype=float), const(0.04), const(0.3)),
+             1: (const(4.0), None, None)}
+    psi0 = raytracer.project_initial_spectrum(space, 30.0, 0.3)
+    segs = [(0, 0.1, 0), (1, 0.07, 1), (2, 0.1, 0), (3, 0.013, 1)]
+    recs, psi = raytracer.march_ray(space, segs, coeff, psi0)
+    ops = {}
+    for key in coeff:
+        mass, g = raytracer.assemble_energy_operators(space, *coeff[key])
+        ops[f"g_{key}"] = g
+    save(
+        "march.npz",
+        mass=space.mass_diagonal(),
+        psi0=psi0,
+        psi_exit=psi,
+        seg_len=np.array([s[1] for s in segs]),
+        seg_key=np.array([s[2] for s in segs]),
+        averages=np.array([r.group_averages for r in recs]),
+        residual=np.array([r.residual_energy for r in recs]),
+        s_min=np.array([float(coeff[k][0](np.array([1.0]))[0]) for k in (0, 1)]),
+        **ops,
+    )
+
+
+if __name__ == "__main__":
+    OUT.mkdir(parents=True, exist_ok=True)
+    what = set(sys.argv[1:])
+    if not what or "angular" in what:
+        make_angular()
+    if not what or "kernels" in what:
+        make_kernels()
+    if not what or "steps" in what:
+        make_steps()
+    if not what or "traverse" in what:
+        make_traverse()
+    if not what or "march" in what:
+        make_march()
+    e2e = {w[4:] for w in what if w.startswith("e2e:")}
+    if not what or "e2e" in what or e2e:
+        make_e2e(e2e)
