@@ -119,6 +119,21 @@ int pnd_traverse(pnd_handle* h, const double* origin3, int n_rays, const double*
                  const double* dirs, int32_t* counts, const int64_t* offsets, int64_t* cells,
                  double* t0, double* t1);
 
+/* ---- measurement and synthetic inputs (bench.py) ------------------------ */
+/* phase timer (CUDA events on the handle stream around every phase of the step) */
+int pnd_timing(pnd_handle* h, int enable);
+int pnd_timing_get(pnd_handle* h, int nphase, double* ms, int* count);
+int pnd_event_record(pnd_handle* h, int slot);
+int pnd_event_elapsed(pnd_handle* h, int slot_a, int slot_b, double* ms);
+/* kernels launched by this process since load */
+int pnd_launch_count(pnd_handle* h, long long* count);
+/* uncollided group table of a +z pencil beam in a laterally uniform phantom:
+ * values[c][g] = lateral[j*nx + i] * depth[k*G + g], formed on the device */
+int pnd_set_flux_separable(pnd_handle* h, int beam, int n_beams, int n_groups,
+                           const double* lateral, const double* depth, const double* t_m);
+/* preset rank-r state: orthonormalised pseudo-random U, V; S = diag(logspace(0, -3, r)) */
+int pnd_state_random(pnd_handle* h, int r, unsigned long long seed);
+
 #ifdef __cplusplus
 }
 #endif

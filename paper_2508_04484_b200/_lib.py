@@ -51,7 +51,17 @@ SIGNATURES = {
     "pnd_orthonormalize": [_P, _P, _I, _I, _P, _P],
     "pnd_svd_small": [_P, _P, _I, _I, _P, _P, _P],
     "pnd_traverse": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
+    "pnd_timing": [_P, _I],
+    "pnd_timing_get": [_P, _I, _P, _P],
+    "pnd_event_record": [_P, _I],
+    "pnd_event_elapsed": [_P, _I, _I, _P],
+    "pnd_launch_count": [_P, _P],
+    "pnd_set_flux_separable": [_P, _I, _I, _I, _P, _P, _P],
+    "pnd_state_random": [_P, _I, ctypes.c_ulonglong],
 }
+
+PHASES = ["kstage", "l_gram", "l_side", "tsqr_n", "tsqr_m", "s_gram", "s_rk4", "svd",
+          "rotate", "scat_k1", "scat_gram", "scat_small", "dose", "defect"]
 
 _lib = None
 

@@ -54,6 +54,73 @@ void traverse(const Geom& g, const double* origin, int n_rays, const double* sta
               const double* dirs, int* counts, const long long* offsets, long long* cells,
               double* t0, double* t1, cudaStream_t st);
 
+static long long g_launches = 0;
+
+void launched() {
+  CK(cudaGetLastError());
+  ++g_launches;
+}
+
+long long launch_count() { return g_launches; }
+
+void phase(Handle& h, int id) {
+  TimerState& t = h.timer;
+  if (!t.on) return;
+  if (t.used == t.pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    t.pool.push_back(e);
+  }
+  CK(cudaEventRecord(t.pool[t.used], h.st));
+  t.ids.push_back(id);
+  ++t.used;
+}
+
+namespace {
+
+__global__ void separable_kernel(const double* lat, const double* depth, int nxy, int n, int G,
+                                 int ld, double* out) {
+  const long long total = (long long)G * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i / n), c = (int)(i - (long long)g * n);
+    const int k = c / nxy, ij = c - k * nxy;
+    out[(size_t)g * ld + c] = lat[ij] * depth[(size_t)k * G + g];
+  }
+}
+
+__device__ __forceinline__ double hash_normalish(unsigned long long x) {
+  // splitmix64 -> two uniforms -> approximately normal (sum of 4 uniforms)
+  double s = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    x += 0x9E3779B97F4A7C15ULL;
+    unsigned long long z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    s += (double)(z >> 11) * (1.0 / 9007199254740992.0);
+  }
+  return (s - 2.0) * 1.7320508075688772;
+}
+
+__global__ void random_fill(double* a, int rows, int cols, int ld, unsigned long long seed) {
+  const long long total = (long long)rows * cols;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / rows), r = (int)(i - (long long)j * rows);
+    a[(size_t)j * ld + r] = hash_normalish(seed * 0x100000001B3ULL + (unsigned long long)i);
+  }
+}
+
+__global__ void logdiag_kernel(double* S, int r) {
+  for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
+    const int a = i / r, b = i % r;
+    S[i] = a == b ? pow(10.0, r > 1 ? -3.0 * a / (r - 1) : 0.0) : 0.0;
+  }
+}
+
+}  // namespace
+
 }  // namespace pnd
 
 struct pnd_handle {
@@ -566,6 +633,110 @@ int pnd_traverse(pnd_handle* hh, const double* origin3, int n_rays, const double
       cudaFree(CE);
     }
     ds.free_(); dd.free_(); dt0.free_(); dt1.free_(); dc.free_();
+  });
+}
+
+int pnd_timing(pnd_handle* hh, int enable) {
+  return guard(hh, [&](Handle& h) {
+    CK(cudaStreamSynchronize(h.st));
+    h.timer.on = enable != 0;
+    h.timer.used = 0;
+    h.timer.ids.clear();
+  });
+}
+
+int pnd_timing_get(pnd_handle* hh, int nphase, double* ms, int* count) {
+  return guard(hh, [&](Handle& h) {
+    CK(cudaStreamSynchronize(h.st));
+    for (int i = 0; i < nphase; ++i) {
+      ms[i] = 0.0;
+      count[i] = 0;
+    }
+    pnd::TimerState& t = h.timer;
+    for (size_t i = 0; i + 1 < t.used; ++i) {
+      const int id = t.ids[i];
+      if (id < 0 || id >= nphase) continue;
+      float e = 0.f;
+      CK(cudaEventElapsedTime(&e, t.pool[i], t.pool[i + 1]));
+      ms[id] += e;
+      count[id] += 1;
+    }
+    t.used = 0;
+    t.ids.clear();
+  });
+}
+
+int pnd_event_record(pnd_handle* hh, int slot) {
+  return guard(hh, [&](Handle& h) {
+    if (slot < 0 || slot >= 8) pnd::fail(PND_ECONFIG, "event slot out of range");
+    if (!h.timer.ev[slot]) CK(cudaEventCreate(&h.timer.ev[slot]));
+    CK(cudaEventRecord(h.timer.ev[slot], h.st));
+  });
+}
+
+int pnd_event_elapsed(pnd_handle* hh, int a, int b, double* ms) {
+  return guard(hh, [&](Handle& h) {
+    CK(cudaEventSynchronize(h.timer.ev[b]));
+    float e = 0.f;
+    CK(cudaEventElapsedTime(&e, h.timer.ev[a], h.timer.ev[b]));
+    *ms = e;
+  });
+}
+
+int pnd_launch_count(pnd_handle* hh, long long* count) {
+  return guard(hh, [&](Handle&) { *count = pnd::launch_count(); });
+}
+
+int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
+                           const double* lateral, const double* depth, const double* t_m) {
+  return guard(hh, [&](Handle& h) {
+    if (n_beams < 1 || n_beams > 4) pnd::fail(PND_ECONFIG, "1..4 beams supported");
+    if (beam == 0) {
+      h.n_groups = n_groups;
+      h.n_beams = n_beams;
+      h.flux.get((size_t)n_beams * n_groups * h.g.ld);
+      h.psi.get((size_t)n_beams * h.g.ld);
+      h.psi_lo.get((size_t)n_beams * h.g.ld);
+      h.tm.get((size_t)n_beams * h.m);
+    }
+    const int nxy = h.g.nx * h.g.ny;
+    pnd::DBuf dl, dd;
+    double* L = dl.get(nxy);
+    double* D = dd.get((size_t)h.g.nz * n_groups);
+    up(L, lateral, nxy, h.st);
+    up(D, depth, (size_t)h.g.nz * n_groups, h.st);
+    pnd::separable_kernel<<<148 * 8, 256, 0, h.st>>>(
+        L, D, nxy, h.g.n, n_groups, h.g.ld, h.flux.p + (size_t)beam * n_groups * h.g.ld);
+    pnd::launched();
+    up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    dl.free_();
+    dd.free_();
+  });
+}
+
+int pnd_state_random(pnd_handle* hh, int r, unsigned long long seed) {
+  return guard(hh, [&](Handle& h) {
+    if (r < 1 || r > 32) pnd::fail(PND_ECONFIG, "random state rank must be 1..32");
+    const int ld = h.g.ld, m = h.m;
+    double* A = h.A.get((size_t)ld * r);
+    pnd::fill_zero(A, (size_t)ld * r, h.st);
+    pnd::random_fill<<<148 * 8, 256, 0, h.st>>>(A, h.g.n, r, ld, seed);
+    pnd::launched();
+    double* U = h.U.get((size_t)ld * r);
+    double* R = h.sm[45].get((size_t)r * r);
+    pnd::tsqr(A, h.g.n, r, ld, U, ld, R, h.tq_n, h.st);
+    double* B = h.sm[44].get((size_t)m * r);
+    pnd::random_fill<<<64, 256, 0, h.st>>>(B, m, r, m, seed + 7);
+    pnd::launched();
+    double* Vc = h.sm[43].get((size_t)m * r);
+    pnd::tsqr(B, m, r, m, Vc, m, R, h.tq_m, h.st);
+    pnd::transpose_out(Vc, m, m, r, h.V.get((size_t)m * r), h.st);
+    double* S = h.S.get((size_t)r * r);
+    pnd::logdiag_kernel<<<1, 256, 0, h.st>>>(S, r);
+    pnd::launched();
+    CK(cudaStreamSynchronize(h.st));
+    h.ru = h.rv = r;
   });
 }
 

@@ -521,7 +521,7 @@ void gemm(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB, dou
   if (M <= 0 || N <= 0 || batch <= 0) return;
   dim3 grid((N + 15) / 16, (M + 15) / 16, batch), block(16, 16);
   gemm_kernel<<<grid, block, 0, st>>>(M, N, K, alpha, A, sA, B, sB, beta, C, sC);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void axpby(int count, double a, const double* x, double b, double* y, cudaStream_t st) {
@@ -529,7 +529,7 @@ void axpby(int count, double a, const double* x, double b, double* y, cudaStream
   int blocks = (count + 255) / 256;
   if (blocks > 1024) blocks = 1024;
   axpby_kernel<<<blocks, 256, 0, st>>>(count, a, x, b, y);
-  CK(cudaGetLastError());
+  launched();
 }
 
 int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfac, TsqrWork& w,
@@ -582,19 +582,19 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
         const size_t sm = ((size_t)p.br * (cols + 1) + 32 + cols) * sizeof(double);
         set_smem((const void*)hh_qr_kernel, sm);
         hh_qr_kernel<<<nreg, 128, sm, st>>>(mat, ld, p, 0, L.tau, Rn, ldn);
-        CK(cudaGetLastError());
+        launched();
       }
       {
         const size_t sm = ((size_t)p.count(tail_b) * (cols + 1) + 32 + cols) * sizeof(double);
         set_smem((const void*)hh_qr_kernel, sm);
         hh_qr_kernel<<<1, 128, sm, st>>>(mat, ld, p, tail_b, L.tau, Rn, ldn);
-        CK(cudaGetLastError());
+        launched();
       }
       lv.push_back(L);
       if (p.nblk == 1) {
         // root: its R block (kc x cols) is the triangular factor
         copy_rfac_kernel<<<1, 256, 0, st>>>(Rn, ldn, p.rows < cols ? p.rows : cols, cols, rfac);
-        CK(cudaGetLastError());
+        launched();
         break;
       }
       lv.back().qexp = qbuf + qoff;  // explicit Q of the NEXT level is stored per level below
@@ -625,7 +625,7 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
       const size_t sm = ((size_t)p.br * (cols + 1 + kcl + 1) + kcl) * sizeof(double);
       set_smem((const void*)hh_applyq_kernel, sm);
       hh_applyq_kernel<<<nreg, 128, sm, st>>>(L.mat, L.ld, p, 0, L.tau, C, ldc, kcl, out, ldo);
-      CK(cudaGetLastError());
+      launched();
     }
     {
       const size_t sm =
@@ -633,7 +633,7 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
       set_smem((const void*)hh_applyq_kernel, sm);
       hh_applyq_kernel<<<1, 128, sm, st>>>(L.mat, L.ld, p, p.nblk - 1, L.tau, C, ldc, kcl, out,
                                            ldo);
-      CK(cudaGetLastError());
+      launched();
     }
     C = out;
     ldc = ldo;
@@ -650,14 +650,14 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
       ((size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N + N2) * sizeof(double) + N * sizeof(int);
   set_smem((const void*)svd_kernel, sm);
   svd_kernel<<<1, 256, sm, st>>>(s, p, q, P, sig, Qt);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void tail_rule(const double* sig, int k, double theta, int rmin, int rmax, int* info,
                double* tail, cudaStream_t st) {
   if (k > 128) fail(PND_ECONFIG, "tail rule supports at most 128 singular values");
   tail_kernel<<<1, 32, 0, st>>>(sig, k, theta, rmin, rmax, info, tail);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void scat_solves(const double* B, const double* coeffs, const double* lcols, int r, int m,
@@ -665,7 +665,7 @@ void scat_solves(const double* B, const double* coeffs, const double* lcols, int
   const size_t sm = ((size_t)r * (r + 1) + r) * sizeof(double);
   set_smem((const void*)scat_solve_kernel, sm);
   scat_solve_kernel<<<m, 64, sm, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt, double*,
@@ -673,7 +673,7 @@ void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, do
   const size_t sm = 4 * (size_t)p * q * sizeof(double);
   set_smem((const void*)s_rk4_kernel, sm);
   s_rk4_kernel<<<1, 1024, sm, st>>>(S, p, q, G, F, ns, dt);
-  CK(cudaGetLastError());
+  launched();
 }
 
 }  // namespace pnd

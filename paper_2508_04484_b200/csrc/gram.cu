@@ -190,9 +190,9 @@ void launch(const GramArgs& a, DBuf& partial, cudaStream_t st) {
   const size_t count = (size_t)a.nphase * a.na * a.nb;
   double* part = partial.get(count * grid);
   gram_kernel<T, NPH, NW><<<grid, NW * 32, smem, st>>>(a, part);
-  CK(cudaGetLastError());
+  launched();
   reduce_partials<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, a.out);
-  CK(cudaGetLastError());
+  launched();
 }
 
 template <int NPH>

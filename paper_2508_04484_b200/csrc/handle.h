@@ -5,6 +5,22 @@
 
 namespace pnd {
 
+// phase timer: CUDA events on the handle's stream around each phase of the
+// step (pnd_timing / pnd_timing_get), used by bench.py for per-kernel
+// durations and roofline fractions
+enum Phase {
+  PH_KSTAGE, PH_LGRAM, PH_LSIDE, PH_TSQR_N, PH_TSQR_M, PH_SGRAM, PH_SRK4, PH_SVD, PH_ROTATE,
+  PH_SCATK1, PH_SCATGRAM, PH_SCATSMALL, PH_DOSE, PH_DEFECT, PH_COUNT
+};
+
+struct TimerState {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<int> ids;  // mark i uses pool[i]
+  cudaEvent_t ev[8] = {};
+};
+
 struct Handle {
   int device = 0;
   cudaStream_t st = nullptr;
@@ -44,7 +60,12 @@ struct Handle {
   DBuf dep, prev;             // dose tally
   DBuf host_stage;            // unused placeholder
   double* pinned = nullptr;   // small pinned readback buffer
+  TimerState timer;
 };
+
+// phase mark: when timing is on, records an event on the handle's stream;
+// the time until the next mark is attributed to `id` (id < 0 closes)
+void phase(Handle& h, int id);
 
 void streaming_step(Handle& h, double dt);
 void scattering_step(Handle& h, double dt);

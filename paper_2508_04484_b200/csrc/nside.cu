@@ -120,7 +120,7 @@ void kstage_launch(const KStageArgs& a, cudaStream_t st) {
   const int cap = sms * 8;
   if (blocks > cap) blocks = cap;
   kstage_kernel<NB><<<blocks, 128, smem, st>>>(a);
-  CK(cudaGetLastError());
+  launched();
 }
 
 template <int NB>
@@ -300,7 +300,7 @@ static void rotate_launch(const Geom& g, const double* X, int ldx, int a, const 
   CK(cudaFuncSetAttribute(rotate_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   rotate_kernel<NB><<<grid_for(g.n, 128), 128, smem, st>>>(g, X, ldx, a, P, ldp, b, out, ldo);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void rotate_ld(const Geom& g, const double* X, int ldx, int a, const double* P, int ldp, int b,
@@ -331,7 +331,7 @@ static void scat_k1_launch(const Geom& g, const double* U0, int ldu, int ra, con
   scat_k1_kernel<NB><<<grid_for(g.n, 128), 128, smem, st>>>(g, U0, ldu, ra, S0, r, dt, inv_s,
                                                             cls, atomic, psi, ldpsi, n_beams,
                                                             rows, A, lda);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void scat_k1(const Geom& g, const double* U0, int ldu, int ra, const double* S0, int r, double dt,
@@ -373,33 +373,33 @@ void dose_accumulate(const Geom& g, const double* U, int ldu, const double* coef
                      int n_beams, double* deposited, double* prev, cudaStream_t st) {
   dose_kernel<<<grid_for(g.n, 256), 256, 0, st>>>(g, U, ldu, coef, r, half_dt, s_field, psi,
                                                    ldpsi, n_beams, deposited, prev);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void class_gather_inv(const int* cls, const double* class_val, int n, double* out_inv,
                       double* out_val, cudaStream_t st) {
   class_gather_kernel<<<grid_for(n, 256), 256, 0, st>>>(cls, class_val, n, out_inv, out_val);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, double w1,
               double* out, cudaStream_t st) {
   lerp_kernel<<<grid_for(n, 256), 256, 0, st>>>(values, ldv, n, j0, w0, j1, w1, out);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void transpose_in(const double* src, int n, int c, double* dst, int ldd, cudaStream_t st) {
   if (n <= 0 || c <= 0) return;
   dim3 grid((c + 31) / 32, (n + 31) / 32), block(32, 8);
   tin_kernel<<<grid, block, 0, st>>>(src, n, c, dst, ldd);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void transpose_out(const double* src, int lds, int n, int c, double* dst, cudaStream_t st) {
   if (n <= 0 || c <= 0) return;
   dim3 grid((c + 31) / 32, (n + 31) / 32), block(32, 8);
   tout_kernel<<<grid, block, 0, st>>>(src, lds, n, c, dst);
-  CK(cudaGetLastError());
+  launched();
 }
 
 void fill_zero(double* p, size_t count, cudaStream_t st) {
@@ -407,7 +407,7 @@ void fill_zero(double* p, size_t count, cudaStream_t st) {
   size_t blocks = (count + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   zero_kernel<<<(int)blocks, 256, 0, st>>>(p, count);
-  CK(cudaGetLastError());
+  launched();
 }
 
 }  // namespace pnd

@@ -33,6 +33,9 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 #define CK(x) ::pnd::check_cuda((x), #x)
+// after every kernel launch: surface launch errors, count the launch
+void launched();
+long long launch_count();
 
 // ------------------------------------------------------------ geometry
 struct Geom {

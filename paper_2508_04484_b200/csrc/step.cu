@@ -58,6 +58,7 @@ void streaming_step(Handle& h, double dt) {
   cudaStream_t st = h.st;
 
   // --- K phase: K1 = RK4 of K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
+  phase(h, PH_LSIDE);
   double* F = slot(h, S_FV, (size_t)ns * b * b);
   moment_factors(h, h.V.p, b, F);
   const int xmax = a > b ? a : b;
@@ -98,11 +99,14 @@ void streaming_step(Handle& h, double dt) {
       }
     }
     ka.ldo = ld;
+    phase(h, PH_KSTAGE);
     kstage(ka, st);
+    phase(h, PH_LSIDE);
   }
 
   // --- L phase: L' = -sum_s A_s L Q_s, Q_s = (D_s S^-1 U0)^T U0, L0 = V0 S0^T
   double* QT = slot(h, S_QT, (size_t)ns * a * a);
+  phase(h, PH_LGRAM);
   {
     GramArgs ga{};
     ga.geo = g;
@@ -114,6 +118,7 @@ void streaming_step(Handle& h, double dt) {
     ga.out = QT;  // QT_s = U0^T D_s U0 = Q_s^T
     gram(ga, h.part, st);
   }
+  phase(h, PH_LSIDE);
   double* L0 = slot(h, S_L0, (size_t)m * a);
   double* LW = slot(h, S_LW, (size_t)m * a);
   double* Z = slot(h, S_ZST, (size_t)ns * m * a);
@@ -136,10 +141,13 @@ void streaming_step(Handle& h, double dt) {
   // --- augmentation: U^ = orth([K1, U0]), V^ = orth([L1, V0])  (dlra.py:220-221)
   double* Uh = h.Uhat.get((size_t)ld * cols);
   double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  phase(h, PH_TSQR_N);
   const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
   double* Vhc = slot(h, S_VHC, (size_t)m * cols);
   double* Rv = slot(h, S_RV, (size_t)cols * cols);
+  phase(h, PH_TSQR_M);
   const int rv = tsqr(BV, m, cols, m, Vhc, m, Rv, h.tq_m, st);
+  phase(h, PH_SRK4);
 
   // --- S^0 = (U^T U0) S0 (V0^T V^) = Ru[:, b:] S0 Rv[:, a:]^T
   double* T1 = slot(h, S_ST1, (size_t)ru * b);
@@ -149,6 +157,7 @@ void streaming_step(Handle& h, double dt) {
 
   // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
   double* G = slot(h, S_G, (size_t)ns * ru * ru);
+  phase(h, PH_SGRAM);
   {
     GramArgs ga{};
     ga.geo = g;
@@ -160,6 +169,7 @@ void streaming_step(Handle& h, double dt) {
     ga.out = G;
     gram(ga, h.part, st);
   }
+  phase(h, PH_SRK4);
   double* Vhr = slot(h, S_VHR, (size_t)m * rv);
   transpose_out(Vhc, m, m, rv, Vhr, st);
   double* Fh = slot(h, S_FH, (size_t)ns * rv * rv);
@@ -174,6 +184,7 @@ void streaming_step(Handle& h, double dt) {
   CK(cudaMemcpyAsync(Vnew, Vhr, sizeof(double) * m * rv, cudaMemcpyDeviceToDevice, st));
   h.ru = ru;
   h.rv = rv;
+  phase(h, -1);
 }
 
 namespace {
@@ -208,23 +219,26 @@ void scattering_step(Handle& h, double dt) {
   if (a > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
 
   // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
+  phase(h, PH_SCATSMALL);
   double* gt = slot(h, S_GT, (size_t)(B > 0 ? B : 1) * 12 * m);
   double* rows = slot(h, S_ROWS, (size_t)(B > 0 ? B : 1) * 12 * b);
   if (B > 0) {
     gt_kernel<<<64, 256, 0, st>>>(h.gdiag.p, h.tm.p, m, B, gt);
-    CK(cudaGetLastError());
+    launched();
     gemm(12 * B, b, m, 1.0, rowm(gt, m), 0, rowm(h.V.p, b), 0, 0.0, rowm(rows, b), 0, 1, st);
   }
 
   // substep 2 input: A = [K1 | U0], K1 = U0 S0 + dt src_rows(V0)  (dlra.py:303)
   const int cols = b + a;
   double* A = h.A.get((size_t)ld * cols);
+  phase(h, PH_SCATK1);
   scat_k1(g, h.U.p, ld, a, h.S.p, b, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p,
           B > 0 ? h.psi.p : nullptr, ld, B, rows, A, ld, st);
 
   // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
   const int nw = h.n_cls <= 12 ? h.n_cls : 12;
   double* H = slot(h, S_H, (size_t)nw * a * a);
+  phase(h, PH_SCATGRAM);
   {
     GramArgs ga{};
     ga.geo = g;
@@ -240,6 +254,7 @@ void scattering_step(Handle& h, double dt) {
     ga.out = H;
     gram(ga, h.part, st);
   }
+  phase(h, PH_SCATSMALL);
   double* Bi = slot(h, S_BI, (size_t)12 * a * a);
   if (h.n_cls <= 12) {
     // B_i = sum_k N_{k,i} H_k
@@ -250,6 +265,7 @@ void scattering_step(Handle& h, double dt) {
   }
   // source projections U0^T (N psi_b / S)  (a x 12B)
   double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
+  phase(h, PH_SCATGRAM);
   if (B > 0) {
     GramArgs ga{};
     ga.geo = g;
@@ -264,14 +280,16 @@ void scattering_step(Handle& h, double dt) {
     ga.out = left;
     gram(ga, h.part, st);
   }
+  phase(h, PH_SCATSMALL);
   double* coeffs = slot(h, S_COEF, (size_t)12 * m);
   coeff_kernel<<<16, 256, 0, st>>>(h.gdiag.p, h.sigt.p, m, coeffs);
-  CK(cudaGetLastError());
+  launched();
   double* lcols = slot(h, S_LCOL, (size_t)a * m);
   gemm(a, m, b, 1.0, rowm(h.S.p, b), 0, tr(rowm(h.V.p, b)), 0, 0.0, rowm(lcols, m), 0, 1, st);
   double* lnew = slot(h, S_LNEW, (size_t)a * m);
   int* flag = h.iflag.get(4);
   init_int<<<1, 1, 0, st>>>(flag, 1 << 30);
+  launched();
   scat_solves(Bi, coeffs, lcols, a, m, dt, lnew, flag, st);
   int singular = 0;
   CK(cudaMemcpyAsync(&singular, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -282,6 +300,7 @@ void scattering_step(Handle& h, double dt) {
                              "; the step size is too large for the scattering stiffness");
   }
   // V~, R~ = qr(L1^T): lnew row-major (a x m) is L1^T column-major (m x a)
+  phase(h, PH_TSQR_M);
   const int kt = m < a ? m : a;
   double* Vtc = slot(h, S_VTC, (size_t)m * kt);
   double* Rt = slot(h, S_RT, (size_t)kt * a);
@@ -290,7 +309,9 @@ void scattering_step(Handle& h, double dt) {
   // substep 2: U^ = orth([K1, U0])
   double* Uh = h.Uhat.get((size_t)ld * cols);
   double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  phase(h, PH_TSQR_N);
   const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
+  phase(h, PH_SCATSMALL);
 
   // substep 3: l3 = V~ S~^T + dt proj^T, V^ = orth([l3, V~])  (dlra.py:306-312)
   const int vcols = a + kt;
@@ -308,7 +329,9 @@ void scattering_step(Handle& h, double dt) {
                      st));
   double* Vhc = slot(h, S_VHC, (size_t)m * vcols);
   double* Rv = slot(h, S_RV, (size_t)vcols * vcols);
+  phase(h, PH_TSQR_M);
   const int rv = tsqr(BV, m, vcols, m, Vhc, m, Rv, h.tq_m, st);
+  phase(h, PH_SCATSMALL);
 
   // substep 4: S1 = (U^T U0) S~ (V~^T V^) + dt U^T (N psi / S)(g o T_M) V^
   double* T1 = slot(h, S_ST1, (size_t)ru * kt);
@@ -317,6 +340,7 @@ void scattering_step(Handle& h, double dt) {
   gemm(ru, rv, kt, 1.0, rowm(T1, kt), 0, Mat{Rv + a, 1, vcols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
   if (B > 0) {
     double* proj2 = slot(h, S_PROJ2, (size_t)ru * 12 * B);
+    phase(h, PH_SCATGRAM);
     GramArgs ga{};
     ga.geo = g;
     ga.X = Uh; ga.ldx = ld; ga.na = ru;
@@ -329,6 +353,7 @@ void scattering_step(Handle& h, double dt) {
     ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
     ga.out = proj2;
     gram(ga, h.part, st);
+    phase(h, PH_SCATSMALL);
     double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
     gemm(12 * B, rv, m, 1.0, rowm(gt, m), 0, colm(Vhc, m), 0, 0.0, rowm(gtv, rv), 0, 1, st);
     for (int beam = 0; beam < B; ++beam) {
@@ -344,6 +369,7 @@ void scattering_step(Handle& h, double dt) {
   transpose_out(Vhc, m, m, rv, Vnew, st);
   h.ru = ru;
   h.rv = rv;
+  phase(h, -1);
 }
 
 namespace {
@@ -371,6 +397,7 @@ __global__ void defect_kernel(const double* G, int r, double* out) {
 void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int* rank_out) {
   const int p = h.ru, q = h.rv, k = p < q ? p : q;
   cudaStream_t st = h.st;
+  phase(h, PH_SVD);
   double* P = slot(h, S_P, (size_t)p * k);
   double* sig = slot(h, S_SIG, (size_t)k);
   double* Qt = slot(h, S_QTM, (size_t)k * q);
@@ -389,8 +416,10 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   }
   const Geom& g = h.g;
   const int m = h.m;
+  phase(h, PH_ROTATE);
   double* Unew = h.Uhat.get((size_t)g.ld * (r1 > 0 ? r1 : 1));
   rotate_ld(g, h.U.p, g.ld, p, P, k, r1, Unew, g.ld, st);
+  phase(h, PH_SVD);
   double* Vn = slot(h, S_VNEW, (size_t)m * r1);
   gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);
   std::swap(h.U, h.Uhat);
@@ -398,8 +427,9 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   CK(cudaMemcpyAsync(V, Vn, sizeof(double) * m * r1, cudaMemcpyDeviceToDevice, st));
   double* S = h.S.get((size_t)r1 * r1);
   diag_kernel<<<1, 256, 0, st>>>(sig, r1, S);
-  CK(cudaGetLastError());
+  launched();
   h.ru = h.rv = r1;
+  phase(h, -1);
   if (tail_out) *tail_out = tail;
   if (rank_out) *rank_out = r1;
 }
@@ -407,6 +437,7 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
 void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
   const Geom& g = h.g;
   cudaStream_t st = h.st;
+  phase(h, PH_DOSE);
   double* coef = slot(h, S_COEFD, (size_t)h.ru);
   // integrand = sqrt(4 pi) U (S V[0, :]) (+ S psi_u(E_lo))  (driver.py:606, 613-621)
   gemm(h.ru, 1, h.rv, 1.0, rowm(h.S.p, h.rv), 0, Mat{h.V.p, 1, 0}, 0, 0.0, Mat{coef, 1, 0}, 0, 1,
@@ -416,11 +447,13 @@ void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
   pnd::dose_accumulate(g, h.U.p, g.ld, coef, h.ru, 0.5 * dt, h.s_field.p,
                        tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr, g.ld, h.n_beams, dep,
                        prev, st);
+  phase(h, -1);
 }
 
 double orth_defect(Handle& h) {
   const Geom& g = h.g;
   cudaStream_t st = h.st;
+  phase(h, PH_DEFECT);
   double* G = slot(h, S_DEF, (size_t)h.ru * h.ru + (size_t)h.rv * h.rv + 2);
   double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
   GramArgs ga{};
@@ -437,8 +470,10 @@ double orth_defect(Handle& h) {
        rowm(GV, h.rv), 0, 1, st);
   fill_zero(out, 1, st);
   defect_kernel<<<1, 256, 0, st>>>(G, h.ru, out);
+  launched();
   defect_kernel<<<1, 256, 0, st>>>(GV, h.rv, out);
-  CK(cudaGetLastError());
+  launched();
+  phase(h, -1);
   CK(cudaMemcpyAsync(h.pinned + 2, out, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return h.pinned[2];

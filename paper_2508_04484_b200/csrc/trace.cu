@@ -128,7 +128,7 @@ void traverse(const Geom& g, const double* origin, int n_rays, const double* sta
     traverse_kernel<false><<<blocks, threads, 0, st>>>(tg, n_rays, starts, dirs, counts, offsets,
                                                        cells, t0, t1);
   }
-  CK(cudaGetLastError());
+  launched();
 }
 
 }  // namespace pnd

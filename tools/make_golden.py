@@ -474,6 +474,32 @@ def make_march():
     )
 
 
+def make_bench_physics():
+    """Physics tables for the synthetic benchmark phantoms (water / bone / lung
+    classes, stopping tables, moment tables up to degree 21 over 1..105 MeV)."""
+    from pndose.driver import MomentTables
+    from pndose.physics import MaterialField, default_schneider_table, default_stopping_library
+
+    hu = np.array([0.0, 1200.0, -700.0])
+    density, weights = default_schneider_table().convert(hu)
+    mat = MaterialField(density=density, weights=weights)
+    lib = default_stopping_library()
+    symbols = list(lib.tables)
+    mt = MomentTables(1.0, 105.0, 21, n_points=48, n_nodes=256, exponent=1.0)
+    save(
+        "bench_physics.npz",
+        hu=hu,
+        class_density=np.asarray(mat.density),
+        class_weights=np.asarray(mat.weights),
+        class_atomic=np.asarray(mat.atomic_densities),
+        stop_e=np.stack([lib.tables[s].energies for s in symbols]),
+        stop_s=np.stack([lib.tables[s].values for s in symbols]),
+        mom_e=mt.energies,
+        mom_g=mt.g,
+        mom_xi1=mt.xi1,
+    )
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     what = set(sys.argv[1:])
@@ -487,6 +513,8 @@ if __name__ == "__main__":
         make_traverse()
     if not what or "march" in what:
         make_march()
+    if not what or "bench" in what:
+        make_bench_physics()
     e2e = {w[4:] for w in what if w.startswith("e2e:")}
     if not what or "e2e" in what or e2e:
         make_e2e(e2e)
