@@ -195,6 +195,10 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     g.h[0] = dx;
     g.h[1] = dy;
     g.h[2] = dz;
+    for (int a = 0; a < 3; ++a) {
+      g.ih[a] = 1.0 / g.h[a];
+      g.i2h[a] = 1.0 / (2.0 * g.h[a]);
+    }
     g.na = 0;
     for (int a = 0; a < 3; ++a)
       if (dims[a] > 1) g.axis[g.na++] = a;

@@ -83,18 +83,18 @@ __global__ void __launch_bounds__(128) kstage_kernel(KStageArgs a) {
       for (int ai = 0; ai < 3; ++ai) {
         if (ai < g.na) {
           const int axis = g.axis[ai];
-          const double h = g.h[axis];
+          const double ih = g.ih[axis], i2h = g.i2h[axis];
           double f[5];
 #pragma unroll
           for (int d = 0; d < 5; ++d) f[d] = ok[ai][d] ? col[off[ai][d]] * is[ai][d] : 0.0;
           // D^+ (minus-biased) and D^- (plus-biased), spatial.py:81-118
           double tp, tm;
-          if (ok[ai][0]) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) / (2.0 * h);
-          else if (ok[ai][1]) tp = (f[2] - f[1]) / h;
-          else tp = f[2] / h;
-          if (ok[ai][4]) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) / (2.0 * h);
-          else if (ok[ai][3]) tm = (f[3] - f[2]) / h;
-          else tm = -f[2] / h;
+          if (ok[ai][0]) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) * i2h;
+          else if (ok[ai][1]) tp = (f[2] - f[1]) * ih;
+          else tp = f[2] * ih;
+          if (ok[ai][4]) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) * i2h;
+          else if (ok[ai][3]) tm = (f[3] - f[2]) * ih;
+          else tm = -f[2] * ih;
           const double* mp = sM + ((2 * ai) * xc + j) * NB;
           const double* mm = sM + ((2 * ai + 1) * xc + j) * NB;
 #pragma unroll

@@ -43,6 +43,8 @@ struct Geom {
   int n;          // cells
   int ld;         // padded leading dimension of n-side matrices
   double h[3];
+  double ih[3];   // 1/h   (the stencil coefficients, no FP64 division in kernels)
+  double i2h[3];  // 1/(2h)
   int na;         // number of active axes
   int axis[3];    // active axis ids in x, y, z order
   int ns;         // number of stencils = 2 * na (order: axis-major, + then -)
@@ -69,7 +71,7 @@ struct IBuf {
 
 // ------------------------------------------------------------ kernels API
 // Gram engine (gram.cu): out[g][a][b] = sum_c X[c][a] * T_g[c][b]
-enum GramGen { GEN_STENCIL = 0, GEN_WEIGHT = 1, GEN_SOURCE = 2, GEN_PLAIN = 3 };
+enum GramGen { GEN_STENCIL = 0, GEN_WEIGHT = 1, GEN_SOURCE = 2, GEN_PLAIN = 3, GEN_LINCOMB = 4 };
 
 struct GramArgs {
   Geom geo;
@@ -82,7 +84,12 @@ struct GramArgs {
   const int* cls; const double* wtab; int n_cls; int wmode;  // see gram.cu
   // source generator: T[c][b] = N[cls][b%12] * inv_s[c] * psi[b/12][c]
   const double* psi; int ldpsi; int n_beams;
-  double* out;                               // nphase x na x nb (row-major)
+  // lincomb generator: T = Y TA - X TB (TA: ny x nb, TB: na x nb, row-major),
+  // written to Yout (ld = ldo) when non-null; Y has ny columns
+  int ny; const double* TA; const double* TB; double* Yout; int ldo;
+  int self_phase;                            // phase whose A operand is T (-1: none)
+  double* out;                               // per phase rows x nb (row-major), phases
+                                             // concatenated; rows = nb for self_phase
 };
 void gram(GramArgs a, DBuf& partial, cudaStream_t st);
 

@@ -1,14 +1,26 @@
 // Orchestration of one pseudo-time (energy) step on the device.
 //
-// Shapes follow the reference: U0 (n x a), S0 (a x b), V0 (m x b); R-sized
-// augmented factors after each substep. The n-side work (O(n r^2) flops,
-// O(n r) bytes) runs in nside.cu / gram.cu / dense.cu TSQR kernels; the
-// m-side and R x R work is replicated small kernels. Horner's form is used for
-// every RK4 of a linear autonomous right-hand side (K, L and S phases): for
-// y' = L y, classic RK4 (dlra.py:118-123) equals
+// Shapes follow the reference: U0 (n x a), S0 (a x b), V0 (m x b).
+//
+// Horner RK4. Every RK4 here integrates a linear autonomous right-hand side
+// (K, L and S phases, dlra.py:118-123), for which classic RK4 equals
 //   y1 = y0 + h L (y0 + h/2 L (y0 + h/3 L (y0 + h/4 L y0)))
-// exactly in exact arithmetic, which takes 4 passes over n-side data instead
-// of the classic scheme's 4 stage evaluations plus 3 combination passes.
+// exactly in exact arithmetic: 4 passes over n-side data instead of the
+// classic scheme's 4 evaluations plus 3 combinations.
+//
+// Augmentation. The reference orthonormalises [K1, U0] with Householder QR
+// (dlra.py:26-43, 220, 304). Since U0 is already orthonormal and
+// K1 = U0 S0 + dK, span[K1, U0] = span[U0, dK]; the device builds
+// U^ = [U0 | Q] with Q an orthonormal basis of (I - U0 U0^T) dK, where dK is
+// the increment itself (the last Horner stage without its base, or the
+// scattering source term), so no cancellation against U0 S0 occurs. Q comes
+// from Gram passes only (block classical Gram-Schmidt with reorthogonalisation
+// + SVQB, Stathopoulos & Wu 2002): directions of the projected increment below
+// 1e-7 of its largest singular value (numerical noise for a one-pass Gram
+// method) are deflated rather than normalised into noise directions. Then
+// U^T U0 = [I; 0] exactly, and the truncation handles the exact-zero case
+// (S^ == 0) with the reference's canonical basis.
+// The moment side (m x 2r, small) keeps Householder TSQR.
 #include <cmath>
 #include <cstring>
 
@@ -22,8 +34,9 @@ enum Slot {
   S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RU, S_RV, S_ST1, S_SHAT, S_G,
   S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
   S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_UNEW, S_VNEW, S_SNEW, S_M2,
-  S_COUNT
+  S_C1, S_OG, S_OTA, S_OTB, S_COUNT
 };
+static_assert(S_COUNT <= 43, "slots 43..47 are reserved by abi.cu");
 
 double* slot(Handle& h, int s, size_t count) { return h.sm[s].get(count > 0 ? count : 1); }
 
@@ -40,9 +53,157 @@ void moment_factors(Handle& h, double* W, int c, double* out) {
        ns, h.st);
 }
 
-// col-major (rows x c, ld) <- row-major (rows x c)
-void to_colmajor(Handle& h, const double* src, int rows, int c, double* dst, int ld) {
-  transpose_in(src, rows, c, dst, ld, h.st);
+// grow an n-side buffer to `cols` columns, keeping its first `keep` columns
+void ensure_cols(Handle& h, DBuf& buf, int keep, int cols) {
+  const size_t need_d = (size_t)h.g.ld * cols;
+  if (buf.cap >= need_d) return;
+  DBuf fresh;
+  fresh.get(need_d);
+  if (keep > 0 && buf.p)
+    CK(cudaMemcpyAsync(fresh.p, buf.p, sizeof(double) * h.g.ld * keep, cudaMemcpyDeviceToDevice,
+                       h.st));
+  CK(cudaStreamSynchronize(h.st));
+  buf.free_();
+  buf = fresh;
+}
+
+// SVQB transform from the Gram pair of Y against (U0, Y):
+//   eigen(G - C^T C) = (P, lam) sorted descending
+//   mode 0 (rank revealing): keep lam_j > tol_rel^2 lam_0,
+//          TA = P_k diag(lam_k^-1/2)  ->  Q = (Y - U0 C) TA = Y TA - U0 (C TA)
+//   mode 1 (re-orthogonalisation): TA = P diag(lam^-1/2) P^T
+//   TB = C TA.  info[0] = k;  dinfo[0] = max(|G - I|, |C|)
+__global__ void svqb_build(const double* G, const double* C, int a, int b, const double* P,
+                           const double* lam, int mode, double tol_rel, double* TA, double* TB,
+                           int* info, double* dinfo) {
+  __shared__ int k_s;
+  __shared__ double scale[64];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int k = 0;
+    if (mode == 0) {
+      const double l0 = b > 0 ? lam[0] : 0.0;
+      for (int j = 0; j < b; ++j) {
+        const double l = lam[j];
+        if (l > 0.0 && l > tol_rel * tol_rel * l0) k = j + 1;
+        else break;
+      }
+    } else {
+      k = b;
+    }
+    k_s = k;
+    for (int j = 0; j < b; ++j) scale[j] = 1.0 / sqrt(lam[j] > 0.0 ? lam[j] : 1e-300);
+    double d = 0.0;
+    for (int i = 0; i < b * b; ++i) {
+      const double v = fabs(G[i] - ((i / b == i % b) ? 1.0 : 0.0));
+      d = v > d ? v : d;
+    }
+    for (int i = 0; i < a * b; ++i) d = fabs(C[i]) > d ? fabs(C[i]) : d;
+    info[0] = k;
+    dinfo[0] = d;
+  }
+  __syncthreads();
+  const int k = k_s;
+  const int ncol = mode == 0 ? k : b;
+  for (int i = tid; i < b * ncol; i += blockDim.x) {
+    const int r = i / ncol, c = i % ncol;
+    double v;
+    if (mode == 0) {
+      v = P[r * b + c] * scale[c];
+    } else {
+      v = 0.0;
+      for (int j = 0; j < b; ++j) v += P[r * b + j] * scale[j] * P[c * b + j];
+    }
+    TA[i] = v;
+  }
+  __syncthreads();
+  for (int i = tid; i < a * ncol; i += blockDim.x) {
+    const int r = i / ncol, c = i % ncol;
+    double v = 0.0;
+    for (int j = 0; j < b; ++j) v += C[r * b + j] * TA[j * ncol + c];
+    TB[i] = v;
+  }
+}
+
+__global__ void eye_kernel(double* I, int b) {
+  for (int i = threadIdx.x; i < b * b; i += blockDim.x) I[i] = (i / b == i % b) ? 1.0 : 0.0;
+}
+
+__global__ void unit_cols_kernel(double* U, int ld, int r) {
+  // U[:, j] = e_j (cells 0..r-1): the reference's canonical basis when S^ == 0
+  for (int j = blockIdx.x; j < r; j += gridDim.x)
+    for (int i = threadIdx.x; i < ld; i += blockDim.x) U[(size_t)j * ld + i] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void zero_rows_kernel(double* S, int row0, int rows, int cols) {
+  for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) S[(size_t)row0 * cols + i] = 0.0;
+}
+
+GramArgs lincomb_args(Handle& h, const double* U0, int a, const double* Y, int ny,
+                      const double* TA, const double* TB, int nb, double* out, double* grams,
+                      int nphase) {
+  GramArgs ga{};
+  ga.geo = h.g;
+  ga.X = U0; ga.ldx = h.g.ld; ga.na = a;
+  ga.Y = Y; ga.ldy = h.g.ld; ga.ny = ny;
+  ga.nb = nb;
+  ga.TA = TA; ga.TB = TB;
+  ga.Yout = out; ga.ldo = h.g.ld;
+  ga.nphase = nphase;
+  ga.self_phase = 1;
+  ga.gen = GEN_LINCOMB;
+  ga.inv_s = h.inv_s.p;
+  ga.out = grams;
+  return ga;
+}
+
+// Q (k cols, written at U[:, a:a+k]) = orthonormal basis of (I - U0 U0^T) X,
+// U0 = U[:, :a], X (b cols, ld). C1 = U0^T X (a x b, device). Returns k.
+int orth_complement(Handle& h, const double* X, int b, const double* C1) {
+  const int a = h.ru, ld = h.g.ld;
+  cudaStream_t st = h.st;
+  const double* U0 = h.U.p;
+  double* Qs = h.U.p + (size_t)a * ld;
+  double* grams = slot(h, S_OG, (size_t)b * (a + b));
+  double* TA = slot(h, S_OTA, (size_t)b * b);
+  double* TB = slot(h, S_OTB, (size_t)a * b);
+  double* P = slot(h, S_P, (size_t)b * b);
+  double* sig = slot(h, S_SIG, (size_t)b + 2);
+  double* Qt = slot(h, S_QTM, (size_t)b * b);
+  int* info = h.iflag.get(8);
+  double* dinfo = slot(h, S_TAIL, 4);
+  // pass 2: Y = X - U0 C1 (identity TA), C2 = U0^T Y, G2 = Y^T Y
+  eye_kernel<<<1, 256, 0, st>>>(TA, b);
+  launched();
+  gram(lincomb_args(h, U0, a, X, b, TA, C1, b, Qs, grams, 2), h.part, st);
+  // eigen(G2 - C2^T C2) (one-sided Jacobi SVD of the symmetric PSD matrix)
+  double* C2 = grams;                  // a x b
+  double* G2 = grams + (size_t)a * b;  // b x b
+  gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
+  svd_small(G2, b, b, P, sig, Qt, nullptr, st);
+  svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 0, 1e-7, TA, TB, info, dinfo);
+  launched();
+  CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int k = *(int*)(h.pinned + 8);
+  if (k == 0) return 0;
+  // pass 3: Q = Y TA - U0 TB (k cols, in place), C3 = U0^T Q, G3 = Q^T Q
+  gram(lincomb_args(h, U0, a, Qs, b, TA, TB, k, Qs, grams, 2), h.part, st);
+  double* C3 = grams;
+  double* G3 = grams + (size_t)a * k;
+  double* G3c = slot(h, S_M2, (size_t)k * k);
+  CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+  gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
+  svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
+  svqb_build<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1, dinfo);
+  launched();
+  CK(cudaMemcpyAsync(h.pinned + 9, dinfo, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h.pinned[9] > 1e-14) {
+    // pass 4: Q <- Q TA - U0 TB, in place (rows are staged before they are written)
+    gram(lincomb_args(h, U0, a, Qs, k, TA, TB, k, Qs, grams, 1), h.part, st);
+  }
+  return k;
 }
 
 }  // namespace
@@ -55,9 +216,10 @@ void streaming_step(Handle& h, double dt) {
   const int m = h.m, ns = g.ns, ld = g.ld;
   const int a = h.ru, b = h.rv;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
+  if (b > 32 || a > 32) fail(PND_ECONFIG, "streaming step supports rank <= 32");
   cudaStream_t st = h.st;
 
-  // --- K phase: K1 = RK4 of K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
+  // --- K phase: K1 = K0 + dK, K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
   phase(h, PH_LSIDE);
   double* F = slot(h, S_FV, (size_t)ns * b * b);
   moment_factors(h, h.V.p, b, F);
@@ -65,16 +227,14 @@ void streaming_step(Handle& h, double dt) {
   double* M = slot(h, S_MST, (size_t)ns * xmax * b);
   double* W1 = h.W1.get((size_t)ld * b);
   double* W2 = h.W2.get((size_t)ld * b);
-  const int cols = a + b;
-  double* A = h.A.get((size_t)ld * cols);
   const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
   for (int stage = 0; stage < 4; ++stage) {
     KStageArgs ka{};
     ka.geo = g;
     ka.inv_s = h.inv_s.p;
-    ka.U0 = h.U.p;
+    ka.U0 = stage == 3 ? nullptr : h.U.p;  // the last stage returns dK = h L(W2) only
     ka.ldu = ld;
-    ka.ra = a;
+    ka.ra = stage == 3 ? 0 : a;
     ka.S0 = h.S.p;
     ka.r = b;
     ka.M = M;
@@ -84,25 +244,21 @@ void streaming_step(Handle& h, double dt) {
       gemm(a, b, b, c, rowm(h.S.p, b), 0, rowm(F, b), (long)b * b, 0.0, rowm(M, b),
            (long)a * b, ns, st);
       ka.X = h.U.p;
-      ka.ldx = ld;
       ka.xc = a;
       ka.out = W1;
     } else {
       axpby(ns * b * b, c, F, 0.0, M, st);
       ka.X = stage == 2 ? W2 : W1;
-      ka.ldx = ld;
       ka.xc = b;
-      ka.out = stage == 3 ? A : (stage == 1 ? W2 : W1);
-      if (stage == 3) {
-        ka.copy_u = A + (size_t)b * ld;  // [K1 | U0] for the augmentation
-        ka.ldc = ld;
-      }
+      ka.out = stage == 2 ? W1 : W2;
     }
+    ka.ldx = ld;
     ka.ldo = ld;
     phase(h, PH_KSTAGE);
     kstage(ka, st);
     phase(h, PH_LSIDE);
   }
+  double* dK = W2;
 
   // --- L phase: L' = -sum_s A_s L Q_s, Q_s = (D_s S^-1 U0)^T U0, L0 = V0 S0^T
   double* QT = slot(h, S_QT, (size_t)ns * a * a);
@@ -118,15 +274,28 @@ void streaming_step(Handle& h, double dt) {
     ga.out = QT;  // QT_s = U0^T D_s U0 = Q_s^T
     gram(ga, h.part, st);
   }
+  // C1 = U0^T dK for the augmentation
+  double* C1 = slot(h, S_C1, (size_t)a * b);
+  {
+    GramArgs ga{};
+    ga.geo = g;
+    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
+    ga.Y = dK; ga.ldy = ld; ga.nb = b;
+    ga.nphase = 1;
+    ga.gen = GEN_PLAIN;
+    ga.inv_s = h.inv_s.p;
+    ga.out = C1;
+    gram(ga, h.part, st);
+  }
   phase(h, PH_LSIDE);
   double* L0 = slot(h, S_L0, (size_t)m * a);
   double* LW = slot(h, S_LW, (size_t)m * a);
   double* Z = slot(h, S_ZST, (size_t)ns * m * a);
   gemm(m, a, b, 1.0, rowm(h.V.p, b), 0, tr(rowm(h.S.p, b)), 0, 0.0, rowm(L0, a), 0, 1, st);
   CK(cudaMemcpyAsync(LW, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
+  const int cols = a + b;
   double* BV = slot(h, S_BV, (size_t)m * cols);
   for (int stage = 0; stage < 4; ++stage) {
-    // Z_s = LW Q_s  (Q_s = QT_s^T)
     gemm(m, a, a, 1.0, rowm(LW, a), 0, tr(rowm(QT, a)), (long)a * a, 0.0, rowm(Z, a),
          (long)m * a, ns, st);
     double* dst = stage == 3 ? slot(h, S_M2, (size_t)m * a) : LW;
@@ -134,26 +303,28 @@ void streaming_step(Handle& h, double dt) {
     // dst = L0 - c h sum_s A_s Z_s  (A_s symmetric: [A_0..A_ns-1] = (stacked A)^T)
     gemm(m, a, ns * m, -coef[stage] * dt, tr(rowm(h.amat.p, m)), 0, rowm(Z, a), 0, 1.0,
          rowm(dst, a), 0, 1, st);
-    if (stage == 3) to_colmajor(h, dst, m, a, BV, m);
+    if (stage == 3) transpose_in(dst, m, a, BV, m, st);
   }
-  to_colmajor(h, h.V.p, m, b, BV + (size_t)a * m, m);
+  transpose_in(h.V.p, m, b, BV + (size_t)a * m, m, st);
 
-  // --- augmentation: U^ = orth([K1, U0]), V^ = orth([L1, V0])  (dlra.py:220-221)
-  double* Uh = h.Uhat.get((size_t)ld * cols);
-  double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  // --- augmentation: U^ = [U0 | orth((I - U0 U0^T) dK)], V^ = orth([L1, V0])
   phase(h, PH_TSQR_N);
-  const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
+  ensure_cols(h, h.U, a, a + b);
+  const int k = orth_complement(h, dK, b, C1);
+  const int ru = a + k;
   double* Vhc = slot(h, S_VHC, (size_t)m * cols);
   double* Rv = slot(h, S_RV, (size_t)cols * cols);
   phase(h, PH_TSQR_M);
   const int rv = tsqr(BV, m, cols, m, Vhc, m, Rv, h.tq_m, st);
   phase(h, PH_SRK4);
 
-  // --- S^0 = (U^T U0) S0 (V0^T V^) = Ru[:, b:] S0 Rv[:, a:]^T
-  double* T1 = slot(h, S_ST1, (size_t)ru * b);
+  // --- S^0 = (U^T U0) S0 (V0^T V^) = [S0 Rv[:, a:]^T ; 0]
   double* Sh = slot(h, S_SHAT, (size_t)ru * rv);
-  gemm(ru, b, a, 1.0, Mat{Ru + b, cols, 1}, 0, rowm(h.S.p, b), 0, 0.0, rowm(T1, b), 0, 1, st);
-  gemm(ru, rv, b, 1.0, rowm(T1, b), 0, Mat{Rv + a, 1, cols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
+  gemm(a, rv, b, 1.0, rowm(h.S.p, b), 0, Mat{Rv + a, 1, cols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
+  if (k > 0) {
+    zero_rows_kernel<<<1, 256, 0, st>>>(Sh, a, k, rv);
+    launched();
+  }
 
   // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
   double* G = slot(h, S_G, (size_t)ns * ru * ru);
@@ -161,8 +332,8 @@ void streaming_step(Handle& h, double dt) {
   {
     GramArgs ga{};
     ga.geo = g;
-    ga.X = Uh; ga.ldx = ld; ga.na = ru;
-    ga.Y = Uh; ga.ldy = ld; ga.nb = ru;
+    ga.X = h.U.p; ga.ldx = ld; ga.na = ru;
+    ga.Y = h.U.p; ga.ldy = ld; ga.nb = ru;
     ga.nphase = ns;
     ga.gen = GEN_STENCIL;
     ga.inv_s = h.inv_s.p;
@@ -176,8 +347,7 @@ void streaming_step(Handle& h, double dt) {
   moment_factors(h, Vhr, rv, Fh);
   s_rk4(Sh, ru, rv, G, Fh, ns, dt, nullptr, st);
 
-  // --- new (augmented) state
-  std::swap(h.U, h.Uhat);
+  // --- new (augmented) state: U already holds [U0 | Q]
   double* Snew = h.S.get((size_t)ru * rv);
   CK(cudaMemcpyAsync(Snew, Sh, sizeof(double) * ru * rv, cudaMemcpyDeviceToDevice, st));
   double* Vnew = h.V.get((size_t)m * rv);
@@ -216,7 +386,7 @@ void scattering_step(Handle& h, double dt) {
   const int B = h.n_beams;
   cudaStream_t st = h.st;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
-  if (a > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
+  if (a > 32 || b > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
 
   // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
   phase(h, PH_SCATSMALL);
@@ -228,12 +398,11 @@ void scattering_step(Handle& h, double dt) {
     gemm(12 * B, b, m, 1.0, rowm(gt, m), 0, rowm(h.V.p, b), 0, 0.0, rowm(rows, b), 0, 1, st);
   }
 
-  // substep 2 input: A = [K1 | U0], K1 = U0 S0 + dt src_rows(V0)  (dlra.py:303)
-  const int cols = b + a;
-  double* A = h.A.get((size_t)ld * cols);
+  // substep 2 increment: dK = dt src_rows(V0)  (dlra.py:303; K1 = U0 S0 + dK)
+  double* dK = h.W2.get((size_t)ld * b);
   phase(h, PH_SCATK1);
-  scat_k1(g, h.U.p, ld, a, h.S.p, b, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p,
-          B > 0 ? h.psi.p : nullptr, ld, B, rows, A, ld, st);
+  scat_k1(g, h.U.p, ld, 0, h.S.p, b, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p,
+          B > 0 ? h.psi.p : nullptr, ld, B, rows, dK, ld, st);
 
   // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
   const int nw = h.n_cls <= 12 ? h.n_cls : 12;
@@ -281,19 +450,28 @@ void scattering_step(Handle& h, double dt) {
     gram(ga, h.part, st);
   }
   phase(h, PH_SCATSMALL);
+  // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass)
+  double* C1 = slot(h, S_C1, (size_t)a * b);
+  if (B > 0) {
+    for (int beam = 0; beam < B; ++beam)
+      gemm(a, b, 12, dt, Mat{left + beam * 12, 12 * B, 1}, 0, rowm(rows + (size_t)beam * 12 * b, b),
+           0, beam == 0 ? 0.0 : 1.0, rowm(C1, b), 0, 1, st);
+  } else {
+    fill_zero(C1, (size_t)a * b, st);
+  }
   double* coeffs = slot(h, S_COEF, (size_t)12 * m);
   coeff_kernel<<<16, 256, 0, st>>>(h.gdiag.p, h.sigt.p, m, coeffs);
   launched();
   double* lcols = slot(h, S_LCOL, (size_t)a * m);
   gemm(a, m, b, 1.0, rowm(h.S.p, b), 0, tr(rowm(h.V.p, b)), 0, 0.0, rowm(lcols, m), 0, 1, st);
   double* lnew = slot(h, S_LNEW, (size_t)a * m);
-  int* flag = h.iflag.get(4);
-  init_int<<<1, 1, 0, st>>>(flag, 1 << 30);
+  int* flag = h.iflag.get(8);
+  init_int<<<1, 1, 0, st>>>(flag + 4, 1 << 30);
   launched();
-  scat_solves(Bi, coeffs, lcols, a, m, dt, lnew, flag, st);
-  int singular = 0;
-  CK(cudaMemcpyAsync(&singular, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  scat_solves(Bi, coeffs, lcols, a, m, dt, lnew, flag + 4, st);
+  CK(cudaMemcpyAsync(h.pinned + 10, flag + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const int singular = *(int*)(h.pinned + 10);
   if (singular != (1 << 30)) {
     fail(PND_ENUMERICAL, "implicit scattering solve singular at moment column " +
                              std::to_string(singular) +
@@ -306,11 +484,11 @@ void scattering_step(Handle& h, double dt) {
   double* Rt = slot(h, S_RT, (size_t)kt * a);
   tsqr(lnew, m, a, m, Vtc, m, Rt, h.tq_m, st);  // S~ = R~^T  (a x kt)
 
-  // substep 2: U^ = orth([K1, U0])
-  double* Uh = h.Uhat.get((size_t)ld * cols);
-  double* Ru = slot(h, S_RU, (size_t)cols * cols);
+  // substep 2: U^ = [U0 | orth((I - U0 U0^T) dK)]
   phase(h, PH_TSQR_N);
-  const int ru = tsqr(A, g.n, cols, ld, Uh, ld, Ru, h.tq_n, st);
+  ensure_cols(h, h.U, a, a + b);
+  const int k = orth_complement(h, dK, b, C1);
+  const int ru = a + k;
   phase(h, PH_SCATSMALL);
 
   // substep 3: l3 = V~ S~^T + dt proj^T, V^ = orth([l3, V~])  (dlra.py:306-312)
@@ -333,27 +511,34 @@ void scattering_step(Handle& h, double dt) {
   const int rv = tsqr(BV, m, vcols, m, Vhc, m, Rv, h.tq_m, st);
   phase(h, PH_SCATSMALL);
 
-  // substep 4: S1 = (U^T U0) S~ (V~^T V^) + dt U^T (N psi / S)(g o T_M) V^
-  double* T1 = slot(h, S_ST1, (size_t)ru * kt);
+  // substep 4: S1 = (U^T U0) S~ (V~^T V^) + dt U^T (N psi / S)(g o T_M) V^, U^T U0 = [I; 0]
   double* Sh = slot(h, S_SHAT, (size_t)ru * rv);
-  gemm(ru, kt, a, 1.0, Mat{Ru + b, cols, 1}, 0, tr(rowm(Rt, a)), 0, 0.0, rowm(T1, kt), 0, 1, st);
-  gemm(ru, rv, kt, 1.0, rowm(T1, kt), 0, Mat{Rv + a, 1, vcols}, 0, 0.0, rowm(Sh, rv), 0, 1, st);
+  gemm(a, rv, kt, 1.0, tr(rowm(Rt, a)), 0, Mat{Rv + a, 1, vcols}, 0, 0.0, rowm(Sh, rv), 0, 1,
+       st);
+  if (k > 0) {
+    zero_rows_kernel<<<1, 256, 0, st>>>(Sh, a, k, rv);
+    launched();
+  }
   if (B > 0) {
+    // U^T X_b = [left_b ; Q^T X_b]
     double* proj2 = slot(h, S_PROJ2, (size_t)ru * 12 * B);
-    phase(h, PH_SCATGRAM);
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = Uh; ga.ldx = ld; ga.na = ru;
-    ga.nb = 12 * B;
-    ga.nphase = 1;
-    ga.gen = GEN_SOURCE;
-    ga.inv_s = h.inv_s.p;
-    ga.cls = h.cls.p;
-    ga.wtab = h.cls_atomic.p;
-    ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
-    ga.out = proj2;
-    gram(ga, h.part, st);
-    phase(h, PH_SCATSMALL);
+    CK(cudaMemcpyAsync(proj2, left, sizeof(double) * a * 12 * B, cudaMemcpyDeviceToDevice, st));
+    if (k > 0) {
+      phase(h, PH_SCATGRAM);
+      GramArgs ga{};
+      ga.geo = g;
+      ga.X = h.U.p + (size_t)a * ld; ga.ldx = ld; ga.na = k;
+      ga.nb = 12 * B;
+      ga.nphase = 1;
+      ga.gen = GEN_SOURCE;
+      ga.inv_s = h.inv_s.p;
+      ga.cls = h.cls.p;
+      ga.wtab = h.cls_atomic.p;
+      ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
+      ga.out = proj2 + (size_t)a * 12 * B;
+      gram(ga, h.part, st);
+      phase(h, PH_SCATSMALL);
+    }
     double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
     gemm(12 * B, rv, m, 1.0, rowm(gt, m), 0, colm(Vhc, m), 0, 0.0, rowm(gtv, rv), 0, 1, st);
     for (int beam = 0; beam < B; ++beam) {
@@ -362,7 +547,6 @@ void scattering_step(Handle& h, double dt) {
     }
   }
 
-  std::swap(h.U, h.Uhat);
   double* Snew = h.S.get((size_t)ru * rv);
   CK(cudaMemcpyAsync(Snew, Sh, sizeof(double) * ru * rv, cudaMemcpyDeviceToDevice, st));
   double* Vnew = h.V.get((size_t)m * rv);
@@ -403,13 +587,15 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   double* Qt = slot(h, S_QTM, (size_t)k * q);
   svd_small(h.S.p, p, q, P, sig, Qt, nullptr, st);
   double* dtail = slot(h, S_TAIL, 2);
-  int* info = h.iflag.get(4);
+  int* info = h.iflag.get(8);
   tail_rule(sig, k, theta, rmin, rmax, info + 1, dtail, st);
   CK(cudaMemcpyAsync(h.pinned, dtail, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync((int*)(h.pinned + 1), info + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h.pinned + 2, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int r1 = *(int*)(h.pinned + 1);
   const double tail = h.pinned[0];
+  const bool all_zero = h.pinned[2] == 0.0;
   if (r1 < 0) {
     fail(PND_ENUMERICAL, "adaptive rank " + std::to_string(-r1 - 1) + " exceeds rank_max=" +
                              std::to_string(rmax) + "; increase the truncation threshold");
@@ -417,8 +603,16 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   const Geom& g = h.g;
   const int m = h.m;
   phase(h, PH_ROTATE);
-  double* Unew = h.Uhat.get((size_t)g.ld * (r1 > 0 ? r1 : 1));
-  rotate_ld(g, h.U.p, g.ld, p, P, k, r1, Unew, g.ld, st);
+  ensure_cols(h, h.Uhat, 0, 2 * (r1 > 0 ? r1 : 1));
+  double* Unew = h.Uhat.p;
+  if (all_zero) {
+    // S^ == 0: the reference's Householder basis of [0 | U0] starts with e_0..e_{r-1}
+    // and svd(0) = (I, 0, I), so U1 is the canonical cell basis (Appendix C.4)
+    unit_cols_kernel<<<r1, 256, 0, st>>>(Unew, g.ld, r1);
+    launched();
+  } else {
+    rotate_ld(g, h.U.p, g.ld, p, P, k, r1, Unew, g.ld, st);
+  }
   phase(h, PH_SVD);
   double* Vn = slot(h, S_VNEW, (size_t)m * r1);
   gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);

@@ -225,6 +225,7 @@ def make_steps():
                 p + "v0": v0,
                 p + "aug_matrix": aug.matrix(),
                 p + "aug_shape": np.array([aug.u.shape[1], aug.v.shape[1]]),
+                p + "aug_sigma": np.linalg.svd(aug.s, compute_uv=False),
                 p + "trunc0_matrix": tr.matrix(),
                 p + "trunc0_rank": np.array(tr.rank),
                 p + "full_matrix": full,
