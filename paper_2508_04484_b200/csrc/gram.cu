@@ -235,7 +235,10 @@ void launch(const GramArgs& a, DBuf& partial, cudaStream_t st) {
     configured = smem;
   }
   const int nchunks = (a.geo.n + CH - 1) / CH;
-  int grid = sm_count() * 2;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_kernel<T, NPH, NW>, NW * 32,
+                                                   smem));
+  int grid = sm_count() * (per_sm > 0 ? per_sm : 1);
   if (grid > nchunks) grid = nchunks;
   if (grid < 1) grid = 1;
   const size_t count =
@@ -265,6 +268,15 @@ void dispatch_t(int t, const GramArgs& a, DBuf& partial, cudaStream_t st) {
 }  // namespace
 
 void gram(GramArgs a, DBuf& partial, cudaStream_t st) {
+  if (a.gen == GEN_STENCIL) {
+    if (a.nphase != a.geo.ns) fail(PND_ECONFIG, "stencil Grams cover every stencil");
+    stencil_grams(a, partial, st);
+    return;
+  }
+  if (a.gen == GEN_LINCOMB) {
+    lincomb(a, partial, a.nphase >= 2, st);
+    return;
+  }
   int w = a.na > a.nb ? a.na : a.nb;
   if (a.gen == GEN_LINCOMB && a.ny > w) w = a.ny;
   const int t = (w + 7) / 8;

@@ -283,15 +283,6 @@ int grid_for(int n, int block) {
 
 }  // namespace
 
-void kstage(const KStageArgs& a, cudaStream_t st) {
-  if (a.r <= 8) kstage_launch<8>(a, st);
-  else if (a.r <= 16) kstage_launch<16>(a, st);
-  else if (a.r <= 24) kstage_launch<24>(a, st);
-  else if (a.r <= 32) kstage_launch<32>(a, st);
-  else if (a.r <= 48) kstage_launch<48>(a, st);
-  else if (a.r <= 64) kstage_launch<64>(a, st);
-  else fail(PND_ECONFIG, "kstage supports at most 64 columns");
-}
 
 template <int NB>
 static void rotate_launch(const Geom& g, const double* X, int ldx, int a, const double* P,

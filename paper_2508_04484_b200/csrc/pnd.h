@@ -92,6 +92,9 @@ struct GramArgs {
                                              // concatenated; rows = nb for self_phase
 };
 void gram(GramArgs a, DBuf& partial, cudaStream_t st);
+// engine.cu: DMMA chunk kernels behind gram() for GEN_STENCIL and GEN_LINCOMB
+void stencil_grams(const GramArgs& a, DBuf& partial, cudaStream_t st);
+void lincomb(const GramArgs& a, DBuf& partial, bool grams, cudaStream_t st);
 
 // n-side streaming kernels (nside.cu)
 struct KStageArgs {
