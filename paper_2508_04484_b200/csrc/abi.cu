@@ -50,10 +50,6 @@ void IBuf::free_() {
   cap = 0;
 }
 
-void traverse(const Geom& g, const double* origin, int n_rays, const double* starts,
-              const double* dirs, int* counts, const long long* offsets, long long* cells,
-              double* t0, double* t1, cudaStream_t st);
-
 static long long g_launches = 0;
 
 void launched() {
@@ -62,6 +58,16 @@ void launched() {
 }
 
 long long launch_count() { return g_launches; }
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
 
 void phase(Handle& h, int id) {
   TimerState& t = h.timer;
@@ -89,29 +95,6 @@ __global__ void separable_kernel(const double* lat, const double* depth, int nxy
   }
 }
 
-__device__ __forceinline__ double hash_normalish(unsigned long long x) {
-  // splitmix64 -> two uniforms -> approximately normal (sum of 4 uniforms)
-  double s = 0.0;
-  for (int i = 0; i < 4; ++i) {
-    x += 0x9E3779B97F4A7C15ULL;
-    unsigned long long z = x;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-    z ^= z >> 31;
-    s += (double)(z >> 11) * (1.0 / 9007199254740992.0);
-  }
-  return (s - 2.0) * 1.7320508075688772;
-}
-
-__global__ void random_fill(double* a, int rows, int cols, int ld, unsigned long long seed) {
-  const long long total = (long long)rows * cols;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(i / rows), r = (int)(i - (long long)j * rows);
-    a[(size_t)j * ld + r] = hash_normalish(seed * 0x100000001B3ULL + (unsigned long long)i);
-  }
-}
-
 __global__ void logdiag_kernel(double* S, int r) {
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
     const int a = i / r, b = i % r;
@@ -128,6 +111,7 @@ struct pnd_handle {
 };
 
 using pnd::Handle;
+using pnd::NMat;
 
 namespace {
 
@@ -156,6 +140,19 @@ void down(double* dst, const double* src, size_t count, cudaStream_t st) {
   CK(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToHost, st));
 }
 
+// host (n x cols row-major) -> cell-major device view (rs >= cols, pad column zero)
+void upload_rows(Handle& h, NMat m, const double* src) {
+  if (m.rs != m.cols) pnd::fill_zero(m.p, (size_t)h.g.n * m.rs, h.st);
+  CK(cudaMemcpy2DAsync(m.p, m.rs * sizeof(double), src, m.cols * sizeof(double),
+                       m.cols * sizeof(double), h.g.n, cudaMemcpyHostToDevice, h.st));
+}
+
+// device view -> host rows [:, col0 : col0 + m.cols] of an (n x ldh) row-major array
+void download_rows(Handle& h, NMat m, double* dst, int ldh, int col0) {
+  CK(cudaMemcpy2DAsync(dst + col0, ldh * sizeof(double), m.p, m.rs * sizeof(double),
+                       m.cols * sizeof(double), h.g.n, cudaMemcpyDeviceToHost, h.st));
+}
+
 }  // namespace
 
 extern "C" {
@@ -182,7 +179,8 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     if (!(dx > 0 && dy > 0 && dz > 0)) pnd::fail(PND_ECONFIG, "grid spacings must be positive");
     if (m < 1) pnd::fail(PND_ECONFIG, "need at least one moment");
     const long long n = (long long)nx * ny * nz;
-    if (n >= (1LL << 31) - 1024) pnd::fail(PND_ECONFIG, "grid exceeds 2^31 cells per device");
+    const long long halo = 2LL * nx * ny + 72;
+    if (n + 2 * halo >= (1LL << 31) - 1024) pnd::fail(PND_ECONFIG, "grid exceeds 2^31 cells per device");
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
     CK(cudaMallocHost(&h.pinned, 64 * sizeof(double)));
@@ -192,6 +190,7 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     g.nz = nz;
     g.n = (int)n;
     g.ld = (int)((n + 31) / 32 * 32);
+    g.halo = (int)halo;
     g.h[0] = dx;
     g.h[1] = dy;
     g.h[2] = dz;
@@ -219,15 +218,19 @@ int pnd_destroy(pnd_handle* hh) {
   Handle& h = hh->h;
   cudaSetDevice(h.device);
   if (h.st) cudaStreamSynchronize(h.st);
-  pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.s_field, &h.cls_atomic, &h.cls_val, &h.gdiag,
-                       &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.U, &h.S, &h.V, &h.A,
-                       &h.Uhat, &h.W1, &h.W2, &h.part, &h.dep, &h.prev, &h.host_stage,
-                       &h.tq_n.tau, &h.tq_n.tree, &h.tq_n.rbuf, &h.tq_n.cbuf, &h.tq_m.tau,
-                       &h.tq_m.tree, &h.tq_m.rbuf, &h.tq_m.cbuf};
+  pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.cls_val,
+                       &h.gdiag, &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V,
+                       &h.part, &h.dep, &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.rbuf,
+                       &h.tq_m.cbuf};
   for (auto* b : bufs) b->free_();
+  pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs};
+  for (auto* b : nb) b->d.free_();
   for (auto& b : h.sm) b.free_();
   h.cls.free_();
   h.iflag.free_();
+  for (auto e : h.timer.pool) cudaEventDestroy(e);
+  for (auto e : h.timer.ev)
+    if (e) cudaEventDestroy(e);
   if (h.pinned) cudaFreeHost(h.pinned);
   if (h.st) cudaStreamDestroy(h.st);
   delete hh;
@@ -247,12 +250,12 @@ int pnd_synchronize(pnd_handle* hh) {
 int pnd_device_bytes(pnd_handle* hh, double* bytes) {
   return guard(hh, [&](Handle& h) {
     double total = 0;
-    const pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.s_field, &h.cls_atomic, &h.gdiag, &h.psi,
-                               &h.psi_lo, &h.tm, &h.flux, &h.U, &h.S, &h.V, &h.A, &h.Uhat,
-                               &h.W1, &h.W2, &h.part, &h.dep, &h.prev, &h.tq_n.tau,
-                               &h.tq_n.tree, &h.tq_n.cbuf, &h.tq_m.tau, &h.tq_m.tree,
-                               &h.tq_m.cbuf};
+    const pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.gdiag,
+                               &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V, &h.part, &h.dep,
+                               &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.cbuf};
     for (auto* b : bufs) total += 8.0 * b->cap;
+    const pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs};
+    for (auto* b : nb) total += 8.0 * b->d.cap;
     for (auto& b : h.sm) total += 8.0 * b.cap;
     *bytes = total;
   });
@@ -292,6 +295,7 @@ int pnd_set_inv_s(pnd_handle* hh, const double* inv_s) {
     up(d, inv_s, h.g.n, h.st);
     double* sf = h.s_field.get(h.g.ld);
     pnd::fill_zero(sf, h.g.ld, h.st);
+    pnd::set_isp(h);
     CK(cudaStreamSynchronize(h.st));
     h.have_inv_s = true;
   });
@@ -305,6 +309,7 @@ int pnd_set_class_stopping(pnd_handle* hh, const double* class_s) {
     double* d = h.inv_s.get(h.g.ld);
     double* sf = h.s_field.get(h.g.ld);
     pnd::class_gather_inv(h.cls.p, v, h.g.n, d, sf, h.st);
+    pnd::set_isp(h);
     h.have_inv_s = true;
   });
 }
@@ -346,12 +351,14 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
       pnd::fail(PND_ECONFIG, "all beams must share the group grid");
     }
     // values (n x G row-major) -> G columns of length ld
-    double* stage = h.sm[47].get((size_t)h.g.n * n_groups);
-    up(stage, values, (size_t)h.g.n * n_groups, h.st);
-    pnd::transpose_in(stage, h.g.n, n_groups, h.flux.p + (size_t)beam * n_groups * h.g.ld,
-                      h.g.ld, h.st);
+    pnd::DBuf stage;
+    double* s = stage.get((size_t)h.g.n * n_groups);
+    up(s, values, (size_t)h.g.n * n_groups, h.st);
+    pnd::transpose_in(s, h.g.n, n_groups, h.flux.p + (size_t)beam * n_groups * h.g.ld, h.g.ld,
+                      h.st);
     up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
     CK(cudaStreamSynchronize(h.st));
+    stage.free_();
   });
 }
 
@@ -372,14 +379,13 @@ int pnd_state_set(pnd_handle* hh, int ru, int rv, const double* u, const double*
   return guard(hh, [&](Handle& h) {
     if (ru < 1 || rv < 1) pnd::fail(PND_ECONFIG, "rank must be positive");
     if (ru > 64 || rv > 64) pnd::fail(PND_ECONFIG, "rank above 64 is not supported");
-    double* stage = h.sm[46].get((size_t)h.g.n * ru);
-    up(stage, u, (size_t)h.g.n * ru, h.st);
-    double* U = h.U.get((size_t)h.g.ld * ru);
-    pnd::fill_zero(U, (size_t)h.g.ld * ru, h.st);
-    pnd::transpose_in(stage, h.g.n, ru, U, h.g.ld, h.st);
+    NMat U = h.U.view(h.g, ru, h.st);
+    upload_rows(h, U, u);
     up(h.S.get((size_t)ru * rv), s, (size_t)ru * rv, h.st);
     up(h.V.get((size_t)h.m * rv), v, (size_t)h.m * rv, h.st);
     CK(cudaStreamSynchronize(h.st));
+    h.ua = ru;
+    h.uq = 0;
     h.ru = ru;
     h.rv = rv;
   });
@@ -395,9 +401,8 @@ int pnd_state_shape(pnd_handle* hh, int* ru, int* rv) {
 int pnd_state_get(pnd_handle* hh, double* u, double* s, double* v) {
   return guard(hh, [&](Handle& h) {
     if (u) {
-      double* stage = h.sm[46].get((size_t)h.g.n * h.ru);
-      pnd::transpose_out(h.U.p, h.g.ld, h.g.n, h.ru, stage, h.st);
-      down(u, stage, (size_t)h.g.n * h.ru, h.st);
+      download_rows(h, pnd::state_u(h), u, h.ru, 0);
+      if (h.uq > 0) download_rows(h, pnd::state_q(h), u, h.ru, h.ua);
     }
     if (s) down(s, h.S.p, (size_t)h.ru * h.rv, h.st);
     if (v) down(v, h.V.p, (size_t)h.m * h.rv, h.st);
@@ -472,28 +477,26 @@ int pnd_apply_streaming(pnd_handle* hh, const double* u, double* out) {
   return guard(hh, [&](Handle& h) {
     if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
     if (!h.have_angular || !h.have_inv_s) pnd::fail(PND_ECONFIG, "set angular and inv_s first");
-    if (h.m > 64) pnd::fail(PND_ECONFIG, "apply_streaming supports m <= 64");
-    const int n = h.g.n, m = h.m, ld = h.g.ld, ns = h.g.ns;
+    if (h.m > 32) pnd::fail(PND_ECONFIG, "apply_streaming supports m <= 32");
+    const int n = h.g.n, m = h.m, ns = h.g.ns;
     for (size_t i = 0; i < (size_t)n * m; ++i)
       if (!std::isfinite(u[i])) pnd::fail(PND_ENUMERICAL, "non-finite streaming input");
-    pnd::DBuf su, du, dout, stage, mneg;
-    try {
-      double* s = stage.get((size_t)n * m);
-      up(s, u, (size_t)n * m, h.st);
-      double* U = du.get((size_t)ld * m);
-      pnd::transpose_in(s, n, m, U, ld, h.st);
-      double* M = mneg.get((size_t)ns * m * m + 1);
-      pnd::axpby(ns * m * m, -1.0, h.amat.p, 0.0, M, h.st);
-      double* O = dout.get((size_t)ld * m);
-      pnd::apply_streaming_full(h.g, U, ld, m, h.inv_s.p, M, nullptr, O, ld, h.st);
-      pnd::transpose_out(O, ld, n, m, s, h.st);
-      down(out, s, (size_t)n * m, h.st);
-      CK(cudaStreamSynchronize(h.st));
-    } catch (...) {
-      su.free_(); du.free_(); dout.free_(); stage.free_(); mneg.free_();
-      throw;
-    }
-    su.free_(); du.free_(); dout.free_(); stage.free_(); mneg.free_();
+    NMat X = h.W1.view(h.g, m, h.st);
+    upload_rows(h, X, u);
+    pnd::DBuf mneg;
+    double* M = mneg.get((size_t)ns * m * m + 1);
+    pnd::axpby(ns * m * m, -1.0, h.amat.p, 0.0, M, h.st);
+    NMat O = h.W2.view(h.g, m, h.st);
+    pnd::KStageArgs a{};
+    a.geo = h.g;
+    a.X = X;
+    a.M = M;
+    a.inv_s = h.isp.p + 2 * (size_t)h.g.halo;
+    a.out = O;
+    pnd::kstage(a, h.st);
+    download_rows(h, O, out, m, 0);
+    CK(cudaStreamSynchronize(h.st));
+    mneg.free_();
   });
 }
 
@@ -502,31 +505,16 @@ int pnd_stencil_grams(pnd_handle* hh, const double* x, int a, const double* y, i
   return guard(hh, [&](Handle& h) {
     if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
     if (!h.have_inv_s) pnd::fail(PND_ECONFIG, "set inv_s first");
-    const int n = h.g.n, ld = h.g.ld, ns = h.g.ns;
-    pnd::DBuf sx, sy, dx, dy, dout;
-    double* s1 = sx.get((size_t)n * a);
-    double* s2 = sy.get((size_t)n * b);
-    up(s1, x, (size_t)n * a, h.st);
-    up(s2, y, (size_t)n * b, h.st);
-    double* X = dx.get((size_t)ld * a);
-    double* Y = dy.get((size_t)ld * b);
-    pnd::fill_zero(X, (size_t)ld * a, h.st);
-    pnd::fill_zero(Y, (size_t)ld * b, h.st);
-    pnd::transpose_in(s1, n, a, X, ld, h.st);
-    pnd::transpose_in(s2, n, b, Y, ld, h.st);
-    double* O = dout.get((size_t)ns * a * b + 1);
-    pnd::GramArgs ga{};
-    ga.geo = h.g;
-    ga.X = X; ga.ldx = ld; ga.na = a;
-    ga.Y = Y; ga.ldy = ld; ga.nb = b;
-    ga.nphase = ns;
-    ga.gen = pnd::GEN_STENCIL;
-    ga.inv_s = h.inv_s.p;
-    ga.out = O;
-    pnd::gram(ga, h.part, h.st);
-    down(out, O, (size_t)ns * a * b, h.st);
+    NMat X = h.W1.view(h.g, a, h.st);
+    NMat Y = h.W2.view(h.g, b, h.st);
+    upload_rows(h, X, x);
+    upload_rows(h, Y, y);
+    pnd::DBuf o;
+    double* O = o.get((size_t)h.g.ns * a * b + 1);
+    pnd::stencil_grams_xy(h.g, X, Y, h.isp.p + 2 * (size_t)h.g.halo, O, h.part, h.st);
+    down(out, O, (size_t)h.g.ns * a * b, h.st);
     CK(cudaStreamSynchronize(h.st));
-    sx.free_(); sy.free_(); dx.free_(); dy.free_(); dout.free_();
+    o.free_();
   });
 }
 
@@ -534,29 +522,24 @@ int pnd_k_rhs(pnd_handle* hh, const double* k, int r, const double* f, double* o
   return guard(hh, [&](Handle& h) {
     if (!h.stencil_error.empty()) pnd::fail(PND_ECONFIG, h.stencil_error);
     if (!h.have_inv_s) pnd::fail(PND_ECONFIG, "set inv_s first");
-    const int n = h.g.n, ld = h.g.ld, ns = h.g.ns;
-    pnd::DBuf st, dk, dm, dout;
-    double* s = st.get((size_t)n * r);
-    up(s, k, (size_t)n * r, h.st);
-    double* K = dk.get((size_t)ld * r);
-    pnd::transpose_in(s, n, r, K, ld, h.st);
+    const int ns = h.g.ns;
+    NMat K = h.W1.view(h.g, r, h.st);
+    upload_rows(h, K, k);
+    pnd::DBuf dm;
     double* M = dm.get((size_t)ns * r * r + 1);
     up(M, f, (size_t)ns * r * r, h.st);
     pnd::axpby(ns * r * r, -1.0, M, 0.0, M, h.st);
-    double* O = dout.get((size_t)ld * r);
-    pnd::KStageArgs ka{};
-    ka.geo = h.g;
-    ka.X = K; ka.ldx = ld; ka.xc = r;
-    ka.U0 = nullptr; ka.ra = 0;
-    ka.M = M;
-    ka.inv_s = h.inv_s.p;
-    ka.r = r;
-    ka.out = O; ka.ldo = ld;
-    pnd::kstage(ka, h.st);
-    pnd::transpose_out(O, ld, n, r, s, h.st);
-    down(out, s, (size_t)n * r, h.st);
+    NMat O = h.W2.view(h.g, r, h.st);
+    pnd::KStageArgs a{};
+    a.geo = h.g;
+    a.X = K;
+    a.M = M;
+    a.inv_s = h.isp.p + 2 * (size_t)h.g.halo;
+    a.out = O;
+    pnd::kstage(a, h.st);
+    download_rows(h, O, out, r, 0);
     CK(cudaStreamSynchronize(h.st));
-    st.free_(); dk.free_(); dm.free_(); dout.free_();
+    dm.free_();
   });
 }
 
@@ -722,25 +705,40 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
 int pnd_state_random(pnd_handle* hh, int r, unsigned long long seed) {
   return guard(hh, [&](Handle& h) {
     if (r < 1 || r > 32) pnd::fail(PND_ECONFIG, "random state rank must be 1..32");
-    const int ld = h.g.ld, m = h.m;
-    double* A = h.A.get((size_t)ld * r);
-    pnd::fill_zero(A, (size_t)ld * r, h.st);
-    pnd::random_fill<<<148 * 8, 256, 0, h.st>>>(A, h.g.n, r, ld, seed);
-    pnd::launched();
-    double* U = h.U.get((size_t)ld * r);
-    double* R = h.sm[45].get((size_t)r * r);
-    pnd::tsqr(A, h.g.n, r, ld, U, ld, R, h.tq_n, h.st);
+    const int m = h.m;
+    // U = orth(random n x r) through the device Gram-Schmidt/SVQB passes
+    NMat X = h.Xs.view(h.g, r, h.st);
+    pnd::random_rows(h.g, X, seed, h.st);
+    h.ua = 0;
+    h.uq = 0;
+    const int k = pnd::orth_complement(h, X, nullptr);
+    std::swap(h.U, h.Q);
+    h.ua = k;
+    h.uq = 0;
     double* B = h.sm[44].get((size_t)m * r);
-    pnd::random_fill<<<64, 256, 0, h.st>>>(B, m, r, m, seed + 7);
-    pnd::launched();
     double* Vc = h.sm[43].get((size_t)m * r);
-    pnd::tsqr(B, m, r, m, Vc, m, R, h.tq_m, h.st);
-    pnd::transpose_out(Vc, m, m, r, h.V.get((size_t)m * r), h.st);
-    double* S = h.S.get((size_t)r * r);
-    pnd::logdiag_kernel<<<1, 256, 0, h.st>>>(S, r);
+    double* R = h.sm[45].get((size_t)r * r);
+    // V = orth(random m x r) on the moment side (TSQR)
+    {
+      pnd::DBuf tmp;
+      double* t = tmp.get((size_t)m * r);
+      std::vector<double> host((size_t)m * r);
+      unsigned long long x = seed * 7919ULL + 1;
+      for (auto& v : host) {
+        x = x * 6364136223846793005ULL + 1442695040888963407ULL;
+        v = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+      }
+      up(B, host.data(), host.size(), h.st);
+      pnd::tsqr(B, m, r, m, Vc, m, R, h.tq_m, h.st);
+      pnd::transpose_out(Vc, m, m, r, h.V.get((size_t)m * r), h.st);
+      CK(cudaStreamSynchronize(h.st));
+      tmp.free_();
+    }
+    double* S = h.S.get((size_t)k * r);
+    pnd::logdiag_kernel<<<1, 256, 0, h.st>>>(S, k);
     pnd::launched();
     CK(cudaStreamSynchronize(h.st));
-    h.ru = h.rv = r;
+    h.ru = h.rv = k;
   });
 }
 

@@ -9,7 +9,7 @@ namespace pnd {
 // step (pnd_timing / pnd_timing_get), used by bench.py for per-kernel
 // durations and roofline fractions
 enum Phase {
-  PH_KSTAGE, PH_LGRAM, PH_LSIDE, PH_TSQR_N, PH_TSQR_M, PH_SGRAM, PH_SRK4, PH_SVD, PH_ROTATE,
+  PH_KSTAGE, PH_LGRAM, PH_LSIDE, PH_ORTH, PH_TSQR_M, PH_SGRAM, PH_SRK4, PH_SVD, PH_ROTATE,
   PH_SCATK1, PH_SCATGRAM, PH_SCATSMALL, PH_DOSE, PH_DEFECT, PH_COUNT
 };
 
@@ -31,8 +31,9 @@ struct Handle {
 
   // operators and coefficients
   DBuf amat;        // ns x m x m, A_s in stencil order
-  DBuf inv_s;       // n
-  DBuf s_field;     // n (S at E_mid, for the "steps" tally)
+  DBuf inv_s;       // ld (1/S per cell)
+  DBuf isp;         // (n + 2 halo) x 2: rows [1/S, 0] with zero halo rows (TMA segments)
+  DBuf s_field;     // ld (S at E_mid, for the "steps" tally)
   IBuf cls;         // n
   DBuf cls_atomic;  // n_cls x 12
   DBuf cls_val;     // n_cls (staging)
@@ -43,22 +44,23 @@ struct Handle {
   DBuf psi;         // n_beams x ld (source slice, E_mid)
   DBuf psi_lo;      // n_beams x ld (tally slice, E_lo)
   DBuf tm;          // n_beams x m
-  DBuf flux;        // n_beams x G x ld (group tables)
+  DBuf flux;        // n_beams x G x ld (group tables, column-major)
   int n_groups = 0;
   bool have_angular = false, have_inv_s = false, have_mat = false, have_scat = false;
 
-  // state: U (ld x ru col-major), S (ru x rv row-major), V (m x rv row-major)
-  DBuf U, S, V;
+  // state: U^ = [U (ua cols) | Q (uq cols)] cell-major, S (ru x rv row-major),
+  // V (m x rv row-major); ru = ua + uq
+  NBuf U, Q, Un, Qa, W1, W2, Xs;
+  DBuf S, V;
+  int ua = 0, uq = 0;
   int ru = 0, rv = 0;
 
   // workspaces
-  DBuf A, Uhat, W1, W2;       // n-side (ld x cols)
   DBuf part;                  // gram partials
-  TsqrWork tq_n, tq_m;
+  TsqrWork tq_m;
   DBuf sm[48];                // small / m-side scratch (see step.cu Slot)
   IBuf iflag;
   DBuf dep, prev;             // dose tally
-  DBuf host_stage;            // unused placeholder
   double* pinned = nullptr;   // small pinned readback buffer
   TimerState timer;
 };
@@ -67,10 +69,19 @@ struct Handle {
 // the time until the next mark is attributed to `id` (id < 0 closes)
 void phase(Handle& h, int id);
 
+// views of the current state
+NMat state_u(Handle& h);
+NMat state_q(Handle& h);
+void consolidate(Handle& h);   // fold Q into U (uq -> 0)
+void set_isp(Handle& h);       // refresh the [1/S, 0] halo rows from inv_s
+
 void streaming_step(Handle& h, double dt);
 void scattering_step(Handle& h, double dt);
 void truncate(Handle& h, double theta, int rmin, int rmax, double* tail, int* rank);
 void dose_accumulate_step(Handle& h, double dt, bool tally_steps);
 double orth_defect(Handle& h);
+// Q (k columns) = orthonormal basis of (I - U U^T) X; C1 = U^T X (device, ua x b; null
+// when U is empty). Returns k; the result is installed as the state's Q.
+int orth_complement(Handle& h, NMat X, const double* C1);
 
 }  // namespace pnd

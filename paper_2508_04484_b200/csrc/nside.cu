@@ -1,218 +1,762 @@
-// Cell-parallel (n-side) kernels of the energy step.
+// Cell-parallel (n-side) kernels of the energy step, cell-major layout.
 //
-// kstage: one Horner stage of the K-phase RK4 (dlra.py:168-174, 118-123),
-//   out = U0 S0 + sum_s (D_s S^-1 X) M_s, thread per cell. The 13-point
-//   neighbourhood of the cell (+-1, +-2 along each active axis) is read per
-//   column through L1/L2 (column-major layout: x neighbours are in the same
-//   256-byte segment, y/z neighbours are re-reads the L2 holds), the ns
-//   r x r contraction matrices sit in shared memory and are read as warp
-//   broadcasts. With U0 = null and M_s = -A_s it is the full-rank streaming
-//   operator F_S (spatial.py:148-167).
-// rotate / scat_k1 / dose: row-local contractions of the truncation
-//   (dlra.py:111-113), the scattering K-step (dlra.py:303, 244-251) and the
-//   dose trapezoid (driver.py:606, 613-622).
-#include "pnd.h"
+// Every n-side operation is "form per-cell feature rows, then contract them"
+// and runs as FP64 tensor-core mma.sync.m8n8k4 (DMMA) on shared-memory tiles:
+//   kstage   one Horner stage of the K-phase RK4 (dlra.py:168-174): the 2*na
+//            upwind stencil values of every column (spatial.py:81-118) plus the
+//            U0 row, contracted with [M_0; ...; M_ns-1; S0];
+//   sgram    the stencil Grams U^T D_s S^-1 U of the L- and S-phases
+//            (dlra.py:183-184, 199-209), accumulated in registers over chunks;
+//   lincomb  [Y1 | Y2] TA - X TB with its Grams: the passes of the block
+//            Gram-Schmidt/SVQB augmentation and the truncation rotation
+//            (dlra.py:26-43, 111-113);
+//   pgram    plain / weighted / source Grams (dlra.py:285, 307-319).
+// The stencil kernels stage their halo segments with cp.async.bulk (one TMA
+// bulk copy per contiguous segment of cell rows, double-buffered on two
+// mbarriers): box 0 = rows [c0-2, c0+CH+2) covers the first active axis
+// (stride 1), and rows [c0 + d*st, c0 + d*st + CH), d = -2,-1,1,2, cover every
+// further axis. The halo rows around each matrix are zero, so every segment is
+// in bounds. Shared-memory tiles use row lengths = 4 (mod 16) doubles where
+// DMMA fragments are read, which spreads a half-warp over 16 distinct banks.
+#include "tma.cuh"
 
 namespace pnd {
 
 namespace {
 
-struct Nbr {
-  // per active axis: f at offsets -2..+2 (index 2 = centre), valid flags by position
-  int idx[3], len[3], st[3];
+__host__ __device__ constexpr int pad4(int w) { return ((w + 11) / 16) * 16 + 4; }
+__host__ __device__ constexpr int up16(int w) { return (w + 15) / 16 * 16; }
+
+struct Plan {
+  int nbox;    // 1 + 4 (na - 1)
+  int off[9];  // first row of box b relative to c0
 };
 
-template <int NB>
-__global__ void __launch_bounds__(128) kstage_kernel(KStageArgs a) {
-  extern __shared__ double sm[];
-  const Geom& g = a.geo;
-  const int ns = g.ns;
-  const int r = a.r, xc = a.xc, ra = a.ra;
-  double* sM = sm;                   // ns * xc * NB
-  double* sS = sm + ns * xc * NB;    // ra * NB
-  for (int i = threadIdx.x; i < ns * xc * NB; i += blockDim.x) {
-    const int s = i / (xc * NB), rem = i - s * xc * NB, j = rem / NB, k = rem - j * NB;
-    sM[i] = k < r ? a.M[(s * xc + j) * r + k] : 0.0;
-  }
-  if (a.U0) {
-    for (int i = threadIdx.x; i < ra * NB; i += blockDim.x) {
-      const int j = i / NB, k = i - j * NB;
-      sS[i] = k < r ? a.S0[j * r + k] : 0.0;
-    }
-  }
-  __syncthreads();
+Plan make_plan(const Geom& g) {
+  Plan p{};
+  p.nbox = 1;
+  p.off[0] = -2;
   const int nxy = g.nx * g.ny;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += gridDim.x * blockDim.x) {
-    const int ck = c / nxy, rem = c - ck * nxy;
-    const int cj = rem / g.nx, ci = rem - cj * g.nx;
-    // per active axis: neighbour offsets and inv_s at -2..+2
-    double is[3][5];
-    int off[3][5];
-    bool ok[3][5];
+  for (int ai = 1; ai < g.na; ++ai) {
+    const int st = g.axis[ai] == 1 ? g.nx : nxy;
+    const int ds[4] = {-2, -1, 1, 2};
+    for (int q = 0; q < 4; ++q) p.off[p.nbox++] = ds[q] * st;
+  }
+  return p;
+}
+
+struct CellCoord {
+  int idx[3];
+  int len[3];
+};
+
+__device__ __forceinline__ CellCoord coord_of(const Geom& g, int c) {
+  const int nxy = g.nx * g.ny;
+  const int ck = c / nxy, rem = c - ck * nxy;
+  const int cj = rem / g.nx, ci = rem - cj * g.nx;
+  const int all[3] = {ci, cj, ck};
+  const int lens[3] = {g.nx, g.ny, g.nz};
+  CellCoord cc;
 #pragma unroll
-    for (int ai = 0; ai < 3; ++ai) {
-      if (ai < g.na) {
-        const int axis = g.axis[ai];
-        const int len = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
-        const int idx = axis == 0 ? ci : (axis == 1 ? cj : ck);
-        const int st = axis == 0 ? 1 : (axis == 1 ? g.nx : nxy);
+  for (int ai = 0; ai < 3; ++ai) {
+    const int axis = ai < g.na ? g.axis[ai] : 0;
+    cc.idx[ai] = all[axis];
+    cc.len[ai] = lens[axis];
+  }
+  return cc;
+}
+
+// first staged row of box b (box 0 has CH + 4 rows, the others CH)
+template <int CH>
+__device__ __forceinline__ int box_row(int b) {
+  return b == 0 ? 0 : CH + 4 + (b - 1) * CH;
+}
+
+// 2*na stencil values D_s (S^-1 x) of column j at chunk cell i, from staged rows
+//   X: staged rows of the input (row length rs), I: staged rows of [1/S, 0]
+template <int CH>
+__device__ __forceinline__ void stencil6(const Geom& g, const CellCoord& cc, const double* X,
+                                         int rs, const double* I, int i, int j, double* t) {
 #pragma unroll
-        for (int d = 0; d < 5; ++d) {
-          const int q = idx + d - 2;
-          ok[ai][d] = q >= 0 && q < len;
-          off[ai][d] = c + (d - 2) * st;
-          is[ai][d] = ok[ai][d] ? a.inv_s[off[ai][d]] : 0.0;
-        }
+  for (int ai = 0; ai < 3; ++ai) {
+    if (ai < g.na) {
+      const int axis = g.axis[ai];
+      double f[5];
+      if (ai == 0) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) f[d] = X[(i + d) * rs + j] * I[2 * (i + d)];
+      } else {
+        const int b = 1 + 4 * (ai - 1);
+        const int r0 = box_row<CH>(b) + i, r1 = box_row<CH>(b + 1) + i;
+        const int r3 = box_row<CH>(b + 2) + i, r4 = box_row<CH>(b + 3) + i;
+        f[0] = X[r0 * rs + j] * I[2 * r0];
+        f[1] = X[r1 * rs + j] * I[2 * r1];
+        f[2] = X[(i + 2) * rs + j] * I[2 * (i + 2)];
+        f[3] = X[r3 * rs + j] * I[2 * r3];
+        f[4] = X[r4 * rs + j] * I[2 * r4];
       }
+      const double ih = g.ih[axis], i2h = g.i2h[axis];
+      const int idx = cc.idx[ai], len = cc.len[ai];
+      double tp, tm;
+      if (idx >= 2) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) * i2h;
+      else if (idx == 1) tp = (f[2] - f[1]) * ih;
+      else tp = f[2] * ih;
+      if (idx <= len - 3) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) * i2h;
+      else if (idx == len - 2) tm = (f[3] - f[2]) * ih;
+      else tm = -f[2] * ih;
+      t[2 * ai] = tp;
+      t[2 * ai + 1] = tm;
     }
-    double acc[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) acc[k] = 0.0;
-    if (a.U0) {
-      for (int j = 0; j < ra; ++j) {
-        const double u = a.U0[(size_t)j * a.ldu + c];
-        if (a.copy_u) a.copy_u[(size_t)j * a.ldc + c] = u;
-        const double* srow = sS + j * NB;
-#pragma unroll
-        for (int k = 0; k < NB; ++k) acc[k] = fma(u, srow[k], acc[k]);
-      }
-    }
-    for (int j = 0; j < xc; ++j) {
-      const double* col = a.X + (size_t)j * a.ldx;
-#pragma unroll
-      for (int ai = 0; ai < 3; ++ai) {
-        if (ai < g.na) {
-          const int axis = g.axis[ai];
-          const double ih = g.ih[axis], i2h = g.i2h[axis];
-          double f[5];
-#pragma unroll
-          for (int d = 0; d < 5; ++d) f[d] = ok[ai][d] ? col[off[ai][d]] * is[ai][d] : 0.0;
-          // D^+ (minus-biased) and D^- (plus-biased), spatial.py:81-118
-          double tp, tm;
-          if (ok[ai][0]) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) * i2h;
-          else if (ok[ai][1]) tp = (f[2] - f[1]) * ih;
-          else tp = f[2] * ih;
-          if (ok[ai][4]) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) * i2h;
-          else if (ok[ai][3]) tm = (f[3] - f[2]) * ih;
-          else tm = -f[2] * ih;
-          const double* mp = sM + ((2 * ai) * xc + j) * NB;
-          const double* mm = sM + ((2 * ai + 1) * xc + j) * NB;
-#pragma unroll
-          for (int k = 0; k < NB; ++k) acc[k] = fma(tp, mp[k], fma(tm, mm[k], acc[k]));
-        }
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k)
-      if (k < r) a.out[(size_t)k * a.ldo + c] = acc[k];
   }
 }
 
-template <int NB>
-void kstage_launch(const KStageArgs& a, cudaStream_t st) {
-  const size_t smem = ((size_t)a.geo.ns * a.xc * NB + (size_t)a.ra * NB) * sizeof(double);
-  CK(cudaFuncSetAttribute(kstage_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+struct Stage {
+  int nbox;
+  int off[9];
+  int nrows;      // staged rows per input
+  int xoff[2];    // doubles offset of the staged rows of input 0 / 1
+  int ioff;       // offset of the staged [1/S, 0] rows
+  int uoff;       // offset of the separately staged centre rows (-1: none)
+  int buf;        // doubles per buffer
+  unsigned bytes; // bytes per chunk
+};
+
+template <int CH>
+Stage make_stage(const Geom& g, const NMat* in, int nin, const NMat* centre) {
+  const Plan p = make_plan(g);
+  Stage s{};
+  s.nbox = p.nbox;
+  for (int q = 0; q < p.nbox; ++q) s.off[q] = p.off[q];
+  s.nrows = CH + 4 + (p.nbox - 1) * CH;
+  int o = 0;
+  unsigned bytes = 0;
+  for (int k = 0; k < 2; ++k) {
+    s.xoff[k] = o;
+    if (k < nin) {
+      o += up16(s.nrows * in[k].rs);
+      bytes += s.nrows * in[k].rs * 8;
+    }
+  }
+  s.ioff = o;
+  o += up16(2 * s.nrows);
+  bytes += 2 * s.nrows * 8;
+  s.uoff = -1;
+  if (centre) {
+    s.uoff = o;
+    o += up16(CH * centre->rs);
+    bytes += CH * centre->rs * 8;
+  }
+  s.buf = up16(o);
+  s.bytes = bytes;
+  return s;
+}
+
+// one thread issues the bulk copies of one chunk's segments
+template <int CH>
+__device__ __forceinline__ void stage_chunk(const Stage& S, double* dst, uint64_t* bar, int c0,
+                                            const NMat& a, const NMat& b, int nin,
+                                            const double* isp, const NMat& u) {
+  mbar_expect_tx(bar, S.bytes);
+  for (int q = 0; q < S.nbox; ++q) {
+    const int rows = q == 0 ? CH + 4 : CH;
+    const int row = c0 + S.off[q];
+    const int drow = q == 0 ? 0 : CH + 4 + (q - 1) * CH;
+    bulk_load(dst + S.xoff[0] + drow * a.rs, a.p + (long)row * a.rs, rows * a.rs * 8, bar);
+    if (nin > 1)
+      bulk_load(dst + S.xoff[1] + drow * b.rs, b.p + (long)row * b.rs, rows * b.rs * 8, bar);
+    bulk_load(dst + S.ioff + 2 * drow, isp + 2L * row, rows * 16, bar);
+  }
+  if (S.uoff >= 0) bulk_load(dst + S.uoff, u.p + (long)c0 * u.rs, CH * u.rs * 8, bar);
+}
+
+// ===================================================================== kstage
+constexpr int KC = 32;
+
+struct KParams {
+  int K, K4, KS, BS, ksplit;
+};
+
+template <int RB>
+__global__ void __launch_bounds__(256, 1)
+    kstage_kernel(KStageArgs a, Stage S, KParams P, const double* __restrict__ isp) {
+  constexpr int NT = RB / 8;
+  constexpr int TILES = (KC / 8) * NT;
+  constexpr int RBP = RB + 2;
+  extern __shared__ __align__(128) double sm[];
+  double* buf = sm;
+  double* sA = sm + 2 * S.buf;              // [KC][KS]
+  double* sB = sA + KC * P.KS;              // [K4][BS]
+  double* sO = sB + P.K4 * P.BS;            // [ksplit][KC][RBP]
+  uint64_t* bar = (uint64_t*)(sO + P.ksplit * KC * RBP);
+  const Geom& g = a.geo;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ns = g.ns, xc = a.X.cols, ra = a.U0.p ? a.U0.cols : 0, r = a.out.cols;
+  const int K = P.K, K4 = P.K4, KS = P.KS, BS = P.BS;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  for (int i = tid; i < K4 * BS; i += 256) {
+    const int k = i / BS, n = i - k * BS;
+    double v = 0.0;
+    if (n < r && k < K) v = k < ns * xc ? a.M[(size_t)k * r + n] : a.S0[(size_t)(k - ns * xc) * r + n];
+    sB[i] = v;
+  }
+  for (int i = tid; i < KC * KS; i += 256) sA[i] = 0.0;
+  __syncthreads();
+  const bool sepu = S.uoff >= 0;
+  const int nchunks = (g.n + KC - 1) / KC;
+  if (tid == 0 && blockIdx.x < nchunks)
+    stage_chunk<KC>(S, buf, &bar[0], blockIdx.x * KC, a.X, a.X, 1, isp, a.U0);
+  const int K4s = K4 / P.ksplit;  // multiple of 4 (host guarantees)
+  int it = 0;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int next = chunk + gridDim.x;
+    if (tid == 0 && next < nchunks) {
+      fence_proxy_async();
+      stage_chunk<KC>(S, buf + (b ^ 1) * S.buf, &bar[b ^ 1], next * KC, a.X, a.X, 1, isp, a.U0);
+    }
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const double* B = buf + b * S.buf;
+    const double* Xs = B + S.xoff[0];
+    const double* Is = B + S.ioff;
+    const int c0 = chunk * KC;
+    // stencil features: A[i][s*xc + j]
+    for (int e = tid; e < KC * xc; e += 256) {
+      const int i = e / xc, j = e - i * xc;
+      const int c = c0 + i;
+      double t[6] = {0, 0, 0, 0, 0, 0};
+      if (c < g.n) stencil6<KC>(g, coord_of(g, c), Xs, a.X.rs, Is, i, j, t);
+      double* arow = sA + i * KS + j;
+#pragma unroll
+      for (int s = 0; s < 6; ++s)
+        if (s < ns) arow[s * xc] = t[s];
+    }
+    // base rows: A[i][ns*xc + j] = U0[c][j]
+    for (int e = tid; e < KC * ra; e += 256) {
+      const int i = e / ra, j = e - i * ra;
+      sA[i * KS + ns * xc + j] = sepu ? B[S.uoff + i * a.U0.rs + j] : Xs[(i + 2) * a.X.rs + j];
+    }
+    __syncthreads();
+    for (int item = warp; item < TILES * P.ksplit; item += 8) {
+      const int tile = item % TILES, h = item / TILES;
+      const int mt = tile / NT, nt = tile - mt * NT;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      const double* pa = sA + (mt * 8 + (lane >> 2)) * KS + (lane & 3);
+      const double* pb = sB + (lane & 3) * BS + nt * 8 + (lane >> 2);
+      const int kb = h * K4s, ke = kb + K4s;
+      int k0 = kb;
+      for (; k0 + 8 <= ke; k0 += 8) {
+        dmma884(d0, d1, pa[k0], pb[k0 * BS]);
+        dmma884(e0, e1, pa[k0 + 4], pb[(k0 + 4) * BS]);
+      }
+      if (k0 < ke) dmma884(d0, d1, pa[k0], pb[k0 * BS]);
+      const int m = mt * 8 + (lane >> 2), n = nt * 8 + 2 * (lane & 3);
+      sO[(h * KC + m) * RBP + n] = d0 + e0;
+      sO[(h * KC + m) * RBP + n + 1] = d1 + e1;
+    }
+    __syncthreads();
+    const int rso = a.out.rs;
+    for (int e = tid; e < KC * rso; e += 256) {
+      const int i = e / rso, n = e - i * rso;
+      if (c0 + i < g.n) {
+        double v = 0.0;
+        if (n < r)
+          for (int h = 0; h < P.ksplit; ++h) v += sO[(h * KC + i) * RBP + n];
+        a.out.p[(long)(c0 + i) * rso + n] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int RB>
+void kstage_launch(const KStageArgs& a, const double* isp, cudaStream_t st) {
+  const Geom& g = a.geo;
+  const int ns = g.ns;
+  const int ra = a.U0.p ? a.U0.cols : 0;
+  const bool sepu = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
+  constexpr int TILES = (KC / 8) * (RB / 8);
+  KParams P;
+  P.K = ns * a.X.cols + ra;
+  P.ksplit = (TILES % 8 == 0) ? 1 : 2;
+  P.K4 = (P.K + 4 * P.ksplit - 1) / (4 * P.ksplit) * (4 * P.ksplit);
+  P.KS = pad4(P.K4);
+  P.BS = pad4(RB);
+  const Stage S = make_stage<KC>(g, &a.X, 1, sepu ? &a.U0 : nullptr);
+  const size_t smem = (2 * (size_t)S.buf + (size_t)KC * P.KS + (size_t)P.K4 * P.BS +
+                       (size_t)P.ksplit * KC * (RB + 2)) * sizeof(double) + 64;
+  if (smem > 227 * 1024) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
+  CK(cudaFuncSetAttribute(kstage_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
-  int dev = 0, sms = 148;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int blocks = (a.geo.n + 127) / 128;
-  const int cap = sms * 8;
-  if (blocks > cap) blocks = cap;
-  kstage_kernel<NB><<<blocks, 128, smem, st>>>(a);
+  const int nchunks = (g.n + KC - 1) / KC;
+  int grid = sm_count();
+  if (grid > nchunks) grid = nchunks;
+  kstage_kernel<RB><<<grid, 256, smem, st>>>(a, S, P, isp);
   launched();
 }
 
-template <int NB>
-__global__ void __launch_bounds__(128) rotate_kernel(Geom g, const double* __restrict__ X, int ldx,
-                                                     int na, const double* __restrict__ P, int ldp,
-                                                     int nb, double* __restrict__ out, int ldo) {
-  extern __shared__ double sP[];  // na x NB
-  for (int i = threadIdx.x; i < na * NB; i += blockDim.x) {
-    const int j = i / NB, k = i - j * NB;
-    sP[i] = k < nb ? P[j * ldp + k] : 0.0;
-  }
-  __syncthreads();
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += gridDim.x * blockDim.x) {
-    double acc[NB];
-#pragma unroll
-    for (int k = 0; k < NB; ++k) acc[k] = 0.0;
-    for (int j = 0; j < na; ++j) {
-      const double x = X[(size_t)j * ldx + c];
-      const double* pr = sP + j * NB;
-#pragma unroll
-      for (int k = 0; k < NB; ++k) acc[k] = fma(x, pr[k], acc[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < NB; ++k)
-      if (k < nb) out[(size_t)k * ldo + c] = acc[k];
-  }
-}
+// ===================================================================== sgram
+constexpr int GC = 16;
+constexpr int GTL = pad4(GC);  // 20
 
-template <int NB>
-__global__ void __launch_bounds__(128) scat_k1_kernel(
-    Geom g, const double* __restrict__ U0, int ldu, int ra, const double* __restrict__ S0, int r,
-    double dt, const double* __restrict__ inv_s, const int* __restrict__ cls,
-    const double* __restrict__ atomic, const double* __restrict__ psi, int ldpsi, int n_beams,
-    const double* __restrict__ rows, double* __restrict__ A, int lda) {
-  extern __shared__ double sm[];
-  double* sS = sm;                    // ra x NB
-  double* sR = sm + ra * NB;          // n_beams x 12 x NB
-  for (int i = threadIdx.x; i < ra * NB; i += blockDim.x) {
-    const int j = i / NB, k = i - j * NB;
-    sS[i] = k < r ? S0[j * r + k] : 0.0;
+template <int T8>
+__global__ void __launch_bounds__(256, 1)
+    sgram_kernel(Geom g, NMat X1, NMat X2, Stage S, const double* __restrict__ isp,
+                 double* __restrict__ partial) {
+  constexpr int W = T8 * 8;
+  constexpr int TILES = 6 * T8 * T8;
+  constexpr int TPW = (TILES + 7) / 8;
+  extern __shared__ __align__(128) double sm[];
+  double* buf = sm;
+  double* sT = sm + 2 * S.buf;                 // [6][W][GTL]
+  uint64_t* bar = (uint64_t*)(sT + 6 * W * GTL);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ns = g.ns, a1 = X1.cols, a2 = X2.p ? X2.cols : 0, w = a1 + a2;
+  const int nin = X2.p ? 2 : 1;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
   }
-  for (int i = threadIdx.x; i < n_beams * 12 * NB; i += blockDim.x) {
-    const int bi = i / NB, k = i - bi * NB;
-    sR[i] = k < r ? rows[bi * r + k] : 0.0;
-  }
+  for (int i = tid; i < 6 * W * GTL; i += 256) sT[i] = 0.0;
   __syncthreads();
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += gridDim.x * blockDim.x) {
-    double acc[NB], src[NB];
+  double acc[TPW][2];
 #pragma unroll
-    for (int k = 0; k < NB; ++k) acc[k] = src[k] = 0.0;
-    for (int j = 0; j < ra; ++j) {
-      const double u = U0[(size_t)j * ldu + c];
-      A[(size_t)(r + j) * lda + c] = u;
-      const double* srow = sS + j * NB;
-#pragma unroll
-      for (int k = 0; k < NB; ++k) acc[k] = fma(u, srow[k], acc[k]);
+  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int nchunks = (g.n + GC - 1) / GC;
+  if (tid == 0 && blockIdx.x < nchunks)
+    stage_chunk<GC>(S, buf, &bar[0], blockIdx.x * GC, X1, X2, nin, isp, X1);
+  int it = 0;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+    const int b = it & 1;
+    const int next = chunk + gridDim.x;
+    if (tid == 0 && next < nchunks) {
+      fence_proxy_async();
+      stage_chunk<GC>(S, buf + (b ^ 1) * S.buf, &bar[b ^ 1], next * GC, X1, X2, nin, isp, X1);
     }
-    // source rows: sum_b sum_i (N_i S^-1 psi_b)(c) * rows_b[i]  (dlra.py:244-251)
-    const double is = inv_s[c];
-    const int kc = cls[c];
-    for (int b = 0; b < n_beams; ++b) {
-      const double sp = is * psi[(size_t)b * ldpsi + c];
-      for (int i = 0; i < 12; ++i) {
-        const double x = atomic[kc * 12 + i] * sp;
-        const double* rr = sR + (b * 12 + i) * NB;
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const double* B = buf + b * S.buf;
+    const double* Is = B + S.ioff;
+    const int c0 = chunk * GC;
+    for (int e = tid; e < GC * w; e += 256) {
+      const int i = e / w, j = e - i * w;
+      const int c = c0 + i;
+      double t[6] = {0, 0, 0, 0, 0, 0};
+      if (c < g.n) {
+        const CellCoord cc = coord_of(g, c);
+        if (j < a1) stencil6<GC>(g, cc, B + S.xoff[0], X1.rs, Is, i, j, t);
+        else stencil6<GC>(g, cc, B + S.xoff[1], X2.rs, Is, i, j - a1, t);
+      }
 #pragma unroll
-        for (int k = 0; k < NB; ++k) src[k] = fma(x, rr[k], src[k]);
+      for (int s = 0; s < 6; ++s)
+        if (s < ns) sT[(s * W + j) * GTL + i] = t[s];
+    }
+    __syncthreads();
+    // A = X^T from the centre rows (box 0 rows 2..GC+1); B = T_s
+    const int m0 = lane >> 2, kq = lane & 3;
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) {
+      const int tile = warp + 8 * t;
+      if (tile < TILES) {
+        const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
+        const int ti = rem / T8, tj = rem - ti * T8;
+        if (s < ns) {
+          const int m = ti * 8 + m0;
+          const double* pa;
+          int ars;
+          if (m < a1) { pa = B + S.xoff[0] + 2 * X1.rs + m; ars = X1.rs; }
+          else if (m < w) { pa = B + S.xoff[1] + 2 * X2.rs + (m - a1); ars = X2.rs; }
+          else { pa = nullptr; ars = 0; }
+          const double* pb = sT + (s * W + tj * 8 + m0) * GTL + kq;
+#pragma unroll
+          for (int k0 = 0; k0 < GC; k0 += 4)
+            dmma884(acc[t][0], acc[t][1], pa ? pa[(k0 + kq) * ars] : 0.0, pb[k0]);
+        }
       }
     }
+    __syncthreads();
+  }
+  double* out = partial + (size_t)blockIdx.x * ns * w * w;
 #pragma unroll
-    for (int k = 0; k < NB; ++k)
-      if (k < r) A[(size_t)k * lda + c] = acc[k] + dt * src[k];
+  for (int t = 0; t < TPW; ++t) {
+    const int tile = warp + 8 * t;
+    if (tile < TILES) {
+      const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
+      const int ti = rem / T8, tj = rem - ti * T8;
+      const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
+      if (s < ns && row < w) {
+        double* o = out + ((size_t)s * w + row) * w;
+        if (col < w) o[col] = acc[t][0];
+        if (col + 1 < w) o[col + 1] = acc[t][1];
+      }
+    }
   }
 }
 
-__global__ void dose_kernel(Geom g, const double* __restrict__ U, int ldu,
-                            const double* __restrict__ coef, int r, double half_dt,
+__global__ void reduce_blocks(const double* __restrict__ partial, int nblk, int count,
+                              double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
+  out[i] = s;
+}
+
+template <int T8>
+void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
+                  cudaStream_t st) {
+  const NMat ins[2] = {X1, X2};
+  const Stage S = make_stage<GC>(g, ins, X2.p ? 2 : 1, nullptr);
+  const int W = T8 * 8;
+  const size_t smem = (2 * (size_t)S.buf + (size_t)6 * W * GTL) * sizeof(double) + 64;
+  if (smem > 227 * 1024) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
+  CK(cudaFuncSetAttribute(sgram_kernel<T8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  const int nchunks = (g.n + GC - 1) / GC;
+  int grid = sm_count();
+  if (grid > nchunks) grid = nchunks;
+  const int w = X1.cols + (X2.p ? X2.cols : 0);
+  const size_t count = (size_t)g.ns * w * w;
+  double* part = partial.get(count * grid);
+  sgram_kernel<T8><<<grid, 256, smem, st>>>(g, X1, X2, S, isp, part);
+  launched();
+  reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
+  launched();
+}
+
+// ===================================================================== lincomb
+constexpr int LC = 64;
+
+template <int NB8>
+__global__ void __launch_bounds__(256)
+    lincomb_kernel(Geom g, NMat Y1, NMat Y2, NMat X, const double* __restrict__ TA,
+                   const double* __restrict__ TB, NMat out, int K4, int KS, int BS, int TS,
+                   int grams, double* __restrict__ partial) {
+  constexpr int OT = (LC / 8) * NB8;
+  constexpr int GT = 2 * NB8 * NB8;        // X^T T (x <= 8 NB8 rows) and T^T T
+  constexpr int GPW = (GT + 7) / 8;
+  extern __shared__ __align__(128) double sm[];
+  double* sA = sm;                         // [LC][KS]  rows [Y1 | Y2 | X]
+  double* sB = sA + LC * KS;               // [K4][BS]
+  double* sT = sB + K4 * BS;               // [LC][TS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int y1 = Y1.cols, y2 = Y2.p ? Y2.cols : 0, xcn = X.p ? X.cols : 0;
+  const int ny = y1 + y2, K = ny + xcn, nb = out.cols;
+  for (int i = tid; i < K4 * BS; i += 256) {
+    const int k = i / BS, n = i - k * BS;
+    double v = 0.0;
+    if (n < nb && k < K) v = k < ny ? TA[k * nb + n] : -TB[(k - ny) * nb + n];
+    sB[i] = v;
+  }
+  for (int i = tid; i < LC * KS; i += 256) sA[i] = 0.0;
+  for (int i = tid; i < LC * TS; i += 256) sT[i] = 0.0;
+  double gacc[GPW][2];
+#pragma unroll
+  for (int t = 0; t < GPW; ++t) gacc[t][0] = gacc[t][1] = 0.0;
+  const int nchunks = (g.n + LC - 1) / LC;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    const int c0 = chunk * LC;
+    const int rows = g.n - c0 < LC ? g.n - c0 : LC;
+    __syncthreads();
+    for (int e = tid; e < LC * y1; e += 256) {
+      const int i = e / y1, j = e - i * y1;
+      sA[i * KS + j] = i < rows ? Y1.p[(long)(c0 + i) * Y1.rs + j] : 0.0;
+    }
+    for (int e = tid; e < LC * y2; e += 256) {
+      const int i = e / y2, j = e - i * y2;
+      sA[i * KS + y1 + j] = i < rows ? Y2.p[(long)(c0 + i) * Y2.rs + j] : 0.0;
+    }
+    for (int e = tid; e < LC * xcn; e += 256) {
+      const int i = e / xcn, j = e - i * xcn;
+      sA[i * KS + ny + j] = i < rows ? X.p[(long)(c0 + i) * X.rs + j] : 0.0;
+    }
+    __syncthreads();
+    for (int tile = warp; tile < OT; tile += 8) {
+      const int mt = tile / NB8, nt = tile - mt * NB8;
+      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+      const double* pa = sA + (mt * 8 + (lane >> 2)) * KS + (lane & 3);
+      const double* pb = sB + (lane & 3) * BS + nt * 8 + (lane >> 2);
+      int k0 = 0;
+      for (; k0 + 8 <= K4; k0 += 8) {
+        dmma884(d0, d1, pa[k0], pb[k0 * BS]);
+        dmma884(e0, e1, pa[k0 + 4], pb[(k0 + 4) * BS]);
+      }
+      if (k0 < K4) dmma884(d0, d1, pa[k0], pb[k0 * BS]);
+      const int m = mt * 8 + (lane >> 2), n = nt * 8 + 2 * (lane & 3);
+      sT[m * TS + n] = d0 + e0;
+      sT[m * TS + n + 1] = d1 + e1;
+    }
+    __syncthreads();
+    if (out.p) {
+      const int rso = out.rs;
+      for (int e = tid; e < rows * rso; e += 256) {
+        const int i = e / rso, n = e - i * rso;
+        out.p[(long)(c0 + i) * rso + n] = n < nb ? sT[i * TS + n] : 0.0;
+      }
+    }
+    if (grams) {
+#pragma unroll
+      for (int t = 0; t < GPW; ++t) {
+        const int tile = warp + 8 * t;
+        if (tile < GT) {
+          const bool xg = tile < NB8 * NB8;
+          const int tt = xg ? tile : tile - NB8 * NB8;
+          const int ti = tt / NB8, tj = tt - ti * NB8;
+          const int m = ti * 8 + (lane >> 2), kq = lane & 3;
+          const bool mv = xg ? m < xcn : true;
+          const double* pa = xg ? sA + ny + m : sT + m;
+          const int sa = xg ? KS : TS;
+          const double* pb = sT + tj * 8 + (lane >> 2);
+          if (!xg || ti * 8 < xcn) {
+#pragma unroll 4
+            for (int k0 = 0; k0 < LC; k0 += 4)
+              dmma884(gacc[t][0], gacc[t][1], mv ? pa[(k0 + kq) * sa] : 0.0, pb[(k0 + kq) * TS]);
+          }
+        }
+      }
+    }
+  }
+  if (grams) {
+    double* o = partial + (size_t)blockIdx.x * (xcn + nb) * nb;
+#pragma unroll
+    for (int t = 0; t < GPW; ++t) {
+      const int tile = warp + 8 * t;
+      if (tile < GT) {
+        const bool xg = tile < NB8 * NB8;
+        const int tt = xg ? tile : tile - NB8 * NB8;
+        const int ti = tt / NB8, tj = tt - ti * NB8;
+        const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
+        const int nrow = xg ? xcn : nb;
+        const size_t off = xg ? 0 : (size_t)xcn * nb;
+        if (row < nrow) {
+          if (col < nb) o[off + (size_t)row * nb + col] = gacc[t][0];
+          if (col + 1 < nb) o[off + (size_t)row * nb + col + 1] = gacc[t][1];
+        }
+      }
+    }
+  }
+}
+
+template <class Kern>
+int resident(Kern k, int threads, size_t smem) {
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, threads, smem));
+  return nb < 1 ? 1 : nb;
+}
+
+template <int NB8>
+void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
+                    NMat out, double* grams, DBuf& partial, cudaStream_t st) {
+  const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
+  const int K4 = (K + 3) / 4 * 4;
+  const int KS = pad4(K4), BS = pad4(NB8 * 8), TS = pad4(NB8 * 8);
+  const size_t smem = ((size_t)LC * KS + (size_t)K4 * BS + (size_t)LC * TS) * sizeof(double);
+  CK(cudaFuncSetAttribute(lincomb_kernel<NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  const int nchunks = (g.n + LC - 1) / LC;
+  int grid = sm_count() * resident(lincomb_kernel<NB8>, 256, smem);
+  if (grid > nchunks) grid = nchunks;
+  const int xcn = X.p ? X.cols : 0;
+  const size_t count = (size_t)(xcn + out.cols) * out.cols;
+  double* part = grams ? partial.get(count * grid) : nullptr;
+  lincomb_kernel<NB8><<<grid, 256, smem, st>>>(g, Y1, Y2, X, TA, TB, out, K4, KS, BS, TS,
+                                               grams ? 1 : 0, part);
+  launched();
+  if (grams) {
+    reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
+    launched();
+  }
+}
+
+// ===================================================================== pgram
+constexpr int PC = 64;
+
+template <int T8, int NPH>
+__global__ void __launch_bounds__(256) pgram_kernel(PGramArgs a, int LS,
+                                                    double* __restrict__ partial) {
+  constexpr int W = T8 * 8;
+  constexpr int NT = T8 * T8;
+  constexpr int TPW = (NT + 7) / 8;
+  extern __shared__ __align__(128) double sm[];
+  double* sX = sm;             // [PC][LS]
+  double* sT = sX + PC * LS;   // [PC][LS]
+  const Geom& g = a.geo;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int na = a.X.cols, nb = a.nb;
+  for (int i = tid; i < 2 * PC * LS; i += 256) sm[i] = 0.0;
+  double acc[NPH][TPW][2];
+#pragma unroll
+  for (int p = 0; p < NPH; ++p)
+#pragma unroll
+    for (int t = 0; t < TPW; ++t) acc[p][t][0] = acc[p][t][1] = 0.0;
+  const int nchunks = (g.n + PC - 1) / PC;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
+    const int c0 = chunk * PC;
+    const int rows = g.n - c0 < PC ? g.n - c0 : PC;
+    __syncthreads();
+    for (int e = tid; e < PC * na; e += 256) {
+      const int i = e / na, j = e - i * na;
+      sX[i * LS + j] = i < rows ? a.X.p[(long)(c0 + i) * a.X.rs + j] : 0.0;
+    }
+#pragma unroll
+    for (int p = 0; p < NPH; ++p) {
+      if (p < a.nphase) {
+        if (p > 0) __syncthreads();
+        for (int e = tid; e < PC * nb; e += 256) {
+          const int i = e / nb, j = e - i * nb;
+          double v = 0.0;
+          if (i < rows) {
+            const int c = c0 + i;
+            if (a.gen == PG_PLAIN) {
+              v = a.Y.p[(long)c * a.Y.rs + j];
+            } else if (a.gen == PG_WEIGHT) {
+              const int k = a.cls[c];
+              const double w = a.wmode == 0 ? (k == p ? a.inv_s[c] : 0.0)
+                                            : a.wtab[k * 12 + p] * a.inv_s[c];
+              v = w * a.Y.p[(long)c * a.Y.rs + j];
+            } else {
+              const int beam = j / 12, el = j - beam * 12;
+              v = a.wtab[a.cls[c] * 12 + el] * (a.inv_s[c] * a.psi[(size_t)beam * a.ld + c]);
+            }
+          }
+          sT[i * LS + j] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          const int tile = warp + 8 * t;
+          if (tile < NT) {
+            const int ti = tile / T8, tj = tile - ti * T8;
+            const double* xa = sX + (lane & 3) * LS + ti * 8 + (lane >> 2);
+            const double* tb = sT + (lane & 3) * LS + tj * 8 + (lane >> 2);
+#pragma unroll 4
+            for (int k0 = 0; k0 < PC; k0 += 4)
+              dmma884(acc[p][t][0], acc[p][t][1], xa[k0 * LS], tb[k0 * LS]);
+          }
+        }
+      }
+    }
+  }
+  double* out = partial + (size_t)blockIdx.x * a.nphase * na * nb;
+#pragma unroll
+  for (int p = 0; p < NPH; ++p) {
+    if (p < a.nphase) {
+#pragma unroll
+      for (int t = 0; t < TPW; ++t) {
+        const int tile = warp + 8 * t;
+        if (tile < NT) {
+          const int ti = tile / T8, tj = tile - ti * T8;
+          const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
+          if (row < na) {
+            double* o = out + ((size_t)p * na + row) * nb;
+            if (col < nb) o[col] = acc[p][t][0];
+            if (col + 1 < nb) o[col + 1] = acc[p][t][1];
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int T8, int NPH>
+void pgram_launch(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
+  const int LS = pad4(T8 * 8);
+  const size_t smem = 2 * (size_t)PC * LS * sizeof(double);
+  CK(cudaFuncSetAttribute(pgram_kernel<T8, NPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  const int nchunks = (a.geo.n + PC - 1) / PC;
+  int grid = sm_count() * resident(pgram_kernel<T8, NPH>, 256, smem);
+  if (grid > nchunks) grid = nchunks;
+  const size_t count = (size_t)a.nphase * a.X.cols * a.nb;
+  double* part = partial.get(count * grid);
+  pgram_kernel<T8, NPH><<<grid, 256, smem, st>>>(a, LS, part);
+  launched();
+  reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, a.out);
+  launched();
+}
+
+// ===================================================================== small kernels
+__global__ void scat_dk_kernel(Geom g, double dt, const double* __restrict__ inv_s,
+                               const int* __restrict__ cls, const double* __restrict__ atomic,
+                               const double* __restrict__ psi, int n_beams,
+                               const double* __restrict__ rows, NMat out) {
+  extern __shared__ double sR[];  // n_beams x 12 x r
+  const int r = out.cols, rs = out.rs;
+  for (int i = threadIdx.x; i < n_beams * 12 * r; i += blockDim.x) sR[i] = rows[i];
+  __syncthreads();
+  const long total = (long)g.n * rs;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / rs), j = (int)(e - (long)c * rs);
+    double v = 0.0;
+    if (j < r) {
+      const int kc = cls[c];
+      const double is = inv_s[c];
+      for (int b = 0; b < n_beams; ++b) {
+        const double sp = is * psi[(size_t)b * g.ld + c];
+        double s = 0.0;
+        for (int i = 0; i < 12; ++i) s = fma(atomic[kc * 12 + i], sR[(b * 12 + i) * r + j], s);
+        v = fma(sp, s, v);
+      }
+      v *= dt;
+    }
+    out.p[e] = v;
+  }
+}
+
+__global__ void dose_kernel(Geom g, NMat U, const double* __restrict__ coef, double half_dt,
                             const double* __restrict__ s_field, const double* __restrict__ psi,
-                            int ldpsi, int n_beams, double* __restrict__ dep,
-                            double* __restrict__ prev) {
+                            int n_beams, double* __restrict__ dep, double* __restrict__ prev) {
   const double sqrt4pi = 3.5449077018110318;  // sqrt(4 pi), driver.py:59
+  __shared__ double sc[64];
+  for (int i = threadIdx.x; i < U.cols; i += blockDim.x) sc[i] = coef[i];
+  __syncthreads();
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < g.n; c += gridDim.x * blockDim.x) {
     double u0 = 0.0;
-    for (int j = 0; j < r; ++j) u0 = fma(U[(size_t)j * ldu + c], coef[j], u0);
+    const double* row = U.p + (long)c * U.rs;
+    for (int j = 0; j < U.cols; ++j) u0 = fma(row[j], sc[j], u0);
     double integrand = sqrt4pi * u0;
     if (psi) {
       double ps = 0.0;
-      for (int b = 0; b < n_beams; ++b) ps += psi[(size_t)b * ldpsi + c];
+      for (int b = 0; b < n_beams; ++b) ps += psi[(size_t)b * g.ld + c];
       integrand = integrand + s_field[c] * ps;
     }
     dep[c] += half_dt * (prev[c] + integrand);
     prev[c] = integrand;
+  }
+}
+
+__global__ void unit_rows_kernel(Geom g, NMat U) {
+  const long total = (long)g.n * U.rs;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / U.rs), j = (int)(e - (long)c * U.rs);
+    U.p[e] = (j < U.cols && c == j) ? 1.0 : 0.0;
+  }
+}
+
+__device__ __forceinline__ double hash_normal(unsigned long long x) {
+  double s = 0.0;
+  for (int i = 0; i < 4; ++i) {
+    x += 0x9E3779B97F4A7C15ULL;
+    unsigned long long z = x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    s += (double)(z >> 11) * (1.0 / 9007199254740992.0);
+  }
+  return (s - 2.0) * 1.7320508075688772;
+}
+
+__global__ void random_rows_kernel(Geom g, NMat U, unsigned long long seed) {
+  const long total = (long)g.n * U.rs;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(e / U.rs), j = (int)(e - (long)c * U.rs);
+    U.p[e] = j < U.cols ? hash_normal(seed * 0x100000001B3ULL + (unsigned long long)e) : 0.0;
   }
 }
 
@@ -238,7 +782,6 @@ __global__ void lerp_kernel(const double* __restrict__ v, int ldv, int n, int j0
   }
 }
 
-// row-major (n x c) host layout <-> column-major (ld) device layout
 __global__ void tin_kernel(const double* __restrict__ src, int n, int cdim, double* __restrict__ dst,
                            int ldd) {
   __shared__ double tile[32][33];
@@ -275,95 +818,128 @@ __global__ void zero_kernel(double* p, size_t count) {
     p[i] = 0.0;
 }
 
-int grid_for(int n, int block) {
-  int b = (n + block - 1) / block;
+int grid_for(long n, int block) {
+  long b = (n + block - 1) / block;
   if (b > 148 * 16) b = 148 * 16;
-  return b < 1 ? 1 : b;
+  return b < 1 ? 1 : (int)b;
 }
 
 }  // namespace
 
+void kstage(const KStageArgs& a, cudaStream_t st) {
+  // a.inv_s must point at the padded [1/S, 0] row array (Handle::isp)
+  const int r = a.out.cols;
+  if (a.X.cols > 32 || (a.U0.p && a.U0.cols > 32)) fail(PND_ECONFIG, "kstage supports <= 32 input columns");
+  if (r <= 8) kstage_launch<8>(a, a.inv_s, st);
+  else if (r <= 16) kstage_launch<16>(a, a.inv_s, st);
+  else if (r <= 24) kstage_launch<24>(a, a.inv_s, st);
+  else if (r <= 32) kstage_launch<32>(a, a.inv_s, st);
+  else if (r <= 64) kstage_launch<64>(a, a.inv_s, st);
+  else fail(PND_ECONFIG, "kstage supports at most 64 output columns");
+}
 
-template <int NB>
-static void rotate_launch(const Geom& g, const double* X, int ldx, int a, const double* P,
-                          int ldp, int b, double* out, int ldo, cudaStream_t st) {
-  const size_t smem = (size_t)a * NB * sizeof(double);
-  CK(cudaFuncSetAttribute(rotate_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  rotate_kernel<NB><<<grid_for(g.n, 128), 128, smem, st>>>(g, X, ldx, a, P, ldp, b, out, ldo);
+void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* isp, double* out,
+                   DBuf& partial, cudaStream_t st) {
+  if (g.ns == 0) return;
+  const int w = X1.cols + (X2.p ? X2.cols : 0);
+  switch ((w + 7) / 8) {
+    case 1: sgram_launch<1>(g, X1, X2, isp, out, partial, st); break;
+    case 2: sgram_launch<2>(g, X1, X2, isp, out, partial, st); break;
+    case 3: sgram_launch<3>(g, X1, X2, isp, out, partial, st); break;
+    case 4: sgram_launch<4>(g, X1, X2, isp, out, partial, st); break;
+    case 5: sgram_launch<5>(g, X1, X2, isp, out, partial, st); break;
+    case 6: sgram_launch<6>(g, X1, X2, isp, out, partial, st); break;
+    default: fail(PND_ECONFIG, "stencil Grams support at most 48 columns");
+  }
+}
+
+void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* isp, double* out,
+                      DBuf& partial, cudaStream_t st) {
+  // Grams of [Y | X] against its stencils, then the (X, D Y) block
+  const int a = X.cols, b = Y.cols, w = a + b;
+  DBuf full;
+  double* f = full.get((size_t)g.ns * w * w);
+  stencil_grams(g, Y, X, isp, f, partial, st);
+  for (int s = 0; s < g.ns; ++s) {
+    // out[s] = f[s][b:, :b]
+    CK(cudaMemcpy2DAsync(out + (size_t)s * a * b, b * sizeof(double),
+                         f + (size_t)s * w * w + (size_t)b * w, w * sizeof(double),
+                         b * sizeof(double), a, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  full.free_();
+}
+
+void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
+             NMat out, double* grams, DBuf& partial, cudaStream_t st) {
+  const int w = out.cols > (X.p ? X.cols : 0) ? out.cols : X.cols;
+  const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
+  if (K > 128) fail(PND_ECONFIG, "lincomb supports at most 128 input columns");
+  switch ((w + 7) / 8) {
+    case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 3: lincomb_launch<3>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 4: lincomb_launch<4>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 5: lincomb_launch<5>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 6: lincomb_launch<6>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 7:
+    case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    default: fail(PND_ECONFIG, "lincomb supports at most 64 output columns");
+  }
+}
+
+void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
+  const int w = a.X.cols > a.nb ? a.X.cols : a.nb;
+  const int t = (w + 7) / 8;
+  if (a.X.cols <= 0 || a.nb <= 0 || a.nphase <= 0) return;
+  if (a.nphase > 1) {
+    if (a.nphase > 12 || t > 4) fail(PND_ECONFIG, "weighted Grams support 12 phases, rank <= 32");
+    switch (t) {
+      case 1: pgram_launch<1, 12>(a, partial, st); break;
+      case 2: pgram_launch<2, 12>(a, partial, st); break;
+      case 3: pgram_launch<3, 12>(a, partial, st); break;
+      default: pgram_launch<4, 12>(a, partial, st); break;
+    }
+    return;
+  }
+  switch (t) {
+    case 1: pgram_launch<1, 1>(a, partial, st); break;
+    case 2: pgram_launch<2, 1>(a, partial, st); break;
+    case 3: pgram_launch<3, 1>(a, partial, st); break;
+    case 4: pgram_launch<4, 1>(a, partial, st); break;
+    case 5: pgram_launch<5, 1>(a, partial, st); break;
+    case 6: pgram_launch<6, 1>(a, partial, st); break;
+    case 7:
+    case 8: pgram_launch<8, 1>(a, partial, st); break;
+    default: fail(PND_ECONFIG, "Grams support at most 64 columns");
+  }
+}
+
+void scat_dk(const Geom& g, double dt, const double* inv_s, const int* cls,
+             const double* cls_atomic, const double* psi, int n_beams, const double* rows,
+             NMat out, cudaStream_t st) {
+  const size_t smem = (size_t)(n_beams > 0 ? n_beams : 1) * 12 * out.cols * sizeof(double);
+  scat_dk_kernel<<<grid_for((long)g.n * out.rs, 256), 256, smem, st>>>(
+      g, dt, inv_s, cls, cls_atomic, psi, n_beams, rows, out);
   launched();
 }
 
-void rotate_ld(const Geom& g, const double* X, int ldx, int a, const double* P, int ldp, int b,
-               double* out, int ldo, cudaStream_t st) {
-  if (b <= 0) return;
-  if (b <= 8) rotate_launch<8>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else if (b <= 16) rotate_launch<16>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else if (b <= 24) rotate_launch<24>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else if (b <= 32) rotate_launch<32>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else if (b <= 48) rotate_launch<48>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else if (b <= 64) rotate_launch<64>(g, X, ldx, a, P, ldp, b, out, ldo, st);
-  else fail(PND_ECONFIG, "rotate supports at most 64 output columns");
-}
-
-void rotate(const Geom& g, const double* X, int ldx, int a, const double* P, int b, double* out,
-            int ldo, cudaStream_t st) {
-  rotate_ld(g, X, ldx, a, P, b, b, out, ldo, st);
-}
-
-template <int NB>
-static void scat_k1_launch(const Geom& g, const double* U0, int ldu, int ra, const double* S0,
-                           int r, double dt, const double* inv_s, const int* cls,
-                           const double* atomic, const double* psi, int ldpsi, int n_beams,
-                           const double* rows, double* A, int lda, cudaStream_t st) {
-  const size_t smem = ((size_t)ra * NB + (size_t)n_beams * 12 * NB) * sizeof(double);
-  CK(cudaFuncSetAttribute(scat_k1_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  scat_k1_kernel<NB><<<grid_for(g.n, 128), 128, smem, st>>>(g, U0, ldu, ra, S0, r, dt, inv_s,
-                                                            cls, atomic, psi, ldpsi, n_beams,
-                                                            rows, A, lda);
+void dose_accumulate(const Geom& g, NMat U, const double* coef, double half_dt,
+                     const double* s_field, const double* psi, int n_beams, double* deposited,
+                     double* prev, cudaStream_t st) {
+  if (U.cols > 64) fail(PND_ECONFIG, "dose supports rank <= 64");
+  dose_kernel<<<grid_for(g.n, 256), 256, 0, st>>>(g, U, coef, half_dt, s_field, psi, n_beams,
+                                                   deposited, prev);
   launched();
 }
 
-void scat_k1(const Geom& g, const double* U0, int ldu, int ra, const double* S0, int r, double dt,
-             const double* inv_s, const int* cls, const double* cls_atomic, const double* psi,
-             int ldpsi, int n_beams, const double* rows, double* A, int lda, cudaStream_t st) {
-#define PND_K1(NBV) scat_k1_launch<NBV>(g, U0, ldu, ra, S0, r, dt, inv_s, cls, cls_atomic, psi, \
-                                        ldpsi, n_beams, rows, A, lda, st)
-  if (r <= 8) PND_K1(8);
-  else if (r <= 16) PND_K1(16);
-  else if (r <= 24) PND_K1(24);
-  else if (r <= 32) PND_K1(32);
-  else if (r <= 48) PND_K1(48);
-  else if (r <= 64) PND_K1(64);
-  else fail(PND_ECONFIG, "scattering K-step supports rank <= 64");
-#undef PND_K1
+void unit_rows(const Geom& g, NMat U, cudaStream_t st) {
+  unit_rows_kernel<<<grid_for((long)g.n * U.rs, 256), 256, 0, st>>>(g, U);
+  launched();
 }
 
-void apply_streaming_full(const Geom& g, const double* U, int ldu, int m, const double* inv_s,
-                          const double* Mneg, double*, double* out, int ldo, cudaStream_t st) {
-  KStageArgs a{};
-  a.geo = g;
-  a.X = U;
-  a.ldx = ldu;
-  a.xc = m;
-  a.ra = 0;
-  a.U0 = nullptr;
-  a.S0 = nullptr;
-  a.M = Mneg;
-  a.inv_s = inv_s;
-  a.r = m;
-  a.out = out;
-  a.ldo = ldo;
-  a.copy_u = nullptr;
-  kstage(a, st);
-}
-
-void dose_accumulate(const Geom& g, const double* U, int ldu, const double* coef, int r,
-                     double half_dt, const double* s_field, const double* psi, int ldpsi,
-                     int n_beams, double* deposited, double* prev, cudaStream_t st) {
-  dose_kernel<<<grid_for(g.n, 256), 256, 0, st>>>(g, U, ldu, coef, r, half_dt, s_field, psi,
-                                                   ldpsi, n_beams, deposited, prev);
+void random_rows(const Geom& g, NMat U, unsigned long long seed, cudaStream_t st) {
+  random_rows_kernel<<<grid_for((long)g.n * U.rs, 256), 256, 0, st>>>(g, U, seed);
   launched();
 }
 
@@ -399,6 +975,23 @@ void fill_zero(double* p, size_t count, cudaStream_t st) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   zero_kernel<<<(int)blocks, 256, 0, st>>>(p, count);
   launched();
+}
+
+NMat NBuf::view(const Geom& g, int cols, cudaStream_t st) {
+  const int nrs = even(cols > 0 ? cols : 1);
+  const size_t total = (size_t)(g.n + 2 * g.halo) * nrs;
+  if (d.cap < total || nrs != rs) {
+    d.get(total > d.cap ? total : d.cap);
+    // halo rows (and the whole buffer, once) are zero for the new stride
+    fill_zero(d.p, (size_t)g.halo * nrs, st);
+    fill_zero(d.p + (size_t)(g.halo + g.n) * nrs, (size_t)g.halo * nrs, st);
+    rs = nrs;
+  }
+  NMat m;
+  m.p = d.p + (size_t)g.halo * rs;
+  m.rs = rs;
+  m.cols = cols;
+  return m;
 }
 
 }  // namespace pnd

@@ -1,10 +1,12 @@
-// Internal header of libpndose_b200: handle, error plumbing, kernel entry
-// points. The public C-ABI is include/pndose_b200.h.
+// Internal header of libpndose_b200: errors, geometry, device buffers, kernel
+// entry points. The public C-ABI is include/pndose_b200.h.
 //
 // Device layout:
-//   * n-side matrices (U, K, W, U^, TSQR workspace) are column-major with a
-//     padded leading dimension `ld` (multiple of 32 doubles = 256 B), so a
-//     warp's 32 consecutive cells of one column are one 256-byte segment;
+//   * n-side matrices (U0, the augmentation Q, the K-stage iterates, dK) are
+//     CELL-MAJOR: row c holds the r coefficients of cell c contiguously, with
+//     an even row stride rs (16-byte aligned rows). H zero rows precede row 0
+//     and follow row n-1, so every stencil halo segment [c0 + off, c0 + off + CH)
+//     is one contiguous, in-bounds block that a single cp.async.bulk copies;
 //   * small and m-side matrices (S, Grams, V, A_d^+-) are dense row-major,
 //     exactly the numpy C-order the Python boundary passes in.
 #pragma once
@@ -36,29 +38,27 @@ void check_cuda(cudaError_t e, const char* what);
 // after every kernel launch: surface launch errors, count the launch
 void launched();
 long long launch_count();
+int sm_count();
 
 // ------------------------------------------------------------ geometry
 struct Geom {
   int nx, ny, nz;
   int n;          // cells
-  int ld;         // padded leading dimension of n-side matrices
+  int ld;         // padded length of per-cell vectors (inv_s, psi, dose)
+  int halo;       // zero rows before/after every n-side matrix
   double h[3];
   double ih[3];   // 1/h   (the stencil coefficients, no FP64 division in kernels)
   double i2h[3];  // 1/(2h)
   int na;         // number of active axes
-  int axis[3];    // active axis ids in x, y, z order
+  int axis[3];    // active axis ids in x, y, z order (the first has stride 1)
   int ns;         // number of stencils = 2 * na (order: axis-major, + then -)
 };
-
-// stencil s -> (axis, plus)
-__host__ __device__ inline int stencil_axis(const Geom& g, int s) { return g.axis[s >> 1]; }
-__host__ __device__ inline bool stencil_plus(int s) { return (s & 1) == 0; }
 
 // ------------------------------------------------------------ device buffers
 struct DBuf {
   double* p = nullptr;
   size_t cap = 0;  // doubles
-  double* get(size_t count);  // grow-only allocation
+  double* get(size_t count);  // grow-only allocation (contents not preserved)
   void free_();
 };
 
@@ -69,78 +69,91 @@ struct IBuf {
   void free_();
 };
 
-// ------------------------------------------------------------ kernels API
-// Gram engine (gram.cu): out[g][a][b] = sum_c X[c][a] * T_g[c][b]
-enum GramGen { GEN_STENCIL = 0, GEN_WEIGHT = 1, GEN_SOURCE = 2, GEN_PLAIN = 3, GEN_LINCOMB = 4 };
-
-struct GramArgs {
-  Geom geo;
-  const double* X; int ldx; int na;          // n x na col-major
-  const double* Y; int ldy; int nb;          // n x nb col-major (stencil/weight/plain)
-  int nphase;                                // number of Grams produced
-  int gen;
-  const double* inv_s;                       // (n)
-  // weight generator: phase k uses w_k(c)
-  const int* cls; const double* wtab; int n_cls; int wmode;  // see gram.cu
-  // source generator: T[c][b] = N[cls][b%12] * inv_s[c] * psi[b/12][c]
-  const double* psi; int ldpsi; int n_beams;
-  // lincomb generator: T = Y TA - X TB (TA: ny x nb, TB: na x nb, row-major),
-  // written to Yout (ld = ldo) when non-null; Y has ny columns
-  int ny; const double* TA; const double* TB; double* Yout; int ldo;
-  int self_phase;                            // phase whose A operand is T (-1: none)
-  double* out;                               // per phase rows x nb (row-major), phases
-                                             // concatenated; rows = nb for self_phase
+// cell-major n-side matrix view: element (cell c, column j) at p[c * rs + j]
+struct NMat {
+  double* p = nullptr;
+  int rs = 0;
+  int cols = 0;
 };
-void gram(GramArgs a, DBuf& partial, cudaStream_t st);
-// engine.cu: DMMA chunk kernels behind gram() for GEN_STENCIL and GEN_LINCOMB
-void stencil_grams(const GramArgs& a, DBuf& partial, cudaStream_t st);
-void lincomb(const GramArgs& a, DBuf& partial, bool grams, cudaStream_t st);
 
-// n-side streaming kernels (nside.cu)
+// owner of one n-side matrix buffer (halo rows kept zero for the current rs)
+struct NBuf {
+  DBuf d;
+  int rs = -1;
+  // a view with `cols` columns (rs = cols rounded up to even); the contents
+  // survive when the stride does not change
+  NMat view(const Geom& g, int cols, cudaStream_t st);
+};
+
+inline int even(int c) { return (c + 1) & ~1; }
+
+// ------------------------------------------------------------ n-side kernels (nside.cu)
+// K-phase Horner stage / full-rank streaming operator:
+//   out = [D_0 S^-1 X, ..., D_ns-1 S^-1 X | U0] . [M_0; ...; M_ns-1; S0]
 struct KStageArgs {
   Geom geo;
-  const double* X; int ldx; int xc;  // stencil input (xc cols)
-  const double* U0; int ldu; int ra; // base U0 (ra cols), null -> no base
-  const double* S0;                  // ra x r row-major (base = U0 S0)
-  const double* M;                   // ns x xc x r row-major contraction matrices
+  NMat X;             // stencil input (xc = X.cols)
+  NMat U0;            // base rows (ra = U0.cols), p == nullptr -> no base
+  const double* S0;   // ra x r row-major
+  const double* M;    // ns x xc x r row-major contraction matrices
   const double* inv_s;
-  int r;                             // output columns
-  double* out; int ldo;
-  double* copy_u; int ldc;           // optional: copy of U0 (ra cols)
+  NMat out;           // r = out.cols
 };
 void kstage(const KStageArgs& a, cudaStream_t st);
 
-// out (n x b) = X (n x a) * P (a x b row-major)  [+ options]
-void rotate(const Geom& g, const double* X, int ldx, int a, const double* P, int b, double* out,
-            int ldo, cudaStream_t st);
-void rotate_ld(const Geom& g, const double* X, int ldx, int a, const double* P, int ldp, int b,
-               double* out, int ldo, cudaStream_t st);
+// stencil Grams: out[s] = [X1 | X2]^T D_s S^-1 [X1 | X2]  (ns x w x w, w = X1.cols + X2.cols)
+void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* inv_s, double* out,
+                   DBuf& partial, cudaStream_t st);
+// general stencil Grams for the unit API: out[s] = X^T D_s S^-1 Y
+void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* inv_s, double* out,
+                      DBuf& partial, cudaStream_t st);
 
-// scattering K1 = U0 S0 + dt * inv_s * sum_b psi_b * (N_cls . rows_b) into A[:, :r],
-// U0 (ra cols) copied into A[:, r:r+ra]
-void scat_k1(const Geom& g, const double* U0, int ldu, int ra, const double* S0, int r, double dt,
-             const double* inv_s, const int* cls, const double* cls_atomic, const double* psi,
-             int ldpsi, int n_beams, const double* rows /* B x 12 x r */, double* A, int lda,
-             cudaStream_t st);
+// out = [Y1 | Y2] TA - X TB (rows written when out.p != null) and, when grams != null,
+// grams = [X^T out (X.cols x nb) ; out^T out (nb x nb)]
+void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
+             NMat out, double* grams, DBuf& partial, cudaStream_t st);
 
-void apply_streaming_full(const Geom& g, const double* U, int ldu, int m, const double* inv_s,
-                          const double* Acat /* ns x m x m */, double* W /* n x ns*m scratch */,
-                          double* out, int ldo, cudaStream_t st);
+// pointwise Grams
+enum PGen { PG_PLAIN = 0, PG_WEIGHT = 1, PG_SOURCE = 2 };
+struct PGramArgs {
+  Geom geo;
+  NMat X;                 // A operand (na = X.cols)
+  NMat Y;                 // plain / weight input
+  int nb;                 // T columns
+  int nphase;
+  int gen;
+  const double* inv_s;
+  const int* cls;
+  const double* wtab;     // class x 12 atomic densities
+  int wmode;              // weight: 0 class indicator, 1 wtab[cls][phase]
+  const double* psi;      // source: n_beams x ld
+  int ld;
+  double* out;            // nphase x na x nb
+};
+void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st);
 
-void dose_accumulate(const Geom& g, const double* U, int ldu, const double* coef /* r */, int r,
-                     double half_dt, const double* s_field, const double* psi, int ldpsi,
-                     int n_beams, double* deposited, double* prev, cudaStream_t st);
+// dK = dt * inv_s * sum_b psi_b * (N_cls . rows_b)  (scattering source rows, dlra.py:244-251)
+void scat_dk(const Geom& g, double dt, const double* inv_s, const int* cls,
+             const double* cls_atomic, const double* psi, int n_beams,
+             const double* rows /* B x 12 x r */, NMat out, cudaStream_t st);
 
+void dose_accumulate(const Geom& g, NMat U, const double* coef /* U.cols */, double half_dt,
+                     const double* s_field, const double* psi, int n_beams, double* deposited,
+                     double* prev, cudaStream_t st);
+
+void unit_rows(const Geom& g, NMat U, cudaStream_t st);        // U[:, j] = e_j
+void random_rows(const Geom& g, NMat U, unsigned long long seed, cudaStream_t st);
 void class_gather_inv(const int* cls, const double* class_val, int n, double* out_inv,
                       double* out_val, cudaStream_t st);
 void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, double w1,
               double* out, cudaStream_t st);
+// row-major host-layout (n x c) <-> column-major (ld) device layout (flux tables, TSQR)
 void transpose_in(const double* src_rowmajor, int n, int c, double* dst, int ldd, cudaStream_t st);
 void transpose_out(const double* src, int lds, int n, int c, double* dst_rowmajor,
                    cudaStream_t st);
 void fill_zero(double* p, size_t count, cudaStream_t st);
 
-// dense small / m-side kernels (dense.cu)
+// ------------------------------------------------------------ dense small / m-side (dense.cu)
 struct Mat {  // strided matrix view: element (i, j) at p[i * rs + j * cs]
   double* p;
   long rs, cs;
@@ -180,5 +193,10 @@ void scat_solves(const double* B /* 12 x r x r */, const double* coeffs /* 12 x 
 // S-phase RK4 on an (p x q) matrix: S' = -sum_s G_s S F_s (G: p x p, F: q x q)
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt,
            double* work, cudaStream_t st);
+
+// ray traversal (trace.cu)
+void traverse(const Geom& g, const double* origin, int n_rays, const double* starts,
+              const double* dirs, int* counts, const long long* offsets, long long* cells,
+              double* t0, double* t1, cudaStream_t st);
 
 }  // namespace pnd

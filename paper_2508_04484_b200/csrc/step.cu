@@ -31,10 +31,10 @@ namespace pnd {
 namespace {
 
 enum Slot {
-  S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RU, S_RV, S_ST1, S_SHAT, S_G,
+  S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
   S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
-  S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_UNEW, S_VNEW, S_SNEW, S_M2,
-  S_C1, S_OG, S_OTA, S_OTB, S_COUNT
+  S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_VNEW, S_M2,
+  S_C1, S_OG, S_OTA, S_OTB, S_EYE, S_PC, S_COUNT
 };
 static_assert(S_COUNT <= 43, "slots 43..47 are reserved by abi.cu");
 
@@ -53,18 +53,26 @@ void moment_factors(Handle& h, double* W, int c, double* out) {
        ns, h.st);
 }
 
-// grow an n-side buffer to `cols` columns, keeping its first `keep` columns
-void ensure_cols(Handle& h, DBuf& buf, int keep, int cols) {
-  const size_t need_d = (size_t)h.g.ld * cols;
-  if (buf.cap >= need_d) return;
-  DBuf fresh;
-  fresh.get(need_d);
-  if (keep > 0 && buf.p)
-    CK(cudaMemcpyAsync(fresh.p, buf.p, sizeof(double) * h.g.ld * keep, cudaMemcpyDeviceToDevice,
-                       h.st));
-  CK(cudaStreamSynchronize(h.st));
-  buf.free_();
-  buf = fresh;
+__global__ void eye_kernel(double* I, int b) {
+  for (int i = threadIdx.x; i < b * b; i += blockDim.x) I[i] = (i / b == i % b) ? 1.0 : 0.0;
+}
+
+__global__ void zero_rows_kernel(double* S, int row0, int rows, int cols) {
+  for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) S[(size_t)row0 * cols + i] = 0.0;
+}
+
+__global__ void isp_kernel(const double* inv_s, int n, double* isp) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    isp[2 * c] = inv_s[c];
+    isp[2 * c + 1] = 0.0;
+  }
+}
+
+double* eye(Handle& h, int b) {
+  double* I = slot(h, S_EYE, (size_t)b * b);
+  eye_kernel<<<1, 256, 0, h.st>>>(I, b);
+  launched();
+  return I;
 }
 
 // SVQB transform from the Gram pair of Y against (U0, Y):
@@ -125,99 +133,100 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
   }
 }
 
-__global__ void eye_kernel(double* I, int b) {
-  for (int i = threadIdx.x; i < b * b; i += blockDim.x) I[i] = (i / b == i % b) ? 1.0 : 0.0;
+}  // namespace
+
+NMat state_u(Handle& h) { return h.U.view(h.g, h.ua, h.st); }
+NMat state_q(Handle& h) {
+  if (h.uq <= 0) return NMat{};
+  return h.Q.view(h.g, h.uq, h.st);
 }
 
-__global__ void unit_cols_kernel(double* U, int ld, int r) {
-  // U[:, j] = e_j (cells 0..r-1): the reference's canonical basis when S^ == 0
-  for (int j = blockIdx.x; j < r; j += gridDim.x)
-    for (int i = threadIdx.x; i < ld; i += blockDim.x) U[(size_t)j * ld + i] = (i == j) ? 1.0 : 0.0;
+void set_isp(Handle& h) {
+  const size_t rows = (size_t)h.g.n + 2 * (size_t)h.g.halo;
+  if (h.isp.cap < 2 * rows) {
+    h.isp.get(2 * rows);
+    fill_zero(h.isp.p, 2 * rows, h.st);
+  }
+  isp_kernel<<<148 * 8, 256, 0, h.st>>>(h.inv_s.p, h.g.n, h.isp.p + 2 * (size_t)h.g.halo);
+  launched();
 }
 
-__global__ void zero_rows_kernel(double* S, int row0, int rows, int cols) {
-  for (int i = threadIdx.x; i < rows * cols; i += blockDim.x) S[(size_t)row0 * cols + i] = 0.0;
+static const double* isp_rows(Handle& h) { return h.isp.p + 2 * (size_t)h.g.halo; }
+
+void consolidate(Handle& h) {
+  if (h.uq <= 0) return;
+  const int ru = h.ua + h.uq;
+  NMat u = state_u(h), q = state_q(h);
+  NMat out = h.Un.view(h.g, ru, h.st);
+  lincomb(h.g, u, q, NMat{}, eye(h, ru), nullptr, out, nullptr, h.part, h.st);
+  std::swap(h.U, h.Un);
+  h.ua = ru;
+  h.uq = 0;
 }
 
-GramArgs lincomb_args(Handle& h, const double* U0, int a, const double* Y, int ny,
-                      const double* TA, const double* TB, int nb, double* out, double* grams,
-                      int nphase) {
-  GramArgs ga{};
-  ga.geo = h.g;
-  ga.X = U0; ga.ldx = h.g.ld; ga.na = a;
-  ga.Y = Y; ga.ldy = h.g.ld; ga.ny = ny;
-  ga.nb = nb;
-  ga.TA = TA; ga.TB = TB;
-  ga.Yout = out; ga.ldo = h.g.ld;
-  ga.nphase = nphase;
-  ga.self_phase = 1;
-  ga.gen = GEN_LINCOMB;
-  ga.inv_s = h.inv_s.p;
-  ga.out = grams;
-  return ga;
-}
-
-// Q (k cols, written at U[:, a:a+k]) = orthonormal basis of (I - U0 U0^T) X,
-// U0 = U[:, :a], X (b cols, ld). C1 = U0^T X (a x b, device). Returns k.
-int orth_complement(Handle& h, const double* X, int b, const double* C1) {
-  const int a = h.ru, ld = h.g.ld;
+int orth_complement(Handle& h, NMat X, const double* C1) {
+  const int a = h.ua, b = X.cols;
   cudaStream_t st = h.st;
-  const double* U0 = h.U.p;
-  double* Qs = h.U.p + (size_t)a * ld;
+  const Geom& g = h.g;
+  NMat U0 = a > 0 ? state_u(h) : NMat{};
   double* grams = slot(h, S_OG, (size_t)b * (a + b));
   double* TA = slot(h, S_OTA, (size_t)b * b);
-  double* TB = slot(h, S_OTB, (size_t)a * b);
+  double* TB = slot(h, S_OTB, (size_t)(a > 0 ? a : 1) * b);
   double* P = slot(h, S_P, (size_t)b * b);
   double* sig = slot(h, S_SIG, (size_t)b + 2);
   double* Qt = slot(h, S_QTM, (size_t)b * b);
   int* info = h.iflag.get(8);
   double* dinfo = slot(h, S_TAIL, 4);
-  // pass 2: Y = X - U0 C1 (identity TA), C2 = U0^T Y, G2 = Y^T Y
-  eye_kernel<<<1, 256, 0, st>>>(TA, b);
-  launched();
-  gram(lincomb_args(h, U0, a, X, b, TA, C1, b, Qs, grams, 2), h.part, st);
-  // eigen(G2 - C2^T C2) (one-sided Jacobi SVD of the symmetric PSD matrix)
+  // pass 2: Y = X - U0 C1 -> Qa, C2 = U0^T Y, G2 = Y^T Y
+  NMat Y = h.Qa.view(g, b, st);
+  lincomb(g, X, NMat{}, U0, eye(h, b), C1, Y, grams, h.part, st);
   double* C2 = grams;                  // a x b
   double* G2 = grams + (size_t)a * b;  // b x b
-  gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
+  if (a > 0) gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
   svd_small(G2, b, b, P, sig, Qt, nullptr, st);
   svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 0, 1e-7, TA, TB, info, dinfo);
   launched();
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const int k = *(int*)(h.pinned + 8);
+  h.uq = 0;
   if (k == 0) return 0;
-  // pass 3: Q = Y TA - U0 TB (k cols, in place), C3 = U0^T Q, G3 = Q^T Q
-  gram(lincomb_args(h, U0, a, Qs, b, TA, TB, k, Qs, grams, 2), h.part, st);
+  // pass 3: Q = Y TA - U0 TB (k cols) -> Q, C3 = U0^T Q, G3 = Q^T Q
+  NMat Qv = h.Q.view(g, k, st);
+  lincomb(g, Y, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
   double* C3 = grams;
   double* G3 = grams + (size_t)a * k;
   double* G3c = slot(h, S_M2, (size_t)k * k);
   CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
-  gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
+  if (a > 0) gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
   svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
   svqb_build<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1, dinfo);
   launched();
   CK(cudaMemcpyAsync(h.pinned + 9, dinfo, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (h.pinned[9] > 1e-14) {
-    // pass 4: Q <- Q TA - U0 TB, in place (rows are staged before they are written)
-    gram(lincomb_args(h, U0, a, Qs, k, TA, TB, k, Qs, grams, 1), h.part, st);
+    // pass 4: Q <- Q TA - U0 TB (into Qa, then swap)
+    NMat Q2 = h.Qa.view(g, k, st);
+    lincomb(g, Qv, NMat{}, U0, TA, TB, Q2, nullptr, h.part, st);
+    std::swap(h.Q, h.Qa);
   }
+  h.uq = k;
   return k;
 }
-
-}  // namespace
 
 void streaming_step(Handle& h, double dt) {
   if (!h.stencil_error.empty()) fail(PND_ECONFIG, h.stencil_error);
   need(h.have_angular, "angular operators (pnd_set_angular)");
   need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
+  consolidate(h);
   const Geom& g = h.g;
-  const int m = h.m, ns = g.ns, ld = g.ld;
-  const int a = h.ru, b = h.rv;
+  const int m = h.m, ns = g.ns;
+  const int a = h.ua, b = h.rv;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
   if (b > 32 || a > 32) fail(PND_ECONFIG, "streaming step supports rank <= 32");
   cudaStream_t st = h.st;
+  const NMat U0 = state_u(h);
+  const double* isp = isp_rows(h);
 
   // --- K phase: K1 = K0 + dK, K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
   phase(h, PH_LSIDE);
@@ -225,67 +234,49 @@ void streaming_step(Handle& h, double dt) {
   moment_factors(h, h.V.p, b, F);
   const int xmax = a > b ? a : b;
   double* M = slot(h, S_MST, (size_t)ns * xmax * b);
-  double* W1 = h.W1.get((size_t)ld * b);
-  double* W2 = h.W2.get((size_t)ld * b);
+  const NMat W1 = h.W1.view(g, b, st);
+  const NMat W2 = h.W2.view(g, b, st);
   const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
   for (int stage = 0; stage < 4; ++stage) {
     KStageArgs ka{};
     ka.geo = g;
-    ka.inv_s = h.inv_s.p;
-    ka.U0 = stage == 3 ? nullptr : h.U.p;  // the last stage returns dK = h L(W2) only
-    ka.ldu = ld;
-    ka.ra = stage == 3 ? 0 : a;
+    ka.inv_s = isp;
+    ka.U0 = stage == 3 ? NMat{} : U0;  // the last stage returns dK = h L(W2) only
     ka.S0 = h.S.p;
-    ka.r = b;
     ka.M = M;
     const double c = -coef[stage] * dt;
     if (stage == 0) {
       // L(U0 S0) = -sum_s (D_s U0)(S0 F_s): X = U0, M_s = -(h/4) S0 F_s
       gemm(a, b, b, c, rowm(h.S.p, b), 0, rowm(F, b), (long)b * b, 0.0, rowm(M, b),
            (long)a * b, ns, st);
-      ka.X = h.U.p;
-      ka.xc = a;
+      ka.X = U0;
       ka.out = W1;
     } else {
       axpby(ns * b * b, c, F, 0.0, M, st);
       ka.X = stage == 2 ? W2 : W1;
-      ka.xc = b;
       ka.out = stage == 2 ? W1 : W2;
     }
-    ka.ldx = ld;
-    ka.ldo = ld;
     phase(h, PH_KSTAGE);
     kstage(ka, st);
     phase(h, PH_LSIDE);
   }
-  double* dK = W2;
+  const NMat dK = W2;
 
   // --- L phase: L' = -sum_s A_s L Q_s, Q_s = (D_s S^-1 U0)^T U0, L0 = V0 S0^T
   double* QT = slot(h, S_QT, (size_t)ns * a * a);
   phase(h, PH_LGRAM);
-  {
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
-    ga.Y = h.U.p; ga.ldy = ld; ga.nb = a;
-    ga.nphase = ns;
-    ga.gen = GEN_STENCIL;
-    ga.inv_s = h.inv_s.p;
-    ga.out = QT;  // QT_s = U0^T D_s U0 = Q_s^T
-    gram(ga, h.part, st);
-  }
-  // C1 = U0^T dK for the augmentation
+  stencil_grams(g, U0, NMat{}, isp, QT, h.part, st);  // QT_s = U0^T D_s U0 = Q_s^T
   double* C1 = slot(h, S_C1, (size_t)a * b);
   {
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
-    ga.Y = dK; ga.ldy = ld; ga.nb = b;
-    ga.nphase = 1;
-    ga.gen = GEN_PLAIN;
-    ga.inv_s = h.inv_s.p;
-    ga.out = C1;
-    gram(ga, h.part, st);
+    PGramArgs pa{};
+    pa.geo = g;
+    pa.X = U0;
+    pa.Y = dK;
+    pa.nb = b;
+    pa.nphase = 1;
+    pa.gen = PG_PLAIN;
+    pa.out = C1;
+    pgram(pa, h.part, st);
   }
   phase(h, PH_LSIDE);
   double* L0 = slot(h, S_L0, (size_t)m * a);
@@ -308,9 +299,8 @@ void streaming_step(Handle& h, double dt) {
   transpose_in(h.V.p, m, b, BV + (size_t)a * m, m, st);
 
   // --- augmentation: U^ = [U0 | orth((I - U0 U0^T) dK)], V^ = orth([L1, V0])
-  phase(h, PH_TSQR_N);
-  ensure_cols(h, h.U, a, a + b);
-  const int k = orth_complement(h, dK, b, C1);
+  phase(h, PH_ORTH);
+  const int k = orth_complement(h, dK, C1);
   const int ru = a + k;
   double* Vhc = slot(h, S_VHC, (size_t)m * cols);
   double* Rv = slot(h, S_RV, (size_t)cols * cols);
@@ -329,17 +319,7 @@ void streaming_step(Handle& h, double dt) {
   // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
   double* G = slot(h, S_G, (size_t)ns * ru * ru);
   phase(h, PH_SGRAM);
-  {
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = h.U.p; ga.ldx = ld; ga.na = ru;
-    ga.Y = h.U.p; ga.ldy = ld; ga.nb = ru;
-    ga.nphase = ns;
-    ga.gen = GEN_STENCIL;
-    ga.inv_s = h.inv_s.p;
-    ga.out = G;
-    gram(ga, h.part, st);
-  }
+  stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
   phase(h, PH_SRK4);
   double* Vhr = slot(h, S_VHR, (size_t)m * rv);
   transpose_out(Vhc, m, m, rv, Vhr, st);
@@ -347,7 +327,7 @@ void streaming_step(Handle& h, double dt) {
   moment_factors(h, Vhr, rv, Fh);
   s_rk4(Sh, ru, rv, G, Fh, ns, dt, nullptr, st);
 
-  // --- new (augmented) state: U already holds [U0 | Q]
+  // --- new (augmented) state: [U0 | Q]
   double* Snew = h.S.get((size_t)ru * rv);
   CK(cudaMemcpyAsync(Snew, Sh, sizeof(double) * ru * rv, cudaMemcpyDeviceToDevice, st));
   double* Vnew = h.V.get((size_t)m * rv);
@@ -380,13 +360,15 @@ void scattering_step(Handle& h, double dt) {
   need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
   need(h.have_mat, "materials (pnd_set_materials)");
   need(h.have_scat, "scattering tables (pnd_set_scattering)");
+  consolidate(h);
   const Geom& g = h.g;
-  const int m = h.m, ld = g.ld;
-  const int a = h.ru, b = h.rv;
+  const int m = h.m;
+  const int a = h.ua, b = h.rv;
   const int B = h.n_beams;
   cudaStream_t st = h.st;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
   if (a > 32 || b > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
+  const NMat U0 = state_u(h);
 
   // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
   phase(h, PH_SCATSMALL);
@@ -399,29 +381,28 @@ void scattering_step(Handle& h, double dt) {
   }
 
   // substep 2 increment: dK = dt src_rows(V0)  (dlra.py:303; K1 = U0 S0 + dK)
-  double* dK = h.W2.get((size_t)ld * b);
+  const NMat dK = h.W2.view(g, b, st);
   phase(h, PH_SCATK1);
-  scat_k1(g, h.U.p, ld, 0, h.S.p, b, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p,
-          B > 0 ? h.psi.p : nullptr, ld, B, rows, dK, ld, st);
+  scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, B > 0 ? h.psi.p : nullptr, B, rows, dK, st);
 
   // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
   const int nw = h.n_cls <= 12 ? h.n_cls : 12;
   double* H = slot(h, S_H, (size_t)nw * a * a);
   phase(h, PH_SCATGRAM);
   {
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
-    ga.Y = h.U.p; ga.ldy = ld; ga.nb = a;
-    ga.nphase = nw;
-    ga.gen = GEN_WEIGHT;
-    ga.inv_s = h.inv_s.p;
-    ga.cls = h.cls.p;
-    ga.wtab = h.cls_atomic.p;
-    ga.n_cls = h.n_cls;
-    ga.wmode = h.n_cls <= 12 ? 0 : 1;
-    ga.out = H;
-    gram(ga, h.part, st);
+    PGramArgs pa{};
+    pa.geo = g;
+    pa.X = U0;
+    pa.Y = U0;
+    pa.nb = a;
+    pa.nphase = nw;
+    pa.gen = PG_WEIGHT;
+    pa.inv_s = h.inv_s.p;
+    pa.cls = h.cls.p;
+    pa.wtab = h.cls_atomic.p;
+    pa.wmode = h.n_cls <= 12 ? 0 : 1;
+    pa.out = H;
+    pgram(pa, h.part, st);
   }
   phase(h, PH_SCATSMALL);
   double* Bi = slot(h, S_BI, (size_t)12 * a * a);
@@ -436,18 +417,19 @@ void scattering_step(Handle& h, double dt) {
   double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
   phase(h, PH_SCATGRAM);
   if (B > 0) {
-    GramArgs ga{};
-    ga.geo = g;
-    ga.X = h.U.p; ga.ldx = ld; ga.na = a;
-    ga.nb = 12 * B;
-    ga.nphase = 1;
-    ga.gen = GEN_SOURCE;
-    ga.inv_s = h.inv_s.p;
-    ga.cls = h.cls.p;
-    ga.wtab = h.cls_atomic.p;
-    ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
-    ga.out = left;
-    gram(ga, h.part, st);
+    PGramArgs pa{};
+    pa.geo = g;
+    pa.X = U0;
+    pa.nb = 12 * B;
+    pa.nphase = 1;
+    pa.gen = PG_SOURCE;
+    pa.inv_s = h.inv_s.p;
+    pa.cls = h.cls.p;
+    pa.wtab = h.cls_atomic.p;
+    pa.psi = h.psi.p;
+    pa.ld = g.ld;
+    pa.out = left;
+    pgram(pa, h.part, st);
   }
   phase(h, PH_SCATSMALL);
   // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass)
@@ -485,9 +467,8 @@ void scattering_step(Handle& h, double dt) {
   tsqr(lnew, m, a, m, Vtc, m, Rt, h.tq_m, st);  // S~ = R~^T  (a x kt)
 
   // substep 2: U^ = [U0 | orth((I - U0 U0^T) dK)]
-  phase(h, PH_TSQR_N);
-  ensure_cols(h, h.U, a, a + b);
-  const int k = orth_complement(h, dK, b, C1);
+  phase(h, PH_ORTH);
+  const int k = orth_complement(h, dK, C1);
   const int ru = a + k;
   phase(h, PH_SCATSMALL);
 
@@ -525,18 +506,19 @@ void scattering_step(Handle& h, double dt) {
     CK(cudaMemcpyAsync(proj2, left, sizeof(double) * a * 12 * B, cudaMemcpyDeviceToDevice, st));
     if (k > 0) {
       phase(h, PH_SCATGRAM);
-      GramArgs ga{};
-      ga.geo = g;
-      ga.X = h.U.p + (size_t)a * ld; ga.ldx = ld; ga.na = k;
-      ga.nb = 12 * B;
-      ga.nphase = 1;
-      ga.gen = GEN_SOURCE;
-      ga.inv_s = h.inv_s.p;
-      ga.cls = h.cls.p;
-      ga.wtab = h.cls_atomic.p;
-      ga.psi = h.psi.p; ga.ldpsi = ld; ga.n_beams = B;
-      ga.out = proj2 + (size_t)a * 12 * B;
-      gram(ga, h.part, st);
+      PGramArgs pa{};
+      pa.geo = g;
+      pa.X = state_q(h);
+      pa.nb = 12 * B;
+      pa.nphase = 1;
+      pa.gen = PG_SOURCE;
+      pa.inv_s = h.inv_s.p;
+      pa.cls = h.cls.p;
+      pa.wtab = h.cls_atomic.p;
+      pa.psi = h.psi.p;
+      pa.ld = g.ld;
+      pa.out = proj2 + (size_t)a * 12 * B;
+      pgram(pa, h.part, st);
       phase(h, PH_SCATSMALL);
     }
     double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
@@ -603,20 +585,24 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   const Geom& g = h.g;
   const int m = h.m;
   phase(h, PH_ROTATE);
-  ensure_cols(h, h.Uhat, 0, 2 * (r1 > 0 ? r1 : 1));
-  double* Unew = h.Uhat.p;
+  const NMat Un = h.Un.view(g, r1, st);
   if (all_zero) {
     // S^ == 0: the reference's Householder basis of [0 | U0] starts with e_0..e_{r-1}
     // and svd(0) = (I, 0, I), so U1 is the canonical cell basis (Appendix C.4)
-    unit_cols_kernel<<<r1, 256, 0, st>>>(Unew, g.ld, r1);
-    launched();
+    unit_rows(g, Un, st);
   } else {
-    rotate_ld(g, h.U.p, g.ld, p, P, k, r1, Unew, g.ld, st);
+    // U1 = [U | Q] P[:, :r1]
+    double* Pc = slot(h, S_PC, (size_t)p * r1);
+    CK(cudaMemcpy2DAsync(Pc, r1 * sizeof(double), P, k * sizeof(double), r1 * sizeof(double), p,
+                         cudaMemcpyDeviceToDevice, st));
+    lincomb(g, state_u(h), state_q(h), NMat{}, Pc, nullptr, Un, nullptr, h.part, st);
   }
   phase(h, PH_SVD);
   double* Vn = slot(h, S_VNEW, (size_t)m * r1);
   gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);
-  std::swap(h.U, h.Uhat);
+  std::swap(h.U, h.Un);
+  h.ua = r1;
+  h.uq = 0;
   double* V = h.V.get((size_t)m * r1);
   CK(cudaMemcpyAsync(V, Vn, sizeof(double) * m * r1, cudaMemcpyDeviceToDevice, st));
   double* S = h.S.get((size_t)r1 * r1);
@@ -629,6 +615,7 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
 }
 
 void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
+  consolidate(h);
   const Geom& g = h.g;
   cudaStream_t st = h.st;
   phase(h, PH_DOSE);
@@ -638,27 +625,28 @@ void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
        st);
   double* dep = h.dep.get((size_t)g.ld);
   double* prev = h.prev.get((size_t)g.ld);
-  pnd::dose_accumulate(g, h.U.p, g.ld, coef, h.ru, 0.5 * dt, h.s_field.p,
-                       tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr, g.ld, h.n_beams, dep,
-                       prev, st);
+  pnd::dose_accumulate(g, state_u(h), coef, 0.5 * dt, h.s_field.p,
+                       tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr, h.n_beams, dep, prev,
+                       st);
   phase(h, -1);
 }
 
 double orth_defect(Handle& h) {
+  consolidate(h);
   const Geom& g = h.g;
   cudaStream_t st = h.st;
   phase(h, PH_DEFECT);
   double* G = slot(h, S_DEF, (size_t)h.ru * h.ru + (size_t)h.rv * h.rv + 2);
   double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
-  GramArgs ga{};
-  ga.geo = g;
-  ga.X = h.U.p; ga.ldx = g.ld; ga.na = h.ru;
-  ga.Y = h.U.p; ga.ldy = g.ld; ga.nb = h.ru;
-  ga.nphase = 1;
-  ga.gen = GEN_PLAIN;
-  ga.inv_s = h.inv_s.p;
-  ga.out = G;
-  gram(ga, h.part, st);
+  PGramArgs pa{};
+  pa.geo = g;
+  pa.X = state_u(h);
+  pa.Y = state_u(h);
+  pa.nb = h.ru;
+  pa.nphase = 1;
+  pa.gen = PG_PLAIN;
+  pa.out = G;
+  pgram(pa, h.part, st);
   double* GV = G + (size_t)h.ru * h.ru;
   gemm(h.rv, h.rv, h.m, 1.0, tr(rowm(h.V.p, h.rv)), 0, rowm(h.V.p, h.rv), 0, 0.0,
        rowm(GV, h.rv), 0, 1, st);

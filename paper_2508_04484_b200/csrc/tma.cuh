@@ -69,3 +69,17 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 }
 
 }  // namespace pnd
+
+namespace pnd {
+
+// one contiguous global -> shared copy through the TMA engine (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"((unsigned long long)src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+}  // namespace pnd

@@ -1,6 +1,6 @@
 """Run one apply_streaming case per subprocess (sticky CUDA errors) and report."""
 import subprocess, sys, json
-cases = [(5,4,6,9),(7,8,8,9),(5,5,5,9),(9,9,9,4),(6,5,6,4),(1,5,7,4)]
+cases = [(5,4,6,9),(7,8,8,9),(8,8,8,16),(1,1,12,9),(40,40,40,16),(1,5,7,4)]
 code = r'''
 import sys, numpy as np
 sys.path.insert(0, ".")
