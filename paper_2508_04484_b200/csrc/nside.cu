@@ -1,23 +1,16 @@
 // Cell-parallel (n-side) kernels of the energy step, cell-major layout.
 //
 // Every n-side operation is "form per-cell feature rows, then contract them"
-// and runs as FP64 tensor-core mma.sync.m8n8k4 (DMMA) on shared-memory tiles:
-//   kstage   one Horner stage of the K-phase RK4 (dlra.py:168-174): the 2*na
-//            upwind stencil values of every column (spatial.py:81-118) plus the
-//            U0 row, contracted with [M_0; ...; M_ns-1; S0];
-//   sgram    the stencil Grams U^T D_s S^-1 U of the L- and S-phases
-//            (dlra.py:183-184, 199-209), accumulated in registers over chunks;
+// and runs as FP64 tensor-core mma.sync.m8n8k4 (DMMA) on shared-memory tiles.
+// The stencil kernels (kstage, stencil Grams) live in stencil.cu; this file
+// holds the pointwise/contraction kernels:
 //   lincomb  [Y1 | Y2] TA - X TB with its Grams: the passes of the block
 //            Gram-Schmidt/SVQB augmentation and the truncation rotation
 //            (dlra.py:26-43, 111-113);
-//   pgram    plain / weighted / source Grams (dlra.py:285, 307-319).
-// The stencil kernels stage their halo segments with cp.async.bulk (one TMA
-// bulk copy per contiguous segment of cell rows, double-buffered on two
-// mbarriers): box 0 = rows [c0-2, c0+CH+2) covers the first active axis
-// (stride 1), and rows [c0 + d*st, c0 + d*st + CH), d = -2,-1,1,2, cover every
-// further axis. The halo rows around each matrix are zero, so every segment is
-// in bounds. Shared-memory tiles use row lengths = 4 (mod 16) doubles where
-// DMMA fragments are read, which spreads a half-warp over 16 distinct banks.
+//   pgram    plain / weighted / source Grams (dlra.py:285, 307-319);
+//   scat_dk, dose, transposes, unit/random rows, class gathers.
+// Shared-memory tiles use row lengths = 4 (mod 16) doubles where DMMA
+// fragments are read, which spreads a half-warp over 16 distinct banks.
 #include "tma.cuh"
 
 namespace pnd {
@@ -27,374 +20,6 @@ namespace {
 __host__ __device__ constexpr int pad4(int w) { return ((w + 11) / 16) * 16 + 4; }
 __host__ __device__ constexpr int up16(int w) { return (w + 15) / 16 * 16; }
 
-struct Plan {
-  int nbox;    // 1 + 4 (na - 1)
-  int off[9];  // first row of box b relative to c0
-};
-
-Plan make_plan(const Geom& g) {
-  Plan p{};
-  p.nbox = 1;
-  p.off[0] = -2;
-  const int nxy = g.nx * g.ny;
-  for (int ai = 1; ai < g.na; ++ai) {
-    const int st = g.axis[ai] == 1 ? g.nx : nxy;
-    const int ds[4] = {-2, -1, 1, 2};
-    for (int q = 0; q < 4; ++q) p.off[p.nbox++] = ds[q] * st;
-  }
-  return p;
-}
-
-struct CellCoord {
-  int idx[3];
-  int len[3];
-};
-
-__device__ __forceinline__ CellCoord coord_of(const Geom& g, int c) {
-  const int nxy = g.nx * g.ny;
-  const int ck = c / nxy, rem = c - ck * nxy;
-  const int cj = rem / g.nx, ci = rem - cj * g.nx;
-  const int all[3] = {ci, cj, ck};
-  const int lens[3] = {g.nx, g.ny, g.nz};
-  CellCoord cc;
-#pragma unroll
-  for (int ai = 0; ai < 3; ++ai) {
-    const int axis = ai < g.na ? g.axis[ai] : 0;
-    cc.idx[ai] = all[axis];
-    cc.len[ai] = lens[axis];
-  }
-  return cc;
-}
-
-// first staged row of box b (box 0 has CH + 4 rows, the others CH)
-template <int CH>
-__device__ __forceinline__ int box_row(int b) {
-  return b == 0 ? 0 : CH + 4 + (b - 1) * CH;
-}
-
-// 2*na stencil values D_s (S^-1 x) of column j at chunk cell i, from staged rows
-//   X: staged rows of the input (row length rs), I: staged rows of [1/S, 0]
-template <int CH>
-__device__ __forceinline__ void stencil6(const Geom& g, const CellCoord& cc, const double* X,
-                                         int rs, const double* I, int i, int j, double* t) {
-#pragma unroll
-  for (int ai = 0; ai < 3; ++ai) {
-    if (ai < g.na) {
-      const int axis = g.axis[ai];
-      double f[5];
-      if (ai == 0) {
-#pragma unroll
-        for (int d = 0; d < 5; ++d) f[d] = X[(i + d) * rs + j] * I[2 * (i + d)];
-      } else {
-        const int b = 1 + 4 * (ai - 1);
-        const int r0 = box_row<CH>(b) + i, r1 = box_row<CH>(b + 1) + i;
-        const int r3 = box_row<CH>(b + 2) + i, r4 = box_row<CH>(b + 3) + i;
-        f[0] = X[r0 * rs + j] * I[2 * r0];
-        f[1] = X[r1 * rs + j] * I[2 * r1];
-        f[2] = X[(i + 2) * rs + j] * I[2 * (i + 2)];
-        f[3] = X[r3 * rs + j] * I[2 * r3];
-        f[4] = X[r4 * rs + j] * I[2 * r4];
-      }
-      const double ih = g.ih[axis], i2h = g.i2h[axis];
-      const int idx = cc.idx[ai], len = cc.len[ai];
-      double tp, tm;
-      if (idx >= 2) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) * i2h;
-      else if (idx == 1) tp = (f[2] - f[1]) * ih;
-      else tp = f[2] * ih;
-      if (idx <= len - 3) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) * i2h;
-      else if (idx == len - 2) tm = (f[3] - f[2]) * ih;
-      else tm = -f[2] * ih;
-      t[2 * ai] = tp;
-      t[2 * ai + 1] = tm;
-    }
-  }
-}
-
-struct Stage {
-  int nbox;
-  int off[9];
-  int nrows;      // staged rows per input
-  int xoff[2];    // doubles offset of the staged rows of input 0 / 1
-  int ioff;       // offset of the staged [1/S, 0] rows
-  int uoff;       // offset of the separately staged centre rows (-1: none)
-  int buf;        // doubles per buffer
-  unsigned bytes; // bytes per chunk
-};
-
-template <int CH>
-Stage make_stage(const Geom& g, const NMat* in, int nin, const NMat* centre) {
-  const Plan p = make_plan(g);
-  Stage s{};
-  s.nbox = p.nbox;
-  for (int q = 0; q < p.nbox; ++q) s.off[q] = p.off[q];
-  s.nrows = CH + 4 + (p.nbox - 1) * CH;
-  int o = 0;
-  unsigned bytes = 0;
-  for (int k = 0; k < 2; ++k) {
-    s.xoff[k] = o;
-    if (k < nin) {
-      o += up16(s.nrows * in[k].rs);
-      bytes += s.nrows * in[k].rs * 8;
-    }
-  }
-  s.ioff = o;
-  o += up16(2 * s.nrows);
-  bytes += 2 * s.nrows * 8;
-  s.uoff = -1;
-  if (centre) {
-    s.uoff = o;
-    o += up16(CH * centre->rs);
-    bytes += CH * centre->rs * 8;
-  }
-  s.buf = up16(o);
-  s.bytes = bytes;
-  return s;
-}
-
-// one thread issues the bulk copies of one chunk's segments
-template <int CH>
-__device__ __forceinline__ void stage_chunk(const Stage& S, double* dst, uint64_t* bar, int c0,
-                                            const NMat& a, const NMat& b, int nin,
-                                            const double* isp, const NMat& u) {
-  mbar_expect_tx(bar, S.bytes);
-  for (int q = 0; q < S.nbox; ++q) {
-    const int rows = q == 0 ? CH + 4 : CH;
-    const int row = c0 + S.off[q];
-    const int drow = q == 0 ? 0 : CH + 4 + (q - 1) * CH;
-    bulk_load(dst + S.xoff[0] + drow * a.rs, a.p + (long)row * a.rs, rows * a.rs * 8, bar);
-    if (nin > 1)
-      bulk_load(dst + S.xoff[1] + drow * b.rs, b.p + (long)row * b.rs, rows * b.rs * 8, bar);
-    bulk_load(dst + S.ioff + 2 * drow, isp + 2L * row, rows * 16, bar);
-  }
-  if (S.uoff >= 0) bulk_load(dst + S.uoff, u.p + (long)c0 * u.rs, CH * u.rs * 8, bar);
-}
-
-// ===================================================================== kstage
-constexpr int KC = 32;
-
-struct KParams {
-  int K, K4, KS, BS, ksplit;
-};
-
-template <int RB>
-__global__ void __launch_bounds__(256, 1)
-    kstage_kernel(KStageArgs a, Stage S, KParams P, const double* __restrict__ isp) {
-  constexpr int NT = RB / 8;
-  constexpr int TILES = (KC / 8) * NT;
-  constexpr int RBP = RB + 2;
-  extern __shared__ __align__(128) double sm[];
-  double* buf = sm;
-  double* sA = sm + 2 * S.buf;              // [KC][KS]
-  double* sB = sA + KC * P.KS;              // [K4][BS]
-  double* sO = sB + P.K4 * P.BS;            // [ksplit][KC][RBP]
-  uint64_t* bar = (uint64_t*)(sO + P.ksplit * KC * RBP);
-  const Geom& g = a.geo;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ns = g.ns, xc = a.X.cols, ra = a.U0.p ? a.U0.cols : 0, r = a.out.cols;
-  const int K = P.K, K4 = P.K4, KS = P.KS, BS = P.BS;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_fence_init();
-  }
-  for (int i = tid; i < K4 * BS; i += 256) {
-    const int k = i / BS, n = i - k * BS;
-    double v = 0.0;
-    if (n < r && k < K) v = k < ns * xc ? a.M[(size_t)k * r + n] : a.S0[(size_t)(k - ns * xc) * r + n];
-    sB[i] = v;
-  }
-  for (int i = tid; i < KC * KS; i += 256) sA[i] = 0.0;
-  __syncthreads();
-  const bool sepu = S.uoff >= 0;
-  const int nchunks = (g.n + KC - 1) / KC;
-  if (tid == 0 && blockIdx.x < nchunks)
-    stage_chunk<KC>(S, buf, &bar[0], blockIdx.x * KC, a.X, a.X, 1, isp, a.U0);
-  const int K4s = K4 / P.ksplit;  // multiple of 4 (host guarantees)
-  int it = 0;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
-    const int b = it & 1;
-    const int next = chunk + gridDim.x;
-    if (tid == 0 && next < nchunks) {
-      fence_proxy_async();
-      stage_chunk<KC>(S, buf + (b ^ 1) * S.buf, &bar[b ^ 1], next * KC, a.X, a.X, 1, isp, a.U0);
-    }
-    mbar_wait(&bar[b], (it >> 1) & 1);
-    const double* B = buf + b * S.buf;
-    const double* Xs = B + S.xoff[0];
-    const double* Is = B + S.ioff;
-    const int c0 = chunk * KC;
-    // stencil features: A[i][s*xc + j]
-    for (int e = tid; e < KC * xc; e += 256) {
-      const int i = e / xc, j = e - i * xc;
-      const int c = c0 + i;
-      double t[6] = {0, 0, 0, 0, 0, 0};
-      if (c < g.n) stencil6<KC>(g, coord_of(g, c), Xs, a.X.rs, Is, i, j, t);
-      double* arow = sA + i * KS + j;
-#pragma unroll
-      for (int s = 0; s < 6; ++s)
-        if (s < ns) arow[s * xc] = t[s];
-    }
-    // base rows: A[i][ns*xc + j] = U0[c][j]
-    for (int e = tid; e < KC * ra; e += 256) {
-      const int i = e / ra, j = e - i * ra;
-      sA[i * KS + ns * xc + j] = sepu ? B[S.uoff + i * a.U0.rs + j] : Xs[(i + 2) * a.X.rs + j];
-    }
-    __syncthreads();
-    for (int item = warp; item < TILES * P.ksplit; item += 8) {
-      const int tile = item % TILES, h = item / TILES;
-      const int mt = tile / NT, nt = tile - mt * NT;
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      const double* pa = sA + (mt * 8 + (lane >> 2)) * KS + (lane & 3);
-      const double* pb = sB + (lane & 3) * BS + nt * 8 + (lane >> 2);
-      const int kb = h * K4s, ke = kb + K4s;
-      int k0 = kb;
-      for (; k0 + 8 <= ke; k0 += 8) {
-        dmma884(d0, d1, pa[k0], pb[k0 * BS]);
-        dmma884(e0, e1, pa[k0 + 4], pb[(k0 + 4) * BS]);
-      }
-      if (k0 < ke) dmma884(d0, d1, pa[k0], pb[k0 * BS]);
-      const int m = mt * 8 + (lane >> 2), n = nt * 8 + 2 * (lane & 3);
-      sO[(h * KC + m) * RBP + n] = d0 + e0;
-      sO[(h * KC + m) * RBP + n + 1] = d1 + e1;
-    }
-    __syncthreads();
-    const int rso = a.out.rs;
-    for (int e = tid; e < KC * rso; e += 256) {
-      const int i = e / rso, n = e - i * rso;
-      if (c0 + i < g.n) {
-        double v = 0.0;
-        if (n < r)
-          for (int h = 0; h < P.ksplit; ++h) v += sO[(h * KC + i) * RBP + n];
-        a.out.p[(long)(c0 + i) * rso + n] = v;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-template <int RB>
-void kstage_launch(const KStageArgs& a, const double* isp, cudaStream_t st) {
-  const Geom& g = a.geo;
-  const int ns = g.ns;
-  const int ra = a.U0.p ? a.U0.cols : 0;
-  const bool sepu = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
-  constexpr int TILES = (KC / 8) * (RB / 8);
-  KParams P;
-  P.K = ns * a.X.cols + ra;
-  P.ksplit = (TILES % 8 == 0) ? 1 : 2;
-  P.K4 = (P.K + 4 * P.ksplit - 1) / (4 * P.ksplit) * (4 * P.ksplit);
-  P.KS = pad4(P.K4);
-  P.BS = pad4(RB);
-  const Stage S = make_stage<KC>(g, &a.X, 1, sepu ? &a.U0 : nullptr);
-  const size_t smem = (2 * (size_t)S.buf + (size_t)KC * P.KS + (size_t)P.K4 * P.BS +
-                       (size_t)P.ksplit * KC * (RB + 2)) * sizeof(double) + 64;
-  if (smem > 227 * 1024) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
-  CK(cudaFuncSetAttribute(kstage_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  const int nchunks = (g.n + KC - 1) / KC;
-  int grid = sm_count();
-  if (grid > nchunks) grid = nchunks;
-  kstage_kernel<RB><<<grid, 256, smem, st>>>(a, S, P, isp);
-  launched();
-}
-
-// ===================================================================== sgram
-constexpr int GC = 16;
-constexpr int GTL = pad4(GC);  // 20
-
-template <int T8>
-__global__ void __launch_bounds__(256, 1)
-    sgram_kernel(Geom g, NMat X1, NMat X2, Stage S, const double* __restrict__ isp,
-                 double* __restrict__ partial) {
-  constexpr int W = T8 * 8;
-  constexpr int TILES = 6 * T8 * T8;
-  constexpr int TPW = (TILES + 7) / 8;
-  extern __shared__ __align__(128) double sm[];
-  double* buf = sm;
-  double* sT = sm + 2 * S.buf;                 // [6][W][GTL]
-  uint64_t* bar = (uint64_t*)(sT + 6 * W * GTL);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int ns = g.ns, a1 = X1.cols, a2 = X2.p ? X2.cols : 0, w = a1 + a2;
-  const int nin = X2.p ? 2 : 1;
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_fence_init();
-  }
-  for (int i = tid; i < 6 * W * GTL; i += 256) sT[i] = 0.0;
-  __syncthreads();
-  double acc[TPW][2];
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
-  const int nchunks = (g.n + GC - 1) / GC;
-  if (tid == 0 && blockIdx.x < nchunks)
-    stage_chunk<GC>(S, buf, &bar[0], blockIdx.x * GC, X1, X2, nin, isp, X1);
-  int it = 0;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
-    const int b = it & 1;
-    const int next = chunk + gridDim.x;
-    if (tid == 0 && next < nchunks) {
-      fence_proxy_async();
-      stage_chunk<GC>(S, buf + (b ^ 1) * S.buf, &bar[b ^ 1], next * GC, X1, X2, nin, isp, X1);
-    }
-    mbar_wait(&bar[b], (it >> 1) & 1);
-    const double* B = buf + b * S.buf;
-    const double* Is = B + S.ioff;
-    const int c0 = chunk * GC;
-    for (int e = tid; e < GC * w; e += 256) {
-      const int i = e / w, j = e - i * w;
-      const int c = c0 + i;
-      double t[6] = {0, 0, 0, 0, 0, 0};
-      if (c < g.n) {
-        const CellCoord cc = coord_of(g, c);
-        if (j < a1) stencil6<GC>(g, cc, B + S.xoff[0], X1.rs, Is, i, j, t);
-        else stencil6<GC>(g, cc, B + S.xoff[1], X2.rs, Is, i, j - a1, t);
-      }
-#pragma unroll
-      for (int s = 0; s < 6; ++s)
-        if (s < ns) sT[(s * W + j) * GTL + i] = t[s];
-    }
-    __syncthreads();
-    // A = X^T from the centre rows (box 0 rows 2..GC+1); B = T_s
-    const int m0 = lane >> 2, kq = lane & 3;
-#pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      const int tile = warp + 8 * t;
-      if (tile < TILES) {
-        const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
-        const int ti = rem / T8, tj = rem - ti * T8;
-        if (s < ns) {
-          const int m = ti * 8 + m0;
-          const double* pa;
-          int ars;
-          if (m < a1) { pa = B + S.xoff[0] + 2 * X1.rs + m; ars = X1.rs; }
-          else if (m < w) { pa = B + S.xoff[1] + 2 * X2.rs + (m - a1); ars = X2.rs; }
-          else { pa = nullptr; ars = 0; }
-          const double* pb = sT + (s * W + tj * 8 + m0) * GTL + kq;
-#pragma unroll
-          for (int k0 = 0; k0 < GC; k0 += 4)
-            dmma884(acc[t][0], acc[t][1], pa ? pa[(k0 + kq) * ars] : 0.0, pb[k0]);
-        }
-      }
-    }
-    __syncthreads();
-  }
-  double* out = partial + (size_t)blockIdx.x * ns * w * w;
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int tile = warp + 8 * t;
-    if (tile < TILES) {
-      const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
-      const int ti = rem / T8, tj = rem - ti * T8;
-      const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
-      if (s < ns && row < w) {
-        double* o = out + ((size_t)s * w + row) * w;
-        if (col < w) o[col] = acc[t][0];
-        if (col + 1 < w) o[col + 1] = acc[t][1];
-      }
-    }
-  }
-}
 
 __global__ void reduce_blocks(const double* __restrict__ partial, int nblk, int count,
                               double* __restrict__ out) {
@@ -403,28 +28,6 @@ __global__ void reduce_blocks(const double* __restrict__ partial, int nblk, int 
   double s = 0.0;
   for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
   out[i] = s;
-}
-
-template <int T8>
-void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
-                  cudaStream_t st) {
-  const NMat ins[2] = {X1, X2};
-  const Stage S = make_stage<GC>(g, ins, X2.p ? 2 : 1, nullptr);
-  const int W = T8 * 8;
-  const size_t smem = (2 * (size_t)S.buf + (size_t)6 * W * GTL) * sizeof(double) + 64;
-  if (smem > 227 * 1024) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
-  CK(cudaFuncSetAttribute(sgram_kernel<T8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  const int nchunks = (g.n + GC - 1) / GC;
-  int grid = sm_count();
-  if (grid > nchunks) grid = nchunks;
-  const int w = X1.cols + (X2.p ? X2.cols : 0);
-  const size_t count = (size_t)g.ns * w * w;
-  double* part = partial.get(count * grid);
-  sgram_kernel<T8><<<grid, 256, smem, st>>>(g, X1, X2, S, isp, part);
-  launched();
-  reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
-  launched();
 }
 
 // ===================================================================== lincomb
@@ -825,50 +428,6 @@ int grid_for(long n, int block) {
 }
 
 }  // namespace
-
-void kstage(const KStageArgs& a, cudaStream_t st) {
-  // a.inv_s must point at the padded [1/S, 0] row array (Handle::isp)
-  const int r = a.out.cols;
-  if (a.X.cols > 32 || (a.U0.p && a.U0.cols > 32)) fail(PND_ECONFIG, "kstage supports <= 32 input columns");
-  if (r <= 8) kstage_launch<8>(a, a.inv_s, st);
-  else if (r <= 16) kstage_launch<16>(a, a.inv_s, st);
-  else if (r <= 24) kstage_launch<24>(a, a.inv_s, st);
-  else if (r <= 32) kstage_launch<32>(a, a.inv_s, st);
-  else if (r <= 64) kstage_launch<64>(a, a.inv_s, st);
-  else fail(PND_ECONFIG, "kstage supports at most 64 output columns");
-}
-
-void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* isp, double* out,
-                   DBuf& partial, cudaStream_t st) {
-  if (g.ns == 0) return;
-  const int w = X1.cols + (X2.p ? X2.cols : 0);
-  switch ((w + 7) / 8) {
-    case 1: sgram_launch<1>(g, X1, X2, isp, out, partial, st); break;
-    case 2: sgram_launch<2>(g, X1, X2, isp, out, partial, st); break;
-    case 3: sgram_launch<3>(g, X1, X2, isp, out, partial, st); break;
-    case 4: sgram_launch<4>(g, X1, X2, isp, out, partial, st); break;
-    case 5: sgram_launch<5>(g, X1, X2, isp, out, partial, st); break;
-    case 6: sgram_launch<6>(g, X1, X2, isp, out, partial, st); break;
-    default: fail(PND_ECONFIG, "stencil Grams support at most 48 columns");
-  }
-}
-
-void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* isp, double* out,
-                      DBuf& partial, cudaStream_t st) {
-  // Grams of [Y | X] against its stencils, then the (X, D Y) block
-  const int a = X.cols, b = Y.cols, w = a + b;
-  DBuf full;
-  double* f = full.get((size_t)g.ns * w * w);
-  stencil_grams(g, Y, X, isp, f, partial, st);
-  for (int s = 0; s < g.ns; ++s) {
-    // out[s] = f[s][b:, :b]
-    CK(cudaMemcpy2DAsync(out + (size_t)s * a * b, b * sizeof(double),
-                         f + (size_t)s * w * w + (size_t)b * w, w * sizeof(double),
-                         b * sizeof(double), a, cudaMemcpyDeviceToDevice, st));
-  }
-  CK(cudaStreamSynchronize(st));
-  full.free_();
-}
 
 void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
              NMat out, double* grams, DBuf& partial, cudaStream_t st) {

@@ -87,7 +87,7 @@ struct NBuf {
 
 inline int even(int c) { return (c + 1) & ~1; }
 
-// ------------------------------------------------------------ n-side kernels (nside.cu)
+// ------------------------------------------------------------ n-side kernels (stencil.cu, nside.cu)
 // K-phase Horner stage / full-rank streaming operator:
 //   out = [D_0 S^-1 X, ..., D_ns-1 S^-1 X | U0] . [M_0; ...; M_ns-1; S0]
 struct KStageArgs {
