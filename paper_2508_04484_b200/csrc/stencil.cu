@@ -38,7 +38,19 @@ struct Seg {
   int coff;        // smem offset of separate centre rows (-1: none)
   int total;       // doubles staged
   unsigned bytes;  // bytes per chunk
+  int cpp, nz;     // chunk order: cpp > 0 -> z-fastest (cpp chunks per z-plane)
 };
+
+// first cell of the p-th processed chunk. With whole chunks per z-plane the
+// chunks are visited z-fastest: the CTAs of one grid-stride step then cover
+// consecutive planes of the same (x, y) run, so the +-1/+-2 plane halo rows are
+// read by neighbouring CTAs at the same time (L2 hits) instead of
+// 2 planes apart in time (which falls out of L2 at 256^3).
+__device__ __forceinline__ int chunk_cell(const Seg& S, int p, int ch) {
+  if (S.cpp == 0) return p * ch;
+  const int zq = p % S.nz, r = p / S.nz;
+  return (zq * S.cpp + r) * ch;
+}
 
 template <int CH>
 Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre) {
@@ -72,6 +84,8 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre) {
   }
   s.total = up16(o);
   s.bytes = bytes;
+  s.cpp = (nxy % CH == 0 && g.nz > 1) ? nxy / CH : 0;
+  s.nz = g.nz;
   return s;
 }
 
@@ -97,78 +111,79 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
   if (S.coff >= 0) bulk_load(dst + S.coff, c.p + (long)c0 * c.rs, CH * c.rs * 8, bar);
 }
 
-// per-thread stencil context of one cell (its axis indices); the staged rows
-// are pre-scaled by 1/S (scale_rows), so f = S^-1 x is read directly
+// Per-thread stencil context of one cell for one chunk: the staged-row
+// pointers of its 1 + 4 NA stencil points (centre, then d = -2,-1,+1,+2 per
+// axis; column offset folded in), 1/S at those points, and the boundary class.
+// apply<FAST>() forms the 2 NA values D_s S^-1 x of column (col0 + off):
+// FAST = every cell of the warp is >= 2 cells from every face (branch-free
+// interior formula); otherwise the boundary closures of spatial.py:81-118.
 template <int CH, int NA>
 struct Ctx {
+  static constexpr int NP = 1 + 4 * NA;
+  const double* xr[NP];
+  double is[NP];
   int idx[NA], len[NA];
+  bool inner;
 
-  __device__ __forceinline__ void init(const Geom& g, int c) {
+  __device__ __forceinline__ static int row_of(int p, int i) {
+    if (p == 0) return i + 2;
+    const int ai = (p - 1) >> 2, q = (p - 1) & 3;
+    if (ai == 0) return i + (q < 2 ? q : q + 1);
+    return box_row<CH>(1 + 4 * (ai - 1) + q) + i;
+  }
+
+  __device__ __forceinline__ void init(const Geom& g, int c, int i, const double* I) {
     const int nxy = g.nx * g.ny;
     const int ck = c / nxy, rem = c - ck * nxy;
     const int cj = rem / g.nx, ci = rem - cj * g.nx;
+    inner = true;
 #pragma unroll
     for (int ai = 0; ai < NA; ++ai) {
       const int axis = g.axis[ai];
       idx[ai] = axis == 0 ? ci : axis == 1 ? cj : ck;
       len[ai] = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
+      inner = inner && idx[ai] >= 2 && idx[ai] <= len[ai] - 3;
     }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) is[p] = I[2 * row_of(p, i)];
   }
 
-  // the 2 NA stencil values of column j (staged rows X with row length rs)
-  __device__ __forceinline__ void apply(const Geom& g, const double* X, int rs, int i, int j,
-                                        double* t) const {
+  // rows of input X (row length rs), column offset col0 folded in
+  __device__ __forceinline__ void rows(const double* X, int rs, int i, int col0) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) xr[p] = X + row_of(p, i) * rs + col0;
+  }
+
+  template <bool FAST>
+  __device__ __forceinline__ void apply(const Geom& g, int off, double* t) const {
+    const double fc = xr[0][off] * is[0];
 #pragma unroll
     for (int ai = 0; ai < NA; ++ai) {
-      double f[5];
-      if (ai == 0) {
-#pragma unroll
-        for (int d = 0; d < 5; ++d) f[d] = X[(i + d) * rs + j];
-      } else {
-        const int b = 1 + 4 * (ai - 1);
-        f[0] = X[(box_row<CH>(b) + i) * rs + j];
-        f[1] = X[(box_row<CH>(b + 1) + i) * rs + j];
-        f[2] = X[(i + 2) * rs + j];
-        f[3] = X[(box_row<CH>(b + 2) + i) * rs + j];
-        f[4] = X[(box_row<CH>(b + 3) + i) * rs + j];
-      }
-      const int id = idx[ai], ln = len[ai];
+      const double f0 = xr[1 + 4 * ai][off] * is[1 + 4 * ai];
+      const double f1 = xr[2 + 4 * ai][off] * is[2 + 4 * ai];
+      const double f3 = xr[3 + 4 * ai][off] * is[3 + 4 * ai];
+      const double f4 = xr[4 + 4 * ai][off] * is[4 + 4 * ai];
       const int axis = g.axis[ai];
       const double ih = axis == 0 ? g.ih[0] : axis == 1 ? g.ih[1] : g.ih[2];
       const double i2h = axis == 0 ? g.i2h[0] : axis == 1 ? g.i2h[1] : g.i2h[2];
       double tp, tm;
-      if (id >= 2) tp = (3.0 * f[2] - 4.0 * f[1] + f[0]) * i2h;
-      else if (id == 1) tp = (f[2] - f[1]) * ih;
-      else tp = f[2] * ih;
-      if (id <= ln - 3) tm = (-3.0 * f[2] + 4.0 * f[3] - f[4]) * i2h;
-      else if (id == ln - 2) tm = (f[3] - f[2]) * ih;
-      else tm = -f[2] * ih;
+      if (FAST) {
+        tp = (3.0 * fc - 4.0 * f1 + f0) * i2h;
+        tm = (-3.0 * fc + 4.0 * f3 - f4) * i2h;
+      } else {
+        const int id = idx[ai], ln = len[ai];
+        if (id >= 2) tp = (3.0 * fc - 4.0 * f1 + f0) * i2h;
+        else if (id == 1) tp = (fc - f1) * ih;
+        else tp = fc * ih;
+        if (id <= ln - 3) tm = (-3.0 * fc + 4.0 * f3 - f4) * i2h;
+        else if (id == ln - 2) tm = (f3 - fc) * ih;
+        else tm = -fc * ih;
+      }
       t[2 * ai] = tp;
       t[2 * ai + 1] = tm;
     }
   }
 };
-
-// in-place X[row][:] *= 1/S[row] over the staged rows of one input; calls
-// keep(row, col, unscaled value) first (the kstage base rows)
-template <class Keep>
-__device__ __forceinline__ void scale_rows(double* X, int rs, int nrows, const double* I,
-                                           Keep keep) {
-  const int total = nrows * rs;
-  const int drow = blockDim.x / rs, dcol = blockDim.x - drow * rs;
-  int row = threadIdx.x / rs, col = threadIdx.x - row * rs;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    const double v = X[e];
-    keep(row, col, v);
-    X[e] = v * I[2 * row];
-    row += drow;
-    col += dcol;
-    if (col >= rs) {
-      col -= rs;
-      ++row;
-    }
-  }
-}
 
 template <class Kern>
 int resident(Kern k, int threads, size_t smem) {
@@ -177,87 +192,191 @@ int resident(Kern k, int threads, size_t smem) {
   return nb < 1 ? 1 : nb;
 }
 
-// ===================================================================== kstage
-constexpr int KC = 32;
-constexpr int KCS = pad4(KC);  // 36: k-major A tile row length
+// ============================================================ pipeline roles
+// Both stencil kernels are warp-specialized, one persistent CTA per SM:
+//   1 producer warp: lane 0 issues the bulk copies of each chunk into a ring
+//     of NSTG staging buffers (sfull[s] completes on the bytes, sempty[s] on
+//     the 8 former-warp releases);
+//   8 "former" warps: wait for chunk k's staging, write its stencil features
+//     F[f] (f = k & 1, double-buffered), release the staging buffer;
+//   contraction warps: DMMA over F[f] while the formers work on k+1.
+// Warps signal with one elected lane after __syncwarp; there is no CTA-wide
+// barrier after the prologue.
+constexpr int FORMW = 8;             // former warps
+constexpr int CONW = 4;              // kstage contraction warps
+constexpr int PTH = 32 * (FORMW + CONW + 1);
+constexpr int GCONW = 7;             // sgram contraction warps (16 warps in all)
+constexpr int GPTH = 32 * (FORMW + GCONW + 1);
+constexpr int NSTG_MAX = 4;
 
-template <int NA, int RB>
-__global__ void __launch_bounds__(256, 2)
-    kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
-                  int K4, Seg S, const double* __restrict__ isp) {
-  constexpr int NS = 2 * NA;
-  constexpr int NT = RB / 8;
-  constexpr int TILES = (KC / 8) * NT;
-  extern __shared__ __align__(128) double sm[];
-  double* buf = sm;
-  double* sA = sm + S.total;                 // [K4][KCS] k-major
-  uint64_t* bar = (uint64_t*)(sA + K4 * KCS);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int xc = X.cols, ra = U0.p ? U0.cols : 0, rso = out.rs;
-  if (tid == 0) {
-    mbar_init(bar, 1);
+struct PipeBars {
+  uint64_t sfull[NSTG_MAX], sempty[NSTG_MAX], ffull[2], fempty[2];
+};
+
+// staging ring depth that fits next to `fixed` bytes of shared memory
+int stages_for(size_t fixed, int stage_doubles) {
+  const size_t cap = 227 * 1024;
+  int n = 0;
+  while (n < NSTG_MAX && fixed + (size_t)(n + 1) * stage_doubles * sizeof(double) <= cap) ++n;
+  return n;
+}
+
+__device__ __forceinline__ void pipe_init(PipeBars* pb, int nstg, int conw) {
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < nstg; ++b) {
+      mbar_init(&pb->sfull[b], 1);
+      mbar_init(&pb->sempty[b], FORMW);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&pb->ffull[b], FORMW);
+      mbar_init(&pb->fempty[b], conw);
+    }
     mbar_fence_init();
   }
-  for (int i = tid; i < (K4 - K) * KCS; i += 256) sA[K * KCS + i] = 0.0;
+}
+
+// ring position of iteration it: slot s, use count k (phase parity k & 1)
+struct Ring {
+  int s = 0, k = 0, n;
+  __device__ explicit Ring(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++s == n) {
+      s = 0;
+      ++k;
+    }
+  }
+};
+
+// one elected lane signals for the whole warp
+__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+}
+
+// ===================================================================== kstage
+// out = [D_0 S^-1 X, ..., D_ns-1 S^-1 X | U0] . Bcat, Bcat = [M_0; ...; M_ns-1; S0]
+// (zero-padded to K4 x RB). Chunk = 32 cells; F[b] = [K4][36] k-major.
+// Former lane = (cell 4w + (lane & 3), column (lane >> 2) + 8t): conflict-free
+// reads of the staged rows and writes of F. Contraction warp m owns m-tile m,
+// all NT n-tiles, k-steps split even/odd over two accumulator sets (2 NT
+// independent DMMA chains).
+constexpr int KC = 32;
+constexpr int KCS = pad4(KC);  // 36
+
+template <int NA, int RB>
+__global__ void __launch_bounds__(PTH, 1)
+    kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
+                  int K4, Seg S, int nstg, const double* __restrict__ isp) {
+  constexpr int NS = 2 * NA;
+  constexpr int NT = RB / 8;
+  extern __shared__ __align__(128) double sm[];
+  // staging slot s: sm + s S.total; feature buffer f: F0 + f K4 KCS
+  double* const F0 = sm + nstg * S.total;
+  PipeBars* pb = reinterpret_cast<PipeBars*>(F0 + 2 * K4 * KCS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int xc = X.cols, ra = U0.p ? U0.cols : 0;
+  pipe_init(pb, nstg, CONW);
+  for (int i = tid; i < (K4 - K) * KCS; i += PTH) {
+    F0[K * KCS + i] = 0.0;
+    F0[K4 * KCS + K * KCS + i] = 0.0;
+  }
   __syncthreads();
   const bool sepc = S.coff >= 0;
   const int nchunks = (g.n + KC - 1) / KC;
-  int it = 0;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
-    const int c0 = chunk * KC;
-    if (tid == 0) {
-      fence_proxy_async();
-      issue_seg<KC, NA>(S, buf, bar, c0, X, X, 1, isp, U0);
-    }
-    mbar_wait(bar, it & 1);
-    // rows past n (chunk tail) read zero halo rows; their results are not stored
-    double* Xs = buf + S.xoff[0];
-    double* base = sA + NS * xc * KCS;
-    if (sepc) {
-      for (int e = tid; e < ra * KC; e += 256) {
-        const int j = e / KC, i = e - j * KC;
-        base[j * KCS + i] = buf[S.coff + i * U0.rs + j];
+
+  if (warp == FORMW + CONW) {
+    if (lane == 0) {
+      Ring r(nstg);
+      for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+        if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
+        issue_seg<KC, NA>(S, sm + r.s * S.total, &pb->sfull[r.s], chunk_cell(S, chunk, KC), X, X,
+                          1, isp, U0);
       }
-      scale_rows(Xs, X.rs, S.nrows, buf + S.ioff, [](int, int, double) {});
-    } else {
-      scale_rows(Xs, X.rs, S.nrows, buf + S.ioff, [&](int row, int col, double v) {
-        if (row >= 2 && row < KC + 2 && col < ra) base[col * KCS + row - 2] = v;
-      });
     }
-    __syncthreads();
-    const int i = lane;
-    Ctx<KC, NA> cx;
-    cx.init(g, c0 + i);
-    for (int j = warp; j < xc; j += 8) {
-      double t[NS];
-      cx.apply(g, Xs, X.rs, i, j, t);
+  } else if (warp < FORMW) {
+    const int ci = 4 * warp + (lane & 3), cj = lane >> 2;
+    Ring r(nstg);
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it, r.next()) {
+      const int f = it & 1, u = it >> 1;
+      const int c0 = chunk_cell(S, chunk, KC);
+      mbar_wait(&pb->sfull[r.s], r.k & 1);
+      if (u >= 1) mbar_wait(&pb->fempty[f], (u - 1) & 1);
+      const double* sb = sm + r.s * S.total;
+      const double* Xs = sb + S.xoff[0];
+      double* Fb = F0 + f * K4 * KCS;
+      double* base = Fb + NS * xc * KCS;
+      // base rows = unscaled centre rows (rows past n are zero halo rows; their
+      // results are not stored)
+      if (sepc) {
+        for (int j = cj; j < ra; j += 8) base[j * KCS + ci] = sb[S.coff + ci * U0.rs + j];
+      } else {
+        for (int j = cj; j < ra; j += 8) base[j * KCS + ci] = Xs[(ci + 2) * X.rs + j];
+      }
+      Ctx<KC, NA> cx;
+      cx.init(g, c0 + ci, ci, sb + S.ioff);
+      cx.rows(Xs, X.rs, ci, cj);
+      const bool fast = __all_sync(0xffffffffu, cx.inner);
 #pragma unroll
-      for (int s = 0; s < NS; ++s) sA[(s * xc + j) * KCS + i] = t[s];
-    }
-    __syncthreads();
-    for (int tile = warp; tile < TILES; tile += 8) {
-      const int mt = tile / NT, nt = tile - mt * NT;
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      const double* pa = sA + (lane & 3) * KCS + mt * 8 + (lane >> 2);
-      const double* pb = Bcat + (lane & 3) * RB + nt * 8 + (lane >> 2);
-      int k0 = 0;
-      for (; k0 + 8 <= K4; k0 += 8) {
-        dmma884(d0, d1, pa[k0 * KCS], __ldg(pb + k0 * RB));
-        dmma884(e0, e1, pa[(k0 + 4) * KCS], __ldg(pb + (k0 + 4) * RB));
+      for (int t = 0; t < RB / 8; ++t) {
+        const int j = cj + 8 * t;
+        if (j < xc) {
+          double v[NS];
+          if (fast) cx.template apply<true>(g, 8 * t, v);
+          else cx.template apply<false>(g, 8 * t, v);
+#pragma unroll
+          for (int s = 0; s < NS; ++s) Fb[(s * xc + j) * KCS + ci] = v[s];
+        }
       }
-      if (k0 < K4) dmma884(d0, d1, pa[k0 * KCS], __ldg(pb + k0 * RB));
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&pb->ffull[f]);
+        mbar_arrive(&pb->sempty[r.s]);
+      }
+    }
+  } else {
+    const int mt = warp - FORMW;
+    const int nks = K4 / 4;
+    const double* pb0 = Bcat + (lane & 3) * RB + (lane >> 2);
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+      const int b = it & 1, u = it >> 1;
+      const int c0 = chunk_cell(S, chunk, KC);
+      mbar_wait(&pb->ffull[b], u & 1);
+      double acc[2][NT][2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+      const double* pa = F0 + b * K4 * KCS + (lane & 3) * KCS + mt * 8 + (lane >> 2);
+#pragma unroll 2
+      for (int ks = 0; ks < nks; ks += 2) {
+        const double a0 = pa[ks * 4 * KCS], a1 = pa[(ks + 1) * 4 * KCS];
+        double b0[NT], b1[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          b0[nt] = __ldg(pb0 + ks * 4 * RB + nt * 8);
+          b1[nt] = __ldg(pb0 + (ks + 1) * 4 * RB + nt * 8);
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dmma884(acc[0][nt][0], acc[0][nt][1], a0, b0[nt]);
+          dmma884(acc[1][nt][0], acc[1][nt][1], a1, b1[nt]);
+        }
+      }
+      warp_arrive(&pb->fempty[b]);
       const int row = c0 + mt * 8 + (lane >> 2);
-      const int n = nt * 8 + 2 * (lane & 3);
       if (row < g.n) {
-        double* o = out.p + (long)row * rso + n;
-        if (n + 1 < rso) {
-          *reinterpret_cast<double2*>(o) = make_double2(d0 + e0, d1 + e1);
-        } else if (n < rso) {
-          o[0] = d0 + e0;
+        double* o = out.p + (long)row * out.rs;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int n = nt * 8 + 2 * (lane & 3);
+          const double v0 = acc[0][nt][0] + acc[1][nt][0], v1 = acc[0][nt][1] + acc[1][nt][1];
+          if (n + 1 < out.rs) *reinterpret_cast<double2*>(o + n) = make_double2(v0, v1);
+          else if (n < out.rs) o[n] = v0;
         }
       }
     }
-    __syncthreads();
   }
 }
 
@@ -285,20 +404,23 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.S0, ra, a.out.cols, K4, RB, B);
   launched();
   const Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
-  const size_t smem = ((size_t)S.total + (size_t)K4 * KCS) * sizeof(double) + 16;
-  if (smem > 227 * 1024) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
+  const size_t fixed = 2 * (size_t)K4 * KCS * sizeof(double) + sizeof(PipeBars);
+  const int nstg = stages_for(fixed, S.total);
+  if (nstg < 2) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
+  const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
   CK(cudaFuncSetAttribute(kstage_kernel<NA, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const int nchunks = (g.n + KC - 1) / KC;
-  int grid = sm_count() * resident(kstage_kernel<NA, RB>, 256, smem);
+  int grid = sm_count() * resident(kstage_kernel<NA, RB>, PTH, smem);
   if (grid > nchunks) grid = nchunks;
-  kstage_kernel<NA, RB><<<grid, 256, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S, a.inv_s);
+  kstage_kernel<NA, RB><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S, nstg,
+                                                  a.inv_s);
   launched();
 }
 
 template <int NA>
 void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
-  const int r = a.out.cols;
+  const int r = a.out.cols > a.X.cols ? a.out.cols : a.X.cols;
   if (r <= 8) kstage_launch<NA, 8>(a, bcat, st);
   else if (r <= 16) kstage_launch<NA, 16>(a, bcat, st);
   else if (r <= 24) kstage_launch<NA, 24>(a, bcat, st);
@@ -307,97 +429,147 @@ void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
 }
 
 // ===================================================================== sgram
+// G_s = [X1 | X2]^T D_s S^-1 [X1 | X2]. Chunk = 16 cells; per buffer b:
+// F[b] = [NS W][20] stencil features (k = cell), C[b] = [16][pad4(W)] unscaled
+// centre rows (the A = X^T operand). Contraction warp m (of 7) owns the
+// stencil-column tiles bt = bt0 + m + 7u (bt = s T8 + tj) against all T8 row tiles, one
+// accumulator per tile (T8 UPW independent chains); launches cover column-tile
+// ranges of at most 32 tiles.
 constexpr int GC = 16;
 constexpr int GTL = pad4(GC);  // 20
 
 template <int NA, int T8>
-__global__ void __launch_bounds__(256, T8 <= 5 ? 2 : 1)
-    sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, const double* __restrict__ isp,
-                 double* __restrict__ partial) {
+__global__ void __launch_bounds__(GPTH, 1)
+    sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, int nstg, const double* __restrict__ isp,
+                 int bt0, int nbt, double* __restrict__ partial) {
   constexpr int NS = 2 * NA;
   constexpr int W = T8 * 8;
-  constexpr int TILES = NS * T8 * T8;
-  constexpr int TPW = (TILES + 7) / 8;
-  extern __shared__ __align__(128) double sm[];
-  double* buf = sm;
   constexpr int XS = pad4(W);
-  double* sT = sm + S.total;                   // [NS][W][GTL] stencils, k = cell
-  double* sX = sT + NS * W * GTL;              // [GC][XS] unscaled centre rows
-  uint64_t* bar = (uint64_t*)(sX + GC * XS);
+  constexpr int NBMAX = 32;
+  constexpr int UPW = ((NS * T8 < NBMAX ? NS * T8 : NBMAX) + GCONW - 1) / GCONW;
+  constexpr int FT = NS * W * GTL + GC * XS;  // doubles per feature buffer
+  extern __shared__ __align__(128) double sm[];
+  // staging slot s: sm + s S.total; feature buffer f: F0 + f FT
+  double* const F0 = sm + nstg * S.total;
+  PipeBars* pb = reinterpret_cast<PipeBars*>(F0 + 2 * FT);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int a1 = X1.cols, a2 = X2.p ? X2.cols : 0, w = a1 + a2;
   const int nin = X2.p ? 2 : 1;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-  }
-  for (int i = tid; i < NS * W * GTL + GC * XS; i += 256) sT[i] = 0.0;
+  pipe_init(pb, nstg, GCONW);
+  for (int i = tid; i < 2 * FT; i += GPTH) F0[i] = 0.0;
   __syncthreads();
-  double acc[TPW][2];
-#pragma unroll
-  for (int t = 0; t < TPW; ++t) acc[t][0] = acc[t][1] = 0.0;
   const int nchunks = (g.n + GC - 1) / GC;
-  const int i = lane & (GC - 1), jh = lane >> 4;
-  int it = 0;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
-    const int c0 = chunk * GC;
-    if (tid == 0) {
-      fence_proxy_async();
-      issue_seg<GC, NA>(S, buf, bar, c0, X1, X2, nin, isp, X1);
-    }
-    mbar_wait(bar, it & 1);
-    // keep the unscaled centre rows (the A = X^T operand), then scale by 1/S;
-    // rows past n are zero halo rows and contribute nothing
-    {
-      double* X1s = buf + S.xoff[0];
-      scale_rows(X1s, X1.rs, S.nrows, buf + S.ioff, [&](int row, int col, double v) {
-        if (row >= 2 && row < GC + 2 && col < a1) sX[(row - 2) * XS + col] = v;
-      });
-      if (a2)
-        scale_rows(buf + S.xoff[1], X2.rs, S.nrows, buf + S.ioff,
-                   [&](int row, int col, double v) {
-                     if (row >= 2 && row < GC + 2 && col < a2) sX[(row - 2) * XS + a1 + col] = v;
-                   });
-    }
-    __syncthreads();
-    Ctx<GC, NA> cx;
-    cx.init(g, c0 + i);
-    for (int j = 2 * warp + jh; j < w; j += 16) {
-      double t[NS];
-      if (j < a1) cx.apply(g, buf + S.xoff[0], X1.rs, i, j, t);
-      else cx.apply(g, buf + S.xoff[1], X2.rs, i, j - a1, t);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) sT[(s * W + j) * GTL + i] = t[s];
-    }
-    __syncthreads();
-    // A = X^T: fragment (m = column, k = cell) from the unscaled centre rows
-    const int m0 = lane >> 2, kq = lane & 3;
-#pragma unroll
-    for (int t = 0; t < TPW; ++t) {
-      const int tile = warp + 8 * t;
-      if (tile < TILES) {
-        const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
-        const int ti = rem / T8, tj = rem - ti * T8;
-        const double* pa = sX + kq * XS + ti * 8 + m0;
-        const double* pb = sT + (s * W + tj * 8 + m0) * GTL + kq;
-#pragma unroll
-        for (int k0 = 0; k0 < GC; k0 += 4) dmma884(acc[t][0], acc[t][1], pa[k0 * XS], pb[k0]);
+
+  if (warp == FORMW + GCONW) {
+    if (lane == 0) {
+      Ring r(nstg);
+      for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+        if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
+        issue_seg<GC, NA>(S, sm + r.s * S.total, &pb->sfull[r.s], chunk_cell(S, chunk, GC), X1,
+                          X2, nin, isp, X1);
       }
     }
-    __syncthreads();
-  }
-  double* out = partial + (size_t)blockIdx.x * NS * w * w;
+  } else if (warp < FORMW) {
+    // lane = (cell 4 (w & 3) + (lane & 3), column (lane >> 2) + 8 (w >> 2) + 16 t)
+    const int ci = 4 * (warp & 3) + (lane & 3), cj = (lane >> 2) + 8 * (warp >> 2);
+    Ring r(nstg);
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it, r.next()) {
+      const int f = it & 1, u = it >> 1;
+      const int c0 = chunk_cell(S, chunk, GC);
+      mbar_wait(&pb->sfull[r.s], r.k & 1);
+      if (u >= 1) mbar_wait(&pb->fempty[f], (u - 1) & 1);
+      const double* sb = sm + r.s * S.total;
+      const double* X1s = sb + S.xoff[0];
+      const double* X2s = sb + S.xoff[1];
+      double* Fb = F0 + f * FT;
+      double* Cb = Fb + NS * W * GTL;
+      // unscaled centre rows (A operand); rows past n are zero halo rows
+      for (int j = cj; j < w; j += 16)
+        Cb[ci * XS + j] = j < a1 ? X1s[(ci + 2) * X1.rs + j] : X2s[(ci + 2) * X2.rs + j - a1];
+      Ctx<GC, NA> cx;
+      cx.init(g, c0 + ci, ci, sb + S.ioff);
+      const bool fast = __all_sync(0xffffffffu, cx.inner);
+      constexpr int TT = (W + 15) / 16;
+      cx.rows(X1s, X1.rs, ci, cj);
 #pragma unroll
-  for (int t = 0; t < TPW; ++t) {
-    const int tile = warp + 8 * t;
-    if (tile < TILES) {
-      const int s = tile / (T8 * T8), rem = tile - s * T8 * T8;
-      const int ti = rem / T8, tj = rem - ti * T8;
-      const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
-      if (row < w) {
-        double* o = out + ((size_t)s * w + row) * w;
-        if (col < w) o[col] = acc[t][0];
-        if (col + 1 < w) o[col + 1] = acc[t][1];
+      for (int t = 0; t < TT; ++t) {
+        const int j = cj + 16 * t;
+        if (j < a1) {
+          double v[NS];
+          if (fast) cx.template apply<true>(g, 16 * t, v);
+          else cx.template apply<false>(g, 16 * t, v);
+#pragma unroll
+          for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
+        }
+      }
+      if (a2) {
+        const int j0 = cj >= a1 ? cj : cj + 16 * ((a1 - cj + 15) / 16);
+        cx.rows(X2s, X2.rs, ci, j0 - a1);
+#pragma unroll
+        for (int t = 0; t < TT; ++t) {
+          const int j = j0 + 16 * t;
+          if (j < w) {
+            double v[NS];
+            if (fast) cx.template apply<true>(g, 16 * t, v);
+            else cx.template apply<false>(g, 16 * t, v);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&pb->ffull[f]);
+        mbar_arrive(&pb->sempty[r.s]);
+      }
+    }
+  } else {
+    const int m = warp - FORMW;
+    double acc[UPW][T8][2];
+#pragma unroll
+    for (int q = 0; q < UPW; ++q)
+#pragma unroll
+      for (int ti = 0; ti < T8; ++ti) acc[q][ti][0] = acc[q][ti][1] = 0.0;
+    const int m0 = lane >> 2, kq = lane & 3;
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+      const int b = it & 1, u = it >> 1;
+      mbar_wait(&pb->ffull[b], u & 1);
+      const double* pa = F0 + b * FT + NS * W * GTL + kq * XS + m0;
+      const double* pbt = F0 + b * FT + ((bt0 + m) * 8 + m0) * GTL + kq;
+#pragma unroll 1
+      for (int k0 = 0; k0 < GC; k0 += 4) {
+        double af[T8];
+#pragma unroll
+        for (int ti = 0; ti < T8; ++ti) af[ti] = pa[k0 * XS + ti * 8];
+#pragma unroll
+        for (int q = 0; q < UPW; ++q) {
+          if (m + GCONW * q < nbt) {
+            const double bf = pbt[q * GCONW * 8 * GTL + k0];
+#pragma unroll
+            for (int ti = 0; ti < T8; ++ti) dmma884(acc[q][ti][0], acc[q][ti][1], af[ti], bf);
+          }
+        }
+      }
+      warp_arrive(&pb->fempty[b]);
+    }
+    double* out = partial + (size_t)blockIdx.x * NS * w * w;
+#pragma unroll
+    for (int q = 0; q < UPW; ++q) {
+      if (m + GCONW * q < nbt) {
+        const int bt = bt0 + m + GCONW * q;
+        const int s = bt / T8, tj = bt - s * T8;
+        const int col = tj * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int ti = 0; ti < T8; ++ti) {
+          const int row = ti * 8 + (lane >> 2);
+          if (row < w) {
+            double* o = out + ((size_t)s * w + row) * w;
+            if (col < w) o[col] = acc[q][ti][0];
+            if (col + 1 < w) o[col + 1] = acc[q][ti][1];
+          }
+        }
       }
     }
   }
@@ -418,19 +590,25 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const NMat ins[2] = {X1, X2};
   const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr);
   const int W = T8 * 8;
-  const size_t smem =
-      ((size_t)S.total + (size_t)2 * NA * W * GTL + (size_t)GC * pad4(W)) * sizeof(double) + 16;
-  if (smem > 227 * 1024) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
+  const size_t ft = (size_t)2 * NA * W * GTL + (size_t)GC * pad4(W);
+  const size_t fixed = 2 * ft * sizeof(double) + sizeof(PipeBars);
+  const int nstg = stages_for(fixed, S.total);
+  if (nstg < 2) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
+  const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
   CK(cudaFuncSetAttribute(sgram_kernel<NA, T8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const int nchunks = (g.n + GC - 1) / GC;
-  int grid = sm_count() * resident(sgram_kernel<NA, T8>, 256, smem);
+  int grid = sm_count() * resident(sgram_kernel<NA, T8>, GPTH, smem);
   if (grid > nchunks) grid = nchunks;
   const int w = X1.cols + (X2.p ? X2.cols : 0);
   const size_t count = (size_t)2 * NA * w * w;
   double* part = partial.get(count * grid);
-  sgram_kernel<NA, T8><<<grid, 256, smem, st>>>(g, X1, X2, S, isp, part);
-  launched();
+  const int nb = 2 * NA * T8;
+  for (int bt0 = 0; bt0 < nb; bt0 += 32) {
+    const int nbt = nb - bt0 < 32 ? nb - bt0 : 32;
+    sgram_kernel<NA, T8><<<grid, GPTH, smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part);
+    launched();
+  }
   reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
   launched();
 }
