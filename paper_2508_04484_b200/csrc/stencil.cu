@@ -117,7 +117,7 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
 // apply<FAST>() forms the 2 NA values D_s S^-1 x of column (col0 + off):
 // FAST = every cell of the warp is >= 2 cells from every face (branch-free
 // interior formula); otherwise the boundary closures of spatial.py:81-118.
-template <int CH, int NA>
+template <int CH, int NA, bool PRE = false>
 struct Ctx {
   static constexpr int NP = 1 + 4 * NA;
   const double* xr[NP];
@@ -144,8 +144,10 @@ struct Ctx {
       len[ai] = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
       inner = inner && idx[ai] >= 2 && idx[ai] <= len[ai] - 3;
     }
+    if (!PRE) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) is[p] = I[2 * row_of(p, i)];
+      for (int p = 0; p < NP; ++p) is[p] = I[2 * row_of(p, i)];
+    }
   }
 
   // rows of input X (row length rs), column offset col0 folded in
@@ -156,13 +158,14 @@ struct Ctx {
 
   template <bool FAST>
   __device__ __forceinline__ void apply(const Geom& g, int off, double* t) const {
-    const double fc = xr[0][off] * is[0];
+    // PRE: the staged rows already hold S^-1 x
+    const double fc = PRE ? xr[0][off] : xr[0][off] * is[0];
 #pragma unroll
     for (int ai = 0; ai < NA; ++ai) {
-      const double f0 = xr[1 + 4 * ai][off] * is[1 + 4 * ai];
-      const double f1 = xr[2 + 4 * ai][off] * is[2 + 4 * ai];
-      const double f3 = xr[3 + 4 * ai][off] * is[3 + 4 * ai];
-      const double f4 = xr[4 + 4 * ai][off] * is[4 + 4 * ai];
+      const double f0 = PRE ? xr[1 + 4 * ai][off] : xr[1 + 4 * ai][off] * is[1 + 4 * ai];
+      const double f1 = PRE ? xr[2 + 4 * ai][off] : xr[2 + 4 * ai][off] * is[2 + 4 * ai];
+      const double f3 = PRE ? xr[3 + 4 * ai][off] : xr[3 + 4 * ai][off] * is[3 + 4 * ai];
+      const double f4 = PRE ? xr[4 + 4 * ai][off] : xr[4 + 4 * ai][off] * is[4 + 4 * ai];
       const int axis = g.axis[ai];
       const double ih = axis == 0 ? g.ih[0] : axis == 1 ? g.ih[1] : g.ih[2];
       const double i2h = axis == 0 ? g.i2h[0] : axis == 1 ? g.i2h[1] : g.i2h[2];
@@ -258,27 +261,35 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar) {
 // (zero-padded to K4 x RB). Chunk = 32 cells; F[b] = [K4][36] k-major.
 // Former lane = (cell 4w + (lane & 3), column (lane >> 2) + 8t): conflict-free
 // reads of the staged rows and writes of F. Contraction warp m owns m-tile m,
-// all NT n-tiles, k-steps split even/odd over two accumulator sets (2 NT
-// independent DMMA chains).
+// all NT n-tiles, k-steps dealt round-robin to four accumulator sets (4 NT
+// independent DMMA chains); B fragments come from a shared-memory copy of
+// Bcat in fragment order.
 constexpr int KC = 32;
 constexpr int KCS = pad4(KC);  // 36
 
-template <int NA, int RB>
+template <int NA, int RB, bool PRE>
 __global__ void __launch_bounds__(PTH, 1)
     kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
-                  int K4, Seg S, int nstg, const double* __restrict__ isp) {
+                  int K4, Seg S, int nstg, const double* __restrict__ isp, int oscale) {
   constexpr int NS = 2 * NA;
   constexpr int NT = RB / 8;
   extern __shared__ __align__(128) double sm[];
   // staging slot s: sm + s S.total; feature buffer f: F0 + f K4 KCS
   double* const F0 = sm + nstg * S.total;
-  PipeBars* pb = reinterpret_cast<PipeBars*>(F0 + 2 * K4 * KCS);
+  // Bcat in DMMA B-fragment order: sB[(ks NT + nt) 32 + lane] =
+  // Bcat[4 ks + (lane & 3)][8 nt + (lane >> 2)] (one contiguous 256-byte load each)
+  double* const sB = F0 + 2 * K4 * KCS;
+  PipeBars* pb = reinterpret_cast<PipeBars*>(sB + K4 * RB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xc = X.cols, ra = U0.p ? U0.cols : 0;
   pipe_init(pb, nstg, CONW);
   for (int i = tid; i < (K4 - K) * KCS; i += PTH) {
     F0[K * KCS + i] = 0.0;
     F0[K4 * KCS + K * KCS + i] = 0.0;
+  }
+  for (int i = tid; i < K4 * RB; i += PTH) {
+    const int l = i & 31, f = i >> 5, ks = f / NT, nt = f - ks * NT;
+    sB[i] = Bcat[(4 * ks + (l & 3)) * RB + 8 * nt + (l >> 2)];
   }
   __syncthreads();
   const bool sepc = S.coff >= 0;
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(PTH, 1)
       } else {
         for (int j = cj; j < ra; j += 8) base[j * KCS + ci] = Xs[(ci + 2) * X.rs + j];
       }
-      Ctx<KC, NA> cx;
+      Ctx<KC, NA, PRE> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       cx.rows(Xs, X.rs, ci, cj);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
@@ -337,41 +348,50 @@ __global__ void __launch_bounds__(PTH, 1)
   } else {
     const int mt = warp - FORMW;
     const int nks = K4 / 4;
-    const double* pb0 = Bcat + (lane & 3) * RB + (lane >> 2);
+    const double* pb0 = sB + lane;
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
       const int b = it & 1, u = it >> 1;
       const int c0 = chunk_cell(S, chunk, KC);
       mbar_wait(&pb->ffull[b], u & 1);
-      double acc[2][NT][2];
+      double acc[4][NT][2];  // four k-step phases x NT tiles: 4 NT independent chains
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < 4; ++h)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
       const double* pa = F0 + b * K4 * KCS + (lane & 3) * KCS + mt * 8 + (lane >> 2);
-#pragma unroll 2
-      for (int ks = 0; ks < nks; ks += 2) {
-        const double a0 = pa[ks * 4 * KCS], a1 = pa[(ks + 1) * 4 * KCS];
-        double b0[NT], b1[NT];
+#pragma unroll 1
+      for (int ks = 0; ks < nks; ks += 4) {
+        double av[4], bv[4][NT];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          b0[nt] = __ldg(pb0 + ks * 4 * RB + nt * 8);
-          b1[nt] = __ldg(pb0 + (ks + 1) * 4 * RB + nt * 8);
+        for (int h = 0; h < 4; ++h) {
+          av[h] = pa[(ks + h) * 4 * KCS];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) bv[h][nt] = pb0[((ks + h) * NT + nt) * 32];
         }
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          dmma884(acc[0][nt][0], acc[0][nt][1], a0, b0[nt]);
-          dmma884(acc[1][nt][0], acc[1][nt][1], a1, b1[nt]);
-        }
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[h][nt][0], acc[h][nt][1], av[h], bv[h][nt]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        acc[0][nt][0] += acc[1][nt][0] + (acc[2][nt][0] + acc[3][nt][0]);
+        acc[0][nt][1] += acc[1][nt][1] + (acc[2][nt][1] + acc[3][nt][1]);
       }
       warp_arrive(&pb->fempty[b]);
       const int row = c0 + mt * 8 + (lane >> 2);
       if (row < g.n) {
         double* o = out.p + (long)row * out.rs;
+        const double is = oscale ? __ldg(isp + 2 * (long)row) : 1.0;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           const int n = nt * 8 + 2 * (lane & 3);
-          const double v0 = acc[0][nt][0] + acc[1][nt][0], v1 = acc[0][nt][1] + acc[1][nt][1];
+          double v0 = acc[0][nt][0], v1 = acc[0][nt][1];
+          if (oscale) {
+            v0 *= is;
+            v1 *= is;
+          }
           if (n + 1 < out.rs) *reinterpret_cast<double2*>(o + n) = make_double2(v0, v1);
           else if (n < out.rs) o[n] = v0;
         }
@@ -393,38 +413,46 @@ __global__ void bcat_kernel(const double* M, int kM, const double* S0, int kS, i
   }
 }
 
-template <int NA, int RB>
+template <int NA, int RB, bool PRE>
 void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
   const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
+  if (PRE && ra > 0 && !sepc) fail(PND_ECONFIG, "kstage: scaled input needs separate base rows");
   const int K = 2 * NA * a.X.cols + ra;
-  const int K4 = (K + 7) / 8 * 8;
+  const int K4 = (K + 15) / 16 * 16;  // whole groups of four k-steps
   double* B = bcat.get((size_t)K4 * RB);
   bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.S0, ra, a.out.cols, K4, RB, B);
   launched();
   const Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
-  const size_t fixed = 2 * (size_t)K4 * KCS * sizeof(double) + sizeof(PipeBars);
+  const size_t fixed =
+      (2 * (size_t)K4 * KCS + (size_t)K4 * RB) * sizeof(double) + sizeof(PipeBars);
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  CK(cudaFuncSetAttribute(kstage_kernel<NA, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(kstage_kernel<NA, RB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const int nchunks = (g.n + KC - 1) / KC;
-  int grid = sm_count() * resident(kstage_kernel<NA, RB>, PTH, smem);
+  int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE>, PTH, smem);
   if (grid > nchunks) grid = nchunks;
-  kstage_kernel<NA, RB><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S, nstg,
-                                                  a.inv_s);
+  kstage_kernel<NA, RB, PRE><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S, nstg,
+                                                       a.inv_s, a.out_scaled ? 1 : 0);
   launched();
+}
+
+template <int NA, int RB>
+void kstage_rb(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
+  if (a.in_scaled) kstage_launch<NA, RB, true>(a, bcat, st);
+  else kstage_launch<NA, RB, false>(a, bcat, st);
 }
 
 template <int NA>
 void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   const int r = a.out.cols > a.X.cols ? a.out.cols : a.X.cols;
-  if (r <= 8) kstage_launch<NA, 8>(a, bcat, st);
-  else if (r <= 16) kstage_launch<NA, 16>(a, bcat, st);
-  else if (r <= 24) kstage_launch<NA, 24>(a, bcat, st);
-  else if (r <= 32) kstage_launch<NA, 32>(a, bcat, st);
+  if (r <= 8) kstage_rb<NA, 8>(a, bcat, st);
+  else if (r <= 16) kstage_rb<NA, 16>(a, bcat, st);
+  else if (r <= 24) kstage_rb<NA, 24>(a, bcat, st);
+  else if (r <= 32) kstage_rb<NA, 32>(a, bcat, st);
   else fail(PND_ECONFIG, "kstage supports at most 32 output columns");
 }
 

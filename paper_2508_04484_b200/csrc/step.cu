@@ -256,6 +256,9 @@ void streaming_step(Handle& h, double dt) {
       ka.X = stage == 2 ? W2 : W1;
       ka.out = stage == 2 ? W1 : W2;
     }
+    // the Horner intermediates W1/W2 are stored pre-scaled by 1/S; dK is not
+    ka.in_scaled = stage > 0;
+    ka.out_scaled = stage < 3;
     phase(h, PH_KSTAGE);
     kstage(ka, st);
     phase(h, PH_LSIDE);

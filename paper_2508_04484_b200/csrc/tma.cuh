@@ -61,6 +61,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// mbarrier wait for a thread that is normally early (the producer): back off
+// with nanosleep instead of spinning on the issue slots the workers need
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, unsigned parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(200);
+}
+
 // arrive (count 1) on an mbarrier; release semantics order this thread's prior writes
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
@@ -90,6 +110,13 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
           smem_u32(dst)),
       "l"((unsigned long long)src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// prefetch a contiguous global range into L2 (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"((unsigned long long)src),
+               "r"(bytes)
+               : "memory");
 }
 
 }  // namespace pnd
