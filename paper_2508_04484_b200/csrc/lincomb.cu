@@ -1,0 +1,284 @@
+// LINCOMB: out = [Y1 | Y2] TA - X TB over all cells, with the Grams
+//   grams = [X^T out (X.cols x nb) ; out^T out (nb x nb)]
+// -- the streaming passes of the block CGS2/SVQB augmentation and the
+// truncation rotation U1 = U^ P (dlra.py:26-43, 111-113).
+//
+// HBM-streaming kernel, warp-specialised like the stencil kernels:
+//   producer warp: one cp.async.bulk per input per 64-cell chunk into a ring
+//     of staging buffers (the rows of a chunk are contiguous in the
+//     cell-major layout; chunks past n read the zero halo rows);
+//   8 compute warps: warp w owns m-tile w (8 cells) of the chunk and all
+//     NB8 n-tiles of out: FP64 DMMA with A fragments straight from the staged
+//     rows (row length = 4 mod 16 doubles: conflict-free) and B fragments
+//     from a shared copy of [TA; -TB] in fragment order; out is stored from
+//     the accumulators and parked in a double-buffered shared tile, from which
+//     the Grams (k = cell) accumulate in registers across all chunks.
+// Per-CTA Gram partials are summed in a fixed order (deterministic).
+#include "tma.cuh"
+
+namespace pnd {
+
+namespace {
+
+__host__ __device__ constexpr int lpad4(int w) { return ((w + 11) / 16) * 16 + 4; }
+
+constexpr int LCH = 64;                 // cells per chunk
+constexpr int LCW = 8;                  // compute warps
+constexpr int LTH = 32 * (LCW + 1);     // + producer warp
+constexpr int LNSTG_MAX = 4;
+constexpr int LZPAD = 16;               // zero doubles after each staged input block
+
+struct LBars {
+  uint64_t sfull[LNSTG_MAX], sempty[LNSTG_MAX];
+};
+
+struct LIn {
+  const double* p[3];
+  int cols[3], rs[3];
+  int off[3];   // smem offset of the staged rows of input q (doubles)
+  int ks0[3];   // first k-step of input q
+  int nin;      // inputs in use (Y1, then Y2 and/or X)
+  int xq;       // index of the X input (-1: none)
+  int stage;    // doubles per staging slot
+  unsigned bytes;
+  int ks;       // total k-steps
+};
+
+template <int NB8>
+__global__ void __launch_bounds__(LTH, 2)
+    lincomb_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
+                   int ny, int nb, NMat out, int nstg, int grams, double* __restrict__ partial) {
+  constexpr int TS = lpad4(NB8 * 8);            // out tile row length
+  extern __shared__ __align__(128) double sm[];
+  double* const sB = sm + nstg * in.stage;      // [ks][NB8][32] fragment order
+  double* const sT = sB + in.ks * NB8 * 32;     // 2 x [LCH][TS]
+  LBars* bars = reinterpret_cast<LBars*>(sT + 2 * LCH * TS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
+  const int XT = (xcn + 7) / 8;                  // X^T out row tiles
+  const int GT = grams ? (XT + NB8) * NB8 : 0;   // Gram tiles
+  if (tid == 0) {
+    for (int b = 0; b < nstg; ++b) {
+      mbar_init(&bars->sfull[b], 1);
+      mbar_init(&bars->sempty[b], LCW);
+    }
+    mbar_fence_init();
+  }
+  // zero pads after each staged block (k-steps past a block's columns read them)
+  for (int s = 0; s < nstg; ++s)
+    for (int q = 0; q < in.nin; ++q)
+      for (int i = tid; i < LZPAD; i += LTH)
+        sm[s * in.stage + in.off[q] + LCH * in.rs[q] + i] = 0.0;
+  // B = [TA; -TB] in fragment order (zero rows past each input's columns)
+  for (int i = tid; i < in.ks * NB8 * 32; i += LTH) {
+    const int l = i & 31, f = i >> 5, ks = f / NB8, nt = f - ks * NB8;
+    int q = 0;
+    while (q + 1 < in.nin && ks >= in.ks0[q + 1]) ++q;
+    const int j = 4 * (ks - in.ks0[q]) + (l & 3), col = nt * 8 + (l >> 2);
+    double v = 0.0;
+    if (j < in.cols[q] && col < nb) {
+      if (q == in.xq) v = -TB[(size_t)j * nb + col];
+      else v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
+    }
+    sB[i] = v;
+  }
+  for (int i = tid; i < 2 * LCH * TS; i += LTH) sT[i] = 0.0;
+  __syncthreads();
+  const int nchunks = (n + LCH - 1) / LCH;
+
+  if (warp == LCW) {  // producer
+    if (lane == 0) {
+      Ring r(nstg);
+      for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+        if (r.k) mbar_wait_sleep(&bars->sempty[r.s], (r.k - 1) & 1);
+        mbar_expect_tx(&bars->sfull[r.s], in.bytes);
+        const long c0 = (long)chunk * LCH;
+        for (int q = 0; q < in.nin; ++q)
+          bulk_load(sm + r.s * in.stage + in.off[q], in.p[q] + c0 * in.rs[q],
+                    LCH * in.rs[q] * 8, &bars->sfull[r.s]);
+      }
+    }
+    return;
+  }
+
+  const int m = lane >> 2, kq = lane & 3;
+  constexpr int GPW_MAX = (2 * NB8 * NB8 + LCW - 1) / LCW;  // X^T out + out^T out tiles
+  double gacc[GPW_MAX][2];
+#pragma unroll
+  for (int t = 0; t < GPW_MAX; ++t) gacc[t][0] = gacc[t][1] = 0.0;
+  Ring r(nstg);
+  int it = 0;
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next(), ++it) {
+    const long c0 = (long)chunk * LCH;
+    mbar_wait(&bars->sfull[r.s], r.k & 1);
+    const double* sb = sm + r.s * in.stage;
+    double* T = sT + (it & 1) * LCH * TS;
+    // ---- out tile: m-tile `warp`, all n-tiles; two accumulator sets
+    double acc[2][NB8][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int nt = 0; nt < NB8; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
+    for (int q = 0; q < in.nin; ++q) {
+      const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
+      const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
+      int ks = k0;
+      for (; ks + 1 < k1; ks += 2) {
+        const double a0 = pa[4 * (ks - k0)], a1 = pa[4 * (ks + 1 - k0)];
+#pragma unroll
+        for (int nt = 0; nt < NB8; ++nt) {
+          dmma884(acc[0][nt][0], acc[0][nt][1], a0, sB[(ks * NB8 + nt) * 32 + lane]);
+          dmma884(acc[1][nt][0], acc[1][nt][1], a1, sB[((ks + 1) * NB8 + nt) * 32 + lane]);
+        }
+      }
+      if (ks < k1) {
+        const double a0 = pa[4 * (ks - k0)];
+#pragma unroll
+        for (int nt = 0; nt < NB8; ++nt)
+          dmma884(acc[0][nt][0], acc[0][nt][1], a0, sB[(ks * NB8 + nt) * 32 + lane]);
+      }
+    }
+    const int il = warp * 8 + m;
+    const long row = c0 + il;
+#pragma unroll
+    for (int nt = 0; nt < NB8; ++nt) {
+      const double v0 = acc[0][nt][0] + acc[1][nt][0], v1 = acc[0][nt][1] + acc[1][nt][1];
+      const int col = nt * 8 + 2 * kq;
+      *reinterpret_cast<double2*>(T + il * TS + col) = make_double2(v0, v1);
+      if (out.p && row < n) {
+        double* o = out.p + row * out.rs + col;
+        if (col + 1 < out.rs) *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+        else if (col < out.rs) o[0] = v0;
+      }
+    }
+    if (grams) {
+      named_sync(1, 32 * LCW);  // out tile of this chunk complete
+      const double* sx = in.xq >= 0 ? sb + in.off[in.xq] : nullptr;
+      const int rsx = in.xq >= 0 ? in.rs[in.xq] : 0;
+#pragma unroll
+      for (int t = 0; t < GPW_MAX; ++t) {
+        const int tile = warp + LCW * t;
+        if (tile < GT) {
+          const int ti = tile / NB8, tj = tile - ti * NB8;
+          const bool xg = ti < XT;
+          const double* pa = xg ? sx + (ti * 8 + m) : T + ((ti - XT) * 8 + m);
+          const int sa = xg ? rsx : TS;
+          const double* pb = T + tj * 8 + m;
+          // rows past n: zero staged rows and zero out rows -> no contribution
+#pragma unroll 4
+          for (int k0 = 0; k0 < LCH; k0 += 4)
+            dmma884(gacc[t][0], gacc[t][1], pa[(k0 + kq) * sa], pb[(k0 + kq) * TS]);
+        }
+      }
+    }
+    warp_arrive(&bars->sempty[r.s]);
+  }
+  if (grams) {
+    double* o = partial + (size_t)blockIdx.x * (xcn + nb) * nb;
+#pragma unroll
+    for (int t = 0; t < GPW_MAX; ++t) {
+      const int tile = warp + LCW * t;
+      if (tile < GT) {
+        const int ti = tile / NB8, tj = tile - ti * NB8;
+        const bool xg = ti < XT;
+        const int rrow = (xg ? ti : ti - XT) * 8 + m, col = tj * 8 + 2 * kq;
+        const int nrow = xg ? xcn : nb;
+        const size_t base = xg ? 0 : (size_t)xcn * nb;
+        if (rrow < nrow) {
+          if (col < nb) o[base + (size_t)rrow * nb + col] = gacc[t][0];
+          if (col + 1 < nb) o[base + (size_t)rrow * nb + col + 1] = gacc[t][1];
+        }
+      }
+    }
+  }
+}
+
+__global__ void lreduce(const double* __restrict__ partial, int nblk, int count,
+                        double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
+  out[i] = s;
+}
+
+template <int NB8>
+void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
+                    NMat out, double* grams, DBuf& partial, cudaStream_t st) {
+  LIn in{};
+  const NMat ms[3] = {Y1, Y2, X};
+  int o = 0, ks = 0;
+  for (int q = 0; q < 3; ++q) {
+    if (!ms[q].p || ms[q].cols <= 0) continue;
+    const int i = in.nin++;
+    in.p[i] = ms[q].p;
+    in.cols[i] = ms[q].cols;
+    in.rs[i] = ms[q].rs;
+    in.off[i] = o;
+    in.ks0[i] = ks;
+    if (q == 2) in.xq = i;
+    o += ((LCH * ms[q].rs + LZPAD) + 15) / 16 * 16;
+    ks += (ms[q].cols + 3) / 4;
+    in.bytes += LCH * ms[q].rs * 8;
+  }
+  if (!X.p || X.cols <= 0) in.xq = -1;
+  in.stage = o;
+  in.ks = ks;
+  const int ny = Y1.cols + (Y2.p ? Y2.cols : 0);
+  const int nb = out.cols;
+  constexpr int TS = lpad4(NB8 * 8);
+  const size_t fixed = ((size_t)ks * NB8 * 32 + 2 * (size_t)LCH * TS) * sizeof(double) +
+                       sizeof(LBars);
+  // two CTAs per SM: keep the whole CTA under ~113 KB
+  const size_t cap = 113 * 1024;
+  int nstg = 0;
+  while (nstg < LNSTG_MAX && fixed + (size_t)(nstg + 1) * in.stage * sizeof(double) <= cap)
+    ++nstg;
+  if (nstg < 2) {
+    nstg = 2;
+    if (fixed + 2 * (size_t)in.stage * sizeof(double) > 227 * 1024)
+      fail(PND_ECONFIG, "lincomb tile exceeds shared memory");
+  }
+  const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
+  CK(cudaFuncSetAttribute(lincomb_kernel<NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  int nblk = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, lincomb_kernel<NB8>, LTH, smem));
+  if (nblk < 1) nblk = 1;
+  const int nchunks = (g.n + LCH - 1) / LCH;
+  int grid = sm_count() * nblk;
+  if (grid > nchunks) grid = nchunks;
+  const int xcn = X.p ? X.cols : 0;
+  const size_t count = (size_t)(xcn + nb) * nb;
+  double* part = grams ? partial.get(count * grid) : nullptr;
+  lincomb_kernel<NB8><<<grid, LTH, smem, st>>>(g.n, in, TA, TB, ny, nb, out, nstg,
+                                               grams ? 1 : 0, part);
+  launched();
+  if (grams) {
+    lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
+    launched();
+  }
+}
+
+}  // namespace
+
+void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
+             NMat out, double* grams, DBuf& partial, cudaStream_t st) {
+  const int w = out.cols > (X.p ? X.cols : 0) ? out.cols : X.cols;
+  const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
+  if (K > 128) fail(PND_ECONFIG, "lincomb supports at most 128 input columns");
+  if (grams && X.p && X.cols > 64) fail(PND_ECONFIG, "lincomb Grams support at most 64 X columns");
+  switch ((w + 7) / 8) {
+    case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 3: lincomb_launch<3>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 4: lincomb_launch<4>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 5: lincomb_launch<5>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 6: lincomb_launch<6>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 7:
+    case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    default: fail(PND_ECONFIG, "lincomb supports at most 64 output columns");
+  }
+}
+
+}  // namespace pnd

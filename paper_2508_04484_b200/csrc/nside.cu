@@ -2,11 +2,9 @@
 //
 // Every n-side operation is "form per-cell feature rows, then contract them"
 // and runs as FP64 tensor-core mma.sync.m8n8k4 (DMMA) on shared-memory tiles.
-// The stencil kernels (kstage, stencil Grams) live in stencil.cu; this file
-// holds the pointwise/contraction kernels:
-//   lincomb  [Y1 | Y2] TA - X TB with its Grams: the passes of the block
-//            Gram-Schmidt/SVQB augmentation and the truncation rotation
-//            (dlra.py:26-43, 111-113);
+// The stencil kernels (kstage, stencil Grams) live in stencil.cu and the
+// LINCOMB passes in lincomb.cu; this file holds the other pointwise /
+// contraction kernels:
 //   pgram    plain / weighted / source Grams (dlra.py:285, 307-319);
 //   scat_dk, dose, transposes, unit/random rows, class gathers.
 // Shared-memory tiles use row lengths = 4 (mod 16) doubles where DMMA
@@ -30,148 +28,11 @@ __global__ void reduce_blocks(const double* __restrict__ partial, int nblk, int 
   out[i] = s;
 }
 
-// ===================================================================== lincomb
-constexpr int LC = 64;
-
-template <int NB8>
-__global__ void __launch_bounds__(256)
-    lincomb_kernel(Geom g, NMat Y1, NMat Y2, NMat X, const double* __restrict__ TA,
-                   const double* __restrict__ TB, NMat out, int K4, int KS, int BS, int TS,
-                   int grams, double* __restrict__ partial) {
-  constexpr int OT = (LC / 8) * NB8;
-  constexpr int GT = 2 * NB8 * NB8;        // X^T T (x <= 8 NB8 rows) and T^T T
-  constexpr int GPW = (GT + 7) / 8;
-  extern __shared__ __align__(128) double sm[];
-  double* sA = sm;                         // [LC][KS]  rows [Y1 | Y2 | X]
-  double* sB = sA + LC * KS;               // [K4][BS]
-  double* sT = sB + K4 * BS;               // [LC][TS]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int y1 = Y1.cols, y2 = Y2.p ? Y2.cols : 0, xcn = X.p ? X.cols : 0;
-  const int ny = y1 + y2, K = ny + xcn, nb = out.cols;
-  for (int i = tid; i < K4 * BS; i += 256) {
-    const int k = i / BS, n = i - k * BS;
-    double v = 0.0;
-    if (n < nb && k < K) v = k < ny ? TA[k * nb + n] : -TB[(k - ny) * nb + n];
-    sB[i] = v;
-  }
-  for (int i = tid; i < LC * KS; i += 256) sA[i] = 0.0;
-  for (int i = tid; i < LC * TS; i += 256) sT[i] = 0.0;
-  double gacc[GPW][2];
-#pragma unroll
-  for (int t = 0; t < GPW; ++t) gacc[t][0] = gacc[t][1] = 0.0;
-  const int nchunks = (g.n + LC - 1) / LC;
-  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x) {
-    const int c0 = chunk * LC;
-    const int rows = g.n - c0 < LC ? g.n - c0 : LC;
-    __syncthreads();
-    for (int e = tid; e < LC * y1; e += 256) {
-      const int i = e / y1, j = e - i * y1;
-      sA[i * KS + j] = i < rows ? Y1.p[(long)(c0 + i) * Y1.rs + j] : 0.0;
-    }
-    for (int e = tid; e < LC * y2; e += 256) {
-      const int i = e / y2, j = e - i * y2;
-      sA[i * KS + y1 + j] = i < rows ? Y2.p[(long)(c0 + i) * Y2.rs + j] : 0.0;
-    }
-    for (int e = tid; e < LC * xcn; e += 256) {
-      const int i = e / xcn, j = e - i * xcn;
-      sA[i * KS + ny + j] = i < rows ? X.p[(long)(c0 + i) * X.rs + j] : 0.0;
-    }
-    __syncthreads();
-    for (int tile = warp; tile < OT; tile += 8) {
-      const int mt = tile / NB8, nt = tile - mt * NB8;
-      double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
-      const double* pa = sA + (mt * 8 + (lane >> 2)) * KS + (lane & 3);
-      const double* pb = sB + (lane & 3) * BS + nt * 8 + (lane >> 2);
-      int k0 = 0;
-      for (; k0 + 8 <= K4; k0 += 8) {
-        dmma884(d0, d1, pa[k0], pb[k0 * BS]);
-        dmma884(e0, e1, pa[k0 + 4], pb[(k0 + 4) * BS]);
-      }
-      if (k0 < K4) dmma884(d0, d1, pa[k0], pb[k0 * BS]);
-      const int m = mt * 8 + (lane >> 2), n = nt * 8 + 2 * (lane & 3);
-      sT[m * TS + n] = d0 + e0;
-      sT[m * TS + n + 1] = d1 + e1;
-    }
-    __syncthreads();
-    if (out.p) {
-      const int rso = out.rs;
-      for (int e = tid; e < rows * rso; e += 256) {
-        const int i = e / rso, n = e - i * rso;
-        out.p[(long)(c0 + i) * rso + n] = n < nb ? sT[i * TS + n] : 0.0;
-      }
-    }
-    if (grams) {
-#pragma unroll
-      for (int t = 0; t < GPW; ++t) {
-        const int tile = warp + 8 * t;
-        if (tile < GT) {
-          const bool xg = tile < NB8 * NB8;
-          const int tt = xg ? tile : tile - NB8 * NB8;
-          const int ti = tt / NB8, tj = tt - ti * NB8;
-          const int m = ti * 8 + (lane >> 2), kq = lane & 3;
-          const bool mv = xg ? m < xcn : true;
-          const double* pa = xg ? sA + ny + m : sT + m;
-          const int sa = xg ? KS : TS;
-          const double* pb = sT + tj * 8 + (lane >> 2);
-          if (!xg || ti * 8 < xcn) {
-#pragma unroll 4
-            for (int k0 = 0; k0 < LC; k0 += 4)
-              dmma884(gacc[t][0], gacc[t][1], mv ? pa[(k0 + kq) * sa] : 0.0, pb[(k0 + kq) * TS]);
-          }
-        }
-      }
-    }
-  }
-  if (grams) {
-    double* o = partial + (size_t)blockIdx.x * (xcn + nb) * nb;
-#pragma unroll
-    for (int t = 0; t < GPW; ++t) {
-      const int tile = warp + 8 * t;
-      if (tile < GT) {
-        const bool xg = tile < NB8 * NB8;
-        const int tt = xg ? tile : tile - NB8 * NB8;
-        const int ti = tt / NB8, tj = tt - ti * NB8;
-        const int row = ti * 8 + (lane >> 2), col = tj * 8 + 2 * (lane & 3);
-        const int nrow = xg ? xcn : nb;
-        const size_t off = xg ? 0 : (size_t)xcn * nb;
-        if (row < nrow) {
-          if (col < nb) o[off + (size_t)row * nb + col] = gacc[t][0];
-          if (col + 1 < nb) o[off + (size_t)row * nb + col + 1] = gacc[t][1];
-        }
-      }
-    }
-  }
-}
-
 template <class Kern>
 int resident(Kern k, int threads, size_t smem) {
   int nb = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, threads, smem));
   return nb < 1 ? 1 : nb;
-}
-
-template <int NB8>
-void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
-                    NMat out, double* grams, DBuf& partial, cudaStream_t st) {
-  const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
-  const int K4 = (K + 3) / 4 * 4;
-  const int KS = pad4(K4), BS = pad4(NB8 * 8), TS = pad4(NB8 * 8);
-  const size_t smem = ((size_t)LC * KS + (size_t)K4 * BS + (size_t)LC * TS) * sizeof(double);
-  CK(cudaFuncSetAttribute(lincomb_kernel<NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  const int nchunks = (g.n + LC - 1) / LC;
-  int grid = sm_count() * resident(lincomb_kernel<NB8>, 256, smem);
-  if (grid > nchunks) grid = nchunks;
-  const int xcn = X.p ? X.cols : 0;
-  const size_t count = (size_t)(xcn + out.cols) * out.cols;
-  double* part = grams ? partial.get(count * grid) : nullptr;
-  lincomb_kernel<NB8><<<grid, 256, smem, st>>>(g, Y1, Y2, X, TA, TB, out, K4, KS, BS, TS,
-                                               grams ? 1 : 0, part);
-  launched();
-  if (grams) {
-    reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
-    launched();
-  }
 }
 
 // ===================================================================== pgram
@@ -428,24 +289,6 @@ int grid_for(long n, int block) {
 }
 
 }  // namespace
-
-void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
-             NMat out, double* grams, DBuf& partial, cudaStream_t st) {
-  const int w = out.cols > (X.p ? X.cols : 0) ? out.cols : X.cols;
-  const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
-  if (K > 128) fail(PND_ECONFIG, "lincomb supports at most 128 input columns");
-  switch ((w + 7) / 8) {
-    case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 3: lincomb_launch<3>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 4: lincomb_launch<4>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 5: lincomb_launch<5>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 6: lincomb_launch<6>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 7:
-    case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    default: fail(PND_ECONFIG, "lincomb supports at most 64 output columns");
-  }
-}
 
 void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
   const int w = a.X.cols > a.nb ? a.X.cols : a.nb;

@@ -238,23 +238,6 @@ __device__ __forceinline__ void pipe_init(PipeBars* pb, int nstg, int conw) {
   }
 }
 
-// ring position of iteration it: slot s, use count k (phase parity k & 1)
-struct Ring {
-  int s = 0, k = 0, n;
-  __device__ explicit Ring(int n_) : n(n_) {}
-  __device__ void next() {
-    if (++s == n) {
-      s = 0;
-      ++k;
-    }
-  }
-};
-
-// one elected lane signals for the whole warp
-__device__ __forceinline__ void warp_arrive(uint64_t* bar) {
-  __syncwarp();
-  if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
-}
 
 // ===================================================================== kstage
 // out = [D_0 S^-1 X, ..., D_ns-1 S^-1 X | U0] . Bcat, Bcat = [M_0; ...; M_ns-1; S0]
