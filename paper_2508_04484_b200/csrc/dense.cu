@@ -494,6 +494,102 @@ __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const dou
   for (int i = tid; i < pq; i += nthr) S[i] = W[i];
 }
 
+// Householder QR of a whole (rows x cols) column-major matrix in one CTA
+// (the m-side factors: rows = m moments <= ~600): the matrix lives in shared
+// memory, the reflectors are those of hh_qr_kernel (beta = -sign(alpha) ||x||,
+// tau = 0 for a zero sub-column), and the explicit Q is then formed in place by
+// applying the reflectors backwards (LAPACK dorg2r order). Replaces a TSQR
+// tree of several launches by one launch for the small m-side QRs.
+__global__ void __launch_bounds__(512)
+    qr_small_kernel(const double* __restrict__ A, int rows, int cols, int lda,
+                    double* __restrict__ Q, int ldq, double* __restrict__ rfac) {
+  extern __shared__ double sm[];
+  const int LDS = cols | 1;  // odd row length: conflict-free column walks
+  double* S = sm;                      // rows x LDS
+  double* red = S + (size_t)rows * LDS;  // 32
+  double* wk = red + 32;               // cols
+  double* tau = wk + cols;             // cols
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  for (int idx = tid; idx < rows * cols; idx += nthr) {
+    const int i = idx % rows, j = idx / rows;
+    S[i * LDS + j] = A[(size_t)i + (size_t)j * lda];
+  }
+  __syncthreads();
+  const int kk = rows < cols ? rows : cols;
+  for (int j = 0; j < kk; ++j) {
+    double part = 0.0;
+    for (int i = j + 1 + tid; i < rows; i += nthr) part += S[i * LDS + j] * S[i * LDS + j];
+    const double xnorm2 = block_sum(part, red);
+    double tj = 0.0;
+    if (xnorm2 > 0.0) {
+      const double alpha = S[j * LDS + j];
+      const double beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+      tj = (beta - alpha) / beta;
+      const double scl = 1.0 / (alpha - beta);
+      for (int i = j + 1 + tid; i < rows; i += nthr) S[i * LDS + j] *= scl;
+      __syncthreads();
+      for (int k = j + 1 + warp; k < cols; k += nw) {
+        double sacc = 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
+        sacc = warp_sum(sacc);
+        if (lane == 0) wk[k] = S[j * LDS + k] + sacc;
+      }
+      __syncthreads();
+      const int w = cols - j - 1;
+      if (w > 0) {
+        for (int idx = tid; idx < (rows - j) * w; idx += nthr) {
+          const int i = j + idx / w, k = j + 1 + idx % w;
+          const double v = (i == j) ? 1.0 : S[i * LDS + j];
+          S[i * LDS + k] -= tj * v * wk[k];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) S[j * LDS + j] = beta;
+    }
+    if (tid == 0) tau[j] = tj;
+    __syncthreads();
+  }
+  // triangular factor (kk x cols, row-major)
+  for (int idx = tid; idx < kk * cols; idx += nthr) {
+    const int i = idx / cols, j = idx - i * cols;
+    rfac[idx] = i <= j ? S[i * LDS + j] : 0.0;
+  }
+  __syncthreads();
+  // explicit Q (rows x kk) in place, reflectors applied backwards
+  for (int j = kk - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (j < kk - 1 && tj != 0.0) {
+      for (int k = j + 1 + warp; k < kk; k += nw) {
+        double sacc = 0.0;
+        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
+        sacc = warp_sum(sacc);
+        if (lane == 0) wk[k] = S[j * LDS + k] + sacc;
+      }
+      __syncthreads();
+      const int w = kk - j - 1;
+      for (int idx = tid; idx < (rows - j) * w; idx += nthr) {
+        const int i = j + idx / w, k = j + 1 + idx % w;
+        const double v = (i == j) ? 1.0 : S[i * LDS + j];
+        S[i * LDS + k] -= tj * v * wk[k];
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < rows; i += nthr) {
+      double v;
+      if (i < j) v = 0.0;
+      else if (i == j) v = 1.0 - tj;
+      else v = -tj * S[i * LDS + j];
+      S[i * LDS + j] = v;
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < rows * kk; idx += nthr) {
+    const int i = idx % rows, j = idx / rows;
+    Q[(size_t)i + (size_t)j * ldq] = S[i * LDS + j];
+  }
+}
+
 void set_smem(const void* fn, size_t bytes) {
   CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
@@ -536,6 +632,16 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
          cudaStream_t st) {
   if (cols > 64) fail(PND_ECONFIG, "orthonormalisation supports at most 64 columns");
   const int kc = rows < cols ? rows : cols;
+  {
+    // whole matrix in one CTA when it fits (the m-side QRs)
+    const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
+    if (sm <= 200 * 1024) {
+      set_smem((const void*)qr_small_kernel, sm);
+      qr_small_kernel<<<1, 512, sm, st>>>(a, rows, cols, lda, q, ldq, rfac);
+      launched();
+      return kc;
+    }
+  }
   // level matrices: level 0 is `a`; level l+1 holds the stacked R's of level l
   struct Level {
     double* mat;
