@@ -47,7 +47,8 @@ struct LIn {
 template <int NB8>
 __global__ void __launch_bounds__(LTH, 2)
     lincomb_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
-                   int ny, int nb, NMat out, int nstg, int grams, double* __restrict__ partial) {
+                   int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
+                   double* __restrict__ partial) {
   constexpr int TS = lpad4(NB8 * 8);            // out tile row length
   extern __shared__ __align__(128) double sm[];
   double* const sB = sm + nstg * in.stage;      // [ks][NB8][32] fragment order
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(LTH, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
   const int XT = (xcn + 7) / 8;                  // X^T out row tiles
-  const int GT = grams ? (XT + NB8) * NB8 : 0;   // Gram tiles
+  const int GT = grams ? (XT + (skip_tt ? 0 : NB8)) * NB8 : 0;  // Gram tiles
   if (tid == 0) {
     for (int b = 0; b < nstg; ++b) {
       mbar_init(&bars->sfull[b], 1);
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(LTH, 2)
     while (q + 1 < in.nin && ks >= in.ks0[q + 1]) ++q;
     const int j = 4 * (ks - in.ks0[q]) + (l & 3), col = nt * 8 + (l >> 2);
     double v = 0.0;
-    if (j < in.cols[q] && col < nb) {
+    if (j < in.cols[q] && col < nb && !copy_y) {
       if (q == in.xq) v = -TB[(size_t)j * nb + col];
       else v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
     }
@@ -113,6 +114,15 @@ __global__ void __launch_bounds__(LTH, 2)
     mbar_wait(&bars->sfull[r.s], r.k & 1);
     const double* sb = sm + r.s * in.stage;
     double* T = sT + (it & 1) * LCH * TS;
+    if (copy_y) {
+      // Gram-only mode: out = Y1 (no contraction), parked for X^T Y1
+      const double* y = sb + in.off[0];
+      for (int e = lane; e < 8 * NB8 * 8; e += 32) {
+        const int i = warp * 8 + e / (NB8 * 8), c = e % (NB8 * 8);
+        T[i * TS + c] = c < in.cols[0] ? y[i * in.rs[0] + c] : 0.0;
+      }
+      __syncwarp();
+    } else {
     // ---- out tile: m-tile `warp`, all n-tiles; two accumulator sets
     double acc[2][NB8][2];
 #pragma unroll
@@ -151,6 +161,7 @@ __global__ void __launch_bounds__(LTH, 2)
         else if (col < out.rs) o[0] = v0;
       }
     }
+    }
     if (grams) {
       named_sync(1, 32 * LCW);  // out tile of this chunk complete
       const double* sx = in.xq >= 0 ? sb + in.off[in.xq] : nullptr;
@@ -174,7 +185,7 @@ __global__ void __launch_bounds__(LTH, 2)
     warp_arrive(&bars->sempty[r.s]);
   }
   if (grams) {
-    double* o = partial + (size_t)blockIdx.x * (xcn + nb) * nb;
+    double* o = partial + (size_t)blockIdx.x * (xcn + (skip_tt ? 0 : nb)) * nb;
 #pragma unroll
     for (int t = 0; t < GPW_MAX; ++t) {
       const int tile = warp + LCW * t;
@@ -183,7 +194,7 @@ __global__ void __launch_bounds__(LTH, 2)
         const bool xg = ti < XT;
         const int rrow = (xg ? ti : ti - XT) * 8 + m, col = tj * 8 + 2 * kq;
         const int nrow = xg ? xcn : nb;
-        const size_t base = xg ? 0 : (size_t)xcn * nb;
+        const size_t base = xg ? 0 : (size_t)xcn * nb;  // (skip_tt: only X^T out tiles)
         if (rrow < nrow) {
           if (col < nb) o[base + (size_t)rrow * nb + col] = gacc[t][0];
           if (col + 1 < nb) o[base + (size_t)rrow * nb + col + 1] = gacc[t][1];
@@ -204,7 +215,7 @@ __global__ void lreduce(const double* __restrict__ partial, int nblk, int count,
 
 template <int NB8>
 void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
-                    NMat out, double* grams, DBuf& partial, cudaStream_t st) {
+                    NMat out, double* grams, DBuf& partial, cudaStream_t st, bool gram_only) {
   LIn in{};
   const NMat ms[3] = {Y1, Y2, X};
   int o = 0, ks = 0;
@@ -249,10 +260,11 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   int grid = sm_count() * nblk;
   if (grid > nchunks) grid = nchunks;
   const int xcn = X.p ? X.cols : 0;
-  const size_t count = (size_t)(xcn + nb) * nb;
+  const size_t count = (size_t)(xcn + (gram_only ? 0 : nb)) * nb;
   double* part = grams ? partial.get(count * grid) : nullptr;
   lincomb_kernel<NB8><<<grid, LTH, smem, st>>>(g.n, in, TA, TB, ny, nb, out, nstg,
-                                               grams ? 1 : 0, part);
+                                               grams ? 1 : 0, gram_only ? 1 : 0,
+                                               gram_only ? 1 : 0, part);
   launched();
   if (grams) {
     lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
@@ -269,15 +281,32 @@ void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const do
   if (K > 128) fail(PND_ECONFIG, "lincomb supports at most 128 input columns");
   if (grams && X.p && X.cols > 64) fail(PND_ECONFIG, "lincomb Grams support at most 64 X columns");
   switch ((w + 7) / 8) {
-    case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 3: lincomb_launch<3>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 4: lincomb_launch<4>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 5: lincomb_launch<5>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
-    case 6: lincomb_launch<6>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
+    case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
+    case 3: lincomb_launch<3>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
+    case 4: lincomb_launch<4>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
+    case 5: lincomb_launch<5>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
+    case 6: lincomb_launch<6>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
     case 7:
-    case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st); break;
+    case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
     default: fail(PND_ECONFIG, "lincomb supports at most 64 output columns");
+  }
+}
+
+void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st) {
+  // out = X^T Y (X.cols x Y.cols) in one streaming pass: the LINCOMB kernel
+  // with out = Y parked in shared memory and only the X^T out Grams formed
+  const int w = Y.cols > X.cols ? Y.cols : X.cols;
+  if (w > 64) fail(PND_ECONFIG, "Grams support at most 64 columns");
+  NMat none{};
+  switch ((w + 7) / 8) {
+    case 1: lincomb_launch<1>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 2: lincomb_launch<2>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 3: lincomb_launch<3>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 4: lincomb_launch<4>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 5: lincomb_launch<5>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 6: lincomb_launch<6>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    default: lincomb_launch<8>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
   }
 }
 

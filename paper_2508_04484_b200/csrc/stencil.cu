@@ -20,6 +20,8 @@
 //   sgram:  G_s += X^T D_s S^-1 X over all chunks for X = [X1 | X2] (the L- and
 //           S-phase factors, dlra.py:183-184, 199-209), accumulated in registers,
 //           per-CTA partials summed in fixed order (bit-reproducible).
+#include <cstdlib>
+
 #include "tma.cuh"
 
 namespace pnd {
@@ -440,22 +442,23 @@ void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
 }
 
 // ===================================================================== sgram
-// G_s = [X1 | X2]^T D_s S^-1 [X1 | X2]. Chunk = 16 cells; per buffer b:
-// F[b] = [NS W][20] stencil features (k = cell), C[b] = [16][pad4(W)] unscaled
+// G_s = [X1 | X2]^T D_s S^-1 [X1 | X2]. Chunk = GC cells (32 for w <= 24,
+// else 16, so a chunk carries enough work per pipeline handoff); per buffer b:
+// F[b] = [NS W][pad4(GC)] stencil features (k = cell), C[b] = [GC][pad4(W)] unscaled
 // centre rows (the A = X^T operand). Contraction warp m (of 7) owns the
 // stencil-column tiles bt = bt0 + m + 7u (bt = s T8 + tj) against all T8 row tiles, one
 // accumulator per tile (T8 UPW independent chains); launches cover column-tile
 // ranges of at most 32 tiles.
-constexpr int GC = 16;
-constexpr int GTL = pad4(GC);  // 20
-
-template <int NA, int T8>
+template <int NA, int T8, int GC>
 __global__ void __launch_bounds__(GPTH, 1)
     sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, int nstg, const double* __restrict__ isp,
-                 int bt0, int nbt, double* __restrict__ partial) {
+                 int bt0, int nbt, double* __restrict__ partial, int dbg) {
   constexpr int NS = 2 * NA;
   constexpr int W = T8 * 8;
   constexpr int XS = pad4(W);
+  constexpr int GTL = pad4(GC);       // feature tile row length (k = cell)
+  constexpr int CG = GC / 4;          // groups of 4 cells: 4 or 8
+  constexpr int JS = 8 * (8 / CG);    // column stride of one former lane
   constexpr int NBMAX = 32;
   constexpr int UPW = ((NS * T8 < NBMAX ? NS * T8 : NBMAX) + GCONW - 1) / GCONW;
   constexpr int FT = NS * W * GTL + GC * XS;  // doubles per feature buffer
@@ -476,13 +479,15 @@ __global__ void __launch_bounds__(GPTH, 1)
       Ring r(nstg);
       for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
         if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
+        if (dbg & 1) mbar_arrive(&pb->sfull[r.s]);
+        else
         issue_seg<GC, NA>(S, sm + r.s * S.total, &pb->sfull[r.s], chunk_cell(S, chunk, GC), X1,
                           X2, nin, isp, X1);
       }
     }
   } else if (warp < FORMW) {
-    // lane = (cell 4 (w & 3) + (lane & 3), column (lane >> 2) + 8 (w >> 2) + 16 t)
-    const int ci = 4 * (warp & 3) + (lane & 3), cj = (lane >> 2) + 8 * (warp >> 2);
+    // lane = (cell 4 (w % CG) + (lane & 3), column (lane >> 2) + 8 (w / CG) + JS t)
+    const int ci = 4 * (warp % CG) + (lane & 3), cj = (lane >> 2) + 8 * (warp / CG);
     Ring r(nstg);
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it, r.next()) {
@@ -496,38 +501,40 @@ __global__ void __launch_bounds__(GPTH, 1)
       double* Fb = F0 + f * FT;
       double* Cb = Fb + NS * W * GTL;
       // unscaled centre rows (A operand); rows past n are zero halo rows
-      for (int j = cj; j < w; j += 16)
+      for (int j = cj; j < w; j += JS)
         Cb[ci * XS + j] = j < a1 ? X1s[(ci + 2) * X1.rs + j] : X2s[(ci + 2) * X2.rs + j - a1];
       Ctx<GC, NA> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
-      constexpr int TT = (W + 15) / 16;
+      constexpr int TT = (W + JS - 1) / JS;
       cx.rows(X1s, X1.rs, ci, cj);
+      if (!(dbg & 2)) {
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
-        const int j = cj + 16 * t;
+        const int j = cj + JS * t;
         if (j < a1) {
           double v[NS];
-          if (fast) cx.template apply<true>(g, 16 * t, v);
-          else cx.template apply<false>(g, 16 * t, v);
+          if (fast) cx.template apply<true>(g, JS * t, v);
+          else cx.template apply<false>(g, JS * t, v);
 #pragma unroll
           for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
         }
       }
       if (a2) {
-        const int j0 = cj >= a1 ? cj : cj + 16 * ((a1 - cj + 15) / 16);
+        const int j0 = cj >= a1 ? cj : cj + JS * ((a1 - cj + JS - 1) / JS);
         cx.rows(X2s, X2.rs, ci, j0 - a1);
 #pragma unroll
         for (int t = 0; t < TT; ++t) {
-          const int j = j0 + 16 * t;
+          const int j = j0 + JS * t;
           if (j < w) {
             double v[NS];
-            if (fast) cx.template apply<true>(g, 16 * t, v);
-            else cx.template apply<false>(g, 16 * t, v);
+            if (fast) cx.template apply<true>(g, JS * t, v);
+            else cx.template apply<false>(g, JS * t, v);
 #pragma unroll
             for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
           }
         }
+      }
       }
       __syncwarp();
       if (lane == 0) {
@@ -550,7 +557,7 @@ __global__ void __launch_bounds__(GPTH, 1)
       const double* pa = F0 + b * FT + NS * W * GTL + kq * XS + m0;
       const double* pbt = F0 + b * FT + ((bt0 + m) * 8 + m0) * GTL + kq;
 #pragma unroll 1
-      for (int k0 = 0; k0 < GC; k0 += 4) {
+      for (int k0 = 0; k0 < ((dbg & 4) ? 0 : GC); k0 += 4) {
         double af[T8];
 #pragma unroll
         for (int ti = 0; ti < T8; ++ti) af[ti] = pa[k0 * XS + ti * 8];
@@ -595,9 +602,10 @@ __global__ void reduce_parts(const double* __restrict__ partial, int nblk, int c
   out[i] = s;
 }
 
-template <int NA, int T8>
+template <int NA, int T8, int GC>
 void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
                   cudaStream_t st) {
+  constexpr int GTL = pad4(GC);
   const NMat ins[2] = {X1, X2};
   const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr);
   const int W = T8 * 8;
@@ -606,10 +614,10 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  CK(cudaFuncSetAttribute(sgram_kernel<NA, T8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(sgram_kernel<NA, T8, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const int nchunks = (g.n + GC - 1) / GC;
-  int grid = sm_count() * resident(sgram_kernel<NA, T8>, GPTH, smem);
+  int grid = sm_count() * resident(sgram_kernel<NA, T8, GC>, GPTH, smem);
   if (grid > nchunks) grid = nchunks;
   const int w = X1.cols + (X2.p ? X2.cols : 0);
   const size_t count = (size_t)2 * NA * w * w;
@@ -617,7 +625,9 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const int nb = 2 * NA * T8;
   for (int bt0 = 0; bt0 < nb; bt0 += 32) {
     const int nbt = nb - bt0 < 32 ? nb - bt0 : 32;
-    sgram_kernel<NA, T8><<<grid, GPTH, smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part);
+        static const int dbg = getenv("PND_SGRAM_DEBUG") ? atoi(getenv("PND_SGRAM_DEBUG")) : 0;
+    sgram_kernel<NA, T8, GC><<<grid, GPTH, smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part,
+                                                        dbg);
     launched();
   }
   reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
@@ -629,14 +639,14 @@ void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, D
               cudaStream_t st) {
   const int w = X1.cols + (X2.p ? X2.cols : 0);
   switch ((w + 7) / 8) {
-    case 1: sgram_launch<NA, 1>(g, X1, X2, isp, out, partial, st); break;
-    case 2: sgram_launch<NA, 2>(g, X1, X2, isp, out, partial, st); break;
-    case 3: sgram_launch<NA, 3>(g, X1, X2, isp, out, partial, st); break;
-    case 4: sgram_launch<NA, 4>(g, X1, X2, isp, out, partial, st); break;
-    case 5: sgram_launch<NA, 5>(g, X1, X2, isp, out, partial, st); break;
-    case 6: sgram_launch<NA, 6>(g, X1, X2, isp, out, partial, st); break;
+    case 1: sgram_launch<NA, 1, 32>(g, X1, X2, isp, out, partial, st); break;
+    case 2: sgram_launch<NA, 2, 32>(g, X1, X2, isp, out, partial, st); break;
+    case 3: sgram_launch<NA, 3, 32>(g, X1, X2, isp, out, partial, st); break;
+    case 4: sgram_launch<NA, 4, 16>(g, X1, X2, isp, out, partial, st); break;
+    case 5: sgram_launch<NA, 5, 16>(g, X1, X2, isp, out, partial, st); break;
+    case 6: sgram_launch<NA, 6, 16>(g, X1, X2, isp, out, partial, st); break;
     case 7:
-    case 8: sgram_launch<NA, 8>(g, X1, X2, isp, out, partial, st); break;
+    case 8: sgram_launch<NA, 8, 16>(g, X1, X2, isp, out, partial, st); break;
     default: fail(PND_ECONFIG, "stencil Grams support at most 64 columns");
   }
 }

@@ -270,17 +270,7 @@ void streaming_step(Handle& h, double dt) {
   phase(h, PH_LGRAM);
   stencil_grams(g, U0, NMat{}, isp, QT, h.part, st);  // QT_s = U0^T D_s U0 = Q_s^T
   double* C1 = slot(h, S_C1, (size_t)a * b);
-  {
-    PGramArgs pa{};
-    pa.geo = g;
-    pa.X = U0;
-    pa.Y = dK;
-    pa.nb = b;
-    pa.nphase = 1;
-    pa.gen = PG_PLAIN;
-    pa.out = C1;
-    pgram(pa, h.part, st);
-  }
+  gram_xy(g, U0, dK, C1, h.part, st);  // C1 = U0^T dK
   phase(h, PH_LSIDE);
   double* L0 = slot(h, S_L0, (size_t)m * a);
   double* LW = slot(h, S_LW, (size_t)m * a);
@@ -641,15 +631,7 @@ double orth_defect(Handle& h) {
   phase(h, PH_DEFECT);
   double* G = slot(h, S_DEF, (size_t)h.ru * h.ru + (size_t)h.rv * h.rv + 2);
   double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
-  PGramArgs pa{};
-  pa.geo = g;
-  pa.X = state_u(h);
-  pa.Y = state_u(h);
-  pa.nb = h.ru;
-  pa.nphase = 1;
-  pa.gen = PG_PLAIN;
-  pa.out = G;
-  pgram(pa, h.part, st);
+  gram_xy(g, state_u(h), state_u(h), G, h.part, st);  // U^T U
   double* GV = G + (size_t)h.ru * h.ru;
   gemm(h.rv, h.rv, h.m, 1.0, tr(rowm(h.V.p, h.rv)), 0, rowm(h.V.p, h.rv), 0, 0.0,
        rowm(GV, h.rv), 0, 1, st);

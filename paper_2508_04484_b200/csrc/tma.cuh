@@ -49,7 +49,26 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+#ifndef PND_MBAR_SPIN
+#define PND_MBAR_SPIN 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+#if PND_MBAR_SPIN
+  // spin on test_wait: a suspended try_wait wakes late, and these waits sit
+  // on the per-chunk critical path of the producer/former/contraction chain
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+#else
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -59,6 +78,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 // mbarrier wait for a thread that is normally early (the producer): back off
