@@ -290,8 +290,9 @@ int pnd_set_materials(pnd_handle* hh, const int32_t* cell_class, int n_class,
 
 int pnd_set_inv_s(pnd_handle* hh, const double* inv_s) {
   return guard(hh, [&](Handle& h) {
-    double* d = h.inv_s.get(h.g.ld);
-    pnd::fill_zero(d, h.g.ld, h.st);
+    // 64 doubles of zero slack: streaming kernels stage whole 64-cell chunks
+    double* d = h.inv_s.get(h.g.ld + 64);
+    pnd::fill_zero(d, h.g.ld + 64, h.st);
     up(d, inv_s, h.g.n, h.st);
     double* sf = h.s_field.get(h.g.ld);
     pnd::fill_zero(sf, h.g.ld, h.st);
@@ -306,8 +307,9 @@ int pnd_set_class_stopping(pnd_handle* hh, const double* class_s) {
     if (!h.have_mat) pnd::fail(PND_ECONFIG, "set materials before class stopping powers");
     double* v = h.cls_val.get(h.n_cls);
     up(v, class_s, h.n_cls, h.st);
-    double* d = h.inv_s.get(h.g.ld);
+    double* d = h.inv_s.get(h.g.ld + 64);
     double* sf = h.s_field.get(h.g.ld);
+    pnd::fill_zero(d + h.g.n, h.g.ld + 64 - h.g.n, h.st);  // zero tail (chunked staging)
     pnd::class_gather_inv(h.cls.p, v, h.g.n, d, sf, h.st);
     pnd::set_isp(h);
     h.have_inv_s = true;

@@ -42,6 +42,8 @@ struct LIn {
   int stage;    // doubles per staging slot
   unsigned bytes;
   int ks;       // total k-steps
+  const double* w;  // optional per-cell weight (Gram-only mode: T = diag(w) Y1)
+  int woff;         // smem offset of the staged weights
 };
 
 template <int NB8>
@@ -97,6 +99,7 @@ __global__ void __launch_bounds__(LTH, 2)
         for (int q = 0; q < in.nin; ++q)
           bulk_load(sm + r.s * in.stage + in.off[q], in.p[q] + c0 * in.rs[q],
                     LCH * in.rs[q] * 8, &bars->sfull[r.s]);
+        if (in.w) bulk_load(sm + r.s * in.stage + in.woff, in.w + c0, LCH * 8, &bars->sfull[r.s]);
       }
     }
     return;
@@ -117,9 +120,11 @@ __global__ void __launch_bounds__(LTH, 2)
     if (copy_y) {
       // Gram-only mode: out = Y1 (no contraction), parked for X^T Y1
       const double* y = sb + in.off[0];
+      const double* wv = in.w ? sb + in.woff : nullptr;
       for (int e = lane; e < 8 * NB8 * 8; e += 32) {
         const int i = warp * 8 + e / (NB8 * 8), c = e % (NB8 * 8);
-        T[i * TS + c] = c < in.cols[0] ? y[i * in.rs[0] + c] : 0.0;
+        const double v = c < in.cols[0] ? y[i * in.rs[0] + c] : 0.0;
+        T[i * TS + c] = wv ? wv[i] * v : v;
       }
       __syncwarp();
     } else {
@@ -215,7 +220,8 @@ __global__ void lreduce(const double* __restrict__ partial, int nblk, int count,
 
 template <int NB8>
 void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
-                    NMat out, double* grams, DBuf& partial, cudaStream_t st, bool gram_only) {
+                    NMat out, double* grams, DBuf& partial, cudaStream_t st, bool gram_only,
+                    const double* weight = nullptr) {
   LIn in{};
   const NMat ms[3] = {Y1, Y2, X};
   int o = 0, ks = 0;
@@ -233,6 +239,12 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
     in.bytes += LCH * ms[q].rs * 8;
   }
   if (!X.p || X.cols <= 0) in.xq = -1;
+  if (weight) {
+    in.w = weight;
+    in.woff = o;
+    o += LCH;
+    in.bytes += LCH * 8;
+  }
   in.stage = o;
   in.ks = ks;
   const int ny = Y1.cols + (Y2.p ? Y2.cols : 0);
@@ -293,20 +305,22 @@ void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const do
   }
 }
 
-void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st) {
-  // out = X^T Y (X.cols x Y.cols) in one streaming pass: the LINCOMB kernel
-  // with out = Y parked in shared memory and only the X^T out Grams formed
+void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st,
+             const double* weight) {
+  // out = X^T diag(weight) Y (X.cols x Y.cols) in one streaming pass: the
+  // LINCOMB kernel with out = diag(weight) Y parked in shared memory and only
+  // the X^T out Grams formed
   const int w = Y.cols > X.cols ? Y.cols : X.cols;
   if (w > 64) fail(PND_ECONFIG, "Grams support at most 64 columns");
-  NMat none{};
+  const NMat none{}, o{nullptr, 0, Y.cols};
   switch ((w + 7) / 8) {
-    case 1: lincomb_launch<1>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    case 2: lincomb_launch<2>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    case 3: lincomb_launch<3>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    case 4: lincomb_launch<4>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    case 5: lincomb_launch<5>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    case 6: lincomb_launch<6>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
-    default: lincomb_launch<8>(g, Y, none, X, nullptr, nullptr, NMat{nullptr, 0, Y.cols}, out, partial, st, true); break;
+    case 1: lincomb_launch<1>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 2: lincomb_launch<2>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 3: lincomb_launch<3>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 4: lincomb_launch<4>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 5: lincomb_launch<5>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 6: lincomb_launch<6>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    default: lincomb_launch<8>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
   }
 }
 

@@ -171,6 +171,22 @@ __global__ void scat_dk_kernel(Geom g, double dt, const double* __restrict__ inv
   }
 }
 
+__global__ void source_rows_kernel(int n, int ld, const double* __restrict__ inv_s,
+                                   const int* __restrict__ cls, const double* __restrict__ atomic,
+                                   const double* __restrict__ psi, int n_beams, NMat Z) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const double* at = atomic + cls[c] * 12;
+    const double is = inv_s[c];
+    double* z = Z.p + (long)c * Z.rs;
+    for (int b = 0; b < n_beams; ++b) {
+      const double sp = is * psi[(size_t)b * ld + c];
+#pragma unroll
+      for (int i = 0; i < 12; i += 2)
+        *reinterpret_cast<double2*>(z + b * 12 + i) = make_double2(at[i] * sp, at[i + 1] * sp);
+    }
+  }
+}
+
 __global__ void dose_kernel(Geom g, NMat U, const double* __restrict__ coef, double half_dt,
                             const double* __restrict__ s_field, const double* __restrict__ psi,
                             int n_beams, double* __restrict__ dep, double* __restrict__ prev) {
@@ -394,6 +410,13 @@ NMat NBuf::view(const Geom& g, int cols, cudaStream_t st) {
   m.rs = rs;
   m.cols = cols;
   return m;
+}
+
+void source_rows(const Geom& g, const double* inv_s, const int* cls, const double* cls_atomic,
+                 const double* psi, int n_beams, NMat Z, cudaStream_t st) {
+  source_rows_kernel<<<grid_for(g.n, 256), 256, 0, st>>>(g.n, g.ld, inv_s, cls, cls_atomic, psi,
+                                                    n_beams, Z);
+  launched();
 }
 
 }  // namespace pnd

@@ -114,8 +114,13 @@ void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* inv_s, double
 // grams = [X^T out (X.cols x nb) ; out^T out (nb x nb)]
 void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
              NMat out, double* grams, DBuf& partial, cudaStream_t st);
-// plain Gram out = X^T Y (X.cols x Y.cols, row-major) in one streaming pass (lincomb.cu)
-void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st);
+// Gram out = X^T diag(w) Y (X.cols x Y.cols, row-major; w = null: plain) in one
+// streaming pass (lincomb.cu)
+void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st,
+             const double* w = nullptr);
+// Z[c][b*12 + i] = N_{cls(c),i} psi_b(c) / S(c): the scattering source rows (dlra.py:244-251)
+void source_rows(const Geom& g, const double* inv_s, const int* cls, const double* cls_atomic,
+                 const double* psi, int n_beams, NMat Z, cudaStream_t st);
 
 // pointwise Grams
 enum PGen { PG_PLAIN = 0, PG_WEIGHT = 1, PG_SOURCE = 2 };

@@ -34,7 +34,7 @@ enum Slot {
   S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
   S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
   S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_VNEW, S_M2,
-  S_C1, S_OG, S_OTA, S_OTB, S_EYE, S_PC, S_COUNT
+  S_C1, S_OG, S_OTA, S_OTB, S_EYE, S_PC, S_TAZ, S_COUNT
 };
 static_assert(S_COUNT <= 43, "slots 43..47 are reserved by abi.cu");
 
@@ -373,16 +373,28 @@ void scattering_step(Handle& h, double dt) {
     gemm(12 * B, b, m, 1.0, rowm(gt, m), 0, rowm(h.V.p, b), 0, 0.0, rowm(rows, b), 0, 1, st);
   }
 
-  // substep 2 increment: dK = dt src_rows(V0)  (dlra.py:303; K1 = U0 S0 + dK)
+  // substep 2 increment: dK = dt src_rows(V0) = dt Z rows  (dlra.py:303; K1 = U0 S0 + dK)
+  // with the source rows Z[c][b*12 + i] = N_{cls,i} psi_b / S materialised once
   const NMat dK = h.W2.view(g, b, st);
   phase(h, PH_SCATK1);
-  scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, B > 0 ? h.psi.p : nullptr, B, rows, dK, st);
+  NMat Z{};
+  if (B > 0) {
+    Z = h.Xs.view(g, 12 * B, st);
+    source_rows(g, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.psi.p, B, Z, st);
+    double* TAz = slot(h, S_TAZ, (size_t)12 * B * b);
+    axpby(12 * B * b, dt, rows, 0.0, TAz, st);
+    lincomb(g, Z, NMat{}, NMat{}, TAz, nullptr, dK, nullptr, h.part, st);
+  } else {
+    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, nullptr, 0, rows, dK, st);
+  }
 
   // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
   const int nw = h.n_cls <= 12 ? h.n_cls : 12;
   double* H = slot(h, S_H, (size_t)nw * a * a);
   phase(h, PH_SCATGRAM);
-  {
+  if (h.n_cls == 1) {
+    gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);  // one class: U0^T diag(1/S) U0
+  } else {
     PGramArgs pa{};
     pa.geo = g;
     pa.X = U0;
@@ -409,21 +421,7 @@ void scattering_step(Handle& h, double dt) {
   // source projections U0^T (N psi_b / S)  (a x 12B)
   double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
   phase(h, PH_SCATGRAM);
-  if (B > 0) {
-    PGramArgs pa{};
-    pa.geo = g;
-    pa.X = U0;
-    pa.nb = 12 * B;
-    pa.nphase = 1;
-    pa.gen = PG_SOURCE;
-    pa.inv_s = h.inv_s.p;
-    pa.cls = h.cls.p;
-    pa.wtab = h.cls_atomic.p;
-    pa.psi = h.psi.p;
-    pa.ld = g.ld;
-    pa.out = left;
-    pgram(pa, h.part, st);
-  }
+  if (B > 0) gram_xy(g, U0, Z, left, h.part, st);
   phase(h, PH_SCATSMALL);
   // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass)
   double* C1 = slot(h, S_C1, (size_t)a * b);
@@ -499,19 +497,7 @@ void scattering_step(Handle& h, double dt) {
     CK(cudaMemcpyAsync(proj2, left, sizeof(double) * a * 12 * B, cudaMemcpyDeviceToDevice, st));
     if (k > 0) {
       phase(h, PH_SCATGRAM);
-      PGramArgs pa{};
-      pa.geo = g;
-      pa.X = state_q(h);
-      pa.nb = 12 * B;
-      pa.nphase = 1;
-      pa.gen = PG_SOURCE;
-      pa.inv_s = h.inv_s.p;
-      pa.cls = h.cls.p;
-      pa.wtab = h.cls_atomic.p;
-      pa.psi = h.psi.p;
-      pa.ld = g.ld;
-      pa.out = proj2 + (size_t)a * 12 * B;
-      pgram(pa, h.part, st);
+      gram_xy(g, state_q(h), Z, proj2 + (size_t)a * 12 * B, h.part, st);
       phase(h, PH_SCATSMALL);
     }
     double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
