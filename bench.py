@@ -291,6 +291,42 @@ def run_cpu_sample(threads, steps, rank):
     }
 
 
+def config1_dose_time(with_cpu):
+    """Per-beam dose time on the reference's CPU-oracle config (BASELINE.json
+    configs[0]: 2-D water, P7, fixed rank 20, 573
+    energy steps, one beam): the whole energy loop + dose tally through the
+    public API, from the exported problem (assembly and ray tracing are the
+    reference's host code and are not part of this path)."""
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(ROOT / "tests" / "golden" / "bundle_config1.npz")
+    run_bundle(b, max_steps=5)  # warm the kernels / allocations
+    t0 = time.perf_counter()
+    res = run_bundle(b)
+    t_gpu = time.perf_counter() - t0
+    steps = len(res.rank_history)
+    out = {"workload": "config 1: 1 x 40 x 35 water, P7 (m=64), fixed rank 20, 573 steps, 1 beam",
+           "gpu_s": t_gpu, "gpu_steps_per_s": steps / t_gpu, "steps": steps}
+    if with_cpu:
+        env = dict(os.environ)
+        res_cpu = subprocess.run(
+            [sys.executable, "-c",
+             "import sys,time,json; sys.path.insert(0, %r)\n"
+             "from oracle import dlra_np\n"
+             "from paper_2508_04484_b200.problem import ProblemBundle\n"
+             "b = ProblemBundle.load(%r)\n"
+             "t = time.perf_counter(); dlra_np.run_energy_loop(b)\n"
+             "print(json.dumps({'s': time.perf_counter() - t}))"
+             % (str(ROOT), str(ROOT / "tests" / "golden" / "bundle_config1.npz"))],
+            capture_output=True, text=True, env=env, timeout=600)
+        if res_cpu.returncode == 0:
+            t_cpu = json.loads(res_cpu.stdout.strip().splitlines()[-1])["s"]
+            out["cpu_port_s"] = t_cpu
+            out["cpu_kind"] = "port (numpy oracle of the reference loop)"
+    return out
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -319,9 +355,16 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dist = None
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("gloo")
+        # one process per GPU; NCCL carries the barriers and the max-over-ranks
+        # timing reduction (the replicas exchange no data)
+        if args.impl != "reference" and torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
 
     config = {"workload": f"{args.nside}^3 homogeneous water, h=0.025 cm, P19 Fokker-Planck, "
                           f"70 MeV +z pencil beam, fixed rank {args.rank}, CFL 0.2, "
@@ -390,7 +433,7 @@ def main():
     clk = clocks.stop()
     dev_s = ms[0] / 1000.0
     if dist:
-        t = torch.tensor([dev_s, t_host], dtype=torch.float64)
+        t = torch.tensor([dev_s, t_host], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dev_s, t_host = float(t[0]), float(t[1])
     if rank_id != 0:
@@ -431,6 +474,12 @@ def main():
             cpu_baseline = run_cpu_sample(host_threads(), 2, args.rank)
         except Exception as exc:  # noqa: BLE001
             cpu_baseline = {"error": str(exc)[:300]}
+    per_beam = None
+    if world == 1:
+        try:
+            per_beam = config1_dose_time(with_cpu=not args.no_cpu_baseline)
+        except Exception as exc:  # noqa: BLE001
+            per_beam = {"error": str(exc)[:300]}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * dev_s / args.steps,
@@ -445,6 +494,7 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu_baseline,
         "phases": phases,
+        "per_beam_dose_time": per_beam,
         "ranks": sorted(set(ranks)),
         "fp64_dgemm_tflops": fp64,
         "reference_step_count": n_steps_total,

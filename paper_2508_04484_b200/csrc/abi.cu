@@ -318,9 +318,9 @@ int pnd_set_class_stopping(pnd_handle* hh, const double* class_s) {
 
 int pnd_set_scattering(pnd_handle* hh, const double* g_diags, const double* sigma_t) {
   return guard(hh, [&](Handle& h) {
+    // small pageable copies: staged by the driver at the call, no stream sync needed
     up(h.gdiag.get((size_t)12 * h.m), g_diags, (size_t)12 * h.m, h.st);
     up(h.sigt.get(12), sigma_t, 12, h.st);
-    CK(cudaStreamSynchronize(h.st));
     h.have_scat = true;
   });
 }

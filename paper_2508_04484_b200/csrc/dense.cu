@@ -755,7 +755,11 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   const size_t sm =
       ((size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N + N2) * sizeof(double) + N * sizeof(int);
   set_smem((const void*)svd_kernel, sm);
-  svd_kernel<<<1, 256, sm, st>>>(s, p, q, P, sig, Qt);
+  // one warp per Jacobi pair of a round: a round is one shuffle-reduction deep
+  int threads = 32 * (N2 / 2);
+  if (threads < 64) threads = 64;
+  if (threads > 1024) threads = 1024;
+  svd_kernel<<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
   launched();
 }
 
