@@ -119,6 +119,32 @@ int pnd_traverse(pnd_handle* h, const double* origin3, int n_rays, const double*
                  const double* dirs, int32_t* counts, const int64_t* offsets, int64_t* cells,
                  double* t0, double* t1);
 
+/* ---- uncollided flux: energy march + deposit ---------------------------- */
+/* Crank-Nicolson march of a batch of distinct ray signatures (march_ray,
+ * raytracer.py:285-350). gmats: n_keys dense (ng*nl)^2 energy operators G
+ * (assemble_energy_operators, raytracer.py:169-274; block tridiagonal);
+ * steppers = distinct (key, dz) pairs (the reference's LU cache), with the dz
+ * each was first built at; per march segment two halves (dz, substeps,
+ * stepper). Outputs per segment the group averages after the first half and
+ * the below-cutoff residual energy; psi_exit per march (may be NULL).
+ * NumericalError "Crank-Nicolson solve failed" / "non-finite flux" as the
+ * reference. */
+int pnd_march(pnd_handle* h, int nl, int ng, int n_keys, const double* gmats,
+              const double* mass, const double* p_lo, double e_min, const double* s_min,
+              const double* psi0, int n_steppers, const int32_t* st_key, const double* st_dz,
+              int n_marches, const int32_t* seg_off, const int32_t* seg_key,
+              const double* half_dz, const int32_t* half_n, const int32_t* half_st,
+              double* averages, double* residual, double* psi_exit);
+/* track-length deposit of trace_beam (raytracer.py:509-519), rays in
+ * enumeration order: values (n x ng row-major) += w * len/V * averages,
+ * residual (n) += w * res / V; segments of ray r are [ray_seg_off[r],
+ * ray_seg_off[r+1]) and map onto march ray_march[r]'s segments. */
+int pnd_deposit(pnd_handle* h, int ng, int n_rays, const int32_t* ray_seg_off,
+                const int64_t* cells, const double* lengths, const int32_t* ray_march,
+                const int32_t* march_seg_off, const double* weight, double volume,
+                int n_march_segs, const double* averages, const double* mres, double* values,
+                double* residual);
+
 /* ---- measurement and synthetic inputs (bench.py) ------------------------ */
 /* phase timer (CUDA events on the handle stream around every phase of the step) */
 int pnd_timing(pnd_handle* h, int enable);

@@ -58,6 +58,9 @@ SIGNATURES = {
     "pnd_launch_count": [_P, _P],
     "pnd_set_flux_separable": [_P, _I, _I, _I, _P, _P, _P],
     "pnd_state_random": [_P, _I, ctypes.c_ulonglong],
+    "pnd_march": [_P, _I, _I, _I, _P, _P, _P, _D, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P,
+                  _P, _P, _P],
+    "pnd_deposit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P, _P],
 }
 
 PHASES = ["kstage", "l_gram", "l_side", "tsqr_n", "tsqr_m", "s_gram", "s_rk4", "svd",

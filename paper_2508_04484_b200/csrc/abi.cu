@@ -1,3 +1,4 @@
+#include <vector>
 // extern "C" boundary (include/pndose_b200.h): argument checks, host<->device
 // staging, error mapping. Every exception raised inside the library becomes
 // a status code plus a message stored in the handle.
@@ -622,6 +623,150 @@ int pnd_traverse(pnd_handle* hh, const double* origin3, int n_rays, const double
       cudaFree(CE);
     }
     ds.free_(); dd.free_(); dt0.free_(); dt1.free_(); dc.free_();
+  });
+}
+
+namespace {
+// split dense block-tridiagonal G (ndof x ndof row-major, nl x nl blocks) into
+// D / L / U block arrays [g][nl][nl]
+void split_blocks(const double* G, int ng, int nl, double* D, double* L, double* U) {
+  const int ndof = ng * nl, b2 = nl * nl;
+  for (int g = 0; g < ng; ++g)
+    for (int i = 0; i < nl; ++i)
+      for (int j = 0; j < nl; ++j) {
+        const size_t row = (size_t)(g * nl + i) * ndof;
+        D[g * b2 + i * nl + j] = G[row + g * nl + j];
+        L[g * b2 + i * nl + j] = g > 0 ? G[row + (g - 1) * nl + j] : 0.0;
+        U[g * b2 + i * nl + j] = g + 1 < ng ? G[row + (g + 1) * nl + j] : 0.0;
+      }
+}
+}  // namespace
+
+int pnd_march(pnd_handle* hh, int nl, int ng, int n_keys, const double* gmats,
+              const double* mass, const double* p_lo, double e_min, const double* s_min,
+              const double* psi0, int n_steppers, const int32_t* st_key, const double* st_dz,
+              int n_marches, const int32_t* seg_off, const int32_t* seg_key,
+              const double* half_dz, const int32_t* half_n, const int32_t* half_st,
+              double* averages, double* residual, double* psi_exit) {
+  return guard(hh, [&](Handle& h) {
+    if (nl < 1 || nl > 4 || ng < 1) pnd::fail(PND_ECONFIG, "bad energy DG space");
+    if (n_marches <= 0) return;
+    const int ndof = ng * nl, b2 = nl * nl;
+    const int nseg = seg_off[n_marches];
+    // operator blocks: reject couplings beyond the neighbour groups
+    std::vector<double> D((size_t)n_keys * ng * b2), L(D.size()), U(D.size());
+    for (int k = 0; k < n_keys; ++k) {
+      const double* G = gmats + (size_t)k * ndof * ndof;
+      for (int r = 0; r < ndof; ++r)
+        for (int c = 0; c < ndof; ++c) {
+          const int gr = r / nl, gc = c / nl;
+          if ((gr - gc > 1 || gc - gr > 1) && G[(size_t)r * ndof + c] != 0.0)
+            pnd::fail(PND_ECONFIG, "energy operator is not block tridiagonal");
+        }
+      split_blocks(G, ng, nl, D.data() + (size_t)k * ng * b2, L.data() + (size_t)k * ng * b2,
+                   U.data() + (size_t)k * ng * b2);
+    }
+    pnd::DBuf dD, dL, dU, dm, dpl, dsm, dps, dsz, dhz, dinv, dE, dpsi, dtmp, dav, dres;
+    pnd::IBuf ik, iso, isk, ihn, ihs, ibad;
+    double* Dd = dD.get(D.size());
+    double* Ld = dL.get(L.size());
+    double* Ud = dU.get(U.size());
+    up(Dd, D.data(), D.size(), h.st);
+    up(Ld, L.data(), L.size(), h.st);
+    up(Ud, U.data(), U.size(), h.st);
+    double* md = dm.get(ndof);
+    up(md, mass, ndof, h.st);
+    double* pld = dpl.get(nl);
+    up(pld, p_lo, nl, h.st);
+    double* smd = dsm.get(n_keys);
+    up(smd, s_min, n_keys, h.st);
+    double* psd = dps.get(ndof);
+    up(psd, psi0, ndof, h.st);
+    int* kd = ik.get(n_steppers);
+    CK(cudaMemcpyAsync(kd, st_key, sizeof(int) * n_steppers, cudaMemcpyHostToDevice, h.st));
+    double* szd = dsz.get(n_steppers);
+    up(szd, st_dz, n_steppers, h.st);
+    int* sod = iso.get(n_marches + 1);
+    CK(cudaMemcpyAsync(sod, seg_off, sizeof(int) * (n_marches + 1), cudaMemcpyHostToDevice,
+                       h.st));
+    int* skd = isk.get(nseg > 0 ? nseg : 1);
+    CK(cudaMemcpyAsync(skd, seg_key, sizeof(int) * nseg, cudaMemcpyHostToDevice, h.st));
+    double* hzd = dhz.get(2 * (size_t)(nseg > 0 ? nseg : 1));
+    up(hzd, half_dz, 2 * (size_t)nseg, h.st);
+    int* hnd = ihn.get(2 * (size_t)(nseg > 0 ? nseg : 1));
+    CK(cudaMemcpyAsync(hnd, half_n, sizeof(int) * 2 * nseg, cudaMemcpyHostToDevice, h.st));
+    int* hsd = ihs.get(2 * (size_t)(nseg > 0 ? nseg : 1));
+    CK(cudaMemcpyAsync(hsd, half_st, sizeof(int) * 2 * nseg, cudaMemcpyHostToDevice, h.st));
+    int* bad = ibad.get(1);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), h.st));
+    double* Dinv = dinv.get((size_t)n_steppers * ng * b2);
+    double* E = dE.get((size_t)n_steppers * ng * b2);
+    pnd::march_steppers(nl, Dd, Ld, Ud, md, ng, n_steppers, kd, szd, Dinv, E, bad, h.st);
+    double* psi = dpsi.get((size_t)n_marches * ndof);
+    double* tmp = dtmp.get((size_t)n_marches * ndof);
+    double* av = dav.get((size_t)(nseg > 0 ? nseg : 1) * ng);
+    double* rs = dres.get(nseg > 0 ? nseg : 1);
+    pnd::march_rays(nl, Dd, Ld, Ud, md, ng, Dinv, E, szd, n_marches, sod, skd, hzd, hnd, hsd,
+                    smd, e_min, psd, pld, psi, tmp, av, rs, bad, h.st);
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, h.st));
+    if (averages) down(averages, av, (size_t)nseg * ng, h.st);
+    if (residual) down(residual, rs, nseg, h.st);
+    if (psi_exit) down(psi_exit, psi, (size_t)n_marches * ndof, h.st);
+    CK(cudaStreamSynchronize(h.st));
+    if (hbad == 1) pnd::fail(PND_ENUMERICAL, "Crank-Nicolson solve failed: singular block");
+    if (hbad == 2) pnd::fail(PND_ENUMERICAL, "ray march produced non-finite flux");
+  });
+}
+
+int pnd_deposit(pnd_handle* hh, int ng, int n_rays, const int32_t* ray_seg_off,
+                const int64_t* cells, const double* lengths, const int32_t* ray_march,
+                const int32_t* march_seg_off, const double* weight, double volume,
+                int n_march_segs, const double* averages, const double* mres, double* values,
+                double* residual) {
+  return guard(hh, [&](Handle& h) {
+    const int n = h.g.n, ld = h.g.ld;
+    pnd::DBuf dv, dr, dl, dw, da, dm;
+    pnd::IBuf io, im, ims;
+    double* V = dv.get((size_t)ng * ld);
+    double* R = dr.get(ld);
+    pnd::fill_zero(V, (size_t)ng * ld, h.st);
+    pnd::fill_zero(R, ld, h.st);
+    if (n_rays > 0) {
+      const int nseg = ray_seg_off[n_rays];
+      int* od = io.get(n_rays + 1);
+      CK(cudaMemcpyAsync(od, ray_seg_off, sizeof(int) * (n_rays + 1), cudaMemcpyHostToDevice,
+                         h.st));
+      long long* cd = nullptr;
+      CK(cudaMalloc(&cd, sizeof(long long) * (nseg > 0 ? nseg : 1)));
+      CK(cudaMemcpyAsync(cd, cells, sizeof(long long) * nseg, cudaMemcpyHostToDevice, h.st));
+      double* ldv = dl.get(nseg > 0 ? nseg : 1);
+      up(ldv, lengths, nseg, h.st);
+      int* rmd = im.get(n_rays);
+      CK(cudaMemcpyAsync(rmd, ray_march, sizeof(int) * n_rays, cudaMemcpyHostToDevice, h.st));
+      int n_m = 0;
+      for (int r = 0; r < n_rays; ++r) n_m = ray_march[r] + 1 > n_m ? ray_march[r] + 1 : n_m;
+      int* msd = ims.get(n_m + 1);
+      CK(cudaMemcpyAsync(msd, march_seg_off, sizeof(int) * (n_m + 1), cudaMemcpyHostToDevice,
+                         h.st));
+      double* wd = dw.get(n_rays);
+      up(wd, weight, n_rays, h.st);
+      double* ad = da.get((size_t)(n_march_segs > 0 ? n_march_segs : 1) * ng);
+      up(ad, averages, (size_t)n_march_segs * ng, h.st);
+      double* mrd = dm.get(n_march_segs > 0 ? n_march_segs : 1);
+      up(mrd, mres, n_march_segs, h.st);
+      pnd::deposit_rays(n_rays, od, cd, ldv, rmd, msd, wd, volume, ad, mrd, V, ld, R, ng, h.st);
+      CK(cudaStreamSynchronize(h.st));
+      cudaFree(cd);
+    }
+    pnd::DBuf dt;
+    if (values) {
+      double* T = dt.get((size_t)n * ng);
+      pnd::transpose_out(V, ld, n, ng, T, h.st);  // (n x ng) row-major, the reference layout
+      down(values, T, (size_t)n * ng, h.st);
+    }
+    if (residual) down(residual, R, n, h.st);
+    CK(cudaStreamSynchronize(h.st));
   });
 }
 

@@ -203,6 +203,22 @@ void scat_solves(const double* B /* 12 x r x r */, const double* coeffs /* 12 x 
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt,
            double* work, cudaStream_t st);
 
+// uncollided energy march + deposit (march.cu)
+void march_steppers(int nl, const double* D, const double* L, const double* U, const double* mass,
+                    int ng, int n_steppers, const int* key, const double* dz, double* Dinv,
+                    double* E, int* bad, cudaStream_t st);
+void march_rays(int nl, const double* D, const double* L, const double* U, const double* mass,
+                int ng, const double* Dinv, const double* E, const double* st_dz, int n_marches,
+                const int* seg_off, const int* seg_key, const double* half_dz, const int* half_n,
+                const int* half_st, const double* s_min, double e_min, const double* psi0,
+                const double* p_lo, double* psi, double* tmp, double* averages,
+                double* residual, int* bad, cudaStream_t st);
+void deposit_rays(int n_rays, const int* ray_seg_off, const long long* cells,
+                  const double* lengths, const int* ray_march, const int* march_seg_off,
+                  const double* weight, double volume, const double* averages,
+                  const double* mres, double* values, int ld, double* residual, int ng,
+                  cudaStream_t st);
+
 // ray traversal (trace.cu)
 void traverse(const Geom& g, const double* origin, int n_rays, const double* starts,
               const double* dirs, int* counts, const long long* offsets, long long* cells,

@@ -188,19 +188,28 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
 def run_simulation(config, solver: str = "dlra"):
     """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541).
 
-    `config` is a reference ProblemConfig. Problem assembly and ray tracing
-    are the reference's unchanged host code; the energy loop runs on the GPU.
+    `config` is a reference ProblemConfig. Problem assembly and the per-beam
+    tracer setup (material keys, coefficient closures; driver.py:398-436) are
+    the reference's unchanged host code; every beam's march and deposit
+    (raytracer.trace_beam) and the energy loop run on the GPU.
     solver="dlra-cpu" / "fullrank" hand the whole run back to the reference.
     """
     from pndose import driver as ref_driver  # the reference package
     from pndose.angular import beam_projection
+
+    from . import raytracer as dev_tracer
 
     if solver in ("dlra-cpu", "fullrank"):
         return ref_driver.run_simulation(config, solver="dlra" if solver == "dlra-cpu" else solver)
     if solver != "dlra":
         raise ConfigError(f"unknown solver '{solver}'")
     problem = ref_driver.assemble_problem(config)
-    fluxes = ref_driver.trace_all_beams(problem)
+    ref_trace = ref_driver.trace_beam
+    ref_driver.trace_beam = dev_tracer.trace_beam
+    try:
+        fluxes = ref_driver.trace_all_beams(problem)
+    finally:
+        ref_driver.trace_beam = ref_trace
     t_ms = [beam_projection(config.pn_order, bm.direction) for bm in config.beams]
     bundle = ProblemBundle.from_arrays(export_problem(problem, fluxes, t_ms))
     return run_bundle(bundle)

@@ -1,0 +1,67 @@
+"""GPU parity of the uncollided tracer (march + deposit) against the reference.
+
+- march_ray (raytracer.py:285-350) on the reference's own march fixture:
+  group averages per segment, below-cutoff residual and exit spectrum;
+- trace_beam (raytracer.py:452-529) for an axial and an oblique beam through
+  the heterogeneous phantom: the (cell x group) flux, the residual energy per
+  cell and the live-ray count, from the reference's assembled operators.
+The device factors each (material, dz) CN system by block elimination
+instead of a dense LU, so agreement is to FP64 rounding (T1-class), not bits.
+"""
+
+from types import SimpleNamespace
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def relmax(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300))
+
+
+def test_march_matches_reference():
+    from paper_2508_04484_b200 import raytracer as rt
+
+    M = golden("march.npz")
+    space = rt.EnergySpace(1.0, 31.5, 32, 2)
+    plan = rt._Marches(rt.MAX_STEP_CM)
+    plan.add([(float(l), int(k)) for l, k in zip(M["seg_len"], M["seg_key"])])
+    psi0 = rt.project_initial_spectrum(space, 30.0, 0.3)
+    assert relmax(psi0, M["psi0"]) < 1e-14
+    av, res, psi = plan.run(space, {0: M["g_0"], 1: M["g_1"]},
+                            {0: float(M["s_min"][0]), 1: float(M["s_min"][1])}, psi0,
+                            want_exit=True)
+    assert relmax(av, M["averages"]) < 1e-11
+    assert relmax(res, M["residual"]) < 1e-11
+    assert relmax(psi[0], M["psi_exit"]) < 1e-11
+
+
+@pytest.mark.parametrize("beam_index", [0, 1])
+def test_trace_beam_matches_reference(beam_index):
+    from paper_2508_04484_b200 import raytracer as rt
+
+    T = golden("trace.npz")
+    p = f"b{beam_index}_"
+    sp = T[p + "space"]
+    space = rt.EnergySpace(float(sp[0]), float(sp[1]), int(sp[2]), int(sp[3]))
+    gr = T[p + "grid"]
+    grid = SimpleNamespace(nx=int(gr[0]), ny=int(gr[1]), nz=int(gr[2]), dx=gr[3], dy=gr[4],
+                           dz=gr[5], origin=tuple(gr[6:9]))
+    b = T[p + "beam"]
+    beam = SimpleNamespace(direction=tuple(b[:3]), energy_mev=b[3], position_cm=tuple(b[4:7]),
+                           weight=b[7], sigma_xy_cm=b[8], sigma_e_mev=b[9])
+    keys = [int(k) for k in T[p + "key_list"]]
+    gm = {k: T[p + f"g_{k}"] for k in keys}
+    smin = {k: float(T[p + f"smin_{k}"]) for k in keys}
+    rays = T[p + "rays"]
+    flux = rt.trace_beam_ops(beam, grid, space, T[p + "keys"], gm, smin, int(rays[0]),
+                             float(rays[1]), float(rays[2]))
+    assert flux.n_rays == int(T[p + "n_rays"])
+    assert relmax(flux.values, T[p + "values"]) < 1e-10
+    assert relmax(flux.residual_energy, T[p + "residual"]) < 1e-10
+    # same cells touched
+    np.testing.assert_array_equal(flux.values != 0.0, T[p + "values"] != 0.0)

@@ -197,3 +197,32 @@ def test_angular_operators_match_reference(n_max):
         assert relmax(ap, A[f"aplus_{n_max}_{axis}"]) < 1e-12
         assert relmax(am, A[f"aminus_{n_max}_{axis}"]) < 1e-12
     assert relmax(beam_projection(n_max, (0.0, 0.6, 0.8)), A[f"tm_{n_max}"]) < 1e-12
+
+
+# ------------------------------------------------------------- tracer host logic
+def test_energy_operators_and_ray_bundle_match_reference():
+    """raytracer.py host restatements: energy operators (169-274), initial
+    spectrum (157-166), ray offsets/weights (406-418), transverse frame (60-69)."""
+    from paper_2508_04484_b200 import raytracer as rt
+
+    M = golden("march.npz")
+    space = rt.EnergySpace(1.0, 31.5, 32, 2)
+
+    def const(v):
+        return lambda e: np.full_like(np.asarray(e, dtype=float), v)
+
+    coeff = {0: (lambda e: 2.0 + 0.05 * np.asarray(e, dtype=float), const(0.04), const(0.3)),
+             1: (const(4.0), None, None)}
+    for k in (0, 1):
+        mass, g = rt.assemble_energy_operators(space, *coeff[k])
+        assert relmax(g, M[f"g_{k}"]) < 1e-14
+        np.testing.assert_array_equal(mass, M["mass"])
+    assert relmax(rt.project_initial_spectrum(space, 30.0, 0.3), M["psi0"]) < 1e-14
+    T = golden("trace.npz")
+    for b in range(int(T["n_beams"])):
+        p = f"b{b}_"
+        beam, rays = T[p + "beam"], T[p + "rays"]
+        off, wts = rt.stratified_ray_offsets(beam[8], int(rays[0]), float(rays[1]))
+        np.testing.assert_array_equal(off, T[p + "offsets"])
+        np.testing.assert_array_equal(wts, T[p + "weights"])
+        np.testing.assert_array_equal(np.stack(rt.transverse_frame(beam[:3])), T[p + "frame"])

@@ -475,6 +475,62 @@ def make_march():
     )
 
 
+def make_trace():
+    """trace_all_beams (driver.py:398-449 -> raytracer.py:452-529) on the
+    heterogeneous phantom with one axial and one oblique beam: the inputs the
+    device tracer consumes (assembled energy operators per material key,
+    s*(e_min), keys per cell, beam + ray parameters) and the reference's
+    outputs (group flux per cell, residual energy per cell, live rays)."""
+    config = driver.ProblemConfig.from_dict(hetero_raw())
+    problem = driver.assemble_problem(config)
+    captured = []
+    orig = driver.trace_beam
+
+    def spy(beam, grid, space, keys, coefficients, **kw):
+        flux = orig(beam, grid, space, keys, coefficients, **kw)
+        captured.append((beam, grid, space, np.asarray(keys), coefficients, kw, flux))
+        return flux
+
+    driver.trace_beam = spy
+    try:
+        driver.trace_all_beams(problem)
+    finally:
+        driver.trace_beam = orig
+    out = {}
+    for i, (beam, grid, space, keys, coeff, kw, flux) in enumerate(captured):
+        p = f"b{i}_"
+        uk = sorted(int(k) for k in np.unique(keys))
+        for k in uk:
+            mass, g = raytracer.assemble_energy_operators(space, *coeff[k])
+            out[p + f"g_{k}"] = g
+            out[p + f"smin_{k}"] = np.array(
+                float(np.atleast_1d(coeff[k][0](np.array([space.e_min])))[0]))
+        e1, e2 = beam.transverse_frame()
+        offs, wts = raytracer.stratified_ray_offsets(beam.sigma_xy_cm, kw["n_side"],
+                                                      kw["span_sigmas"])
+        out.update({
+            p + "keys": keys.astype(np.int32),
+            p + "key_list": np.array(uk),
+            p + "mass": space.mass_diagonal(),
+            p + "space": np.array([space.e_min, space.e_max, space.n_groups, space.degree]),
+            p + "grid": np.array([grid.nx, grid.ny, grid.nz, grid.dx, grid.dy, grid.dz,
+                                  *grid.origin]),
+            p + "beam": np.array([*beam.direction, beam.energy_mev, *beam.position_cm,
+                                  beam.weight, beam.sigma_xy_cm, beam.sigma_e_mev]),
+            p + "rays": np.array([kw["n_side"], kw["span_sigmas"], kw["max_step"]]),
+            p + "frame": np.stack([e1, e2]),
+            p + "offsets": offs,
+            p + "weights": wts,
+            p + "psi0": raytracer.project_initial_spectrum(space, beam.energy_mev,
+                                                           beam.sigma_e_mev),
+            p + "values": flux.values,
+            p + "residual": flux.residual_energy,
+            p + "n_rays": np.array(flux.n_rays),
+        })
+    out["n_beams"] = np.array(len(captured))
+    save("trace.npz", **out)
+
+
 def make_bench_physics():
     """Physics tables for the synthetic benchmark phantoms (water / bone / lung
     classes, stopping tables, moment tables up to degree 21 over 1..105 MeV)."""
@@ -512,6 +568,8 @@ if __name__ == "__main__":
         make_steps()
     if not what or "traverse" in what:
         make_traverse()
+    if not what or "trace" in what:
+        make_trace()
     if not what or "march" in what:
         make_march()
     if not what or "bench" in what:
