@@ -97,10 +97,11 @@ __global__ void kdfma(double* out, double seed) {
 }
 
 template <class K>
-void run(const char* name, K kern, double flop_per_warp_iter, int warps_per_block, double* d) {
+void run(const char* name, K kern, double flop_per_warp_iter, int warps_per_block, double* d,
+         int blocks_per_sm = 2) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int blocks = sms * 2;
+  const int blocks = sms * blocks_per_sm;
   kern<<<blocks, 32 * warps_per_block>>>(d, 1.0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -112,7 +113,8 @@ void run(const char* name, K kern, double flop_per_warp_iter, int warps_per_bloc
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double flops = 5.0 * blocks * warps_per_block * (double)ITERS * flop_per_warp_iter;
-  printf("%-28s warps/blk=%2d  %8.2f TFLOP/s\n", name, warps_per_block, flops / (ms * 1e-3) / 1e12);
+  printf("%-28s warps/blk=%2d blk/SM=%d  %8.2f TFLOP/s\n", name, warps_per_block, blocks_per_sm,
+         flops / (ms * 1e-3) / 1e12);
 }
 
 int main() {
@@ -126,6 +128,14 @@ int main() {
     run("m16n8k16 ilp4", k16816<4>, 4 * 4096.0, w, d);
     run("dfma ilp8", kdfma<8>, 8 * 64.0, w, d);
   }
+  // one warp per SM sub-partition (4 warps per SM) vs two
+  run("m8n8k4 ilp4 1w/SMSP", k884<4>, 4 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp8 1w/SMSP", k884<8>, 8 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp12 1w/SMSP", k884<12>, 12 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp4 2w/SMSP", k884<4>, 4 * 512.0, 8, d, 1);
+  run("m16n8k8 ilp4 1w/SMSP", k1688<4>, 4 * 2048.0, 4, d, 1);
+  run("m16n8k16 ilp4 1w/SMSP", k16816<4>, 4 * 4096.0, 4, d, 1);
+  run("dfma ilp8 1w/SMSP", kdfma<8>, 8 * 64.0, 4, d, 1);
   cudaError_t e = cudaGetLastError();
   printf("status: %s\n", cudaGetErrorString(e));
   return 0;
