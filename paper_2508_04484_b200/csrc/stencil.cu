@@ -208,7 +208,7 @@ int resident(Kern k, int threads, size_t smem) {
 // Warps signal with one elected lane after __syncwarp; there is no CTA-wide
 // barrier after the prologue.
 constexpr int FORMW = 8;             // former warps
-constexpr int CONW = 4;              // kstage contraction warps
+constexpr int CONW = 8;              // kstage contraction warps (m-tile x k-half)
 constexpr int PTH = 32 * (FORMW + CONW + 1);
 constexpr int GCONW = 7;             // sgram contraction warps (16 warps in all)
 constexpr int GPTH = 32 * (FORMW + GCONW + 1);
@@ -331,55 +331,88 @@ __global__ void __launch_bounds__(PTH, 1)
       }
     }
   } else {
-    const int mt = warp - FORMW;
+    // contraction warp q: m-tile q & 3, k-half q >> 2 (two warps per SM
+    // sub-partition, so one issues DMMAs while the other waits on its loads);
+    // the upper half's partials go through the consumed feature buffer
+    const int q = warp - FORMW, mt = q & 3, kh = q >> 2;
     const int nks = K4 / 4;
+    const int ks0 = kh ? nks / 2 : 0, ks1 = kh ? nks : nks / 2;
     const double* pb0 = sB + lane;
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
       const int b = it & 1, u = it >> 1;
       const int c0 = chunk_cell(S, chunk, KC);
       mbar_wait(&pb->ffull[b], u & 1);
-      double acc[4][NT][2];  // four k-step phases x NT tiles: 4 NT independent chains
+      double acc[2][NT][2];
 #pragma unroll
-      for (int h = 0; h < 4; ++h)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
-      const double* pa = F0 + b * K4 * KCS + (lane & 3) * KCS + mt * 8 + (lane >> 2);
-#pragma unroll 1
-      for (int ks = 0; ks < nks; ks += 4) {
-        double av[4], bv[4][NT];
+      double* Fb = F0 + b * K4 * KCS;
+      const double* pa = Fb + (lane & 3) * KCS + mt * 8 + (lane >> 2);
+      int ks = ks0;
+#pragma unroll 2
+      for (; ks + 1 < ks1; ks += 2) {
+        double av[2], bv[2][NT];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < 2; ++h) {
           av[h] = pa[(ks + h) * 4 * KCS];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) bv[h][nt] = pb0[((ks + h) * NT + nt) * 32];
         }
 #pragma unroll
-        for (int h = 0; h < 4; ++h)
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) dmma884(acc[h][nt][0], acc[h][nt][1], av[h], bv[h][nt]);
       }
+      if (ks < ks1) {
+        const double a0 = pa[ks * 4 * KCS];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          dmma884(acc[0][nt][0], acc[0][nt][1], a0, pb0[(ks * NT + nt) * 32]);
+      }
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        acc[0][nt][0] += acc[1][nt][0] + (acc[2][nt][0] + acc[3][nt][0]);
-        acc[0][nt][1] += acc[1][nt][1] + (acc[2][nt][1] + acc[3][nt][1]);
+        acc[0][nt][0] += acc[1][nt][0];
+        acc[0][nt][1] += acc[1][nt][1];
       }
-      warp_arrive(&pb->fempty[b]);
-      const int row = c0 + mt * 8 + (lane >> 2);
-      if (row < g.n) {
-        double* o = out.p + (long)row * out.rs;
-        const double is = oscale ? __ldg(isp + 2 * (long)row) : 1.0;
+      named_sync(2, 32 * CONW);  // every contraction warp is done reading F[b]
+      double* red = Fb;          // [4 m-tiles][NT][64] upper-half partials
+      if (kh) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+          *reinterpret_cast<double2*>(red + (mt * NT + nt) * 64 + 2 * lane) =
+              make_double2(acc[0][nt][0], acc[0][nt][1]);
+      }
+      named_sync(2, 32 * CONW);
+      if (!kh) {
+        const int row = c0 + mt * 8 + (lane >> 2);
+        double v[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const int n = nt * 8 + 2 * (lane & 3);
-          double v0 = acc[0][nt][0], v1 = acc[0][nt][1];
-          if (oscale) {
-            v0 *= is;
-            v1 *= is;
-          }
-          if (n + 1 < out.rs) *reinterpret_cast<double2*>(o + n) = make_double2(v0, v1);
-          else if (n < out.rs) o[n] = v0;
+          const double2 pv = *reinterpret_cast<const double2*>(red + (mt * NT + nt) * 64 + 2 * lane);
+          v[nt][0] = acc[0][nt][0] + pv.x;
+          v[nt][1] = acc[0][nt][1] + pv.y;
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pb->fempty[b]);
+        if (row < g.n) {
+          double* o = out.p + (long)row * out.rs;
+          const double is = oscale ? __ldg(isp + 2 * (long)row) : 1.0;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            const int n = nt * 8 + 2 * (lane & 3);
+            double v0 = v[nt][0], v1 = v[nt][1];
+            if (oscale) {
+              v0 *= is;
+              v1 *= is;
+            }
+            if (n + 1 < out.rs) *reinterpret_cast<double2*>(o + n) = make_double2(v0, v1);
+            else if (n < out.rs) o[n] = v0;
+          }
+        }
+      } else {
+        warp_arrive(&pb->fempty[b]);
       }
     }
   }
