@@ -204,7 +204,9 @@ int orth_complement(Handle& h, NMat X, const double* C1) {
   launched();
   CK(cudaMemcpyAsync(h.pinned + 9, dinfo, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  if (h.pinned[9] > 1e-14) {
+  // re-orthogonalise when the block's defect exceeds the reference's own
+  // re-orthonormalisation trigger (orthonormal_columns, dlra.py:36-41: 1e-12)
+  if (h.pinned[9] > 1e-12) {
     // pass 4: Q <- Q TA - U0 TB (into Qa, then swap)
     NMat Q2 = h.Qa.view(g, k, st);
     lincomb(g, Qv, NMat{}, U0, TA, TB, Q2, nullptr, h.part, st);
