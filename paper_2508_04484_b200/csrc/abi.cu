@@ -439,10 +439,17 @@ int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max
     pnd::streaming_step(h, dt);
     if (truncate_after & 1) pnd::truncate(h, theta, rank_min, rank_max, &t1, &rank);
     pnd::scattering_step(h, dt);
-    if (truncate_after & 2) pnd::truncate(h, theta, rank_min, rank_max, &t2, &rank);
+    bool ugram = false;
+    if (truncate_after & 2) {
+      // the last rotation of the step also forms U^T U for the defect diagnostic
+      const int kmax = h.ru < h.rv ? h.ru : h.rv;  // the truncated rank is at most this
+      double* G = want_defect ? pnd::defect_gram_slot(h, kmax, kmax) : nullptr;
+      pnd::truncate(h, theta, rank_min, rank_max, &t2, &rank, G);
+      ugram = want_defect;
+    }
     pnd::dose_accumulate_step(h, dt, tally_steps != 0);
     double defect = 0.0;
-    if (want_defect) defect = pnd::orth_defect(h);
+    if (want_defect) defect = pnd::orth_defect(h, ugram);
     if (out) {
       out[0] = t1;
       out[1] = t2;

@@ -77,9 +77,13 @@ void set_isp(Handle& h);       // refresh the [1/S, 0] halo rows from inv_s
 
 void streaming_step(Handle& h, double dt);
 void scattering_step(Handle& h, double dt);
-void truncate(Handle& h, double theta, int rmin, int rmax, double* tail, int* rank);
+// ugram (optional, r1 x r1): also form U1^T U1 in the rotation pass
+void truncate(Handle& h, double theta, int rmin, int rmax, double* tail, int* rank,
+              double* ugram = nullptr);
 void dose_accumulate_step(Handle& h, double dt, bool tally_steps);
-double orth_defect(Handle& h);
+// have_ugram: U^T U is already in defect_gram_slot (from the last truncation)
+double orth_defect(Handle& h, bool have_ugram = false);
+double* defect_gram_slot(Handle& h, int ru, int rv);
 // Q (k columns) = orthonormal basis of (I - U U^T) X; C1 = U^T X (device, ua x b; null
 // when U is empty). Returns k; the result is installed as the state's Q.
 int orth_complement(Handle& h, NMat X, const double* C1);

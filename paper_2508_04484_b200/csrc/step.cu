@@ -541,7 +541,8 @@ __global__ void defect_kernel(const double* G, int r, double* out) {
 }
 }  // namespace
 
-void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int* rank_out) {
+void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int* rank_out,
+              double* ugram) {
   const int p = h.ru, q = h.rv, k = p < q ? p : q;
   cudaStream_t st = h.st;
   phase(h, PH_SVD);
@@ -576,8 +577,11 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
     double* Pc = slot(h, S_PC, (size_t)p * r1);
     CK(cudaMemcpy2DAsync(Pc, r1 * sizeof(double), P, k * sizeof(double), r1 * sizeof(double), p,
                          cudaMemcpyDeviceToDevice, st));
-    lincomb(g, state_u(h), state_q(h), NMat{}, Pc, nullptr, Un, nullptr, h.part, st);
+    // ugram: the rotated basis' Gram U1^T U1 (the orthonormality diagnostic)
+    // comes out of the same pass
+    lincomb(g, state_u(h), state_q(h), NMat{}, Pc, nullptr, Un, ugram, h.part, st);
   }
+  if (ugram && all_zero) gram_xy(g, Un, Un, ugram, h.part, st);
   phase(h, PH_SVD);
   double* Vn = slot(h, S_VNEW, (size_t)m * r1);
   gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);
@@ -612,14 +616,18 @@ void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
   phase(h, -1);
 }
 
-double orth_defect(Handle& h) {
+double* defect_gram_slot(Handle& h, int ru, int rv) {
+  return slot(h, S_DEF, (size_t)ru * ru + (size_t)rv * rv + 2);
+}
+
+double orth_defect(Handle& h, bool have_ugram) {
   consolidate(h);
   const Geom& g = h.g;
   cudaStream_t st = h.st;
   phase(h, PH_DEFECT);
-  double* G = slot(h, S_DEF, (size_t)h.ru * h.ru + (size_t)h.rv * h.rv + 2);
+  double* G = defect_gram_slot(h, h.ru, h.rv);
   double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
-  gram_xy(g, state_u(h), state_u(h), G, h.part, st);  // U^T U
+  if (!have_ugram) gram_xy(g, state_u(h), state_u(h), G, h.part, st);  // U^T U
   double* GV = G + (size_t)h.ru * h.ru;
   gemm(h.rv, h.rv, h.m, 1.0, tr(rowm(h.V.p, h.rv)), 0, rowm(h.V.p, h.rv), 0, 0.0,
        rowm(GV, h.rv), 0, 1, st);
