@@ -32,6 +32,23 @@ struct LBars {
   uint64_t sfull[LNSTG_MAX], sempty[LNSTG_MAX];
 };
 
+// Gram tile index -> (row tile, column tile): X^T out tiles (row tiles < XT)
+// first, then the upper triangle (column tile >= row tile - XT) of out^T out
+__device__ __forceinline__ void gram_tile(int tile, int XT, int NB8, int& ti, int& tj) {
+  if (tile < XT * NB8) {
+    ti = tile / NB8;
+    tj = tile - ti * NB8;
+    return;
+  }
+  int u = tile - XT * NB8, r = 0;
+  while (u >= NB8 - r) {
+    u -= NB8 - r;
+    ++r;
+  }
+  ti = XT + r;
+  tj = r + u;
+}
+
 struct LIn {
   const double* p[3];
   int cols[3], rs[3];
@@ -59,7 +76,9 @@ __global__ void __launch_bounds__(LTH, 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
   const int XT = (xcn + 7) / 8;                  // X^T out row tiles
-  const int GT = grams ? (XT + (skip_tt ? 0 : NB8)) * NB8 : 0;  // Gram tiles
+  // Gram tiles: X^T out (XT x NB8), then the upper triangle of the symmetric
+  // out^T out (mirrored when stored)
+  const int GT = grams ? XT * NB8 + (skip_tt ? 0 : NB8 * (NB8 + 1) / 2) : 0;
   if (tid == 0) {
     for (int b = 0; b < nstg; ++b) {
       mbar_init(&bars->sfull[b], 1);
@@ -106,7 +125,7 @@ __global__ void __launch_bounds__(LTH, 2)
   }
 
   const int m = lane >> 2, kq = lane & 3;
-  constexpr int GPW_MAX = (2 * NB8 * NB8 + LCW - 1) / LCW;  // X^T out + out^T out tiles
+  constexpr int GPW_MAX = (NB8 * NB8 + NB8 * (NB8 + 1) / 2 + LCW - 1) / LCW;
   double gacc[GPW_MAX][2];
 #pragma unroll
   for (int t = 0; t < GPW_MAX; ++t) gacc[t][0] = gacc[t][1] = 0.0;
@@ -175,7 +194,8 @@ __global__ void __launch_bounds__(LTH, 2)
       for (int t = 0; t < GPW_MAX; ++t) {
         const int tile = warp + LCW * t;
         if (tile < GT) {
-          const int ti = tile / NB8, tj = tile - ti * NB8;
+          int ti, tj;
+          gram_tile(tile, XT, NB8, ti, tj);
           const bool xg = ti < XT;
           const double* pa = xg ? sx + (ti * 8 + m) : T + ((ti - XT) * 8 + m);
           const int sa = xg ? rsx : TS;
@@ -195,7 +215,8 @@ __global__ void __launch_bounds__(LTH, 2)
     for (int t = 0; t < GPW_MAX; ++t) {
       const int tile = warp + LCW * t;
       if (tile < GT) {
-        const int ti = tile / NB8, tj = tile - ti * NB8;
+        int ti, tj;
+        gram_tile(tile, XT, NB8, ti, tj);
         const bool xg = ti < XT;
         const int rrow = (xg ? ti : ti - XT) * 8 + m, col = tj * 8 + 2 * kq;
         const int nrow = xg ? xcn : nb;
@@ -203,6 +224,12 @@ __global__ void __launch_bounds__(LTH, 2)
         if (rrow < nrow) {
           if (col < nb) o[base + (size_t)rrow * nb + col] = gacc[t][0];
           if (col + 1 < nb) o[base + (size_t)rrow * nb + col + 1] = gacc[t][1];
+        }
+        if (!xg && ti - XT != tj) {  // mirror the off-diagonal out^T out tile
+          if (rrow < nb) {
+            if (col < nb) o[base + (size_t)col * nb + rrow] = gacc[t][0];
+            if (col + 1 < nb) o[base + (size_t)(col + 1) * nb + rrow] = gacc[t][1];
+          }
         }
       }
     }
