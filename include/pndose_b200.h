@@ -145,6 +145,14 @@ int pnd_deposit(pnd_handle* h, int ng, int n_rays, const int32_t* ray_seg_off,
                 int n_march_segs, const double* averages, const double* mres, double* values,
                 double* residual);
 
+/* ---- z-slab decomposition (one process per GPU) -------- */
+/* NCCL unique id (128 bytes) made on rank 0 and broadcast by the caller */
+int pnd_comm_unique_id(char* out128);
+/* This handle's grid (nx, ny, nz) is planes [z0, z0 + nz) of a grid with
+ * nz_global planes; with world > 1 the stencil halo planes and every Gram sum
+ * go over NCCL (comm.cu). Call right after pnd_create. */
+int pnd_set_slab(pnd_handle* h, int z0, int nz_global, const char* id128, int rank, int world);
+
 /* ---- measurement and synthetic inputs (bench.py) ------------------------ */
 /* phase timer (CUDA events on the handle stream around every phase of the step) */
 int pnd_timing(pnd_handle* h, int enable);

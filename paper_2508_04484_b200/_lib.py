@@ -61,6 +61,8 @@ SIGNATURES = {
     "pnd_march": [_P, _I, _I, _I, _P, _P, _P, _D, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P,
                   _P, _P, _P],
     "pnd_deposit": [_P, _I, _I, _P, _P, _P, _P, _P, _P, _D, _I, _P, _P, _P, _P],
+    "pnd_comm_unique_id": [ctypes.c_char_p],
+    "pnd_set_slab": [_P, _I, _I, ctypes.c_char_p, _I, _I],
 }
 
 PHASES = ["kstage", "l_gram", "l_side", "tsqr_n", "tsqr_m", "s_gram", "s_rk4", "svd",
@@ -139,6 +141,13 @@ class Handle:
             pass
 
     # ------------------------------------------------------------ helpers
+    def set_slab(self, z0, nz_global, comm_id=None, rank=0, world=1):
+        """This handle holds planes [z0, z0 + nz) of a grid of nz_global planes
+        (comm.cu); comm_id: the 128-byte NCCL id shared by the world."""
+        cid = comm_id if comm_id is not None else bytes(128)
+        self.call("pnd_set_slab", int(z0), int(nz_global), ctypes.c_char_p(bytes(cid)),
+                  int(rank), int(world))
+
     def set_angular(self, a_plus, a_minus):
         ap, am = f64(a_plus), f64(a_minus)
         self.call("pnd_set_angular", ptr(ap), ptr(am))
@@ -175,3 +184,12 @@ class Handle:
         v = np.empty((self.m, rv.value))
         self.call("pnd_state_get", ptr(u), ptr(s), ptr(v))
         return u, s, v
+
+
+def comm_unique_id():
+    """A fresh NCCL unique id (128 bytes) for pnd_set_slab."""
+    buf = ctypes.create_string_buffer(128)
+    rc = lib().pnd_comm_unique_id(buf)
+    if rc != 0:
+        raise BY_CODE.get(rc, PnDoseError)("cannot create an NCCL unique id")
+    return buf.raw

@@ -60,6 +60,17 @@ void launched() {
 
 long long launch_count() { return g_launches; }
 
+int max_smem_optin() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0, x = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&x, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    v = x;
+  }
+  return v;
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -226,6 +237,8 @@ int pnd_destroy(pnd_handle* hh) {
   for (auto* b : bufs) b->free_();
   pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs};
   for (auto* b : nb) b->d.free_();
+  pnd::comm_destroy(h.comm);
+  h.comm = nullptr;
   for (auto& b : h.sm) b.free_();
   h.cls.free_();
   h.iflag.free_();
@@ -774,6 +787,47 @@ int pnd_deposit(pnd_handle* hh, int ng, int n_rays, const int32_t* ray_seg_off,
     }
     if (residual) down(residual, R, n, h.st);
     CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_comm_unique_id(char* out128) {
+  try {
+    pnd::comm_unique_id(out128);
+    return PND_OK;
+  } catch (const pnd::Error& e) {
+    return e.code;
+  } catch (...) {
+    return PND_EDEVICE;
+  }
+}
+
+int pnd_set_slab(pnd_handle* hh, int z0, int nz_global, const char* id128, int rank, int world) {
+  return guard(hh, [&](Handle& h) {
+    pnd::Geom& g = h.g;
+    if (z0 < 0 || nz_global < g.nz || z0 + g.nz > nz_global)
+      pnd::fail(PND_ECONFIG, "slab planes outside the global grid");
+    if (world > 1 && g.nz < 2) pnd::fail(PND_ECONFIG, "a slab needs at least 2 planes");
+    if (world < 1 || rank < 0 || rank >= world) pnd::fail(PND_ECONFIG, "bad rank / world");
+    g.z0 = z0;
+    g.nzg = nz_global;
+    // active axes and the 2-cell rule follow the global grid (spatial.py:84-88)
+    const int dims[3] = {g.nx, g.ny, nz_global};
+    h.stencil_error.clear();
+    const char* names[3] = {"nx", "ny", "nz"};
+    for (int a = 0; a < 3; ++a)
+      if (dims[a] == 2 && h.stencil_error.empty())
+        h.stencil_error = std::string("grid.") + names[a] +
+                          "=2: grids with 2 cells along a used axis cannot host the 3-point "
+                          "one-sided stencil; use 1 (inactive) or >= 3";
+    g.na = 0;
+    for (int a = 0; a < 3; ++a)
+      if (dims[a] > 1) g.axis[g.na++] = a;
+    for (int a = g.na; a < 3; ++a) g.axis[a] = 0;
+    g.ns = 2 * g.na;
+    pnd::comm_destroy(h.comm);
+    h.comm = nullptr;
+    if (world > 1) h.comm = pnd::comm_create(id128, rank, world);
+    g.comm = h.comm;
   });
 }
 

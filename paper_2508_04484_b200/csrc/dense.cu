@@ -591,7 +591,8 @@ __global__ void __launch_bounds__(512)
 }
 
 void set_smem(const void* fn, size_t bytes) {
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  if (bytes > (size_t)kMaxDynSmem) fail(PND_ECONFIG, "kernel tile exceeds shared memory");
+  allow_max_smem(fn);
 }
 
 // partition of a level: leaves of `br` rows, a short tail merged into the

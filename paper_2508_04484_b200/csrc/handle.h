@@ -62,6 +62,7 @@ struct Handle {
   IBuf iflag;
   DBuf dep, prev;             // dose tally
   double* pinned = nullptr;   // small pinned readback buffer
+  Comm* comm = nullptr;       // z-slab communicator (multi-GPU), null on one device
   TimerState timer;
 };
 

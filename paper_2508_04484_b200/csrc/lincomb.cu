@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(LTH, 2)
       const double* wv = in.w ? sb + in.woff : nullptr;
       for (int e = lane; e < 8 * NB8 * 8; e += 32) {
         const int i = warp * 8 + e / (NB8 * 8), c = e % (NB8 * 8);
-        const double v = c < in.cols[0] ? y[i * in.rs[0] + c] : 0.0;
+        // rows past n are halo rows (possibly a neighbour slab's): no Gram input
+        const double v = c < in.cols[0] && c0 + i < n ? y[i * in.rs[0] + c] : 0.0;
         T[i * TS + c] = wv ? wv[i] * v : v;
       }
       __syncwarp();
@@ -178,7 +179,9 @@ __global__ void __launch_bounds__(LTH, 2)
     for (int nt = 0; nt < NB8; ++nt) {
       const double v0 = acc[0][nt][0] + acc[1][nt][0], v1 = acc[0][nt][1] + acc[1][nt][1];
       const int col = nt * 8 + 2 * kq;
-      *reinterpret_cast<double2*>(T + il * TS + col) = make_double2(v0, v1);
+      // rows past n (halo rows, possibly a neighbour slab's) stay out of the Grams
+      *reinterpret_cast<double2*>(T + il * TS + col) =
+          row < n ? make_double2(v0, v1) : make_double2(0.0, 0.0);
       if (out.p && row < n) {
         double* o = out.p + row * out.rs + col;
         if (col + 1 < out.rs) *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
@@ -290,8 +293,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
       fail(PND_ECONFIG, "lincomb tile exceeds shared memory");
   }
   const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
-  CK(cudaFuncSetAttribute(lincomb_kernel<NB8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  allow_max_smem(lincomb_kernel<NB8>);
   int nblk = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, lincomb_kernel<NB8>, LTH, smem));
   if (nblk < 1) nblk = 1;
@@ -308,6 +310,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   if (grams) {
     lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
     launched();
+    comm_allreduce(g, grams, count, st);
   }
 }
 

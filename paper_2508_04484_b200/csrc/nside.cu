@@ -129,8 +129,7 @@ template <int T8, int NPH>
 void pgram_launch(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
   const int LS = pad4(T8 * 8);
   const size_t smem = 2 * (size_t)PC * LS * sizeof(double);
-  CK(cudaFuncSetAttribute(pgram_kernel<T8, NPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  allow_max_smem(pgram_kernel<T8, NPH>);
   const int nchunks = (a.geo.n + PC - 1) / PC;
   int grid = sm_count() * resident(pgram_kernel<T8, NPH>, 256, smem);
   if (grid > nchunks) grid = nchunks;
@@ -140,6 +139,7 @@ void pgram_launch(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
   launched();
   reduce_blocks<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, a.out);
   launched();
+  comm_allreduce(a.geo, a.out, count, st);
 }
 
 // ===================================================================== small kernels
@@ -214,7 +214,8 @@ __global__ void unit_rows_kernel(Geom g, NMat U) {
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x) {
     const int c = (int)(e / U.rs), j = (int)(e - (long)c * U.rs);
-    U.p[e] = (j < U.cols && c == j) ? 1.0 : 0.0;
+    const long cg = c + (long)g.z0 * g.nx * g.ny;  // global cell index (slabs)
+    U.p[e] = (j < U.cols && cg == j) ? 1.0 : 0.0;
   }
 }
 
@@ -236,7 +237,9 @@ __global__ void random_rows_kernel(Geom g, NMat U, unsigned long long seed) {
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x) {
     const int c = (int)(e / U.rs), j = (int)(e - (long)c * U.rs);
-    U.p[e] = j < U.cols ? hash_normal(seed * 0x100000001B3ULL + (unsigned long long)e) : 0.0;
+    // keyed by the global cell, so a slab decomposition draws the same matrix
+    const unsigned long long key = (unsigned long long)(c + (long)g.z0 * g.nx * g.ny) * U.rs + j;
+    U.p[e] = j < U.cols ? hash_normal(seed * 0x100000001B3ULL + key) : 0.0;
   }
 }
 

@@ -35,6 +35,22 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 void check_cuda(cudaError_t e, const char* what);
 #define CK(x) ::pnd::check_cuda((x), #x)
+
+// Allow a kernel the device's whole opt-in shared memory (227 KB). The
+// attribute is a per-function cap shared by every host thread, so it is set
+// to the maximum once instead of to each launch's size (a per-launch value
+// would let a concurrent smaller launch on another handle shrink the cap
+// under a larger one).
+constexpr int kMaxDynSmem = 227 * 1024;
+int max_smem_optin();  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the current device
+template <class F>
+inline void allow_max_smem(F* fn) {
+  cudaFuncAttributes fa{};
+  check_cuda(cudaFuncGetAttributes(&fa, (const void*)fn), "cudaFuncGetAttributes");
+  check_cuda(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  max_smem_optin() - (int)fa.sharedSizeBytes),
+             "cudaFuncSetAttribute");
+}
 // after every kernel launch: surface launch errors, count the launch
 void launched();
 long long launch_count();
@@ -52,7 +68,22 @@ struct Geom {
   int na;         // number of active axes
   int axis[3];    // active axis ids in x, y, z order (the first has stride 1)
   int ns;         // number of stencils = 2 * na (order: axis-major, + then -)
+  // z-slab of a multi-GPU grid (comm.cu): this device holds global planes
+  // [z0, z0 + nz) of nzg; comm != null -> halo planes and Gram sums go over NCCL
+  int z0 = 0;
+  int nzg = 0;    // 0: single device (nzg = nz)
+  void* comm = nullptr;
 };
+
+// ------------------------------------------------------------ slab communication (comm.cu)
+struct Comm;
+void comm_unique_id(char* out128);
+Comm* comm_create(const char* id128, int rank, int world);
+void comm_destroy(Comm* c);
+// sum a small device block over the slabs (no-op on one device)
+void comm_allreduce(const Geom& g, double* p, size_t count, cudaStream_t st);
+// fill the 2-plane halo rows of an n-side matrix from the neighbouring slabs
+void comm_halo_rows(const Geom& g, double* rows, int rs, cudaStream_t st);
 
 // ------------------------------------------------------------ device buffers
 struct DBuf {

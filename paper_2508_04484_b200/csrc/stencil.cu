@@ -139,11 +139,13 @@ struct Ctx {
     const int ck = c / nxy, rem = c - ck * nxy;
     const int cj = rem / g.nx, ci = rem - cj * g.nx;
     inner = true;
+    // z in global planes (a slab's faces are interior unless they are the grid's)
+    const int gk = ck + g.z0, gnz = g.nzg > 0 ? g.nzg : g.nz;
 #pragma unroll
     for (int ai = 0; ai < NA; ++ai) {
       const int axis = g.axis[ai];
-      idx[ai] = axis == 0 ? ci : axis == 1 ? cj : ck;
-      len[ai] = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
+      idx[ai] = axis == 0 ? ci : axis == 1 ? cj : gk;
+      len[ai] = axis == 0 ? g.nx : axis == 1 ? g.ny : gnz;
       inner = inner && idx[ai] >= 2 && idx[ai] <= len[ai] - 3;
     }
     if (!PRE) {
@@ -448,8 +450,7 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  CK(cudaFuncSetAttribute(kstage_kernel<NA, RB, PRE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  allow_max_smem(kstage_kernel<NA, RB, PRE>);
   const int nchunks = (g.n + KC - 1) / KC;
   int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE>, PTH, smem);
   if (grid > nchunks) grid = nchunks;
@@ -535,7 +536,9 @@ __global__ void __launch_bounds__(GPTH, 1)
       double* Cb = Fb + NS * W * GTL;
       // unscaled centre rows (A operand); rows past n are zero halo rows
       for (int j = cj; j < w; j += JS)
-        Cb[ci * XS + j] = j < a1 ? X1s[(ci + 2) * X1.rs + j] : X2s[(ci + 2) * X2.rs + j - a1];
+        Cb[ci * XS + j] = c0 + ci >= g.n ? 0.0  // past n: halo rows (maybe a neighbour's)
+                          : j < a1 ? X1s[(ci + 2) * X1.rs + j]
+                                   : X2s[(ci + 2) * X2.rs + j - a1];
       Ctx<GC, NA> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
@@ -647,8 +650,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  CK(cudaFuncSetAttribute(sgram_kernel<NA, T8, GC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  allow_max_smem(sgram_kernel<NA, T8, GC>);
   const int nchunks = (g.n + GC - 1) / GC;
   int grid = sm_count() * resident(sgram_kernel<NA, T8, GC>, GPTH, smem);
   if (grid > nchunks) grid = nchunks;
@@ -665,6 +667,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   }
   reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
   launched();
+  comm_allreduce(g, out, count, st);
 }
 
 template <int NA>

@@ -149,6 +149,7 @@ void set_isp(Handle& h) {
   }
   isp_kernel<<<148 * 8, 256, 0, h.st>>>(h.inv_s.p, h.g.n, h.isp.p + 2 * (size_t)h.g.halo);
   launched();
+  comm_halo_rows(h.g, h.isp.p + 2 * (size_t)h.g.halo, 2, h.st);  // slab faces
 }
 
 static const double* isp_rows(Handle& h) { return h.isp.p + 2 * (size_t)h.g.halo; }
@@ -229,6 +230,7 @@ void streaming_step(Handle& h, double dt) {
   cudaStream_t st = h.st;
   const NMat U0 = state_u(h);
   const double* isp = isp_rows(h);
+  comm_halo_rows(g, U0.p, U0.rs, st);  // U0's neighbour planes (K stage 0, L- and S-Grams)
 
   // --- K phase: K1 = K0 + dK, K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
   phase(h, PH_LSIDE);
@@ -262,6 +264,7 @@ void streaming_step(Handle& h, double dt) {
     ka.in_scaled = stage > 0;
     ka.out_scaled = stage < 3;
     phase(h, PH_KSTAGE);
+    if (stage > 0) comm_halo_rows(g, ka.X.p, ka.X.rs, st);  // the previous stage's output
     kstage(ka, st);
     phase(h, PH_LSIDE);
   }
@@ -314,6 +317,7 @@ void streaming_step(Handle& h, double dt) {
   // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
   double* G = slot(h, S_G, (size_t)ns * ru * ru);
   phase(h, PH_SGRAM);
+  if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
   stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
   phase(h, PH_SRK4);
   double* Vhr = slot(h, S_VHR, (size_t)m * rv);

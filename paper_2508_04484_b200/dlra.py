@@ -15,6 +15,8 @@ contract is on U S V^T, singular values and ranks (tests/test_gpu_parity.py).
 
 from dataclasses import dataclass, field
 
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -35,8 +37,9 @@ def _a_split(ops):
 
 
 def handle_for(shape, spacing, m):
-    """Shared device handle per (grid, m) for the function-level API."""
-    key = (tuple(shape), tuple(spacing), int(m))
+    """Shared device handle per (grid, m, host thread) for the function-level
+    API (a handle is stream-ordered state: one per thread, never shared)."""
+    key = (tuple(shape), tuple(spacing), int(m), threading.get_ident())
     h = _HANDLES.get(key)
     if h is None:
         h = _lib.Handle(shape, spacing, m)

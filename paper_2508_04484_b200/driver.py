@@ -55,15 +55,23 @@ class SimulationResult:
 class DeviceSolver:
     """One bundle's device state: operators, flux tables, low-rank factors."""
 
-    def __init__(self, bundle: ProblemBundle, device: int = 0):
+    def __init__(self, bundle: ProblemBundle, device: int = 0, slab=None, comm_id=None):
+        """slab: a slabs.Slab (this process's z-planes of a multi-GPU solve)
+        with comm_id the world's NCCL id; None = the whole grid on one GPU."""
         self.bundle = bundle
         b = bundle
-        self.h = _lib.Handle(b.shape, b.spacing, b.n_moments, device)
+        self.slab = slab
+        lo, hi = (0, b.n_cells) if slab is None else slab.rows
+        shape = b.shape if slab is None else (b.shape[0], b.shape[1], slab.planes)
+        self.rows = (lo, hi)
+        self.h = _lib.Handle(shape, b.spacing, b.n_moments, device)
+        if slab is not None:
+            self.h.set_slab(slab.z0, b.shape[2], comm_id, slab.rank, slab.world)
         self.h.set_angular(*b.a_split())
-        self.h.set_materials(b.cell_class, b.class_atomic)
+        self.h.set_materials(b.cell_class[lo:hi], b.class_atomic)
         nb = len(b.fluxes)
         for i, (f, tm) in enumerate(zip(b.fluxes, b.t_ms)):
-            vals = _lib.f64(f.values)
+            vals = _lib.f64(f.values[lo:hi])
             t = _lib.f64(tm)
             self.h.call("pnd_set_flux_table", i, nb, int(vals.shape[1]), _lib.ptr(vals),
                         _lib.ptr(t))
@@ -75,7 +83,8 @@ class DeviceSolver:
         n, m = b.n_cells, b.n_moments
         r0 = min(b.rank_min if rank is None else rank, n, m)
         st = LowRankState.zero(n, m, r0, seed=b.seed if seed is None else seed)
-        self.h.set_state(st.u, st.s, st.v)
+        lo, hi = self.rows
+        self.h.set_state(st.u[lo:hi], st.s, st.v)
 
     def select_flux(self, which: int, e_mev: float):
         fl = self.bundle.fluxes
@@ -111,7 +120,8 @@ class DeviceSolver:
         return out
 
     def dose(self) -> np.ndarray:
-        out = np.empty(self.bundle.n_cells)
+        """Deposited energy of this device's cells (the slab's rows)."""
+        out = np.empty(self.rows[1] - self.rows[0])
         self.h.call("pnd_get_dose", _lib.ptr(out))
         return out
 
@@ -123,14 +133,17 @@ class DeviceSolver:
 
 
 def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0,
-               solver="dlra") -> SimulationResult:
-    """The pseudo-time loop of run_simulation (driver.py:541-666) on the device."""
+               solver="dlra", slab=None, comm_id=None) -> SimulationResult:
+    """The pseudo-time loop of run_simulation (driver.py:541-666) on the device.
+
+    slab / comm_id: this process's z-slab of a multi-GPU solve (slabs.plan)
+    and the world's communicator id; the dose then covers the slab's cells."""
     if solver != "dlra":
         raise ConfigError(f"unknown solver '{solver}'")
     t_start = time.perf_counter()
     b = bundle
     n, m = b.n_cells, b.n_moments
-    solver_ = DeviceSolver(b, device)
+    solver_ = DeviceSolver(b, device, slab=slab, comm_id=comm_id)
     solver_.init_state()
     edges = b.pseudo_time_edges()
     n_steps = len(edges) - 1
@@ -155,12 +168,13 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         peak_state = max(peak_state, n * r + r * r + m * r)
         peak_transient = max(peak_transient, n * 2 * r + 4 * r * r + m * 2 * r)
     deposited = solver_.dose()
+    lo, hi = solver_.rows
     unc = None
     if b.uncollided_tally == "groups":
-        unc = b.uncollided_dose()
+        unc = b.uncollided_dose()[lo:hi]
         deposited = deposited + unc
     solver_.close()
-    density = b.density
+    density = b.density[lo:hi]
     dose = DoseGrid(deposited=deposited, dose=deposited / density)
     full = n * m
     diagnostics = {
