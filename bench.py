@@ -18,10 +18,10 @@ exported to tests/golden/bench_physics.npz.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1 (torchrun): every rank runs an independent replica of the workload on
-its own GPU ("scaling": "weak"; the slab-sharded joint solve is not built yet,
-DESIGN.md §Multi-GPU). Timing: CUDA events on the handle's stream around the
-K timed steps, barrier + synchronize on both sides, max over ranks.
+N > 1 (torchrun): one joint solve of the same 256^3 grid, z-slab sharded (each
+rank owns nz/N planes; the stencil halo planes and every Gram sum go over NCCL,
+DESIGN.md §6), "scaling": "strong". Timing: CUDA events on the handle's stream
+around the K timed steps, barrier + synchronize on both sides, max over ranks.
 """
 
 import argparse
@@ -112,7 +112,9 @@ def separable_flux(b, beam):
 
 
 class Workload:
-    def __init__(self, nside=256, rank=20, device=0, n_max=19):
+    def __init__(self, nside=256, rank=20, device=0, n_max=19, slab=None, comm_id=None):
+        """slab: this process's z-planes of the joint multi-GPU solve (slabs.plan),
+        comm_id the world's NCCL id; None = the whole grid on this GPU."""
         from paper_2508_04484_b200 import _lib
         from paper_2508_04484_b200.driver import DeviceSolver
 
@@ -121,11 +123,18 @@ class Workload:
         self.rank = rank
         self.solver = DeviceSolver.__new__(DeviceSolver)
         self.solver.bundle = b
-        self.solver.h = _lib.Handle(b.shape, b.spacing, b.n_moments, device)
+        lo, hi = (0, b.n_cells) if slab is None else slab.rows
+        z0, z1 = (0, b.shape[2]) if slab is None else (slab.z0, slab.z1)
+        shape = (b.shape[0], b.shape[1], z1 - z0)
+        self.solver.rows = (lo, hi)
+        self.solver.h = _lib.Handle(shape, b.spacing, b.n_moments, device)
         h = self.solver.h
+        if slab is not None:
+            h.set_slab(z0, b.shape[2], comm_id, slab.rank, slab.world)
         h.set_angular(*b.a_split())
-        h.set_materials(b.cell_class, b.class_atomic)
+        h.set_materials(b.cell_class[lo:hi], b.class_atomic)
         lat, depth = separable_flux(b, beam)
+        depth = depth[z0:z1]
         lat, depth, tm = _lib.f64(lat), _lib.f64(depth), _lib.f64(b.t_ms[0])
         h.call("pnd_set_flux_separable", 0, 1, int(depth.shape[1]), _lib.ptr(lat),
                _lib.ptr(depth), _lib.ptr(tm))
@@ -372,7 +381,8 @@ def main():
               "grid": [args.nside] * 3, "pn_order": 19, "moments": 400, "rank": args.rank,
               "model": "fokker-planck", "n_gpus": args.gpus,
               "l2": "inputs larger than L2 (U is n x r doubles = 2.7 GB per factor)",
-              "parallelism": f"replicas x{world}" if world > 1 else "single"}
+              "parallelism": f"z-slabs x{world} (NCCL halo planes + Gram allreduce)"
+              if world > 1 else "single"}
 
     if args.impl == "reference":
         if rank_id != 0:
@@ -399,7 +409,17 @@ def main():
     from paper_2508_04484_b200 import _lib
 
     torch.cuda.set_device(local)
-    wl = Workload(nside=args.nside, rank=args.rank, device=local)
+    slab, cid = None, None
+    if world > 1:
+        # one joint solve, z-slab sharded: halo planes + Gram allreduces over NCCL
+        from paper_2508_04484_b200 import _lib as plib
+        from paper_2508_04484_b200 import slabs
+
+        obj = [plib.comm_unique_id() if rank_id == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cid = obj[0]
+        slab = slabs.plan(args.nside, args.nside, args.nside, world, rank_id)
+    wl = Workload(nside=args.nside, rank=args.rank, device=local, slab=slab, comm_id=cid)
     h = wl.solver.h
     n_steps_total = len(wl.edges) - 1
     if wl.k0 + args.warmup + args.steps > n_steps_total:
@@ -439,8 +459,9 @@ def main():
     if rank_id != 0:
         dist.barrier()
         return
-    value = world * args.steps / dev_s
-    e2e = world * args.steps / t_host
+    # one joint solve over all ranks: a step is one energy step of the whole grid
+    value = args.steps / dev_s
+    e2e = args.steps / t_host
 
     b = wl.bundle
     model = phase_model(b.n_cells, args.rank, b.n_moments, 2 * 3)
@@ -483,8 +504,8 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": wl.h2d_bytes_per_step(),
                 "d2h_bytes_per_step": wl.d2h_bytes_per_step(),
                 "path": "paper_2508_04484_b200.driver.DeviceSolver (public API, host coefficients "
