@@ -202,6 +202,8 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     g.nz = nz;
     g.n = (int)n;
     g.ld = (int)((n + 31) / 32 * 32);
+    g.inv_nx = 1.0 / nx;
+    g.inv_nxy = 1.0 / ((double)nx * ny);
     g.halo = (int)halo;
     g.h[0] = dx;
     g.h[1] = dy;

@@ -72,6 +72,7 @@ struct Geom {
   // [z0, z0 + nz) of nzg; comm != null -> halo planes and Gram sums go over NCCL
   int z0 = 0;
   int nzg = 0;    // 0: single device (nzg = nz)
+  double inv_nx = 0.0, inv_nxy = 0.0;  // 1/nx, 1/(nx ny): cell -> (i, j, k) without division
   void* comm = nullptr;
 };
 

@@ -135,9 +135,15 @@ struct Ctx {
   }
 
   __device__ __forceinline__ void init(const Geom& g, int c, int i, const double* I) {
+    // cell -> (i, j, k) by reciprocal multiply + one correction step (exact
+    // for c < 2^31: the double product is within one of the true quotient)
     const int nxy = g.nx * g.ny;
-    const int ck = c / nxy, rem = c - ck * nxy;
-    const int cj = rem / g.nx, ci = rem - cj * g.nx;
+    int ck = __double2int_rz((double)c * g.inv_nxy);
+    ck += (c - ck * nxy >= nxy) - (c - ck * nxy < 0);
+    const int rem = c - ck * nxy;
+    int cj = __double2int_rz((double)rem * g.inv_nx);
+    cj += (rem - cj * g.nx >= g.nx) - (rem - cj * g.nx < 0);
+    const int ci = rem - cj * g.nx;
     inner = true;
     // z in global planes (a slab's faces are interior unless they are the grid's)
     const int gk = ck + g.z0, gnz = g.nzg > 0 ? g.nzg : g.nz;
