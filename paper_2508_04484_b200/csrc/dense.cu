@@ -636,7 +636,7 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
   {
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
-    if (sm <= 200 * 1024) {
+    if (sm + 1024 <= (size_t)kMaxDynSmem) {
       set_smem((const void*)qr_small_kernel, sm);
       qr_small_kernel<<<1, 512, sm, st>>>(a, rows, cols, lda, q, ldq, rfac);
       launched();

@@ -257,15 +257,17 @@ __device__ __forceinline__ void pipe_init(PipeBars* pb, int nstg, int conw) {
 // all NT n-tiles, k-steps dealt round-robin to four accumulator sets (4 NT
 // independent DMMA chains); B fragments come from a shared-memory copy of
 // Bcat in fragment order.
-constexpr int KC = 32;
-constexpr int KCS = pad4(KC);  // 36
-
-template <int NA, int RB, bool PRE>
+template <int NA, int RB, bool PRE, int KC>
 __global__ void __launch_bounds__(PTH, 1)
     kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
                   int K4, Seg S, int nstg, const double* __restrict__ isp, int oscale) {
   constexpr int NS = 2 * NA;
   constexpr int NT = RB / 8;
+  constexpr int KCS = pad4(KC);       // feature tile row length (k-major: k = feature)
+  constexpr int MT = KC / 8;          // m-tiles per chunk
+  constexpr int CG = KC / 4;          // former cell groups (4 cells each)
+  constexpr int JS = 8 * (FORMW / CG);  // former column stride
+  constexpr int KSPLIT = CONW / MT;   // contraction k-parts
   extern __shared__ __align__(128) double sm[];
   // staging slot s: sm + s S.total; feature buffer f: F0 + f K4 KCS
   double* const F0 = sm + nstg * S.total;
@@ -298,7 +300,8 @@ __global__ void __launch_bounds__(PTH, 1)
       }
     }
   } else if (warp < FORMW) {
-    const int ci = 4 * warp + (lane & 3), cj = lane >> 2;
+    // lane = (cell 4 (w % CG) + (lane & 3), column (lane >> 2) + 8 (w / CG) + JS t)
+    const int ci = 4 * (warp % CG) + (lane & 3), cj = (lane >> 2) + 8 * (warp / CG);
     Ring r(nstg);
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it, r.next()) {
@@ -313,21 +316,21 @@ __global__ void __launch_bounds__(PTH, 1)
       // base rows = unscaled centre rows (rows past n are zero halo rows; their
       // results are not stored)
       if (sepc) {
-        for (int j = cj; j < ra; j += 8) base[j * KCS + ci] = sb[S.coff + ci * U0.rs + j];
+        for (int j = cj; j < ra; j += JS) base[j * KCS + ci] = sb[S.coff + ci * U0.rs + j];
       } else {
-        for (int j = cj; j < ra; j += 8) base[j * KCS + ci] = Xs[(ci + 2) * X.rs + j];
+        for (int j = cj; j < ra; j += JS) base[j * KCS + ci] = Xs[(ci + 2) * X.rs + j];
       }
       Ctx<KC, NA, PRE> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       cx.rows(Xs, X.rs, ci, cj);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
 #pragma unroll
-      for (int t = 0; t < RB / 8; ++t) {
-        const int j = cj + 8 * t;
+      for (int t = 0; t < (RB + JS - 1) / JS; ++t) {
+        const int j = cj + JS * t;
         if (j < xc) {
           double v[NS];
-          if (fast) cx.template apply<true>(g, 8 * t, v);
-          else cx.template apply<false>(g, 8 * t, v);
+          if (fast) cx.template apply<true>(g, JS * t, v);
+          else cx.template apply<false>(g, JS * t, v);
 #pragma unroll
           for (int s = 0; s < NS; ++s) Fb[(s * xc + j) * KCS + ci] = v[s];
         }
@@ -339,12 +342,12 @@ __global__ void __launch_bounds__(PTH, 1)
       }
     }
   } else {
-    // contraction warp q: m-tile q & 3, k-half q >> 2 (two warps per SM
+    // contraction warp q: m-tile q % MT, k-part q / MT (two warps per SM
     // sub-partition, so one issues DMMAs while the other waits on its loads);
-    // the upper half's partials go through the consumed feature buffer
-    const int q = warp - FORMW, mt = q & 3, kh = q >> 2;
+    // the k-parts' partials go through the consumed feature buffer
+    const int q = warp - FORMW, mt = q % MT, kh = q / MT;
     const int nks = K4 / 4;
-    const int ks0 = kh ? nks / 2 : 0, ks1 = kh ? nks : nks / 2;
+    const int ks0 = (nks * kh) / KSPLIT, ks1 = (nks * (kh + 1)) / KSPLIT;
     const double* pb0 = sB + lane;
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
@@ -385,11 +388,11 @@ __global__ void __launch_bounds__(PTH, 1)
         acc[0][nt][1] += acc[1][nt][1];
       }
       named_sync(2, 32 * CONW);  // every contraction warp is done reading F[b]
-      double* red = Fb;          // [4 m-tiles][NT][64] upper-half partials
+      double* red = Fb;          // [k-part - 1][MT][NT][64] partials
       if (kh) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
-          *reinterpret_cast<double2*>(red + (mt * NT + nt) * 64 + 2 * lane) =
+          *reinterpret_cast<double2*>(red + (((kh - 1) * MT + mt) * NT + nt) * 64 + 2 * lane) =
               make_double2(acc[0][nt][0], acc[0][nt][1]);
       }
       named_sync(2, 32 * CONW);
@@ -398,9 +401,15 @@ __global__ void __launch_bounds__(PTH, 1)
         double v[NT][2];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          const double2 pv = *reinterpret_cast<const double2*>(red + (mt * NT + nt) * 64 + 2 * lane);
-          v[nt][0] = acc[0][nt][0] + pv.x;
-          v[nt][1] = acc[0][nt][1] + pv.y;
+          v[nt][0] = acc[0][nt][0];
+          v[nt][1] = acc[0][nt][1];
+#pragma unroll
+          for (int p = 1; p < KSPLIT; ++p) {
+            const double2 pv = *reinterpret_cast<const double2*>(
+                red + (((p - 1) * MT + mt) * NT + nt) * 64 + 2 * lane);
+            v[nt][0] += pv.x;
+            v[nt][1] += pv.y;
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&pb->fempty[b]);
@@ -439,9 +448,29 @@ __global__ void bcat_kernel(const double* M, int kM, const double* S0, int kS, i
   }
 }
 
+template <int NA, int RB, bool PRE, int KC>
+bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_t st) {
+  const Geom& g = a.geo;
+  const int ra = a.U0.p ? a.U0.cols : 0;
+  const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
+  const Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
+  const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (size_t)K4 * RB) * sizeof(double) +
+                       sizeof(PipeBars);
+  const int nstg = stages_for(fixed, S.total);
+  if (nstg < 2) return false;
+  const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
+  allow_max_smem(kstage_kernel<NA, RB, PRE, KC>);
+  const int nchunks = (g.n + KC - 1) / KC;
+  int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC>, PTH, smem);
+  if (grid > nchunks) grid = nchunks;
+  kstage_kernel<NA, RB, PRE, KC><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S,
+                                                           nstg, a.inv_s, a.out_scaled ? 1 : 0);
+  launched();
+  return true;
+}
+
 template <int NA, int RB, bool PRE>
 void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
-  const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
   const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
   if (PRE && ra > 0 && !sepc) fail(PND_ECONFIG, "kstage: scaled input needs separate base rows");
@@ -450,19 +479,10 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   double* B = bcat.get((size_t)K4 * RB);
   bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.S0, ra, a.out.cols, K4, RB, B);
   launched();
-  const Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
-  const size_t fixed =
-      (2 * (size_t)K4 * KCS + (size_t)K4 * RB) * sizeof(double) + sizeof(PipeBars);
-  const int nstg = stages_for(fixed, S.total);
-  if (nstg < 2) fail(PND_ECONFIG, "kstage tile exceeds shared memory");
-  const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  allow_max_smem(kstage_kernel<NA, RB, PRE>);
-  const int nchunks = (g.n + KC - 1) / KC;
-  int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE>, PTH, smem);
-  if (grid > nchunks) grid = nchunks;
-  kstage_kernel<NA, RB, PRE><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S, nstg,
-                                                       a.inv_s, a.out_scaled ? 1 : 0);
-  launched();
+  // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks)
+  if (kstage_try<NA, RB, PRE, 32>(a, B, K, K4, st)) return;
+  if (kstage_try<NA, RB, PRE, 16>(a, B, K, K4, st)) return;
+  fail(PND_ECONFIG, "kstage tile exceeds shared memory");
 }
 
 template <int NA, int RB>
@@ -687,8 +707,8 @@ void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, D
     case 4: sgram_launch<NA, 4, 16>(g, X1, X2, isp, out, partial, st); break;
     case 5: sgram_launch<NA, 5, 16>(g, X1, X2, isp, out, partial, st); break;
     case 6: sgram_launch<NA, 6, 16>(g, X1, X2, isp, out, partial, st); break;
-    case 7:
-    case 8: sgram_launch<NA, 8, 16>(g, X1, X2, isp, out, partial, st); break;
+    case 7: sgram_launch<NA, 7, 8>(g, X1, X2, isp, out, partial, st); break;
+    case 8: sgram_launch<NA, 8, 8>(g, X1, X2, isp, out, partial, st); break;
     default: fail(PND_ECONFIG, "stencil Grams support at most 64 columns");
   }
 }

@@ -315,3 +315,34 @@ def test_end_to_end_dose(tag):
     dev_coll = rel(dep - unc, g["deposited"] - unc)
     assert dev_total <= max(10.0 * floor["total"], 1e-12), (dev_total, floor)
     assert dev_coll <= max(10.0 * floor["collided"], 1e-10), (dev_coll, floor)
+
+
+# ------------------------------------------------------------------ larger ranks
+@pytest.mark.parametrize("r", [24, 30, 32])
+def test_streaming_step_large_rank_vs_oracle(dl, r):
+    """Ranks above the bench's 20 (16-cell K-stage chunks, 8-cell Gram chunks):
+    a streaming step + truncation against the numpy oracle (pinned to the
+    reference by test_oracle.py), T2 tolerances."""
+    from oracle import dlra_np
+    from paper_2508_04484_b200.angular import PNOperators
+
+    ops = PNOperators.build(7)
+    nx, ny, nz = 10, 9, 11
+    n, m = nx * ny * nz, ops.size
+    rng = np.random.default_rng(r)
+    inv_s = 1.0 / rng.uniform(5.0, 12.0, n)
+    u0 = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    v0 = np.linalg.qr(rng.standard_normal((m, r)))[0]
+    s0 = np.diag(np.logspace(0, -4, r)) + 1e-3 * rng.standard_normal((r, r))
+    grid = SimpleNamespace(nx=nx, ny=ny, nz=nz, dx=0.1, dy=0.12, dz=0.09)
+    ctx = dl.StreamingContext(inv_s, SimpleNamespace(grid=grid), ops)
+    aug = dl.streaming_step(dl.LowRankState(u0, s0, v0), 0.01, ctx)
+    ou, os_, ov = dlra_np.streaming_step(u0, s0, v0, 0.01, inv_s,
+                                         dlra_np.Grid(nx, ny, nz, 0.1, 0.12, 0.09),
+                                         dlra_np.Ops(ops.eig_v, ops.lam_plus, ops.lam_minus))
+    want = ou @ os_ @ ov.T
+    assert aug.orthonormality_defect() < 1e-12
+    assert rel(aug.matrix(), want) < 1e-11
+    tr, _ = dl.truncate(aug, dl.TruncationPolicy(1e300, r, r))
+    _, ts, _, _ = dlra_np.truncate(ou, os_, ov, 1e300, r, r)
+    np.testing.assert_allclose(np.diag(tr.s), np.diag(ts), rtol=1e-9)
