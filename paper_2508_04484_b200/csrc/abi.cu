@@ -828,7 +828,11 @@ int pnd_set_slab(pnd_handle* hh, int z0, int nz_global, const char* id128, int r
     g.ns = 2 * g.na;
     pnd::comm_destroy(h.comm);
     h.comm = nullptr;
-    if (world > 1) h.comm = pnd::comm_create(id128, rank, world);
+    bool have_id = false;
+    for (int i = 0; id128 && i < 128 && !have_id; ++i) have_id = id128[i] != 0;
+    // a communicator whenever an id is given (world 1 included: exercises the
+    // transport's setup on a single GPU; its exchanges are no-ops there)
+    if (have_id) h.comm = pnd::comm_create(id128, rank, world);
     g.comm = h.comm;
   });
 }

@@ -55,3 +55,18 @@ def test_slab_solve_matches_single_device(tag, world):
         assert p.diagnostics["max_orthonormality_defect"] < 1e-10
     ref = full.dose.deposited
     assert np.linalg.norm(dep - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_nccl_world_of_one():
+    """The NCCL transport's setup on one GPU: dlopen, unique id, a one-rank
+    communicator; the solve is unchanged (exchanges are no-ops at world 1)."""
+    from paper_2508_04484_b200 import _lib, slabs
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_smoke.npz")
+    cid = _lib.comm_unique_id()
+    assert len(cid) == 128 and any(cid)
+    full = run_bundle(b, max_steps=4)
+    one = run_bundle(b, max_steps=4, slab=slabs.plan(*b.shape, 1, 0), comm_id=cid)
+    np.testing.assert_array_equal(one.dose.deposited, full.dose.deposited)
