@@ -1,3 +1,4 @@
+#include <atomic>
 #include <vector>
 // extern "C" boundary (include/pndose_b200.h): argument checks, host<->device
 // staging, error mapping. Every exception raised inside the library becomes
@@ -51,7 +52,7 @@ void IBuf::free_() {
   cap = 0;
 }
 
-static long long g_launches = 0;
+static std::atomic<long long> g_launches{0};  // kernel launches (bench gpu_launches)
 
 void launched() {
   CK(cudaGetLastError());
@@ -232,7 +233,7 @@ int pnd_destroy(pnd_handle* hh) {
   Handle& h = hh->h;
   cudaSetDevice(h.device);
   if (h.st) cudaStreamSynchronize(h.st);
-  pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.cls_val,
+  pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.cls_val, &h.bcat,
                        &h.gdiag, &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V,
                        &h.part, &h.dep, &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.rbuf,
                        &h.tq_m.cbuf};
@@ -513,6 +514,7 @@ int pnd_apply_streaming(pnd_handle* hh, const double* u, double* out) {
     pnd::axpby(ns * m * m, -1.0, h.amat.p, 0.0, M, h.st);
     NMat O = h.W2.view(h.g, m, h.st);
     pnd::KStageArgs a{};
+    a.bcat = &h.bcat;
     a.geo = h.g;
     a.X = X;
     a.M = M;
@@ -556,6 +558,7 @@ int pnd_k_rhs(pnd_handle* hh, const double* k, int r, const double* f, double* o
     pnd::axpby(ns * r * r, -1.0, M, 0.0, M, h.st);
     NMat O = h.W2.view(h.g, r, h.st);
     pnd::KStageArgs a{};
+    a.bcat = &h.bcat;
     a.geo = h.g;
     a.X = K;
     a.M = M;

@@ -57,6 +57,7 @@ struct Handle {
 
   // workspaces
   DBuf part;                  // gram partials
+  DBuf bcat;                  // K-stage [M; S0] (stream-ordered reuse within this handle)
   TsqrWork tq_m;
   DBuf sm[48];                // small / m-side scratch (see step.cu Slot)
   IBuf iflag;

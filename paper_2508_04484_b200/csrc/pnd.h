@@ -130,6 +130,7 @@ struct KStageArgs {
   const double* M;    // ns x xc x r row-major contraction matrices
   const double* inv_s;
   NMat out;           // r = out.cols
+  DBuf* bcat = nullptr;     // per-handle scratch for the fragment-ordered [M; S0]
   bool in_scaled = false;   // X holds S^-1 x (the Horner intermediates)
   bool out_scaled = false;  // store S^-1 out instead of out
 };

@@ -713,17 +713,17 @@ void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, D
   }
 }
 
-DBuf g_bcat;  // concatenated [M; S0] of the current kstage launch (stream-ordered reuse)
 
 }  // namespace
 
 void kstage(const KStageArgs& a, cudaStream_t st) {
+  if (!a.bcat) fail(PND_ECONFIG, "kstage: no [M; S0] scratch buffer");
   if (a.X.cols > 32 || (a.U0.p && a.U0.cols > 32))
     fail(PND_ECONFIG, "kstage supports <= 32 input columns");
   switch (a.geo.na) {
-    case 1: kstage_na<1>(a, g_bcat, st); break;
-    case 2: kstage_na<2>(a, g_bcat, st); break;
-    case 3: kstage_na<3>(a, g_bcat, st); break;
+    case 1: kstage_na<1>(a, *a.bcat, st); break;
+    case 2: kstage_na<2>(a, *a.bcat, st); break;
+    case 3: kstage_na<3>(a, *a.bcat, st); break;
     default: fail(PND_ECONFIG, "grid has no active axis");
   }
 }

@@ -243,6 +243,7 @@ void streaming_step(Handle& h, double dt) {
   const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
   for (int stage = 0; stage < 4; ++stage) {
     KStageArgs ka{};
+    ka.bcat = &h.bcat;
     ka.geo = g;
     ka.inv_s = isp;
     ka.U0 = stage == 3 ? NMat{} : U0;  // the last stage returns dK = h L(W2) only
