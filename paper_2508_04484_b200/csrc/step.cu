@@ -31,7 +31,7 @@ namespace pnd {
 namespace {
 
 enum Slot {
-  S_FV, S_MST, S_YST, S_QT, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
+  S_FV, S_MST, S_YST, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
   S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
   S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_VNEW, S_M2,
   S_C1, S_OG, S_OTA, S_OTB, S_EYE, S_PC, S_TAZ, S_COUNT
@@ -271,22 +271,35 @@ void streaming_step(Handle& h, double dt) {
   }
   const NMat dK = W2;
 
-  // --- L phase: L' = -sum_s A_s L Q_s, Q_s = (D_s S^-1 U0)^T U0, L0 = V0 S0^T
-  double* QT = slot(h, S_QT, (size_t)ns * a * a);
-  phase(h, PH_LGRAM);
-  stencil_grams(g, U0, NMat{}, isp, QT, h.part, st);  // QT_s = U0^T D_s U0 = Q_s^T
   double* C1 = slot(h, S_C1, (size_t)a * b);
+  phase(h, PH_LGRAM);
   gram_xy(g, U0, dK, C1, h.part, st);  // C1 = U0^T dK
+
+  // --- U augmentation: U^ = [U0 | orth((I - U0 U0^T) dK)]
+  phase(h, PH_ORTH);
+  const int k = orth_complement(h, dK, C1);
+  const int ru = a + k;
+
+  // --- S-phase Grams G_s = U^T D_s S^-1 U^ (dlra.py:199-209). Their leading
+  // a x a block is the L phase's U0^T D_s S^-1 U0 = Q_s^T (dlra.py:183-184):
+  // same factor, same 1/S, so the L phase reads it there instead of a
+  // separate pass over n (the L phase does not depend on the augmentation).
+  double* G = slot(h, S_G, (size_t)ns * ru * ru);
+  phase(h, PH_SGRAM);
+  if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
+  stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
+
+  // --- L phase: L' = -sum_s A_s L Q_s, Q_s^T = G_s[:a, :a], L0 = V0 S0^T
   phase(h, PH_LSIDE);
+  const int cols = a + b;
   double* L0 = slot(h, S_L0, (size_t)m * a);
   double* LW = slot(h, S_LW, (size_t)m * a);
   double* Z = slot(h, S_ZST, (size_t)ns * m * a);
   gemm(m, a, b, 1.0, rowm(h.V.p, b), 0, tr(rowm(h.S.p, b)), 0, 0.0, rowm(L0, a), 0, 1, st);
   CK(cudaMemcpyAsync(LW, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
-  const int cols = a + b;
   double* BV = slot(h, S_BV, (size_t)m * cols);
   for (int stage = 0; stage < 4; ++stage) {
-    gemm(m, a, a, 1.0, rowm(LW, a), 0, tr(rowm(QT, a)), (long)a * a, 0.0, rowm(Z, a),
+    gemm(m, a, a, 1.0, rowm(LW, a), 0, tr(rowm(G, ru)), (long)ru * ru, 0.0, rowm(Z, a),
          (long)m * a, ns, st);
     double* dst = stage == 3 ? slot(h, S_M2, (size_t)m * a) : LW;
     CK(cudaMemcpyAsync(dst, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
@@ -297,10 +310,7 @@ void streaming_step(Handle& h, double dt) {
   }
   transpose_in(h.V.p, m, b, BV + (size_t)a * m, m, st);
 
-  // --- augmentation: U^ = [U0 | orth((I - U0 U0^T) dK)], V^ = orth([L1, V0])
-  phase(h, PH_ORTH);
-  const int k = orth_complement(h, dK, C1);
-  const int ru = a + k;
+  // --- V augmentation: V^ = orth([L1, V0])
   double* Vhc = slot(h, S_VHC, (size_t)m * cols);
   double* Rv = slot(h, S_RV, (size_t)cols * cols);
   phase(h, PH_TSQR_M);
@@ -315,12 +325,7 @@ void streaming_step(Handle& h, double dt) {
     launched();
   }
 
-  // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams
-  double* G = slot(h, S_G, (size_t)ns * ru * ru);
-  phase(h, PH_SGRAM);
-  if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
-  stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
-  phase(h, PH_SRK4);
+  // --- S phase: S' = -sum_s (U^T D_s S^-1 U^) S F_s(V^), precontracted Grams G
   double* Vhr = slot(h, S_VHR, (size_t)m * rv);
   transpose_out(Vhc, m, m, rv, Vhr, st);
   double* Fh = slot(h, S_FH, (size_t)ns * rv * rv);

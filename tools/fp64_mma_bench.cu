@@ -129,7 +129,21 @@ int main() {
     run("dfma ilp8", kdfma<8>, 8 * 64.0, w, d);
   }
   // one warp per SM sub-partition (4 warps per SM) vs two
+  run("m8n8k4 ilp1 1w/SMSP", k884<1>, 1 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp2 1w/SMSP", k884<2>, 2 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp3 1w/SMSP", k884<3>, 3 * 512.0, 4, d, 1);
   run("m8n8k4 ilp4 1w/SMSP", k884<4>, 4 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp6 1w/SMSP", k884<6>, 6 * 512.0, 4, d, 1);
+  run("m8n8k4 ilp1 2w/SMSP", k884<1>, 1 * 512.0, 8, d, 1);
+  run("m8n8k4 ilp2 2w/SMSP", k884<2>, 2 * 512.0, 8, d, 1);
+  run("m8n8k4 ilp3 2w/SMSP", k884<3>, 3 * 512.0, 8, d, 1);
+  run("m16n8k4 ilp1 1w/SMSP", k1684<1>, 1 * 1024.0, 4, d, 1);
+  run("m16n8k4 ilp2 1w/SMSP", k1684<2>, 2 * 1024.0, 4, d, 1);
+  run("m16n8k8 ilp1 1w/SMSP", k1688<1>, 1 * 2048.0, 4, d, 1);
+  run("m16n8k8 ilp2 1w/SMSP", k1688<2>, 2 * 2048.0, 4, d, 1);
+  run("m16n8k16 ilp1 1w/SMSP", k16816<1>, 1 * 4096.0, 4, d, 1);
+  run("m16n8k16 ilp2 1w/SMSP", k16816<2>, 2 * 4096.0, 4, d, 1);
+  run("m16n8k16 ilp1 2w/SMSP", k16816<1>, 1 * 4096.0, 8, d, 1);
   run("m8n8k4 ilp8 1w/SMSP", k884<8>, 8 * 512.0, 4, d, 1);
   run("m8n8k4 ilp12 1w/SMSP", k884<12>, 12 * 512.0, 4, d, 1);
   run("m8n8k4 ilp4 2w/SMSP", k884<4>, 4 * 512.0, 8, d, 1);
