@@ -355,6 +355,8 @@ def main():
     ap.add_argument("--cpu-sample", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config1", action="store_true",
+                    help="skip the config-1 per-beam dose timing (profiling runs)")
     args = ap.parse_args()
     if args.cpu_sample:
         return cpu_sample_main(args)
@@ -496,7 +498,7 @@ def main():
         except Exception as exc:  # noqa: BLE001
             cpu_baseline = {"error": str(exc)[:300]}
     per_beam = None
-    if world == 1:
+    if world == 1 and not args.no_config1:
         try:
             per_beam = config1_dose_time(with_cpu=not args.no_cpu_baseline)
         except Exception as exc:  # noqa: BLE001

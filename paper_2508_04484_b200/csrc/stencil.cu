@@ -218,8 +218,11 @@ int resident(Kern k, int threads, size_t smem) {
 constexpr int FORMW = 8;             // former warps
 constexpr int CONW = 8;              // kstage contraction warps (m-tile x k-half)
 constexpr int PTH = 32 * (FORMW + CONW + 1);
-constexpr int GCONW = 7;             // sgram contraction warps (16 warps in all)
-constexpr int GPTH = 32 * (FORMW + GCONW + 1);
+// sgram contraction warps: 8 (two per SM sub-partition, so the DMMA work is
+// even across the four) while the accumulators fit the 120-register cap of
+// 17 warps; 7 for the widest tiles
+__host__ __device__ constexpr int gconw(int t8) { return t8 <= 5 ? 8 : 7; }
+__host__ __device__ constexpr int gpth(int t8) { return 32 * (FORMW + gconw(t8) + 1); }
 constexpr int NSTG_MAX = 4;
 
 struct PipeBars {
@@ -510,12 +513,13 @@ void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
 // accumulator per tile (T8 UPW independent chains); launches cover column-tile
 // ranges of at most 32 tiles.
 template <int NA, int T8, int GC>
-__global__ void __launch_bounds__(GPTH, 1)
+__global__ void __launch_bounds__(gpth(T8), 1)
     sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, int nstg, const double* __restrict__ isp,
                  int bt0, int nbt, double* __restrict__ partial, int dbg) {
   constexpr int NS = 2 * NA;
   constexpr int W = T8 * 8;
   constexpr int XS = pad4(W);
+  constexpr int GCONW = gconw(T8), GPTH = gpth(T8);
   constexpr int GTL = pad4(GC);       // feature tile row length (k = cell)
   constexpr int CG = GC / 4;          // groups of 4 cells: 4 or 8
   constexpr int JS = 8 * (8 / CG);    // column stride of one former lane
@@ -678,7 +682,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
   allow_max_smem(sgram_kernel<NA, T8, GC>);
   const int nchunks = (g.n + GC - 1) / GC;
-  int grid = sm_count() * resident(sgram_kernel<NA, T8, GC>, GPTH, smem);
+  int grid = sm_count() * resident(sgram_kernel<NA, T8, GC>, gpth(T8), smem);
   if (grid > nchunks) grid = nchunks;
   const int w = X1.cols + (X2.p ? X2.cols : 0);
   const size_t count = (size_t)2 * NA * w * w;
@@ -687,7 +691,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   for (int bt0 = 0; bt0 < nb; bt0 += 32) {
     const int nbt = nb - bt0 < 32 ? nb - bt0 : 32;
         static const int dbg = getenv("PND_SGRAM_DEBUG") ? atoi(getenv("PND_SGRAM_DEBUG")) : 0;
-    sgram_kernel<NA, T8, GC><<<grid, GPTH, smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part,
+    sgram_kernel<NA, T8, GC><<<grid, gpth(T8), smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part,
                                                         dbg);
     launched();
   }
