@@ -166,37 +166,51 @@ struct Ctx {
     for (int p = 0; p < NP; ++p) xr[p] = X + row_of(p, i) * rs + col0;
   }
 
+  // The 1/(2h) of the second-order upwind differences is folded into the
+  // operand each stencil is contracted with (bcat_kernel: M_s; reduce_parts:
+  // G_s), so a feature costs 2 FP64 ops (+ one shared 3 x centre): the
+  // formers share the FP64 pipe with the contraction warps' DMMAs. The
+  // first-order boundary closures (1/h = 2 x 1/(2h)) carry the exact factor 2.
   template <bool FAST>
   __device__ __forceinline__ void apply(const Geom& g, int off, double* t) const {
     // PRE: the staged rows already hold S^-1 x
     const double fc = PRE ? xr[0][off] : xr[0][off] * is[0];
+    const double c3 = 3.0 * fc;
 #pragma unroll
     for (int ai = 0; ai < NA; ++ai) {
       const double f0 = PRE ? xr[1 + 4 * ai][off] : xr[1 + 4 * ai][off] * is[1 + 4 * ai];
       const double f1 = PRE ? xr[2 + 4 * ai][off] : xr[2 + 4 * ai][off] * is[2 + 4 * ai];
       const double f3 = PRE ? xr[3 + 4 * ai][off] : xr[3 + 4 * ai][off] * is[3 + 4 * ai];
       const double f4 = PRE ? xr[4 + 4 * ai][off] : xr[4 + 4 * ai][off] * is[4 + 4 * ai];
-      const int axis = g.axis[ai];
-      const double ih = axis == 0 ? g.ih[0] : axis == 1 ? g.ih[1] : g.ih[2];
-      const double i2h = axis == 0 ? g.i2h[0] : axis == 1 ? g.i2h[1] : g.i2h[2];
       double tp, tm;
       if (FAST) {
-        tp = (3.0 * fc - 4.0 * f1 + f0) * i2h;
-        tm = (-3.0 * fc + 4.0 * f3 - f4) * i2h;
+        tp = fma(-4.0, f1, c3) + f0;
+        tm = fma(4.0, f3, -c3) - f4;
       } else {
         const int id = idx[ai], ln = len[ai];
-        if (id >= 2) tp = (3.0 * fc - 4.0 * f1 + f0) * i2h;
-        else if (id == 1) tp = (fc - f1) * ih;
-        else tp = fc * ih;
-        if (id <= ln - 3) tm = (-3.0 * fc + 4.0 * f3 - f4) * i2h;
-        else if (id == ln - 2) tm = (f3 - fc) * ih;
-        else tm = -fc * ih;
+        if (id >= 2) tp = fma(-4.0, f1, c3) + f0;
+        else if (id == 1) tp = 2.0 * (fc - f1);
+        else tp = 2.0 * fc;
+        if (id <= ln - 3) tm = fma(4.0, f3, -c3) - f4;
+        else if (id == ln - 2) tm = 2.0 * (f3 - fc);
+        else tm = -2.0 * fc;
       }
       t[2 * ai] = tp;
       t[2 * ai + 1] = tm;
     }
   }
 };
+
+// 1/(2h) of the axis of each stencil s (= 2 ai + {0: D+, 1: D-})
+struct StScale {
+  double v[6];
+};
+
+StScale stencil_scale(const Geom& g) {
+  StScale sc{};
+  for (int s = 0; s < 2 * g.na && s < 6; ++s) sc.v[s] = g.i2h[g.axis[s / 2]];
+  return sc;
+}
 
 template <class Kern>
 int resident(Kern k, int threads, size_t smem) {
@@ -438,13 +452,13 @@ __global__ void __launch_bounds__(PTH, 1)
   }
 }
 
-__global__ void bcat_kernel(const double* M, int kM, const double* S0, int kS, int r, int K4,
-                            int RB, double* B) {
+__global__ void bcat_kernel(const double* M, int kM, int xc, StScale sc, const double* S0, int kS,
+                            int r, int K4, int RB, double* B) {
   for (int i = threadIdx.x + blockIdx.x * blockDim.x; i < K4 * RB; i += blockDim.x * gridDim.x) {
     const int k = i / RB, n = i % RB;
     double v = 0.0;
     if (n < r) {
-      if (k < kM) v = M[(size_t)k * r + n];
+      if (k < kM) v = M[(size_t)k * r + n] * sc.v[k / xc];  // 1/(2h) of stencil k / xc
       else if (k < kM + kS) v = S0[(size_t)(k - kM) * r + n];
     }
     B[i] = v;
@@ -480,7 +494,8 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   const int K = 2 * NA * a.X.cols + ra;
   const int K4 = (K + 15) / 16 * 16;  // whole groups of four k-steps
   double* B = bcat.get((size_t)K4 * RB);
-  bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.S0, ra, a.out.cols, K4, RB, B);
+  bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.X.cols, stencil_scale(a.geo), a.S0,
+                                  ra, a.out.cols, K4, RB, B);
   launched();
   // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks)
   if (kstage_try<NA, RB, PRE, 32>(a, B, K, K4, st)) return;
@@ -659,13 +674,15 @@ __global__ void __launch_bounds__(gpth(T8), 1)
   }
 }
 
-__global__ void reduce_parts(const double* __restrict__ partial, int nblk, int count,
-                             double* __restrict__ out) {
+// sums the per-CTA Gram partials in a fixed order and applies the stencil's
+// 1/(2h) (count = ns * per)
+__global__ void reduce_parts(const double* __restrict__ partial, int nblk, int count, int per,
+                             StScale sc, double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double s = 0.0;
   for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
-  out[i] = s;
+  out[i] = s * sc.v[i / per];
 }
 
 template <int NA, int T8, int GC>
@@ -695,7 +712,8 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
                                                         dbg);
     launched();
   }
-  reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, out);
+  reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, w * w,
+                                                           stencil_scale(g), out);
   launched();
   comm_allreduce(g, out, count, st);
 }
