@@ -239,6 +239,197 @@ __global__ void __launch_bounds__(LTH, 2)
   }
 }
 
+// Per-warp Gram variant (out tiles up to 32 columns): warp w's Gram work is
+// its own 8 cells of the chunk -- X^T out and out^T out over those cells, all
+// tiles, 2 k-steps each (every tile an independent DMMA chain) -- so no
+// CTA-wide barrier per chunk: the out tile goes through a private shared
+// tile (only __syncwarp), and in Gram-only mode the staged Y rows are the B
+// operand directly. The out^T out A and B fragments are the same loads. Each
+// warp writes its own partial; lreduce sums grid x 8 partials in fixed order.
+template <int NB8>
+__global__ void __launch_bounds__(LTH, 2)
+    lincomb_pw_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
+                      int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
+                      double* __restrict__ partial) {
+  constexpr int TS = lpad4(NB8 * 8);            // out tile row length
+  constexpr int NTT = NB8 * (NB8 + 1) / 2;      // upper-triangle out^T out tiles
+  extern __shared__ __align__(128) double sm[];
+  double* const sB = sm + nstg * in.stage;      // [ks][NB8][32] fragment order
+  double* const sT = sB + in.ks * NB8 * 32;     // per warp [8][TS]
+  LBars* bars = reinterpret_cast<LBars*>(sT + LCW * 8 * TS);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
+  const int XT = (xcn + 7) / 8;
+  if (tid == 0) {
+    for (int b = 0; b < nstg; ++b) {
+      mbar_init(&bars->sfull[b], 1);
+      mbar_init(&bars->sempty[b], LCW);
+    }
+    mbar_fence_init();
+  }
+  for (int s = 0; s < nstg; ++s)
+    for (int q = 0; q < in.nin; ++q)
+      for (int i = tid; i < LZPAD; i += LTH)
+        sm[s * in.stage + in.off[q] + LCH * in.rs[q] + i] = 0.0;
+  for (int i = tid; i < in.ks * NB8 * 32; i += LTH) {
+    const int l = i & 31, f = i >> 5, ks = f / NB8, nt = f - ks * NB8;
+    int q = 0;
+    while (q + 1 < in.nin && ks >= in.ks0[q + 1]) ++q;
+    const int j = 4 * (ks - in.ks0[q]) + (l & 3), col = nt * 8 + (l >> 2);
+    double v = 0.0;
+    if (j < in.cols[q] && col < nb && !copy_y) {
+      if (q == in.xq) v = -TB[(size_t)j * nb + col];
+      else v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
+    }
+    sB[i] = v;
+  }
+  for (int i = tid; i < LCW * 8 * TS; i += LTH) sT[i] = 0.0;
+  __syncthreads();
+  const int nchunks = (n + LCH - 1) / LCH;
+
+  if (warp == LCW) {  // producer
+    if (lane == 0) {
+      Ring r(nstg);
+      for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+        if (r.k) mbar_wait_sleep(&bars->sempty[r.s], (r.k - 1) & 1);
+        mbar_expect_tx(&bars->sfull[r.s], in.bytes);
+        const long c0 = (long)chunk * LCH;
+        for (int q = 0; q < in.nin; ++q)
+          bulk_load(sm + r.s * in.stage + in.off[q], in.p[q] + c0 * in.rs[q],
+                    LCH * in.rs[q] * 8, &bars->sfull[r.s]);
+        if (in.w) bulk_load(sm + r.s * in.stage + in.woff, in.w + c0, LCH * 8, &bars->sfull[r.s]);
+      }
+    }
+    return;
+  }
+
+  const int m = lane >> 2, kq = lane & 3;
+  double gx[NB8][NB8][2], gt[NTT][2];
+#pragma unroll
+  for (int ti = 0; ti < NB8; ++ti)
+#pragma unroll
+    for (int tj = 0; tj < NB8; ++tj) gx[ti][tj][0] = gx[ti][tj][1] = 0.0;
+#pragma unroll
+  for (int t = 0; t < NTT; ++t) gt[t][0] = gt[t][1] = 0.0;
+  double* const T = sT + warp * 8 * TS;
+  const int rsx = in.xq >= 0 ? in.rs[in.xq] : 0;
+  Ring r(nstg);
+  for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+    const long c0 = (long)chunk * LCH;
+    const long w0 = c0 + warp * 8;  // this warp's first cell
+    mbar_wait(&bars->sfull[r.s], r.k & 1);
+    const double* sb = sm + r.s * in.stage;
+    const double* sy;
+    int rsy;
+    if (copy_y) {
+      sy = sb + in.off[0] + warp * 8 * in.rs[0];
+      rsy = in.rs[0];
+    } else {
+      // ---- out tile: m-tile `warp`, all n-tiles (NB8 independent chains)
+      double acc[NB8][2];
+#pragma unroll
+      for (int nt = 0; nt < NB8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      for (int q = 0; q < in.nin; ++q) {
+        const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
+        const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
+#pragma unroll 2
+        for (int ks = k0; ks < k1; ++ks) {
+          const double a0 = pa[4 * (ks - k0)];
+#pragma unroll
+          for (int nt = 0; nt < NB8; ++nt)
+            dmma884(acc[nt][0], acc[nt][1], a0, sB[(ks * NB8 + nt) * 32 + lane]);
+        }
+      }
+      const long row = w0 + m;
+#pragma unroll
+      for (int nt = 0; nt < NB8; ++nt) {
+        const double v0 = acc[nt][0], v1 = acc[nt][1];
+        const int col = nt * 8 + 2 * kq;
+        // rows past n (halo rows, possibly a neighbour slab's) stay out of the Grams
+        *reinterpret_cast<double2*>(T + m * TS + col) =
+            row < n ? make_double2(v0, v1) : make_double2(0.0, 0.0);
+        if (out.p && row < n) {
+          double* o = out.p + row * out.rs + col;
+          if (col + 1 < out.rs) *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+          else if (col < out.rs) o[0] = v0;
+        }
+      }
+      __syncwarp();
+      sy = T;
+      rsy = TS;
+    }
+    if (grams) {
+      const double* sx = in.xq >= 0 ? sb + in.off[in.xq] + warp * 8 * rsx : nullptr;
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int cl = 4 * s + kq;  // k index = this lane's cell
+        double bf[NB8];
+        if (copy_y) {
+          // Gram-only: B = diag(w) Y; rows past n contribute nothing
+          const bool live = w0 + cl < n;
+          const double wv = in.w ? sb[in.woff + warp * 8 + cl] : 1.0;
+#pragma unroll
+          for (int tj = 0; tj < NB8; ++tj)
+            bf[tj] = live ? wv * sy[cl * rsy + tj * 8 + m] : 0.0;
+        } else {
+#pragma unroll
+          for (int tj = 0; tj < NB8; ++tj) bf[tj] = sy[cl * rsy + tj * 8 + m];
+        }
+#pragma unroll
+        for (int ti = 0; ti < NB8; ++ti) {
+          if (ti < XT) {
+            const double a = sx[cl * rsx + ti * 8 + m];
+#pragma unroll
+            for (int tj = 0; tj < NB8; ++tj) dmma884(gx[ti][tj][0], gx[ti][tj][1], a, bf[tj]);
+          }
+        }
+        if (!skip_tt) {
+          // out^T out: the A fragment of row tile ti is the B fragment of tile ti
+#pragma unroll
+          for (int ti = 0, t = 0; ti < NB8; ++ti)
+#pragma unroll
+            for (int tj = ti; tj < NB8; ++tj, ++t) dmma884(gt[t][0], gt[t][1], bf[ti], bf[tj]);
+        }
+      }
+    }
+    warp_arrive(&bars->sempty[r.s]);
+  }
+  if (grams) {
+    const size_t count = (size_t)(xcn + (skip_tt ? 0 : nb)) * nb;
+    double* o = partial + ((size_t)blockIdx.x * LCW + warp) * count;
+    const int col = 2 * kq;
+#pragma unroll
+    for (int ti = 0; ti < NB8; ++ti) {
+      const int rrow = ti * 8 + m;
+#pragma unroll
+      for (int tj = 0; tj < NB8; ++tj) {
+        const int c = tj * 8 + col;
+        if (ti < XT && rrow < xcn) {
+          if (c < nb) o[(size_t)rrow * nb + c] = gx[ti][tj][0];
+          if (c + 1 < nb) o[(size_t)rrow * nb + c + 1] = gx[ti][tj][1];
+        }
+      }
+    }
+    if (!skip_tt) {
+      double* ot = o + (size_t)xcn * nb;
+#pragma unroll
+      for (int ti = 0, t = 0; ti < NB8; ++ti)
+#pragma unroll
+        for (int tj = ti; tj < NB8; ++tj, ++t) {
+          const int rrow = ti * 8 + m, c = tj * 8 + col;
+          if (rrow < nb) {
+            if (c < nb) ot[(size_t)rrow * nb + c] = gt[t][0];
+            if (c + 1 < nb) ot[(size_t)rrow * nb + c + 1] = gt[t][1];
+          }
+          if (ti != tj && rrow < nb) {  // mirror the off-diagonal tile
+            if (c < nb) ot[(size_t)c * nb + rrow] = gt[t][0];
+            if (c + 1 < nb) ot[(size_t)(c + 1) * nb + rrow] = gt[t][1];
+          }
+        }
+    }
+  }
+}
+
 __global__ void lreduce(const double* __restrict__ partial, int nblk, int count,
                         double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -280,8 +471,11 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   const int ny = Y1.cols + (Y2.p ? Y2.cols : 0);
   const int nb = out.cols;
   constexpr int TS = lpad4(NB8 * 8);
-  const size_t fixed = ((size_t)ks * NB8 * 32 + 2 * (size_t)LCH * TS) * sizeof(double) +
-                       sizeof(LBars);
+  // per-warp Grams (lincomb_pw_kernel) while the registers allow
+  constexpr bool PWOK = NB8 <= 3;
+  const bool PW = PWOK && gram_only;
+  const size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
+  const size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
   // two CTAs per SM: keep the whole CTA under ~113 KB
   const size_t cap = 113 * 1024;
   int nstg = 0;
@@ -293,22 +487,26 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
       fail(PND_ECONFIG, "lincomb tile exceeds shared memory");
   }
   const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
-  allow_max_smem(lincomb_kernel<NB8>);
+  auto kern = lincomb_kernel<NB8>;
+  if constexpr (PWOK) {
+    if (PW) kern = lincomb_pw_kernel<NB8>;
+  }
+  allow_max_smem(kern);
   int nblk = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, lincomb_kernel<NB8>, LTH, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, kern, LTH, smem));
   if (nblk < 1) nblk = 1;
   const int nchunks = (g.n + LCH - 1) / LCH;
   int grid = sm_count() * nblk;
   if (grid > nchunks) grid = nchunks;
   const int xcn = X.p ? X.cols : 0;
   const size_t count = (size_t)(xcn + (gram_only ? 0 : nb)) * nb;
-  double* part = grams ? partial.get(count * grid) : nullptr;
-  lincomb_kernel<NB8><<<grid, LTH, smem, st>>>(g.n, in, TA, TB, ny, nb, out, nstg,
-                                               grams ? 1 : 0, gram_only ? 1 : 0,
-                                               gram_only ? 1 : 0, part);
+  const int nparts = PW ? grid * LCW : grid;  // per-warp or per-CTA partials
+  double* part = grams ? partial.get(count * nparts) : nullptr;
+  kern<<<grid, LTH, smem, st>>>(g.n, in, TA, TB, ny, nb, out, nstg, grams ? 1 : 0,
+                                gram_only ? 1 : 0, gram_only ? 1 : 0, part);
   launched();
   if (grams) {
-    lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, grams);
+    lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, nparts, (int)count, grams);
     launched();
     comm_allreduce(g, grams, count, st);
   }
