@@ -446,8 +446,11 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   LIn in{};
   const NMat ms[3] = {Y1, Y2, X};
   int o = 0, ks = 0;
+  // Gram-only X^T diag(w) X: the one matrix is staged once and read as both operands
+  const bool same = gram_only && X.p == Y1.p && X.rs == Y1.rs && X.cols == Y1.cols;
   for (int q = 0; q < 3; ++q) {
     if (!ms[q].p || ms[q].cols <= 0) continue;
+    if (q == 2 && same) continue;
     const int i = in.nin++;
     in.p[i] = ms[q].p;
     in.cols[i] = ms[q].cols;
@@ -460,6 +463,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
     in.bytes += LCH * ms[q].rs * 8;
   }
   if (!X.p || X.cols <= 0) in.xq = -1;
+  if (same) in.xq = 0;
   if (weight) {
     in.w = weight;
     in.woff = o;
