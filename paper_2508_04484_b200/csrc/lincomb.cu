@@ -430,13 +430,24 @@ __global__ void __launch_bounds__(LTH, 2)
   }
 }
 
-__global__ void lreduce(const double* __restrict__ partial, int nblk, int count,
-                        double* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= count) return;
+// sums nblk partials of `count` entries: 32 consecutive entries per block
+// (coalesced), 8 fixed strided subsets of the partials per entry, combined in
+// a fixed order (bit-reproducible)
+__global__ void __launch_bounds__(256) lreduce(const double* __restrict__ partial, int nblk,
+                                               int count, double* __restrict__ out) {
+  __shared__ double red[8][33];
+  const int i = blockIdx.x * 32 + threadIdx.x;
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
-  out[i] = s;
+  if (i < count)
+    for (int b = threadIdx.y; b < nblk; b += 8) s += partial[(size_t)b * count + i];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < count) {
+    double t = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) t += red[y][threadIdx.x];
+    out[i] = t;
+  }
 }
 
 template <int NB8>
@@ -510,7 +521,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
                                 gram_only ? 1 : 0, gram_only ? 1 : 0, part);
   launched();
   if (grams) {
-    lreduce<<<(int)((count + 255) / 256), 256, 0, st>>>(part, nparts, (int)count, grams);
+    lreduce<<<(int)((count + 31) / 32), dim3(32, 8), 0, st>>>(part, nparts, (int)count, grams);
     launched();
     comm_allreduce(g, grams, count, st);
   }
