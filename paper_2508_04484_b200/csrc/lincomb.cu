@@ -59,6 +59,7 @@ struct LIn {
   int stage;    // doubles per staging slot
   unsigned bytes;
   int ks;       // total k-steps
+  int ident;        // TA = I: out = Y1 - X TB, Y1 added to the accumulators
   const double* w;  // optional per-cell weight (Gram-only mode: T = diag(w) Y1)
   int woff;         // smem offset of the staged weights
 };
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(LTH, 2)
     double v = 0.0;
     if (j < in.cols[q] && col < nb && !copy_y) {
       if (q == in.xq) v = -TB[(size_t)j * nb + col];
-      else v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
+      else if (!in.ident) v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
     }
     sB[i] = v;
   }
@@ -126,9 +127,9 @@ __global__ void __launch_bounds__(LTH, 2)
 
   const int m = lane >> 2, kq = lane & 3;
   constexpr int GPW_MAX = (NB8 * NB8 + NB8 * (NB8 + 1) / 2 + LCW - 1) / LCW;
-  double gacc[GPW_MAX][2];
+  double gacc[GPW_MAX][2], gacc2[GPW_MAX][2];  // even / odd k-steps: two chains per tile
 #pragma unroll
-  for (int t = 0; t < GPW_MAX; ++t) gacc[t][0] = gacc[t][1] = 0.0;
+  for (int t = 0; t < GPW_MAX; ++t) gacc[t][0] = gacc[t][1] = gacc2[t][0] = gacc2[t][1] = 0.0;
   Ring r(nstg);
   int it = 0;
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next(), ++it) {
@@ -154,7 +155,17 @@ __global__ void __launch_bounds__(LTH, 2)
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int nt = 0; nt < NB8; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
-    for (int q = 0; q < in.nin; ++q) {
+    if (in.ident) {
+      // TA = I: start from the Y1 rows (accumulator layout: row m, columns 2 kq, 2 kq + 1)
+      const double* y = sb + in.off[0] + (warp * 8 + m) * in.rs[0];
+#pragma unroll
+      for (int nt = 0; nt < NB8; ++nt) {
+        const int col = nt * 8 + 2 * kq;
+        if (col < in.cols[0]) acc[0][nt][0] = y[col];
+        if (col + 1 < in.cols[0]) acc[0][nt][1] = y[col + 1];
+      }
+    }
+    for (int q = in.ident ? 1 : 0; q < in.nin; ++q) {
       const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
       const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
       int ks = k0;
@@ -205,8 +216,10 @@ __global__ void __launch_bounds__(LTH, 2)
           const double* pb = T + tj * 8 + m;
           // rows past n: zero staged rows and zero out rows -> no contribution
 #pragma unroll 4
-          for (int k0 = 0; k0 < LCH; k0 += 4)
+          for (int k0 = 0; k0 < LCH; k0 += 8) {
             dmma884(gacc[t][0], gacc[t][1], pa[(k0 + kq) * sa], pb[(k0 + kq) * TS]);
+            dmma884(gacc2[t][0], gacc2[t][1], pa[(k0 + 4 + kq) * sa], pb[(k0 + 4 + kq) * TS]);
+          }
         }
       }
     }
@@ -214,6 +227,11 @@ __global__ void __launch_bounds__(LTH, 2)
   }
   if (grams) {
     double* o = partial + (size_t)blockIdx.x * (xcn + (skip_tt ? 0 : nb)) * nb;
+#pragma unroll
+    for (int t = 0; t < GPW_MAX; ++t) {
+      gacc[t][0] += gacc2[t][0];
+      gacc[t][1] += gacc2[t][1];
+    }
 #pragma unroll
     for (int t = 0; t < GPW_MAX; ++t) {
       const int tile = warp + LCW * t;
@@ -475,6 +493,9 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   }
   if (!X.p || X.cols <= 0) in.xq = -1;
   if (same) in.xq = 0;
+  in.ident = (!gram_only && TA == nullptr) ? 1 : 0;
+  if (in.ident && (Y2.p || Y1.cols != out.cols))
+    fail(PND_ECONFIG, "lincomb: TA = I needs out = Y1 - X TB with matching columns");
   if (weight) {
     in.w = weight;
     in.woff = o;

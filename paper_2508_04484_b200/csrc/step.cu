@@ -180,7 +180,7 @@ int orth_complement(Handle& h, NMat X, const double* C1) {
   double* dinfo = slot(h, S_TAIL, 4);
   // pass 2: Y = X - U0 C1 -> Qa, C2 = U0^T Y, G2 = Y^T Y
   NMat Y = h.Qa.view(g, b, st);
-  lincomb(g, X, NMat{}, U0, eye(h, b), C1, Y, grams, h.part, st);
+  lincomb(g, X, NMat{}, U0, nullptr, C1, Y, grams, h.part, st);
   double* C2 = grams;                  // a x b
   double* G2 = grams + (size_t)a * b;  // b x b
   if (a > 0) gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
