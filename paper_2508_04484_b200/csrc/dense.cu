@@ -210,7 +210,9 @@ __global__ void copy_rfac_kernel(const double* Rn, int ldn, int kc, int cols, do
 }
 
 // ----------------------------------------------------------------- SVD
-__global__ void svd_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
+template <int MT>  // column elements per lane: M <= 32 MT
+__global__ void __launch_bounds__(1024, 1)
+    svd_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
   extern __shared__ double sm[];
   const bool tall = p >= q;
   const int M = tall ? p : q, N = tall ? q : p;
@@ -232,7 +234,18 @@ __global__ void svd_kernel(const double* s, int p, int q, double* P, double* sig
   for (int idx = tid; idx < N2 * N2; idx += nthr) Vm[idx] = (idx % N2 == idx / N2) ? 1.0 : 0.0;
   __syncthreads();
   const int npair = N2 / 2;
+  // Hestenes one-sided Jacobi, round-robin pairs; per pair one warp holds the
+  // two columns in registers (MT per lane), so a rotation costs one
+  // dot product (the column norms are carried: a' = a - t g, b' = b + t g,
+  // recomputed exactly at the start of every sweep)
+  double* nrm = sg;  // column norms^2 during the sweeps (sg is rewritten below)
   for (int sweep = 0; sweep < 60 && N2 > 1; ++sweep) {
+    for (int j = warp; j < N2; j += nw) {
+      double x = 0.0;
+      for (int i = lane; i < M; i += 32) x += A[j * M + i] * A[j * M + i];
+      x = warp_sum(x);
+      if (lane == 0) nrm[j] = x;
+    }
     if (tid == 0) rotated = 0;
     __syncthreads();
     for (int round = 0; round < N2 - 1; ++round) {
@@ -246,31 +259,39 @@ __global__ void svd_kernel(const double* s, int p, int q, double* P, double* sig
           b = (round + N2 - 1 - k) % (N2 - 1);
         }
         if (a > b) { const int t = a; a = b; b = t; }
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < M; i += 32) {
-          const double x = A[a * M + i], y = A[b * M + i];
-          al += x * x;
-          be += y * y;
-          ga += x * y;
+        double xa[MT], yb[MT];
+        double ga = 0.0;
+#pragma unroll
+        for (int t = 0; t < MT; ++t) {
+          const int i = lane + 32 * t;
+          xa[t] = i < M ? A[a * M + i] : 0.0;
+          yb[t] = i < M ? A[b * M + i] : 0.0;
+          ga = fma(xa[t], yb[t], ga);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
         ga = warp_sum(ga);
+        const double al = nrm[a], be = nrm[b];
         if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-          for (int i = lane; i < M; i += 32) {
-            const double x = A[a * M + i], y = A[b * M + i];
-            A[a * M + i] = c * x - sn * y;
-            A[b * M + i] = sn * x + c * y;
+          const double c = rsqrt(1.0 + t * t), sn = c * t;
+#pragma unroll
+          for (int u = 0; u < MT; ++u) {
+            const int i = lane + 32 * u;
+            if (i < M) {
+              A[a * M + i] = c * xa[u] - sn * yb[u];
+              A[b * M + i] = sn * xa[u] + c * yb[u];
+            }
           }
           for (int i = lane; i < N2; i += 32) {
             const double x = Vm[a * N2 + i], y = Vm[b * N2 + i];
             Vm[a * N2 + i] = c * x - sn * y;
             Vm[b * N2 + i] = sn * x + c * y;
           }
-          if (lane == 0) rotated = 1;
+          if (lane == 0) {
+            nrm[a] = al - t * ga;
+            nrm[b] = be + t * ga;
+            rotated = 1;
+          }
         }
       }
       __syncthreads();
@@ -755,12 +776,20 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   const int N2 = N + (N & 1);
   const size_t sm =
       ((size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N + N2) * sizeof(double) + N * sizeof(int);
-  set_smem((const void*)svd_kernel, sm);
   // one warp per Jacobi pair of a round: a round is one shuffle-reduction deep
   int threads = 32 * (N2 / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
-  svd_kernel<<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+  if (M <= 64) {
+    set_smem((const void*)svd_kernel<2>, sm);
+    svd_kernel<2><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+  } else if (M <= 128) {
+    set_smem((const void*)svd_kernel<4>, sm);
+    svd_kernel<4><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+  } else {
+    set_smem((const void*)svd_kernel<8>, sm);
+    svd_kernel<8><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+  }
   launched();
 }
 
