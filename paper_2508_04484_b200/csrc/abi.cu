@@ -347,7 +347,7 @@ int pnd_set_sources(pnd_handle* hh, int n_beams, const double* psi, const double
     if (n_beams < 0 || n_beams > 4) pnd::fail(PND_ECONFIG, "0..4 uncollided sources supported");
     h.n_beams = n_beams;
     if (!n_beams) return;
-    double* d = h.psi.get((size_t)n_beams * h.g.ld);
+    double* d = h.psi.get((size_t)n_beams * h.g.ld + 64);
     for (int b = 0; b < n_beams; ++b) up(d + (size_t)b * h.g.ld, psi + (size_t)b * h.g.n, h.g.n, h.st);
     up(h.tm.get((size_t)n_beams * h.m), t_m, (size_t)n_beams * h.m, h.st);
     CK(cudaStreamSynchronize(h.st));
@@ -363,7 +363,7 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
       h.n_groups = n_groups;
       h.n_beams = n_beams;
       h.flux.get((size_t)n_beams * n_groups * h.g.ld);
-      h.psi.get((size_t)n_beams * h.g.ld);
+      h.psi.get((size_t)n_beams * h.g.ld + 64);
       h.psi_lo.get((size_t)n_beams * h.g.ld);
       h.tm.get((size_t)n_beams * h.m);
     } else if (n_groups != h.n_groups || n_beams != h.n_beams) {
@@ -899,7 +899,7 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
       h.n_groups = n_groups;
       h.n_beams = n_beams;
       h.flux.get((size_t)n_beams * n_groups * h.g.ld);
-      h.psi.get((size_t)n_beams * h.g.ld);
+      h.psi.get((size_t)n_beams * h.g.ld + 64);
       h.psi_lo.get((size_t)n_beams * h.g.ld);
       h.tm.get((size_t)n_beams * h.m);
     }

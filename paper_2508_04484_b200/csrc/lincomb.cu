@@ -141,10 +141,16 @@ __global__ void __launch_bounds__(LTH, 2)
       // Gram-only mode: out = Y1 (no contraction), parked for X^T Y1
       const double* y = sb + in.off[0];
       const double* wv = in.w ? sb + in.woff : nullptr;
+      const int y2 = in.nin > 1 && in.xq != 1 ? 1 : -1;  // second Y input, if any
+      const int c1 = in.cols[0], c2 = y2 >= 0 ? in.cols[y2] : 0;
       for (int e = lane; e < 8 * NB8 * 8; e += 32) {
         const int i = warp * 8 + e / (NB8 * 8), c = e % (NB8 * 8);
         // rows past n are halo rows (possibly a neighbour slab's): no Gram input
-        const double v = c < in.cols[0] && c0 + i < n ? y[i * in.rs[0] + c] : 0.0;
+        double v = 0.0;
+        if (c0 + i < n) {
+          if (c < c1) v = y[i * in.rs[0] + c];
+          else if (c - c1 < c2) v = sb[in.off[y2] + i * in.rs[y2] + c - c1];
+        }
         T[i * TS + c] = wv ? wv[i] * v : v;
       }
       __syncwarp();
@@ -331,6 +337,8 @@ __global__ void __launch_bounds__(LTH, 2)
   for (int t = 0; t < NTT; ++t) gt[t][0] = gt[t][1] = 0.0;
   double* const T = sT + warp * 8 * TS;
   const int rsx = in.xq >= 0 ? in.rs[in.xq] : 0;
+  // Gram-only second Y input: staged at index 1 unless that is X
+  const int y2 = copy_y && in.nin > 1 && in.xq != 1 ? 1 : -1;
   Ring r(nstg);
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
     const long c0 = (long)chunk * LCH;
@@ -383,12 +391,24 @@ __global__ void __launch_bounds__(LTH, 2)
         const int cl = 4 * s + kq;  // k index = this lane's cell
         double bf[NB8];
         if (copy_y) {
-          // Gram-only: B = diag(w) Y; rows past n contribute nothing
+          // Gram-only: B = diag(w) [Y1 | Y2]; rows past n contribute nothing
           const bool live = w0 + cl < n;
           const double wv = in.w ? sb[in.woff + warp * 8 + cl] : 1.0;
+          if (y2 < 0) {
 #pragma unroll
-          for (int tj = 0; tj < NB8; ++tj)
-            bf[tj] = live ? wv * sy[cl * rsy + tj * 8 + m] : 0.0;
+            for (int tj = 0; tj < NB8; ++tj)
+              bf[tj] = live ? wv * sy[cl * rsy + tj * 8 + m] : 0.0;
+          } else {
+            const int c1 = in.cols[0];
+            const double* s2 = sb + in.off[y2] + (warp * 8 + cl) * in.rs[y2];
+#pragma unroll
+            for (int tj = 0; tj < NB8; ++tj) {
+              const int col = tj * 8 + m;
+              const double v = col < c1 ? sy[cl * rsy + col]
+                               : col - c1 < in.cols[y2] ? s2[col - c1] : 0.0;
+              bf[tj] = live ? wv * v : 0.0;
+            }
+          }
         } else {
 #pragma unroll
           for (int tj = 0; tj < NB8; ++tj) bf[tj] = sy[cl * rsy + tj * 8 + m];
@@ -566,6 +586,24 @@ void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const do
     case 7:
     case 8: lincomb_launch<8>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
     default: fail(PND_ECONFIG, "lincomb supports at most 64 output columns");
+  }
+}
+
+void gram_xy2(const Geom& g, NMat X, NMat Y1, NMat Y2, double* out, DBuf& partial,
+              cudaStream_t st, const double* weight) {
+  // out = X^T diag(weight) [Y1 | Y2]: the Gram-only pass with two staged Y inputs
+  const int ny = Y1.cols + Y2.cols;
+  const int w = ny > X.cols ? ny : X.cols;
+  if (w > 64) fail(PND_ECONFIG, "Grams support at most 64 columns");
+  const NMat o{nullptr, 0, ny};
+  switch ((w + 7) / 8) {
+    case 1: lincomb_launch<1>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 2: lincomb_launch<2>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 3: lincomb_launch<3>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 4: lincomb_launch<4>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 5: lincomb_launch<5>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    case 6: lincomb_launch<6>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
+    default: lincomb_launch<8>(g, Y1, Y2, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
   }
 }
 

@@ -143,31 +143,47 @@ void pgram_launch(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
 }
 
 // ===================================================================== small kernels
+// dK[c] = dt sum_b (psi_b(c) / S(c)) T[cls(c)][b], T[k][b] = N_k^T rows_b (r-vector
+// per class and beam, in shared memory). One warp per 32 cells: the lanes
+// load the cells' class and 1/S once, then write one row (rs <= 32 doubles)
+// per store instruction.
 __global__ void scat_dk_kernel(Geom g, double dt, const double* __restrict__ inv_s,
                                const int* __restrict__ cls, const double* __restrict__ atomic,
-                               const double* __restrict__ psi, int n_beams,
+                               int n_cls, const double* __restrict__ psi, int n_beams,
                                const double* __restrict__ rows, NMat out) {
-  extern __shared__ double sR[];  // n_beams x 12 x r
-  const int r = out.cols, rs = out.rs;
-  for (int i = threadIdx.x; i < n_beams * 12 * r; i += blockDim.x) sR[i] = rows[i];
+  extern __shared__ double sT[];  // n_cls x n_beams x r
+  const int r = out.cols, rs = out.rs, nb = n_beams > 0 ? n_beams : 1;
+  for (int idx = threadIdx.x; idx < n_cls * nb * r; idx += blockDim.x) {
+    const int k = idx / (nb * r), rem = idx - k * nb * r, b = rem / r, j = rem - b * r;
+    double t = 0.0;
+    for (int i = 0; i < 12; ++i) t = fma(atomic[k * 12 + i], rows[(b * 12 + i) * r + j], t);
+    sT[idx] = t;
+  }
   __syncthreads();
-  const long total = (long)g.n * rs;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
-       e += (long)gridDim.x * blockDim.x) {
-    const int c = (int)(e / rs), j = (int)(e - (long)c * rs);
-    double v = 0.0;
-    if (j < r) {
-      const int kc = cls[c];
-      const double is = inv_s[c];
-      for (int b = 0; b < n_beams; ++b) {
-        const double sp = is * psi[(size_t)b * g.ld + c];
-        double s = 0.0;
-        for (int i = 0; i < 12; ++i) s = fma(atomic[kc * 12 + i], sR[(b * 12 + i) * r + j], s);
-        v = fma(sp, s, v);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5, nwarps = gridDim.x * wpb;
+  for (int c0 = (blockIdx.x * wpb + (threadIdx.x >> 5)) * 32; c0 < g.n; c0 += nwarps * 32) {
+    const int c = c0 + lane;
+    const int kc = c < g.n ? cls[c] : 0;
+    const double is = c < g.n ? inv_s[c] : 0.0;
+    double sp[4];  // psi_b / S of this lane's cell (n_beams <= 4)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      sp[b] = (psi && b < n_beams && c < g.n) ? dt * is * psi[(size_t)b * g.ld + c] : 0.0;
+    const int nrow = g.n - c0 < 32 ? g.n - c0 : 32;
+#pragma unroll 4
+    for (int q = 0; q < nrow; ++q) {
+      const int kr = __shfl_sync(0xffffffffu, kc, q);
+      double v = 0.0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (b < n_beams) {  // warp-uniform
+          const double s = __shfl_sync(0xffffffffu, sp[b], q);
+          if (lane < r) v = fma(s, sT[(kr * nb + b) * r + lane], v);
+        }
       }
-      v *= dt;
+      if (lane < rs) out.p[(size_t)(c0 + q) * rs + lane] = v;
     }
-    out.p[e] = v;
   }
 }
 
@@ -337,11 +353,13 @@ void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
 }
 
 void scat_dk(const Geom& g, double dt, const double* inv_s, const int* cls,
-             const double* cls_atomic, const double* psi, int n_beams, const double* rows,
-             NMat out, cudaStream_t st) {
-  const size_t smem = (size_t)(n_beams > 0 ? n_beams : 1) * 12 * out.cols * sizeof(double);
-  scat_dk_kernel<<<grid_for((long)g.n * out.rs, 256), 256, smem, st>>>(
-      g, dt, inv_s, cls, cls_atomic, psi, n_beams, rows, out);
+             const double* cls_atomic, int n_cls, const double* psi, int n_beams,
+             const double* rows, NMat out, cudaStream_t st) {
+  if (out.rs > 32) fail(PND_ECONFIG, "scattering increment supports rank <= 32");
+  const size_t smem = (size_t)n_cls * (n_beams > 0 ? n_beams : 1) * out.cols * sizeof(double);
+  if (smem > 48 * 1024) fail(PND_ECONFIG, "scattering increment: too many material classes");
+  scat_dk_kernel<<<sm_count() * 8, 256, smem, st>>>(g, dt, inv_s, cls, cls_atomic, n_cls, psi,
+                                                    n_beams, rows, out);
   launched();
 }
 

@@ -152,6 +152,9 @@ void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const do
 // streaming pass (lincomb.cu)
 void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStream_t st,
              const double* w = nullptr);
+// out = X^T diag(w) [Y1 | Y2] (X.cols x (Y1.cols + Y2.cols)) in one pass
+void gram_xy2(const Geom& g, NMat X, NMat Y1, NMat Y2, double* out, DBuf& partial,
+              cudaStream_t st, const double* w = nullptr);
 // Z[c][b*12 + i] = N_{cls(c),i} psi_b(c) / S(c): the scattering source rows (dlra.py:244-251)
 void source_rows(const Geom& g, const double* inv_s, const int* cls, const double* cls_atomic,
                  const double* psi, int n_beams, NMat Z, cudaStream_t st);
@@ -177,7 +180,7 @@ void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st);
 
 // dK = dt * inv_s * sum_b psi_b * (N_cls . rows_b)  (scattering source rows, dlra.py:244-251)
 void scat_dk(const Geom& g, double dt, const double* inv_s, const int* cls,
-             const double* cls_atomic, const double* psi, int n_beams,
+             const double* cls_atomic, int n_cls, const double* psi, int n_beams,
              const double* rows /* B x 12 x r */, NMat out, cudaStream_t st);
 
 void dose_accumulate(const Geom& g, NMat U, const double* coef /* U.cols */, double half_dt,

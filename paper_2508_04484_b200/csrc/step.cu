@@ -31,7 +31,7 @@ namespace pnd {
 namespace {
 
 enum Slot {
-  S_FV, S_MST, S_YST, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
+  S_FV, S_MST, S_YST, S_HU, S_QV, S_L0, S_LW, S_ZST, S_BV, S_VHC, S_RV, S_SHAT, S_G,
   S_FH, S_VHR, S_GT, S_ROWS, S_H, S_BI, S_COEF, S_LCOL, S_LNEW, S_RT, S_VTC, S_LEFT, S_PROJ,
   S_PROJ2, S_GTV, S_P, S_SIG, S_QTM, S_TAIL, S_DEF, S_COEFD, S_VNEW, S_M2,
   S_C1, S_OG, S_OTA, S_OTB, S_EYE, S_PC, S_TAZ, S_COUNT
@@ -385,26 +385,44 @@ void scattering_step(Handle& h, double dt) {
     gemm(12 * B, b, m, 1.0, rowm(gt, m), 0, rowm(h.V.p, b), 0, 0.0, rowm(rows, b), 0, 1, st);
   }
 
+  // One material class and one beam: the source rows are rank one,
+  // Z[c][i] = N_i psi(c) / S(c), so Z is never formed -- dK = dt (psi/S) (N^T rows)
+  // row by row, and every projection X^T Z = (X^T diag(1/S) psi) N^T comes
+  // out of a Gram-only pass against the psi column (the one with B_0 for U0).
+  const bool rank1 = h.n_cls == 1 && B == 1;
+  const NMat psi_col{h.psi.p, 1, 1};
+
   // substep 2 increment: dK = dt src_rows(V0) = dt Z rows  (dlra.py:303; K1 = U0 S0 + dK)
   // with the source rows Z[c][b*12 + i] = N_{cls,i} psi_b / S materialised once
   const NMat dK = h.W2.view(g, b, st);
   phase(h, PH_SCATK1);
   NMat Z{};
-  if (B > 0) {
+  if (rank1) {
+    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, 1, h.psi.p, 1, rows, dK, st);
+  } else if (B > 0) {
     Z = h.Xs.view(g, 12 * B, st);
     source_rows(g, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.psi.p, B, Z, st);
     double* TAz = slot(h, S_TAZ, (size_t)12 * B * b);
     axpby(12 * B * b, dt, rows, 0.0, TAz, st);
     lincomb(g, Z, NMat{}, NMat{}, TAz, nullptr, dK, nullptr, h.part, st);
   } else {
-    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, nullptr, 0, rows, dK, st);
+    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.n_cls, nullptr, 0, rows, dK, st);
   }
 
   // substep 1: B_i = U0^T diag(N_i / S) U0 (dlra.py:284-285)
   const int nw = h.n_cls <= 12 ? h.n_cls : 12;
   double* H = slot(h, S_H, (size_t)nw * a * a);
   phase(h, PH_SCATGRAM);
-  if (h.n_cls == 1) {
+  double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
+  if (rank1) {
+    // [H | u] = U0^T diag(1/S) [U0 | psi]; left = U0^T Z = u N^T
+    double* Hu = slot(h, S_HU, (size_t)a * (a + 1));
+    gram_xy2(g, U0, U0, psi_col, Hu, h.part, st, h.inv_s.p);
+    CK(cudaMemcpy2DAsync(H, a * sizeof(double), Hu, (a + 1) * sizeof(double), a * sizeof(double),
+                         a, cudaMemcpyDeviceToDevice, st));
+    gemm(a, 12, 1, 1.0, Mat{Hu + a, a + 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0,
+         rowm(left, 12), 0, 1, st);
+  } else if (h.n_cls == 1) {
     gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);  // one class: U0^T diag(1/S) U0
   } else {
     PGramArgs pa{};
@@ -431,9 +449,8 @@ void scattering_step(Handle& h, double dt) {
     CK(cudaMemcpyAsync(Bi, H, sizeof(double) * 12 * a * a, cudaMemcpyDeviceToDevice, st));
   }
   // source projections U0^T (N psi_b / S)  (a x 12B)
-  double* left = slot(h, S_LEFT, (size_t)a * 12 * (B > 0 ? B : 1));
   phase(h, PH_SCATGRAM);
-  if (B > 0) gram_xy(g, U0, Z, left, h.part, st);
+  if (B > 0 && !rank1) gram_xy(g, U0, Z, left, h.part, st);
   phase(h, PH_SCATSMALL);
   // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass)
   double* C1 = slot(h, S_C1, (size_t)a * b);
@@ -509,7 +526,15 @@ void scattering_step(Handle& h, double dt) {
     CK(cudaMemcpyAsync(proj2, left, sizeof(double) * a * 12 * B, cudaMemcpyDeviceToDevice, st));
     if (k > 0) {
       phase(h, PH_SCATGRAM);
-      gram_xy(g, state_q(h), Z, proj2 + (size_t)a * 12 * B, h.part, st);
+      if (rank1) {
+        // Q^T Z = (Q^T diag(1/S) psi) N^T
+        double* qv = slot(h, S_QV, (size_t)k);
+        gram_xy(g, state_q(h), psi_col, qv, h.part, st, h.inv_s.p);
+        gemm(k, 12, 1, 1.0, Mat{qv, 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0,
+             rowm(proj2 + (size_t)a * 12, 12), 0, 1, st);
+      } else {
+        gram_xy(g, state_q(h), Z, proj2 + (size_t)a * 12 * B, h.part, st);
+      }
       phase(h, PH_SCATSMALL);
     }
     double* gtv = slot(h, S_GTV, (size_t)B * 12 * rv);
