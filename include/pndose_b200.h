@@ -67,6 +67,27 @@ int pnd_set_flux_table(pnd_handle* h, int beam, int n_beams, int n_groups, const
                        const double* t_m);
 int pnd_select_flux(pnd_handle* h, int which, const int32_t* j0, const double* w0,
                     const int32_t* j1, const double* w1);
+/* Per-step coefficient assembly on the device: the
+ * tables behind Problem.class_stopping (stopping.py:48-56, 107-120: log E and
+ * log S per element, 12 x K), Problem.scattering_tables (driver.py:277-362,
+ * angular.py:217-248: moment-table energies (P), Boltzmann moments 12 x P x nd,
+ * Fokker-Planck xi1 12 x P; model 0 Boltzmann / 1 Fokker-Planck) and the
+ * uncollided group grids ((e_min, e_max) per beam, raytracer.py:440-449), uploaded
+ * once. Needs pnd_set_materials and, for the sources, pnd_set_flux_table. */
+int pnd_set_coefficient_tables(pnd_handle* h, int k, const double* log_e, const double* log_s,
+                               const double* class_density, const double* class_weights, int p,
+                               const double* mom_e, int nd, const double* mom_g,
+                               const double* mom_xi1, int model, int pn_order,
+                               int boltzmann_correction, double fp_correction_scale,
+                               int n_beams, const double* flux_range);
+/* driver.step_contexts (driver.py:523-538) on the device: S and 1/S per cell, the
+ * scattering tables and the uncollided slice at e_mid (+ the tally slice at e_lo
+ * when want_lo), with no host->device copy. */
+int pnd_coefficients_at(pnd_handle* h, double e_mid, double e_lo, int want_lo);
+/* Read back the current coefficients (tests): class S (n_cls), g_diags (12 x m),
+ * sigma_t (12), psi and psi_lo (n_beams x n each; null to skip). */
+int pnd_get_coefficients(pnd_handle* h, double* class_s, double* g_diags, double* sigma_t,
+                         double* psi, double* psi_lo);
 
 /* ---- low-rank state (LowRankState, dlra.py:46-72) --------------------- */
 int pnd_state_set(pnd_handle* h, int ru, int rv, const double* u, const double* s, const double* v);

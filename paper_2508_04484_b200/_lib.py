@@ -50,6 +50,10 @@ SIGNATURES = {
     "pnd_k_rhs": [_P, _P, _I, _P, _P],
     "pnd_orthonormalize": [_P, _P, _I, _I, _P, _P],
     "pnd_svd_small": [_P, _P, _I, _I, _P, _P, _P],
+    "pnd_set_coefficient_tables": [_P, _I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _I, _D,
+                                   _I, _P],
+    "pnd_coefficients_at": [_P, _D, _D, _I],
+    "pnd_get_coefficients": [_P, _P, _P, _P, _P, _P],
     "pnd_traverse": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "pnd_timing": [_P, _I],
     "pnd_timing_get": [_P, _I, _P, _P],

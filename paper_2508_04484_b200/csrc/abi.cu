@@ -381,6 +381,66 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
   });
 }
 
+int pnd_set_coefficient_tables(pnd_handle* hh, int k, const double* log_e, const double* log_s,
+                               const double* class_density, const double* class_weights, int p,
+                               const double* mom_e, int nd, const double* mom_g,
+                               const double* mom_xi1, int model, int pn_order,
+                               int boltzmann_correction, double fp_correction_scale,
+                               int n_beams, const double* flux_range) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.have_mat) pnd::fail(PND_ECONFIG, "set materials before the coefficient tables");
+    if (k < 2 || p < 2 || nd < pn_order + 2 || (model != 0 && model != 1))
+      pnd::fail(PND_ECONFIG, "coefficient tables: bad sizes or model");
+    if (n_beams < 0 || n_beams > 4) pnd::fail(PND_ECONFIG, "0..4 beams supported");
+    const size_t nel = 12, nc = h.n_cls;
+    const size_t total = 2 * nel * k + nc + nc * nel + p + nel * p * nd + nel * p + 2 * n_beams;
+    double* d = h.ctab.get(total);
+    size_t o = 0;
+    auto put = [&](const double* src, size_t cnt) {
+      if (cnt) up(d + o, src, cnt, h.st);
+      o += cnt;
+    };
+    put(log_e, nel * k);
+    put(log_s, nel * k);
+    put(class_density, nc);
+    put(class_weights, nc * nel);
+    put(mom_e, p);
+    put(mom_g, nel * p * nd);
+    put(mom_xi1, nel * p);
+    put(flux_range, 2 * (size_t)n_beams);
+    h.ct_K = k;
+    h.ct_P = p;
+    h.ct_nd = nd;
+    h.ct_model = model;
+    h.ct_pn = pn_order;
+    h.ct_bcorr = boltzmann_correction;
+    h.ct_fpscale = fp_correction_scale;
+    if (n_beams && (!h.flux.p || n_beams != h.n_beams))
+      pnd::fail(PND_ECONFIG, "coefficient tables: set the flux tables of every beam first");
+    h.csel.get(32);
+    CK(cudaStreamSynchronize(h.st));
+    h.have_ctab = true;
+  });
+}
+
+int pnd_coefficients_at(pnd_handle* hh, double e_mid, double e_lo, int want_lo) {
+  return guard(hh, [&](Handle& h) { pnd::coefficients_at(h, e_mid, e_lo, want_lo != 0); });
+}
+
+int pnd_get_coefficients(pnd_handle* hh, double* class_s, double* g_diags, double* sigma_t,
+                         double* psi, double* psi_lo) {
+  return guard(hh, [&](Handle& h) {
+    if (class_s) down(class_s, h.cls_val.p, h.n_cls, h.st);
+    if (g_diags) down(g_diags, h.gdiag.p, (size_t)12 * h.m, h.st);
+    if (sigma_t) down(sigma_t, h.sigt.p, 12, h.st);
+    for (int b = 0; b < h.n_beams; ++b) {
+      if (psi) down(psi + (size_t)b * h.g.n, h.psi.p + (size_t)b * h.g.ld, h.g.n, h.st);
+      if (psi_lo) down(psi_lo + (size_t)b * h.g.n, h.psi_lo.p + (size_t)b * h.g.ld, h.g.n, h.st);
+    }
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
 int pnd_select_flux(pnd_handle* hh, int which, const int32_t* j0, const double* w0,
                     const int32_t* j1, const double* w1) {
   return guard(hh, [&](Handle& h) {

@@ -47,6 +47,14 @@ struct Handle {
   DBuf flux;        // n_beams x G x ld (group tables, column-major)
   int n_groups = 0;
   bool have_angular = false, have_inv_s = false, have_mat = false, have_scat = false;
+  // per-step coefficient tables (coeff.cu, pnd_set_coefficient_tables):
+  // [log E | log S (12 x K each) | rho (n_cls) | w (n_cls x 12) | E_mom (P) |
+  //  g (12 x P x nd) | xi1 (12 x P) | flux (e_min, e_max) per beam]
+  DBuf ctab;
+  DBuf csel;        // device-side flux selections (j0, j1; w0, w1)
+  int ct_K = 0, ct_P = 0, ct_nd = 0, ct_model = 0, ct_pn = 0, ct_bcorr = 0;
+  double ct_fpscale = 0.0;
+  bool have_ctab = false;
 
   // state: U^ = [U (ua cols) | Q (uq cols)] cell-major, S (ru x rv row-major),
   // V (m x rv row-major); ru = ua + uq
@@ -76,6 +84,9 @@ NMat state_u(Handle& h);
 NMat state_q(Handle& h);
 void consolidate(Handle& h);   // fold Q into U (uq -> 0)
 void set_isp(Handle& h);       // refresh the [1/S, 0] halo rows from inv_s
+// step coefficients at e_mid (and the uncollided tally slice at e_lo) from the
+// device-resident tables: no host->device copy per step (coeff.cu)
+void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo);
 
 void streaming_step(Handle& h, double dt);
 void scattering_step(Handle& h, double dt);

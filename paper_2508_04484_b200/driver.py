@@ -55,9 +55,13 @@ class SimulationResult:
 class DeviceSolver:
     """One bundle's device state: operators, flux tables, low-rank factors."""
 
-    def __init__(self, bundle: ProblemBundle, device: int = 0, slab=None, comm_id=None):
+    def __init__(self, bundle: ProblemBundle, device: int = 0, slab=None, comm_id=None,
+                 device_coefficients: bool = True):
         """slab: a slabs.Slab (this process's z-planes of a multi-GPU solve)
-        with comm_id the world's NCCL id; None = the whole grid on one GPU."""
+        with comm_id the world's NCCL id; None = the whole grid on one GPU.
+        device_coefficients: evaluate the per-step coefficients on the GPU from
+        tables uploaded once (no host->device copy per step); False = the host
+        restatement (problem.py) uploads them every step."""
         self.bundle = bundle
         b = bundle
         self.slab = slab
@@ -76,6 +80,27 @@ class DeviceSolver:
             self.h.call("pnd_set_flux_table", i, nb, int(vals.shape[1]), _lib.ptr(vals),
                         _lib.ptr(t))
         self.h.call("pnd_dose_reset")
+        self.device_coefficients = False
+        if device_coefficients:
+            self.upload_coefficient_tables()
+
+    def upload_coefficient_tables(self):
+        """Stopping-power, moment and group tables for pnd_coefficients_at (once)."""
+        b = self.bundle
+        log_e, log_s = np.log(b.stop_e), np.log(b.stop_s)  # problem.class_stopping's tables
+        p = len(b.mom_e)
+        mom_g = b.mom_g if b.mom_g is not None else np.zeros((12, p, b.pn_order + 2))
+        xi1 = b.mom_xi1 if b.mom_xi1 is not None else np.zeros((12, p))
+        fr = np.array([[f.e_min, f.e_max] for f in b.fluxes], dtype=np.float64).reshape(-1)
+        arrs = [_lib.f64(x) for x in (log_e, log_s, b.class_density, b.class_weights, b.mom_e,
+                                      mom_g, xi1, fr if fr.size else np.zeros(2))]
+        self.h.call("pnd_set_coefficient_tables", int(log_e.shape[1]), _lib.ptr(arrs[0]),
+                    _lib.ptr(arrs[1]), _lib.ptr(arrs[2]), _lib.ptr(arrs[3]), p,
+                    _lib.ptr(arrs[4]), int(mom_g.shape[2]), _lib.ptr(arrs[5]),
+                    _lib.ptr(arrs[6]), 0 if b.model == "boltzmann" else 1, int(b.pn_order),
+                    1 if b.boltzmann_correction else 0, float(b.fp_correction_scale),
+                    len(b.fluxes), _lib.ptr(arrs[7]))
+        self.device_coefficients = True
 
     def init_state(self, rank=None, seed=None):
         """LowRankState.zero (dlra.py:54-60): seeded Gaussian bases, S = 0."""
@@ -102,6 +127,10 @@ class DeviceSolver:
         """driver.step_contexts (driver.py:523-538), coefficients only."""
         b = self.bundle
         e_mid = 0.5 * (e_hi + e_lo)
+        if self.device_coefficients:
+            self.h.call("pnd_coefficients_at", e_mid, e_lo,
+                        1 if b.uncollided_tally == "steps" else 0)
+            return
         self.h.set_class_stopping(b.class_stopping(e_mid))
         g, s = b.scattering_tables(e_mid)
         self.h.set_scattering(g, s)
