@@ -89,6 +89,20 @@ int pnd_coefficients_at(pnd_handle* h, double e_mid, double e_lo, int want_lo);
 int pnd_get_coefficients(pnd_handle* h, double* class_s, double* g_diags, double* sigma_t,
                          double* psi, double* psi_lo);
 
+/* ---- full-rank oracle on the device (fullrank.py:16-45) --
+ * The dense n x m moment matrix (u, row-major on the host) kept on the GPU in
+ * 32-column blocks; the streaming step is RK4 on apply_streaming (the K-stage
+ * kernel block by block), the scattering step implicit Euler on the
+ * self-scattering rates plus the explicit source (same contexts as the
+ * low-rank steps). pnd_fullrank_step = streaming + scattering + dose tally
+ * (driver.py:607-621). */
+int pnd_fullrank_reset(pnd_handle* h);
+int pnd_fullrank_set(pnd_handle* h, const double* u);
+int pnd_fullrank_get(pnd_handle* h, double* u);
+int pnd_fullrank_streaming_step(pnd_handle* h, double dt);
+int pnd_fullrank_scattering_step(pnd_handle* h, double dt);
+int pnd_fullrank_step(pnd_handle* h, double dt, int tally_steps);
+
 /* ---- low-rank state (LowRankState, dlra.py:46-72) --------------------- */
 int pnd_state_set(pnd_handle* h, int ru, int rv, const double* u, const double* s, const double* v);
 int pnd_state_shape(pnd_handle* h, int* ru, int* rv);

@@ -53,6 +53,12 @@ SIGNATURES = {
     "pnd_set_coefficient_tables": [_P, _I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _I, _D,
                                    _I, _P],
     "pnd_coefficients_at": [_P, _D, _D, _I],
+    "pnd_fullrank_reset": [_P],
+    "pnd_fullrank_set": [_P, _P],
+    "pnd_fullrank_get": [_P, _P],
+    "pnd_fullrank_streaming_step": [_P, _D],
+    "pnd_fullrank_scattering_step": [_P, _D],
+    "pnd_fullrank_step": [_P, _D, _I],
     "pnd_get_coefficients": [_P, _P, _P, _P, _P, _P],
     "pnd_traverse": [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P],
     "pnd_timing": [_P, _I],

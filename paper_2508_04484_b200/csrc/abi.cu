@@ -587,6 +587,50 @@ int pnd_apply_streaming(pnd_handle* hh, const double* u, double* out) {
   });
 }
 
+int pnd_fullrank_reset(pnd_handle* hh) {
+  return guard(hh, [&](Handle& h) { pnd::fullrank_reset(h); });
+}
+
+int pnd_fullrank_set(pnd_handle* hh, const double* u) {
+  return guard(hh, [&](Handle& h) {
+    const int n = h.g.n, m = h.m;
+    for (size_t i = 0; i < (size_t)n * m; ++i)
+      if (!std::isfinite(u[i])) pnd::fail(PND_ENUMERICAL, "non-finite full-rank state");
+    pnd::fullrank_reset(h);
+    for (int b = 0; b < pnd::fullrank_blocks(h); ++b) {
+      const NMat blk = pnd::fullrank_block(h, b);
+      CK(cudaMemcpy2DAsync(blk.p, blk.rs * sizeof(double), u + 32 * b, m * sizeof(double),
+                           blk.cols * sizeof(double), n, cudaMemcpyHostToDevice, h.st));
+    }
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_fullrank_get(pnd_handle* hh, double* u) {
+  return guard(hh, [&](Handle& h) {
+    if (!h.have_fr) pnd::fail(PND_ECONFIG, "no full-rank state");
+    for (int b = 0; b < pnd::fullrank_blocks(h); ++b)
+      download_rows(h, pnd::fullrank_block(h, b), u, h.m, 32 * b);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_fullrank_streaming_step(pnd_handle* hh, double dt) {
+  return guard(hh, [&](Handle& h) { pnd::fullrank_streaming_step(h, dt); });
+}
+
+int pnd_fullrank_scattering_step(pnd_handle* hh, double dt) {
+  return guard(hh, [&](Handle& h) { pnd::fullrank_scattering_step(h, dt); });
+}
+
+int pnd_fullrank_step(pnd_handle* hh, double dt, int tally_steps) {
+  return guard(hh, [&](Handle& h) {
+    pnd::fullrank_streaming_step(h, dt);
+    pnd::fullrank_scattering_step(h, dt);
+    pnd::fullrank_dose_step(h, dt, tally_steps != 0);
+  });
+}
+
 int pnd_stencil_grams(pnd_handle* hh, const double* x, int a, const double* y, int b,
                       double* out) {
   return guard(hh, [&](Handle& h) {

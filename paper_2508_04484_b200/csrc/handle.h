@@ -55,6 +55,11 @@ struct Handle {
   int ct_K = 0, ct_P = 0, ct_nd = 0, ct_model = 0, ct_pn = 0, ct_bcorr = 0;
   double ct_fpscale = 0.0;
   bool have_ctab = false;
+  // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
+  std::vector<NBuf> fr_u, fr_w1, fr_w2;
+  NBuf fr_t[2];
+  DBuf fr_scr, fr_scr2, fr_scr3, fr_eye;
+  bool have_fr = false;
 
   // state: U^ = [U (ua cols) | Q (uq cols)] cell-major, S (ru x rv row-major),
   // V (m x rv row-major); ru = ua + uq
@@ -87,6 +92,14 @@ void set_isp(Handle& h);       // refresh the [1/S, 0] halo rows from inv_s
 // step coefficients at e_mid (and the uncollided tally slice at e_lo) from the
 // device-resident tables: no host->device copy per step (coeff.cu)
 void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo);
+
+// full-rank oracle on the device (fullrank.cu, fullrank.py:16-45)
+void fullrank_reset(Handle& h);                    // u = 0
+NMat fullrank_block(Handle& h, int b);             // columns [32 b, 32 b + 32)
+int fullrank_blocks(const Handle& h);
+void fullrank_streaming_step(Handle& h, double dt);
+void fullrank_scattering_step(Handle& h, double dt);
+void fullrank_dose_step(Handle& h, double dt, bool tally_steps);
 
 void streaming_step(Handle& h, double dt);
 void scattering_step(Handle& h, double dt);

@@ -167,8 +167,10 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
 
     slab / comm_id: this process's z-slab of a multi-GPU solve (slabs.plan)
     and the world's communicator id; the dose then covers the slab's cells."""
-    if solver != "dlra":
+    if solver not in ("dlra", "fullrank"):
         raise ConfigError(f"unknown solver '{solver}'")
+    if solver == "fullrank":
+        return _run_fullrank(bundle, max_steps, device, slab, comm_id)
     t_start = time.perf_counter()
     b = bundle
     n, m = b.n_cells, b.n_moments
@@ -228,6 +230,44 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
                             uncollided=unc)
 
 
+def _run_fullrank(b: ProblemBundle, max_steps, device, slab, comm_id) -> SimulationResult:
+    """The solver="fullrank" branch of the loop (driver.py:607-621) on the device:
+    the dense n x m matrix from zero, streaming RK4 + scattering + dose per step."""
+    t_start = time.perf_counter()
+    n, m = b.n_cells, b.n_moments
+    solver_ = DeviceSolver(b, device, slab=slab, comm_id=comm_id)
+    solver_.h.call("pnd_fullrank_reset")
+    edges = b.pseudo_time_edges()
+    n_steps = len(edges) - 1 if max_steps is None else min(len(edges) - 1, int(max_steps))
+    tally = 1 if b.uncollided_tally == "steps" else 0
+    ranks = []
+    for k in range(n_steps):
+        e_hi, e_lo = edges[k], edges[k + 1]
+        solver_.set_coefficients(e_hi, e_lo)
+        solver_.h.call("pnd_fullrank_step", float(e_hi - e_lo), tally)
+        ranks.append((k, float(e_lo), min(n, m)))
+    deposited = solver_.dose()
+    lo, hi = solver_.rows
+    unc = None
+    if b.uncollided_tally == "groups":
+        unc = b.uncollided_dose()[lo:hi]
+        deposited = deposited + unc
+    solver_.close()
+    dose = DoseGrid(deposited=deposited, dose=deposited / b.density[lo:hi])
+    diagnostics = {
+        "solver": "fullrank-b200",
+        "n_cells": n,
+        "n_moments": m,
+        "n_steps": n_steps,
+        "energy_step_mev": float(edges[0] - edges[1]),
+        "fullrank_numbers": int(n * m),
+        "negativity": dose.negativity,
+        "runtime_s": time.perf_counter() - t_start,
+    }
+    return SimulationResult(bundle=b, dose=dose, rank_history=ranks, diagnostics=diagnostics,
+                            uncollided=unc)
+
+
 def run_simulation(config, solver: str = "dlra"):
     """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541).
 
@@ -235,16 +275,17 @@ def run_simulation(config, solver: str = "dlra"):
     tracer setup (material keys, coefficient closures; driver.py:398-436) are
     the reference's unchanged host code; every beam's march and deposit
     (raytracer.trace_beam) and the energy loop run on the GPU.
-    solver="dlra-cpu" / "fullrank" hand the whole run back to the reference.
+    solver="fullrank" runs the dense oracle on the device (fullrank.cu);
+    solver="dlra-cpu" hands the whole run back to the reference.
     """
     from pndose import driver as ref_driver  # the reference package
     from pndose.angular import beam_projection
 
     from . import raytracer as dev_tracer
 
-    if solver in ("dlra-cpu", "fullrank"):
-        return ref_driver.run_simulation(config, solver="dlra" if solver == "dlra-cpu" else solver)
-    if solver != "dlra":
+    if solver == "dlra-cpu":
+        return ref_driver.run_simulation(config, solver="dlra")
+    if solver not in ("dlra", "fullrank"):
         raise ConfigError(f"unknown solver '{solver}'")
     problem = ref_driver.assemble_problem(config)
     ref_trace = ref_driver.trace_beam
@@ -255,7 +296,7 @@ def run_simulation(config, solver: str = "dlra"):
         ref_driver.trace_beam = ref_trace
     t_ms = [beam_projection(config.pn_order, bm.direction) for bm in config.beams]
     bundle = ProblemBundle.from_arrays(export_problem(problem, fluxes, t_ms))
-    return run_bundle(bundle)
+    return run_bundle(bundle, solver=solver)
 
 
 __all__ = ["DeviceSolver", "run_bundle", "run_simulation", "SimulationResult", "DoseGrid",
