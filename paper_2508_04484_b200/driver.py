@@ -268,6 +268,23 @@ def _run_fullrank(b: ProblemBundle, max_steps, device, slab, comm_id) -> Simulat
                             uncollided=unc)
 
 
+def write_dose_volume(result: SimulationResult, path, binary: bool = True, slab=None):
+    """The dose.vtk of driver.write_outputs (driver.py:672-690) for a run_bundle
+    result: binary legacy VTK by default (output.py; binary=False is the
+    reference's ASCII form). slab: this rank's slabs.Slab of a multi-GPU run,
+    whose result holds only its cells -- each rank then writes its own byte
+    ranges of the one file (output.write_volume_slab)."""
+    from .output import VolumeGrid, write_volume, write_volume_slab
+
+    b = result.bundle
+    grid = VolumeGrid(*b.shape, *b.spacing, tuple(b.origin))
+    arrays = {"deposited_energy": result.dose.deposited, "dose": result.dose.dose}
+    if slab is None:
+        write_volume(path, grid, arrays, binary=binary)
+    else:
+        write_volume_slab(path, grid, list(arrays), arrays, slab.rows[0], slab.rank)
+
+
 def run_simulation(config, solver: str = "dlra"):
     """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541).
 

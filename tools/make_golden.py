@@ -557,6 +557,19 @@ def make_bench_physics():
     )
 
 
+def make_volume():
+    """A small volume in the reference's own ASCII VTK writer (driver.py:672-690)
+    for the output-reader parity test."""
+    from pndose.driver import write_volume
+    from pndose.spatial import Grid3D
+
+    grid = Grid3D(4, 3, 5, 0.1, 0.2, 0.3, origin=(1.0, 2.0, 3.0))
+    rng = np.random.default_rng(0)
+    dep = rng.random(grid.n_cells) * np.exp(rng.uniform(-30, 5, grid.n_cells))
+    write_volume(OUT / "volume_ref.vtk", grid, {"deposited_energy": dep, "dose": 2.0 * dep})
+    save("volume_ref.npz", deposited_energy=dep, dose=2.0 * dep)
+
+
 if __name__ == "__main__":
     OUT.mkdir(parents=True, exist_ok=True)
     what = set(sys.argv[1:])
@@ -574,6 +587,8 @@ if __name__ == "__main__":
         make_march()
     if not what or "bench" in what:
         make_bench_physics()
+    if not what or "volume" in what:
+        make_volume()
     e2e = {w[4:] for w in what if w.startswith("e2e:")}
     if not what or "e2e" in what or e2e:
         make_e2e(e2e)
