@@ -284,7 +284,8 @@ __global__ void lerp_kernel(const double* __restrict__ v, int ldv, int n, int j0
 __global__ void tin_kernel(const double* __restrict__ src, int n, int cdim, double* __restrict__ dst,
                            int ldd) {
   __shared__ double tile[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  // rows on grid x (up to 2^31 - 1 blocks), columns on grid y
+  const int c0 = blockIdx.y * 32, r0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int row = r0 + i, col = c0 + threadIdx.x;
     tile[i][threadIdx.x] = (row < n && col < cdim) ? src[(size_t)row * cdim + col] : 0.0;
@@ -299,7 +300,7 @@ __global__ void tin_kernel(const double* __restrict__ src, int n, int cdim, doub
 __global__ void tout_kernel(const double* __restrict__ src, int lds, int n, int cdim,
                             double* __restrict__ dst) {
   __shared__ double tile[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int c0 = blockIdx.y * 32, r0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int col = c0 + i, row = r0 + threadIdx.x;
     tile[threadIdx.x][i] = (row < n && col < cdim) ? src[(size_t)col * lds + row] : 0.0;
@@ -396,14 +397,14 @@ void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, d
 
 void transpose_in(const double* src, int n, int c, double* dst, int ldd, cudaStream_t st) {
   if (n <= 0 || c <= 0) return;
-  dim3 grid((c + 31) / 32, (n + 31) / 32), block(32, 8);
+  dim3 grid((n + 31) / 32, (c + 31) / 32), block(32, 8);
   tin_kernel<<<grid, block, 0, st>>>(src, n, c, dst, ldd);
   launched();
 }
 
 void transpose_out(const double* src, int lds, int n, int c, double* dst, cudaStream_t st) {
   if (n <= 0 || c <= 0) return;
-  dim3 grid((c + 31) / 32, (n + 31) / 32), block(32, 8);
+  dim3 grid((n + 31) / 32, (c + 31) / 32), block(32, 8);
   tout_kernel<<<grid, block, 0, st>>>(src, lds, n, c, dst);
   launched();
 }

@@ -123,6 +123,16 @@ def test_orthonormalize_tsqr(dl, shape):
     assert np.abs(q @ (q.T @ a) - a).max() < 1e-12 * max(1.0, np.abs(a).max())
 
 
+def test_orthonormalize_tall_beyond_grid_y(dl):
+    """n > 65535 x 32 rows (the 128^3 initial state): the layout transposes put
+    rows on grid x (grid y is capped at 65535 blocks)."""
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((2_200_000, 2))
+    q = dl.orthonormal_columns(a)
+    assert np.abs(q.T @ q - np.eye(2)).max() < 1e-13
+    assert np.abs(q @ (q.T @ a) - a).max() < 1e-10 * np.abs(a).max()
+
+
 def test_orthonormalize_zero_block_is_canonical(dl):
     # [0 | U0] -> first columns are +e_0.. (reference step-0 behaviour, Appendix C.4)
     rng = np.random.default_rng(5)

@@ -1,0 +1,35 @@
+"""Adaptive-rank probe on the bench workload (256^3 water, P19 FP): run the
+first energy steps from a rank-2 zero state with the tail threshold set
+relative to the running largest singular value, and print the rank history
+(how far the rank-adaptive config 2 of SURVEY.md §8(d) goes)."""
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2508_04484_b200 import _lib as bench_lib  # noqa: E402
+
+nside = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+rel = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-8
+steps = int(sys.argv[3]) if len(sys.argv) > 3 else 400
+wl = bench.Workload(nside=nside, rank=2)
+s = wl.solver
+b = wl.bundle
+s.init_state(rank=2)
+wl.k = 0
+edges = wl.edges
+smax = 0.0
+for k in range(min(steps, len(edges) - 1)):
+    e_hi, e_lo = edges[k], edges[k + 1]
+    b.truncation_tolerance = max(rel * smax, 1e-300)
+    b.rank_min, b.rank_max = 2, 32
+    s.set_coefficients(e_hi, e_lo)
+    out = s.step(e_hi - e_lo, want_defect=False)
+    r = int(out[2])
+    sm = np.empty((r, r))
+    s.h.call("pnd_state_get", None, bench_lib.ptr(sm), None)
+    sig = np.linalg.svd(sm, compute_uv=False)
+    smax = max(smax, float(sig[0]) if sig.size else 0.0)
+    if k % 25 == 0 or int(out[2]) >= 30:
+        print(k, f"E={e_lo:.2f}", "rank", int(out[2]), f"smax={smax:.3e}", flush=True)
