@@ -86,29 +86,38 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
                            int* info, double* dinfo) {
   __shared__ int k_s;
   __shared__ double scale[64];
+  __shared__ int keep[64];
+  __shared__ double red[256];
   const int tid = threadIdx.x;
+  // per column: 1/sqrt(lambda) and the deflation test (parallel; the serial
+  // scan below only reads shared memory)
+  const double l0 = b > 0 ? lam[0] : 0.0;
+  for (int j = tid; j < b; j += blockDim.x) {
+    const double l = lam[j];
+    scale[j] = 1.0 / sqrt(l > 0.0 ? l : 1e-300);
+    keep[j] = l > 0.0 && l > tol_rel * tol_rel * l0;
+  }
+  // orthonormality defect of the previous pass: max |G - I|, max |C|
+  double d = 0.0;
+  for (int i = tid; i < b * b + a * b; i += blockDim.x) {
+    const double v = i < b * b ? fabs(G[i] - ((i / b == i % b) ? 1.0 : 0.0)) : fabs(C[i - b * b]);
+    d = v > d ? v : d;
+  }
+  red[tid] = d;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
+    __syncthreads();
+  }
   if (tid == 0) {
-    int k = 0;
+    int k = b;
     if (mode == 0) {
-      const double l0 = b > 0 ? lam[0] : 0.0;
-      for (int j = 0; j < b; ++j) {
-        const double l = lam[j];
-        if (l > 0.0 && l > tol_rel * tol_rel * l0) k = j + 1;
-        else break;
-      }
-    } else {
-      k = b;
+      k = 0;
+      while (k < b && keep[k]) ++k;
     }
     k_s = k;
-    for (int j = 0; j < b; ++j) scale[j] = 1.0 / sqrt(lam[j] > 0.0 ? lam[j] : 1e-300);
-    double d = 0.0;
-    for (int i = 0; i < b * b; ++i) {
-      const double v = fabs(G[i] - ((i / b == i % b) ? 1.0 : 0.0));
-      d = v > d ? v : d;
-    }
-    for (int i = 0; i < a * b; ++i) d = fabs(C[i]) > d ? fabs(C[i]) : d;
     info[0] = k;
-    dinfo[0] = d;
+    dinfo[0] = red[0];
   }
   __syncthreads();
   const int k = k_s;
