@@ -475,8 +475,12 @@ __global__ void scat_solve_kernel(const double* B, const double* coeffs, const d
   for (int a = tid; a < r; a += nthr) lnew[a * m + q] = x[a];
 }
 
+// RK4 (Horner form) of S' = -sum_s G_s S F_s on the R x R coefficient matrix in
+// one CTA; with `staged` the Grams and moment factors are copied to shared
+// memory first (the products then read only shared memory), and every
+// product element is formed from two interleaved partial sums.
 __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const double* F, int ns,
-                             double dt) {
+                             double dt, int staged) {
   extern __shared__ double sm[];
   const int pq = p * q;
   double* S0 = sm;
@@ -484,27 +488,47 @@ __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const dou
   double* T = W + pq;
   double* Acc = T + pq;
   const int tid = threadIdx.x, nthr = blockDim.x;
+  const double* Gb = G;
+  const double* Fb = F;
+  if (staged) {
+    double* sg = Acc + pq;
+    double* sf = sg + (size_t)ns * p * p;
+    for (int i = tid; i < ns * p * p; i += nthr) sg[i] = G[i];
+    for (int i = tid; i < ns * q * q; i += nthr) sf[i] = F[i];
+    Gb = sg;
+    Fb = sf;
+  }
   for (int i = tid; i < pq; i += nthr) S0[i] = W[i] = S[i];
   __syncthreads();
   const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
   for (int st = 0; st < 4; ++st) {
     for (int i = tid; i < pq; i += nthr) Acc[i] = 0.0;
     for (int s = 0; s < ns; ++s) {
-      const double* Gs = G + (size_t)s * p * p;
-      const double* Fs = F + (size_t)s * q * q;
+      const double* Gs = Gb + (size_t)s * p * p;
+      const double* Fs = Fb + (size_t)s * q * q;
       __syncthreads();
       for (int i = tid; i < pq; i += nthr) {
         const int a = i / q, b = i % q;
-        double t = 0.0;
-        for (int k = 0; k < p; ++k) t = fma(Gs[a * p + k], W[k * q + b], t);
-        T[i] = t;
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < p; k += 2) {
+          t0 = fma(Gs[a * p + k], W[k * q + b], t0);
+          t1 = fma(Gs[a * p + k + 1], W[(k + 1) * q + b], t1);
+        }
+        if (k < p) t0 = fma(Gs[a * p + k], W[k * q + b], t0);
+        T[i] = t0 + t1;
       }
       __syncthreads();
       for (int i = tid; i < pq; i += nthr) {
         const int a = i / q, b = i % q;
-        double t = 0.0;
-        for (int k = 0; k < q; ++k) t = fma(T[a * q + k], Fs[k * q + b], t);
-        Acc[i] -= t;
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < q; k += 2) {
+          t0 = fma(T[a * q + k], Fs[k * q + b], t0);
+          t1 = fma(T[a * q + k + 1], Fs[(k + 1) * q + b], t1);
+        }
+        if (k < q) t0 = fma(T[a * q + k], Fs[k * q + b], t0);
+        Acc[i] -= t0 + t1;
       }
     }
     __syncthreads();
@@ -811,8 +835,10 @@ void scat_solves(const double* B, const double* coeffs, const double* lcols, int
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt, double*,
            cudaStream_t st) {
   const size_t sm = 4 * (size_t)p * q * sizeof(double);
-  set_smem((const void*)s_rk4_kernel, sm);
-  s_rk4_kernel<<<1, 1024, sm, st>>>(S, p, q, G, F, ns, dt);
+  const size_t sm_staged = sm + ((size_t)ns * ((size_t)p * p + (size_t)q * q)) * sizeof(double);
+  const bool staged = sm_staged + 1024 <= (size_t)kMaxDynSmem;
+  set_smem((const void*)s_rk4_kernel, staged ? sm_staged : sm);
+  s_rk4_kernel<<<1, 1024, staged ? sm_staged : sm, st>>>(S, p, q, G, F, ns, dt, staged ? 1 : 0);
   launched();
 }
 
