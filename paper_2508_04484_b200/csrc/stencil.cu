@@ -530,7 +530,7 @@ void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
 template <int NA, int T8, int GC>
 __global__ void __launch_bounds__(gpth(T8), 1)
     sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, int nstg, const double* __restrict__ isp,
-                 int bt0, int nbt, double* __restrict__ partial, int dbg) {
+                 int bt0, int nbt, double* __restrict__ partial) {
   constexpr int NS = 2 * NA;
   constexpr int W = T8 * 8;
   constexpr int XS = pad4(W);
@@ -558,8 +558,6 @@ __global__ void __launch_bounds__(gpth(T8), 1)
       Ring r(nstg);
       for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
         if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
-        if (dbg & 1) mbar_arrive(&pb->sfull[r.s]);
-        else
         issue_seg<GC, NA>(S, sm + r.s * S.total, &pb->sfull[r.s], chunk_cell(S, chunk, GC), X1,
                           X2, nin, isp, X1);
       }
@@ -589,7 +587,6 @@ __global__ void __launch_bounds__(gpth(T8), 1)
       const bool fast = __all_sync(0xffffffffu, cx.inner);
       constexpr int TT = (W + JS - 1) / JS;
       cx.rows(X1s, X1.rs, ci, cj);
-      if (!(dbg & 2)) {
 #pragma unroll
       for (int t = 0; t < TT; ++t) {
         const int j = cj + JS * t;
@@ -616,7 +613,6 @@ __global__ void __launch_bounds__(gpth(T8), 1)
           }
         }
       }
-      }
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&pb->ffull[f]);
@@ -638,7 +634,7 @@ __global__ void __launch_bounds__(gpth(T8), 1)
       const double* pa = F0 + b * FT + NS * W * GTL + kq * XS + m0;
       const double* pbt = F0 + b * FT + ((bt0 + m) * 8 + m0) * GTL + kq;
 #pragma unroll 1
-      for (int k0 = 0; k0 < ((dbg & 4) ? 0 : GC); k0 += 4) {
+      for (int k0 = 0; k0 < GC; k0 += 4) {
         double af[T8];
 #pragma unroll
         for (int ti = 0; ti < T8; ++ti) af[ti] = pa[k0 * XS + ti * 8];
@@ -707,9 +703,8 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   const int nb = 2 * NA * T8;
   for (int bt0 = 0; bt0 < nb; bt0 += 32) {
     const int nbt = nb - bt0 < 32 ? nb - bt0 : 32;
-        static const int dbg = getenv("PND_SGRAM_DEBUG") ? atoi(getenv("PND_SGRAM_DEBUG")) : 0;
-    sgram_kernel<NA, T8, GC><<<grid, gpth(T8), smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt, part,
-                                                        dbg);
+    sgram_kernel<NA, T8, GC><<<grid, gpth(T8), smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt,
+                                                        part);
     launched();
   }
   reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, w * w,
