@@ -212,15 +212,17 @@ __global__ void copy_rfac_kernel(const double* Rn, int ldn, int kc, int cols, do
 // ----------------------------------------------------------------- SVD
 template <int MT>  // column elements per lane: M <= 32 MT
 __global__ void __launch_bounds__(1024, 1)
-    svd_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
+    svd_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt, double* gw) {
   extern __shared__ double sm[];
   const bool tall = p >= q;
   const int M = tall ? p : q, N = tall ? q : p;
   const int N2 = N + (N & 1);
-  double* A = sm;                  // column-major M x N2
+  // gw: A, V and U in a global (L2-resident) work buffer when they do not fit
+  // in shared memory (the wide R x R case); sg and perm stay in shared memory
+  double* A = gw ? gw : sm;        // column-major M x N2
   double* Vm = A + M * N2;         // column-major N2 x N2
   double* U = Vm + N2 * N2;        // column-major M x N (sorted, completed)
-  double* sg = U + M * N;          // N2
+  double* sg = gw ? sm : U + M * N;  // N2
   int* perm = (int*)(sg + N2);     // N
   __shared__ int rotated;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -480,10 +482,10 @@ __global__ void scat_solve_kernel(const double* B, const double* coeffs, const d
 // memory first (the products then read only shared memory), and every
 // product element is formed from two interleaved partial sums.
 __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const double* F, int ns,
-                             double dt, int staged) {
+                             double dt, int staged, double* __restrict__ gw) {
   extern __shared__ double sm[];
   const int pq = p * q;
-  double* S0 = sm;
+  double* S0 = gw ? gw : sm;  // gw: global work for the wide (R > ~90) case
   double* W = S0 + pq;
   double* T = W + pq;
   double* Acc = T + pq;
@@ -545,13 +547,16 @@ __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const dou
 // tau = 0 for a zero sub-column), and the explicit Q is then formed in place by
 // applying the reflectors backwards (LAPACK dorg2r order). Replaces a TSQR
 // tree of several launches by one launch for the small m-side QRs.
+// gw: when the matrix does not fit in shared memory (wide factors: cols > 64)
+// it lives in this global (L2-resident) work buffer instead -- same algorithm
 __global__ void __launch_bounds__(512)
     qr_small_kernel(const double* __restrict__ A, int rows, int cols, int lda,
-                    double* __restrict__ Q, int ldq, double* __restrict__ rfac) {
+                    double* __restrict__ Q, int ldq, double* __restrict__ rfac,
+                    double* __restrict__ gw) {
   extern __shared__ double sm[];
   const int LDS = cols | 1;  // odd row length: conflict-free column walks
-  double* S = sm;                      // rows x LDS
-  double* red = S + (size_t)rows * LDS;  // 32
+  double* S = gw ? gw : sm;            // rows x LDS
+  double* red = gw ? sm : S + (size_t)rows * LDS;  // 32
   double* wk = red + 32;               // cols
   double* tau = wk + cols;             // cols
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -676,14 +681,25 @@ void axpby(int count, double a, const double* x, double b, double* y, cudaStream
 
 int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfac, TsqrWork& w,
          cudaStream_t st) {
-  if (cols > 64) fail(PND_ECONFIG, "orthonormalisation supports at most 64 columns");
+  if (cols > 128) fail(PND_ECONFIG, "orthonormalisation supports at most 128 columns");
   const int kc = rows < cols ? rows : cols;
   {
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
     if (sm + 1024 <= (size_t)kMaxDynSmem) {
       set_smem((const void*)qr_small_kernel, sm);
-      qr_small_kernel<<<1, 512, sm, st>>>(a, rows, cols, lda, q, ldq, rfac);
+      qr_small_kernel<<<1, 512, sm, st>>>(a, rows, cols, lda, q, ldq, rfac, nullptr);
+      launched();
+      return kc;
+    }
+    if (cols > 64) {
+      // wide factors (more than 64 columns): the same one-CTA Householder QR
+      // with the matrix in a global, L2-resident work buffer
+      if ((size_t)rows * cols > ((size_t)1 << 24))
+        fail(PND_ECONFIG, "orthonormalisation of more than 64 columns supports <= 2^24 entries");
+      double* gw = w.rbuf.get((size_t)rows * (cols | 1));
+      const size_t sms = (32 + 2 * (size_t)cols) * sizeof(double);
+      qr_small_kernel<<<1, 512, sms, st>>>(a, rows, cols, lda, q, ldq, rfac, gw);
       launched();
       return kc;
     }
@@ -796,25 +812,32 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
 void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt, double*,
                cudaStream_t st) {
   const int M = p >= q ? p : q, N = p >= q ? q : p;
-  if (M > 256 || N > 64) fail(PND_ECONFIG, "truncation SVD supports at most 256 x 64");
+  if (M > 256 || N > 128) fail(PND_ECONFIG, "truncation SVD supports at most 256 x 128");
   const int N2 = N + (N & 1);
-  const size_t sm =
-      ((size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N + N2) * sizeof(double) + N * sizeof(int);
-  // one warp per Jacobi pair of a round: a round is one shuffle-reduction deep
+  const size_t mats = (size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N;
+  size_t sm = (mats + N2) * sizeof(double) + N * sizeof(int);
+  double* gw = nullptr;
+  if (sm + 1024 > (size_t)kMaxDynSmem) {
+    // wide R x R: A, V, U in a global (L2-resident) work buffer, stream-ordered
+    CK(cudaMallocAsync((void**)&gw, mats * sizeof(double), st));
+    sm = N2 * sizeof(double) + N * sizeof(int);
+  }
+  // one warp per Jacobi pair of a round (two per warp above 64 columns)
   int threads = 32 * (N2 / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
   if (M <= 64) {
     set_smem((const void*)svd_kernel<2>, sm);
-    svd_kernel<2><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+    svd_kernel<2><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
   } else if (M <= 128) {
     set_smem((const void*)svd_kernel<4>, sm);
-    svd_kernel<4><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+    svd_kernel<4><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
   } else {
     set_smem((const void*)svd_kernel<8>, sm);
-    svd_kernel<8><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt);
+    svd_kernel<8><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
   }
   launched();
+  if (gw) CK(cudaFreeAsync(gw, st));
 }
 
 void tail_rule(const double* sig, int k, double theta, int rmin, int rmax, int* info,
@@ -837,8 +860,18 @@ void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, do
   const size_t sm = 4 * (size_t)p * q * sizeof(double);
   const size_t sm_staged = sm + ((size_t)ns * ((size_t)p * p + (size_t)q * q)) * sizeof(double);
   const bool staged = sm_staged + 1024 <= (size_t)kMaxDynSmem;
+  if (!staged && sm + 1024 > (size_t)kMaxDynSmem) {
+    // wide: the four R x R work matrices in global memory (stream-ordered)
+    double* gw = nullptr;
+    CK(cudaMallocAsync((void**)&gw, 4 * (size_t)p * q * sizeof(double), st));
+    s_rk4_kernel<<<1, 1024, 0, st>>>(S, p, q, G, F, ns, dt, 0, gw);
+    launched();
+    CK(cudaFreeAsync(gw, st));
+    return;
+  }
   set_smem((const void*)s_rk4_kernel, staged ? sm_staged : sm);
-  s_rk4_kernel<<<1, 1024, staged ? sm_staged : sm, st>>>(S, p, q, G, F, ns, dt, staged ? 1 : 0);
+  s_rk4_kernel<<<1, 1024, staged ? sm_staged : sm, st>>>(S, p, q, G, F, ns, dt, staged ? 1 : 0,
+                                                           nullptr);
   launched();
 }
 

@@ -108,7 +108,7 @@ def test_two_cell_axis_rejected(dl, kernels_npz):
 
 
 @pytest.mark.parametrize("shape", [(7, 3), (40, 6), (300, 12), (1000, 40), (5, 9), (129, 64),
-                                   (4000, 2)])
+                                   (4000, 2), (400, 128), (600, 100)])
 def test_orthonormalize_tsqr(dl, shape):
     rng = np.random.default_rng(sum(shape))
     a = rng.standard_normal(shape)
@@ -141,7 +141,9 @@ def test_orthonormalize_zero_block_is_canonical(dl):
     np.testing.assert_array_equal(q[:, :5], np.eye(700)[:, :5])
 
 
-@pytest.mark.parametrize("pq", [(6, 6), (10, 4), (4, 10), (40, 40), (32, 16)])
+@pytest.mark.parametrize("pq", [(6, 6), (10, 4), (4, 10), (40, 40), (32, 16),
+                                # wide R x R (global work buffer): ranks up to 64
+                                (100, 100), (128, 128), (128, 80), (90, 128)])
 def test_svd_small(pq):
     from paper_2508_04484_b200 import _lib
     from paper_2508_04484_b200.dlra import _generic_handle
