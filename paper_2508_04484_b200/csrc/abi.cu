@@ -457,7 +457,8 @@ int pnd_state_set(pnd_handle* hh, int ru, int rv, const double* u, const double*
                   const double* v) {
   return guard(hh, [&](Handle& h) {
     if (ru < 1 || rv < 1) pnd::fail(PND_ECONFIG, "rank must be positive");
-    if (ru > 64 || rv > 64) pnd::fail(PND_ECONFIG, "rank above 64 is not supported");
+    // 64 columns per factor, 128 for an augmented state (truncate input)
+    if (ru > 128 || rv > 128) pnd::fail(PND_ECONFIG, "rank above 64 is not supported");
     NMat U = h.U.view(h.g, ru, h.st);
     upload_rows(h, U, u);
     up(h.S.get((size_t)ru * rv), s, (size_t)ru * rv, h.st);
@@ -642,7 +643,26 @@ int pnd_stencil_grams(pnd_handle* hh, const double* x, int a, const double* y, i
     upload_rows(h, Y, y);
     pnd::DBuf o;
     double* O = o.get((size_t)h.g.ns * a * b + 1);
-    pnd::stencil_grams_xy(h.g, X, Y, h.isp.p + 2 * (size_t)h.g.halo, O, h.part, h.st);
+    if (a + b > 64) {
+      // wider than one S-Gram launch: the block pairs of the streaming step
+      std::vector<NMat> bl = pnd::split_blocks(h, Y, h.wide_u0b);
+      const int nby = (int)bl.size();
+      for (const NMat& q : pnd::split_blocks(h, X, h.wide_qb)) bl.push_back(q);
+      const int w = a + b;
+      pnd::DBuf full;
+      double* F = full.get((size_t)h.g.ns * w * w);
+      pnd::stencil_grams_blocks(h, bl, h.isp.p + 2 * (size_t)h.g.halo, F);
+      (void)nby;
+      // the (X, D Y) block: rows b.., columns 0..b (G = [Y | X]^T D [Y | X])
+      for (int s2 = 0; s2 < h.g.ns; ++s2)
+        CK(cudaMemcpy2DAsync(O + (size_t)s2 * a * b, b * sizeof(double),
+                             F + ((size_t)s2 * w + b) * w, w * sizeof(double), b * sizeof(double),
+                             a, cudaMemcpyDeviceToDevice, h.st));
+      CK(cudaStreamSynchronize(h.st));
+      full.free_();
+    } else {
+      pnd::stencil_grams_xy(h.g, X, Y, h.isp.p + 2 * (size_t)h.g.halo, O, h.part, h.st);
+    }
     down(out, O, (size_t)h.g.ns * a * b, h.st);
     CK(cudaStreamSynchronize(h.st));
     o.free_();
@@ -661,15 +681,23 @@ int pnd_k_rhs(pnd_handle* hh, const double* k, int r, const double* f, double* o
     up(M, f, (size_t)ns * r * r, h.st);
     pnd::axpby(ns * r * r, -1.0, M, 0.0, M, h.st);
     NMat O = h.W2.view(h.g, r, h.st);
-    pnd::KStageArgs a{};
-    a.bcat = &h.bcat;
-    a.geo = h.g;
-    a.X = K;
-    a.M = M;
-    a.inv_s = h.isp.p + 2 * (size_t)h.g.halo;
-    a.out = O;
-    pnd::kstage(a, h.st);
-    download_rows(h, O, out, r, 0);
+    if (r > 32) {
+      // ranks above 32: the block chain of the streaming step (wide.cu)
+      const auto xb = pnd::split_blocks(h, K, h.wide_w1b);
+      const auto ob = pnd::block_views(h, h.wide_w2b, r);
+      pnd::kstage_blocks(h, xb, NMat{}, nullptr, M, ob, false, false);
+      for (size_t b = 0; b < ob.size(); ++b) download_rows(h, ob[b], out, r, 32 * (int)b);
+    } else {
+      pnd::KStageArgs a{};
+      a.bcat = &h.bcat;
+      a.geo = h.g;
+      a.X = K;
+      a.M = M;
+      a.inv_s = h.isp.p + 2 * (size_t)h.g.halo;
+      a.out = O;
+      pnd::kstage(a, h.st);
+      download_rows(h, O, out, r, 0);
+    }
     CK(cudaStreamSynchronize(h.st));
     dm.free_();
   });
@@ -1025,7 +1053,7 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
 
 int pnd_state_random(pnd_handle* hh, int r, unsigned long long seed) {
   return guard(hh, [&](Handle& h) {
-    if (r < 1 || r > 32) pnd::fail(PND_ECONFIG, "random state rank must be 1..32");
+    if (r < 1 || r > 64) pnd::fail(PND_ECONFIG, "random state rank must be 1..64");
     const int m = h.m;
     // U = orth(random n x r) through the device Gram-Schmidt/SVQB passes
     NMat X = h.Xs.view(h.g, r, h.st);

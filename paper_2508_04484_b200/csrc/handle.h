@@ -55,6 +55,10 @@ struct Handle {
   int ct_K = 0, ct_P = 0, ct_nd = 0, ct_model = 0, ct_pn = 0, ct_bcorr = 0;
   double ct_fpscale = 0.0;
   bool have_ctab = false;
+  // ranks above 32 (wide.cu): 32-column block copies and chain workspaces
+  std::vector<NBuf> wide_u0b, wide_qb, wide_w1b, wide_w2b;
+  NBuf wide_base, wide_tmp[2];
+  DBuf wide_m, wide_t, wide_i, wide_g;
   // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
   std::vector<NBuf> fr_u, fr_w1, fr_w2;
   NBuf fr_t[2];
@@ -93,6 +97,15 @@ void set_isp(Handle& h);       // refresh the [1/S, 0] halo rows from inv_s
 // device-resident tables: no host->device copy per step (coeff.cu)
 void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo);
 
+// ranks above 32 (wide.cu): 32-column blocks of an n-side matrix, the
+// K-stage chained over blocks, the S-Grams over block pairs
+std::vector<NMat> block_views(Handle& h, std::vector<NBuf>& bufs, int cols);
+std::vector<NMat> split_blocks(Handle& h, NMat src, std::vector<NBuf>& bufs);
+void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double* S0,
+                   const double* M, const std::vector<NMat>& out, bool in_scaled,
+                   bool out_scaled);
+void stencil_grams_blocks(Handle& h, const std::vector<NMat>& B, const double* isp, double* G);
+
 // full-rank oracle on the device (fullrank.cu, fullrank.py:16-45)
 void fullrank_reset(Handle& h);                    // u = 0
 NMat fullrank_block(Handle& h, int b);             // columns [32 b, 32 b + 32)
@@ -112,6 +125,6 @@ double orth_defect(Handle& h, bool have_ugram = false);
 double* defect_gram_slot(Handle& h, int ru, int rv);
 // Q (k columns) = orthonormal basis of (I - U U^T) X; C1 = U^T X (device, ua x b; null
 // when U is empty). Returns k; the result is installed as the state's Q.
-int orth_complement(Handle& h, NMat X, const double* C1);
+int orth_complement(Handle& h, NMat X, const double* C1, NMat X2 = NMat{});
 
 }  // namespace pnd

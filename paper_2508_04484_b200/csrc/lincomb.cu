@@ -59,21 +59,22 @@ struct LIn {
   int stage;    // doubles per staging slot
   unsigned bytes;
   int ks;       // total k-steps
-  int ident;        // TA = I: out = Y1 - X TB, Y1 added to the accumulators
+  int ident;        // TA = I: out = [Y1 | Y2] - X TB; the number of Y inputs added
   const double* w;  // optional per-cell weight (Gram-only mode: T = diag(w) Y1)
   int woff;         // smem offset of the staged weights
 };
 
-template <int NB8>
+template <int NB8, int TBUF = 2>
 __global__ void __launch_bounds__(LTH, 2)
     lincomb_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
                    int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
-                   double* __restrict__ partial) {
+                   double* __restrict__ partial, int) {
+  constexpr int tb = TBUF;
   constexpr int TS = lpad4(NB8 * 8);            // out tile row length
   extern __shared__ __align__(128) double sm[];
   double* const sB = sm + nstg * in.stage;      // [ks][NB8][32] fragment order
-  double* const sT = sB + in.ks * NB8 * 32;     // 2 x [LCH][TS]
-  LBars* bars = reinterpret_cast<LBars*>(sT + 2 * LCH * TS);
+  double* const sT = sB + in.ks * NB8 * 32;     // tb x [LCH][TS] (tb = 1: 128 wide inputs)
+  LBars* bars = reinterpret_cast<LBars*>(sT + tb * LCH * TS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
   const int XT = (xcn + 7) / 8;                  // X^T out row tiles
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(LTH, 2)
     }
     sB[i] = v;
   }
-  for (int i = tid; i < 2 * LCH * TS; i += LTH) sT[i] = 0.0;
+  for (int i = tid; i < tb * LCH * TS; i += LTH) sT[i] = 0.0;
   __syncthreads();
   const int nchunks = (n + LCH - 1) / LCH;
 
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(LTH, 2)
     const long c0 = (long)chunk * LCH;
     mbar_wait(&bars->sfull[r.s], r.k & 1);
     const double* sb = sm + r.s * in.stage;
-    double* T = sT + (it & 1) * LCH * TS;
+    double* T = sT + (tb == 2 ? (it & 1) : 0) * LCH * TS;
     if (copy_y) {
       // Gram-only mode: out = Y1 (no contraction), parked for X^T Y1
       const double* y = sb + in.off[0];
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(LTH, 2)
 #pragma unroll
       for (int nt = 0; nt < NB8; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
     if (in.ident) {
-      // TA = I: start from the Y1 rows (accumulator layout: row m, columns 2 kq, 2 kq + 1)
+      // TA = I: start from the Y1 rows (accumulator layout: row m, columns
+      // 2 kq, 2 kq + 1), then Y2's after Y1's columns (two Y blocks)
       const double* y = sb + in.off[0] + (warp * 8 + m) * in.rs[0];
 #pragma unroll
       for (int nt = 0; nt < NB8; ++nt) {
@@ -170,8 +172,18 @@ __global__ void __launch_bounds__(LTH, 2)
         if (col < in.cols[0]) acc[0][nt][0] = y[col];
         if (col + 1 < in.cols[0]) acc[0][nt][1] = y[col + 1];
       }
+      if (in.ident == 2) {
+        const int c1 = in.cols[0], c2 = in.cols[1];
+        const double* y2 = sb + in.off[1] + (warp * 8 + m) * in.rs[1];
+#pragma unroll
+        for (int nt = 0; nt < NB8; ++nt) {
+          const int col = nt * 8 + 2 * kq;
+          if (col >= c1 && col < c1 + c2) acc[0][nt][0] = y2[col - c1];
+          if (col + 1 >= c1 && col + 1 < c1 + c2) acc[0][nt][1] = y2[col + 1 - c1];
+        }
+      }
     }
-    for (int q = in.ident ? 1 : 0; q < in.nin; ++q) {
+    for (int q = in.ident; q < in.nin; ++q) {
       const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
       const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
       int ks = k0;
@@ -228,6 +240,8 @@ __global__ void __launch_bounds__(LTH, 2)
           }
         }
       }
+      // one out tile: every warp is done reading it before the next chunk's writes
+      if constexpr (TBUF == 1) named_sync(1, 32 * LCW);
     }
     warp_arrive(&bars->sempty[r.s]);
   }
@@ -274,7 +288,7 @@ template <int NB8>
 __global__ void __launch_bounds__(LTH, 2)
     lincomb_pw_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
                       int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
-                      double* __restrict__ partial) {
+                      double* __restrict__ partial, int) {
   constexpr int TS = lpad4(NB8 * 8);            // out tile row length
   constexpr int NTT = NB8 * (NB8 + 1) / 2;      // upper-triangle out^T out tiles
   extern __shared__ __align__(128) double sm[];
@@ -513,9 +527,9 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   }
   if (!X.p || X.cols <= 0) in.xq = -1;
   if (same) in.xq = 0;
-  in.ident = (!gram_only && TA == nullptr) ? 1 : 0;
-  if (in.ident && (Y2.p || Y1.cols != out.cols))
-    fail(PND_ECONFIG, "lincomb: TA = I needs out = Y1 - X TB with matching columns");
+  in.ident = (!gram_only && TA == nullptr) ? (Y2.p && Y2.cols > 0 ? 2 : 1) : 0;
+  if (in.ident && Y1.cols + (Y2.p ? Y2.cols : 0) != out.cols)
+    fail(PND_ECONFIG, "lincomb: TA = I needs out = [Y1 | Y2] - X TB with matching columns");
   if (weight) {
     in.w = weight;
     in.woff = o;
@@ -530,8 +544,9 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   // per-warp Grams (lincomb_pw_kernel) while the registers allow
   constexpr bool PWOK = NB8 <= 3;
   const bool PW = PWOK && gram_only;
-  const size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
-  const size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
+  int tb = 2;  // out-tile buffers
+  size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
+  size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
   // two CTAs per SM: keep the whole CTA under ~113 KB
   const size_t cap = 113 * 1024;
   int nstg = 0;
@@ -539,11 +554,18 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
     ++nstg;
   if (nstg < 2) {
     nstg = 2;
-    if (fixed + 2 * (size_t)in.stage * sizeof(double) > 227 * 1024)
+    if (!PW && fixed + 2 * (size_t)in.stage * sizeof(double) > (size_t)kMaxDynSmem) {
+      // 128 input columns x 64 outputs: one out tile (a barrier per chunk)
+      tb = 1;
+      tile = (size_t)LCH * TS;
+      fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
+    }
+    if (fixed + 2 * (size_t)in.stage * sizeof(double) > (size_t)kMaxDynSmem)
       fail(PND_ECONFIG, "lincomb tile exceeds shared memory");
   }
   const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
   auto kern = lincomb_kernel<NB8>;
+  if (tb == 1) kern = lincomb_kernel<NB8, 1>;
   if constexpr (PWOK) {
     if (PW) kern = lincomb_pw_kernel<NB8>;
   }
@@ -559,7 +581,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   const int nparts = PW ? grid * LCW : grid;  // per-warp or per-CTA partials
   double* part = grams ? partial.get(count * nparts) : nullptr;
   kern<<<grid, LTH, smem, st>>>(g.n, in, TA, TB, ny, nb, out, nstg, grams ? 1 : 0,
-                                gram_only ? 1 : 0, gram_only ? 1 : 0, part);
+                                gram_only ? 1 : 0, gram_only ? 1 : 0, part, tb);
   launched();
   if (grams) {
     lreduce<<<(int)((count + 31) / 32), dim3(32, 8), 0, st>>>(part, nparts, (int)count, grams);

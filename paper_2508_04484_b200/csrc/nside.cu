@@ -147,6 +147,7 @@ void pgram_launch(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
 // per class and beam, in shared memory). One warp per 32 cells: the lanes
 // load the cells' class and 1/S once, then write one row (rs <= 32 doubles)
 // per store instruction.
+template <bool WIDE>  // WIDE: rows of up to 64 doubles (ranks above 32)
 __global__ void scat_dk_kernel(Geom g, double dt, const double* __restrict__ inv_s,
                                const int* __restrict__ cls, const double* __restrict__ atomic,
                                int n_cls, const double* __restrict__ psi, int n_beams,
@@ -183,6 +184,18 @@ __global__ void scat_dk_kernel(Geom g, double dt, const double* __restrict__ inv
         }
       }
       if (lane < rs) out.p[(size_t)(c0 + q) * rs + lane] = v;
+      // columns 32..63 (ranks above 32)
+      if (WIDE) {
+        double v2 = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (b < n_beams) {
+            const double s = __shfl_sync(0xffffffffu, sp[b], q);
+            if (lane + 32 < r) v2 = fma(s, sT[(kr * nb + b) * r + lane + 32], v2);
+          }
+        }
+        if (lane + 32 < rs) out.p[(size_t)(c0 + q) * rs + lane + 32] = v2;
+      }
     }
   }
 }
@@ -356,11 +369,15 @@ void pgram(const PGramArgs& a, DBuf& partial, cudaStream_t st) {
 void scat_dk(const Geom& g, double dt, const double* inv_s, const int* cls,
              const double* cls_atomic, int n_cls, const double* psi, int n_beams,
              const double* rows, NMat out, cudaStream_t st) {
-  if (out.rs > 32) fail(PND_ECONFIG, "scattering increment supports rank <= 32");
+  if (out.rs > 64) fail(PND_ECONFIG, "scattering increment supports rank <= 64");
   const size_t smem = (size_t)n_cls * (n_beams > 0 ? n_beams : 1) * out.cols * sizeof(double);
   if (smem > 48 * 1024) fail(PND_ECONFIG, "scattering increment: too many material classes");
-  scat_dk_kernel<<<sm_count() * 8, 256, smem, st>>>(g, dt, inv_s, cls, cls_atomic, n_cls, psi,
-                                                    n_beams, rows, out);
+  if (out.rs > 32)
+    scat_dk_kernel<true><<<sm_count() * 8, 256, smem, st>>>(g, dt, inv_s, cls, cls_atomic, n_cls,
+                                                            psi, n_beams, rows, out);
+  else
+    scat_dk_kernel<false><<<sm_count() * 8, 256, smem, st>>>(g, dt, inv_s, cls, cls_atomic, n_cls,
+                                                             psi, n_beams, rows, out);
   launched();
 }
 

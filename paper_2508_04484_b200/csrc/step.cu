@@ -174,8 +174,8 @@ void consolidate(Handle& h) {
   h.uq = 0;
 }
 
-int orth_complement(Handle& h, NMat X, const double* C1) {
-  const int a = h.ua, b = X.cols;
+int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
+  const int a = h.ua, b = X.cols + (X2.p ? X2.cols : 0);
   cudaStream_t st = h.st;
   const Geom& g = h.g;
   NMat U0 = a > 0 ? state_u(h) : NMat{};
@@ -189,7 +189,7 @@ int orth_complement(Handle& h, NMat X, const double* C1) {
   double* dinfo = slot(h, S_TAIL, 4);
   // pass 2: Y = X - U0 C1 -> Qa, C2 = U0^T Y, G2 = Y^T Y
   NMat Y = h.Qa.view(g, b, st);
-  lincomb(g, X, NMat{}, U0, nullptr, C1, Y, grams, h.part, st);
+  lincomb(g, X, X2, U0, nullptr, C1, Y, grams, h.part, st);
   double* C2 = grams;                  // a x b
   double* G2 = grams + (size_t)a * b;  // b x b
   if (a > 0) gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
@@ -235,11 +235,19 @@ void streaming_step(Handle& h, double dt) {
   const int m = h.m, ns = g.ns;
   const int a = h.ua, b = h.rv;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
-  if (b > 32 || a > 32) fail(PND_ECONFIG, "streaming step supports rank <= 32");
+  if (b > 64 || a > 64) fail(PND_ECONFIG, "streaming step supports rank <= 64");
   cudaStream_t st = h.st;
   const NMat U0 = state_u(h);
   const double* isp = isp_rows(h);
   comm_halo_rows(g, U0.p, U0.rs, st);  // U0's neighbour planes (K stage 0, L- and S-Grams)
+  // ranks above 32: the stencil kernels run on 32-column blocks (wide.cu)
+  const bool wide = a > 32 || b > 32;
+  std::vector<NMat> u0b, w1b, w2b;
+  if (wide) {
+    u0b = split_blocks(h, U0, h.wide_u0b);
+    w1b = block_views(h, h.wide_w1b, b);
+    w2b = block_views(h, h.wide_w2b, b);
+  }
 
   // --- K phase: K1 = K0 + dK, K' = -sum_s (D_s S^-1 K) F_s(V0), K0 = U0 S0
   phase(h, PH_LSIDE);
@@ -274,19 +282,31 @@ void streaming_step(Handle& h, double dt) {
     ka.in_scaled = stage > 0;
     ka.out_scaled = stage < 3;
     phase(h, PH_KSTAGE);
-    if (stage > 0) comm_halo_rows(g, ka.X.p, ka.X.rs, st);  // the previous stage's output
-    kstage(ka, st);
+    if (wide) {
+      const std::vector<NMat>& xin = stage == 0 ? u0b : stage == 2 ? w2b : w1b;
+      if (stage > 0)
+        for (const NMat& x : xin) comm_halo_rows(g, x.p, x.rs, st);
+      // the same buffer rotation as below: U0 -> W1 -> W2 -> W1 -> W2
+      kstage_blocks(h, xin, ka.U0, h.S.p, M, stage == 0 || stage == 2 ? w1b : w2b,
+                    ka.in_scaled, ka.out_scaled);
+    } else {
+      if (stage > 0) comm_halo_rows(g, ka.X.p, ka.X.rs, st);  // the previous stage's output
+      kstage(ka, st);
+    }
     phase(h, PH_LSIDE);
   }
-  const NMat dK = W2;
+  // dK = W2 (one matrix, or its <= 2 column blocks at ranks above 32)
+  const NMat dK = wide ? w2b[0] : W2;
+  const NMat dK2 = wide && w2b.size() > 1 ? w2b[1] : NMat{};
 
   double* C1 = slot(h, S_C1, (size_t)a * b);
   phase(h, PH_LGRAM);
-  gram_xy(g, U0, dK, C1, h.part, st);  // C1 = U0^T dK
+  if (dK2.p) gram_xy2(g, U0, dK, dK2, C1, h.part, st);  // C1 = U0^T dK
+  else gram_xy(g, U0, dK, C1, h.part, st);
 
   // --- U augmentation: U^ = [U0 | orth((I - U0 U0^T) dK)]
   phase(h, PH_ORTH);
-  const int k = orth_complement(h, dK, C1);
+  const int k = orth_complement(h, dK, C1, dK2);
   const int ru = a + k;
 
   // --- S-phase Grams G_s = U^T D_s S^-1 U^ (dlra.py:199-209). Their leading
@@ -296,7 +316,14 @@ void streaming_step(Handle& h, double dt) {
   double* G = slot(h, S_G, (size_t)ns * ru * ru);
   phase(h, PH_SGRAM);
   if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
-  stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
+  if (ru > 64 || wide) {
+    std::vector<NMat> blocks = u0b.empty() ? split_blocks(h, U0, h.wide_u0b) : u0b;
+    if (k > 0)
+      for (const NMat& q : split_blocks(h, state_q(h), h.wide_qb)) blocks.push_back(q);
+    stencil_grams_blocks(h, blocks, isp, G);
+  } else {
+    stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);
+  }
 
   // --- L phase: L' = -sum_s A_s L Q_s, Q_s^T = G_s[:a, :a], L0 = V0 S0^T
   phase(h, PH_LSIDE);
@@ -368,6 +395,17 @@ __global__ void coeff_kernel(const double* g, const double* sig, int m, double* 
 
 __global__ void init_int(int* p, int v) { *p = v; }
 
+// per-cell weight of Gram i: [cls == i] / S (phase < 0) or wtab[cls][phase] / S;
+// zero past n (the chunked staging reads up to 64 rows beyond)
+__global__ void class_weight_kernel(const int* cls, const double* wtab, const double* inv_s, int n,
+                                    int phase, int cl, double* w) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n + 64; c += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (c < n) v = inv_s[c] * (phase < 0 ? (cls[c] == cl ? 1.0 : 0.0) : wtab[cls[c] * 12 + phase]);
+    w[c] = v;
+  }
+}
+
 }  // namespace
 
 void scattering_step(Handle& h, double dt) {
@@ -381,7 +419,7 @@ void scattering_step(Handle& h, double dt) {
   const int B = h.n_beams;
   cudaStream_t st = h.st;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
-  if (a > 32 || b > 32) fail(PND_ECONFIG, "scattering step supports rank <= 32");
+  if (a > 64 || b > 64) fail(PND_ECONFIG, "scattering step supports rank <= 64");
   const NMat U0 = state_u(h);
 
   // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
@@ -426,13 +464,29 @@ void scattering_step(Handle& h, double dt) {
   if (rank1) {
     // [H | u] = U0^T diag(1/S) [U0 | psi]; left = U0^T Z = u N^T
     double* Hu = slot(h, S_HU, (size_t)a * (a + 1));
-    gram_xy2(g, U0, U0, psi_col, Hu, h.part, st, h.inv_s.p);
-    CK(cudaMemcpy2DAsync(H, a * sizeof(double), Hu, (a + 1) * sizeof(double), a * sizeof(double),
-                         a, cudaMemcpyDeviceToDevice, st));
-    gemm(a, 12, 1, 1.0, Mat{Hu + a, a + 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0,
-         rowm(left, 12), 0, 1, st);
+    if (a + 1 <= 64) {
+      gram_xy2(g, U0, U0, psi_col, Hu, h.part, st, h.inv_s.p);
+      CK(cudaMemcpy2DAsync(H, a * sizeof(double), Hu, (a + 1) * sizeof(double),
+                           a * sizeof(double), a, cudaMemcpyDeviceToDevice, st));
+      gemm(a, 12, 1, 1.0, Mat{Hu + a, a + 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0,
+           rowm(left, 12), 0, 1, st);
+    } else {  // 64 columns: the Gram-only pass takes at most 64
+      gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);
+      gram_xy(g, U0, psi_col, Hu, h.part, st, h.inv_s.p);
+      gemm(a, 12, 1, 1.0, Mat{Hu, 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0, rowm(left, 12), 0,
+           1, st);
+    }
   } else if (h.n_cls == 1) {
     gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);  // one class: U0^T diag(1/S) U0
+  } else if (a > 32) {
+    // ranks above 32: one weighted Gram-only pass per class / phase
+    double* wv = h.wide_t.get((size_t)g.ld + 64);
+    for (int i = 0; i < nw; ++i) {
+      class_weight_kernel<<<148 * 8, 256, 0, st>>>(h.cls.p, h.cls_atomic.p, h.inv_s.p, g.n,
+                                                   h.n_cls <= 12 ? -1 : i, i, wv);
+      launched();
+      gram_xy(g, U0, U0, H + (size_t)i * a * a, h.part, st, wv);
+    }
   } else {
     PGramArgs pa{};
     pa.geo = g;

@@ -330,11 +330,12 @@ def test_end_to_end_dose(tag):
 
 
 # ------------------------------------------------------------------ larger ranks
-@pytest.mark.parametrize("r", [24, 30, 32])
+@pytest.mark.parametrize("r", [24, 30, 32, 40, 48, 64])
 def test_streaming_step_large_rank_vs_oracle(dl, r):
-    """Ranks above the bench's 20 (16-cell K-stage chunks, 8-cell Gram chunks):
-    a streaming step + truncation against the numpy oracle (pinned to the
-    reference by test_oracle.py), T2 tolerances."""
+    """Ranks above the bench's 20 (16-cell K-stage chunks, 8-cell Gram chunks;
+    above 32 the 32-column block chains of wide.cu): a streaming step +
+    truncation against the numpy oracle (pinned to the reference by
+    test_oracle.py), T2 tolerances."""
     from oracle import dlra_np
     from paper_2508_04484_b200.angular import PNOperators
 
@@ -358,3 +359,65 @@ def test_streaming_step_large_rank_vs_oracle(dl, r):
     tr, _ = dl.truncate(aug, dl.TruncationPolicy(1e300, r, r))
     _, ts, _, _ = dlra_np.truncate(ou, os_, ov, 1e300, r, r)
     np.testing.assert_allclose(np.diag(tr.s), np.diag(ts), rtol=1e-9)
+
+
+@pytest.mark.parametrize("r,hetero", [(40, False), (48, True), (64, False)])
+def test_scattering_step_wide_rank_vs_oracle(dl, r, hetero):
+    """Ranks above 32 in the scattering step (one class: the rank-one source
+    path; several classes and two beams: the source-row path with per-class
+    Gram passes) against the numpy oracle, T2 tolerances."""
+    from oracle import dlra_np
+
+    rng = np.random.default_rng(r)
+    n, m = 700, 81
+    if hetero:
+        cls = rng.integers(0, 3, n)
+        weights = (np.abs(rng.standard_normal((3, 12))) * 1e22)[cls]
+        n_src = 2
+    else:
+        weights = np.tile(np.abs(rng.standard_normal(12)), (n, 1)) * 1e22
+        n_src = 1
+    g_diags = np.abs(rng.standard_normal((12, m))) * 1e-28
+    sigma_t = g_diags[:, 0] + np.abs(rng.standard_normal(12)) * 1e-28
+    inv_s = 1.0 / rng.uniform(8.0, 20.0, n)
+    sources = [(np.abs(rng.standard_normal(n)), rng.standard_normal(m)) for _ in range(n_src)]
+    u0 = np.linalg.qr(rng.standard_normal((n, r)))[0]
+    v0 = np.linalg.qr(rng.standard_normal((m, r)))[0]
+    s0 = np.diag(np.logspace(0, -1, r)) + 0.05 * rng.standard_normal((r, r))
+    ctx = dl.ScatteringContext(weights, inv_s, g_diags, sigma_t, sources)
+    aug = dl.scattering_step(dl.LowRankState(u0, s0, v0), 0.3, ctx)
+    ou, os_, ov = dlra_np.scattering_step(u0, s0, v0, 0.3, weights, inv_s, g_diags, sigma_t,
+                                          sources)
+    assert aug.orthonormality_defect() < 1e-12
+    assert rel(aug.matrix(), ou @ os_ @ ov.T) < 1e-11
+
+
+@pytest.mark.parametrize("r", [40, 64])
+def test_wide_k_rhs_and_stencil_grams_vs_oracle(dl, r):
+    """The block chains of wide.cu in isolation: K' = -sum_s (D_s S^-1 K) F_s
+    and the stencil Grams X^T D_s S^-1 Y for more than 32 / 64 columns,
+    against the numpy oracle's stencils (T1 tolerance)."""
+    from oracle import dlra_np
+    from paper_2508_04484_b200.angular import PNOperators
+
+    ops = PNOperators.build(7)
+    nx, ny, nz = 7, 6, 9
+    n = nx * ny * nz
+    rng = np.random.default_rng(r + 1)
+    grid = dlra_np.Grid(nx, ny, nz, 0.1, 0.12, 0.09)
+    inv_s = 1.0 / rng.uniform(5.0, 12.0, n)
+    ctx = dl.StreamingContext(inv_s, SimpleNamespace(grid=SimpleNamespace(
+        nx=nx, ny=ny, nz=nz, dx=0.1, dy=0.12, dz=0.09)), ops)
+    k = rng.standard_normal((n, r))
+    fac = [(rng.standard_normal((r, r)), rng.standard_normal((r, r))) for _ in range(3)]
+    got = ctx.k_rhs(k, fac)
+    want = np.zeros_like(k)
+    for i, (axis, sign) in enumerate(grid.stencils()):
+        want -= dlra_np.stencil(grid, axis, sign, inv_s[:, None] * k) @ fac[axis][0 if sign > 0 else 1]
+    assert relmax(got, want) < 1e-12
+    x = rng.standard_normal((n, r))
+    y = rng.standard_normal((n, r))
+    got_g = ctx.stencil_grams(x, y)
+    for i, (axis, sign) in enumerate(grid.stencils()):
+        ref = x.T @ dlra_np.stencil(grid, axis, sign, inv_s[:, None] * y)
+        assert relmax(got_g[i], ref) < 1e-12
