@@ -23,7 +23,7 @@ smax = 0.0
 for k in range(min(steps, len(edges) - 1)):
     e_hi, e_lo = edges[k], edges[k + 1]
     b.truncation_tolerance = max(rel * smax, 1e-300)
-    b.rank_min, b.rank_max = 2, 32
+    b.rank_min, b.rank_max = 2, int(sys.argv[4]) if len(sys.argv) > 4 else 64
     s.set_coefficients(e_hi, e_lo)
     out = s.step(e_hi - e_lo, want_defect=False)
     r = int(out[2])
