@@ -686,7 +686,11 @@ int pnd_k_rhs(pnd_handle* hh, const double* k, int r, const double* f, double* o
       const auto xb = pnd::split_blocks(h, K, h.wide_w1b);
       const auto ob = pnd::block_views(h, h.wide_w2b, r);
       pnd::kstage_blocks(h, xb, NMat{}, nullptr, M, ob, false, false);
-      for (size_t b = 0; b < ob.size(); ++b) download_rows(h, ob[b], out, r, 32 * (int)b);
+      int c0 = 0;
+      for (size_t b = 0; b < ob.size(); ++b) {
+        download_rows(h, ob[b], out, r, c0);
+        c0 += ob[b].cols;
+      }
     } else {
       pnd::KStageArgs a{};
       a.bcat = &h.bcat;

@@ -63,20 +63,29 @@ int grid_n(long n) {
 
 }  // namespace
 
-std::vector<NMat> block_views(Handle& h, std::vector<NBuf>& bufs, int cols) {
+// ceil(cols / 32) blocks of balanced width (40 -> 20 + 20: the kernels' tiles
+// are fuller than with 32 + 8)
+int block_width(int cols) {
   const int nb = (cols + WB - 1) / WB;
+  return (cols + nb - 1) / nb;
+}
+
+std::vector<NMat> block_views(Handle& h, std::vector<NBuf>& bufs, int cols) {
+  const int bw = block_width(cols), nb = (cols + bw - 1) / bw;
   if ((int)bufs.size() < nb) bufs.resize(nb);
   std::vector<NMat> v;
-  for (int b = 0; b < nb; ++b) v.push_back(bufs[b].view(h.g, b + 1 < nb ? WB : cols - WB * b, h.st));
+  for (int b = 0; b < nb; ++b) v.push_back(bufs[b].view(h.g, b + 1 < nb ? bw : cols - bw * b, h.st));
   return v;
 }
 
 std::vector<NMat> split_blocks(Handle& h, NMat src, std::vector<NBuf>& bufs) {
   std::vector<NMat> v = block_views(h, bufs, src.cols);
+  int c0 = 0;
   for (size_t b = 0; b < v.size(); ++b) {
-    split_kernel<<<grid_n((long)h.g.n * v[b].rs), 256, 0, h.st>>>(src, WB * (int)b, v[b], h.g.n);
+    split_kernel<<<grid_n((long)h.g.n * v[b].rs), 256, 0, h.st>>>(src, c0, v[b], h.g.n);
     launched();
     comm_halo_rows(h.g, v[b].p, v[b].rs, h.st);  // slab faces of the copy
+    c0 += v[b].cols;
   }
   return v;
 }
@@ -94,8 +103,9 @@ void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double*
   double* Ms = h.wide_m.get((size_t)ns * WB * WB + 1);
   double* Ts = h.wide_t.get((size_t)(a > 0 ? a : 1) * WB + 1);
   double* I = h.wide_i.get((size_t)WB * WB);
-  for (size_t ob = 0; ob < out.size(); ++ob) {
-    const int bo = out[ob].cols, o0 = WB * (int)ob;
+  int o0 = 0;
+  for (size_t ob = 0; ob < out.size(); o0 += out[ob].cols, ++ob) {
+    const int bo = out[ob].cols;
     eye_b_kernel<<<1, 256, 0, st>>>(I, bo);  // S0 of the chained partial sums
     launched();
     NMat base{};
@@ -106,9 +116,10 @@ void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double*
       base = h.wide_base.view(g, bo, st);
       lincomb(g, U0, NMat{}, NMat{}, Ts, nullptr, base, nullptr, h.part, st);
     }
-    for (size_t xb = 0; xb < X.size(); ++xb) {
+    int x0 = 0;
+    for (size_t xb = 0; xb < X.size(); x0 += X[xb].cols, ++xb) {
       const bool last = xb + 1 == X.size();
-      msub_kernel<<<64, 256, 0, st>>>(M, ns, xc, b, WB * (int)xb, X[xb].cols, o0, bo, Ms);
+      msub_kernel<<<64, 256, 0, st>>>(M, ns, xc, b, x0, X[xb].cols, o0, bo, Ms);
       launched();
       KStageArgs ka{};
       ka.bcat = &h.bcat;
