@@ -217,12 +217,13 @@ __global__ void __launch_bounds__(1024, 1)
   const bool tall = p >= q;
   const int M = tall ? p : q, N = tall ? q : p;
   const int N2 = N + (N & 1);
-  // gw: A, V and U in a global (L2-resident) work buffer when they do not fit
-  // in shared memory (the wide R x R case); sg and perm stay in shared memory
-  double* A = gw ? gw : sm;        // column-major M x N2
-  double* Vm = A + M * N2;         // column-major N2 x N2
+  // gw: V and U in a global (L2-resident) work buffer when they do not fit in
+  // shared memory (the wide R x R case); A (the dot products of every round),
+  // sg and perm stay in shared memory
+  double* A = sm;                  // column-major M x N2
+  double* Vm = gw ? gw : A + M * N2;       // column-major N2 x N2
   double* U = Vm + N2 * N2;        // column-major M x N (sorted, completed)
-  double* sg = gw ? sm : U + M * N;  // N2
+  double* sg = gw ? A + M * N2 : U + M * N;  // N2
   int* perm = (int*)(sg + N2);     // N
   __shared__ int rotated;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -818,9 +819,11 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   size_t sm = (mats + N2) * sizeof(double) + N * sizeof(int);
   double* gw = nullptr;
   if (sm + 1024 > (size_t)kMaxDynSmem) {
-    // wide R x R: A, V, U in a global (L2-resident) work buffer, stream-ordered
-    CK(cudaMallocAsync((void**)&gw, mats * sizeof(double), st));
-    sm = N2 * sizeof(double) + N * sizeof(int);
+    // wide R x R: V and U in a global (L2-resident) work buffer, stream-ordered
+    const size_t vu = (size_t)N2 * N2 + (size_t)M * N;
+    CK(cudaMallocAsync((void**)&gw, vu * sizeof(double), st));
+    sm = ((size_t)M * N2 + N2) * sizeof(double) + N * sizeof(int);
+    if (sm + 1024 > (size_t)kMaxDynSmem) fail(PND_ECONFIG, "truncation SVD too large");
   }
   // one warp per Jacobi pair of a round (two per warp above 64 columns)
   int threads = 32 * (N2 / 2);
