@@ -56,7 +56,7 @@ struct Handle {
   double ct_fpscale = 0.0;
   bool have_ctab = false;
   // ranks above 32 (wide.cu): 32-column block copies and chain workspaces
-  std::vector<NBuf> wide_u0b, wide_qb, wide_w1b, wide_w2b;
+  std::vector<NBuf> wide_u0b, wide_qb, wide_w1b, wide_w2b, wide_gb;
   NBuf wide_base, wide_tmp[2];
   DBuf wide_m, wide_t, wide_i, wide_g;
   // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
@@ -101,6 +101,8 @@ void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo);
 // K-stage chained over blocks, the S-Grams over block pairs
 std::vector<NMat> block_views(Handle& h, std::vector<NBuf>& bufs, int cols);
 std::vector<NMat> split_blocks(Handle& h, NMat src, std::vector<NBuf>& bufs);
+// balanced blocks of <= maxw columns of [X1 | X2] (the S-Gram pairs)
+std::vector<NMat> split_joint(Handle& h, NMat X1, NMat X2, int maxw, std::vector<NBuf>& bufs);
 void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double* S0,
                    const double* M, const std::vector<NMat>& out, bool in_scaled,
                    bool out_scaled);

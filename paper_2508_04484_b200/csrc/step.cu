@@ -317,9 +317,10 @@ void streaming_step(Handle& h, double dt) {
   phase(h, PH_SGRAM);
   if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
   if (ru > 64 || wide) {
-    std::vector<NMat> blocks = u0b.empty() ? split_blocks(h, U0, h.wide_u0b) : u0b;
-    if (k > 0)
-      for (const NMat& q : split_blocks(h, state_q(h), h.wide_qb)) blocks.push_back(q);
+    // [U0 | Q] in balanced blocks of <= 20 columns: every pair is a <= 40-column
+    // S-Gram launch, the kernel's best-tuned width
+    const std::vector<NMat> blocks =
+        split_joint(h, U0, k > 0 ? state_q(h) : NMat{}, 20, h.wide_gb);
     stencil_grams_blocks(h, blocks, isp, G);
   } else {
     stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);

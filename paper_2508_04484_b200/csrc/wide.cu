@@ -29,6 +29,19 @@ __global__ void split_kernel(NMat src, int c0, NMat dst, int n) {
   }
 }
 
+// dst = columns [c0, c0 + dst.cols) of [X1 | X2]
+__global__ void split2_kernel(NMat x1, NMat x2, int c0, NMat dst, int n) {
+  const long total = (long)n * dst.rs;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const long c = e / dst.rs;
+    const int j = (int)(e - c * dst.rs), gc = c0 + j;
+    double v = 0.0;
+    if (j < dst.cols) v = gc < x1.cols ? x1.p[c * x1.rs + gc] : x2.p[c * x2.rs + gc - x1.cols];
+    dst.p[e] = v;
+  }
+}
+
 // M (ns x rows x ld, row-major) -> sub (ns x bx x bo): rows x0.., columns o0..
 __global__ void msub_kernel(const double* __restrict__ M, int ns, int rows, int ld, int x0, int bx,
                             int o0, int bo, double* __restrict__ out) {
@@ -86,6 +99,21 @@ std::vector<NMat> split_blocks(Handle& h, NMat src, std::vector<NBuf>& bufs) {
     launched();
     comm_halo_rows(h.g, v[b].p, v[b].rs, h.st);  // slab faces of the copy
     c0 += v[b].cols;
+  }
+  return v;
+}
+
+std::vector<NMat> split_joint(Handle& h, NMat X1, NMat X2, int maxw, std::vector<NBuf>& bufs) {
+  const int cols = X1.cols + (X2.p ? X2.cols : 0);
+  const int nb = (cols + maxw - 1) / maxw, bw = (cols + nb - 1) / nb;
+  if ((int)bufs.size() < nb) bufs.resize(nb);
+  std::vector<NMat> v;
+  for (int b = 0, c0 = 0; b < nb; ++b, c0 += bw) {
+    const NMat d = bufs[b].view(h.g, b + 1 < nb ? bw : cols - bw * b, h.st);
+    split2_kernel<<<grid_n((long)h.g.n * d.rs), 256, 0, h.st>>>(X1, X2.p ? X2 : X1, c0, d, h.g.n);
+    launched();
+    comm_halo_rows(h.g, d.p, d.rs, h.st);
+    v.push_back(d);
   }
   return v;
 }
