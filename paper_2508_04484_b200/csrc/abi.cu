@@ -196,6 +196,9 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     if (n + 2 * halo >= (1LL << 31) - 1024) pnd::fail(PND_ECONFIG, "grid exceeds 2^31 cells per device");
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&h.st2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
     CK(cudaMallocHost(&h.pinned, 64 * sizeof(double)));
     pnd::Geom& g = h.g;
     g.nx = nx;
@@ -250,6 +253,9 @@ int pnd_destroy(pnd_handle* hh) {
     if (e) cudaEventDestroy(e);
   if (h.pinned) cudaFreeHost(h.pinned);
   if (h.st) cudaStreamDestroy(h.st);
+  if (h.st2) cudaStreamDestroy(h.st2);
+  if (h.ev_fork) cudaEventDestroy(h.ev_fork);
+  if (h.ev_join) cudaEventDestroy(h.ev_join);
   delete hh;
   return PND_OK;
 }

@@ -24,6 +24,8 @@ struct TimerState {
 struct Handle {
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;       // side stream: independent passes overlapped with st
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Geom g{};
   int m = 0;
   std::string err;

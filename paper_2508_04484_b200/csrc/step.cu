@@ -445,8 +445,15 @@ void scattering_step(Handle& h, double dt) {
   const NMat dK = h.W2.view(g, b, st);
   phase(h, PH_SCATK1);
   NMat Z{};
+  bool forked = false;
   if (rank1) {
-    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, 1, h.psi.p, 1, rows, dK, st);
+    // dK (memory-bound, on the side stream) overlaps the B_0 / projection Gram
+    // pass below (reads only U0 and psi); joined before dK is used
+    CK(cudaEventRecord(h.ev_fork, st));
+    CK(cudaStreamWaitEvent(h.st2, h.ev_fork, 0));
+    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, 1, h.psi.p, 1, rows, dK, h.st2);
+    CK(cudaEventRecord(h.ev_join, h.st2));
+    forked = true;
   } else if (B > 0) {
     Z = h.Xs.view(g, 12 * B, st);
     source_rows(g, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.psi.p, B, Z, st);
@@ -552,6 +559,7 @@ void scattering_step(Handle& h, double dt) {
 
   // substep 2: U^ = [U0 | orth((I - U0 U0^T) dK)]
   phase(h, PH_ORTH);
+  if (forked) CK(cudaStreamWaitEvent(st, h.ev_join, 0));  // dK from the side stream
   const int k = orth_complement(h, dK, C1);
   const int ru = a + k;
   phase(h, PH_SCATSMALL);
