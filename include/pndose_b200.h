@@ -126,6 +126,12 @@ int pnd_step(pnd_handle* h, double dt, double theta, int rank_min, int rank_max,
 int pnd_dose_reset(pnd_handle* h);
 int pnd_dose_accumulate(pnd_handle* h, double dt, int tally_steps);
 int pnd_get_dose(pnd_handle* h, double* deposited);
+/* Checkpoint / resume at a step boundary (a LowRankState
+ * snapshot plus the dose trapezoid's running sum and previous integrand,
+ * driver.py:613-621): read and restore the tally (n values each); the
+ * factors go through pnd_state_get / pnd_state_set. */
+int pnd_dose_state(pnd_handle* h, double* deposited, double* prev);
+int pnd_dose_restore(pnd_handle* h, const double* deposited, const double* prev);
 /* LowRankState.orthonormality_defect() (dlra.py:67-70) on the device state. */
 int pnd_orth_defect(pnd_handle* h, double* defect);
 

@@ -44,6 +44,8 @@ SIGNATURES = {
     "pnd_dose_reset": [_P],
     "pnd_dose_accumulate": [_P, _D, _I],
     "pnd_get_dose": [_P, _P],
+    "pnd_dose_state": [_P, _P, _P],
+    "pnd_dose_restore": [_P, _P, _P],
     "pnd_orth_defect": [_P, _P],
     "pnd_apply_streaming": [_P, _P, _P],
     "pnd_stencil_grams": [_P, _P, _I, _P, _I, _P],

@@ -9,6 +9,8 @@
 #include <stdexcept>
 
 #include "../../include/pndose_b200.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "handle.h"
 
 namespace pnd {
@@ -83,6 +85,13 @@ int sm_count() {
 }
 
 void phase(Handle& h, int id) {
+  // NVTX ranges per phase (no-ops unless a profiler is attached)
+  static const char* const names[PH_COUNT] = {
+      "kstage", "l_gram", "l_side", "tsqr_n", "tsqr_m", "s_gram", "s_rk4",
+      "svd", "rotate", "scat_k1", "scat_gram", "scat_small", "dose", "defect"};
+  if (h.nvtx_open) nvtxRangePop();
+  h.nvtx_open = id >= 0 && id < PH_COUNT;
+  if (h.nvtx_open) nvtxRangePushA(names[id]);
   TimerState& t = h.timer;
   if (!t.on) return;
   if (t.used == t.pool.size()) {
@@ -552,6 +561,24 @@ int pnd_dose_reset(pnd_handle* hh) {
 
 int pnd_dose_accumulate(pnd_handle* hh, double dt, int tally_steps) {
   return guard(hh, [&](Handle& h) { pnd::dose_accumulate_step(h, dt, tally_steps != 0); });
+}
+
+int pnd_dose_state(pnd_handle* hh, double* deposited, double* prev) {
+  return guard(hh, [&](Handle& h) {
+    if (deposited) down(deposited, h.dep.get(h.g.ld), h.g.n, h.st);
+    if (prev) down(prev, h.prev.get(h.g.ld), h.g.n, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
+}
+
+int pnd_dose_restore(pnd_handle* hh, const double* deposited, const double* prev) {
+  return guard(hh, [&](Handle& h) {
+    pnd::fill_zero(h.dep.get(h.g.ld), h.g.ld, h.st);
+    pnd::fill_zero(h.prev.get(h.g.ld), h.g.ld, h.st);
+    up(h.dep.p, deposited, h.g.n, h.st);
+    up(h.prev.p, prev, h.g.n, h.st);
+    CK(cudaStreamSynchronize(h.st));
+  });
 }
 
 int pnd_get_dose(pnd_handle* hh, double* deposited) {

@@ -84,6 +84,7 @@ struct Handle {
   double* pinned = nullptr;   // small pinned readback buffer
   Comm* comm = nullptr;       // z-slab communicator (multi-GPU), null on one device
   TimerState timer;
+  bool nvtx_open = false;  // an NVTX phase range is open
 };
 
 // phase mark: when timing is on, records an event on the handle's stream;

@@ -148,6 +148,23 @@ class DeviceSolver:
         )
         return out
 
+    def checkpoint(self, step: int) -> dict:
+        """Snapshot at a step boundary: the factors, the dose
+        trapezoid state and the next step index; np.savez-able."""
+        u, s_, v = self.state()
+        n = self.rows[1] - self.rows[0]
+        dep, prev = np.empty(n), np.empty(n)
+        self.h.call("pnd_dose_state", _lib.ptr(dep), _lib.ptr(prev))
+        return {"u": u, "s": s_, "v": v, "deposited": dep, "prev": prev,
+                "step": np.array(int(step))}
+
+    def restore(self, ckpt) -> int:
+        """Resume from checkpoint(): returns the step to continue from."""
+        self.h.set_state(ckpt["u"], ckpt["s"], ckpt["v"])
+        dep, prev = _lib.f64(ckpt["deposited"]), _lib.f64(ckpt["prev"])
+        self.h.call("pnd_dose_restore", _lib.ptr(dep), _lib.ptr(prev))
+        return int(ckpt["step"])
+
     def dose(self) -> np.ndarray:
         """Deposited energy of this device's cells (the slab's rows)."""
         out = np.empty(self.rows[1] - self.rows[0])
@@ -162,11 +179,15 @@ class DeviceSolver:
 
 
 def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0,
-               solver="dlra", slab=None, comm_id=None) -> SimulationResult:
+               solver="dlra", slab=None, comm_id=None, resume=None,
+               checkpoint_at=None) -> SimulationResult:
     """The pseudo-time loop of run_simulation (driver.py:541-666) on the device.
 
     slab / comm_id: this process's z-slab of a multi-GPU solve (slabs.plan)
-    and the world's communicator id; the dose then covers the slab's cells."""
+    and the world's communicator id; the dose then covers the slab's cells.
+    resume: a DeviceSolver.checkpoint() dict to continue from; checkpoint_at:
+    a step index whose boundary snapshot is returned in
+    diagnostics["checkpoint"]. max_steps counts from the start (or resume) step."""
     if solver not in ("dlra", "fullrank"):
         raise ConfigError(f"unknown solver '{solver}'")
     if solver == "fullrank":
@@ -177,14 +198,18 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
     solver_ = DeviceSolver(b, device, slab=slab, comm_id=comm_id)
     solver_.init_state()
     edges = b.pseudo_time_edges()
+    k0 = solver_.restore(resume) if resume is not None else 0
     n_steps = len(edges) - 1
     if max_steps is not None:
-        n_steps = min(n_steps, int(max_steps))
+        n_steps = min(n_steps, k0 + int(max_steps))
     de = float(edges[0] - edges[1])
     ranks, max_tail, violations, max_defect = [], 0.0, 0, 0.0
     peak_state = 0
     peak_transient = 0
-    for k in range(n_steps):
+    snapshot = None
+    for k in range(k0, n_steps):
+        if checkpoint_at is not None and k == int(checkpoint_at):
+            snapshot = solver_.checkpoint(k)
         e_hi, e_lo = edges[k], edges[k + 1]
         solver_.set_coefficients(e_hi, e_lo)
         out = solver_.step(e_hi - e_lo, want_defect)
@@ -226,6 +251,8 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         "negativity": dose.negativity,
         "runtime_s": time.perf_counter() - t_start,
     }
+    if snapshot is not None:
+        diagnostics["checkpoint"] = snapshot
     return SimulationResult(bundle=b, dose=dose, rank_history=ranks, diagnostics=diagnostics,
                             uncollided=unc)
 

@@ -421,3 +421,35 @@ def test_wide_k_rhs_and_stencil_grams_vs_oracle(dl, r):
     for i, (axis, sign) in enumerate(grid.stencils()):
         ref = x.T @ dlra_np.stencil(grid, axis, sign, inv_s[:, None] * y)
         assert relmax(got_g[i], ref) < 1e-12
+
+
+# ------------------------------------------------------------------ determinism, checkpoint
+def test_rerun_is_bit_identical():
+    """Determinism contract (driver.py:12-13, test_driver.py:266-283): the
+    same bundle run twice gives byte-identical doses and rank histories
+    (fixed-order reductions everywhere, no atomics on the Gram paths)."""
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_hetero.npz")
+    r1 = run_bundle(b, max_steps=60)
+    r2 = run_bundle(b, max_steps=60)
+    assert r1.dose.deposited.tobytes() == r2.dose.deposited.tobytes()
+    assert r1.rank_history == r2.rank_history
+
+
+def test_checkpoint_resume_is_bit_identical(tmp_path):
+    """SURVEY.md §5 checkpoint/resume: a snapshot at a step boundary, saved,
+    reloaded into a fresh solver, continues to the same bytes as the
+    uninterrupted run."""
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_config1.npz")
+    full = run_bundle(b, max_steps=40, checkpoint_at=17)
+    path = tmp_path / "ckpt.npz"
+    np.savez(path, **full.diagnostics["checkpoint"])
+    ck = dict(np.load(path))
+    rest = run_bundle(b, max_steps=40 - 17, resume=ck)
+    assert rest.dose.deposited.tobytes() == full.dose.deposited.tobytes()
+    assert rest.rank_history == full.rank_history[17:]
