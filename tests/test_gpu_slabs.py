@@ -70,3 +70,24 @@ def test_nccl_world_of_one():
     full = run_bundle(b, max_steps=4)
     one = run_bundle(b, max_steps=4, slab=slabs.plan(*b.shape, 1, 0), comm_id=cid)
     np.testing.assert_array_equal(one.dose.deposited, full.dose.deposited)
+
+
+def test_slab_solve_wide_rank():
+    """Ranks above 32 (the 32-column block chains of wide.cu) under the slab
+    decomposition: halo planes of every block copy, Gram allreduces of every
+    pair, against the undecomposed solve."""
+    import dataclasses
+
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_config1.npz")
+    b = dataclasses.replace(b, truncation_tolerance=1e300, rank_min=40, rank_max=40)
+    full = run_bundle(b, max_steps=25)
+    parts = _run_slabs(b, 2, max_steps=25)
+    dep = np.concatenate([p.dose.deposited for p in parts])
+    for p in parts:
+        assert [r for _, _, r in p.rank_history] == [r for _, _, r in full.rank_history]
+        assert p.rank_history[-1][2] == 40
+    ref = full.dose.deposited
+    assert np.linalg.norm(dep - ref) / np.linalg.norm(ref) < 1e-10
