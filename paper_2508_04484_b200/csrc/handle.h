@@ -85,6 +85,7 @@ struct Handle {
   Comm* comm = nullptr;       // z-slab communicator (multi-GPU), null on one device
   TimerState timer;
   bool nvtx_open = false;  // an NVTX phase range is open
+  bool singular_pending = false;  // scattering solve flag awaiting the next sync
 };
 
 // phase mark: when timing is on, records an event on the handle's stream;

@@ -174,6 +174,19 @@ void consolidate(Handle& h) {
   h.uq = 0;
 }
 
+// the scattering step's implicit solves report a singular column through a
+// flag read back with the next synchronisation (the augmentation's)
+void check_singular(Handle& h) {
+  if (!h.singular_pending) return;
+  h.singular_pending = false;
+  const int singular = *(int*)(h.pinned + 10);
+  if (singular != (1 << 30)) {
+    fail(PND_ENUMERICAL, "implicit scattering solve singular at moment column " +
+                             std::to_string(singular) +
+                             "; the step size is too large for the scattering stiffness");
+  }
+}
+
 int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
   const int a = h.ua, b = X.cols + (X2.p ? X2.cols : 0);
   cudaStream_t st = h.st;
@@ -198,6 +211,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
   launched();
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  check_singular(h);
   const int k = *(int*)(h.pinned + 8);
   h.uq = 0;
   if (k == 0) return 0;
@@ -227,6 +241,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
 }
 
 void streaming_step(Handle& h, double dt) {
+  h.singular_pending = false;
   if (!h.stencil_error.empty()) fail(PND_ECONFIG, h.stencil_error);
   need(h.have_angular, "angular operators (pnd_set_angular)");
   need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
@@ -410,6 +425,7 @@ __global__ void class_weight_kernel(const int* cls, const double* wtab, const do
 }  // namespace
 
 void scattering_step(Handle& h, double dt) {
+  h.singular_pending = false;
   need(h.have_inv_s, "stopping power (pnd_set_inv_s)");
   need(h.have_mat, "materials (pnd_set_materials)");
   need(h.have_scat, "scattering tables (pnd_set_scattering)");
@@ -542,14 +558,10 @@ void scattering_step(Handle& h, double dt) {
   init_int<<<1, 1, 0, st>>>(flag + 4, 1 << 30);
   launched();
   scat_solves(Bi, coeffs, lcols, a, m, dt, lnew, flag + 4, st);
+  // the singular-column flag is read back with the augmentation's first
+  // synchronisation below (no extra host round trip)
   CK(cudaMemcpyAsync(h.pinned + 10, flag + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const int singular = *(int*)(h.pinned + 10);
-  if (singular != (1 << 30)) {
-    fail(PND_ENUMERICAL, "implicit scattering solve singular at moment column " +
-                             std::to_string(singular) +
-                             "; the step size is too large for the scattering stiffness");
-  }
+  h.singular_pending = true;
   // V~, R~ = qr(L1^T): lnew row-major (a x m) is L1^T column-major (m x a)
   phase(h, PH_TSQR_M);
   const int kt = m < a ? m : a;
@@ -664,6 +676,7 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   CK(cudaMemcpyAsync((int*)(h.pinned + 1), info + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h.pinned + 2, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  check_singular(h);
   const int r1 = *(int*)(h.pinned + 1);
   const double tail = h.pinned[0];
   const bool all_zero = h.pinned[2] == 0.0;
