@@ -145,7 +145,7 @@ void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* inv_s, double
 
 // out = [Y1 | Y2] TA - X TB (rows written when out.p != null) and, when grams != null,
 // grams = [X^T out (X.cols x nb) ; out^T out (nb x nb)]. TA == nullptr means
-// TA = I (out = Y1 - X TB: Y1 is added, not multiplied; needs Y2 empty).
+// TA = I (out = [Y1 | Y2] - X TB: the Y rows are added, not multiplied).
 void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
              NMat out, double* grams, DBuf& partial, cudaStream_t st);
 // Gram out = X^T diag(w) Y (X.cols x Y.cols, row-major; w = null: plain) in one
