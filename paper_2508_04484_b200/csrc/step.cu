@@ -81,6 +81,23 @@ double* eye(Handle& h, int b) {
 //          TA = P_k diag(lam_k^-1/2)  ->  Q = (Y - U0 C) TA = Y TA - U0 (C TA)
 //   mode 1 (re-orthogonalisation): TA = P diag(lam^-1/2) P^T
 //   TB = C TA.  info[0] = k;  dinfo[0] = max(|G - I|, |C|)
+// max(|G - I|, |C|) (the block's orthonormality defect) into out[0]
+__global__ void defect_gc_kernel(const double* G, const double* C, int a, int b, double* out) {
+  __shared__ double red[256];
+  double d = 0.0;
+  for (int i = threadIdx.x; i < b * b + a * b; i += blockDim.x) {
+    const double v = i < b * b ? fabs(G[i] - ((i / b == i % b) ? 1.0 : 0.0)) : fabs(C[i - b * b]);
+    d = v > d ? v : d;
+  }
+  red[threadIdx.x] = d;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
 __global__ void svqb_build(const double* G, const double* C, int a, int b, const double* P,
                            const double* lam, int mode, double tol_rel, double* TA, double* TB,
                            int* info, double* dinfo) {
@@ -220,17 +237,22 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
   lincomb(g, Y, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
   double* C3 = grams;
   double* G3 = grams + (size_t)a * k;
-  double* G3c = slot(h, S_M2, (size_t)k * k);
-  CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
-  if (a > 0) gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
-  svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
-  svqb_build<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1, dinfo);
+  // the block's defect max(|Q^T Q - I|, |U0^T Q|) decides on a further pass;
+  // its SVQB coefficients are only formed when it is needed
+  defect_gc_kernel<<<1, 256, 0, st>>>(G3, C3, a, k, dinfo);
   launched();
   CK(cudaMemcpyAsync(h.pinned + 9, dinfo, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   // re-orthogonalise when the block's defect exceeds the reference's own
   // re-orthonormalisation trigger (orthonormal_columns, dlra.py:36-41: 1e-12)
   if (h.pinned[9] > 1e-12) {
+    double* G3c = slot(h, S_M2, (size_t)k * k);
+    CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+    if (a > 0)
+      gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
+    svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
+    svqb_build<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1, dinfo);
+    launched();
     // pass 4: Q <- Q TA - U0 TB (into Qa, then swap)
     NMat Q2 = h.Qa.view(g, k, st);
     lincomb(g, Qv, NMat{}, U0, TA, TB, Q2, nullptr, h.part, st);
