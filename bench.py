@@ -41,6 +41,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "DLRA energy steps/s (256^3 water, P19 Fokker-Planck, rank 20)"
+
+
+def metric_name(nside, rank):
+    """The headline metric; non-default --nside / --rank name their own workload."""
+    return f"DLRA energy steps/s ({nside}^3 water, P19 Fokker-Planck, rank {rank})"
 UNIT = "steps/s"
 
 
@@ -401,7 +406,8 @@ def main():
             per.append(cb["value"])
         v = float(np.median(per))
         cb["value"] = v
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        line = {"metric": metric_name(args.nside, args.rank), "value": v, "unit": UNIT,
+                "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference",
@@ -509,7 +515,8 @@ def main():
         except Exception as exc:  # noqa: BLE001
             per_beam = {"error": str(exc)[:300]}
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args.nside, args.rank), "value": value, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * dev_s / args.steps,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
