@@ -206,6 +206,14 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&h.st2, cudaStreamNonBlocking));
+    {
+      // stream-ordered scratch (split-K partials, wide R x R work) stays in the
+      // device pool instead of going back to the driver at every synchronisation
+      cudaMemPool_t pool;
+      CK(cudaDeviceGetDefaultMemPool(&pool, device));
+      uint64_t keep = UINT64_MAX;
+      CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     CK(cudaEventCreateWithFlags(&h.ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h.ev_join, cudaEventDisableTiming));
     CK(cudaMallocHost(&h.pinned, 64 * sizeof(double)));

@@ -47,8 +47,9 @@ __device__ double block_sum(double v, double* red) {
 }
 
 // ----------------------------------------------------------------- gemm
+// Ktot > 0: split-K -- batch b covers k in [b K, b K + K) of Ktot (the last clipped)
 __global__ void gemm_kernel(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB,
-                            double beta, Mat C, long sC) {
+                            double beta, Mat C, long sC, int Ktot) {
   __shared__ double As[16][17];
   __shared__ double Bs[16][17];
   const int b = blockIdx.z;
@@ -57,6 +58,7 @@ __global__ void gemm_kernel(int M, int N, int K, double alpha, Mat A, long sA, M
   double* c = C.p + (size_t)b * sC;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  if (Ktot > 0 && K > Ktot - b * K) K = Ktot - b * K;  // the last slice
   double acc = 0.0;
   for (int k0 = 0; k0 < K; k0 += 16) {
     // A tile: (row block, k0..k0+15); load with tx running along k
@@ -664,11 +666,47 @@ Part make_part(int rows, int cols, int br) {
 
 }  // namespace
 
+namespace {
+// C = beta C + alpha sum_s P_s over the split-K partials (fixed order)
+__global__ void splitk_reduce(const double* __restrict__ P, int splits, int M, int N, double alpha,
+                              double beta, Mat C) {
+  const int total = M * N;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < splits; ++b) s += P[(size_t)b * total + e];
+    const int i = e / N, j = e - i * N;
+    double* c = C.p + (long)i * C.rs + (long)j * C.cs;
+    *c = beta == 0.0 ? alpha * s : alpha * s + beta * (*c);
+  }
+}
+}  // namespace
+
 void gemm(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB, double beta, Mat C,
           long sC, int batch, cudaStream_t st) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
+  const int tiles = ((N + 15) / 16) * ((M + 15) / 16);
+  if (batch == 1 && K >= 512 && tiles < 148) {
+    // long-K, few tiles (the L phase's A^T Z, K = ns m): split K over CTAs,
+    // partials reduced in a fixed order
+    int splits = K / 128;
+    if (splits > 16) splits = 16;
+    const int kb = (K + splits - 1) / splits;
+    splits = (K + kb - 1) / kb;
+    double* P = nullptr;
+    CK(cudaMallocAsync((void**)&P, (size_t)splits * M * N * sizeof(double), st));
+    dim3 grid((N + 15) / 16, (M + 15) / 16, splits), block(16, 16);
+    const Mat Pm{P, N, 1};
+    // batch b multiplies K-slice [b kb, b kb + kb): A advanced along k (cs), B along k (rs)
+    gemm_kernel<<<grid, block, 0, st>>>(M, N, kb, 1.0, A, (long)kb * A.cs, B, (long)kb * B.rs, 0.0,
+                                         Pm, (long)M * N, K);
+    launched();
+    splitk_reduce<<<(M * N + 255) / 256, 256, 0, st>>>(P, splits, M, N, alpha, beta, C);
+    launched();
+    CK(cudaFreeAsync(P, st));
+    return;
+  }
   dim3 grid((N + 15) / 16, (M + 15) / 16, batch), block(16, 16);
-  gemm_kernel<<<grid, block, 0, st>>>(M, N, K, alpha, A, sA, B, sB, beta, C, sC);
+  gemm_kernel<<<grid, block, 0, st>>>(M, N, K, alpha, A, sA, B, sB, beta, C, sC, 0);
   launched();
 }
 
