@@ -685,7 +685,7 @@ void gemm(int M, int N, int K, double alpha, Mat A, long sA, Mat B, long sB, dou
           long sC, int batch, cudaStream_t st) {
   if (M <= 0 || N <= 0 || batch <= 0) return;
   const int tiles = ((N + 15) / 16) * ((M + 15) / 16);
-  if (batch == 1 && K >= 512 && tiles < 148) {
+  if (batch == 1 && K >= 256 && tiles < 148) {
     // long-K, few tiles (the L phase's A^T Z, K = ns m): split K over CTAs,
     // partials reduced in a fixed order
     int splits = K / 128;
