@@ -253,13 +253,19 @@ int pnd_destroy(pnd_handle* hh) {
   Handle& h = hh->h;
   cudaSetDevice(h.device);
   if (h.st) cudaStreamSynchronize(h.st);
+  if (h.st2) cudaStreamSynchronize(h.st2);
   pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.cls_val, &h.bcat,
                        &h.gdiag, &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V,
                        &h.part, &h.dep, &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.rbuf,
-                       &h.tq_m.cbuf};
+                       &h.tq_m.cbuf, &h.ctab, &h.csel, &h.wide_m, &h.wide_t, &h.wide_i,
+                       &h.wide_g, &h.fr_scr, &h.fr_scr2, &h.fr_scr3, &h.fr_eye};
   for (auto* b : bufs) b->free_();
-  pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs};
+  pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs, &h.wide_base,
+                     &h.wide_tmp[0], &h.wide_tmp[1], &h.fr_t[0], &h.fr_t[1]};
   for (auto* b : nb) b->d.free_();
+  for (auto* v : {&h.wide_u0b, &h.wide_qb, &h.wide_w1b, &h.wide_w2b, &h.wide_gb, &h.fr_u,
+                  &h.fr_w1, &h.fr_w2})
+    for (auto& b : *v) b.d.free_();
   pnd::comm_destroy(h.comm);
   h.comm = nullptr;
   for (auto& b : h.sm) b.free_();
