@@ -50,9 +50,24 @@ UNIT = "steps/s"
 
 
 # ----------------------------------------------------------------- workload
+SLAB_PHANTOM = ((0.0, 3.0, 0), (3.0, 4.0, 1), (4.0, 7.0, 2))  # (z0, z1 cm, class)
+
+
+def plane_classes(nz, h, phantom):
+    """Material class of every z plane: "water", or "slabs" -- SURVEY.md §8(d)
+    config 3: water 0 HU z in [0, 3) cm, bone +1200 HU [3, 4), lung -700 HU
+    [4, 7), water beyond (classes 0, 1, 2 of bench_physics.npz)."""
+    zc = np.zeros(nz, dtype=np.int32)
+    if phantom == "slabs":
+        z = (np.arange(nz) + 0.5) * h
+        for z0, z1, c in SLAB_PHANTOM:
+            zc[(z >= z0) & (z < z1)] = c
+    return zc
+
+
 def make_workload(nside=256, h=0.025, n_max=19, rank=20, model="fokker-planck",
-                  energy=70.0, sigma_xy=0.3, groups=128):
-    """ProblemBundle of the synthetic water phantom (no flux table attached)."""
+                  energy=70.0, sigma_xy=0.3, groups=128, phantom="water"):
+    """ProblemBundle of a synthetic phantom (no flux table attached)."""
     from paper_2508_04484_b200.angular import PNOperators
     from paper_2508_04484_b200.problem import ProblemBundle, UncollidedSlices
 
@@ -60,12 +75,13 @@ def make_workload(nside=256, h=0.025, n_max=19, rank=20, model="fokker-planck",
     ops = PNOperators.build(n_max)
     sigma_e = 0.01 * energy
     e_max = energy + 5.0 * sigma_e
-    n = nside ** 3
+    zc = plane_classes(nside, h, phantom)
+    nc = int(zc.max()) + 1
     b = ProblemBundle(
         shape=(nside, nside, nside), spacing=(h, h, h), origin=(0.0, 0.0, 0.0),
-        cell_class=np.zeros(n, dtype=np.int32),
-        class_density=ph["class_density"][:1], class_weights=ph["class_weights"][:1],
-        class_atomic=ph["class_atomic"][:1],
+        cell_class=np.repeat(zc, nside * nside),
+        class_density=ph["class_density"][:nc], class_weights=ph["class_weights"][:nc],
+        class_atomic=ph["class_atomic"][:nc],
         stop_e=ph["stop_e"], stop_s=ph["stop_s"], mom_e=ph["mom_e"],
         mom_g=ph["mom_g"][..., : n_max + 2], mom_xi1=ph["mom_xi1"],
         eig_v=np.stack(ops.eig_v), lam_plus=np.stack(ops.lam_plus),
@@ -73,9 +89,10 @@ def make_workload(nside=256, h=0.025, n_max=19, rank=20, model="fokker-planck",
         t_ms=np.array([_beam_tm(n_max)]),
         fluxes=[UncollidedSlices(np.zeros((1, groups)), np.zeros(1), 1.0, e_max)],
         model=model, pn_order=n_max, e_min=1.0, e_max=e_max, cfl_number=0.2,
-        truncation_tolerance=1e300, rank_min=rank, rank_max=rank, name="bench256",
+        truncation_tolerance=1e300, rank_min=rank, rank_max=rank, name=f"bench{nside}",
     )
-    return b, ops, dict(energy=energy, sigma_e=sigma_e, sigma_xy=sigma_xy, groups=groups)
+    return b, ops, dict(energy=energy, sigma_e=sigma_e, sigma_xy=sigma_xy, groups=groups,
+                        plane_class=zc)
 
 
 def _beam_tm(n_max):
@@ -99,6 +116,7 @@ def separable_flux(b, beam):
     lat = np.exp(-0.5 * (x[None, :] ** 2 + y[:, None] ** 2) / sx ** 2) / (2 * math.pi * sx ** 2)
     f = b.fluxes[0]
     centers = f.centers
+    zc = beam.get("plane_class", np.zeros(nz, dtype=np.int32))
     z = (np.arange(nz) + 0.5) * hz
     e = beam["energy"]
     depth = np.zeros((nz, f.n_groups))
@@ -106,7 +124,7 @@ def separable_flux(b, beam):
     for k in range(nz):
         while zz < z[k] and e > 1.0:
             dz = min(0.001, z[k] - zz)
-            e -= float(b.class_stopping(max(e, 1.0))[0]) * dz
+            e -= float(b.class_stopping(max(e, 1.0))[zc[k]]) * dz
             zz += dz
         if e <= 1.0:
             break
@@ -117,13 +135,15 @@ def separable_flux(b, beam):
 
 
 class Workload:
-    def __init__(self, nside=256, rank=20, device=0, n_max=19, slab=None, comm_id=None):
+    def __init__(self, nside=256, rank=20, device=0, n_max=19, slab=None, comm_id=None,
+                 model="fokker-planck", energy=70.0, phantom="water"):
         """slab: this process's z-planes of the joint multi-GPU solve (slabs.plan),
         comm_id the world's NCCL id; None = the whole grid on this GPU."""
         from paper_2508_04484_b200 import _lib
         from paper_2508_04484_b200.driver import DeviceSolver
 
-        self.bundle, self.ops, beam = make_workload(nside=nside, rank=rank, n_max=n_max)
+        self.bundle, self.ops, beam = make_workload(nside=nside, rank=rank, n_max=n_max,
+                                                    model=model, energy=energy, phantom=phantom)
         b = self.bundle
         self.rank = rank
         self.solver = DeviceSolver.__new__(DeviceSolver)

@@ -203,7 +203,9 @@ int pnd_event_elapsed(pnd_handle* h, int slot_a, int slot_b, double* ms);
 /* kernels launched by this process since load */
 int pnd_launch_count(pnd_handle* h, long long* count);
 /* uncollided group table of a +z pencil beam in a laterally uniform phantom:
- * values[c][g] = lateral[j*nx + i] * depth[k*G + g], formed on the device */
+ * values[c][g] = lateral[j*nx + i] * depth[k*G + g]; only the two factors are
+ * kept on the device and each step's flux slices are formed from them (the
+ * dense n x G table is 137 GB per beam at 512^3 x 128 groups) */
 int pnd_set_flux_separable(pnd_handle* h, int beam, int n_beams, int n_groups,
                            const double* lateral, const double* depth, const double* t_m);
 /* preset rank-r state: orthonormalised pseudo-random U, V; S = diag(logspace(0, -3, r)) */

@@ -106,17 +106,6 @@ void phase(Handle& h, int id) {
 
 namespace {
 
-__global__ void separable_kernel(const double* lat, const double* depth, int nxy, int n, int G,
-                                 int ld, double* out) {
-  const long long total = (long long)G * n;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int g = (int)(i / n), c = (int)(i - (long long)g * n);
-    const int k = c / nxy, ij = c - k * nxy;
-    out[(size_t)g * ld + c] = lat[ij] * depth[(size_t)k * G + g];
-  }
-}
-
 __global__ void logdiag_kernel(double* S, int r) {
   for (int i = threadIdx.x; i < r * r; i += blockDim.x) {
     const int a = i / r, b = i % r;
@@ -258,7 +247,8 @@ int pnd_destroy(pnd_handle* hh) {
                        &h.gdiag, &h.sigt, &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V,
                        &h.part, &h.dep, &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.rbuf,
                        &h.tq_m.cbuf, &h.ctab, &h.csel, &h.wide_m, &h.wide_t, &h.wide_i,
-                       &h.wide_g, &h.fr_scr, &h.fr_scr2, &h.fr_scr3, &h.fr_eye};
+                       &h.wide_g, &h.fr_scr, &h.fr_scr2, &h.fr_scr3, &h.fr_eye,
+                       &h.sep_lat, &h.sep_depth};
   for (auto* b : bufs) b->free_();
   pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs, &h.wide_base,
                      &h.wide_tmp[0], &h.wide_tmp[1], &h.fr_t[0], &h.fr_t[1]};
@@ -298,7 +288,7 @@ int pnd_device_bytes(pnd_handle* hh, double* bytes) {
     double total = 0;
     const pnd::DBuf* bufs[] = {&h.amat, &h.inv_s, &h.isp, &h.s_field, &h.cls_atomic, &h.gdiag,
                                &h.psi, &h.psi_lo, &h.tm, &h.flux, &h.S, &h.V, &h.part, &h.dep,
-                               &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.cbuf};
+                               &h.prev, &h.sep_lat, &h.sep_depth, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.cbuf};
     for (auto* b : bufs) total += 8.0 * b->cap;
     const pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs};
     for (auto* b : nb) total += 8.0 * b->d.cap;
@@ -391,6 +381,9 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
     if (beam == 0) {
       h.n_groups = n_groups;
       h.n_beams = n_beams;
+      h.flux_sep = false;
+      h.sep_lat.free_();
+      h.sep_depth.free_();
       h.flux.get((size_t)n_beams * n_groups * h.g.ld);
       h.psi.get((size_t)n_beams * h.g.ld + 64);
       h.psi_lo.get((size_t)n_beams * h.g.ld);
@@ -444,7 +437,7 @@ int pnd_set_coefficient_tables(pnd_handle* hh, int k, const double* log_e, const
     h.ct_pn = pn_order;
     h.ct_bcorr = boltzmann_correction;
     h.ct_fpscale = fp_correction_scale;
-    if (n_beams && (!h.flux.p || n_beams != h.n_beams))
+    if (n_beams && (!h.have_flux() || n_beams != h.n_beams))
       pnd::fail(PND_ECONFIG, "coefficient tables: set the flux tables of every beam first");
     h.csel.get(32);
     CK(cudaStreamSynchronize(h.st));
@@ -475,6 +468,14 @@ int pnd_select_flux(pnd_handle* hh, int which, const int32_t* j0, const double* 
   return guard(hh, [&](Handle& h) {
     double* dst = which == 0 ? h.psi.p : h.psi_lo.p;
     for (int b = 0; b < h.n_beams; ++b) {
+      if (h.flux_sep) {
+        const int nxy = h.g.nx * h.g.ny;
+        pnd::psi_lerp_separable(h.sep_lat.p + (size_t)b * nxy,
+                                h.sep_depth.p + (size_t)b * h.g.nz * h.n_groups, nxy, h.n_groups,
+                                h.g.n, nullptr, nullptr, j0[b], w0[b], j1[b], w1[b],
+                                dst + (size_t)b * h.g.ld, h.st);
+        continue;
+      }
       const double* tab = h.flux.p + (size_t)b * h.n_groups * h.g.ld;
       pnd::psi_lerp(tab, h.g.ld, h.g.n, j0[b], w0[b], j1[b], w1[b], dst + (size_t)b * h.g.ld,
                     h.st);
@@ -1078,27 +1079,25 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
                            const double* lateral, const double* depth, const double* t_m) {
   return guard(hh, [&](Handle& h) {
     if (n_beams < 1 || n_beams > 4) pnd::fail(PND_ECONFIG, "1..4 beams supported");
+    if (beam < 0 || beam >= n_beams) pnd::fail(PND_ECONFIG, "beam index out of range");
+    const int nxy = h.g.nx * h.g.ny;
     if (beam == 0) {
       h.n_groups = n_groups;
       h.n_beams = n_beams;
-      h.flux.get((size_t)n_beams * n_groups * h.g.ld);
+      h.flux.free_();  // the factors replace any dense tables
+      h.flux_sep = true;
+      h.sep_lat.get((size_t)n_beams * nxy);
+      h.sep_depth.get((size_t)n_beams * h.g.nz * n_groups);
       h.psi.get((size_t)n_beams * h.g.ld + 64);
       h.psi_lo.get((size_t)n_beams * h.g.ld);
       h.tm.get((size_t)n_beams * h.m);
+    } else if (!h.flux_sep || n_beams != h.n_beams || n_groups != h.n_groups) {
+      pnd::fail(PND_ECONFIG, "separable flux: set beam 0 first with the same beam/group counts");
     }
-    const int nxy = h.g.nx * h.g.ny;
-    pnd::DBuf dl, dd;
-    double* L = dl.get(nxy);
-    double* D = dd.get((size_t)h.g.nz * n_groups);
-    up(L, lateral, nxy, h.st);
-    up(D, depth, (size_t)h.g.nz * n_groups, h.st);
-    pnd::separable_kernel<<<148 * 8, 256, 0, h.st>>>(
-        L, D, nxy, h.g.n, n_groups, h.g.ld, h.flux.p + (size_t)beam * n_groups * h.g.ld);
-    pnd::launched();
+    up(h.sep_lat.p + (size_t)beam * nxy, lateral, nxy, h.st);
+    up(h.sep_depth.p + (size_t)beam * h.g.nz * n_groups, depth, (size_t)h.g.nz * n_groups, h.st);
     up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
     CK(cudaStreamSynchronize(h.st));
-    dl.free_();
-    dd.free_();
   });
 }
 

@@ -220,7 +220,7 @@ void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo) {
   a.fp_scale = h.ct_fpscale;
   a.m = h.m;
   a.n_groups = h.n_groups;
-  a.n_beams = h.flux.p ? h.n_beams : 0;
+  a.n_beams = h.have_flux() ? h.n_beams : 0;
   double* cs = h.cls_val.get(h.n_cls);
   double* gd = h.gdiag.get((size_t)NEL * h.m);
   double* sg = h.sigt.get(NEL);
@@ -242,6 +242,14 @@ void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo) {
     if (!dst) continue;
     for (int b = 0; b < a.n_beams; ++b) {
       const int s = which * a.n_beams + b;
+      if (h.flux_sep) {
+        const int nxy = h.g.nx * h.g.ny;
+        psi_lerp_separable(h.sep_lat.p + (size_t)b * nxy,
+                           h.sep_depth.p + (size_t)b * h.g.nz * h.n_groups, nxy, h.n_groups,
+                           h.g.n, sj + 2 * s, sw + 2 * s, 0, 0.0, 0, 0.0,
+                           dst + (size_t)b * h.g.ld, h.st);
+        continue;
+      }
       lerp_dev_kernel<<<sm_count() * 8, 256, 0, h.st>>>(
           h.flux.p + (size_t)b * h.n_groups * h.g.ld, h.g.ld, h.g.n, sj + 2 * s, sw + 2 * s,
           dst + (size_t)b * h.g.ld);

@@ -48,6 +48,12 @@ struct Handle {
   DBuf tm;          // n_beams x m
   DBuf flux;        // n_beams x G x ld (group tables, column-major)
   int n_groups = 0;
+  // separable group tables (pnd_set_flux_separable): psi(c, g) = lat(x, y) depth(z, g),
+  // kept as the factors (n_beams x nx ny, n_beams x nz x G) -- a 512^3 x 128-group
+  // dense table is 137 GB per beam; the per-step slices are formed from the factors
+  DBuf sep_lat, sep_depth;
+  bool flux_sep = false;
+  bool have_flux() const { return flux.p != nullptr || flux_sep; }
   bool have_angular = false, have_inv_s = false, have_mat = false, have_scat = false;
   // per-step coefficient tables (coeff.cu, pnd_set_coefficient_tables):
   // [log E | log S (12 x K each) | rho (n_cls) | w (n_cls x 12) | E_mom (P) |

@@ -294,6 +294,33 @@ __global__ void lerp_kernel(const double* __restrict__ v, int ldv, int n, int j0
   }
 }
 
+// lerp_kernel on the separable table: v[g][c] = lat[c % nxy] * depth[c / nxy][g],
+// the product rounded as the expanded table stores it
+__global__ void lerp_sep_kernel(const double* __restrict__ lat, const double* __restrict__ depth,
+                                int nxy, int G, int n, const int* __restrict__ sel_j,
+                                const double* __restrict__ sel_w, int j0, double w0, int j1,
+                                double w1, double* __restrict__ out) {
+  if (sel_j) {
+    j0 = sel_j[0];
+    j1 = sel_j[1];
+    w0 = sel_w[0];
+    w1 = sel_w[1];
+  }
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const int k = c / nxy;
+    const double l = lat[c - k * nxy];
+    const double v0 = __dmul_rn(l, depth[(size_t)k * G + j0]);
+    double x;
+    if (w1 == 0.0) {
+      x = w0 == 1.0 ? v0 : w0 * v0;
+    } else {
+      const double v1 = __dmul_rn(l, depth[(size_t)k * G + j1]);
+      x = w0 * v0 + w1 * v1;
+    }
+    out[c] = x;
+  }
+}
+
 __global__ void tin_kernel(const double* __restrict__ src, int n, int cdim, double* __restrict__ dst,
                            int ldd) {
   __shared__ double tile[32][33];
@@ -403,6 +430,14 @@ void random_rows(const Geom& g, NMat U, unsigned long long seed, cudaStream_t st
 void class_gather_inv(const int* cls, const double* class_val, int n, double* out_inv,
                       double* out_val, cudaStream_t st) {
   class_gather_kernel<<<grid_for(n, 256), 256, 0, st>>>(cls, class_val, n, out_inv, out_val);
+  launched();
+}
+
+void psi_lerp_separable(const double* lat, const double* depth, int nxy, int G, int n,
+                        const int* sel_j, const double* sel_w, int j0, double w0, int j1,
+                        double w1, double* out, cudaStream_t st) {
+  lerp_sep_kernel<<<grid_for(n, 256), 256, 0, st>>>(lat, depth, nxy, G, n, sel_j, sel_w, j0, w0,
+                                                    j1, w1, out);
   launched();
 }
 

@@ -191,6 +191,12 @@ void unit_rows(const Geom& g, NMat U, cudaStream_t st);        // U[:, j] = e_j
 void random_rows(const Geom& g, NMat U, unsigned long long seed, cudaStream_t st);
 void class_gather_inv(const int* cls, const double* class_val, int n, double* out_inv,
                       double* out_val, cudaStream_t st);
+// psi = w0 lat depth[:, j0] + w1 lat depth[:, j1] of a separable table (the same
+// arithmetic as psi_lerp on the expanded table); sel_j/sel_w: device selections
+// (nullptr: the host scalars)
+void psi_lerp_separable(const double* lat, const double* depth, int nxy, int G, int n,
+                        const int* sel_j, const double* sel_w, int j0, double w0, int j1,
+                        double w1, double* out, cudaStream_t st);
 void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, double w1,
               double* out, cudaStream_t st);
 // row-major host-layout (n x c) <-> column-major (ld) device layout (flux tables, TSQR)

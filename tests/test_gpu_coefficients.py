@@ -81,3 +81,60 @@ def test_device_coefficient_steps_match_host_steps():
         doses.append(s.dose())
         s.close()
     assert rel(doses[1], doses[0]) < 1e-11
+
+
+def test_separable_flux_matches_dense_table():
+    """pnd_set_flux_separable keeps lat(x, y) and depth(z, g) on the device and forms
+    each step's slices from them (no n x G table); the slices are bit-identical to
+    the lerp of the expanded table, for device- and host-selected groups."""
+    from paper_2508_04484_b200 import _lib
+    from paper_2508_04484_b200.driver import DeviceSolver
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_hetero.npz")
+    nx, ny, nz = b.shape
+    n, G, nb = b.n_cells, b.fluxes[0].n_groups, len(b.fluxes)
+    rng = np.random.default_rng(11)
+    lats = [rng.random(nx * ny) for _ in range(nb)]
+    depths = [rng.random((nz, G)) * np.exp(-rng.random((nz, G)) * 30.0) for _ in range(nb)]
+    vals = [np.ascontiguousarray((d[:, None, :] * lat[None, :, None]).reshape(n, G))
+            for lat, d in zip(lats, depths)]
+    devs = []
+    for sep in (False, True):
+        dev = DeviceSolver(b, device_coefficients=True)
+        for i in range(nb):
+            tm = _lib.f64(b.t_ms[i])
+            if sep:
+                dev.h.call("pnd_set_flux_separable", i, nb, G, _lib.ptr(lats[i]),
+                           _lib.ptr(depths[i]), _lib.ptr(tm))
+            else:
+                dev.h.call("pnd_set_flux_table", i, nb, G, _lib.ptr(vals[i]), _lib.ptr(tm))
+        dev.upload_coefficient_tables()
+        devs.append(dev)
+    es = energies(b)
+    for e_mid, e_lo in zip(es, es[1:] + es[:1]):
+        got = []
+        for dev in devs:
+            psi, psi_lo = np.empty((nb, n)), np.empty((nb, n))
+            dev.h.call("pnd_coefficients_at", float(e_mid), float(e_lo), 1)
+            dev.h.call("pnd_get_coefficients", None, None, None, _lib.ptr(psi), _lib.ptr(psi_lo))
+            got.append((psi, psi_lo))
+        np.testing.assert_array_equal(got[0][0], got[1][0])
+        np.testing.assert_array_equal(got[0][1], got[1][1])
+    for j0, w0, j1, w1 in [(3, 1.0, 4, 0.0), (3, 0.25, 4, 0.75), (G - 2, 0.5, G - 1, 0.5),
+                           (0, 0.7, 1, 0.0)]:
+        got = []
+        for dev in devs:
+            psi = np.empty((nb, n))
+            dev.h.call("pnd_select_flux", 0, _lib.ptr(np.full(nb, j0, np.int32)),
+                       _lib.ptr(np.full(nb, w0)), _lib.ptr(np.full(nb, j1, np.int32)),
+                       _lib.ptr(np.full(nb, w1)))
+            dev.h.call("pnd_get_coefficients", None, None, None, _lib.ptr(psi), None)
+            got.append(psi)
+        np.testing.assert_array_equal(got[0], got[1])
+        for i in range(nb):
+            v = vals[i]
+            want = w0 * v[:, j0] + w1 * v[:, j1] if w1 != 0.0 else w0 * v[:, j0]
+            np.testing.assert_allclose(got[1][i], want, rtol=1e-15, atol=0)
+    for dev in devs:
+        dev.close()
