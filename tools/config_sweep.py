@@ -10,6 +10,8 @@ one point never limits the next):
   lung -700 HU at 0-3-4-7 cm), Boltzmann scattering, P7 (m = 64), 100 MeV
   +z beam, fixed rank 20, on ONE B200 (the factor and work buffers of r = 20
   at 134 M cells are ~142 GB);
+- config 4: the 256^3 water P19 Fokker-Planck workload with four 90 MeV
+  beams (gantry 0/45/90/135 deg in the y-z plane) in one solve, fixed rank 20;
 - config 5: the rank sweep r = 10, 20, 40, 64 on the bench's 256^3 water
   P19 Fokker-Planck workload.
 Timing as bench.py: W warm-up steps, then K steps between CUDA events on the
@@ -31,7 +33,53 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-POINTS = ["256:10:water", "256:20:water", "256:40:water", "256:64:water", "512:20:slabs"]
+POINTS = ["256:10:water", "256:20:water", "256:40:water", "256:64:water", "512:20:slabs",
+          "256:20:beams4"]
+GANTRY = (0.0, 45.0, 90.0, 135.0)
+
+
+def attach_gantry_beams(wl, groups=32):
+    """Config 4: four 90 MeV pencil beams at gantry 0/45/90/135 deg in the y-z plane,
+    aimed at the grid centre, in one solve. Each beam's uncollided group table
+    (n x G, dense -- the beams are not z-separable) is the +z pencil's depth
+    spectrum laid along the beam axis with a Gaussian lateral profile."""
+    import math
+
+    import bench
+    from paper_2508_04484_b200 import _lib
+    from paper_2508_04484_b200.angular import beam_projection
+    from paper_2508_04484_b200.problem import UncollidedSlices
+
+    b = wl.bundle
+    nx, ny, nz = b.shape
+    h = b.spacing[0]
+    b1, _, beam = bench.make_workload(nside=nz, n_max=b.pn_order, energy=90.0, groups=groups)
+    _, depth = bench.separable_flux(b1, beam)
+    f0 = b1.fluxes[0]
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    x = ((i.ravel() + 0.5) * h - 0.5 * nx * h)
+    y = ((j.ravel() + 0.5) * h - 0.5 * ny * h)
+    z = ((k.ravel() + 0.5) * h - 0.5 * nz * h)
+    del i, j, k
+    sx = beam["sigma_xy"]
+    tms, fluxes = [], []
+    for bi, deg in enumerate(GANTRY):
+        th = math.radians(deg)
+        d = (0.0, math.sin(th), math.cos(th))
+        t = y * d[1] + z * d[2]                       # along the axis, 0 at the centre
+        rho2 = x * x + (y - t * d[1]) ** 2 + (z - t * d[2]) ** 2
+        kd = np.clip(((t + 0.5 * nz * h) / h).astype(np.int64), 0, nz - 1)
+        lat = np.exp(-0.5 * rho2 / sx ** 2) / (2 * math.pi * sx ** 2)
+        vals = np.ascontiguousarray(depth[kd] * lat[:, None])
+        tm = _lib.f64(beam_projection(b.pn_order, d))
+        wl.solver.h.call("pnd_set_flux_table", bi, len(GANTRY), groups, _lib.ptr(vals),
+                         _lib.ptr(tm))
+        del vals, lat, rho2, kd, t
+        tms.append(tm)
+        fluxes.append(UncollidedSlices(np.zeros((1, groups)), np.zeros(1), f0.e_min, f0.e_max))
+    b.fluxes = fluxes
+    b.t_ms = np.stack(tms)
+    wl.solver.upload_coefficient_tables()
 
 
 def run_point(spec, steps, warmup):
@@ -43,9 +91,11 @@ def run_point(spec, steps, warmup):
     nside, rank, phantom = spec.split(":")
     nside, rank = int(nside), int(rank)
     kw = dict(model="boltzmann", n_max=7, energy=100.0, phantom="slabs") \
-        if phantom == "slabs" else {}
+        if phantom == "slabs" else dict(energy=90.0) if phantom == "beams4" else {}
     t0 = time.perf_counter()
     wl = bench.Workload(nside=nside, rank=rank, **kw)
+    if phantom == "beams4":
+        attach_gantry_beams(wl)
     setup_s = time.perf_counter() - t0
     h = wl.solver.h
     for _ in range(warmup):
@@ -69,6 +119,7 @@ def run_point(spec, steps, warmup):
     out = {
         "point": spec, "grid": [nside] * 3, "rank": rank, "moments": b.n_moments,
         "model": b.model, "classes": int(b.n_classes), "phantom": phantom,
+        "beams": len(b.fluxes),
         "ms_per_step": 1000.0 * t, "steps_per_s": 1.0 / t, "steps": steps, "warmup": warmup,
         "reference_step_count": len(wl.edges) - 1,
         "whole_run_s_extrapolated": t * (len(wl.edges) - 1),
