@@ -63,8 +63,7 @@ def beam_projection(n_max, omega):
     return real_basis(n_max, mu, phi)[:, 0]
 
 
-def flux_matrices(n_max):
-    """(A_x, A_y, A_z) by exact product quadrature."""
+def _quadrature(n_max):
     nq = n_max + 2
     x, w = np.polynomial.legendre.leggauss(nq)
     nphi = 2 * n_max + 4
@@ -75,6 +74,12 @@ def flux_matrices(n_max):
     basis = real_basis(n_max, mu, ph)
     s = np.sqrt(1.0 - mu * mu)
     comps = (s * np.cos(ph), s * np.sin(ph), mu)
+    return basis, wt, comps
+
+
+def flux_matrices(n_max):
+    """(A_x, A_y, A_z) by exact product quadrature."""
+    basis, wt, comps = _quadrature(n_max)
     out = []
     for c in comps:
         a = (basis * (wt * c)) @ basis.T
@@ -94,13 +99,38 @@ class PNOperators:
     lam_minus: tuple
 
     @classmethod
-    def build(cls, n_max: int) -> "PNOperators":
+    def build(cls, n_max: int, device=None) -> "PNOperators":
+        """device (e.g. "cuda:0"): the three quadrature Grams and their
+        eigendecompositions run on the GPU (cuBLAS DGEMM, cuSOLVER syevd via
+        torch; SURVEY.md §8(f) row 4 -- the O(m^3) setup that takes seconds on
+        the host at N >= 39); the same arithmetic as the host path."""
+        if device is not None:
+            return cls._build_device(n_max, device)
         vs, lp, lm = [], [], []
         for a in flux_matrices(n_max):
             lam, v = np.linalg.eigh(a)
             vs.append(v)
             lp.append(np.maximum(lam, 0.0))
             lm.append(np.minimum(lam, 0.0))
+        return cls(n_max, tuple(vs), tuple(lp), tuple(lm))
+
+    @classmethod
+    def _build_device(cls, n_max, device):
+        import torch
+
+        basis, wt, comps = _quadrature(n_max)
+        bd = torch.from_numpy(basis).to(device)
+        vs, lp, lm = [], [], []
+        for c in comps:
+            a = (bd * torch.from_numpy(wt * c).to(device)) @ bd.T
+            a = 0.5 * (a + a.T)
+            a = torch.where(a.abs() < 1e-15, torch.zeros_like(a), a)
+            lam, v = torch.linalg.eigh(a)
+            vs.append(v.cpu().numpy())
+            lam = lam.cpu().numpy()
+            lp.append(np.maximum(lam, 0.0))
+            lm.append(np.minimum(lam, 0.0))
+            del a, v
         return cls(n_max, tuple(vs), tuple(lp), tuple(lm))
 
     @property
