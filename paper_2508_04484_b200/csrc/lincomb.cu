@@ -65,7 +65,7 @@ struct LIn {
 };
 
 template <int NB8, int TBUF = 2>
-__global__ void __launch_bounds__(LTH, 2)
+__global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
     lincomb_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
                    int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
                    double* __restrict__ partial, int) {
