@@ -388,8 +388,8 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
       h.psi.get((size_t)n_beams * h.g.ld + 64);
       h.psi_lo.get((size_t)n_beams * h.g.ld);
       h.tm.get((size_t)n_beams * h.m);
-    } else if (n_groups != h.n_groups || n_beams != h.n_beams) {
-      pnd::fail(PND_ECONFIG, "all beams must share the group grid");
+    } else if (n_groups != h.n_groups || n_beams != h.n_beams || !h.flux.p) {
+      pnd::fail(PND_ECONFIG, "all beams must share the group grid (set beam 0 first)");
     }
     // values (n x G row-major) -> G columns of length ld
     pnd::DBuf stage;
