@@ -6,8 +6,9 @@ cells at h = 0.025 cm (6.4 cm cube), P_19 (m = 400 moments), Fokker-Planck
 collided equation, 70 MeV +z pencil beam (sigma_xy = 0.3 cm), CFL 0.2
 (the step count the reference would take is reported). The rank is pinned at
 r = 20 (truncation runs after both substeps with the rank clamped,
-theta = 1e300, rank_min = rank_max = 20): the kernels hold at most rank 32,
-and a pinned rank makes every step the same work, so steps/s is a rate.
+theta = 1e300, rank_min = rank_max = 20): a pinned rank makes every step the
+same work, so steps/s is a rate (--rank up to 64; configs 3-5 of SURVEY.md
+§8(d) are measured by tools/config_sweep.py).
 One "step" is the reference's full energy step (driver.py:578-622):
 streaming -> truncate -> scattering -> truncate -> dose trapezoid, plus the
 orthonormality diagnostic, starting from a preset rank-20 state at step
