@@ -44,9 +44,16 @@ sys.path.insert(0, str(ROOT))
 METRIC = "DLRA energy steps/s (256^3 water, P19 Fokker-Planck, rank 20)"
 
 
-def metric_name(nside, rank):
-    """The headline metric; non-default --nside / --rank name their own workload."""
+def metric_name(nside, rank, phantom="water"):
+    """The headline metric; non-default --nside / --rank / --phantom name their own workload."""
+    if phantom == "slabs":
+        return f"DLRA energy steps/s ({nside}^3 water/bone/lung slabs, P7 Boltzmann, rank {rank})"
     return f"DLRA energy steps/s ({nside}^3 water, P19 Fokker-Planck, rank {rank})"
+
+
+# --phantom slabs: SURVEY.md §8(d) config 3's physics
+PHANTOM_KW = {"water": {}, "slabs": dict(model="boltzmann", n_max=7, energy=100.0,
+                                         phantom="slabs")}
 UNIT = "steps/s"
 
 
@@ -383,6 +390,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--rank", type=int, default=20)
     ap.add_argument("--nside", type=int, default=256)
+    ap.add_argument("--phantom", default="water", choices=["water", "slabs"],
+                    help="slabs: SURVEY.md §8(d) config 3 (use with --nside 512)")
     ap.add_argument("--cpu-sample", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -413,6 +422,11 @@ def main():
                           "steps from floor(n_steps/3)",
               "grid": [args.nside] * 3, "pn_order": 19, "moments": 400, "rank": args.rank,
               "model": "fokker-planck", "n_gpus": args.gpus,
+              **({"workload": f"{args.nside}^3 z-slabs water [0,3) / bone +1200 HU [3,4) / "
+                              "lung -700 HU [4,7) cm / water, h=0.025 cm, P7 Boltzmann, 100 MeV "
+                              f"+z pencil beam, fixed rank {args.rank}, CFL 0.2, steps from "
+                              "floor(n_steps/3)", "pn_order": 7, "moments": 64,
+                  "model": "boltzmann"} if args.phantom == "slabs" else {}),
               "l2": "inputs larger than L2 (U is n x r doubles = 2.7 GB per factor)",
               "parallelism": f"z-slabs x{world} (NCCL halo planes + Gram allreduce)"
               if world > 1 else "single"}
@@ -427,7 +441,7 @@ def main():
             per.append(cb["value"])
         v = float(np.median(per))
         cb["value"] = v
-        line = {"metric": metric_name(args.nside, args.rank), "value": v, "unit": UNIT,
+        line = {"metric": metric_name(args.nside, args.rank, args.phantom), "value": v, "unit": UNIT,
                 "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -453,7 +467,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         cid = obj[0]
         slab = slabs.plan(args.nside, args.nside, args.nside, world, rank_id)
-    wl = Workload(nside=args.nside, rank=args.rank, device=local, slab=slab, comm_id=cid)
+    wl = Workload(nside=args.nside, rank=args.rank, device=local, slab=slab, comm_id=cid,
+                  **PHANTOM_KW[args.phantom])
     h = wl.solver.h
     n_steps_total = len(wl.edges) - 1
     if wl.k0 + args.warmup + args.steps > n_steps_total:
@@ -536,7 +551,7 @@ def main():
         except Exception as exc:  # noqa: BLE001
             per_beam = {"error": str(exc)[:300]}
     line = {
-        "metric": metric_name(args.nside, args.rank), "value": value, "unit": UNIT,
+        "metric": metric_name(args.nside, args.rank, args.phantom), "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 * dev_s / args.steps,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
