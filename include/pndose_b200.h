@@ -119,8 +119,10 @@ int pnd_truncate(pnd_handle* h, double theta, int rank_min, int rank_max, double
 /* one step of the energy loop (driver.py:578-622): streaming, truncate
  * (truncate_after & 1), scattering, truncate (truncate_after & 2), dose
  * trapezoid; tally_steps adds S * sum_b psi_b(E_lo) to the integrand.
- * out[0..3] = tail after streaming, tail after scattering, rank, defect
- * (defect only when want_defect != 0). */
+ * out[0..7] = tail after streaming, tail after scattering, rank, defect
+ * (defect only when want_defect != 0), the (U, V) ranks entering the
+ * streaming substep and entering the scattering substep (the driver's
+ * augmented-size diagnostics, driver.py:583-601). */
 int pnd_step(pnd_handle* h, double dt, double theta, int rank_min, int rank_max,
              int truncate_after, int tally_steps, int want_defect, double* out);
 int pnd_dose_reset(pnd_handle* h);
@@ -144,6 +146,14 @@ int pnd_stencil_grams(pnd_handle* h, const double* x, int a, const double* y, in
                       double* out);
 /* k_rhs(K, F) = -sum_s (D_s S^-1 K) F_s (dlra.py:168-174); f is ns x r x r. */
 int pnd_k_rhs(pnd_handle* h, const double* k, int r, const double* f, double* out);
+/* The n-side augmentation of streaming_step / scattering_step (the span of
+ * orthonormal_columns([K1, U0]), dlra.py:26-43, 220, 304): u (n x a, orthonormal
+ * columns) and an increment x (n x b); q (n x b, row-major) receives, in its
+ * first *k_out columns, an orthonormal basis of (I - u u^T) x as the device
+ * computes it in the step (Gram-based CGS2 + SVQB with the graded-increment
+ * second level); rank_bound <= 0 means none. */
+int pnd_augment_basis(pnd_handle* h, const double* u, int a, const double* x, int b,
+                      int rank_bound, double* q, int* k_out);
 /* orthonormal_columns(a) (dlra.py:26-43) via device TSQR; q is rows x min(rows, cols),
  * r is min(rows, cols) x cols. Independent of the handle's grid. */
 int pnd_orthonormalize(pnd_handle* h, const double* a, int rows, int cols, double* q, double* r);

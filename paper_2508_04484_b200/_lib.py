@@ -50,6 +50,7 @@ SIGNATURES = {
     "pnd_apply_streaming": [_P, _P, _P],
     "pnd_stencil_grams": [_P, _P, _I, _P, _I, _P],
     "pnd_k_rhs": [_P, _P, _I, _P, _P],
+    "pnd_augment_basis": [_P, _P, _I, _P, _I, _I, _P, _P],
     "pnd_orthonormalize": [_P, _P, _I, _I, _P, _P],
     "pnd_svd_small": [_P, _P, _I, _I, _P, _P, _P],
     "pnd_set_coefficient_tables": [_P, _I, _P, _P, _P, _P, _I, _P, _I, _P, _P, _I, _I, _I, _D,

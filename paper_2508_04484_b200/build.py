@@ -35,7 +35,7 @@ def _sources():
 
 
 def _headers_mtime():
-    hs = list(CSRC.glob("*.h")) + list((ROOT / "include").glob("*.h"))
+    hs = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
     return max((h.stat().st_mtime for h in hs), default=0.0)
 
 

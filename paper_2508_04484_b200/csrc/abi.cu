@@ -543,8 +543,10 @@ int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max
   return guard(hh, [&](Handle& h) {
     double t1 = 0.0, t2 = 0.0;
     int rank = 0;
+    const int ru0 = h.ru, rv0 = h.rv;
     pnd::streaming_step(h, dt);
     if (truncate_after & 1) pnd::truncate(h, theta, rank_min, rank_max, &t1, &rank);
+    const int ru1 = h.ru, rv1 = h.rv;
     pnd::scattering_step(h, dt);
     bool ugram = false;
     if (truncate_after & 2) {
@@ -562,6 +564,10 @@ int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max
       out[1] = t2;
       out[2] = (double)(h.ru < h.rv ? h.ru : h.rv);
       out[3] = defect;
+      out[4] = ru0;  // factor ranks entering the streaming substep
+      out[5] = rv0;
+      out[6] = ru1;  // ... and entering the scattering substep
+      out[7] = rv1;
     }
   });
 }
@@ -714,6 +720,28 @@ int pnd_stencil_grams(pnd_handle* hh, const double* x, int a, const double* y, i
     down(out, O, (size_t)h.g.ns * a * b, h.st);
     CK(cudaStreamSynchronize(h.st));
     o.free_();
+  });
+}
+
+int pnd_augment_basis(pnd_handle* hh, const double* u, int a, const double* x, int b,
+                      int rank_bound, double* q, int* k_out) {
+  return guard(hh, [&](Handle& h) {
+    if (a < 0 || b < 1 || a > 64 || b > 64) pnd::fail(PND_ECONFIG, "augment_basis: 0 <= a, 1 <= b <= 64");
+    h.ua = a;
+    h.uq = 0;
+    if (a > 0) upload_rows(h, h.U.view(h.g, a, h.st), u);
+    NMat X = h.W2.view(h.g, b, h.st);
+    upload_rows(h, X, x);
+    pnd::DBuf c1;
+    double* C1 = c1.get((size_t)(a > 0 ? a : 1) * b);
+    if (a > 0) pnd::gram_xy(h.g, pnd::state_u(h), X, C1, h.part, h.st);
+    const int k = pnd::orth_complement(h, X, a > 0 ? C1 : nullptr, NMat{},
+                                       rank_bound > 0 ? rank_bound : (1 << 30));
+    if (k > 0) download_rows(h, pnd::state_q(h), q, b, 0);
+    CK(cudaStreamSynchronize(h.st));
+    *k_out = k;
+    h.uq = 0;
+    c1.free_();
   });
 }
 

@@ -137,6 +137,10 @@ double orth_defect(Handle& h, bool have_ugram = false);
 double* defect_gram_slot(Handle& h, int ru, int rv);
 // Q (k columns) = orthonormal basis of (I - U U^T) X; C1 = U^T X (device, ua x b; null
 // when U is empty). Returns k; the result is installed as the state's Q.
-int orth_complement(Handle& h, NMat X, const double* C1, NMat X2 = NMat{});
+// rank_bound: an upper bound on rank(X) known from its construction (the
+// scattering source rows); directions beyond it are rounding noise, so the
+// graded-increment second level is skipped once k reaches it.
+int orth_complement(Handle& h, NMat X, const double* C1, NMat X2 = NMat{},
+                    int rank_bound = 1 << 30);
 
 }  // namespace pnd

@@ -80,6 +80,9 @@ double* eye(Handle& h, int b) {
 //   mode 0 (rank revealing): keep lam_j > tol_rel^2 lam_0,
 //          TA = P_k diag(lam_k^-1/2)  ->  Q = (Y - U0 C) TA = Y TA - U0 (C TA)
 //   mode 1 (re-orthogonalisation): TA = P diag(lam^-1/2) P^T
+//   mode 2 (graded increment, level 1 of two): TA = [P_k diag(lam_k^-1/2) | P_rest]
+//          -> W = (Y - U0 C) TA holds Q in its first k columns and the
+//          deflated directions, unnormalised, in the rest
 //   TB = C TA.  info[0] = k;  dinfo[0] = max(|G - I|, |C|)
 // max(|G - I|, |C|) (the block's orthonormality defect) into out[0]
 __global__ void defect_gc_kernel(const double* G, const double* C, int a, int b, double* out) {
@@ -128,7 +131,7 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
   }
   if (tid == 0) {
     int k = b;
-    if (mode == 0) {
+    if (mode == 0 || mode == 2) {
       k = 0;
       while (k < b && keep[k]) ++k;
     }
@@ -144,6 +147,8 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
     double v;
     if (mode == 0) {
       v = P[r * b + c] * scale[c];
+    } else if (mode == 2) {
+      v = P[r * b + c] * (c < k ? scale[c] : 1.0);
     } else {
       v = 0.0;
       for (int j = 0; j < b; ++j) v += P[r * b + j] * scale[j] * P[c * b + j];
@@ -155,6 +160,88 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
     const int r = i / ncol, c = i % ncol;
     double v = 0.0;
     for (int j = 0; j < b; ++j) v += C[r * b + j] * TA[j * ncol + c];
+    TB[i] = v;
+  }
+}
+
+// Level 2 of the augmentation (graded increments). W = [Q | Z] from svqb
+// mode 2, G3 = W^T W, C3 = U0^T W formed from the explicit vectors, so every
+// entry is accurate to eps |w_i| |w_j| -- unlike the level-1 Gram, whose small
+// eigenvalues are lost below eps lam_0. M = G3 - C3^T C3 (W projected out of
+// U0); the columns kept are Q's and every Z column with norm above
+// *floor_p (1e-13 |X|_F: the rounding noise of forming and projecting the
+// increment X = U0 C1 + Y is ~eps |X|, so only real content passes);
+// Ms = D^-1 M_JJ D^-1 (unit diagonal, zero rows and columns outside J) is
+// the well-conditioned Gram of the scaled columns.
+__global__ void level2_gram(const double* G3, const double* C3, int a, int b, int k1,
+                            const double* floor_p, double* Ms, double* dinv) {
+  const int tid = threadIdx.x;
+  __shared__ double d[128];
+  const double floor_abs = *floor_p;
+  for (int j = tid; j < b; j += blockDim.x) {
+    double mjj = G3[j * b + j];
+    for (int t = 0; t < a; ++t) mjj -= C3[t * b + j] * C3[t * b + j];
+    const double nj = mjj > 0.0 ? sqrt(mjj) : 0.0;
+    const bool keep = j < k1 || nj > floor_abs;
+    d[j] = keep ? 1.0 / nj : 0.0;
+    dinv[j] = d[j];
+  }
+  __syncthreads();
+  for (int i = tid; i < b * b; i += blockDim.x) {
+    const int r = i / b, c = i % b;
+    double v = G3[i];
+    for (int t = 0; t < a; ++t) v -= C3[t * b + r] * C3[t * b + c];
+    Ms[i] = v * d[r] * d[c];
+  }
+}
+
+// out[0] = rel * |X|_F, |X|_F^2 = trace(Y^T Y) + |U0^T X|_F^2 (the level-2 floor)
+__global__ void xnorm_kernel(const double* G2, const double* C1, int a, int b, double rel,
+                             double* out) {
+  __shared__ double red[256];
+  const int tid = threadIdx.x;
+  double x2 = 0.0;
+  for (int j = tid; j < b; j += blockDim.x) x2 += G2[j * b + j];
+  if (C1)
+    for (int i = tid; i < a * b; i += blockDim.x) x2 += C1[i] * C1[i];
+  red[tid] = x2;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w) red[tid] += red[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) out[0] = rel * sqrt(red[0] > 0.0 ? red[0] : 0.0);
+}
+
+// SVQB of the scaled level-2 Gram (eigen-pairs P2, mu descending): keep
+// mu > tol * mu_0 (the rest are dependent columns), T = D^-1 P2_k mu_k^-1/2,
+// TB = C3 T; info[0] = k2.
+__global__ void level2_build(const double* C3, int a, int b, const double* dinv,
+                             const double* P2, const double* mu, double tol, double* T,
+                             double* TB, int* info) {
+  __shared__ int k_s;
+  __shared__ double scale[128];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int k = 0;
+    const double m0 = b > 0 ? mu[0] : 0.0;
+    while (k < b && mu[k] > 0.0 && mu[k] > tol * m0) ++k;
+    k_s = k;
+    info[0] = k;
+  }
+  __syncthreads();
+  const int k = k_s;
+  for (int j = tid; j < k; j += blockDim.x) scale[j] = 1.0 / sqrt(mu[j]);
+  __syncthreads();
+  for (int i = tid; i < b * k; i += blockDim.x) {
+    const int r = i / k, c = i % k;
+    T[i] = dinv[r] * P2[r * b + c] * scale[c];
+  }
+  __syncthreads();
+  for (int i = tid; i < a * k; i += blockDim.x) {
+    const int r = i / k, c = i % k;
+    double v = 0.0;
+    for (int j = 0; j < b; ++j) v += C3[r * b + j] * T[j * k + c];
     TB[i] = v;
   }
 }
@@ -204,7 +291,7 @@ void check_singular(Handle& h) {
   }
 }
 
-int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
+int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound) {
   const int a = h.ua, b = X.cols + (X2.p ? X2.cols : 0);
   cudaStream_t st = h.st;
   const Geom& g = h.g;
@@ -227,16 +314,55 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2) {
   svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 0, 1e-7, TA, TB, info, dinfo);
   launched();
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(h.pinned + 11, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   check_singular(h);
-  const int k = *(int*)(h.pinned + 8);
+  int k = *(int*)(h.pinned + 8);
+  const double lam0 = h.pinned[11];
   h.uq = 0;
-  if (k == 0) return 0;
-  // pass 3: Q = Y TA - U0 TB (k cols) -> Q, C3 = U0^T Q, G3 = Q^T Q
-  NMat Qv = h.Q.view(g, k, st);
-  lincomb(g, Y, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
+  // Level 2 (graded increments): the one-pass Gram resolves directions only
+  // down to ~1e-7 of the largest (its eigenvalues carry eps lam_0 absolute
+  // error), where the reference's Householder QR keeps every direction. When
+  // directions were deflated and the increment's rank bound allows more, the
+  // deflated directions are formed explicitly (W = Y' [P_k lam^-1/2 | P_rest]),
+  // their Gram recomputed from the vectors themselves and re-orthonormalised
+  // after column scaling: directions down to 1e-13 of |X| are kept (the
+  // content below that is under T2's 1e-11 bound), rounding noise is not.
+  const bool level2 = k < b && k < rank_bound && lam0 > 0.0;
+  if (k == 0 && !level2) return 0;
+  NMat Qv;
   double* C3 = grams;
-  double* G3 = grams + (size_t)a * k;
+  double* G3 = nullptr;
+  if (level2) {
+    svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 2, 1e-7, TA, TB, info, dinfo);
+    launched();
+    xnorm_kernel<<<1, 256, 0, st>>>(G2, a > 0 ? C1 : nullptr, a, b, 1e-13, dinfo + 1);
+    launched();
+    // pass 3': W = Y TA - U0 TB (b cols) -> Q, C3 = U0^T W, G3 = W^T W
+    NMat W = h.Q.view(g, b, st);
+    lincomb(g, Y, NMat{}, U0, TA, TB, W, grams, h.part, st);
+    double* Ms = slot(h, S_M2, (size_t)b * b);
+    double* dinv = slot(h, S_PC, (size_t)b);
+    level2_gram<<<1, 256, 0, st>>>(grams + (size_t)a * b, grams, a, b, k, dinfo + 1, Ms, dinv);
+    launched();
+    svd_small(Ms, b, b, P, sig, Qt, nullptr, st);
+    level2_build<<<1, 256, 0, st>>>(grams, a, b, dinv, P, sig, 1e-14, TA, TB, info + 2);
+    launched();
+    CK(cudaMemcpyAsync(h.pinned + 8, info + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    k = *(int*)(h.pinned + 8);
+    if (k == 0) return 0;
+    // pass 4': Q = W T - U0 TB (k cols) -> Qa, then swapped into Q
+    Qv = h.Qa.view(g, k, st);
+    lincomb(g, W, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
+    std::swap(h.Q, h.Qa);
+    Qv = h.Q.view(g, k, st);
+  } else {
+    // pass 3: Q = Y TA - U0 TB (k cols) -> Q, C3 = U0^T Q, G3 = Q^T Q
+    Qv = h.Q.view(g, k, st);
+    lincomb(g, Y, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
+  }
+  G3 = grams + (size_t)a * k;
   // the block's defect max(|Q^T Q - I|, |U0^T Q|) decides on a further pass;
   // its SVQB coefficients are only formed when it is needed
   defect_gc_kernel<<<1, 256, 0, st>>>(G3, C3, a, k, dinfo);
@@ -594,7 +720,9 @@ void scattering_step(Handle& h, double dt) {
   // substep 2: U^ = [U0 | orth((I - U0 U0^T) dK)]
   phase(h, PH_ORTH);
   if (forked) CK(cudaStreamWaitEvent(st, h.ev_join, 0));  // dK from the side stream
-  const int k = orth_complement(h, dK, C1);
+  // rank(dK) <= rank of the source rows: one per (material class, beam)
+  const int bound = rank1 ? 1 : (long)h.n_cls * B < b ? h.n_cls * B : b;
+  const int k = orth_complement(h, dK, C1, NMat{}, bound);
   const int ru = a + k;
   phase(h, PH_SCATSMALL);
 

@@ -27,6 +27,8 @@ from .errors import ConfigError
 from .problem import SQRT_4PI, ProblemBundle, export_problem
 
 TRUNCATE_FLAGS = {"streaming": 1, "scattering": 2, "both": 3}
+# largest factor rank the step kernels take (an augmented state holds 2x this)
+MAX_RANK = 64
 
 
 @dataclass
@@ -140,7 +142,7 @@ class DeviceSolver:
 
     def step(self, dt: float, want_defect: bool = True):
         b = self.bundle
-        out = np.zeros(4)
+        out = np.zeros(8)
         self.h.call(
             "pnd_step", float(dt), float(b.truncation_tolerance), int(b.rank_min),
             int(b.rank_max), TRUNCATE_FLAGS[b.truncate_after],
@@ -178,6 +180,31 @@ class DeviceSolver:
         self.h.close()
 
 
+def augmented_sizes(n, m, a0, b0, a1, b1):
+    """state.u.size + state.s.size + state.v.size right after each substep,
+    as the reference's loop records them (driver.py:583-596): the sizes of
+    its Householder bases, which depend only on the incoming ranks --
+    streaming: U^ = orth([K1, U0]) (n x min(n, a+b)), V^ = orth([L1, V0])
+    (m x min(m, a+b)), dlra.py:213-225; scattering: U^ = orth([K1, U0])
+    (n x min(n, 2a)), V^ = orth([l3, V~]) with V~ m x min(m, a), dlra.py:270-322."""
+    cu, cv = min(n, a0 + b0), min(m, a0 + b0)
+    du, dv = min(n, 2 * a1), min(m, a1 + min(m, a1))
+    return n * cu + cu * cv + m * cv, n * du + du * dv + m * dv
+
+
+def check_rank_cap(bundle: ProblemBundle):
+    """Ranks the device kernels support: refuse a run whose
+    rank_max cannot be reached before it starts, not at the step where the
+    adaptive rank first passes the cap (the whole run would be lost)."""
+    cap = MAX_RANK if bundle.truncate_after == "both" else MAX_RANK // 2
+    if bundle.rank_max > cap and bundle.truncation_tolerance < 1e300:
+        raise ConfigError(
+            f"rank_max={bundle.rank_max} exceeds the device's rank capacity {cap} for "
+            f"truncate_after='{bundle.truncate_after}'")
+    if bundle.rank_min > cap:
+        raise ConfigError(f"rank_min={bundle.rank_min} exceeds the device's rank capacity {cap}")
+
+
 def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0,
                solver="dlra", slab=None, comm_id=None, resume=None,
                checkpoint_at=None) -> SimulationResult:
@@ -194,6 +221,7 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         return _run_fullrank(bundle, max_steps, device, slab, comm_id)
     t_start = time.perf_counter()
     b = bundle
+    check_rank_cap(b)
     n, m = b.n_cells, b.n_moments
     solver_ = DeviceSolver(b, device, slab=slab, comm_id=comm_id)
     solver_.init_state()
@@ -214,6 +242,7 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         solver_.set_coefficients(e_hi, e_lo)
         out = solver_.step(e_hi - e_lo, want_defect)
         r = int(out[2])
+        peak_transient = max(peak_transient, *augmented_sizes(n, m, *out[4:8].astype(int)))
         for idx, flag in ((0, 1), (1, 2)):
             if TRUNCATE_FLAGS[b.truncate_after] & flag:
                 tail = float(out[idx])
@@ -222,7 +251,6 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         max_defect = max(max_defect, float(out[3]))
         ranks.append((k, float(e_lo), r))
         peak_state = max(peak_state, n * r + r * r + m * r)
-        peak_transient = max(peak_transient, n * 2 * r + 4 * r * r + m * 2 * r)
     deposited = solver_.dose()
     lo, hi = solver_.rows
     unc = None
@@ -313,14 +341,20 @@ def write_dose_volume(result: SimulationResult, path, binary: bool = True, slab=
 
 
 def run_simulation(config, solver: str = "dlra"):
-    """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541).
+    """Drop-in for pndose.driver.run_simulation(config, solver) (driver.py:541-666).
 
-    `config` is a reference ProblemConfig. Problem assembly and the per-beam
-    tracer setup (material keys, coefficient closures; driver.py:398-436) are
-    the reference's unchanged host code; every beam's march and deposit
-    (raytracer.trace_beam) and the energy loop run on the GPU.
-    solver="fullrank" runs the dense oracle on the device (fullrank.cu);
-    solver="dlra-cpu" hands the whole run back to the reference.
+    `config` is a reference ProblemConfig and the return value is the
+    reference's own SimulationResult (problem, DoseGrid(grid, deposited,
+    dose), rank_history, diagnostics with every key the reference sets,
+    fluxes), so write_outputs (driver.py:809-849) and the CLI (cli.py:18-37)
+    consume it unchanged. Problem assembly and the per-beam tracer setup
+    (material keys, coefficient closures; driver.py:398-436) are the
+    reference's host code; every beam's march and deposit (raytracer.
+    trace_beam) and the energy loop run on the GPU. solver="fullrank" runs
+    the dense oracle on the device (fullrank.cu); solver="dlra-cpu" hands
+    the whole run back to the reference. Errors are the reference's classes
+    (errors.py binds pndose.errors when it is importable), so cli.py:130 maps
+    them to its exit codes.
     """
     from pndose import driver as ref_driver  # the reference package
     from pndose.angular import beam_projection
@@ -328,9 +362,17 @@ def run_simulation(config, solver: str = "dlra"):
     from . import raytracer as dev_tracer
 
     if solver == "dlra-cpu":
-        return ref_driver.run_simulation(config, solver="dlra")
+        if _REFERENCE_RUN is not None:  # routed by install(): the original function
+            return _REFERENCE_RUN(config, solver="dlra")
+        try:  # routed by the source edit of INTEGRATION.md §2, which keeps "dlra-cpu"
+            return ref_driver.run_simulation(config, solver="dlra-cpu")
+        except ConfigError as exc:  # not routed at all: the reference's own "dlra"
+            if "unknown solver" not in str(exc):
+                raise
+            return ref_driver.run_simulation(config, solver="dlra")
     if solver not in ("dlra", "fullrank"):
         raise ConfigError(f"unknown solver '{solver}'")
+    t_start = time.perf_counter()
     problem = ref_driver.assemble_problem(config)
     ref_trace = ref_driver.trace_beam
     ref_driver.trace_beam = dev_tracer.trace_beam
@@ -340,8 +382,75 @@ def run_simulation(config, solver: str = "dlra"):
         ref_driver.trace_beam = ref_trace
     t_ms = [beam_projection(config.pn_order, bm.direction) for bm in config.beams]
     bundle = ProblemBundle.from_arrays(export_problem(problem, fluxes, t_ms))
-    return run_bundle(bundle, solver=solver)
+    res = run_bundle(bundle, solver=solver)
+    return reference_result(ref_driver, problem, fluxes, res, solver, t_start)
 
 
-__all__ = ["DeviceSolver", "run_bundle", "run_simulation", "SimulationResult", "DoseGrid",
-           "SQRT_4PI", "math", "orthonormal_columns"]
+_REFERENCE_RUN = None
+
+
+def install():
+    """Route the reference's run_simulation to the device
+    without editing its source: pndose.driver.run_simulation -- and the name
+    pndose.cli imported from it -- become this module's run_simulation;
+    solver="dlra-cpu" still reaches the original CPU function."""
+    global _REFERENCE_RUN
+    from pndose import driver as ref_driver
+
+    if getattr(ref_driver.run_simulation, "_pnd_b200", False):
+        return
+    _REFERENCE_RUN = ref_driver.run_simulation
+
+    def routed(config, solver: str = "dlra"):
+        return run_simulation(config, solver)
+
+    routed._pnd_b200 = True
+    routed.__doc__ = run_simulation.__doc__
+    ref_driver.run_simulation = routed
+    try:
+        from pndose import cli as ref_cli
+    except ImportError:
+        return
+    ref_cli.run_simulation = routed
+
+
+def reference_result(ref_driver, problem, fluxes, res: SimulationResult, solver: str,
+                     t_start: float):
+    """The reference's SimulationResult (driver.py:494-500) for a device run:
+    DoseGrid with the problem's grid, the reference's diagnostics keys and
+    order (driver.py:634-659; solver named as the caller asked), the traced
+    fluxes, runtime over the whole pipeline."""
+    d = res.diagnostics
+    n, m = d["n_cells"], d["n_moments"]
+    full = n * m
+    dose = ref_driver.DoseGrid(grid=problem.grid, deposited=res.dose.deposited,
+                               dose=res.dose.dose)
+    ranks = [r for _, _, r in res.rank_history]
+    dlra = solver == "dlra"
+    diagnostics = {
+        "solver": solver,
+        "n_cells": n,
+        "n_moments": m,
+        "n_steps": d["n_steps"],
+        "energy_step_mev": d["energy_step_mev"],
+        "max_orthonormality_defect": float(d.get("max_orthonormality_defect", 0.0)),
+        "max_truncation_tail": float(d.get("max_truncation_tail", 0.0)),
+        "tail_violations": int(d.get("tail_violations", 0)),
+        "mean_rank": float(np.mean(ranks)),
+        "max_rank": int(max(ranks)),
+        "peak_state_numbers": int(d["peak_state_numbers"] if dlra else full),
+        "peak_transient_numbers": int(d["peak_transient_numbers"] if dlra else full),
+        "fullrank_numbers": int(full),
+        "state_memory_fraction": float((d["peak_state_numbers"] if dlra else full) / full),
+        "negativity": dose.negativity,
+        "uncollided_undershoot": float(min((f.undershoot for f in fluxes), default=0.0)),
+        "runtime_s": time.perf_counter() - t_start,
+        "rays_per_beam": [f.n_rays for f in fluxes],
+    }
+    return ref_driver.SimulationResult(problem=problem, dose=dose,
+                                       rank_history=res.rank_history,
+                                       diagnostics=diagnostics, fluxes=fluxes)
+
+
+__all__ = ["DeviceSolver", "run_bundle", "run_simulation", "reference_result", "install",
+           "SimulationResult", "DoseGrid", "SQRT_4PI", "math", "orthonormal_columns"]

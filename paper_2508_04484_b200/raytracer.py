@@ -309,6 +309,22 @@ class UncollidedFlux:
     def group_energies(self):
         return EnergySpace.of(self.space).centers
 
+    @property
+    def undershoot(self) -> float:
+        """Most negative flux value (raytracer.py:432-435; 0 if none)."""
+        return float(min(self.values.min(initial=0.0), 0.0))
+
+    def at_energy(self, e_mev) -> np.ndarray:
+        """Group-centre interpolation, zero outside (raytracer.py:437-449)."""
+        centers = self.group_energies
+        if e_mev <= centers[0] or e_mev >= centers[-1]:
+            j = 0 if e_mev <= centers[0] else self.values.shape[1] - 1
+            inside = self.space.e_min <= e_mev <= self.space.e_max
+            return self.values[:, j] if inside else np.zeros(self.values.shape[0])
+        j = int(np.searchsorted(centers, e_mev)) - 1
+        w = (e_mev - centers[j]) / (centers[j + 1] - centers[j])
+        return (1.0 - w) * self.values[:, j] + w * self.values[:, j + 1]
+
 
 def trace_beam_ops(beam, grid, space, key_of_cell, gmats, s_min, n_side=21, span_sigmas=3.0,
                    max_step=MAX_STEP_CM):

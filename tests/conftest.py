@@ -38,3 +38,25 @@ def steps_npz():
 @pytest.fixture(scope="session")
 def traverse_npz():
     return golden("traverse.npz")
+
+
+# Measured GPU-vs-reference deviations, collected by the parity tests and
+# written at session end to $PND_PARITY_OUT (the round's profiles/parity_rNN.json
+# is a copy of that file from the GPU box): every deviation next to its bound.
+PARITY_RECORDS = []
+
+
+@pytest.fixture(scope="session")
+def parity_log():
+    return PARITY_RECORDS
+
+
+def pytest_sessionfinish(session, exitstatus):
+    import json
+    import os
+
+    path = os.environ.get("PND_PARITY_OUT")
+    if not path or not PARITY_RECORDS:
+        return
+    Path(path).parent.mkdir(parents=True, exist_ok=True)
+    Path(path).write_text(json.dumps({"records": PARITY_RECORDS}, indent=1) + "\n")

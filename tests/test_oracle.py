@@ -139,6 +139,29 @@ def test_oracle_traversal_bit_exact(traverse_npz):
             np.testing.assert_array_equal(t1.view(np.int64), T[p + "t1"][lo:hi].view(np.int64))
 
 
+# ------------------------------------------------------------- T2 at the benchmarked physics
+@pytest.mark.parametrize("tag,k", [("fp19", 25), ("slabs7", 150)])
+def test_oracle_lockstep_substeps(tag, k):
+    """The oracle's substeps from the reference's own states at the bench's
+    physics (P19 Fokker-Planck m = 400; three-class Boltzmann P7; rank 20)
+    reproduce the reference's augmented factors (T2, lock_<tag>.npz)."""
+    L = golden(f"lock_{tag}.npz")
+    B = golden(f"bundle_{tag}.npz")
+    grid = grid_of(L["grid"])
+    ops = dlra_np.Ops(list(B["eig_v"]), list(B["lam_plus"]), list(B["lam_minus"]))
+    p = f"k{k}_"
+    dt, inv_s = float(L[p + "dt"]), L[p + "inv_s"]
+    u, s, v = dlra_np.streaming_step(L[p + "u"], L[p + "s"], L[p + "v"], dt, inv_s, grid, ops)
+    want = L[p + "sa_u"] @ L[p + "sa_s"] @ L[p + "sa_v"].T
+    assert rel(u @ s @ v.T, want) < 1e-11
+    sources = list(zip(L[p + "psi"], L["t_ms"]))
+    u, s, v = dlra_np.scattering_step(L[p + "st_u"], L[p + "st_s"], L[p + "st_v"], dt,
+                                      L["weights"], inv_s, L[p + "g_diags"], L[p + "sigma_t"],
+                                      sources)
+    want = L[p + "ca_u"] @ L[p + "ca_s"] @ L[p + "ca_v"].T
+    assert rel(u @ s @ v.T, want) < 1e-11
+
+
 # ------------------------------------------------------------- end to end
 FLOORS = json.loads((GOLDEN / "floors.json").read_text())
 

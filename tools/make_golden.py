@@ -394,6 +394,102 @@ def rank1_raw():
     return raw
 
 
+def fp19_raw():
+    """The benchmarked physics (BASELINE configs[1]: water, P19 Fokker-Planck,
+    m = 400, fixed rank 20) on a 10 x 10 x 12 grid the reference finishes in
+    seconds per step."""
+    return {
+        "name": "fp19",
+        "grid": {"nx": 10, "ny": 10, "nz": 12,
+                 "delta_x_cm": 0.1, "delta_y_cm": 0.1, "delta_z_cm": 0.1},
+        "phantom": {"background_hu": 0.0},
+        "beams": [{"direction": [0, 0, 1], "energy_mev": 30.0, "position_cm": [0.5, 0.5, 0.0],
+                   "sigma_xy_cm": 0.2}],
+        "model": "fokker-planck",
+        "pn_order": 19,
+        "transport": {"cfl_number": 0.2, "truncation_tolerance": 1e300,
+                      "rank_min": 20, "rank_max": 20},
+        "energy": {"groups": 128},
+        "rays": {"n_side": 11},
+    }
+
+
+def slabs7_raw():
+    """BASELINE configs[2]'s physics (water / bone / lung z-slabs, Boltzmann
+    P7, fixed rank 20) on a 10 x 10 x 24 grid: water z < 0.6 cm, bone
+    [0.6, 0.9), lung [0.9, 1.5), water beyond."""
+    return {
+        "name": "slabs7",
+        "grid": {"nx": 10, "ny": 10, "nz": 24,
+                 "delta_x_cm": 0.1, "delta_y_cm": 0.1, "delta_z_cm": 0.1},
+        "phantom": {
+            "background_hu": 0.0,
+            "boxes": [
+                {"origin_cm": [0, 0, 0.6], "size_cm": [1, 1, 0.3], "hu": 1200.0},
+                {"origin_cm": [0, 0, 0.9], "size_cm": [1, 1, 0.6], "hu": -700.0},
+            ],
+        },
+        "beams": [{"direction": [0, 0, 1], "energy_mev": 40.0, "position_cm": [0.5, 0.5, 0.0],
+                   "sigma_xy_cm": 0.2}],
+        "model": "boltzmann",
+        "pn_order": 7,
+        "transport": {"cfl_number": 0.2, "truncation_tolerance": 1e300,
+                      "rank_min": 20, "rank_max": 20},
+        "energy": {"groups": 128},
+        "rays": {"n_side": 11},
+    }
+
+
+def run_lockstep_record(tag, raw, record):
+    """The reference's own energy loop (driver.py:577-622, the same calls in
+    the same order as run_simulation) recording, at the steps in `record`,
+    the input state, the frozen contexts and the factors after each substep
+    and truncation: the T2 per-step fixtures (lock_<tag>.npz). Each substep
+    also runs from the reference's own previous output, so a GPU test can
+    check every substep of every recorded step in isolation."""
+    config = driver.ProblemConfig.from_dict(raw)
+    problem = driver.assemble_problem(config)
+    fluxes = driver.trace_all_beams(problem)
+    t_ms = [angular.beam_projection(config.pn_order, b.direction) for b in config.beams]
+    edges = driver.pseudo_time_edges(problem)
+    n, m = problem.n_cells, problem.n_moments
+    policy = dlra.TruncationPolicy(config.truncation_tolerance, rank_min=config.rank_min,
+                                   rank_max=config.rank_max)
+    state = dlra.LowRankState.zero(n, m, min(config.rank_min, n, m), seed=config.seed)
+    out = {"steps": np.array(sorted(record)), "edges": edges,
+           "weights": np.asarray(problem.material.atomic_densities),
+           "t_ms": np.stack(t_ms)}
+    g = problem.grid  # the P_N operators are the bundle's (bundle_<tag>.npz)
+    out["grid"] = np.array([g.nx, g.ny, g.nz, g.dx, g.dy, g.dz])
+    for k in range(max(record) + 1):
+        e_hi, e_lo = edges[k], edges[k + 1]
+        dt = e_hi - e_lo
+        sc, cc, _ = driver.step_contexts(problem, fluxes, t_ms, e_hi, e_lo)
+        p = f"k{k}_"
+        if k in record:
+            out.update({p + "u": state.u, p + "s": state.s, p + "v": state.v,
+                        p + "dt": np.array(dt), p + "inv_s": sc.inv_s,
+                        p + "g_diags": cc.g_diags, p + "sigma_t": cc.sigma_t,
+                        p + "psi": np.array([s[0] for s in cc.sources])})
+        state = dlra.streaming_step(state, dt, sc)
+        if k in record:
+            out.update({p + "sa_u": state.u, p + "sa_s": state.s, p + "sa_v": state.v})
+        if config.truncate_after in ("streaming", "both"):
+            state, tail = dlra.truncate(state, policy)
+            if k in record:
+                out.update({p + "st_u": state.u, p + "st_s": state.s, p + "st_v": state.v,
+                            p + "st_tail": np.array(tail)})
+        state = dlra.scattering_step(state, dt, cc)
+        if k in record:
+            out.update({p + "ca_u": state.u, p + "ca_s": state.s, p + "ca_v": state.v})
+        if config.truncate_after in ("scattering", "both"):
+            state, tail = dlra.truncate(state, policy)
+            if k in record:
+                out.update({p + "ct_u": state.u, p + "ct_s": state.s, p + "ct_v": state.v,
+                            p + "ct_tail": np.array(tail)})
+    save(f"lock_{tag}.npz", **out)
+
+
 def run_e2e(tag, raw, with_contexts=True):
     t0 = time.perf_counter()
     config = driver.ProblemConfig.from_dict(raw)
@@ -438,11 +534,24 @@ def make_e2e(which):
         "hetero": hetero_raw(),
         "fp": fp_raw(),
         "rank1": rank1_raw(),
+        "fp19": fp19_raw(),
+        "slabs7": slabs7_raw(),
     }
     for tag, raw in cases.items():
         if which and tag not in which:
             continue
         run_e2e(tag, raw, with_contexts=(tag != "lockstep"))
+
+
+def make_lock(which):
+    """T2 per-step fixtures at the benchmarked physics (lock_<tag>.npz)."""
+    cases = {"fp19": (fp19_raw(), {2, 25, 50}), "slabs7": (slabs7_raw(), {2, 150, 300})}
+    for tag, (raw, record) in cases.items():
+        if which and tag not in which:
+            continue
+        t0 = time.perf_counter()
+        run_lockstep_record(tag, raw, record)
+        print(f"  lock {tag}: {time.perf_counter() - t0:.1f}s")
 
 
 def make_march():
@@ -592,3 +701,6 @@ if __name__ == "__main__":
     e2e = {w[4:] for w in what if w.startswith("e2e:")}
     if not what or "e2e" in what or e2e:
         make_e2e(e2e)
+    lock = {w[5:] for w in what if w.startswith("lock:")}
+    if not what or "lock" in what or lock:
+        make_lock(lock)
