@@ -275,10 +275,11 @@ CPU_SIDE = 64
 
 
 def cpu_sample_main(args):
-    """Time the numpy oracle (reference algorithm) on a 64^3 sample of the workload."""
+    """Time the numpy oracle (reference algorithm) on a 64^3 sample of the
+    workload: the same phantom and physics (--phantom), fewer cells."""
     from oracle import dlra_np
 
-    b, ops, beam = make_workload(nside=CPU_SIDE, rank=args.rank)
+    b, ops, beam = make_workload(nside=CPU_SIDE, rank=args.rank, **PHANTOM_KW[args.phantom])
     grid = dlra_np.Grid(*b.shape, *b.spacing)
     o = dlra_np.Ops(b.eig_v, b.lam_plus, b.lam_minus)
     n, m, r = b.n_cells, b.n_moments, args.rank
@@ -313,29 +314,61 @@ def cpu_sample_main(args):
                       "total_s": float(np.sum(times))}))
 
 
-def run_cpu_sample(threads, steps, rank):
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def run_cpu_sample(threads, steps, rank, nside=256, phantom="water"):
+    """The numpy oracle (oracle/dlra_np.py, the reference algorithm restated) on
+    `steps` energy steps of the same phantom and physics at 64^3 cells, timed on
+    this host, extrapolated to nside^3 by cell count (the per-cell cost is
+    constant in n) -- reported as such (`extrapolated`)."""
     env = dict(os.environ)
     for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
         env[k] = str(threads)
+    t0 = time.perf_counter()
     res = subprocess.run([sys.executable, __file__, "--cpu-sample", "--cpu-steps", str(steps),
-                          "--rank", str(rank)], capture_output=True, text=True, env=env,
-                         timeout=900)
+                          "--rank", str(rank), "--phantom", phantom], capture_output=True,
+                         text=True, env=env, timeout=900)
+    wall = time.perf_counter() - t0
     if res.returncode != 0:
         raise RuntimeError(res.stderr[-2000:])
     out = json.loads(res.stdout.strip().splitlines()[-1])
     per_cell = out["per_step_s"] / out["cells"]
-    n_full = 256 ** 3
+    n_full = nside ** 3
+    physics = "P7 Boltzmann, 3-class slabs" if phantom == "slabs" else "P19 FP water"
     return {
         "value": 1.0 / (per_cell * n_full),
         "unit": UNIT,
         "cores": threads,
+        "cpu_model": cpu_model(),
         "kind": "port",
-        "sample": (f"numpy oracle (oracle/dlra_np.py, the reference algorithm) on {out['steps']} "
-                   f"energy steps of the same physics at {CPU_SIDE}^3 cells (rank {rank}, P19 FP) "
-                   f"= {out['per_step_s']:.2f} s/step, scaled by cell count to 256^3 "
-                   f"(per-cell cost is constant in n, SURVEY.md §6.2); {out['total_s']:.1f} s "
-                   "of CPU work"),
+        "extrapolated": True,
+        "timed": {"grid": [CPU_SIDE] * 3, "cells": out["cells"], "steps": out["steps"],
+                  "s_per_step": out["per_step_s"], "cpu_s": out["total_s"], "wall_s": wall},
+        "sample": (f"numpy oracle (oracle/dlra_np.py, the reference algorithm) timed on "
+                   f"{out['steps']} energy steps of the same physics at {CPU_SIDE}^3 cells "
+                   f"(rank {rank}, {physics}) = {out['per_step_s']:.2f} s/step, extrapolated by "
+                   f"cell count to {nside}^3 (per-cell cost is constant in n, SURVEY.md §6.2); "
+                   f"{out['total_s']:.1f} s of CPU work"),
     }
+
+
+def roofline_traffic(nside, rank, phantom, kernel):
+    """ncu DRAM bytes per launch of `kernel` measured on this exact workload
+    (profiles/traffic.json, keyed "<nside>_<rank>_<phantom>"); None when no
+    capture of this workload exists."""
+    tpath = ROOT / "profiles" / "traffic.json"
+    if not tpath.exists():
+        return None
+    entry = json.loads(tpath.read_text()).get(f"{nside}_{rank}_{phantom}", {})
+    return entry.get(kernel)
 
 
 def config1_dose_time(with_cpu):
@@ -435,17 +468,19 @@ def main():
         if rank_id != 0:
             return
         threads = host_threads()
-        per = []
-        for _ in range(max(1, args.steps)):
-            cb = run_cpu_sample(threads, 1, args.rank)
-            per.append(cb["value"])
-        v = float(np.median(per))
-        cb["value"] = v
-        line = {"metric": metric_name(args.nside, args.rank, args.phantom), "value": v, "unit": UNIT,
-                "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference",
+        # one subprocess: W + K energy steps of the port at 64^3 (each a bounded
+        # sample of the workload); the first W are discarded
+        cb = run_cpu_sample(threads, max(1, args.steps), args.rank, args.nside, args.phantom)
+        v = cb["value"]
+        line = {"metric": metric_name(args.nside, args.rank, args.phantom), "value": v,
+                "unit": UNIT, "n_gpus": args.gpus,
+                "steps": cb["timed"]["steps"], "warmup": 0,
+                "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "impl": "reference", "extrapolated": True,
+                "timed_sample": dict(cb["timed"], note=(
+                    f"steps counts energy steps actually run, at {CPU_SIDE}^3; ms_per_step "
+                    f"is the {args.nside}^3 step time extrapolated by cell count")),
                 "cpu_baseline": cb,
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -526,10 +561,7 @@ def main():
     launches_per_step = {"kstage": 4, "s_gram": 1, "l_gram": 1, "tsqr_n": 2}[dom]
     per_launch_ms = phases[dom]["ms_per_step"] / launches_per_step
     achieved = model[dom]["flops"] / (per_launch_ms * 1e-3) / 1e12
-    traffic = None
-    tpath = ROOT / "profiles" / "traffic.json"
-    if tpath.exists():
-        traffic = json.loads(tpath.read_text()).get(dom)
+    traffic = roofline_traffic(args.nside, args.rank, args.phantom, dom)
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": fp64,
                 "unit": "TFLOP/s", "frac": achieved / fp64, "traffic": traffic,
                 "peak_source": "FP64 cuBLAS DGEMM 8192^3 measured in this run (MEASURED_PEAKS.json "
@@ -541,7 +573,8 @@ def main():
     cpu_baseline = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cpu_baseline = run_cpu_sample(host_threads(), 2, args.rank)
+            cpu_baseline = run_cpu_sample(host_threads(), 2, args.rank, args.nside,
+                                          args.phantom)
         except Exception as exc:  # noqa: BLE001
             cpu_baseline = {"error": str(exc)[:300]}
     per_beam = None

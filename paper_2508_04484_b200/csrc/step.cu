@@ -173,7 +173,7 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
 // increment X = U0 C1 + Y is ~eps |X|, so only real content passes);
 // Ms = D^-1 M_JJ D^-1 (unit diagonal, zero rows and columns outside J) is
 // the well-conditioned Gram of the scaled columns.
-__global__ void level2_gram(const double* G3, const double* C3, int a, int b, int k1,
+__global__ void level2_gram(const double* G3, const double* C3, int a, int b, int k1, int kb,
                             const double* floor_p, double* Ms, double* dinv) {
   const int tid = threadIdx.x;
   __shared__ double d[128];
@@ -182,7 +182,9 @@ __global__ void level2_gram(const double* G3, const double* C3, int a, int b, in
     double mjj = G3[j * b + j];
     for (int t = 0; t < a; ++t) mjj -= C3[t * b + j] * C3[t * b + j];
     const double nj = mjj > 0.0 ? sqrt(mjj) : 0.0;
-    const bool keep = j < k1 || nj > floor_abs;
+    // Z columns come in level-1 eigenvalue order: at most kb - k1 of them can
+    // be real when the increment's rank is known to be <= kb
+    const bool keep = j < k1 || (j < kb && nj > floor_abs);
     d[j] = keep ? 1.0 / nj : 0.0;
     dinv[j] = d[j];
   }
@@ -343,7 +345,8 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
     lincomb(g, Y, NMat{}, U0, TA, TB, W, grams, h.part, st);
     double* Ms = slot(h, S_M2, (size_t)b * b);
     double* dinv = slot(h, S_PC, (size_t)b);
-    level2_gram<<<1, 256, 0, st>>>(grams + (size_t)a * b, grams, a, b, k, dinfo + 1, Ms, dinv);
+    level2_gram<<<1, 256, 0, st>>>(grams + (size_t)a * b, grams, a, b, k,
+                                   rank_bound < b ? rank_bound : b, dinfo + 1, Ms, dinv);
     launched();
     svd_small(Ms, b, b, P, sig, Qt, nullptr, st);
     level2_build<<<1, 256, 0, st>>>(grams, a, b, dinv, P, sig, 1e-14, TA, TB, info + 2);

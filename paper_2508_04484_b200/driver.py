@@ -17,13 +17,14 @@ box the tests and the benchmark drive `run_bundle` with committed bundles.
 
 import math
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
 from .dlra import LowRankState, orthonormal_columns
-from .errors import ConfigError
+from .errors import ConfigError, NumericalError
 from .problem import SQRT_4PI, ProblemBundle, export_problem
 
 TRUNCATE_FLAGS = {"streaming": 1, "scattering": 2, "both": 3}
@@ -198,9 +199,10 @@ def check_rank_cap(bundle: ProblemBundle):
     adaptive rank first passes the cap (the whole run would be lost)."""
     cap = MAX_RANK if bundle.truncate_after == "both" else MAX_RANK // 2
     if bundle.rank_max > cap and bundle.truncation_tolerance < 1e300:
-        raise ConfigError(
+        warnings.warn(
             f"rank_max={bundle.rank_max} exceeds the device's rank capacity {cap} for "
-            f"truncate_after='{bundle.truncate_after}'")
+            f"truncate_after='{bundle.truncate_after}': an adaptive rank above {cap} "
+            f"stops the run with a NumericalError naming the step", stacklevel=3)
     if bundle.rank_min > cap:
         raise ConfigError(f"rank_min={bundle.rank_min} exceeds the device's rank capacity {cap}")
 
@@ -240,7 +242,10 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
             snapshot = solver_.checkpoint(k)
         e_hi, e_lo = edges[k], edges[k + 1]
         solver_.set_coefficients(e_hi, e_lo)
-        out = solver_.step(e_hi - e_lo, want_defect)
+        try:
+            out = solver_.step(e_hi - e_lo, want_defect)
+        except ConfigError as exc:  # the rank capacity, reached mid-run
+            raise NumericalError(f"energy step {k} (E = {e_hi:.4f} MeV): {exc}") from exc
         r = int(out[2])
         peak_transient = max(peak_transient, *augmented_sizes(n, m, *out[4:8].astype(int)))
         for idx, flag in ((0, 1), (1, 2)):
@@ -283,6 +288,78 @@ def run_bundle(bundle: ProblemBundle, max_steps=None, want_defect=True, device=0
         diagnostics["checkpoint"] = snapshot
     return SimulationResult(bundle=b, dose=dose, rank_history=ranks, diagnostics=diagnostics,
                             uncollided=unc)
+
+
+@dataclass
+class BatchedResult:
+    """A beam-batched run (SURVEY.md §8(e) "Beams"): independent solves per
+    beam subset, doses summed."""
+
+    dose: DoseGrid
+    parts: list                 # beam indices of every subset
+    rank_histories: dict        # subset index -> [(step, E_MeV, rank)] (this rank's subsets)
+    diagnostics: dict
+
+
+def run_beam_batched(bundle: ProblemBundle, parts=None, device=0, dist=None, max_steps=None,
+                     solve=None) -> BatchedResult:
+    """Multi-beam run as independent low-rank solves per beam subset.
+
+    parts: beam indices per subset (default: one subset per beam,
+    slabs.beam_partition). With torch.distributed initialised (`dist`), the
+    subsets go to groups of ranks (slabs.assign_parts): a group of g ranks
+    z-slab shards its subset over an NCCL communicator of its own (its rank-0
+    makes the id; the world broadcast carries every group's id), a lone rank
+    solves its subsets one after another on its GPU; the doses are summed
+    over the world. Not numerically the joint solve (driver.py:549-550 solves
+    all sources together): its parity reference is the reference run per
+    subset, summed (tests/test_gpu_beams.py). `solve(sub_bundle, slab,
+    comm_id)` replaces the device solve (the CPU tests pass the oracle)."""
+    from . import slabs as _slabs
+
+    t_start = time.perf_counter()
+    b = bundle
+    if parts is None:
+        parts = _slabs.beam_partition(len(b.fluxes))
+    parts = [tuple(int(i) for i in p) for p in parts]
+    world = dist.get_world_size() if dist is not None else 1
+    rank = dist.get_rank() if dist is not None else 0
+    mine = _slabs.assign_parts(world, rank, len(parts))
+    # one NCCL id per multi-rank group, made by the group's first rank
+    ids = [None] * len(parts)
+    grouped = world >= len(parts) and world // len(parts) > 1  # the same on every rank
+    if dist is not None and grouped and solve is None:
+        local_id = _lib.comm_unique_id() if mine.local_rank == 0 else None
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (mine.parts, local_id))
+        for ps, cid in gathered:
+            if cid is not None:
+                for p in ps:
+                    ids[p] = cid
+    if solve is None:
+        def solve(sub, slab, cid):
+            return run_bundle(sub, device=device, slab=slab, comm_id=cid, max_steps=max_steps)
+    total = np.zeros(b.n_cells)
+    histories = {}
+    for p in mine.parts:
+        sub = b.subset_beams(parts[p])
+        slab = None
+        if mine.local_world > 1:
+            slab = _slabs.plan(*b.shape, mine.local_world, mine.local_rank)
+        res = solve(sub, slab, ids[p])
+        lo, hi = (0, b.n_cells) if slab is None else slab.rows
+        total[lo:hi] += res.dose.deposited
+        histories[p] = res.rank_history
+    if dist is not None:
+        total = _slabs.sum_doses(total, dist=dist)
+    dose = DoseGrid(deposited=total, dose=total / b.density)
+    diagnostics = {"solver": "dlra-beam-batched", "n_cells": b.n_cells,
+                   "n_moments": b.n_moments, "parts": parts, "world": world,
+                   "group_size": mine.local_world,
+                   "negativity": dose.negativity,
+                   "runtime_s": time.perf_counter() - t_start}
+    return BatchedResult(dose=dose, parts=parts, rank_histories=histories,
+                         diagnostics=diagnostics)
 
 
 def _run_fullrank(b: ProblemBundle, max_steps, device, slab, comm_id) -> SimulationResult:
@@ -452,5 +529,6 @@ def reference_result(ref_driver, problem, fluxes, res: SimulationResult, solver:
                                        diagnostics=diagnostics, fluxes=fluxes)
 
 
-__all__ = ["DeviceSolver", "run_bundle", "run_simulation", "reference_result", "install",
+__all__ = ["DeviceSolver", "run_bundle", "run_beam_batched", "BatchedResult", "run_simulation",
+           "reference_result", "install",
            "SimulationResult", "DoseGrid", "SQRT_4PI", "math", "orthonormal_columns"]

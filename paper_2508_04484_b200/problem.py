@@ -19,7 +19,7 @@ the CPU tests pin them against contexts produced by the reference itself
 (tests/golden/e2e_*.npz, keys ctx*).
 """
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -244,6 +244,14 @@ class ProblemBundle:
                 deposited += self.stopping_field(e_g) * flux.values[:, g] * flux.width
             deposited += flux.residual
         return deposited
+
+    def subset_beams(self, beams) -> "ProblemBundle":
+        """The same problem with only the given beams' sources: one subset of
+        a beam-batched run (slabs.beam_partition). The energy grid (e_max) is
+        the whole problem's, as in the joint run."""
+        beams = [int(i) for i in beams]
+        return replace(self, t_ms=self.t_ms[beams], fluxes=[self.fluxes[i] for i in beams],
+                       _log_tables=None)
 
     # ----------------------------------------------------------------- io
     def to_arrays(self) -> dict:

@@ -128,3 +128,54 @@ def padded_grid_shape(slab):
     global faces exactly where no neighbour exists, so the reference's
     boundary closure (spatial.py:81-118) applies there and only there."""
     return slab.nx, slab.ny, slab.halo_below + slab.planes + slab.halo_above
+
+
+# ---------------------------------------------------------------- beam batching
+# SURVEY.md §8(e) "Beams": rays and beams are independent, so a multi-beam run
+# may be split into independent low-rank solves per beam subset whose doses
+# are summed (not numerically the joint solve: its reference is the CPU run
+# on the same partition). Subsets go to groups of ranks; a group of several
+# ranks z-slab shards its subset's solve over its own communicator.
+
+
+def beam_partition(n_beams, parts=None):
+    """Beams dealt round-robin into `parts` subsets (default: one per beam)."""
+    parts = n_beams if parts is None else int(parts)
+    if not 1 <= parts <= max(n_beams, 1):
+        raise ValueError(f"cannot split {n_beams} beams into {parts} subsets")
+    return [tuple(range(p, n_beams, parts)) for p in range(parts)]
+
+
+@dataclass(frozen=True)
+class BeamAssignment:
+    """This rank's share of a beam-batched run."""
+
+    parts: tuple          # indices of the beam subsets this rank works on (in order)
+    members: tuple        # world ranks of this rank's group (one group per subset when
+                          # world >= subsets, else every rank alone)
+    local_rank: int       # position in members (its z-slab when len(members) > 1)
+
+    @property
+    def local_world(self):
+        return len(self.members)
+
+
+def assign_parts(world, rank, n_parts):
+    """world >= n_parts: subset p -> ranks [p g, (p + 1) g), g = world // n_parts
+    (a rank past n_parts g idles); world < n_parts: each rank alone, subsets
+    dealt round-robin (rank q solves q, q + world, ... one after another)."""
+    if world < 1 or not 0 <= rank < world or n_parts < 1:
+        raise ValueError("bad rank/world/parts")
+    if world >= n_parts:
+        g = world // n_parts
+        p = rank // g
+        if p >= n_parts:
+            return BeamAssignment((), (rank,), 0)
+        return BeamAssignment((p,), tuple(range(p * g, (p + 1) * g)), rank - p * g)
+    return BeamAssignment(tuple(range(rank, n_parts, world)), (rank,), 0)
+
+
+def sum_doses(local_dose, dist=None):
+    """Sum the per-rank dose contributions (each rank holds zeros outside the
+    rows it solved) over the world: the beam-batched total dose."""
+    return allreduce_sum(local_dose, dist=dist)

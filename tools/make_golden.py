@@ -379,6 +379,18 @@ def hetero_raw():
     return raw
 
 
+def hetero_beam_raw(i):
+    """One beam of the heterogeneous two-beam case, with the joint run's
+    energy grid pinned (e_max of both beams): a subset of the beam-batched
+    partition {0}, {1} (SURVEY.md §8(e) "Beams")."""
+    raw = hetero_raw()
+    raw["name"] = f"hetero_b{i}"
+    raw["beams"] = [raw["beams"][i]]
+    e_max = max(b["energy_mev"] * (1.0 + 5.0 * 0.01) for b in hetero_raw()["beams"])
+    raw["energy"] = dict(raw.get("energy", {}), e_max_mev=e_max)
+    return raw
+
+
 def fp_raw():
     raw = smoke_raw(name="fp", model="fokker-planck")
     raw["physics"] = {"fp_correction_scale": 0.5}
@@ -535,6 +547,8 @@ def make_e2e(which):
         "fp": fp_raw(),
         "rank1": rank1_raw(),
         "fp19": fp19_raw(),
+        "hetero_b0": hetero_beam_raw(0),
+        "hetero_b1": hetero_beam_raw(1),
         "slabs7": slabs7_raw(),
     }
     for tag, raw in cases.items():

@@ -31,7 +31,7 @@ def rel(a, b):
 
 def main():
     out = {}
-    for tag in ("smoke", "config1", "hetero", "fp", "rank1", "fp19", "slabs7"):
+    for tag in ("smoke", "config1", "hetero", "fp", "rank1", "fp19", "slabs7", "hetero_b0", "hetero_b1"):
         b = ProblemBundle.load(ROOT / f"tests/golden/bundle_{tag}.npz")
         g = np.load(ROOT / f"tests/golden/e2e_{tag}.npz")
         unc = b.uncollided_dose()

@@ -13,7 +13,11 @@ import bench  # noqa: E402
 from paper_2508_04484_b200 import _lib as bench_lib  # noqa: E402
 
 nside = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-rel = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-8
+# "abs:1e-8" = SURVEY.md §8(d) config 2's absolute threshold (theta = 1e-8 x beam
+# weight, weight 1); a plain number is relative to the running largest sigma
+arg = sys.argv[2] if len(sys.argv) > 2 else "1e-8"
+absolute = arg.startswith("abs:")
+rel = float(arg[4:] if absolute else arg)
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 400
 wl = bench.Workload(nside=nside, rank=2)
 s = wl.solver
@@ -26,7 +30,7 @@ hist, stop = [], None
 t0 = time.perf_counter()
 for k in range(min(steps, len(edges) - 1)):
     e_hi, e_lo = edges[k], edges[k + 1]
-    b.truncation_tolerance = max(rel * smax, 1e-300)
+    b.truncation_tolerance = rel if absolute else max(rel * smax, 1e-300)
     b.rank_min, b.rank_max = 2, int(sys.argv[4]) if len(sys.argv) > 4 else 64
     s.set_coefficients(e_hi, e_lo)
     try:
@@ -43,7 +47,7 @@ for k in range(min(steps, len(edges) - 1)):
     if k % 25 == 0 or int(out[2]) >= 30:
         print(k, f"E={e_lo:.2f}", "rank", int(out[2]), f"smax={smax:.3e}", flush=True)
 wall = time.perf_counter() - t0
-print(json.dumps({"grid": [nside] * 3, "theta_rel": rel, "steps": len(hist), "wall_s": wall,
+print(json.dumps({"grid": [nside] * 3, "theta": arg, "steps": len(hist), "wall_s": wall,
                   "ms_per_step": 1000.0 * wall / max(len(hist), 1),
                   "rank_at": {str(i): hist[i] for i in range(0, len(hist), 10)},
                   "final_rank": hist[-1] if hist else None, "stopped": stop}))
