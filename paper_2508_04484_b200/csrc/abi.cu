@@ -487,10 +487,15 @@ int pnd_state_set(pnd_handle* hh, int ru, int rv, const double* u, const double*
                   const double* v) {
   return guard(hh, [&](Handle& h) {
     if (ru < 1 || rv < 1) pnd::fail(PND_ECONFIG, "rank must be positive");
-    // 64 columns per factor, 128 for an augmented state (truncate input)
-    if (ru > 128 || rv > 128) pnd::fail(PND_ECONFIG, "rank above 64 is not supported");
-    NMat U = h.U.view(h.g, ru, h.st);
-    upload_rows(h, U, u);
+    // ranks up to 256 per factor, 512 for an augmented state (truncate input)
+    if (ru > 512 || rv > 512) pnd::fail(PND_ECONFIG, "rank above 256 is not supported");
+    if (ru > 64) {
+      pnd::upload_blocked(h, u, ru);  // 32-column blocks (xwide.cu)
+    } else {
+      NMat U = h.U.view(h.g, ru, h.st);
+      upload_rows(h, U, u);
+      h.blocked = false;
+    }
     up(h.S.get((size_t)ru * rv), s, (size_t)ru * rv, h.st);
     up(h.V.get((size_t)h.m * rv), v, (size_t)h.m * rv, h.st);
     CK(cudaStreamSynchronize(h.st));
@@ -510,7 +515,9 @@ int pnd_state_shape(pnd_handle* hh, int* ru, int* rv) {
 
 int pnd_state_get(pnd_handle* hh, double* u, double* s, double* v) {
   return guard(hh, [&](Handle& h) {
-    if (u) {
+    if (u && h.blocked) {
+      pnd::download_blocked(h, u, h.ru);
+    } else if (u) {
       download_rows(h, pnd::state_u(h), u, h.ru, 0);
       if (h.uq > 0) download_rows(h, pnd::state_q(h), u, h.ru, h.ua);
     }
@@ -1131,17 +1138,23 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
 
 int pnd_state_random(pnd_handle* hh, int r, unsigned long long seed) {
   return guard(hh, [&](Handle& h) {
-    if (r < 1 || r > 64) pnd::fail(PND_ECONFIG, "random state rank must be 1..64");
+    if (r < 1 || r > 256) pnd::fail(PND_ECONFIG, "random state rank must be 1..256");
     const int m = h.m;
     // U = orth(random n x r) through the device Gram-Schmidt/SVQB passes
-    NMat X = h.Xs.view(h.g, r, h.st);
-    pnd::random_rows(h.g, X, seed, h.st);
-    h.ua = 0;
-    h.uq = 0;
-    const int k = pnd::orth_complement(h, X, nullptr);
-    std::swap(h.U, h.Q);
-    h.ua = k;
-    h.uq = 0;
+    int k;
+    if (r > 64) {
+      k = pnd::random_state_x(h, r, seed);
+    } else {
+      NMat X = h.Xs.view(h.g, r, h.st);
+      pnd::random_rows(h.g, X, seed, h.st);
+      h.ua = 0;
+      h.uq = 0;
+      h.blocked = false;
+      k = pnd::orth_complement(h, X, nullptr);
+      std::swap(h.U, h.Q);
+      h.ua = k;
+      h.uq = 0;
+    }
     double* B = h.sm[44].get((size_t)m * r);
     double* Vc = h.sm[43].get((size_t)m * r);
     double* R = h.sm[45].get((size_t)r * r);

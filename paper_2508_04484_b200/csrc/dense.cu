@@ -222,10 +222,13 @@ __global__ void __launch_bounds__(1024, 1)
   // gw: V and U in a global (L2-resident) work buffer when they do not fit in
   // shared memory (the wide R x R case); A (the dot products of every round),
   // sg and perm stay in shared memory
-  double* A = sm;                  // column-major M x N2
+  // a_in_gw (the widest, R > ~160): A lives in the global work buffer as well
+  const bool a_in_gw = gw && ((size_t)M * N2 + N2) * sizeof(double) + N * sizeof(int) + 1024 >
+                                 (size_t)kMaxDynSmem;
+  double* A = a_in_gw ? gw + (size_t)N2 * N2 + (size_t)M * N : sm;  // column-major M x N2
   double* Vm = gw ? gw : A + M * N2;       // column-major N2 x N2
   double* U = Vm + N2 * N2;        // column-major M x N (sorted, completed)
-  double* sg = gw ? A + M * N2 : U + M * N;  // N2
+  double* sg = a_in_gw ? sm : gw ? A + M * N2 : U + M * N;  // N2
   int* perm = (int*)(sg + N2);     // N
   __shared__ int rotated;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -338,9 +341,9 @@ __global__ void __launch_bounds__(1024, 1)
     for (int j = 0; j < N; ++j) {
       if (sg[perm[j]] > 0.0) continue;
       for (; cand < M; ++cand) {
-        double vloc[8];
+        double vloc[16];
         // v = e_cand - sum_k U_k U_k[cand] over filled columns, twice
-        for (int t = 0; t < 8; ++t) vloc[t] = 0.0;
+        for (int t = 0; t < 16; ++t) vloc[t] = 0.0;
         for (int i = lane, t = 0; i < M; i += 32, ++t) vloc[t] = (i == cand) ? 1.0 : 0.0;
         for (int pass = 0; pass < 2; ++pass) {
           for (int k = 0; k < N; ++k) {
@@ -390,9 +393,9 @@ __global__ void __launch_bounds__(1024, 1)
 
 __global__ void tail_kernel(const double* sig, int k, double theta, int rmin, int rmax, int* info,
                             double* tail) {
+  __shared__ double tails[513];
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   // tails[j] = sum_{i >= j} sigma_i accumulated from the smallest (np.cumsum of sigma[::-1])
-  double tails[129];
   tails[k] = 0.0;
   double acc = 0.0;
   for (int j = k - 1; j >= 0; --j) {
@@ -415,12 +418,15 @@ __global__ void tail_kernel(const double* sig, int k, double theta, int rmin, in
 }
 
 __global__ void scat_solve_kernel(const double* B, const double* coeffs, const double* lcols,
-                                  int r, int m, double dt, double* lnew, int* singular) {
+                                  int r, int m, double dt, double* lnew, int* singular,
+                                  double* gw) {
   extern __shared__ double sm[];
   const int q = blockIdx.x;
   const int LD = r + 1;
-  double* Mx = sm;           // r x LD
-  double* x = sm + r * LD;   // r
+  // gw: ranks whose r x r system does not fit in shared memory (r > ~160)
+  double* const base = gw ? gw + (size_t)q * ((size_t)r * LD + r) : sm;
+  double* Mx = base;           // r x LD
+  double* x = base + r * LD;   // r
   __shared__ int piv;
   __shared__ int bad;
   const int tid = threadIdx.x, nthr = blockDim.x;
@@ -720,7 +726,7 @@ void axpby(int count, double a, const double* x, double b, double* y, cudaStream
 
 int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfac, TsqrWork& w,
          cudaStream_t st) {
-  if (cols > 128) fail(PND_ECONFIG, "orthonormalisation supports at most 128 columns");
+  if (cols > 512) fail(PND_ECONFIG, "orthonormalisation supports at most 512 columns");
   const int kc = rows < cols ? rows : cols;
   {
     // whole matrix in one CTA when it fits (the m-side QRs)
@@ -851,17 +857,18 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
 void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt, double*,
                cudaStream_t st) {
   const int M = p >= q ? p : q, N = p >= q ? q : p;
-  if (M > 256 || N > 128) fail(PND_ECONFIG, "truncation SVD supports at most 256 x 128");
+  if (M > 512 || N > 512) fail(PND_ECONFIG, "truncation SVD supports at most 512 x 512");
   const int N2 = N + (N & 1);
   const size_t mats = (size_t)M * N2 + (size_t)N2 * N2 + (size_t)M * N;
   size_t sm = (mats + N2) * sizeof(double) + N * sizeof(int);
   double* gw = nullptr;
   if (sm + 1024 > (size_t)kMaxDynSmem) {
-    // wide R x R: V and U in a global (L2-resident) work buffer, stream-ordered
-    const size_t vu = (size_t)N2 * N2 + (size_t)M * N;
+    // wide R x R: V and U in a global (L2-resident) work buffer, stream-ordered;
+    // above ~160 columns A as well (svd_kernel a_in_gw)
+    const size_t vu = (size_t)N2 * N2 + (size_t)M * N + (size_t)M * N2;
     CK(cudaMallocAsync((void**)&gw, vu * sizeof(double), st));
     sm = ((size_t)M * N2 + N2) * sizeof(double) + N * sizeof(int);
-    if (sm + 1024 > (size_t)kMaxDynSmem) fail(PND_ECONFIG, "truncation SVD too large");
+    if (sm + 1024 > (size_t)kMaxDynSmem) sm = (size_t)N2 * sizeof(double) + N * sizeof(int);
   }
   // one warp per Jacobi pair of a round (two per warp above 64 columns)
   int threads = 32 * (N2 / 2);
@@ -873,9 +880,12 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   } else if (M <= 128) {
     set_smem((const void*)svd_kernel<4>, sm);
     svd_kernel<4><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
-  } else {
+  } else if (M <= 256) {
     set_smem((const void*)svd_kernel<8>, sm);
     svd_kernel<8><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
+  } else {
+    set_smem((const void*)svd_kernel<16>, sm);
+    svd_kernel<16><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
   }
   launched();
   if (gw) CK(cudaFreeAsync(gw, st));
@@ -883,7 +893,7 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
 
 void tail_rule(const double* sig, int k, double theta, int rmin, int rmax, int* info,
                double* tail, cudaStream_t st) {
-  if (k > 128) fail(PND_ECONFIG, "tail rule supports at most 128 singular values");
+  if (k > 512) fail(PND_ECONFIG, "tail rule supports at most 512 singular values");
   tail_kernel<<<1, 32, 0, st>>>(sig, k, theta, rmin, rmax, info, tail);
   launched();
 }
@@ -891,8 +901,16 @@ void tail_rule(const double* sig, int k, double theta, int rmin, int rmax, int* 
 void scat_solves(const double* B, const double* coeffs, const double* lcols, int r, int m,
                  double dt, double* lnew, int* singular, cudaStream_t st) {
   const size_t sm = ((size_t)r * (r + 1) + r) * sizeof(double);
+  if (sm + 1024 > (size_t)kMaxDynSmem) {
+    double* gw = nullptr;
+    CK(cudaMallocAsync((void**)&gw, sm * m, st));
+    scat_solve_kernel<<<m, 128, 0, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular, gw);
+    launched();
+    CK(cudaFreeAsync(gw, st));
+    return;
+  }
   set_smem((const void*)scat_solve_kernel, sm);
-  scat_solve_kernel<<<m, 64, sm, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular);
+  scat_solve_kernel<<<m, 64, sm, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular, nullptr);
   launched();
 }
 

@@ -67,6 +67,12 @@ struct Handle {
   std::vector<NBuf> wide_u0b, wide_qb, wide_w1b, wide_w2b, wide_gb;
   NBuf wide_base, wide_tmp[2];
   DBuf wide_m, wide_t, wide_i, wide_g;
+  // ranks above 64 (xwide.cu): the n-side matrices as 32-column cell-major
+  // blocks; `blocked` = the state's U / Q live in xU / xQ
+  std::vector<NBuf> xU, xQ, xUn, xY, xW1, xW2;
+  NBuf xpart[2];
+  std::vector<DBuf> xsm;
+  bool blocked = false;
   // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
   std::vector<NBuf> fr_u, fr_w1, fr_w2;
   NBuf fr_t[2];
@@ -117,6 +123,36 @@ void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double*
                    const double* M, const std::vector<NMat>& out, bool in_scaled,
                    bool out_scaled);
 void stencil_grams_blocks(Handle& h, const std::vector<NMat>& B, const double* isp, double* G);
+
+// ranks above 64 (xwide.cu): column-blocked storage, every product a chain
+// over 32-column blocks
+using BMat = std::vector<NMat>;
+struct XTerm {
+  const BMat* in;
+  const double* T;  // in.cols x out.cols row-major (ld: 0 = out.cols); null = identity
+  double scale;
+  int ld = 0;
+};
+BMat bview(Handle& h, std::vector<NBuf>& bufs, int cols);
+int bcols(const BMat& m);
+void bm_gram(Handle& h, const BMat& X, const BMat& Y, double* out, const double* w, bool sym);
+void bm_lincomb(Handle& h, const std::vector<XTerm>& terms, const BMat& out);
+void to_blocked(Handle& h);
+void from_blocked(Handle& h);
+BMat xstate_u(Handle& h);
+BMat xstate_q(Handle& h);
+void consolidate_x(Handle& h);
+int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound);
+void streaming_step_x(Handle& h, double dt);
+void scattering_step_x(Handle& h, double dt);
+void rotate_x(Handle& h, const double* P, int p, int kcols, int r1, bool all_zero,
+              double* ugram);
+void dose_accumulate_x(Handle& h, const double* coef, double half_dt, const double* psi,
+                       double* dep, double* prev);
+double orth_defect_x(Handle& h, double* G, bool have_ugram);
+void upload_blocked(Handle& h, const double* u, int ru);
+void download_blocked(Handle& h, double* u, int ld);
+int random_state_x(Handle& h, int r, unsigned long long seed);
 
 // full-rank oracle on the device (fullrank.cu, fullrank.py:16-45)
 void fullrank_reset(Handle& h);                    // u = 0

@@ -105,8 +105,8 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
                            const double* lam, int mode, double tol_rel, double* TA, double* TB,
                            int* info, double* dinfo) {
   __shared__ int k_s;
-  __shared__ double scale[64];
-  __shared__ int keep[64];
+  __shared__ double scale[512];
+  __shared__ int keep[512];
   __shared__ double red[256];
   const int tid = threadIdx.x;
   // per column: 1/sqrt(lambda) and the deflation test (parallel; the serial
@@ -176,7 +176,7 @@ __global__ void svqb_build(const double* G, const double* C, int a, int b, const
 __global__ void level2_gram(const double* G3, const double* C3, int a, int b, int k1, int kb,
                             const double* floor_p, double* Ms, double* dinv) {
   const int tid = threadIdx.x;
-  __shared__ double d[128];
+  __shared__ double d[512];
   const double floor_abs = *floor_p;
   for (int j = tid; j < b; j += blockDim.x) {
     double mjj = G3[j * b + j];
@@ -222,7 +222,7 @@ __global__ void level2_build(const double* C3, int a, int b, const double* dinv,
                              const double* P2, const double* mu, double tol, double* T,
                              double* TB, int* info) {
   __shared__ int k_s;
-  __shared__ double scale[128];
+  __shared__ double scale[512];
   const int tid = threadIdx.x;
   if (tid == 0) {
     int k = 0;
@@ -271,6 +271,11 @@ static const double* isp_rows(Handle& h) { return h.isp.p + 2 * (size_t)h.g.halo
 
 void consolidate(Handle& h) {
   if (h.uq <= 0) return;
+  if (h.blocked || h.ua + h.uq > 64) {  // ranks above 64: the blocked layout (xwide.cu)
+    to_blocked(h);
+    consolidate_x(h);
+    return;
+  }
   const int ru = h.ua + h.uq;
   NMat u = state_u(h), q = state_q(h);
   NMat out = h.Un.view(h.g, ru, h.st);
@@ -401,7 +406,7 @@ void streaming_step(Handle& h, double dt) {
   const int m = h.m, ns = g.ns;
   const int a = h.ua, b = h.rv;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
-  if (b > 64 || a > 64) fail(PND_ECONFIG, "streaming step supports rank <= 64");
+  if (h.blocked || a > 64 || b > 64) return streaming_step_x(h, dt);  // xwide.cu
   cudaStream_t st = h.st;
   const NMat U0 = state_u(h);
   const double* isp = isp_rows(h);
@@ -587,7 +592,7 @@ void scattering_step(Handle& h, double dt) {
   const int B = h.n_beams;
   cudaStream_t st = h.st;
   if (a <= 0 || b <= 0) fail(PND_ECONFIG, "empty low-rank state");
-  if (a > 64 || b > 64) fail(PND_ECONFIG, "scattering step supports rank <= 64");
+  if (h.blocked || a > 64 || b > 64) return scattering_step_x(h, dt);  // xwide.cu
   const NMat U0 = state_u(h);
 
   // gt_b = g o T_M^b (12 x m), rows_b = gt_b V0 (12 x b)
@@ -840,6 +845,25 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   const Geom& g = h.g;
   const int m = h.m;
   phase(h, PH_ROTATE);
+  if (h.blocked || r1 > 64) {
+    // ranks above 64: the rotation into 32-column blocks (xwide.cu); back to
+    // the row-major layout when the rank has come down to 64 or less
+    rotate_x(h, P, p, k, r1, all_zero, ugram);
+    phase(h, PH_SVD);
+    double* Vn = slot(h, S_VNEW, (size_t)m * r1);
+    gemm(m, r1, q, 1.0, rowm(h.V.p, q), 0, Mat{Qt, 1, q}, 0, 0.0, rowm(Vn, r1), 0, 1, st);
+    double* V = h.V.get((size_t)m * r1);
+    CK(cudaMemcpyAsync(V, Vn, sizeof(double) * m * r1, cudaMemcpyDeviceToDevice, st));
+    double* S = h.S.get((size_t)r1 * r1);
+    diag_kernel<<<1, 256, 0, st>>>(sig, r1, S);
+    launched();
+    h.ru = h.rv = r1;
+    if (r1 <= 64) from_blocked(h);
+    phase(h, -1);
+    if (tail_out) *tail_out = tail;
+    if (rank_out) *rank_out = r1;
+    return;
+  }
   const NMat Un = h.Un.view(g, r1, st);
   if (all_zero) {
     // S^ == 0: the reference's Householder basis of [0 | U0] starts with e_0..e_{r-1}
@@ -883,6 +907,12 @@ void dose_accumulate_step(Handle& h, double dt, bool tally_steps) {
        st);
   double* dep = h.dep.get((size_t)g.ld);
   double* prev = h.prev.get((size_t)g.ld);
+  if (h.blocked) {
+    dose_accumulate_x(h, coef, 0.5 * dt, tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr,
+                      dep, prev);
+    phase(h, -1);
+    return;
+  }
   pnd::dose_accumulate(g, state_u(h), coef, 0.5 * dt, h.s_field.p,
                        tally_steps && h.n_beams > 0 ? h.psi_lo.p : nullptr, h.n_beams, dep, prev,
                        st);
@@ -900,6 +930,11 @@ double orth_defect(Handle& h, bool have_ugram) {
   phase(h, PH_DEFECT);
   double* G = defect_gram_slot(h, h.ru, h.rv);
   double* out = G + (size_t)h.ru * h.ru + (size_t)h.rv * h.rv;
+  if (h.blocked) {
+    const double d = orth_defect_x(h, G, have_ugram);
+    phase(h, -1);
+    return d;
+  }
   if (!have_ugram) gram_xy(g, state_u(h), state_u(h), G, h.part, st);  // U^T U
   double* GV = G + (size_t)h.ru * h.ru;
   gemm(h.rv, h.rv, h.m, 1.0, tr(rowm(h.V.p, h.rv)), 0, rowm(h.V.p, h.rv), 0, 0.0,

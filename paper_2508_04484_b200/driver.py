@@ -28,8 +28,9 @@ from .errors import ConfigError, NumericalError
 from .problem import SQRT_4PI, ProblemBundle, export_problem
 
 TRUNCATE_FLAGS = {"streaming": 1, "scattering": 2, "both": 3}
-# largest factor rank the step kernels take (an augmented state holds 2x this)
-MAX_RANK = 64
+# largest factor rank the step kernels take (an augmented state holds 2x this;
+# above 64 the n-side factors are column-blocked, csrc/xwide.cu)
+MAX_RANK = 256
 
 
 @dataclass
