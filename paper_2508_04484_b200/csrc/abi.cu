@@ -492,6 +492,7 @@ int pnd_state_set(pnd_handle* hh, int ru, int rv, const double* u, const double*
     if (ru > 64) {
       pnd::upload_blocked(h, u, ru);  // 32-column blocks (xwide.cu)
     } else {
+      if (h.blocked) pnd::release_blocked(h);
       NMat U = h.U.view(h.g, ru, h.st);
       upload_rows(h, U, u);
       h.blocked = false;

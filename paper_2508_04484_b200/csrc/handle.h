@@ -69,8 +69,7 @@ struct Handle {
   DBuf wide_m, wide_t, wide_i, wide_g;
   // ranks above 64 (xwide.cu): the n-side matrices as 32-column cell-major
   // blocks; `blocked` = the state's U / Q live in xU / xQ
-  std::vector<NBuf> xU, xQ, xUn, xY, xW1, xW2;
-  NBuf xpart[2];
+  std::vector<NBuf> xU, xQ, xUn, xW1, xW2;  // the CGS scratch Y shares xW1
   std::vector<DBuf> xsm;
   bool blocked = false;
   // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
@@ -139,6 +138,8 @@ void bm_gram(Handle& h, const BMat& X, const BMat& Y, double* out, const double*
 void bm_lincomb(Handle& h, const std::vector<XTerm>& terms, const BMat& out);
 void to_blocked(Handle& h);
 void from_blocked(Handle& h);
+void release_narrow(Handle& h);
+void release_blocked(Handle& h);
 BMat xstate_u(Handle& h);
 BMat xstate_q(Handle& h);
 void consolidate_x(Handle& h);

@@ -465,7 +465,8 @@ void bm_lincomb(Handle& h, const std::vector<XTerm>& terms, const BMat& out) {
         launched();
       }
       const bool last = pos >= items.size();
-      NMat dst = last ? out[jb] : h.xpart[pingpong].view(g, bj, st);
+      // the partial sums share the K-stage chain temporaries (not live here)
+      NMat dst = last ? out[jb] : h.wide_tmp[pingpong].view(g, bj, st);
       lincomb(g, Y1, Y2, Xm, TA, tb.nseg ? TB : nullptr, dst, nullptr, h.part, st);
       partial = dst;
       pingpong ^= 1;
@@ -474,6 +475,27 @@ void bm_lincomb(Handle& h, const std::vector<XTerm>& terms, const BMat& out) {
 }
 
 // ------------------------------------------------------------ layout changes
+// The two layouts never need their buffers at the same time: a layout change
+// frees the other one's n-side buffers (at 256^3 a rank-64 row-major set and
+// a rank-110 blocked set together exceed the 180 GB).
+static void release(NBuf& b) {
+  b.d.free_();
+  b.rs = -1;
+}
+
+void release_narrow(Handle& h) {
+  CK(cudaStreamSynchronize(h.st));
+  for (NBuf* b : {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2}) release(*b);
+  for (std::vector<NBuf>* v : {&h.wide_u0b, &h.wide_qb, &h.wide_w1b, &h.wide_w2b, &h.wide_gb})
+    for (NBuf& b : *v) release(b);
+}
+
+void release_blocked(Handle& h) {
+  CK(cudaStreamSynchronize(h.st));
+  for (std::vector<NBuf>* v : {&h.xU, &h.xQ, &h.xUn, &h.xW1, &h.xW2})
+    for (NBuf& b : *v) release(b);
+}
+
 // the state's U (ua columns) in row-major form -> blocks (and Q likewise)
 void to_blocked(Handle& h) {
   if (h.blocked) return;
@@ -488,6 +510,7 @@ void to_blocked(Handle& h) {
   if (h.ua > 0) cut(h.U.view(g, h.ua, h.st), h.xU);
   if (h.uq > 0) cut(h.Q.view(g, h.uq, h.st), h.xQ);
   h.blocked = true;
+  release_narrow(h);
 }
 
 // blocks -> row-major U (ua <= 64) when the rank has come down again
@@ -502,6 +525,7 @@ void from_blocked(Handle& h) {
     launched();
   }
   h.blocked = false;
+  release_blocked(h);
 }
 
 BMat xstate_u(Handle& h) { return bview(h, h.xU, h.ua); }
@@ -542,8 +566,9 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
   double* dinfo = xs(h, X_DEF, 4);
   int* info = h.iflag.get(8);
   double* I = eye_x(h, b);
-  // pass 2: Y = X - U0 C1 -> xY, C2 = U0^T Y, G2 = Y^T Y
-  const BMat Y = bview(h, h.xY, b);
+  // pass 2: Y = X - U0 C1 -> xW1 (free once the K stages are done; X is in
+  // xW2), C2 = U0^T Y, G2 = Y^T Y
+  const BMat Y = bview(h, h.xW1, b);
   if (a > 0) bm_lincomb(h, {XTerm{&X, nullptr, 1.0}, XTerm{&U0, C1, -1.0}}, Y);
   else bm_lincomb(h, {XTerm{&X, I, 1.0}}, Y);
   if (a > 0) bm_gram(h, U0, Y, C2, nullptr, false);
@@ -623,6 +648,8 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
 
 // ------------------------------------------------------------ streaming step
 // K stage chained over blocks: out_j = S^-1? (U0 S0[:, j] + sum_x sum_s (D_s S^-1 X_x) M_s[x, j])
+// (the base rows' bm_lincomb uses wide_tmp for its partial sums before the
+// chain below takes them over)
 static void kstage_x(Handle& h, const BMat& X, const BMat& U0, const double* S0, const double* M,
                      const BMat& out, bool in_scaled, bool out_scaled) {
   const Geom& g = h.g;
@@ -981,6 +1008,7 @@ void rotate_x(Handle& h, const double* P, int p, int kcols, int r1, bool all_zer
   }
   if (ugram) bm_gram(h, Un, Un, ugram, nullptr, true);
   std::swap(h.xU, h.xUn);
+  if (!h.blocked) release_narrow(h);
   h.blocked = true;
   h.ua = r1;
   h.uq = 0;
@@ -1047,6 +1075,7 @@ __global__ void random_block_kernel(Geom g, NMat U, int c0, int cols, unsigned l
 
 // U = orth(pseudo-random n x r) on blocks (pnd_state_random above rank 64)
 int random_state_x(Handle& h, int r, unsigned long long seed) {
+  if (!h.blocked) release_narrow(h);
   const BMat X = bview(h, h.xW2, r);
   for (size_t i = 0, c0 = 0; i < X.size(); c0 += X[i].cols, ++i) {
     random_block_kernel<<<gsz((long)h.g.n * X[i].rs), 256, 0, h.st>>>(h.g, X[i], (int)c0, r,
@@ -1065,6 +1094,7 @@ int random_state_x(Handle& h, int r, unsigned long long seed) {
 
 // host <-> blocked state (pnd_state_set / pnd_state_get above rank 64)
 void upload_blocked(Handle& h, const double* u, int ru) {
+  if (!h.blocked) release_narrow(h);
   const BMat b = bview(h, h.xU, ru);
   for (size_t i = 0, c0 = 0; i < b.size(); c0 += b[i].cols, ++i) {
     if (b[i].rs != b[i].cols) fill_zero(b[i].p, (size_t)h.g.n * b[i].rs, h.st);

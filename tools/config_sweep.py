@@ -12,8 +12,9 @@ one point never limits the next):
   at 134 M cells are ~142 GB);
 - config 4: the 256^3 water P19 Fokker-Planck workload with four 90 MeV
   beams (gantry 0/45/90/135 deg in the y-z plane) in one solve, fixed rank 20;
-- config 5: the rank sweep r = 10, 20, 40, 64 on the bench's 256^3 water
-  P19 Fokker-Planck workload.
+- config 5: the rank sweep r = 10, 20, 40, 64, 80, 120, 160, 200 on the
+  bench's 256^3 water P19 Fokker-Planck workload (above 64 the column-blocked
+  layout of csrc/xwide.cu).
 Timing as bench.py: W warm-up steps, then K steps between CUDA events on the
 handle's stream; steps start at floor(n_steps / 3). Reported next to SURVEY.md
 §8(d)'s cost model: fp64_frac = 192 n r^2 flops / t / (measured FP64 DGEMM
@@ -33,8 +34,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-POINTS = ["256:10:water", "256:20:water", "256:40:water", "256:64:water", "512:20:slabs",
-          "256:20:beams4"]
+POINTS = ["256:10:water", "256:20:water", "256:40:water", "256:64:water", "256:80:water",
+          "256:120:water", "256:160:water", "256:200:water", "512:20:slabs", "256:20:beams4"]
 GANTRY = (0.0, 45.0, 90.0, 135.0)
 
 
