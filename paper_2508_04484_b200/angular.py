@@ -10,7 +10,7 @@ trigonometric polynomial in phi of degree <= 2N+1 (the same identity the
 reference's own tests/oracles.py uses). The basis is the reference's: index
 p = l^2 + l + k, real combinations of orthonormal harmonics with the
 Condon-Shortley phase cancelled (angular.py:58-80), so V, T_M and the
-degree-diagonal scattering matrices line up with it. tests/test_host.py pins
+degree-diagonal scattering matrices line up with it. tests/test_oracle.py::test_angular_operators_match_reference pins
 A_d^+- against the reference for N = 1..7.
 """
 

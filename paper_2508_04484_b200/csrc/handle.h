@@ -72,6 +72,7 @@ struct Handle {
   std::vector<NBuf> xU, xQ, xUn, xW1, xW2;  // the CGS scratch Y shares xW1
   std::vector<DBuf> xsm;
   bool blocked = false;
+  DBuf cq_work;  // pivoted-Cholesky work matrices that do not fit in shared memory
   // full-rank state (fullrank.cu): ceil(m / 32) cell-major column blocks
   std::vector<NBuf> fr_u, fr_w1, fr_w2;
   NBuf fr_t[2];
@@ -122,6 +123,12 @@ void kstage_blocks(Handle& h, const std::vector<NMat>& X, NMat U0, const double*
                    const double* M, const std::vector<NMat>& out, bool in_scaled,
                    bool out_scaled);
 void stencil_grams_blocks(Handle& h, const std::vector<NMat>& B, const double* isp, double* G);
+
+// rank-revealing pivoted Cholesky of the augmentation's small Gram (step.cu);
+// mode 0 deflate, 1 re-orthogonalise, 2 deflated residuals, 3 level-2 scaled
+void cholqr_build(const double* G, const double* C, int a, int b, int mode, double tol2,
+                  const double* dinv, double* TA, double* TB, int* info, double* d0out,
+                  DBuf& work, cudaStream_t st);
 
 // ranks above 64 (xwide.cu): column-blocked storage, every product a chain
 // over 32-column blocks

@@ -75,15 +75,6 @@ double* eye(Handle& h, int b) {
   return I;
 }
 
-// SVQB transform from the Gram pair of Y against (U0, Y):
-//   eigen(G - C^T C) = (P, lam) sorted descending
-//   mode 0 (rank revealing): keep lam_j > tol_rel^2 lam_0,
-//          TA = P_k diag(lam_k^-1/2)  ->  Q = (Y - U0 C) TA = Y TA - U0 (C TA)
-//   mode 1 (re-orthogonalisation): TA = P diag(lam^-1/2) P^T
-//   mode 2 (graded increment, level 1 of two): TA = [P_k diag(lam_k^-1/2) | P_rest]
-//          -> W = (Y - U0 C) TA holds Q in its first k columns and the
-//          deflated directions, unnormalised, in the rest
-//   TB = C TA.  info[0] = k;  dinfo[0] = max(|G - I|, |C|)
 // max(|G - I|, |C|) (the block's orthonormality defect) into out[0]
 __global__ void defect_gc_kernel(const double* G, const double* C, int a, int b, double* out) {
   __shared__ double red[256];
@@ -101,74 +92,11 @@ __global__ void defect_gc_kernel(const double* G, const double* C, int a, int b,
   if (threadIdx.x == 0) out[0] = red[0];
 }
 
-__global__ void svqb_build(const double* G, const double* C, int a, int b, const double* P,
-                           const double* lam, int mode, double tol_rel, double* TA, double* TB,
-                           int* info, double* dinfo) {
-  __shared__ int k_s;
-  __shared__ double scale[512];
-  __shared__ int keep[512];
-  __shared__ double red[256];
-  const int tid = threadIdx.x;
-  // per column: 1/sqrt(lambda) and the deflation test (parallel; the serial
-  // scan below only reads shared memory)
-  const double l0 = b > 0 ? lam[0] : 0.0;
-  for (int j = tid; j < b; j += blockDim.x) {
-    const double l = lam[j];
-    scale[j] = 1.0 / sqrt(l > 0.0 ? l : 1e-300);
-    keep[j] = l > 0.0 && l > tol_rel * tol_rel * l0;
-  }
-  // orthonormality defect of the previous pass: max |G - I|, max |C|
-  double d = 0.0;
-  for (int i = tid; i < b * b + a * b; i += blockDim.x) {
-    const double v = i < b * b ? fabs(G[i] - ((i / b == i % b) ? 1.0 : 0.0)) : fabs(C[i - b * b]);
-    d = v > d ? v : d;
-  }
-  red[tid] = d;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (tid < w) red[tid] = fmax(red[tid], red[tid + w]);
-    __syncthreads();
-  }
-  if (tid == 0) {
-    int k = b;
-    if (mode == 0 || mode == 2) {
-      k = 0;
-      while (k < b && keep[k]) ++k;
-    }
-    k_s = k;
-    info[0] = k;
-    dinfo[0] = red[0];
-  }
-  __syncthreads();
-  const int k = k_s;
-  const int ncol = mode == 0 ? k : b;
-  for (int i = tid; i < b * ncol; i += blockDim.x) {
-    const int r = i / ncol, c = i % ncol;
-    double v;
-    if (mode == 0) {
-      v = P[r * b + c] * scale[c];
-    } else if (mode == 2) {
-      v = P[r * b + c] * (c < k ? scale[c] : 1.0);
-    } else {
-      v = 0.0;
-      for (int j = 0; j < b; ++j) v += P[r * b + j] * scale[j] * P[c * b + j];
-    }
-    TA[i] = v;
-  }
-  __syncthreads();
-  for (int i = tid; i < a * ncol; i += blockDim.x) {
-    const int r = i / ncol, c = i % ncol;
-    double v = 0.0;
-    for (int j = 0; j < b; ++j) v += C[r * b + j] * TA[j * ncol + c];
-    TB[i] = v;
-  }
-}
-
-// Level 2 of the augmentation (graded increments). W = [Q | Z] from svqb
-// mode 2, G3 = W^T W, C3 = U0^T W formed from the explicit vectors, so every
-// entry is accurate to eps |w_i| |w_j| -- unlike the level-1 Gram, whose small
-// eigenvalues are lost below eps lam_0. M = G3 - C3^T C3 (W projected out of
-// U0); the columns kept are Q's and every Z column with norm above
+// Level 2 of the augmentation (graded increments). W = [Q | Z] from
+// cholqr mode 2, G3 = W^T W, C3 = U0^T W formed from the explicit vectors, so
+// every entry is accurate to eps |w_i| |w_j| -- unlike the level-1 Gram, whose
+// small directions are lost below eps |Y|^2. M = G3 - C3^T C3 (W projected out
+// of U0); the columns kept are Q's and every Z column with norm above
 // *floor_p (1e-13 |X|_F: the rounding noise of forming and projecting the
 // increment X = U0 C1 + Y is ~eps |X|, so only real content passes);
 // Ms = D^-1 M_JJ D^-1 (unit diagonal, zero rows and columns outside J) is
@@ -182,12 +110,20 @@ __global__ void level2_gram(const double* G3, const double* C3, int a, int b, in
     double mjj = G3[j * b + j];
     for (int t = 0; t < a; ++t) mjj -= C3[t * b + j] * C3[t * b + j];
     const double nj = mjj > 0.0 ? sqrt(mjj) : 0.0;
-    // Z columns come in level-1 eigenvalue order: at most kb - k1 of them can
-    // be real when the increment's rank is known to be <= kb
-    const bool keep = j < k1 || (j < kb && nj > floor_abs);
-    d[j] = keep ? 1.0 / nj : 0.0;
-    dinv[j] = d[j];
+    d[j] = nj;
   }
+  __syncthreads();
+  // at most kb - k1 of the deflated columns can be real when the increment's
+  // rank is known to be <= kb: the largest residuals above the floor
+  for (int j = tid; j < b; j += blockDim.x) {
+    const double nj = d[j];
+    int above = 0;
+    for (int i = k1; i < b; ++i) above += d[i] > nj || (d[i] == nj && i < j);
+    const bool keep = j < k1 || (above < kb - k1 && nj > floor_abs);
+    dinv[j] = keep ? 1.0 / nj : 0.0;
+  }
+  __syncthreads();
+  for (int j = tid; j < b; j += blockDim.x) d[j] = dinv[j];
   __syncthreads();
   for (int i = tid; i < b * b; i += blockDim.x) {
     const int r = i / b, c = i % b;
@@ -215,40 +151,177 @@ __global__ void xnorm_kernel(const double* G2, const double* C1, int a, int b, d
   if (tid == 0) out[0] = rel * sqrt(red[0] > 0.0 ? red[0] : 0.0);
 }
 
-// SVQB of the scaled level-2 Gram (eigen-pairs P2, mu descending): keep
-// mu > tol * mu_0 (the rest are dependent columns), T = D^-1 P2_k mu_k^-1/2,
-// TB = C3 T; info[0] = k2.
-__global__ void level2_build(const double* C3, int a, int b, const double* dinv,
-                             const double* P2, const double* mu, double tol, double* T,
-                             double* TB, int* info) {
-  __shared__ int k_s;
-  __shared__ double scale[512];
-  const int tid = threadIdx.x;
+}  // namespace
+
+// Rank-revealing pivoted Cholesky of the small Gram of the augmentation
+// (CholeskyQR with diagonal pivoting): G = P R^T R P^T,
+// pivots taken while the largest remaining diagonal -- the squared residual
+// norm of that column after projecting out the columns already taken --
+// exceeds tol2 x the first pivot. Every column left out therefore has a
+// residual below sqrt(tol2) of the largest column (the deflation guarantee the
+// second level builds on). Replaces an eigen-decomposition (SVQB) of the same
+// Gram: one pass over b^2 entries instead of Jacobi sweeps.
+//   mode 0: TA (b x k) = P_J R^-1, so Q = (Y - U0 C) TA has orthonormal columns
+//   mode 1: the same without the deflation threshold (re-orthogonalisation)
+//   mode 2: TA (b x b) = [P_J R^-1 | e_rest - P_J G_JJ^-1 G_J,rest]: the
+//           deflated columns' residuals after Q, unnormalised (level 2 input)
+//   mode 3: G is the unit-scaled level-2 Gram (dinv: the column scales):
+//           TA (b x k) = D^-1 P_J R^-1
+// TB = C TA (a x ncol); info[0] = k. work: 2 b^2 doubles (global) when the
+// matrices do not fit in shared memory.
+__global__ void __launch_bounds__(256)
+    cholqr_kernel(const double* __restrict__ G, const double* __restrict__ C, int a, int b,
+                  int mode, double tol2, const double* __restrict__ dinv, double* TA,
+                  double* TB, int* info, double* d0out, double* work, int in_smem) {
+  extern __shared__ double sm[];
+  double* A = in_smem ? sm : work;               // b x b working copy (R in its upper part)
+  double* Ri = A + (size_t)b * b;                // k x k inverse of R
+  __shared__ int perm[512];
+  __shared__ int k_s, piv_s;
+  __shared__ double d0_s;
+  const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < b * b; i += nthr) A[i] = G[i];
+  for (int i = tid; i < b; i += nthr) perm[i] = i;
   if (tid == 0) {
-    int k = 0;
-    const double m0 = b > 0 ? mu[0] : 0.0;
-    while (k < b && mu[k] > 0.0 && mu[k] > tol * m0) ++k;
-    k_s = k;
-    info[0] = k;
+    k_s = b;
+    d0_s = 0.0;
   }
   __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    if (warp == 0) {
+      double best = -1.0;
+      int bi = j;
+      for (int i = j + lane; i < b; i += 32) {
+        const double v = A[(size_t)i * b + i];
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (lane == 0) {
+        if (j == 0) d0_s = best;
+        const double d0 = j == 0 ? best : d0_s;
+        if (!(best > 0.0) || best <= tol2 * d0) k_s = j;
+        piv_s = bi;
+      }
+    }
+    __syncthreads();
+    if (k_s == j) break;
+    const int p = piv_s;
+    if (p != j) {  // symmetric swap of rows / columns j and p
+      for (int i = tid; i < b; i += nthr) {
+        const double t = A[(size_t)j * b + i];
+        A[(size_t)j * b + i] = A[(size_t)p * b + i];
+        A[(size_t)p * b + i] = t;
+      }
+      __syncthreads();
+      for (int i = tid; i < b; i += nthr) {
+        const double t = A[(size_t)i * b + j];
+        A[(size_t)i * b + j] = A[(size_t)i * b + p];
+        A[(size_t)i * b + p] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[j];
+        perm[j] = perm[p];
+        perm[p] = t;
+      }
+      __syncthreads();
+    }
+    const double rjj = sqrt(A[(size_t)j * b + j]);
+    __syncthreads();
+    if (tid == 0) A[(size_t)j * b + j] = rjj;
+    for (int i = j + 1 + tid; i < b; i += nthr) A[(size_t)j * b + i] /= rjj;
+    __syncthreads();
+    const int w = b - j - 1;
+    for (int e = tid; e < w * w; e += nthr) {
+      const int r = j + 1 + e / w, c = j + 1 + e % w;
+      A[(size_t)r * b + c] -= A[(size_t)j * b + r] * A[(size_t)j * b + c];
+    }
+    __syncthreads();
+  }
   const int k = k_s;
-  for (int j = tid; j < k; j += blockDim.x) scale[j] = 1.0 / sqrt(mu[j]);
-  __syncthreads();
-  for (int i = tid; i < b * k; i += blockDim.x) {
-    const int r = i / k, c = i % k;
-    T[i] = dinv[r] * P2[r * b + c] * scale[c];
+  if (tid == 0) {
+    info[0] = k;
+    if (d0out) d0out[0] = d0_s;
+  }
+  // R^-1 (k x k upper), one column per thread: R x = e_c by back substitution
+  for (int c = tid; c < k; c += nthr) {
+    for (int r = k - 1; r >= 0; --r) {
+      double v = r == c ? 1.0 : 0.0;
+      for (int t = r + 1; t <= c; ++t) v -= A[(size_t)r * b + t] * Ri[(size_t)t * k + c];
+      Ri[(size_t)r * k + c] = r > c ? 0.0 : v / A[(size_t)r * b + r];
+    }
   }
   __syncthreads();
-  for (int i = tid; i < a * k; i += blockDim.x) {
-    const int r = i / k, c = i % k;
+  const int ncol = mode == 2 ? b : k;
+  for (int e = tid; e < b * ncol; e += nthr) TA[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < k * k; e += nthr) {
+    const int i = e / k, c = e % k;
+    const double sc = mode == 3 ? dinv[perm[i]] : 1.0;
+    TA[(size_t)perm[i] * ncol + c] = sc * Ri[e];
+  }
+  if (mode == 2) {
+    // rest column t (original index q = perm[k + t]): e_q - P_J c, c = R^-1 R^-T G[J, q]
+    for (int t = tid; t < b - k; t += nthr) {
+      const int q = perm[k + t];
+      double y[512 / 8];  // R^-T g, chunked: k <= 64 in registers, else recomputed
+      if (k <= 64) {
+        for (int i = 0; i < k; ++i) {
+          double v = 0.0;
+          for (int l = 0; l <= i; ++l) v += Ri[(size_t)l * k + i] * G[(size_t)perm[l] * b + q];
+          y[i] = v;
+        }
+        for (int i = 0; i < k; ++i) {
+          double v = 0.0;
+          for (int l = i; l < k; ++l) v += Ri[(size_t)i * k + l] * y[l];
+          TA[(size_t)perm[i] * ncol + k + t] = -v;
+        }
+      } else {
+        for (int i = 0; i < k; ++i) {
+          double v = 0.0;
+          for (int l = i; l < k; ++l) {
+            double yl = 0.0;
+            for (int m = 0; m <= l; ++m) yl += Ri[(size_t)m * k + l] * G[(size_t)perm[m] * b + q];
+            v += Ri[(size_t)i * k + l] * yl;
+          }
+          TA[(size_t)perm[i] * ncol + k + t] = -v;
+        }
+      }
+      TA[(size_t)q * ncol + k + t] = 1.0;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < a * ncol; e += nthr) {
+    const int r = e / ncol, c = e % ncol;
     double v = 0.0;
-    for (int j = 0; j < b; ++j) v += C3[r * b + j] * T[j * k + c];
-    TB[i] = v;
+    for (int j = 0; j < b; ++j) v += C[(size_t)r * b + j] * TA[(size_t)j * ncol + c];
+    TB[e] = v;
   }
 }
 
-}  // namespace
+void cholqr_build(const double* G, const double* C, int a, int b, int mode, double tol2,
+                  const double* dinv, double* TA, double* TB, int* info, double* d0out,
+                  DBuf& work, cudaStream_t st) {
+  if (b > 512) fail(PND_ECONFIG, "augmentation block wider than 512 columns");
+  const size_t need = 2 * (size_t)b * b * sizeof(double);
+  const bool in_smem = need + 8192 <= (size_t)kMaxDynSmem;
+  double* w = nullptr;
+  if (in_smem) {
+    static bool init = false;
+    if (!init) {
+      allow_max_smem(cholqr_kernel);
+      init = true;
+    }
+  } else {
+    w = work.get(2 * (size_t)b * b);
+  }
+  cholqr_kernel<<<1, 256, in_smem ? need : 0, st>>>(G, C, a, b, mode, tol2, dinv, TA, TB, info,
+                                                   d0out, w, in_smem ? 1 : 0);
+  launched();
+}
 
 NMat state_u(Handle& h) { return h.U.view(h.g, h.ua, h.st); }
 NMat state_q(Handle& h) {
@@ -306,9 +379,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   double* grams = slot(h, S_OG, (size_t)b * (a + b));
   double* TA = slot(h, S_OTA, (size_t)b * b);
   double* TB = slot(h, S_OTB, (size_t)(a > 0 ? a : 1) * b);
-  double* P = slot(h, S_P, (size_t)b * b);
   double* sig = slot(h, S_SIG, (size_t)b + 2);
-  double* Qt = slot(h, S_QTM, (size_t)b * b);
   int* info = h.iflag.get(8);
   double* dinfo = slot(h, S_TAIL, 4);
   // pass 2: Y = X - U0 C1 -> Qa, C2 = U0^T Y, G2 = Y^T Y
@@ -317,9 +388,9 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   double* C2 = grams;                  // a x b
   double* G2 = grams + (size_t)a * b;  // b x b
   if (a > 0) gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
-  svd_small(G2, b, b, P, sig, Qt, nullptr, st);
-  svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 0, 1e-7, TA, TB, info, dinfo);
-  launched();
+  // rank-revealing pivoted Cholesky of the projected Gram: columns whose
+  // residual falls below 1e-7 of the largest are deflated (to level 2)
+  cholqr_build(G2, C2, a, b, 0, 1e-14, nullptr, TA, TB, info, sig, h.cq_work, st);
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h.pinned + 11, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -328,21 +399,21 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   const double lam0 = h.pinned[11];
   h.uq = 0;
   // Level 2 (graded increments): the one-pass Gram resolves directions only
-  // down to ~1e-7 of the largest (its eigenvalues carry eps lam_0 absolute
+  // down to ~1e-7 of the largest column (its entries carry eps |Y|^2 absolute
   // error), where the reference's Householder QR keeps every direction. When
-  // directions were deflated and the increment's rank bound allows more, the
-  // deflated directions are formed explicitly (W = Y' [P_k lam^-1/2 | P_rest]),
-  // their Gram recomputed from the vectors themselves and re-orthonormalised
-  // after column scaling: directions down to 1e-13 of |X| are kept (the
-  // content below that is under T2's 1e-11 bound), rounding noise is not.
+  // columns were deflated and the increment's rank bound allows more, their
+  // residuals after Q are formed explicitly (W = Y' [P_J R^-1 | rest residual
+  // columns], cholqr mode 2), their Gram recomputed from the vectors
+  // themselves and re-orthonormalised after column scaling: directions down to
+  // 1e-13 of |X| are kept (the content below that is under T2's 1e-11
+  // bound), rounding noise is not.
   const bool level2 = k < b && k < rank_bound && lam0 > 0.0;
   if (k == 0 && !level2) return 0;
   NMat Qv;
   double* C3 = grams;
   double* G3 = nullptr;
   if (level2) {
-    svqb_build<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 2, 1e-7, TA, TB, info, dinfo);
-    launched();
+    cholqr_build(G2, C2, a, b, 2, 1e-14, nullptr, TA, TB, info, nullptr, h.cq_work, st);
     xnorm_kernel<<<1, 256, 0, st>>>(G2, a > 0 ? C1 : nullptr, a, b, 1e-13, dinfo + 1);
     launched();
     // pass 3': W = Y TA - U0 TB (b cols) -> Q, C3 = U0^T W, G3 = W^T W
@@ -353,9 +424,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
     level2_gram<<<1, 256, 0, st>>>(grams + (size_t)a * b, grams, a, b, k,
                                    rank_bound < b ? rank_bound : b, dinfo + 1, Ms, dinv);
     launched();
-    svd_small(Ms, b, b, P, sig, Qt, nullptr, st);
-    level2_build<<<1, 256, 0, st>>>(grams, a, b, dinv, P, sig, 1e-14, TA, TB, info + 2);
-    launched();
+    cholqr_build(Ms, grams, a, b, 3, 1e-14, dinv, TA, TB, info + 2, nullptr, h.cq_work, st);
     CK(cudaMemcpyAsync(h.pinned + 8, info + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     k = *(int*)(h.pinned + 8);
@@ -384,9 +453,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
     CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
     if (a > 0)
       gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
-    svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
-    svqb_build<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1, dinfo);
-    launched();
+    cholqr_build(G3c, C3, a, k, 1, 0.0, nullptr, TA, TB, info + 1, nullptr, h.cq_work, st);
     // pass 4: Q <- Q TA - U0 TB (into Qa, then swap)
     NMat Q2 = h.Qa.view(g, k, st);
     lincomb(g, Qv, NMat{}, U0, TA, TB, Q2, nullptr, h.part, st);

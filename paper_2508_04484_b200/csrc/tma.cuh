@@ -1,21 +1,15 @@
-// TMA (cp.async.bulk.tensor) + mbarrier helpers for the stencil kernels.
+// Bulk-copy TMA (cp.async.bulk) + mbarrier helpers for the streaming kernels.
 //
-// An n-side matrix (column-major, leading dimension ld, n valid cells) is
-// described to the TMA unit as a 2-D tensor {cells, columns}; a box
-// {box_cells, box_cols} starting at any cell coordinate -- negative or past n
-// included -- lands in shared memory with the out-of-range cells zero-filled,
-// which is exactly the halo behaviour the stencil needs at the grid ends.
+// Every n-side matrix is cell-major with zero halo rows around it (pnd.h), so
+// the rows a chunk needs -- stencil reach included -- are contiguous, in-bounds
+// byte ranges: one cp.async.bulk each, completing on an mbarrier. No tensor
+// map is needed for this layout (the column-blocked layout of ranks above 64
+// keeps every block contiguous the same way, csrc/xwide.cu).
 #pragma once
-
-#include <cuda.h>
-#include <cudaTypedefs.h>
 
 #include "pnd.h"
 
 namespace pnd {
-
-void make_tmap(CUtensorMap* map, const double* base, int n, int ld, int cols, int box_cells,
-               int box_cols);
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -38,15 +32,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
-      "l"((unsigned long long)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
 }
 
 #ifndef PND_MBAR_SPIN

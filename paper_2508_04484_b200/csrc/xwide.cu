@@ -204,55 +204,7 @@ __global__ void coeff_x_kernel(const double* g, const double* sig, int m, double
 
 __global__ void init_int_x(int* p, int v) { *p = v; }
 
-// the level-1 / level-2 SVQB helpers of step.cu, for any b (<= 512)
-__global__ void svqb_x(const double* G, const double* C, int a, int b, const double* P,
-                       const double* lam, int mode, double tol_rel, double* TA, double* TB,
-                       int* info) {
-  __shared__ int k_s;
-  __shared__ double scale[512];
-  __shared__ int keep[512];
-  const int tid = threadIdx.x;
-  const double l0 = b > 0 ? lam[0] : 0.0;
-  for (int j = tid; j < b; j += blockDim.x) {
-    const double l = lam[j];
-    scale[j] = 1.0 / sqrt(l > 0.0 ? l : 1e-300);
-    keep[j] = l > 0.0 && l > tol_rel * tol_rel * l0;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int k = b;
-    if (mode != 1) {
-      k = 0;
-      while (k < b && keep[k]) ++k;
-    }
-    k_s = k;
-    info[0] = k;
-  }
-  __syncthreads();
-  const int k = k_s;
-  const int ncol = mode == 0 ? k : b;
-  for (int i = tid; i < b * ncol; i += blockDim.x) {
-    const int r = i / ncol, c = i % ncol;
-    double v;
-    if (mode == 0) {
-      v = P[r * b + c] * scale[c];
-    } else if (mode == 2) {
-      v = P[r * b + c] * (c < k ? scale[c] : 1.0);
-    } else {
-      v = 0.0;
-      for (int j = 0; j < b; ++j) v += P[r * b + j] * scale[j] * P[c * b + j];
-    }
-    TA[i] = v;
-  }
-  __syncthreads();
-  for (int i = tid; i < a * ncol; i += blockDim.x) {
-    const int r = i / ncol, c = i % ncol;
-    double v = 0.0;
-    for (int j = 0; j < b; ++j) v += C[r * b + j] * TA[j * ncol + c];
-    TB[i] = v;
-  }
-}
-
+// the augmentation helpers of step.cu, for any b (<= 512)
 __global__ void defect_gc_x(const double* G, const double* C, int a, int b, double* out) {
   __shared__ double red[256];
   double d = 0.0;
@@ -295,10 +247,18 @@ __global__ void level2_gram_x(const double* G3, const double* C3, int a, int b, 
     double mjj = G3[j * b + j];
     for (int t = 0; t < a; ++t) mjj -= C3[t * b + j] * C3[t * b + j];
     const double nj = mjj > 0.0 ? sqrt(mjj) : 0.0;
-    const bool keep = j < k1 || (j < kb && nj > floor_abs);
-    d[j] = keep ? 1.0 / nj : 0.0;
-    dinv[j] = d[j];
+    d[j] = nj;
   }
+  __syncthreads();
+  for (int j = tid; j < b; j += blockDim.x) {
+    const double nj = d[j];
+    int above = 0;
+    for (int i = k1; i < b; ++i) above += d[i] > nj || (d[i] == nj && i < j);
+    const bool keep = j < k1 || (above < kb - k1 && nj > floor_abs);
+    dinv[j] = keep ? 1.0 / nj : 0.0;
+  }
+  __syncthreads();
+  for (int j = tid; j < b; j += blockDim.x) d[j] = dinv[j];
   __syncthreads();
   for (int i = tid; i < b * b; i += blockDim.x) {
     const int r = i / b, c = i % b;
@@ -308,39 +268,9 @@ __global__ void level2_gram_x(const double* G3, const double* C3, int a, int b, 
   }
 }
 
-__global__ void level2_build_x(const double* C3, int a, int b, const double* dinv,
-                               const double* P2, const double* mu, double tol, double* T,
-                               double* TB, int* info) {
-  __shared__ int k_s;
-  __shared__ double scale[512];
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    int k = 0;
-    const double m0 = b > 0 ? mu[0] : 0.0;
-    while (k < b && mu[k] > 0.0 && mu[k] > tol * m0) ++k;
-    k_s = k;
-    info[0] = k;
-  }
-  __syncthreads();
-  const int k = k_s;
-  for (int j = tid; j < k; j += blockDim.x) scale[j] = 1.0 / sqrt(mu[j]);
-  __syncthreads();
-  for (int i = tid; i < b * k; i += blockDim.x) {
-    const int r = i / k, c = i % k;
-    T[i] = dinv[r] * P2[r * b + c] * scale[c];
-  }
-  __syncthreads();
-  for (int i = tid; i < a * k; i += blockDim.x) {
-    const int r = i / k, c = i % k;
-    double v = 0.0;
-    for (int j = 0; j < b; ++j) v += C3[r * b + j] * T[j * k + c];
-    TB[i] = v;
-  }
-}
-
 // small scratch of the x path (its own slots: step.cu's are file-local)
 enum XSlot {
-  X_C1, X_OG, X_TA, X_TB, X_P, X_SIG, X_QT, X_M2, X_PC, X_INFO, X_EYE, X_TCA, X_TCB, X_GT,
+  X_C1, X_OG, X_TA, X_TB, X_SIG, X_M2, X_PC, X_INFO, X_EYE, X_TCA, X_TCB, X_GT,
   X_FV, X_MST, X_G, X_L0, X_LW, X_Z, X_BV, X_VHC, X_RV, X_SH, X_VHR, X_FH, X_ROWS, X_H, X_BI,
   X_LEFT, X_HU, X_COEF, X_LCOL, X_LNEW, X_VTC, X_RT, X_PROJ, X_PROJ2, X_GTV, X_TAZ, X_QV,
   X_VN, X_DEF, X_COEFD, X_ROWSJ, X_TMP, X_COUNT
@@ -560,9 +490,7 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
   double* G2 = C2 + (size_t)a * b;
   double* TA = xs(h, X_TA, (size_t)b * b);
   double* TB = xs(h, X_TB, (size_t)(a > 0 ? a : 1) * b);
-  double* P = xs(h, X_P, (size_t)b * b);
   double* sig = xs(h, X_SIG, (size_t)b + 2);
-  double* Qt = xs(h, X_QT, (size_t)b * b);
   double* dinfo = xs(h, X_DEF, 4);
   int* info = h.iflag.get(8);
   double* I = eye_x(h, b);
@@ -574,9 +502,7 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
   if (a > 0) bm_gram(h, U0, Y, C2, nullptr, false);
   bm_gram(h, Y, Y, G2, nullptr, true);
   if (a > 0) gemm(b, b, a, -1.0, tr(rowm(C2, b)), 0, rowm(C2, b), 0, 1.0, rowm(G2, b), 0, 1, st);
-  svd_small(G2, b, b, P, sig, Qt, nullptr, st);
-  svqb_x<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 0, 1e-7, TA, TB, info);
-  launched();
+  cholqr_build(G2, C2, a, b, 0, 1e-14, nullptr, TA, TB, info, sig, h.cq_work, st);
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h.pinned + 11, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -588,8 +514,7 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
   double* C3 = C2;
   BMat Qv;
   if (level2) {
-    svqb_x<<<1, 256, 0, st>>>(G2, C2, a, b, P, sig, 2, 1e-7, TA, TB, info);
-    launched();
+    cholqr_build(G2, C2, a, b, 2, 1e-14, nullptr, TA, TB, info, nullptr, h.cq_work, st);
     xnorm_x<<<1, 256, 0, st>>>(G2, a > 0 ? C1 : nullptr, a, b, 1e-13, dinfo + 1);
     launched();
     // pass 3': W = Y TA - U0 TB (b cols) -> xQ, C3 = U0^T W, G3 = W^T W
@@ -604,9 +529,7 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
     level2_gram_x<<<1, 256, 0, st>>>(G3, C3, a, b, k, rank_bound < b ? rank_bound : b, dinfo + 1,
                                      Ms, dinv);
     launched();
-    svd_small(Ms, b, b, P, sig, Qt, nullptr, st);
-    level2_build_x<<<1, 256, 0, st>>>(C3, a, b, dinv, P, sig, 1e-14, TA, TB, info + 2);
-    launched();
+    cholqr_build(Ms, C3, a, b, 3, 1e-14, dinv, TA, TB, info + 2, nullptr, h.cq_work, st);
     CK(cudaMemcpyAsync(h.pinned + 8, info + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     k = *(int*)(h.pinned + 8);
@@ -634,9 +557,7 @@ int orth_complement_x(Handle& h, const BMat& X, const double* C1, int rank_bound
     CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
     if (a > 0)
       gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
-    svd_small(G3c, k, k, P, sig, Qt, nullptr, st);
-    svqb_x<<<1, 256, 0, st>>>(G3, C3, a, k, P, sig, 1, 0.0, TA, TB, info + 1);
-    launched();
+    cholqr_build(G3c, C3, a, k, 1, 0.0, nullptr, TA, TB, info + 1, nullptr, h.cq_work, st);
     const BMat Q2 = bview(h, h.xUn, k);
     if (a > 0) bm_lincomb(h, {XTerm{&Qv, TA, 1.0}, XTerm{&U0, TB, -1.0}}, Q2);
     else bm_lincomb(h, {XTerm{&Qv, TA, 1.0}}, Q2);

@@ -2,7 +2,7 @@
 
 PNOperators.build(N, device=...) forms the three P_N flux matrices by the same
 exact product quadrature as the host path (angular.py; the host path is pinned
-to the reference's angular.py:101-202 by tests/test_host.py) with cuBLAS, and
+to the reference's angular.py:101-202 by tests/test_oracle.py::test_angular_operators_match_reference) with cuBLAS, and
 splits them with cuSOLVER eigendecompositions. Eigenvectors are not unique
 (degenerate eigenvalues), so the comparison is on what the solver consumes:
 A_d^+- = V diag(lambda^+-) V^T and the spectral radius (the CFL step).

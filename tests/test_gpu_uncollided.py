@@ -65,3 +65,22 @@ def test_trace_beam_matches_reference(beam_index):
     assert relmax(flux.residual_energy, T[p + "residual"]) < 1e-10
     # same cells touched
     np.testing.assert_array_equal(flux.values != 0.0, T[p + "values"] != 0.0)
+
+
+@pytest.mark.parametrize("tag", ["deg0", "deg30", "beams4"])
+def test_trace40_matches_reference(tag):
+    """BASELINE.md's tracer timing cases (40^3 water, 121 rays/beam, 0 deg,
+    30 deg, four beams 0/30/60/90 deg): the device tracer's flux against the
+    reference's at 4,000 sampled cells, its group sums and residual energy."""
+    import sys
+
+    from conftest import ROOT
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    import trace_bench
+
+    from paper_2508_04484_b200 import raytracer as rt
+
+    T = trace_bench.load()
+    fluxes = trace_bench.trace_case(T, tag, rt)
+    assert trace_bench.check(T, tag, fluxes) < 1e-10

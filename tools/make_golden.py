@@ -654,6 +654,104 @@ def make_trace():
     save("trace.npz", **out)
 
 
+TRACE40_CASES = {"deg0": (0.0,), "deg30": (30.0,), "beams4": (0.0, 30.0, 60.0, 90.0)}
+
+
+def trace40_raw(angles):
+    """BASELINE.md / SURVEY.md §6.2's tracer timing case: 40^3 water at 1 mm,
+    121 rays per beam (n_side 11), 70 MeV beams in the y-z plane aimed at the
+    grid centre from 2.5 cm outside it."""
+    import math
+
+    beams = []
+    for deg in angles:
+        th = math.radians(deg)
+        d = (0.0, math.sin(th), math.cos(th))
+        beams.append({"direction": list(d), "energy_mev": 70.0,
+                      "position_cm": [2.0, 2.0 - 4.5 * d[1], 2.0 - 4.5 * d[2]]})
+    return {
+        "name": "trace40",
+        "grid": {"nx": 40, "ny": 40, "nz": 40,
+                 "delta_x_cm": 0.1, "delta_y_cm": 0.1, "delta_z_cm": 0.1},
+        "phantom": {"background_hu": 0.0},
+        "beams": beams,
+        "pn_order": 3,
+        "transport": {"cfl_number": 0.2},
+        "energy": {"groups": 128},
+        "rays": {"n_side": 11},
+    }
+
+
+def make_trace40():
+    """Inputs and (sampled) outputs of the reference tracer on the 40^3 timing
+    cases, with the reference's own trace_all_beams wall time on this host's
+    CPU (the GPU box cannot run the reference): tools/trace_bench.py times the
+    device tracer on the same inputs and checks it against these values."""
+    out = {}
+    rng = np.random.default_rng(40)
+    sample = np.sort(rng.choice(40 ** 3, 4000, replace=False))
+    out["sample"] = sample
+    for tag, angles in TRACE40_CASES.items():
+        config = driver.ProblemConfig.from_dict(trace40_raw(angles))
+        problem = driver.assemble_problem(config)
+        captured = []
+        orig = driver.trace_beam
+        calls = {"march": 0, "lu": 0}
+        om, olu = raytracer.march_ray, raytracer.lu_factor
+
+        def spy(beam, grid, space, keys, coefficients, **kw):
+            flux = orig(beam, grid, space, keys, coefficients, **kw)
+            captured.append((beam, space, np.asarray(keys), coefficients, kw, flux))
+            return flux
+
+        def mspy(*a, **k):
+            calls["march"] += 1
+            return om(*a, **k)
+
+        def luspy(*a, **k):
+            calls["lu"] += 1
+            return olu(*a, **k)
+
+        driver.trace_beam = spy
+        raytracer.march_ray, raytracer.lu_factor = mspy, luspy
+        try:
+            t0 = time.perf_counter()
+            driver.trace_all_beams(problem)
+            wall = time.perf_counter() - t0
+        finally:
+            driver.trace_beam = orig
+            raytracer.march_ray, raytracer.lu_factor = om, olu
+        p = tag + "_"
+        out[p + "cpu_s"] = np.array(wall)
+        out[p + "marches"] = np.array(calls["march"])
+        out[p + "lus"] = np.array(calls["lu"])
+        out[p + "n_beams"] = np.array(len(captured))
+        for i, (beam, space, keys, coeff, kw, flux) in enumerate(captured):
+            q = f"{p}b{i}_"
+            if "g" not in out:  # one material (water): one energy operator for every case
+                mass, g = raytracer.assemble_energy_operators(space, *coeff[0])
+                out["g"] = g
+                out["mass"] = space.mass_diagonal()
+                out["smin"] = np.array(
+                    float(np.atleast_1d(coeff[0][0](np.array([space.e_min])))[0]))
+                out["space"] = np.array([space.e_min, space.e_max, space.n_groups,
+                                         space.degree])
+                out["keys"] = keys.astype(np.int32)
+            out.update({
+                q + "beam": np.array([*beam.direction, beam.energy_mev, *beam.position_cm,
+                                      beam.weight, beam.sigma_xy_cm, beam.sigma_e_mev]),
+                q + "rays": np.array([kw["n_side"], kw["span_sigmas"], kw["max_step"]]),
+                q + "values_sample": flux.values[sample],
+                q + "values_norm": np.array(np.linalg.norm(flux.values)),
+                q + "values_colsum": flux.values.sum(axis=0),
+                q + "residual": flux.residual_energy,
+                q + "n_rays": np.array(flux.n_rays),
+            })
+        print(f"  trace40 {tag}: reference {wall:.2f} s, {calls['march']} marches, "
+              f"{calls['lu']} LUs")
+    save("trace40.npz", **out)
+
+
 def make_bench_physics():
     """Physics tables for the synthetic benchmark phantoms (water / bone / lung
     classes, stopping tables, moment tables up to degree 21 over 1..105 MeV)."""
@@ -710,6 +808,8 @@ if __name__ == "__main__":
         make_march()
     if not what or "bench" in what:
         make_bench_physics()
+    if not what or "trace40" in what:
+        make_trace40()
     if not what or "volume" in what:
         make_volume()
     e2e = {w[4:] for w in what if w.startswith("e2e:")}
