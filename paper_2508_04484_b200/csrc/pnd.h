@@ -139,6 +139,11 @@ void kstage(const KStageArgs& a, cudaStream_t st);
 // stencil Grams: out[s] = [X1 | X2]^T D_s S^-1 [X1 | X2]  (ns x w x w, w = X1.cols + X2.cols)
 void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* inv_s, double* out,
                    DBuf& partial, cudaStream_t st);
+// rectangular stencil Grams of two <= 32-column blocks, placed into an
+// ns x w x w Gram at rows r0.., columns c0..: G_s[r0 + i][c0 + j] = (XA^T D_s S^-1 XB)_ij
+// (not summed over slabs: the caller allreduces the assembled Gram)
+void stencil_grams_rect(const Geom& g, NMat XA, NMat XB, const double* isp, double* G, int w,
+                        int r0, int c0, DBuf& partial, cudaStream_t st);
 // general stencil Grams for the unit API: out[s] = X^T D_s S^-1 Y
 void stencil_grams_xy(const Geom& g, NMat X, NMat Y, const double* inv_s, double* out,
                       DBuf& partial, cudaStream_t st);

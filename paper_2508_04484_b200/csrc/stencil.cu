@@ -670,6 +670,135 @@ __global__ void __launch_bounds__(gpth(T8), 1)
   }
 }
 
+// Rectangular stencil Grams G_s = XA^T D_s S^-1 XB for the column-blocked
+// layout of ranks above 64 (xwide.cu): the features are formed from ONE
+// block XB (<= 32 columns, halo segments staged) and contracted against the
+// centre rows of another block XA (<= 32 columns, staged without halo), so
+// every (A, B) block pair is one launch of exactly its own work -- the
+// square kernel above, run on [XA | XB], would also recompute both diagonal
+// blocks and form XA's features. Same roles and pipeline as sgram_kernel.
+template <int NA, int T8A, int T8B, int GC>
+__global__ void __launch_bounds__(gpth(T8B), 1)
+    sgram_rect_kernel(Geom g, NMat XA, NMat XB, Seg S, int nstg, const double* __restrict__ isp,
+                      double* __restrict__ partial) {
+  constexpr int NS = 2 * NA;
+  constexpr int WA = T8A * 8, WB = T8B * 8;
+  constexpr int XS = pad4(WA);
+  constexpr int GCONW = gconw(T8B), GPTH = gpth(T8B);
+  constexpr int GTL = pad4(GC);
+  constexpr int CG = GC / 4;
+  constexpr int JS = 8 * (8 / CG);
+  constexpr int NBT = NS * T8B;                       // feature column tiles
+  constexpr int UPW = (NBT + GCONW - 1) / GCONW;
+  constexpr int FT = NS * WB * GTL + GC * XS;
+  extern __shared__ __align__(128) double sm[];
+  double* const F0 = sm + nstg * S.total;
+  PipeBars* pb = reinterpret_cast<PipeBars*>(F0 + 2 * FT);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wa = XA.cols, wb = XB.cols;
+  pipe_init(pb, nstg, GCONW);
+  for (int i = tid; i < 2 * FT; i += GPTH) F0[i] = 0.0;
+  __syncthreads();
+  const int nchunks = (g.n + GC - 1) / GC;
+
+  if (warp == FORMW + GCONW) {
+    if (lane == 0) {
+      Ring r(nstg);
+      for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
+        if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
+        issue_seg<GC, NA>(S, sm + r.s * S.total, &pb->sfull[r.s], chunk_cell(S, chunk, GC), XB,
+                          XB, 1, isp, XA);
+      }
+    }
+  } else if (warp < FORMW) {
+    const int ci = 4 * (warp % CG) + (lane & 3), cj = (lane >> 2) + 8 * (warp / CG);
+    Ring r(nstg);
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it, r.next()) {
+      const int f = it & 1, u = it >> 1;
+      const int c0 = chunk_cell(S, chunk, GC);
+      mbar_wait(&pb->sfull[r.s], r.k & 1);
+      if (u >= 1) mbar_wait(&pb->fempty[f], (u - 1) & 1);
+      const double* sb = sm + r.s * S.total;
+      const double* XBs = sb + S.xoff[0];
+      double* Fb = F0 + f * FT;
+      double* Cb = Fb + NS * WB * GTL;
+      // XA centre rows (the A operand); rows past n stay out of the Grams
+      for (int j = cj; j < wa; j += JS)
+        Cb[ci * XS + j] = c0 + ci >= g.n ? 0.0 : sb[S.coff + ci * XA.rs + j];
+      Ctx<GC, NA> cx;
+      cx.init(g, c0 + ci, ci, sb + S.ioff);
+      const bool fast = __all_sync(0xffffffffu, cx.inner);
+      constexpr int TT = (WB + JS - 1) / JS;
+      cx.rows(XBs, XB.rs, ci, cj);
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        const int j = cj + JS * t;
+        if (j < wb) {
+          double v[NS];
+          if (fast) cx.template apply<true>(g, JS * t, v);
+          else cx.template apply<false>(g, JS * t, v);
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2) Fb[(s2 * WB + j) * GTL + ci] = v[s2];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&pb->ffull[f]);
+        mbar_arrive(&pb->sempty[r.s]);
+      }
+    }
+  } else {
+    const int m = warp - FORMW;
+    double acc[UPW][T8A][2];
+#pragma unroll
+    for (int q = 0; q < UPW; ++q)
+#pragma unroll
+      for (int ti = 0; ti < T8A; ++ti) acc[q][ti][0] = acc[q][ti][1] = 0.0;
+    const int m0 = lane >> 2, kq = lane & 3;
+    int it = 0;
+    for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
+      const int b = it & 1, u = it >> 1;
+      mbar_wait(&pb->ffull[b], u & 1);
+      const double* pa = F0 + b * FT + NS * WB * GTL + kq * XS + m0;
+      const double* pbt = F0 + b * FT + (m * 8 + m0) * GTL + kq;
+#pragma unroll 1
+      for (int k0 = 0; k0 < GC; k0 += 4) {
+        double af[T8A];
+#pragma unroll
+        for (int ti = 0; ti < T8A; ++ti) af[ti] = pa[k0 * XS + ti * 8];
+#pragma unroll
+        for (int q = 0; q < UPW; ++q) {
+          if (m + GCONW * q < NBT) {
+            const double bf = pbt[q * GCONW * 8 * GTL + k0];
+#pragma unroll
+            for (int ti = 0; ti < T8A; ++ti) dmma884(acc[q][ti][0], acc[q][ti][1], af[ti], bf);
+          }
+        }
+      }
+      warp_arrive(&pb->fempty[b]);
+    }
+    double* out = partial + (size_t)blockIdx.x * NS * wa * wb;
+#pragma unroll
+    for (int q = 0; q < UPW; ++q) {
+      if (m + GCONW * q < NBT) {
+        const int bt = m + GCONW * q;
+        const int s2 = bt / T8B, tj = bt - s2 * T8B;
+        const int col = tj * 8 + 2 * (lane & 3);
+#pragma unroll
+        for (int ti = 0; ti < T8A; ++ti) {
+          const int row = ti * 8 + (lane >> 2);
+          if (row < wa) {
+            double* o = out + ((size_t)s2 * wa + row) * wb;
+            if (col < wb) o[col] = acc[q][ti][0];
+            if (col + 1 < wb) o[col + 1] = acc[q][ti][1];
+          }
+        }
+      }
+    }
+  }
+}
+
 // sums the per-CTA Gram partials in a fixed order and applies the stencil's
 // 1/(2h) (count = ns * per)
 __global__ void reduce_parts(const double* __restrict__ partial, int nblk, int count, int per,
@@ -713,6 +842,43 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   comm_allreduce(g, out, count, st);
 }
 
+// the rectangular per-CTA partials (ns x wa x wb) summed in fixed order, scaled
+// by 1/(2h), placed at rows r0.., columns c0.. of each ns x w x w Gram
+__global__ void reduce_place(const double* __restrict__ partial, int nblk, int ns, int wa, int wb,
+                             StScale sc, double* __restrict__ G, int w, int r0, int c0) {
+  const int count = ns * wa * wb;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double v = 0.0;
+  for (int b = 0; b < nblk; ++b) v += partial[(size_t)b * count + i];
+  const int s2 = i / (wa * wb), rem = i - s2 * wa * wb, r = rem / wb, c = rem - r * wb;
+  G[((size_t)s2 * w + r0 + r) * w + c0 + c] = v * sc.v[s2];
+}
+
+template <int NA, int GC>
+void sgram_rect_launch(const Geom& g, NMat XA, NMat XB, const double* isp, double* G, int w,
+                       int r0, int c0, DBuf& partial, cudaStream_t st) {
+  constexpr int T8 = 4;  // 32-column blocks
+  const Seg S = make_seg<GC>(g, &XB, 1, &XA);
+  const size_t ft = (size_t)2 * NA * (T8 * 8) * pad4(GC) + (size_t)GC * pad4(T8 * 8);
+  const size_t fixed = 2 * ft * sizeof(double) + sizeof(PipeBars);
+  const int nstg = stages_for(fixed, S.total);
+  if (nstg < 2) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
+  const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
+  allow_max_smem(sgram_rect_kernel<NA, T8, T8, GC>);
+  const int nchunks = (g.n + GC - 1) / GC;
+  int grid = sm_count() * resident(sgram_rect_kernel<NA, T8, T8, GC>, gpth(T8), smem);
+  if (grid > nchunks) grid = nchunks;
+  const int ns = 2 * NA;
+  const size_t count = (size_t)ns * XA.cols * XB.cols;
+  double* part = partial.get(count * grid);
+  sgram_rect_kernel<NA, T8, T8, GC><<<grid, gpth(T8), smem, st>>>(g, XA, XB, S, nstg, isp, part);
+  launched();
+  reduce_place<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, ns, XA.cols, XB.cols,
+                                                           stencil_scale(g), G, w, r0, c0);
+  launched();
+}
+
 template <int NA>
 void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
               cudaStream_t st) {
@@ -751,6 +917,17 @@ void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* isp, double* o
     case 1: sgram_na<1>(g, X1, X2, isp, out, partial, st); break;
     case 2: sgram_na<2>(g, X1, X2, isp, out, partial, st); break;
     case 3: sgram_na<3>(g, X1, X2, isp, out, partial, st); break;
+    default: return;
+  }
+}
+
+void stencil_grams_rect(const Geom& g, NMat XA, NMat XB, const double* isp, double* G, int w,
+                        int r0, int c0, DBuf& partial, cudaStream_t st) {
+  if (XA.cols > 32 || XB.cols > 32) fail(PND_ECONFIG, "rectangular stencil Grams take 32 columns");
+  switch (g.na) {
+    case 1: sgram_rect_launch<1, 32>(g, XA, XB, isp, G, w, r0, c0, partial, st); break;
+    case 2: sgram_rect_launch<2, 16>(g, XA, XB, isp, G, w, r0, c0, partial, st); break;
+    case 3: sgram_rect_launch<3, 16>(g, XA, XB, isp, G, w, r0, c0, partial, st); break;
     default: return;
   }
 }

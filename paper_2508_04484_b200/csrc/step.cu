@@ -555,10 +555,10 @@ void streaming_step(Handle& h, double dt) {
   phase(h, PH_SGRAM);
   if (k > 0) comm_halo_rows(g, state_q(h).p, state_q(h).rs, st);
   if (ru > 64 || wide) {
-    // [U0 | Q] in balanced blocks of <= 20 columns: every pair is a <= 40-column
-    // S-Gram launch, the kernel's best-tuned width
+    // [U0 | Q] in balanced blocks of <= 32 columns, one rectangular S-Gram
+    // launch per block pair (stencil_grams_blocks)
     const std::vector<NMat> blocks =
-        split_joint(h, U0, k > 0 ? state_q(h) : NMat{}, 20, h.wide_gb);
+        split_joint(h, U0, k > 0 ? state_q(h) : NMat{}, 32, h.wide_gb);
     stencil_grams_blocks(h, blocks, isp, G);
   } else {
     stencil_grams(g, U0, k > 0 ? state_q(h) : NMat{}, isp, G, h.part, st);

@@ -9,8 +9,8 @@
 //             -- the U0 S0 term as one LINCOMB pass, then one K-stage per input
 //             block, each taking the previous partial sum as its base rows
 //             (S0 = I); only the last one applies the output's 1/S;
-//   S-Grams:  G_s over every pair of blocks (i, j) (one <= 64-column S-Gram
-//             launch each), scattered into the w x w Grams.
+//   S-Grams:  G_s block by block: one rectangular launch per (i, j) pair
+//             (stencil_grams_rect), placed into the w x w Grams.
 #include "handle.h"
 
 namespace pnd {
@@ -54,18 +54,6 @@ __global__ void msub_kernel(const double* __restrict__ M, int ns, int rows, int 
 
 __global__ void eye_b_kernel(double* I, int b) {
   for (int i = threadIdx.x; i < b * b; i += blockDim.x) I[i] = (i / b == i % b) ? 1.0 : 0.0;
-}
-
-// pair Gram P (ns x w2 x w2, w2 = ci + cj) -> its four blocks of G (ns x w x w)
-__global__ void scatter_pair_kernel(const double* __restrict__ P, int ns, int ci, int cj, int oi,
-                                    int oj, int w, double* __restrict__ G) {
-  const int w2 = ci + cj, total = ns * w2 * w2;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const int s = e / (w2 * w2), rem = e - s * w2 * w2, p = rem / w2, q = rem - p * w2;
-    const int gr = p < ci ? oi + p : oj + p - ci;
-    const int gc = q < ci ? oi + q : oj + q - ci;
-    G[((size_t)s * w + gr) * w + gc] = P[e];
-  }
 }
 
 int grid_n(long n) {
@@ -179,15 +167,13 @@ void stencil_grams_blocks(Handle& h, const std::vector<NMat>& B, const double* i
     stencil_grams(g, B[0], NMat{}, isp, G, h.part, h.st);
     return;
   }
-  double* P = h.wide_g.get((size_t)ns * 2 * WB * 2 * WB);  // one size: no reallocation
+  // every (A, B) block pair: one rectangular launch (B's features contracted
+  // with A's rows), placed into the w x w Grams; one allreduce at the end
+  (void)ns;
   for (int i = 0; i < nb; ++i)
-    for (int j = i + 1; j < nb; ++j) {
-      const int w2 = B[i].cols + B[j].cols;
-      stencil_grams(g, B[i], B[j], isp, P, h.part, h.st);
-      scatter_pair_kernel<<<grid_n((long)ns * w2 * w2), 256, 0, h.st>>>(
-          P, ns, B[i].cols, B[j].cols, off[i], off[j], w, G);
-      launched();
-    }
+    for (int j = 0; j < nb; ++j)
+      stencil_grams_rect(g, B[i], B[j], isp, G, w, off[i], off[j], h.part, h.st);
+  comm_allreduce(g, G, (size_t)g.ns * w * w, h.st);
 }
 
 }  // namespace pnd

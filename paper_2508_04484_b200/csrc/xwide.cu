@@ -17,7 +17,8 @@
 //               two Y blocks per pass; symmetric Grams only j >= i);
 //   K-stage     one chain per output block (wide.cu: base rows U0 S0 by
 //               bm_lincomb, then one K-stage per input block);
-//   S-Grams     stencil_grams_blocks over all block pairs of [U0 | Q];
+//   S-Grams     one rectangular launch per (A, B) block pair of [U0 | Q]
+//               (stencil_grams_rect: B's features contracted with A's rows);
 // and the small side (R x R SVD / QR / RK4, m-side QR, the r x r implicit
 // solves) runs on the same kernels with their work matrices in global
 // (L2-resident) memory above the shared-memory sizes (dense.cu).
@@ -676,6 +677,8 @@ void streaming_step_x(Handle& h, double dt) {
       blocks.push_back(q);
     }
   }
+  // every (A, B) block pair: one rectangular launch (features of B formed
+  // once per pair, no diagonal-block recomputation), one allreduce at the end
   stencil_grams_blocks(h, blocks, isp, G);
 
   phase(h, PH_LSIDE);
