@@ -144,13 +144,13 @@ def separable_flux(b, beam):
 
 class Workload:
     def __init__(self, nside=256, rank=20, device=0, n_max=19, slab=None, comm_id=None,
-                 model="fokker-planck", energy=70.0, phantom="water"):
+                 model="fokker-planck", energy=70.0, phantom="water", h=0.025):
         """slab: this process's z-planes of the joint multi-GPU solve (slabs.plan),
         comm_id the world's NCCL id; None = the whole grid on this GPU."""
         from paper_2508_04484_b200 import _lib
         from paper_2508_04484_b200.driver import DeviceSolver
 
-        self.bundle, self.ops, beam = make_workload(nside=nside, rank=rank, n_max=n_max,
+        self.bundle, self.ops, beam = make_workload(nside=nside, h=h, rank=rank, n_max=n_max,
                                                     model=model, energy=energy, phantom=phantom)
         b = self.bundle
         self.rank = rank

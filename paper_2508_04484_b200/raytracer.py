@@ -343,18 +343,26 @@ def trace_beam_ops(beam, grid, space, key_of_cell, gmats, s_min, n_side=21, span
     by_sig = {}
     ray_seg_off, r_cells, r_len, ray_march, ray_w = [0], [], [], [], []
     n_alive = 0
+    # the bundle's segments as Python scalars once (the per-ray loop below then
+    # touches no numpy scalars); lengths are the same float64 differences
+    off_l = offsets.tolist()
+    cell_l = cells.tolist()
+    len_l = (t1 - t0).tolist()
+    # round(numpy float64, 12) as the reference's signature rounds (np.round)
+    rnd_l = np.round(t1 - t0, 12).tolist()
+    key_l = keys[cells].tolist() if len(cells) else []
     for r in range(len(offs)):
-        lo, hi = int(offsets[r]), int(offsets[r + 1])
+        lo, hi = off_l[r], off_l[r + 1]
         if hi == lo:
             continue                                         # ray misses the domain
         n_alive += 1
-        segs = [(int(c), b - a) for c, a, b in zip(cells[lo:hi], t0[lo:hi], t1[lo:hi])
-                if b - a > 1e-12]
+        idx = [i for i in range(lo, hi) if len_l[i] > 1e-12]
+        segs = [(cell_l[i], len_l[i]) for i in idx]
         if not segs:
             continue
-        sig = tuple((int(keys[c]), round(length, 12)) for c, length in segs)
+        sig = tuple((key_l[i], rnd_l[i]) for i in idx)
         if sig not in by_sig:
-            by_sig[sig] = plan.add([(length, int(keys[c])) for c, length in segs])
+            by_sig[sig] = plan.add([(len_l[i], key_l[i]) for i in idx])
         ray_march.append(by_sig[sig])
         r_cells.extend(c for c, _ in segs)
         r_len.extend(length for _, length in segs)

@@ -1,5 +1,8 @@
+"""Config 1 (BASELINE configs[0]) step timing: wall time per energy step of the
+device loop and the per-phase CUDA-event split (python tools/config1_profile.py [STEPS])."""
 import sys, time, json
 sys.path.insert(0, '.')
+STEPS = int(sys.argv[1]) if len(sys.argv) > 1 else 200
 import numpy as np
 from paper_2508_04484_b200 import _lib
 from paper_2508_04484_b200.driver import DeviceSolver
@@ -13,12 +16,12 @@ h = s.h
 h.call("pnd_synchronize")
 h.call("pnd_timing", 1)
 t0 = time.perf_counter(); tc = 0.0
-for k in range(5, 205):
+for k in range(5, 5 + STEPS):
     a = time.perf_counter(); s.set_coefficients(edges[k], edges[k+1]); tc += time.perf_counter() - a
     s.step(edges[k]-edges[k+1])
 h.call("pnd_synchronize")
 t = time.perf_counter() - t0
 nph = len(_lib.PHASES); ms = np.zeros(nph); cnt = np.zeros(nph, dtype=np.int32)
 h.call("pnd_timing_get", nph, _lib.ptr(ms), _lib.ptr(cnt))
-print("per step ms", 1000*t/200, "host coeff ms", 1000*tc/200)
-for n, v in zip(_lib.PHASES, ms): print(n, round(v/200, 4))
+print("per step ms", 1000*t/STEPS, "host coeff ms", 1000*tc/STEPS)
+for n, v in zip(_lib.PHASES, ms): print(n, round(v/STEPS, 4))
