@@ -67,6 +67,13 @@ int pnd_set_flux_table(pnd_handle* h, int beam, int n_beams, int n_groups, const
                        const double* t_m);
 int pnd_select_flux(pnd_handle* h, int which, const int32_t* j0, const double* w0,
                     const int32_t* j1, const double* w1);
+/* The same group table stored on its ray footprint only (trace_beam deposits
+ * into the cells its rays cross, raytracer.py:509-519): cells (nnz, strictly
+ * increasing) and their values (nnz x G row-major); at_energy() is 0 in every
+ * other cell. A traced pencil beam touches a small fraction of a 256^3 grid,
+ * whose dense table would be 17 GB per beam at 128 groups. */
+int pnd_set_flux_table_sparse(pnd_handle* h, int beam, int n_beams, int n_groups, int nnz,
+                              const int32_t* cells, const double* values, const double* t_m);
 /* Per-step coefficient assembly on the device: the
  * tables behind Problem.class_stopping (stopping.py:48-56, 107-120: log E and
  * log S per element, 12 x K), Problem.scattering_tables (driver.py:277-362,

@@ -248,8 +248,14 @@ int pnd_destroy(pnd_handle* hh) {
                        &h.part, &h.dep, &h.prev, &h.tq_m.tau, &h.tq_m.tree, &h.tq_m.rbuf,
                        &h.tq_m.cbuf, &h.ctab, &h.csel, &h.wide_m, &h.wide_t, &h.wide_i,
                        &h.wide_g, &h.fr_scr, &h.fr_scr2, &h.fr_scr3, &h.fr_eye,
-                       &h.sep_lat, &h.sep_depth};
+                       &h.sep_lat, &h.sep_depth, &h.cq_work};
   for (auto* b : bufs) b->free_();
+  // ranks above 64 (xwide.cu) and the sparse flux tables
+  for (auto* v : {&h.xU, &h.xQ, &h.xUn, &h.xW1, &h.xW2})
+    for (auto& b : *v) b.d.free_();
+  for (auto& b : h.xsm) b.free_();
+  for (auto& b : h.sp_vals) b.free_();
+  for (auto& b : h.sp_cells) b.free_();
   pnd::NBuf* nb[] = {&h.U, &h.Q, &h.Un, &h.Qa, &h.W1, &h.W2, &h.Xs, &h.wide_base,
                      &h.wide_tmp[0], &h.wide_tmp[1], &h.fr_t[0], &h.fr_t[1]};
   for (auto* b : nb) b->d.free_();
@@ -335,6 +341,9 @@ int pnd_set_inv_s(pnd_handle* hh, const double* inv_s) {
     pnd::set_isp(h);
     CK(cudaStreamSynchronize(h.st));
     h.have_inv_s = true;
+    int uni = 1;
+    for (int i = 1; i < h.g.n && uni; ++i) uni = inv_s[i] == inv_s[0];
+    h.g.uniform_s = uni;
   });
 }
 
@@ -349,6 +358,7 @@ int pnd_set_class_stopping(pnd_handle* hh, const double* class_s) {
     pnd::class_gather_inv(h.cls.p, v, h.g.n, d, sf, h.st);
     pnd::set_isp(h);
     h.have_inv_s = true;
+    h.g.uniform_s = h.n_cls == 1;
   });
 }
 
@@ -382,6 +392,7 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
       h.n_groups = n_groups;
       h.n_beams = n_beams;
       h.flux_sep = false;
+      h.flux_sparse = false;
       h.sep_lat.free_();
       h.sep_depth.free_();
       h.flux.get((size_t)n_beams * n_groups * h.g.ld);
@@ -400,6 +411,44 @@ int pnd_set_flux_table(pnd_handle* hh, int beam, int n_beams, int n_groups, cons
     up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
     CK(cudaStreamSynchronize(h.st));
     stage.free_();
+  });
+}
+
+int pnd_set_flux_table_sparse(pnd_handle* hh, int beam, int n_beams, int n_groups, int nnz,
+                              const int32_t* cells, const double* values, const double* t_m) {
+  return guard(hh, [&](Handle& h) {
+    if (n_beams < 1 || n_beams > 4) pnd::fail(PND_ECONFIG, "1..4 beams supported");
+    if (beam < 0 || beam >= n_beams) pnd::fail(PND_ECONFIG, "beam index out of range");
+    if (nnz < 0 || nnz > h.g.n) pnd::fail(PND_ECONFIG, "sparse flux: bad cell count");
+    for (int i = 0; i < nnz; ++i)
+      if (cells[i] < 0 || cells[i] >= h.g.n || (i && cells[i] <= cells[i - 1]))
+        pnd::fail(PND_ECONFIG, "sparse flux: cells must be increasing and inside the grid");
+    if (beam == 0) {
+      h.n_groups = n_groups;
+      h.n_beams = n_beams;
+      h.flux_sep = false;
+      h.flux_sparse = true;
+      h.flux.free_();
+      h.sep_lat.free_();
+      h.sep_depth.free_();
+      h.sp_cells.resize(n_beams);
+      h.sp_vals.resize(n_beams);
+      h.sp_nnz.assign(n_beams, 0);
+      h.psi.get((size_t)n_beams * h.g.ld + 64);
+      h.psi_lo.get((size_t)n_beams * h.g.ld);
+      h.tm.get((size_t)n_beams * h.m);
+    } else if (n_groups != h.n_groups || n_beams != h.n_beams || !h.flux_sparse) {
+      pnd::fail(PND_ECONFIG, "all beams must share the group grid (set beam 0 first)");
+    }
+    h.sp_nnz[beam] = nnz;
+    int* dc = h.sp_cells[beam].get((size_t)(nnz > 0 ? nnz : 1));
+    double* dv = h.sp_vals[beam].get((size_t)(nnz > 0 ? nnz : 1) * n_groups);
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(dc, cells, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, h.st));
+      up(dv, values, (size_t)nnz * n_groups, h.st);
+    }
+    up(h.tm.p + (size_t)beam * h.m, t_m, h.m, h.st);
+    CK(cudaStreamSynchronize(h.st));
   });
 }
 
@@ -474,6 +523,12 @@ int pnd_select_flux(pnd_handle* hh, int which, const int32_t* j0, const double* 
                                 h.sep_depth.p + (size_t)b * h.g.nz * h.n_groups, nxy, h.n_groups,
                                 h.g.n, nullptr, nullptr, j0[b], w0[b], j1[b], w1[b],
                                 dst + (size_t)b * h.g.ld, h.st);
+        continue;
+      }
+      if (h.flux_sparse) {
+        pnd::psi_lerp_sparse(h.sp_cells[b].p, h.sp_vals[b].p, h.sp_nnz[b], h.n_groups, h.g.n,
+                             nullptr, nullptr, j0[b], w0[b], j1[b], w1[b],
+                             dst + (size_t)b * h.g.ld, h.st);
         continue;
       }
       const double* tab = h.flux.p + (size_t)b * h.n_groups * h.g.ld;
@@ -1122,6 +1177,7 @@ int pnd_set_flux_separable(pnd_handle* hh, int beam, int n_beams, int n_groups,
       h.n_beams = n_beams;
       h.flux.free_();  // the factors replace any dense tables
       h.flux_sep = true;
+      h.flux_sparse = false;
       h.sep_lat.get((size_t)n_beams * nxy);
       h.sep_depth.get((size_t)n_beams * h.g.nz * n_groups);
       h.psi.get((size_t)n_beams * h.g.ld + 64);

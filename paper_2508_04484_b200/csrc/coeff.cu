@@ -235,6 +235,7 @@ void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo) {
   class_gather_inv(h.cls.p, cs, h.g.n, d, sf, h.st);
   set_isp(h);
   h.have_inv_s = true;
+  h.g.uniform_s = h.n_cls == 1;
   h.have_scat = true;
   // uncollided slices
   for (int which = 0; which < (want_lo ? 2 : 1); ++which) {
@@ -248,6 +249,11 @@ void coefficients_at(Handle& h, double e_mid, double e_lo, bool want_lo) {
                            h.sep_depth.p + (size_t)b * h.g.nz * h.n_groups, nxy, h.n_groups,
                            h.g.n, sj + 2 * s, sw + 2 * s, 0, 0.0, 0, 0.0,
                            dst + (size_t)b * h.g.ld, h.st);
+        continue;
+      }
+      if (h.flux_sparse) {
+        psi_lerp_sparse(h.sp_cells[b].p, h.sp_vals[b].p, h.sp_nnz[b], h.n_groups, h.g.n,
+                        sj + 2 * s, sw + 2 * s, 0, 0.0, 0, 0.0, dst + (size_t)b * h.g.ld, h.st);
         continue;
       }
       lerp_dev_kernel<<<sm_count() * 8, 256, 0, h.st>>>(

@@ -163,6 +163,11 @@ void comm_destroy(Comm* c) {
   delete c;
 }
 
+int comm_world(const Geom& g) {
+  auto* c = static_cast<Comm*>(g.comm);
+  return c ? c->world : 1;
+}
+
 void comm_allreduce(const Geom& g, double* p, size_t count, cudaStream_t st) {
   auto* c = static_cast<Comm*>(g.comm);
   if (!c || c->world <= 1 || count == 0) return;

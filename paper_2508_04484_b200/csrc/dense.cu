@@ -649,83 +649,6 @@ __global__ void __launch_bounds__(512)
   }
 }
 
-// The same Householder QR (same reflectors, same explicit-Q formation) in ONE
-// warp: the m-side factors (rows = m moments, <= 64 columns) are small enough
-// that the one-CTA version spends its time in block-wide barriers and
-// reductions (3 per column); a warp needs only __syncwarp and shuffles.
-__global__ void __launch_bounds__(32)
-    qr_warp_kernel(const double* __restrict__ A, int rows, int cols, int lda,
-                   double* __restrict__ Q, int ldq, double* __restrict__ rfac) {
-  extern __shared__ double sm[];
-  const int LDS = cols | 1;
-  double* S = sm;                       // rows x LDS
-  double* tau = S + (size_t)rows * LDS;  // cols
-  const int lane = threadIdx.x;
-  for (int idx = lane; idx < rows * cols; idx += 32) {
-    const int i = idx % rows, j = idx / rows;
-    S[i * LDS + j] = A[(size_t)i + (size_t)j * lda];
-  }
-  __syncwarp();
-  const int kk = rows < cols ? rows : cols;
-  for (int j = 0; j < kk; ++j) {
-    double part = 0.0;
-    for (int i = j + 1 + lane; i < rows; i += 32) part += S[i * LDS + j] * S[i * LDS + j];
-    const double xnorm2 = warp_sum(part);
-    double tj = 0.0;
-    if (xnorm2 > 0.0) {
-      const double alpha = S[j * LDS + j];
-      const double beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
-      tj = (beta - alpha) / beta;
-      const double scl = 1.0 / (alpha - beta);
-      for (int i = j + 1 + lane; i < rows; i += 32) S[i * LDS + j] *= scl;
-      __syncwarp();
-      for (int k = j + 1; k < cols; ++k) {
-        double sacc = 0.0;
-        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
-        const double w = S[j * LDS + k] + warp_sum(sacc);
-        __syncwarp();
-        if (lane == 0) S[j * LDS + k] -= tj * w;
-        for (int i = j + 1 + lane; i < rows; i += 32) S[i * LDS + k] -= tj * S[i * LDS + j] * w;
-        __syncwarp();
-      }
-      if (lane == 0) S[j * LDS + j] = beta;
-    }
-    if (lane == 0) tau[j] = tj;
-    __syncwarp();
-  }
-  for (int idx = lane; idx < kk * cols; idx += 32) {
-    const int i = idx / cols, j = idx - i * cols;
-    rfac[idx] = i <= j ? S[i * LDS + j] : 0.0;
-  }
-  __syncwarp();
-  for (int j = kk - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (j < kk - 1 && tj != 0.0) {
-      for (int k = j + 1; k < kk; ++k) {
-        double sacc = 0.0;
-        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
-        const double w = S[j * LDS + k] + warp_sum(sacc);
-        __syncwarp();
-        if (lane == 0) S[j * LDS + k] -= tj * w;
-        for (int i = j + 1 + lane; i < rows; i += 32) S[i * LDS + k] -= tj * S[i * LDS + j] * w;
-        __syncwarp();
-      }
-    }
-    for (int i = lane; i < rows; i += 32) {
-      double v;
-      if (i < j) v = 0.0;
-      else if (i == j) v = 1.0 - tj;
-      else v = -tj * S[i * LDS + j];
-      S[i * LDS + j] = v;
-    }
-    __syncwarp();
-  }
-  for (int idx = lane; idx < rows * kk; idx += 32) {
-    const int i = idx % rows, j = idx / rows;
-    Q[(size_t)i + (size_t)j * ldq] = S[i * LDS + j];
-  }
-}
-
 void set_smem(const void* fn, size_t bytes) {
   if (bytes > (size_t)kMaxDynSmem) fail(PND_ECONFIG, "kernel tile exceeds shared memory");
   allow_max_smem(fn);
@@ -806,14 +729,6 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
   if (cols > 512) fail(PND_ECONFIG, "orthonormalisation supports at most 512 columns");
   const int kc = rows < cols ? rows : cols;
   {
-    // small m-side factors: one warp (no block barriers)
-    const size_t smw = ((size_t)rows * (cols | 1) + (size_t)cols) * sizeof(double);
-    if (cols <= 64 && smw + 1024 <= (size_t)kMaxDynSmem) {
-      set_smem((const void*)qr_warp_kernel, smw);
-      qr_warp_kernel<<<1, 32, smw, st>>>(a, rows, cols, lda, q, ldq, rfac);
-      launched();
-      return kc;
-    }
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
     if (sm + 1024 <= (size_t)kMaxDynSmem) {

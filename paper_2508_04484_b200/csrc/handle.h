@@ -53,7 +53,15 @@ struct Handle {
   // dense table is 137 GB per beam; the per-step slices are formed from the factors
   DBuf sep_lat, sep_depth;
   bool flux_sep = false;
-  bool have_flux() const { return flux.p != nullptr || flux_sep; }
+  // ray-footprint (sparse) group tables (pnd_set_flux_table_sparse): per beam
+  // the cells its rays touched and their nnz x G values -- a traced 121-ray
+  // pencil at 256^3 touches ~0.2 % of the cells; the dense table would be
+  // 17 GB per beam at 128 groups
+  std::vector<IBuf> sp_cells;
+  std::vector<DBuf> sp_vals;
+  std::vector<int> sp_nnz;
+  bool flux_sparse = false;
+  bool have_flux() const { return flux.p != nullptr || flux_sep || flux_sparse; }
   bool have_angular = false, have_inv_s = false, have_mat = false, have_scat = false;
   // per-step coefficient tables (coeff.cu, pnd_set_coefficient_tables):
   // [log E | log S (12 x K each) | rho (n_cls) | w (n_cls x 12) | E_mom (P) |

@@ -441,6 +441,33 @@ void psi_lerp_separable(const double* lat, const double* depth, int nxy, int G, 
   launched();
 }
 
+namespace {
+__global__ void lerp_sparse_kernel(const int* __restrict__ cells, const double* __restrict__ v,
+                                   int nnz, int G, const int* __restrict__ sel_j,
+                                   const double* __restrict__ sel_w, int j0h, double w0h, int j1h,
+                                   double w1h, double* __restrict__ out) {
+  const int j0 = sel_j ? sel_j[0] : j0h, j1 = sel_j ? sel_j[1] : j1h;
+  const double w0 = sel_w ? sel_w[0] : w0h, w1 = sel_w ? sel_w[1] : w1h;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += gridDim.x * blockDim.x) {
+    const double* row = v + (size_t)i * G;
+    double x;
+    if (w1 == 0.0) x = w0 == 1.0 ? row[j0] : w0 * row[j0];
+    else x = w0 * row[j0] + w1 * row[j1];
+    out[cells[i]] = x;
+  }
+}
+}  // namespace
+
+void psi_lerp_sparse(const int* cells, const double* values, int nnz, int G, int n,
+                     const int* sel_j, const double* sel_w, int j0, double w0, int j1, double w1,
+                     double* out, cudaStream_t st) {
+  fill_zero(out, (size_t)n, st);
+  if (nnz <= 0) return;
+  lerp_sparse_kernel<<<grid_for(nnz, 256), 256, 0, st>>>(cells, values, nnz, G, sel_j, sel_w, j0,
+                                                         w0, j1, w1, out);
+  launched();
+}
+
 void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, double w1,
               double* out, cudaStream_t st) {
   lerp_kernel<<<grid_for(n, 256), 256, 0, st>>>(values, ldv, n, j0, w0, j1, w1, out);

@@ -74,6 +74,9 @@ struct Geom {
   int nzg = 0;    // 0: single device (nzg = nz)
   double inv_nx = 0.0, inv_nxy = 0.0;  // 1/nx, 1/(nx ny): cell -> (i, j, k) without division
   void* comm = nullptr;
+  // 1/S is the same in every cell (one material class): the stencil Grams then
+  // form only the D+ stencils and take D- = -(D+)^T + boundary rows (stencil.cu)
+  int uniform_s = 0;
 };
 
 // ------------------------------------------------------------ slab communication (comm.cu)
@@ -81,6 +84,8 @@ struct Comm;
 void comm_unique_id(char* out128);
 Comm* comm_create(const char* id128, int rank, int world);
 void comm_destroy(Comm* c);
+// ranks of the slab communicator (1 without one)
+int comm_world(const Geom& g);
 // sum a small device block over the slabs (no-op on one device)
 void comm_allreduce(const Geom& g, double* p, size_t count, cudaStream_t st);
 // fill the 2-plane halo rows of an n-side matrix from the neighbouring slabs
@@ -139,6 +144,10 @@ void kstage(const KStageArgs& a, cudaStream_t st);
 // stencil Grams: out[s] = [X1 | X2]^T D_s S^-1 [X1 | X2]  (ns x w x w, w = X1.cols + X2.cols)
 void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* inv_s, double* out,
                    DBuf& partial, cudaStream_t st);
+// one material class: the D- stencil Grams from the D+ ones (out holds the D+
+// Grams in its even slots): D- = -(D+)^T + boundary rows, per axis
+void minus_from_plus(const Geom& g, NMat X1, NMat X2, const double* isp, double* out,
+                     DBuf& partial, cudaStream_t st);
 // rectangular stencil Grams of two <= 32-column blocks, placed into an
 // ns x w x w Gram at rows r0.., columns c0..: G_s[r0 + i][c0 + j] = (XA^T D_s S^-1 XB)_ij
 // (not summed over slabs: the caller allreduces the assembled Gram)
@@ -204,6 +213,11 @@ void psi_lerp_separable(const double* lat, const double* depth, int nxy, int G, 
                         double w1, double* out, cudaStream_t st);
 void psi_lerp(const double* values, int ldv, int n, int j0, double w0, int j1, double w1,
               double* out, cudaStream_t st);
+// sparse (ray-footprint) table: out = 0, then out[cells[i]] = w0 v[i][j0] + w1 v[i][j1]
+// (v: nnz x G row-major; sel_j / sel_w on the device, or the host scalars)
+void psi_lerp_sparse(const int* cells, const double* values, int nnz, int G, int n,
+                     const int* sel_j, const double* sel_w, int j0, double w0, int j1, double w1,
+                     double* out, cudaStream_t st);
 // row-major host-layout (n x c) <-> column-major (ld) device layout (flux tables, TSQR)
 void transpose_in(const double* src_rowmajor, int n, int c, double* dst, int ldd, cudaStream_t st);
 void transpose_out(const double* src, int lds, int n, int c, double* dst_rowmajor,

@@ -527,11 +527,14 @@ void kstage_na(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
 // stencil-column tiles bt = bt0 + m + 7u (bt = s T8 + tj) against all T8 row tiles, one
 // accumulator per tile (T8 UPW independent chains); launches cover column-tile
 // ranges of at most 32 tiles.
-template <int NA, int T8, int GC>
+// PO (plus only): only the D+ stencil of every axis is formed and contracted
+// (NA Grams); the D- Grams follow from them (reduce_minus: one material
+// class, single device)
+template <int NA, int T8, int GC, bool PO = false>
 __global__ void __launch_bounds__(gpth(T8), 1)
     sgram_kernel(Geom g, NMat X1, NMat X2, Seg S, int nstg, const double* __restrict__ isp,
                  int bt0, int nbt, double* __restrict__ partial) {
-  constexpr int NS = 2 * NA;
+  constexpr int NS = PO ? NA : 2 * NA;  // stencils formed
   constexpr int W = T8 * 8;
   constexpr int XS = pad4(W);
   constexpr int GCONW = gconw(T8), GPTH = gpth(T8);
@@ -591,11 +594,11 @@ __global__ void __launch_bounds__(gpth(T8), 1)
       for (int t = 0; t < TT; ++t) {
         const int j = cj + JS * t;
         if (j < a1) {
-          double v[NS];
+          double v[2 * NA];
           if (fast) cx.template apply<true>(g, JS * t, v);
           else cx.template apply<false>(g, JS * t, v);
 #pragma unroll
-          for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
+          for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[PO ? 2 * s : s];
         }
       }
       if (a2) {
@@ -605,11 +608,11 @@ __global__ void __launch_bounds__(gpth(T8), 1)
         for (int t = 0; t < TT; ++t) {
           const int j = j0 + JS * t;
           if (j < w) {
-            double v[NS];
+            double v[2 * NA];
             if (fast) cx.template apply<true>(g, JS * t, v);
             else cx.template apply<false>(g, JS * t, v);
 #pragma unroll
-            for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[s];
+            for (int s = 0; s < NS; ++s) Fb[(s * W + j) * GTL + ci] = v[PO ? 2 * s : s];
           }
         }
       }
@@ -799,6 +802,17 @@ __global__ void __launch_bounds__(gpth(T8B), 1)
   }
 }
 
+// the D+ partials (NA x per) summed in fixed order into the even stencil slots
+__global__ void reduce_parts_po(const double* __restrict__ partial, int nblk, int count, int per,
+                                StScale sc, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
+  const int a = i / per;
+  out[(size_t)(2 * a) * per + (i - a * per)] = s * sc.v[a];
+}
+
 // sums the per-CTA Gram partials in a fixed order and applies the stencil's
 // 1/(2h) (count = ns * per)
 __global__ void reduce_parts(const double* __restrict__ partial, int nblk, int count, int per,
@@ -810,31 +824,43 @@ __global__ void reduce_parts(const double* __restrict__ partial, int nblk, int c
   out[i] = s * sc.v[i / per];
 }
 
-template <int NA, int T8, int GC>
+template <int NA, int T8, int GC, bool PO = false>
 void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
                   cudaStream_t st) {
   constexpr int GTL = pad4(GC);
+  constexpr int NSF = PO ? NA : 2 * NA;
   const NMat ins[2] = {X1, X2};
   const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr);
   const int W = T8 * 8;
-  const size_t ft = (size_t)2 * NA * W * GTL + (size_t)GC * pad4(W);
+  const size_t ft = (size_t)NSF * W * GTL + (size_t)GC * pad4(W);
   const size_t fixed = 2 * ft * sizeof(double) + sizeof(PipeBars);
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) fail(PND_ECONFIG, "stencil Gram tile exceeds shared memory");
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  allow_max_smem(sgram_kernel<NA, T8, GC>);
+  allow_max_smem(sgram_kernel<NA, T8, GC, PO>);
   const int nchunks = (g.n + GC - 1) / GC;
-  int grid = sm_count() * resident(sgram_kernel<NA, T8, GC>, gpth(T8), smem);
+  int grid = sm_count() * resident(sgram_kernel<NA, T8, GC, PO>, gpth(T8), smem);
   if (grid > nchunks) grid = nchunks;
   const int w = X1.cols + (X2.p ? X2.cols : 0);
-  const size_t count = (size_t)2 * NA * w * w;
+  const size_t count = (size_t)NSF * w * w;
   double* part = partial.get(count * grid);
-  const int nb = 2 * NA * T8;
+  const int nb = NSF * T8;
   for (int bt0 = 0; bt0 < nb; bt0 += 32) {
     const int nbt = nb - bt0 < 32 ? nb - bt0 : 32;
-    sgram_kernel<NA, T8, GC><<<grid, gpth(T8), smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt,
-                                                        part);
+    sgram_kernel<NA, T8, GC, PO><<<grid, gpth(T8), smem, st>>>(g, X1, X2, S, nstg, isp, bt0, nbt,
+                                                            part);
     launched();
+  }
+  if (PO) {
+    // the D+ Grams into the even stencil slots, then D- = -(D+)^T + boundary rows
+    StScale sc = stencil_scale(g), sp{};
+    for (int a = 0; a < NA; ++a) sp.v[a] = sc.v[2 * a];
+    reduce_parts_po<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, w * w,
+                                                                sp, out);
+    launched();
+    minus_from_plus(g, X1, X2, isp, out, partial, st);
+    comm_allreduce(g, out, (size_t)2 * NA * w * w, st);
+    return;
   }
   reduce_parts<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, w * w,
                                                            stencil_scale(g), out);
@@ -883,6 +909,20 @@ template <int NA>
 void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, DBuf& partial,
               cudaStream_t st) {
   const int w = X1.cols + (X2.p ? X2.cols : 0);
+  // one material class on one device: half the stencil Grams (the D+ ones)
+  if (g.uniform_s && comm_world(g) == 1 && !getenv("PND_SGRAM_FULL")) {
+    switch ((w + 7) / 8) {
+      case 1: sgram_launch<NA, 1, 32, true>(g, X1, X2, isp, out, partial, st); return;
+      case 2: sgram_launch<NA, 2, 32, true>(g, X1, X2, isp, out, partial, st); return;
+      case 3: sgram_launch<NA, 3, 32, true>(g, X1, X2, isp, out, partial, st); return;
+      case 4: sgram_launch<NA, 4, 16, true>(g, X1, X2, isp, out, partial, st); return;
+      case 5: sgram_launch<NA, 5, 16, true>(g, X1, X2, isp, out, partial, st); return;
+      case 6: sgram_launch<NA, 6, 16, true>(g, X1, X2, isp, out, partial, st); return;
+      case 7: sgram_launch<NA, 7, 8, true>(g, X1, X2, isp, out, partial, st); return;
+      case 8: sgram_launch<NA, 8, 8, true>(g, X1, X2, isp, out, partial, st); return;
+      default: break;
+    }
+  }
   switch ((w + 7) / 8) {
     case 1: sgram_launch<NA, 1, 32>(g, X1, X2, isp, out, partial, st); break;
     case 2: sgram_launch<NA, 2, 32>(g, X1, X2, isp, out, partial, st); break;
@@ -919,6 +959,123 @@ void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* isp, double* o
     case 3: sgram_na<3>(g, X1, X2, isp, out, partial, st); break;
     default: return;
   }
+}
+
+// ---------------------------------------------------------------- D- from D+
+// One material class (1/S = sigma in every cell), one device: along an axis
+// the reference's stencils (spatial.py:81-118) satisfy D- = -(D+)^T + E with
+// E nonzero only in the rows of the first two and last two cells of each
+// line, so X^T D- S^-1 X = -(X^T D+ S^-1 X)^T + sigma X^T E X: the D- Grams
+// cost a pass over the boundary cells (2 x 2 planes per axis) instead of a
+// stencil contraction over the whole grid.
+namespace {
+
+// coefficients x 2h of the reference's D+ (minus-biased) and D- rows
+double dplus_c(int r, int c) {
+  if (r >= 2) return c == r ? 3.0 : c == r - 1 ? -4.0 : c == r - 2 ? 1.0 : 0.0;
+  if (r == 1) return c == 1 ? 2.0 : c == 0 ? -2.0 : 0.0;
+  return c == 0 ? 2.0 : 0.0;
+}
+double dminus_c(int L, int r, int c) {
+  if (r <= L - 3) return c == r ? -3.0 : c == r + 1 ? 4.0 : c == r + 2 ? -1.0 : 0.0;
+  if (r == L - 2) return c == r ? -2.0 : c == r + 1 ? 2.0 : 0.0;
+  return c == r ? -2.0 : 0.0;
+}
+
+struct ERows {
+  int nb;          // boundary rows (<= 4)
+  int row[4];
+  double e[4][5];  // E[row][row + d], d = -2..2 (x 2h)
+};
+
+ERows e_rows(int L) {
+  ERows er{};
+  for (int i = 0; i < L; ++i) {
+    double e[5];
+    bool any = false;
+    for (int d = -2; d <= 2; ++d) {
+      const int j = i + d;
+      e[d + 2] = (j >= 0 && j < L) ? dminus_c(L, i, j) + dplus_c(j, i) : 0.0;
+      any = any || e[d + 2] != 0.0;
+    }
+    if (!any) continue;
+    if (er.nb >= 4) fail(PND_ECONFIG, "stencil transpose: unexpected interior rows");
+    er.row[er.nb] = i;
+    for (int d = 0; d < 5; ++d) er.e[er.nb][d] = e[d];
+    ++er.nb;
+  }
+  return er;
+}
+
+// boundary cells b of one axis -> Xb[b] = X[c], Zb[b] = sigma_c sum_d E[i][i+d] X[c + d s]
+__global__ void e_gather_kernel(int n, int L, long s, ERows er, NMat X1, NMat X2,
+                                const double* __restrict__ isp, NMat Xb, NMat Zb) {
+  const long M = n / L;
+  const long nb = er.nb * M;
+  const int a1 = X1.cols, w = a1 + (X2.p ? X2.cols : 0);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nb * w;
+       e += (long)gridDim.x * blockDim.x) {
+    const long b = e / w;
+    const int col = (int)(e - b * w);
+    const int p = (int)(b / M);
+    const long q = b - (long)p * M;
+    const long c = (q / s) * (s * L) + er.row[p] * s + (q % s);
+    auto at = [&](long cc) {
+      return col < a1 ? X1.p[cc * X1.rs + col] : X2.p[cc * X2.rs + col - a1];
+    };
+    double z = 0.0;
+    for (int d = 0; d < 5; ++d)
+      if (er.e[p][d] != 0.0) z += er.e[p][d] * at(c + (d - 2) * s);
+    Xb.p[b * Xb.rs + col] = at(c);
+    Zb.p[b * Zb.rs + col] = isp[2 * c] * z;
+  }
+}
+
+// out[2a + 1] = -out[2a]^T + corr * i2h
+__global__ void minus_assemble_kernel(double* out, int w, int a, const double* corr, double i2h) {
+  const int ww = w * w;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ww; e += gridDim.x * blockDim.x) {
+    const int r = e / w, c = e - r * w;
+    out[(size_t)(2 * a + 1) * ww + e] = -out[(size_t)(2 * a) * ww + (size_t)c * w + r] +
+                                        corr[e] * i2h;
+  }
+}
+
+}  // namespace
+
+void minus_from_plus(const Geom& g, NMat X1, NMat X2, const double* isp, double* out,
+                     DBuf& partial, cudaStream_t st) {
+  const int w = X1.cols + (X2.p ? X2.cols : 0);
+  const int rs = even(w);
+  double* corr = nullptr;
+  CK(cudaMallocAsync((void**)&corr, (size_t)w * w * sizeof(double), st));
+  for (int ai = 0; ai < g.na; ++ai) {
+    const int axis = g.axis[ai];
+    const int L = axis == 0 ? g.nx : axis == 1 ? g.ny : g.nz;
+    const long s = axis == 0 ? 1 : axis == 1 ? g.nx : (long)g.nx * g.ny;
+    const ERows er = e_rows(L);
+    const long nb = (long)er.nb * (g.n / L);
+    // compact boundary-cell matrices with 64 zero rows after them (chunked Gram)
+    Geom gb = g;
+    gb.n = (int)nb;
+    gb.halo = 64;
+    gb.comm = nullptr;
+    const size_t rows = (size_t)nb + 2 * 64;
+    double* buf = nullptr;
+    CK(cudaMallocAsync((void**)&buf, 2 * rows * rs * sizeof(double), st));
+    fill_zero(buf, 2 * rows * rs, st);
+    NMat Xb{buf + 64 * (size_t)rs, rs, w}, Zb{buf + (rows + 64) * (size_t)rs, rs, w};
+    long tot = nb * w;
+    int grid = (int)((tot + 255) / 256);
+    if (grid > 148 * 16) grid = 148 * 16;
+    e_gather_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(g.n, L, s, er, X1, X2, isp, Xb, Zb);
+    launched();
+    gram_xy(gb, Xb, Zb, corr, partial, st);
+    minus_assemble_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(out, w, ai, corr, g.i2h[axis]);
+    launched();
+    CK(cudaFreeAsync(buf, st));
+  }
+  CK(cudaFreeAsync(corr, st));
 }
 
 void stencil_grams_rect(const Geom& g, NMat XA, NMat XB, const double* isp, double* G, int w,

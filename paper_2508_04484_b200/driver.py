@@ -25,7 +25,7 @@ import numpy as np
 from . import _lib
 from .dlra import LowRankState, orthonormal_columns
 from .errors import ConfigError, NumericalError
-from .problem import SQRT_4PI, ProblemBundle, export_problem
+from .problem import SQRT_4PI, ProblemBundle, UncollidedSlices, export_bundle, export_problem
 
 TRUNCATE_FLAGS = {"streaming": 1, "scattering": 2, "both": 3}
 # largest factor rank the step kernels take (an augmented state holds 2x this;
@@ -78,9 +78,20 @@ class DeviceSolver:
         self.h.set_angular(*b.a_split())
         self.h.set_materials(b.cell_class[lo:hi], b.class_atomic)
         nb = len(b.fluxes)
+        sparse = any(f.cells is not None for f in b.fluxes)
         for i, (f, tm) in enumerate(zip(b.fluxes, b.t_ms)):
-            vals = _lib.f64(f.values[lo:hi])
             t = _lib.f64(tm)
+            if sparse:  # ray-footprint tables (pnd_set_flux_table_sparse)
+                f = f if f.cells is not None else UncollidedSlices(
+                    f.values, f.residual, f.e_min, f.e_max,
+                    np.arange(b.n_cells, dtype=np.int32), b.n_cells)
+                sel = (f.cells >= lo) & (f.cells < hi)
+                cells = np.ascontiguousarray(f.cells[sel] - lo, dtype=np.int32)
+                vals = _lib.f64(f.values[sel])
+                self.h.call("pnd_set_flux_table_sparse", i, nb, int(f.values.shape[1]),
+                            len(cells), _lib.ptr(cells), _lib.ptr(vals), _lib.ptr(t))
+                continue
+            vals = _lib.f64(f.values[lo:hi])
             self.h.call("pnd_set_flux_table", i, nb, int(vals.shape[1]), _lib.ptr(vals),
                         _lib.ptr(t))
         self.h.call("pnd_dose_reset")
@@ -459,7 +470,7 @@ def run_simulation(config, solver: str = "dlra"):
     finally:
         ref_driver.trace_beam = ref_trace
     t_ms = [beam_projection(config.pn_order, bm.direction) for bm in config.beams]
-    bundle = ProblemBundle.from_arrays(export_problem(problem, fluxes, t_ms))
+    bundle = export_bundle(problem, fluxes, t_ms)  # keeps ray-footprint tables sparse
     res = run_bundle(bundle, solver=solver)
     return reference_result(ref_driver, problem, fluxes, res, solver, t_start)
 

@@ -34,12 +34,27 @@ def pn_degrees(n_max: int) -> np.ndarray:
 
 @dataclass
 class UncollidedSlices:
-    """Group-sampled uncollided flux of one beam (raytracer.UncollidedFlux)."""
+    """Group-sampled uncollided flux of one beam (raytracer.UncollidedFlux).
 
-    values: np.ndarray        # (n, G) group representatives
-    residual: np.ndarray      # (n,) below-cutoff energy density
+    Dense (cells = None): values (n, G), residual (n,). Ray-footprint form
+    (cells = the strictly increasing cells the beam's rays touched): values
+    (nnz, G), residual (nnz,), zero in every other cell of the n_cells."""
+
+    values: np.ndarray        # (n, G) or (nnz, G) group representatives
+    residual: np.ndarray      # (n,) or (nnz,) below-cutoff energy density
     e_min: float
     e_max: float
+    cells: np.ndarray = None  # (nnz,) int32 footprint cells, or None (dense)
+    n_cells: int = 0          # grid cells (footprint form)
+
+    def dense(self) -> "UncollidedSlices":
+        if self.cells is None:
+            return self
+        v = np.zeros((self.n_cells, self.values.shape[1]))
+        r = np.zeros(self.n_cells)
+        v[self.cells] = self.values
+        r[self.cells] = self.residual
+        return UncollidedSlices(v, r, self.e_min, self.e_max)
 
     @property
     def n_groups(self) -> int:
@@ -72,6 +87,11 @@ class UncollidedSlices:
         return (j, 1.0 - w, j + 1, w)
 
     def at_energy(self, e: float) -> np.ndarray:
+        if self.cells is not None:
+            out = np.zeros(self.n_cells)
+            out[self.cells] = UncollidedSlices(self.values, self.residual, self.e_min,
+                                               self.e_max).at_energy(e)
+            return out
         j0, w0, j1, w1 = self.lerp_weights(e)
         if w0 == 0.0 and w1 == 0.0:
             return np.zeros(self.values.shape[0])
@@ -240,9 +260,10 @@ class ProblemBundle:
         """Group-sum tally sum_g S(E_g) psi_g h + residual (driver.py:452-461)."""
         deposited = np.zeros(self.n_cells)
         for flux in self.fluxes:
+            rows = slice(None) if flux.cells is None else flux.cells
             for g, e_g in enumerate(flux.centers):
-                deposited += self.stopping_field(e_g) * flux.values[:, g] * flux.width
-            deposited += flux.residual
+                deposited[rows] += self.stopping_field(e_g)[rows] * flux.values[:, g] * flux.width
+            deposited[rows] += flux.residual
         return deposited
 
     def subset_beams(self, beams) -> "ProblemBundle":
@@ -272,8 +293,8 @@ class ProblemBundle:
             "lam_plus": self.lam_plus,
             "lam_minus": self.lam_minus,
             "t_ms": self.t_ms,
-            "flux_values": np.stack([f.values for f in self.fluxes]),
-            "flux_residual": np.stack([f.residual for f in self.fluxes]),
+            "flux_values": np.stack([f.dense().values for f in self.fluxes]),
+            "flux_residual": np.stack([f.dense().residual for f in self.fluxes]),
             "flux_range": np.array([[f.e_min, f.e_max] for f in self.fluxes]),
             "scalars": np.array(
                 [self.pn_order, float(self.boltzmann_correction), self.fp_correction_scale,
@@ -334,7 +355,13 @@ class ProblemBundle:
 
 
 def export_problem(problem, fluxes, t_ms) -> dict:
-    """Compact arrays of a reference `Problem` + traced fluxes.
+    """Compact arrays of a reference `Problem` + traced fluxes (export_bundle's
+    ProblemBundle as .npz-able arrays; footprint tables densified)."""
+    return export_bundle(problem, fluxes, t_ms).to_arrays()
+
+
+def export_bundle(problem, fluxes, t_ms) -> "ProblemBundle":
+    """A reference `Problem` + traced fluxes as a ProblemBundle.
 
     `problem` is duck-typed on pndose.driver.Problem (driver.py:310-321);
     material classes are the unique (density, weights) rows, exactly the
@@ -373,7 +400,8 @@ def export_problem(problem, fluxes, t_ms) -> dict:
         lam_minus=np.stack(problem.ops.lam_minus),
         t_ms=np.stack(t_ms),
         fluxes=[
-            UncollidedSlices(f.values, f.residual_energy, f.space.e_min, f.space.e_max)
+            UncollidedSlices(f.values, f.residual_energy, f.space.e_min, f.space.e_max,
+                             getattr(f, "cells", None), int(getattr(f, "n_cells", 0) or 0))
             for f in fluxes
         ],
         model=cfg.model,
@@ -391,4 +419,4 @@ def export_problem(problem, fluxes, t_ms) -> dict:
         seed=cfg.seed,
         name=cfg.name,
     )
-    return bundle.to_arrays()
+    return bundle

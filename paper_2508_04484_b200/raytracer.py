@@ -304,6 +304,10 @@ class UncollidedFlux:
     values: np.ndarray
     residual_energy: np.ndarray
     n_rays: int
+    # ray-footprint form: the cells the rays touched (strictly increasing);
+    # values / residual_energy then hold only those rows (zero elsewhere)
+    cells: np.ndarray = None
+    n_cells: int = 0
 
     @property
     def group_energies(self):
@@ -316,6 +320,11 @@ class UncollidedFlux:
 
     def at_energy(self, e_mev) -> np.ndarray:
         """Group-centre interpolation, zero outside (raytracer.py:437-449)."""
+        if self.cells is not None:
+            out = np.zeros(self.n_cells)
+            out[self.cells] = UncollidedFlux(self.beam, self.space, self.values,
+                                             self.residual_energy, self.n_rays).at_energy(e_mev)
+            return out
         centers = self.group_energies
         if e_mev <= centers[0] or e_mev >= centers[-1]:
             j = 0 if e_mev <= centers[0] else self.values.shape[1] - 1
@@ -326,9 +335,16 @@ class UncollidedFlux:
         return (1.0 - w) * self.values[:, j] + w * self.values[:, j + 1]
 
 
+# traced tables larger than this are kept on the rays' footprint (sparse)
+SPARSE_BYTES = 1 << 31
+
+
 def trace_beam_ops(beam, grid, space, key_of_cell, gmats, s_min, n_side=21, span_sigmas=3.0,
-                   max_step=MAX_STEP_CM):
-    """trace_beam from assembled operators: gmats / s_min keyed by material."""
+                   max_step=MAX_STEP_CM, sparse=None):
+    """trace_beam from assembled operators: gmats / s_min keyed by material.
+
+    sparse: keep the (cell x group) table on the cells the rays touched only
+    (UncollidedFlux.cells); None = when the dense table would exceed 2 GB."""
     shape, spacing, origin = _grid_params(grid)
     d = np.asarray(beam.direction, dtype=float)
     e1, e2 = transverse_frame(d)
@@ -371,24 +387,42 @@ def trace_beam_ops(beam, grid, space, key_of_cell, gmats, s_min, n_side=21, span
     av, res, _ = plan.run(space, gmats, s_min, psi0)
     sp = EnergySpace.of(space)
     n = shape[0] * shape[1] * shape[2]
-    values = np.zeros((n, sp.n_groups))
-    residual = np.zeros(n)
-    h = handle_for(shape, spacing, 1)
+    if sparse is None:
+        sparse = n * sp.n_groups * 8 > SPARSE_BYTES
     volume = spacing[0] * spacing[1] * spacing[2]
+    dep_cells = np.asarray(r_cells, dtype=np.int64)
+    cells_u = None
+    if sparse:
+        # deposit into the footprint's rows: the same per-cell accumulation order
+        cells_u = np.unique(dep_cells)
+        dep_cells = np.searchsorted(cells_u, dep_cells).astype(np.int64)
+        rows = max(len(cells_u), 1)
+        h = handle_for((rows, 1, 1), (1.0, 1.0, 1.0), 1)
+    else:
+        rows = n
+        h = handle_for(shape, spacing, 1)
+    values = np.zeros((rows, sp.n_groups))
+    residual = np.zeros(rows)
     h.call("pnd_deposit", sp.n_groups, len(ray_march), _lib.ptr(_lib.i32(ray_seg_off)),
-           _lib.ptr(np.asarray(r_cells, dtype=np.int64)), _lib.ptr(_lib.f64(r_len)),
+           _lib.ptr(dep_cells), _lib.ptr(_lib.f64(r_len)),
            _lib.ptr(_lib.i32(ray_march)), _lib.ptr(_lib.i32(plan.seg_off)),
            _lib.ptr(_lib.f64(ray_w)), float(volume), len(plan.seg_key), _lib.ptr(av),
            _lib.ptr(res), _lib.ptr(values), _lib.ptr(residual))
+    if sparse:
+        k = len(cells_u)
+        return UncollidedFlux(beam=beam, space=space, values=values[:k],
+                              residual_energy=residual[:k], n_rays=n_alive,
+                              cells=cells_u.astype(np.int32), n_cells=n)
     return UncollidedFlux(beam=beam, space=space, values=values, residual_energy=residual,
                           n_rays=n_alive)
 
 
 def trace_beam(beam, grid, space, material_key_of_cell, coefficients, n_side=21,
-               span_sigmas=3.0, max_step=MAX_STEP_CM, spectra_dump=None):
+               span_sigmas=3.0, max_step=MAX_STEP_CM, spectra_dump=None, sparse=None):
     """Drop-in for raytracer.trace_beam (raytracer.py:452-529): stratified
     bundle, device traversal, one device march per distinct ray signature,
-    device deposit in ray order."""
+    device deposit in ray order. Tables above 2 GB are returned on the rays'
+    footprint (UncollidedFlux.cells; trace_beam_ops)."""
     if spectra_dump is not None:
         raise ConfigError("spectra_dump is served by the reference tracer (solver dlra-cpu)")
     keys = sorted(int(k) for k in np.unique(np.asarray(material_key_of_cell)))
@@ -397,4 +431,4 @@ def trace_beam(beam, grid, space, material_key_of_cell, coefficients, n_side=21,
         gm[k] = assemble_energy_operators(space, *coefficients[k])[1]
         smin[k] = float(np.atleast_1d(coefficients[k][0](np.array([space.e_min])))[0])
     return trace_beam_ops(beam, grid, space, material_key_of_cell, gm, smin, n_side,
-                          span_sigmas, max_step)
+                          span_sigmas, max_step, sparse)

@@ -529,3 +529,30 @@ def test_augmentation_drops_rounding_noise():
     h.call("pnd_augment_basis", _lib.ptr(np.ascontiguousarray(u)), a,
            _lib.ptr(np.ascontiguousarray(x)), b, 0, _lib.ptr(q), _lib.ptr(k))
     assert int(k[0]) == 3
+
+
+@pytest.mark.parametrize("shape", [(7, 6, 9), (3, 4, 5), (1, 6, 7), (1, 1, 12), (5, 3, 1),
+                                   (10, 9, 11)])
+def test_stencil_grams_uniform_s_transpose(dl, shape):
+    """One material class (1/S the same in every cell): the device forms only
+    the D+ stencil Grams and takes D- = -(D+)^T + the boundary rows
+    (stencil.cu minus_from_plus); every stencil Gram must still equal the
+    oracle's X^T D_s S^-1 Y (T1), on grids with 3- and 4-cell axes, 2-D and 1-D."""
+    from oracle import dlra_np
+    from paper_2508_04484_b200.angular import PNOperators
+
+    ops = PNOperators.build(3)
+    nx, ny, nz = shape
+    n = nx * ny * nz
+    rng = np.random.default_rng(n)
+    grid = dlra_np.Grid(nx, ny, nz, 0.1, 0.12, 0.09)
+    inv_s = np.full(n, 1.0 / 7.3)
+    ctx = dl.StreamingContext(inv_s, SimpleNamespace(grid=SimpleNamespace(
+        nx=nx, ny=ny, nz=nz, dx=0.1, dy=0.12, dz=0.09)), ops)
+    for a, b in ((5, 7), (12, 20)):
+        x = rng.standard_normal((n, a))
+        y = rng.standard_normal((n, b))
+        got = ctx.stencil_grams(x, y)
+        for i, (axis, sign) in enumerate(grid.stencils()):
+            ref = x.T @ dlra_np.stencil(grid, axis, sign, inv_s[:, None] * y)
+            assert relmax(got[i], ref) < 1e-12, (i, relmax(got[i], ref))

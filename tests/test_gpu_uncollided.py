@@ -84,3 +84,51 @@ def test_trace40_matches_reference(tag):
     T = trace_bench.load()
     fluxes = trace_bench.trace_case(T, tag, rt)
     assert trace_bench.check(T, tag, fluxes) < 1e-10
+
+
+def test_trace_footprint_table_matches_dense():
+    """trace_beam_ops(sparse=True) keeps the table on the rays' footprint: its
+    rows equal the dense table's there (same per-cell deposit order, bit for
+    bit) and the dense table is zero elsewhere; a device run from the sparse
+    tables gives the dense run's dose bit for bit."""
+    import dataclasses
+
+    from conftest import GOLDEN
+    from paper_2508_04484_b200 import raytracer as rt
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle, UncollidedSlices
+
+    T = golden("trace.npz")
+    p = "b1_"
+    sp = T[p + "space"]
+    space = rt.EnergySpace(float(sp[0]), float(sp[1]), int(sp[2]), int(sp[3]))
+    gr = T[p + "grid"]
+    grid = SimpleNamespace(nx=int(gr[0]), ny=int(gr[1]), nz=int(gr[2]), dx=gr[3], dy=gr[4],
+                           dz=gr[5], origin=tuple(gr[6:9]))
+    b = T[p + "beam"]
+    beam = SimpleNamespace(direction=tuple(b[:3]), energy_mev=b[3], position_cm=tuple(b[4:7]),
+                           weight=b[7], sigma_xy_cm=b[8], sigma_e_mev=b[9])
+    keys = [int(k) for k in T[p + "key_list"]]
+    gm = {k: T[p + f"g_{k}"] for k in keys}
+    smin = {k: float(T[p + f"smin_{k}"]) for k in keys}
+    rays = T[p + "rays"]
+    args = (beam, grid, space, T[p + "keys"], gm, smin, int(rays[0]), float(rays[1]),
+            float(rays[2]))
+    dense = rt.trace_beam_ops(*args, sparse=False)
+    sparse = rt.trace_beam_ops(*args, sparse=True)
+    assert sparse.cells is not None and len(sparse.cells) < dense.values.shape[0]
+    np.testing.assert_array_equal(sparse.values, dense.values[sparse.cells])
+    np.testing.assert_array_equal(sparse.residual_energy, dense.residual_energy[sparse.cells])
+    mask = np.ones(dense.values.shape[0], bool)
+    mask[sparse.cells] = False
+    assert not dense.values[mask].any()
+    # device runs from dense vs footprint tables
+    bb = ProblemBundle.load(GOLDEN / "bundle_hetero.npz")
+    fl = []
+    for f in bb.fluxes:
+        cells = np.flatnonzero(np.any(f.values != 0.0, axis=1) | (f.residual != 0.0))
+        fl.append(UncollidedSlices(f.values[cells], f.residual[cells], f.e_min, f.e_max,
+                                   cells.astype(np.int32), bb.n_cells))
+    r_dense = run_bundle(bb, max_steps=25)
+    r_sparse = run_bundle(dataclasses.replace(bb, fluxes=fl), max_steps=25)
+    assert r_sparse.dose.deposited.tobytes() == r_dense.dose.deposited.tobytes()

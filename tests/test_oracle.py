@@ -249,3 +249,25 @@ def test_energy_operators_and_ray_bundle_match_reference():
         np.testing.assert_array_equal(off, T[p + "offsets"])
         np.testing.assert_array_equal(wts, T[p + "weights"])
         np.testing.assert_array_equal(np.stack(rt.transverse_frame(beam[:3])), T[p + "frame"])
+
+
+def test_footprint_flux_equals_dense():
+    """The ray-footprint (sparse) form of an uncollided table (UncollidedSlices
+    with cells): at_energy and the group-sum tally equal the dense table's
+    bit for bit (the cells outside the footprint hold zeros)."""
+    import dataclasses
+
+    from paper_2508_04484_b200.problem import ProblemBundle, UncollidedSlices
+
+    b = ProblemBundle.load(GOLDEN / "bundle_hetero.npz")
+    sparse = []
+    for f in b.fluxes:
+        cells = np.flatnonzero(np.any(f.values != 0.0, axis=1) | (f.residual != 0.0))
+        sparse.append(UncollidedSlices(f.values[cells], f.residual[cells], f.e_min, f.e_max,
+                                       cells.astype(np.int32), b.n_cells))
+        assert len(cells) < b.n_cells
+    bs = dataclasses.replace(b, fluxes=sparse)
+    for e in (1.0, 5.3, 12.77, 22.0, 25.9, 30.0):
+        np.testing.assert_array_equal(bs.psi_at(e), b.psi_at(e))
+    np.testing.assert_array_equal(bs.uncollided_dose(), b.uncollided_dose())
+    np.testing.assert_array_equal(sparse[0].dense().values, b.fluxes[0].values)
