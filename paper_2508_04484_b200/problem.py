@@ -261,8 +261,9 @@ class ProblemBundle:
         deposited = np.zeros(self.n_cells)
         for flux in self.fluxes:
             rows = slice(None) if flux.cells is None else flux.cells
+            cls = self.cell_class[rows]  # S(E_g) per cell = the class value, gathered
             for g, e_g in enumerate(flux.centers):
-                deposited[rows] += self.stopping_field(e_g)[rows] * flux.values[:, g] * flux.width
+                deposited[rows] += self.class_stopping(e_g)[cls] * flux.values[:, g] * flux.width
             deposited[rows] += flux.residual
         return deposited
 
