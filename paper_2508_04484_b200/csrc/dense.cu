@@ -732,8 +732,11 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
     if (sm + 1024 <= (size_t)kMaxDynSmem) {
+      // a block of 4 warps for the small m-side factors (its barriers are the
+      // cost at 64 rows), 16 warps from a few hundred rows
+      const int thr = rows <= 128 ? 128 : 512;
       set_smem((const void*)qr_small_kernel, sm);
-      qr_small_kernel<<<1, 512, sm, st>>>(a, rows, cols, lda, q, ldq, rfac, nullptr);
+      qr_small_kernel<<<1, thr, sm, st>>>(a, rows, cols, lda, q, ldq, rfac, nullptr);
       launched();
       return kc;
     }
