@@ -274,10 +274,34 @@ __device__ __forceinline__ void pipe_init(PipeBars* pb, int nstg, int conw) {
 // all NT n-tiles, k-steps dealt round-robin to four accumulator sets (4 NT
 // independent DMMA chains); B fragments come from a shared-memory copy of
 // Bcat in fragment order.
-template <int NA, int RB, bool PRE, int KC>
-__global__ void __launch_bounds__(PTH, 1)
+// KHR > 0: the register-rebalanced variant. The CTA has 20 warps = 5
+// warpgroups (formers, formers, contraction, contraction, producer + 3 idle
+// warps); `setmaxnreg` moves registers from the producer and former
+// warpgroups to the contraction ones, which then hold their k-half of the B
+// fragments ([M; S0] is the same for every chunk) in registers for the whole
+// kernel: per chunk a contraction warp loads only its KHR A fragments instead
+// of KHR (1 + NT) fragments -- the B stream was the largest shared-memory
+// stream of the kernel.
+// setmaxnreg moves registers within the CTA's launch allocation (96 per
+// thread x 640 = 61,440): 2 x 128 x 80 + 2 x 128 x 144 + 128 x 24 = 60,416
+constexpr int RPTH = 32 * 20;
+constexpr int REG_FORM = 80, REG_CON = 144, REG_PROD = 24;
+static_assert(2 * 128 * REG_FORM + 2 * 128 * REG_CON + 128 * REG_PROD <= RPTH * 96,
+              "register budget exceeds the CTA's launch allocation");
+template <int N>
+__device__ __forceinline__ void reg_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(N));
+}
+
+template <int NA, int RB, bool PRE, int KC, int KHR = 0>
+__global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
     kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
                   int K4, Seg S, int nstg, const double* __restrict__ isp, int oscale) {
+  constexpr int NTH = KHR > 0 ? RPTH : PTH;
   constexpr int NS = 2 * NA;
   constexpr int NT = RB / 8;
   constexpr int KCS = pad4(KC);       // feature tile row length (k-major: k = feature)
@@ -295,11 +319,11 @@ __global__ void __launch_bounds__(PTH, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xc = X.cols, ra = U0.p ? U0.cols : 0;
   pipe_init(pb, nstg, CONW);
-  for (int i = tid; i < (K4 - K) * KCS; i += PTH) {
+  for (int i = tid; i < (K4 - K) * KCS; i += NTH) {
     F0[K * KCS + i] = 0.0;
     F0[K4 * KCS + K * KCS + i] = 0.0;
   }
-  for (int i = tid; i < K4 * RB; i += PTH) {
+  for (int i = tid; i < K4 * RB; i += NTH) {
     const int l = i & 31, f = i >> 5, ks = f / NT, nt = f - ks * NT;
     sB[i] = Bcat[(4 * ks + (l & 3)) * RB + 8 * nt + (l >> 2)];
   }
@@ -307,8 +331,9 @@ __global__ void __launch_bounds__(PTH, 1)
   const bool sepc = S.coff >= 0;
   const int nchunks = (g.n + KC - 1) / KC;
 
-  if (warp == FORMW + CONW) {
-    if (lane == 0) {
+  if (warp >= FORMW + CONW) {
+    if constexpr (KHR > 0) reg_dec<REG_PROD>();
+    if (warp == FORMW + CONW && lane == 0) {
       Ring r(nstg);
       for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next()) {
         if (r.k) mbar_wait(&pb->sempty[r.s], (r.k - 1) & 1);
@@ -317,6 +342,7 @@ __global__ void __launch_bounds__(PTH, 1)
       }
     }
   } else if (warp < FORMW) {
+    if constexpr (KHR > 0) reg_dec<REG_FORM>();
     // lane = (cell 4 (w % CG) + (lane & 3), column (lane >> 2) + 8 (w / CG) + JS t)
     const int ci = 4 * (warp % CG) + (lane & 3), cj = (lane >> 2) + 8 * (warp / CG);
     Ring r(nstg);
@@ -362,10 +388,19 @@ __global__ void __launch_bounds__(PTH, 1)
     // contraction warp q: m-tile q % MT, k-part q / MT (two warps per SM
     // sub-partition, so one issues DMMAs while the other waits on its loads);
     // the k-parts' partials go through the consumed feature buffer
+    if constexpr (KHR > 0) reg_inc<REG_CON>();
     const int q = warp - FORMW, mt = q % MT, kh = q / MT;
     const int nks = K4 / 4;
     const int ks0 = (nks * kh) / KSPLIT, ks1 = (nks * (kh + 1)) / KSPLIT;
     const double* pb0 = sB + lane;
+    constexpr int KHA = KHR > 0 ? KHR : 1;
+    double breg[KHA][NT];
+    if constexpr (KHR > 0) {
+#pragma unroll
+      for (int i = 0; i < KHR; ++i)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) breg[i][nt] = pb0[((ks0 + i) * NT + nt) * 32];
+    }
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
       const int b = it & 1, u = it >> 1;
@@ -379,6 +414,17 @@ __global__ void __launch_bounds__(PTH, 1)
       double* Fb = F0 + b * K4 * KCS;
       const double* pa = Fb + (lane & 3) * KCS + mt * 8 + (lane >> 2);
       int ks = ks0;
+      if constexpr (KHR > 0) {
+        const double* pak = pa + ks0 * 4 * KCS;
+#pragma unroll
+        for (int i = 0; i < KHR; ++i) {
+          const double a0 = pak[i * 4 * KCS];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+            dmma884(acc[i & 1][nt][0], acc[i & 1][nt][1], a0, breg[i][nt]);
+        }
+        ks = ks1;
+      }
 #pragma unroll 2
       for (; ks + 1 < ks1; ks += 2) {
         double av[2], bv[2][NT];
@@ -465,7 +511,7 @@ __global__ void bcat_kernel(const double* M, int kM, int xc, StScale sc, const d
   }
 }
 
-template <int NA, int RB, bool PRE, int KC>
+template <int NA, int RB, bool PRE, int KC, int KHR = 0>
 bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_t st) {
   const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
@@ -476,12 +522,13 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) return false;
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
-  allow_max_smem(kstage_kernel<NA, RB, PRE, KC>);
+  constexpr int nth = KHR > 0 ? RPTH : PTH;
+  allow_max_smem(kstage_kernel<NA, RB, PRE, KC, KHR>);
   const int nchunks = (g.n + KC - 1) / KC;
-  int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC>, PTH, smem);
+  int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem);
   if (grid > nchunks) grid = nchunks;
-  kstage_kernel<NA, RB, PRE, KC><<<grid, PTH, smem, st>>>(g, a.X, a.U0, a.out, B, K, K4, S,
-                                                           nstg, a.inv_s, a.out_scaled ? 1 : 0);
+  kstage_kernel<NA, RB, PRE, KC, KHR><<<grid, nth, smem, st>>>(
+      g, a.X, a.U0, a.out, B, K, K4, S, nstg, a.inv_s, a.out_scaled ? 1 : 0);
   launched();
   return true;
 }
@@ -497,7 +544,13 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   bcat_kernel<<<16, 256, 0, st>>>(a.M, 2 * NA * a.X.cols, a.X.cols, stencil_scale(a.geo), a.S0,
                                   ra, a.out.cols, K4, RB, B);
   launched();
-  // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks)
+  // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks);
+  // the register-rebalanced variant for the bench's 3-D r = 20 tiles
+  if (NA == 3 && RB == 24 && !getenv("PND_KSTAGE_SMEM_B")) {
+    const int khr = K4 / 8;  // k-steps per contraction k-half (KC = 32: 4 m-tiles x 2)
+    if (khr == 18 && kstage_try<NA, RB, PRE, 32, 18>(a, B, K, K4, st)) return;
+    if (khr == 16 && kstage_try<NA, RB, PRE, 32, 16>(a, B, K, K4, st)) return;
+  }
   if (kstage_try<NA, RB, PRE, 32>(a, B, K, K4, st)) return;
   if (kstage_try<NA, RB, PRE, 16>(a, B, K, K4, st)) return;
   fail(PND_ECONFIG, "kstage tile exceeds shared memory");

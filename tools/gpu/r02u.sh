@@ -1,0 +1,5 @@
+export PND_PARITY_OUT=gpurun_out/parity_r02.json
+timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -30 > gpurun_out/r02u_pytest_all.txt
+timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-config1 > gpurun_out/r02u_bench.json 2> gpurun_out/r02u_bench.err
+PND_KSTAGE_SMEM_B=1 timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-config1 > gpurun_out/r02u_bench_smemB.json 2> gpurun_out/r02u_bench_smemB.err
+timeout 120 python tools/config1_profile.py 200 > gpurun_out/r02u_config1.txt 2>&1
