@@ -377,17 +377,48 @@ def config1_dose_time(with_cpu):
     energy steps, one beam): the whole energy loop + dose tally through the
     public API, from the exported problem (assembly and ray tracing are the
     reference's host code and are not part of this path)."""
+    import dataclasses
+    from types import SimpleNamespace
+
+    from paper_2508_04484_b200 import raytracer as rt
     from paper_2508_04484_b200.driver import run_bundle
-    from paper_2508_04484_b200.problem import ProblemBundle
+    from paper_2508_04484_b200.problem import ProblemBundle, UncollidedSlices
 
     b = ProblemBundle.load(ROOT / "tests" / "golden" / "bundle_config1.npz")
     run_bundle(b, max_steps=5)  # warm the kernels / allocations
+    # the beam's uncollided flux traced on the device (441 rays, the reference's
+    # water operator for this 90 MeV energy space), checked against the
+    # reference-traced table of the bundle
+    W = np.load(ROOT / "tests" / "golden" / "water_ops90.npz")
+    sp = W["space"]
+    space = rt.EnergySpace(float(sp[0]), float(sp[1]), int(sp[2]), int(sp[3]))
+    nx, ny, nz = b.shape
+    grid = SimpleNamespace(nx=nx, ny=ny, nz=nz, dx=b.spacing[0], dy=b.spacing[1],
+                           dz=b.spacing[2], origin=tuple(b.origin))
+    beam = SimpleNamespace(direction=(0.0, 0.0, 1.0), energy_mev=90.0,
+                           position_cm=(1.0, 1.0, 0.0), weight=1.0, sigma_xy_cm=0.3,
+                           sigma_e_mev=0.9)
+    keys = np.zeros(b.n_cells, dtype=np.int32)
+    args = (beam, grid, space, keys, {0: W["g"]}, {0: float(W["smin"])}, 21, 3.0, 0.01)
+    rt.trace_beam_ops(*args)  # warm-up
     t0 = time.perf_counter()
-    res = run_bundle(b)
+    flux = rt.trace_beam_ops(*args)
+    t_trace = time.perf_counter() - t0
+    ref_vals = b.fluxes[0].values
+    trace_dev = float(np.abs(flux.values - ref_vals).max() / np.abs(ref_vals).max())
+    b = dataclasses.replace(b, fluxes=[UncollidedSlices(flux.values, flux.residual_energy,
+                                                        space.e_min, space.e_max)])
+    t0 = time.perf_counter()
+    res = run_bundle(b)  # the energy loop + the uncollided group-sum tally
     t_gpu = time.perf_counter() - t0
     steps = len(res.rank_history)
-    out = {"workload": "config 1: 1 x 40 x 35 water, P7 (m=64), fixed rank 20, 573 steps, 1 beam",
-           "gpu_s": t_gpu, "gpu_steps_per_s": steps / t_gpu, "steps": steps}
+    out = {"workload": "config 1: 1 x 20 x 70 water (2 cm x 1 mm), P7 (m=64), fixed rank 20, 573 steps, 1 beam",
+           "gpu_s": t_trace + t_gpu, "trace_s": t_trace, "loop_and_tally_s": t_gpu,
+           "trace_max_rel_dev_vs_reference": trace_dev,
+           "gpu_steps_per_s": steps / t_gpu, "steps": steps,
+           "assembly": "problem assembly is the reference's host code (unchanged; 1.0 s on the "
+                       "build host, SURVEY.md §6.2) -- not on the device path, not timed here",
+           "reference_per_beam_s": 21.6}
     if with_cpu:
         env = dict(os.environ)
         res_cpu = subprocess.run(

@@ -132,3 +132,28 @@ def test_trace_footprint_table_matches_dense():
     r_dense = run_bundle(bb, max_steps=25)
     r_sparse = run_bundle(dataclasses.replace(bb, fluxes=fl), max_steps=25)
     assert r_sparse.dose.deposited.tobytes() == r_dense.dose.deposited.tobytes()
+
+
+def test_config1_beam_traced_matches_reference_table():
+    """BASELINE configs[0]'s beam (90 MeV +z, 441 rays, 1 x 20 x 70 at 2 cm x
+    1 mm) traced on the device with the reference's water operator for that
+    energy space (water_ops90.npz) reproduces the reference-traced table the
+    config-1 bundle carries (trace_all_beams output, bundle_config1.npz)."""
+    from conftest import GOLDEN
+    from paper_2508_04484_b200 import raytracer as rt
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_config1.npz")
+    W = golden("water_ops90.npz")
+    sp = W["space"]
+    space = rt.EnergySpace(float(sp[0]), float(sp[1]), int(sp[2]), int(sp[3]))
+    nx, ny, nz = b.shape
+    grid = SimpleNamespace(nx=nx, ny=ny, nz=nz, dx=b.spacing[0], dy=b.spacing[1],
+                           dz=b.spacing[2], origin=tuple(b.origin))
+    beam = SimpleNamespace(direction=(0.0, 0.0, 1.0), energy_mev=90.0,
+                           position_cm=(1.0, 1.0, 0.0), weight=1.0, sigma_xy_cm=0.3,
+                           sigma_e_mev=0.9)
+    flux = rt.trace_beam_ops(beam, grid, space, np.zeros(b.n_cells, dtype=np.int32),
+                             {0: W["g"]}, {0: float(W["smin"])}, 21, 3.0, 0.01)
+    assert relmax(flux.values, b.fluxes[0].values) < 1e-10
+    assert relmax(flux.residual_energy, b.fluxes[0].residual) < 1e-10
