@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Dense small / m-side linear algebra on the device, so no step leaves the GPU.
 //
 //   gemm        strided batched FP64 GEMM for the m-side factors

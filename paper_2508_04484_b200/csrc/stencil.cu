@@ -546,7 +546,7 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   launched();
   // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks);
   // the register-rebalanced variant for the bench's 3-D r = 20 tiles
-  if (NA == 3 && RB == 24 && !getenv("PND_KSTAGE_SMEM_B")) {
+  if (NA == 3 && RB == 24 && getenv("PND_KSTAGE_REG_B")) {  // measured: no gain
     const int khr = K4 / 8;  // k-steps per contraction k-half (KC = 32: 4 m-tiles x 2)
     if (khr == 18 && kstage_try<NA, RB, PRE, 32, 18>(a, B, K, K4, st)) return;
     if (khr == 16 && kstage_try<NA, RB, PRE, 32, 16>(a, B, K, K4, st)) return;
