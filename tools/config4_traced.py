@@ -51,7 +51,7 @@ def main():
     grid = SimpleNamespace(nx=nside, ny=nside, nz=nside, dx=h, dy=h, dz=h,
                            origin=(0.0, 0.0, 0.0))
     keys = np.zeros(b.n_cells, dtype=np.int32)
-    gm, smin = {0: W["g"]}, {0: float(W["smin"])}
+    gm, smin = {0: W["g_fp19"]}, {0: float(W["smin_fp19"])}  # P19 Fokker-Planck water
     fluxes, t_ms, traces = [], [], []
     rt.trace_beam_ops(SimpleNamespace(direction=(0.0, 0.0, 1.0), energy_mev=90.0,
                                       position_cm=(L / 2, L / 2, -0.5), weight=1.0,

@@ -754,32 +754,37 @@ def make_trace40():
 
 def make_water_ops90():
     """The reference's CN energy operator for water on the energy space of a
-    90 MeV beam (e_max = 94.5 MeV, 128 groups, P2 DG) and its s*(e_min): the
-    inputs of the device tracer for SURVEY.md §8(d) config 4's beams
-    (tools/config4_traced.py traces them at 256^3 on the GPU box)."""
-    raw = trace40_raw((0.0,))
-    raw["grid"] = {"nx": 6, "ny": 6, "nz": 6, "delta_x_cm": 0.1, "delta_y_cm": 0.1,
-                   "delta_z_cm": 0.1}
-    raw["beams"][0].update({"energy_mev": 90.0, "position_cm": [0.3, 0.3, -1.0],
-                            "direction": [0.0, 0.0, 1.0]})
-    config = driver.ProblemConfig.from_dict(raw)
-    problem = driver.assemble_problem(config)
+    90 MeV beam (e_max = 94.5 MeV, 128 groups, P2 DG) and its s*(e_min), for
+    the physics it depends on (sigma_t carries the transport correction of the
+    P_N order and model): keys g / smin -- P7 Boltzmann (BASELINE configs[0],
+    the config-1 beam traced in bench.py); g_fp19 / smin_fp19 -- P19
+    Fokker-Planck (tools/config4_traced.py)."""
     got = {}
-    orig = driver.trace_beam
+    for tag, model, pn in (("", "boltzmann", 7), ("_fp19", "fokker-planck", 19)):
+        raw = trace40_raw((0.0,))
+        raw["grid"] = {"nx": 6, "ny": 6, "nz": 6, "delta_x_cm": 0.1, "delta_y_cm": 0.1,
+                       "delta_z_cm": 0.1}
+        raw["beams"][0].update({"energy_mev": 90.0, "position_cm": [0.3, 0.3, -1.0],
+                                "direction": [0.0, 0.0, 1.0]})
+        raw["model"], raw["pn_order"] = model, pn
+        config = driver.ProblemConfig.from_dict(raw)
+        problem = driver.assemble_problem(config)
+        orig = driver.trace_beam
 
-    def spy(beam, grid, space, keys, coefficients, **kw):
-        mass, g = raytracer.assemble_energy_operators(space, *coefficients[0])
-        got.update(g=g, mass=mass, space=np.array([space.e_min, space.e_max, space.n_groups,
-                                                   space.degree]),
-                   smin=np.array(float(np.atleast_1d(
-                       coefficients[0][0](np.array([space.e_min])))[0])))
-        return orig(beam, grid, space, keys, coefficients, **kw)
+        def spy(beam, grid, space, keys, coefficients, **kw):
+            mass, g = raytracer.assemble_energy_operators(space, *coefficients[0])
+            got.update({"g" + tag: g, "mass": mass,
+                        "space": np.array([space.e_min, space.e_max, space.n_groups,
+                                           space.degree]),
+                        "smin" + tag: np.array(float(np.atleast_1d(
+                            coefficients[0][0](np.array([space.e_min])))[0]))})
+            return orig(beam, grid, space, keys, coefficients, **kw)
 
-    driver.trace_beam = spy
-    try:
-        driver.trace_all_beams(problem)
-    finally:
-        driver.trace_beam = orig
+        driver.trace_beam = spy
+        try:
+            driver.trace_all_beams(problem)
+        finally:
+            driver.trace_beam = orig
     save("water_ops90.npz", **got)
 
 
