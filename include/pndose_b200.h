@@ -96,6 +96,18 @@ int pnd_coefficients_at(pnd_handle* h, double e_mid, double e_lo, int want_lo);
 int pnd_get_coefficients(pnd_handle* h, double* class_s, double* g_diags, double* sigma_t,
                          double* psi, double* psi_lo);
 
+/* Per-element Legendre moments of the screened elastic kernel on an energy
+ * grid -- MomentTables (driver.py:269-307) via legendre_moments
+ * (physics/moliere.py:111-147): the de-peaked Gauss-Legendre quadrature with
+ * nn and 2 nn nodes per piece (x1/w1, x2/w2: numpy leggauss nodes) and the
+ * doubled-node convergence test (rtol; NumericalError "did not converge").
+ * z, a: atomic and mass numbers of the n_el elements; g is n_el x n_e x
+ * (max_degree + 1), xi1 n_el x n_e, both per atom [cm^2], the 2 nn results. */
+int pnd_moment_tables(pnd_handle* h, int n_e, const double* energies, int n_el,
+                      const int32_t* z, const int32_t* a, int nn, const double* x1,
+                      const double* w1, const double* x2, const double* w2, int max_degree,
+                      double exponent, double rtol, double* g, double* xi1);
+
 /* ---- full-rank oracle on the device (fullrank.py:16-45) --
  * The dense n x m moment matrix (u, row-major on the host) kept on the GPU in
  * 32-column blocks; the streaming step is RK4 on apply_streaming (the K-stage

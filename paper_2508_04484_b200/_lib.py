@@ -35,6 +35,7 @@ SIGNATURES = {
     "pnd_set_flux_table": [_P, _I, _I, _I, _P, _P],
     "pnd_select_flux": [_P, _I, _P, _P, _P, _P],
     "pnd_set_flux_table_sparse": [_P, _I, _I, _I, _I, _P, _P, _P],
+    "pnd_moment_tables": [_P, _I, _P, _I, _P, _P, _I, _P, _P, _P, _P, _I, _D, _D, _P, _P],
     "pnd_state_set": [_P, _I, _I, _P, _P, _P],
     "pnd_state_shape": [_P, _P, _P],
     "pnd_state_get": [_P, _P, _P, _P],

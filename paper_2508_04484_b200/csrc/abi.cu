@@ -452,6 +452,24 @@ int pnd_set_flux_table_sparse(pnd_handle* hh, int beam, int n_beams, int n_group
   });
 }
 
+int pnd_moment_tables(pnd_handle* hh, int n_e, const double* energies, int n_el,
+                      const int32_t* z, const int32_t* a, int nn, const double* x1,
+                      const double* w1, const double* x2, const double* w2, int max_degree,
+                      double exponent, double rtol, double* g, double* xi1) {
+  return guard(hh, [&](Handle& h) {
+    if (n_e < 1 || n_el < 1 || nn < 1) pnd::fail(PND_ECONFIG, "moment tables: empty grid");
+    const int bad = pnd::moment_tables(energies, n_e, z, a, n_el, x1, w1, x2, w2, nn, max_degree,
+                                       exponent, rtol, g, xi1, h.st);
+    if (bad >= 0) {
+      char msg[160];
+      snprintf(msg, sizeof msg,
+               "moment quadrature for element %d at %g MeV did not converge, tolerance %.3e",
+               bad / n_e, energies[bad % n_e], rtol);
+      pnd::fail(PND_ENUMERICAL, msg);
+    }
+  });
+}
+
 int pnd_set_coefficient_tables(pnd_handle* hh, int k, const double* log_e, const double* log_s,
                                const double* class_density, const double* class_weights, int p,
                                const double* mom_e, int nd, const double* mom_g,

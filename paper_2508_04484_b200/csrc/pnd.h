@@ -281,6 +281,14 @@ void deposit_rays(int n_rays, const int* ray_seg_off, const long long* cells,
                   const double* mres, double* values, int ld, double* residual, int ng,
                   cudaStream_t st);
 
+// per-element Legendre moments of the screened kernel on an energy grid
+// (moments.cu, moliere.py:111-147): g (n_el x n_e x (L+1)), xi1 (n_el x n_e);
+// returns -1, or the first element * n_e + energy whose quadrature failed rtol
+int moment_tables(const double* energies, int n_e, const int* z, const int* a, int n_el,
+                  const double* x1, const double* w1, const double* x2, const double* w2, int nn,
+                  int max_degree, double exponent, double rtol, double* g, double* xi1,
+                  cudaStream_t st);
+
 // ray traversal (trace.cu)
 void traverse(const Geom& g, const double* origin, int n_rays, const double* starts,
               const double* dirs, int* counts, const long long* offsets, long long* cells,

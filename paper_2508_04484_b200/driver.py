@@ -461,8 +461,19 @@ def run_simulation(config, solver: str = "dlra"):
             return ref_driver.run_simulation(config, solver="dlra")
     if solver not in ("dlra", "fullrank"):
         raise ConfigError(f"unknown solver '{solver}'")
+    from .moments import MomentTables as DeviceMomentTables
+
     t_start = time.perf_counter()
-    problem = ref_driver.assemble_problem(config)
+    # problem assembly is the reference's host code, with its moment tables
+    # (driver.py:269-307) evaluated on the device
+    ref_tables = getattr(ref_driver, "MomentTables", None)
+    if ref_tables is not None:
+        ref_driver.MomentTables = DeviceMomentTables
+    try:
+        problem = ref_driver.assemble_problem(config)
+    finally:
+        if ref_tables is not None:
+            ref_driver.MomentTables = ref_tables
     ref_trace = ref_driver.trace_beam
     ref_driver.trace_beam = dev_tracer.trace_beam
     try:

@@ -138,3 +138,32 @@ def test_separable_flux_matches_dense_table():
             np.testing.assert_allclose(got[1][i], want, rtol=1e-15, atol=0)
     for dev in devs:
         dev.close()
+
+
+def test_device_moment_tables_match_reference():
+    """MomentTables on the device (moments.cu; driver.py:269-307 via
+    moliere.py:111-147) against the reference's own tables for 1..105 MeV up
+    to degree 21 (tests/golden/bench_physics.npz, written by the reference)."""
+    import numpy as np
+
+    from conftest import golden
+    from paper_2508_04484_b200.moments import MomentTables
+
+    ph = golden("bench_physics.npz")
+    t = MomentTables(1.0, 105.0, 21, n_points=48, n_nodes=256, exponent=1.0)
+    np.testing.assert_array_equal(t.energies, ph["mom_e"])
+    g, ref = t.g, ph["mom_g"]
+    assert np.abs(g - ref).max() / np.abs(ref).max() < 1e-12
+    for el in range(12):  # every element to its own scale
+        assert np.abs(g[el] - ref[el]).max() <= 1e-12 * np.abs(ref[el]).max()
+    assert np.abs(t.xi1 - ph["mom_xi1"]).max() <= 1e-12 * np.abs(ph["mom_xi1"]).max()
+
+
+def test_device_moment_tables_report_non_convergence():
+    import pytest
+
+    from paper_2508_04484_b200.errors import NumericalError
+    from paper_2508_04484_b200.moments import device_moments
+
+    with pytest.raises(NumericalError, match="did not converge"):
+        device_moments([50.0], 7, n_nodes=4, rtol=1e-12)

@@ -91,3 +91,31 @@ def test_slab_solve_wide_rank():
         assert p.rank_history[-1][2] == 40
     ref = full.dose.deposited
     assert np.linalg.norm(dep - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_slab_solve_blocked_rank_and_footprint_flux():
+    """Ranks above 64 (the column-blocked layout of xwide.cu: per-block halo
+    planes, rectangular S-Gram pairs, Gram allreduces) and ray-footprint
+    uncollided tables restricted to each slab's rows, under a three-slab
+    decomposition, against the undecomposed solve."""
+    import dataclasses
+
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle, UncollidedSlices
+
+    b = ProblemBundle.load(GOLDEN / "bundle_fp19.npz")  # 10 x 10 x 12, m = 400
+    fl = []
+    for f in b.fluxes:
+        cells = np.flatnonzero(np.any(f.values != 0.0, axis=1) | (f.residual != 0.0))
+        fl.append(UncollidedSlices(f.values[cells], f.residual[cells], f.e_min, f.e_max,
+                                   cells.astype(np.int32), b.n_cells))
+    b = dataclasses.replace(b, fluxes=fl, truncation_tolerance=1e300, rank_min=70,
+                            rank_max=70)
+    full = run_bundle(b, max_steps=6)
+    parts = _run_slabs(b, 3, max_steps=6)
+    dep = np.concatenate([p.dose.deposited for p in parts])
+    for p in parts:
+        assert [r for _, _, r in p.rank_history] == [r for _, _, r in full.rank_history]
+        assert p.rank_history[-1][2] == 70
+    ref = full.dose.deposited
+    assert np.linalg.norm(dep - ref) / np.linalg.norm(ref) < 1e-10
