@@ -89,6 +89,23 @@ def flux_matrices(n_max):
     return tuple(out)
 
 
+def _eig_jacobi(a):
+    """Symmetric eigen-decomposition by the device's one-sided Jacobi SVD
+    (pnd_svd_small): A + c I with c = |A|_1 + 1 is SPD, so its singular vectors
+    are A's eigenvectors and sigma - c its eigenvalues (absolute error ~ eps c,
+    as a dense symmetric eigensolver's)."""
+    from . import _lib
+    from .dlra import _generic_handle
+
+    m = a.shape[0]
+    c = float(np.abs(a).sum(axis=0).max()) + 1.0
+    s = _lib.f64(a + c * np.eye(m))
+    p, sig, qt = np.empty((m, m)), np.empty(m), np.empty((m, m))
+    _generic_handle().call("pnd_svd_small", _lib.ptr(s), m, m, _lib.ptr(p), _lib.ptr(sig),
+                           _lib.ptr(qt))
+    return sig - c, p
+
+
 @dataclass(frozen=True)
 class PNOperators:
     """eig_v / lam_plus / lam_minus per axis, as the reference's PNOperators."""
@@ -100,10 +117,12 @@ class PNOperators:
 
     @classmethod
     def build(cls, n_max: int, device=None) -> "PNOperators":
-        """device (e.g. "cuda:0"): the three quadrature Grams and their
-        eigendecompositions run on the GPU (cuBLAS DGEMM, cuSOLVER syevd via
-        torch; SURVEY.md §8(f) row 4 -- the O(m^3) setup that takes seconds on
-        the host at N >= 39); the same arithmetic as the host path."""
+        """device (e.g. "cuda:0"): the three quadrature Grams on the GPU (cuBLAS
+        DGEMM via torch) and their eigendecompositions by the library's own
+        one-CTA Jacobi kernel (m <= 512: the SPD shift A + c I, c >= rho(A),
+        has the eigenvectors of A and sigma = lambda + c; cuSOLVER syevd above
+        that); SURVEY.md §8(f) row 4 -- the O(m^3) setup that takes seconds on
+        the host at N >= 39."""
         if device is not None:
             return cls._build_device(n_max, device)
         vs, lp, lm = [], [], []
@@ -121,16 +140,20 @@ class PNOperators:
         basis, wt, comps = _quadrature(n_max)
         bd = torch.from_numpy(basis).to(device)
         vs, lp, lm = [], [], []
+        m = basis.shape[0]
         for c in comps:
             a = (bd * torch.from_numpy(wt * c).to(device)) @ bd.T
             a = 0.5 * (a + a.T)
             a = torch.where(a.abs() < 1e-15, torch.zeros_like(a), a)
-            lam, v = torch.linalg.eigh(a)
-            vs.append(v.cpu().numpy())
-            lam = lam.cpu().numpy()
+            if m <= 512:
+                lam, v = _eig_jacobi(a.cpu().numpy())
+            else:
+                lam_t, v_t = torch.linalg.eigh(a)
+                lam, v = lam_t.cpu().numpy(), v_t.cpu().numpy()
+            vs.append(v)
             lp.append(np.maximum(lam, 0.0))
             lm.append(np.minimum(lam, 0.0))
-            del a, v
+            del a
         return cls(n_max, tuple(vs), tuple(lp), tuple(lm))
 
     @property
