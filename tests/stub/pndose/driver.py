@@ -140,14 +140,83 @@ class UncollidedFlux:
 
 
 def trace_beam(*args, **kwargs):  # replaced by the device tracer during run_simulation
-    raise AssertionError("the stub never traces; fluxes come from the fixture")
+    raise AssertionError("run_simulation must route trace_beam to the device tracer")
+
+
+# --- the reference's straggling model (physics/stopping.py:123-165), restated
+_E_CHARGE, _EPS0, _ME_KG, _MEV_J, _C = (1.602176634e-19, 8.8541878128e-12, 9.1093837015e-31,
+                                        1.602176634e-13, 2.99792458e8)
+_Z = np.array([1, 6, 7, 8, 11, 12, 15, 16, 17, 18, 19, 20], dtype=float)
+_I_J = np.array([19.2, 78.0, 82.0, 95.0, 149.0, 156.0, 173.0, 180.0, 174.0, 188.0, 190.0,
+                 191.0]) * _E_CHARGE
+_PREF = 4.0 * np.pi * _E_CHARGE ** 4 / (4.0 * np.pi * _EPS0) ** 2
+
+
+def _straggling_t(n_i, e):
+    p = np.sqrt(e * (e + 2.0 * 938.272))
+    v = p / (e + 938.272) * _C
+    me_v2 = _ME_KG * v * v
+    log_arg = 2.0 * me_v2 / _I_J
+    term = np.where(log_arg > 1.0, 4.0 * _I_J / (3.0 * me_v2) * np.log(log_arg), 0.0)
+    return (n_i * 1e6 @ (_PREF * _Z * term)) / _MEV_J ** 2 / 100.0
+
+
+def _straggling_dt(n_i, e, rel_step=1e-4):
+    h = rel_step * max(abs(e), 1.0)
+    return (_straggling_t(n_i, e + h) - _straggling_t(n_i, e - h)) / (2.0 * h)
 
 
 def trace_all_beams(problem):
-    a = np.load(GOLDEN / problem.config.resolved["bundle"], allow_pickle=False)
-    return [UncollidedFlux(space=SimpleNamespace(e_min=float(r[0]), e_max=float(r[1])),
-                           values=v, residual_energy=res, n_rays=441)
-            for v, res, r in zip(a["flux_values"], a["flux_residual"], a["flux_range"])]
+    """driver.py:398-449: one energy-operator closure triple per unique
+    material row, then trace_beam per beam (the device tracer once
+    run_simulation has routed it). The closures restate the reference's
+    (stopping power by Bragg mixing of the log-log element tables, Williams
+    straggling, the corrected total cross section) over the bundle's class
+    tables -- the paper_2508_04484_b200.problem restatements, pinned to the
+    reference's contexts by tests/test_oracle.py."""
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    cfg = problem.config
+    if not cfg.resolved.get("trace"):
+        a = np.load(GOLDEN / cfg.resolved["bundle"], allow_pickle=False)
+        return [UncollidedFlux(space=SimpleNamespace(e_min=float(r[0]), e_max=float(r[1])),
+                               values=v, residual_energy=res, n_rays=441)
+                for v, res, r in zip(a["flux_values"], a["flux_residual"], a["flux_range"])]
+    b = ProblemBundle.load(GOLDEN / cfg.resolved["bundle"])
+    keys = b.cell_class
+    coefficients = {}
+    for key in range(b.n_classes):
+        n_i = b.class_atomic[key]
+
+        def s_star(e, key=key, n_i=n_i):
+            e = np.asarray(e, dtype=float)
+            s = np.array([b.class_stopping(float(x))[key] for x in np.atleast_1d(e).ravel()])
+            dt = np.array([_straggling_dt(n_i, float(x)) for x in np.atleast_1d(e).ravel()])
+            return (s + 0.5 * dt).reshape(np.shape(e))
+
+        def t_coeff(e, n_i=n_i):
+            e = np.asarray(e, dtype=float)
+            return np.array([_straggling_t(n_i, float(x))
+                             for x in np.atleast_1d(e).ravel()]).reshape(np.shape(e))
+
+        def sigma_t_fn(e, n_i=n_i):
+            e = np.asarray(e, dtype=float)
+            return np.array([float(n_i @ b.scattering_tables(float(x))[1])
+                             for x in np.atleast_1d(e).ravel()]).reshape(np.shape(e))
+
+        coefficients[key] = (s_star, t_coeff, sigma_t_fn)
+    t = cfg.resolved["trace"]
+    space = SimpleNamespace(e_min=b.fluxes[0].e_min, e_max=b.fluxes[0].e_max,
+                            n_groups=b.fluxes[0].n_groups, degree=2)
+    out = []
+    for bm in t["beams"]:
+        beam = SimpleNamespace(direction=tuple(bm["direction"]), energy_mev=bm["energy_mev"],
+                               position_cm=tuple(bm["position_cm"]), weight=bm.get("weight", 1.0),
+                               sigma_xy_cm=bm.get("sigma_xy_cm", 0.3),
+                               sigma_e_mev=0.01 * bm["energy_mev"])
+        out.append(trace_beam(beam, problem.grid, space, keys, coefficients,
+                              n_side=t["n_side"], span_sigmas=3.0, max_step=0.01))
+    return out
 
 
 def run_simulation(config, solver="dlra"):

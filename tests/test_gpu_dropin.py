@@ -48,6 +48,53 @@ def _config(tmp_path, name, bundle, transport=None):
     return str(path), out
 
 
+TRACE_CHILD = r'''
+import json, sys
+sys.path[:0] = [sys.argv[1], sys.argv[2]]
+import numpy as np
+import pndose.driver
+from paper_2508_04484_b200 import driver as dev
+dev.install()
+cfg = pndose.driver.ProblemConfig.load(sys.argv[3])
+res = pndose.driver.run_simulation(cfg)
+ref = np.load(sys.argv[4])
+dev_v = max(float(np.abs(f.values - v).max() / np.abs(v).max())
+            for f, v in zip(res.fluxes, ref["flux_values"]))
+np.save(sys.argv[5], res.dose.deposited)
+print("RESULT " + json.dumps({"flux_dev": dev_v, "n_fluxes": len(res.fluxes),
+                              "rays": [f.n_rays for f in res.fluxes]}))
+'''
+
+
+def test_trace_all_beams_coupling_through_device_tracer(tmp_path):
+    """driver.py:398-449 (d5): the per-material closure triples and the
+    per-beam trace_beam calls of trace_all_beams, with trace_beam routed to
+    the device tracer by run_simulation -- the two-beam heterogeneous phantom
+    (three material classes, an axial and an oblique beam): the traced tables
+    equal the reference-traced ones the bundle carries, and the dose the
+    reference's run (T5 floors)."""
+    g = golden("e2e_hetero.npz")
+    path = tmp_path / "hetero.json"
+    path.write_text(json.dumps({
+        "bundle": "bundle_hetero.npz", "output": str(tmp_path / "out"), "name": "hetero",
+        "trace": {"n_side": 5, "beams": [
+            {"direction": [0, 0, 1], "energy_mev": 25.0, "position_cm": [1.0, 1.0, 0.0]},
+            {"direction": [0, 0.6, 0.8], "energy_mev": 22.0, "position_cm": [1.0, 0.3, 0.0],
+             "weight": 0.5}]}}))
+    dose_path = tmp_path / "dose.npy"
+    proc = subprocess.run([sys.executable, "-c", TRACE_CHILD, str(ROOT / "tests" / "stub"),
+                           str(ROOT), str(path), str(GOLDEN / "bundle_hetero.npz"),
+                           str(dose_path)], capture_output=True, text=True, timeout=600)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    res = json.loads([x for x in proc.stdout.splitlines() if x.startswith("RESULT ")][-1][7:])
+    assert res["n_fluxes"] == 2
+    assert res["flux_dev"] < 1e-10, res
+    dep = np.load(dose_path)
+    floors = json.loads((GOLDEN / "floors.json").read_text())["hetero"]
+    assert np.linalg.norm(dep - g["deposited"]) / np.linalg.norm(g["deposited"]) <= \
+        max(10 * floors["total"], 1e-12)
+
+
 def test_run_simulation_dropin_through_reference_cli(tmp_path):
     ok, ok_out = _config(tmp_path, "ok", "bundle_smoke.npz")
     fr, fr_out = _config(tmp_path, "fr", "bundle_smoke.npz")
