@@ -141,9 +141,18 @@ int pnd_truncate(pnd_handle* h, double theta, int rank_min, int rank_max, double
  * out[0..7] = tail after streaming, tail after scattering, rank, defect
  * (defect only when want_defect != 0), the (U, V) ranks entering the
  * streaming substep and entering the scattering substep (the driver's
- * augmented-size diagnostics, driver.py:583-601). */
+ * augmented-size diagnostics, driver.py:583-601).
+ * On small single-device grids (n x rank <= 2^22) with truncation after both
+ * substeps the step runs speculatively: the augmentation and truncation
+ * ranks are predicted on the host (full increments, last step's ranks), the
+ * whole step is launched without a host round trip and the device flags a
+ * wrong prediction; the one synchronisation at the end either accepts the
+ * step or restores the state and recomputes it on the synchronous path, so
+ * the result is the same either way (PND_NO_SPEC=1 disables it). */
 int pnd_step(pnd_handle* h, double dt, double theta, int rank_min, int rank_max,
              int truncate_after, int tally_steps, int want_defect, double* out);
+/* speculative steps accepted / recomputed so far (two long longs) */
+int pnd_spec_stats(pnd_handle* h, long long* hits_misses);
 int pnd_dose_reset(pnd_handle* h);
 int pnd_dose_accumulate(pnd_handle* h, double dt, int tally_steps);
 int pnd_get_dose(pnd_handle* h, double* deposited);

@@ -71,6 +71,7 @@ SIGNATURES = {
     "pnd_event_record": [_P, _I],
     "pnd_event_elapsed": [_P, _I, _I, _P],
     "pnd_launch_count": [_P, _P],
+    "pnd_spec_stats": [_P, _P],
     "pnd_set_flux_separable": [_P, _I, _I, _I, _P, _P, _P],
     "pnd_state_random": [_P, _I, ctypes.c_ulonglong],
     "pnd_march": [_P, _I, _I, _I, _P, _P, _P, _D, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P, _P,

@@ -4,6 +4,10 @@
 // staging, error mapping. Every exception raised inside the library becomes
 // a status code plus a message stored in the handle.
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <unordered_set>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -55,6 +59,30 @@ void IBuf::free_() {
 }
 
 static std::atomic<long long> g_launches{0};  // kernel launches (bench gpu_launches)
+
+bool smem_set_once(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> seen;
+  std::lock_guard<std::mutex> lk(mu);
+  return seen.insert(fn).second;
+}
+
+int occupancy_cached(const void* fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  const auto key = std::make_tuple(fn, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+  if (nb < 1) nb = 1;
+  std::lock_guard<std::mutex> lk(mu);
+  cache[key] = nb;
+  return nb;
+}
 
 void launched() {
   CK(cudaGetLastError());
@@ -622,24 +650,48 @@ int pnd_truncate(pnd_handle* hh, double theta, int rank_min, int rank_max, doubl
 int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max,
              int truncate_after, int tally_steps, int want_defect, double* out) {
   return guard(hh, [&](Handle& h) {
-    double t1 = 0.0, t2 = 0.0;
+    double t1 = 0.0, t2 = 0.0, defect = 0.0;
     int rank = 0;
     const int ru0 = h.ru, rv0 = h.rv;
-    pnd::streaming_step(h, dt);
-    if (truncate_after & 1) pnd::truncate(h, theta, rank_min, rank_max, &t1, &rank);
-    const int ru1 = h.ru, rv1 = h.rv;
-    pnd::scattering_step(h, dt);
-    bool ugram = false;
-    if (truncate_after & 2) {
-      // the last rotation of the step also forms U^T U for the defect diagnostic
-      const int kmax = h.ru < h.rv ? h.ru : h.rv;  // the truncated rank is at most this
-      double* G = want_defect ? pnd::defect_gram_slot(h, kmax, kmax) : nullptr;
-      pnd::truncate(h, theta, rank_min, rank_max, &t2, &rank, G);
-      ugram = want_defect;
+    int ru1 = 0, rv1 = 0;
+    auto body = [&]() {
+      h.spec_tr = 0;
+      pnd::streaming_step(h, dt);
+      if (truncate_after & 1) pnd::truncate(h, theta, rank_min, rank_max, &t1, &rank);
+      ru1 = h.ru;
+      rv1 = h.rv;
+      h.spec_tr = 1;
+      pnd::scattering_step(h, dt);
+      bool ugram = false;
+      if (truncate_after & 2) {
+        // the last rotation of the step also forms U^T U for the defect diagnostic
+        const int kmax = h.ru < h.rv ? h.ru : h.rv;  // the truncated rank is at most this
+        double* G = want_defect ? pnd::defect_gram_slot(h, kmax, kmax) : nullptr;
+        pnd::truncate(h, theta, rank_min, rank_max, &t2, &rank, G);
+        ugram = want_defect;
+      }
+      pnd::dose_accumulate_step(h, dt, tally_steps != 0);
+      if (want_defect) defect = pnd::orth_defect(h, ugram);
+    };
+    if (h.spec_pause > 0) --h.spec_pause;
+    bool done = false;
+    if (pnd::spec_eligible(h, truncate_after)) {
+      // no host round trip inside the step: one synchronisation at its end
+      pnd::spec_begin(h);
+      try {
+        body();
+      } catch (...) {
+        pnd::spec_end(h, true);
+        throw;
+      }
+      done = pnd::spec_end(h, false);
+      if (done) {
+        t1 = h.pinned[20];
+        t2 = h.pinned[21];
+        if (want_defect) defect = h.pinned[22];
+      }
     }
-    pnd::dose_accumulate_step(h, dt, tally_steps != 0);
-    double defect = 0.0;
-    if (want_defect) defect = pnd::orth_defect(h, ugram);
+    if (!done) body();
     if (out) {
       out[0] = t1;
       out[1] = t2;
@@ -650,6 +702,13 @@ int pnd_step(pnd_handle* hh, double dt, double theta, int rank_min, int rank_max
       out[6] = ru1;  // ... and entering the scattering substep
       out[7] = rv1;
     }
+  });
+}
+
+int pnd_spec_stats(pnd_handle* hh, long long* hits_misses) {
+  return guard(hh, [&](Handle& h) {
+    hits_misses[0] = h.spec_hits;
+    hits_misses[1] = h.spec_misses;
   });
 }
 

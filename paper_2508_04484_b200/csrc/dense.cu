@@ -21,9 +21,13 @@
 //   s_rk4       Horner-form RK4 of the precontracted Galerkin S-phase.
 #include <float.h>
 
+#include <cooperative_groups.h>
+
 #include "pnd.h"
 
 namespace pnd {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -392,6 +396,363 @@ __global__ void __launch_bounds__(1024, 1)
   }
 }
 
+// QR-preconditioned one-sided Jacobi for the small truncation SVDs (M <= 64),
+// everything in shared memory. A Pi = Q R by Householder with column pivoting
+// (the hh_qr conventions: beta = -sign(alpha) |x|, tau = 0 for a zero
+// sub-column), then Hestenes Jacobi on X = R^T, whose columns are the rows of
+// R: X Vx = Ux Sigma, so R = Vx Sigma Ux^T and A = (Q Vx) Sigma (Pi Ux)^T.
+// On the graded augmented S^ of the DLRA steps the pivoted triangular factor
+// needs ~5 sweeps where the plain matrix needs 9-16 (its rounding-noise
+// columns converge slowly). Q Vx is formed by applying the reflectors to
+// [Vx; 0] backwards. Exact zero singular values are completed with canonical
+// unit vectors as in svd_kernel (svd(0) = I, I: no pivoting, tau = 0).
+//
+// These matrices are tiny, so the kernel is instruction-bound, not
+// latency-bound (ncu: IPC 2 on the one SM with 20 warps doing redundant
+// scalar work): every Jacobi pair and every column update is handled by a
+// group of 8 lanes (RPL rows per lane), so a round costs 5 warps, not 20.
+constexpr int QJ_G = 8;
+
+// T[:, k0:k1] <- H_j T[:, k0:k1] (column-major, leading dimension M) for the
+// reflector in column j of V (v_j = 1, v_i = V[j M + i] below), one 8-lane
+// group per column
+template <int RPL>
+__device__ __forceinline__ void qj_apply(const double* V, double* T, int M, int j, int k0, int k1,
+                                         double tj) {
+  const int nc = k1 - k0;
+  const int tid = threadIdx.x, grp = tid / QJ_G, l = tid % QJ_G, ngrp = blockDim.x / QJ_G;
+  const int trips = (nc + ngrp - 1) / ngrp;
+  for (int t = 0; t < trips; ++t) {
+    const int c = grp + t * ngrp;
+    const bool act = c < nc;
+    const int k = k0 + (act ? c : 0);
+    double v[RPL], x[RPL];
+    double w = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = j + 1 + l + QJ_G * u;
+      const bool in = act && i < M;
+      v[u] = in ? V[j * M + i] : 0.0;
+      x[u] = in ? T[k * M + i] : 0.0;
+      w = fma(v[u], x[u], w);
+    }
+    const double tjk = act ? T[k * M + j] : 0.0;
+    w += __shfl_xor_sync(0xffffffffu, w, 4);
+    w += __shfl_xor_sync(0xffffffffu, w, 2);
+    w += __shfl_xor_sync(0xffffffffu, w, 1);
+    if (act) {
+      w = tj * (w + tjk);
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = j + 1 + l + QJ_G * u;
+        if (i < M) T[k * M + i] = x[u] - w * v[u];
+      }
+      if (l == 0) T[k * M + j] = tjk - w;
+    }
+  }
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(256, 1)
+    svd_qrj_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
+  extern __shared__ double sm[];
+  const bool tall = p >= q;
+  const int M = tall ? p : q, N = tall ? q : p;
+  const int N2 = N + (N & 1);
+  double* A = sm;                // M x N column-major: R on/above the diagonal, reflectors below
+  double* X = A + M * N;         // N x N2 column-major, X = R^T
+  double* Vm = X + N * N2;       // N2 x N2 column-major
+  double* U = Vm + N2 * N2;      // N x N: normalised X columns in singular value order
+  double* B = U + N * N;         // M x N: Q Vx (sorted)
+  double* tau = B + M * N;       // N
+  double* nrm = tau + N;         // N2
+  double* sg = nrm + N2;         // N2
+  int* perm = (int*)(sg + N2);   // N: column pivots (A Pi)[:, j] = A[:, perm[j]]
+  int* order = perm + N;         // N: singular values, descending
+  __shared__ int rotated;
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  const int grp = tid / QJ_G, l = tid % QJ_G, ngrp = nthr / QJ_G;
+  for (int idx = tid; idx < M * N; idx += nthr) {
+    const int i = idx % M, j = idx / M;
+    A[idx] = tall ? s[i * q + j] : s[j * q + i];
+  }
+  for (int j = tid; j < N; j += nthr) perm[j] = j;
+  __syncthreads();
+  for (int c = warp; c < N; c += nw) {
+    double x = 0.0;
+    for (int i = lane; i < M; i += 32) x += A[c * M + i] * A[c * M + i];
+    x = warp_sum(x);
+    if (lane == 0) nrm[c] = x;
+  }
+  __syncthreads();
+  // ---- Householder QR with column pivoting
+  for (int j = 0; j < N; ++j) {
+    if (warp == 0) {
+      // pivot: the largest trailing column norm, the first on ties
+      double best = -1.0;
+      int bi = j;
+      for (int c = j + lane; c < N; c += 32)
+        if (nrm[c] > best) { best = nrm[c]; bi = c; }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (bi != j) {
+        for (int i = lane; i < M; i += 32) {
+          const double t = A[j * M + i];
+          A[j * M + i] = A[bi * M + i];
+          A[bi * M + i] = t;
+        }
+        if (lane == 0) {
+          const int t = perm[j]; perm[j] = perm[bi]; perm[bi] = t;
+        }
+      }
+      __syncwarp();
+      double x = 0.0;
+      for (int i = j + 1 + lane; i < M; i += 32) x += A[j * M + i] * A[j * M + i];
+      const double xn2 = warp_sum(x);
+      const double alpha = A[j * M + j];
+      double tj = 0.0;
+      if (xn2 > 0.0) {
+        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tj = (beta - alpha) / beta;
+        const double scl = 1.0 / (alpha - beta);
+        for (int i = j + 1 + lane; i < M; i += 32) A[j * M + i] *= scl;
+        __syncwarp();
+        if (lane == 0) A[j * M + j] = beta;
+      }
+      if (lane == 0) tau[j] = tj;
+    }
+    __syncthreads();
+    // apply H_j to the trailing columns (8-lane groups); refresh their norms
+    // over rows > j for the next pivot
+    {
+      const double tj = tau[j];
+      const int nc = N - j - 1;
+      const int trips = (nc + ngrp - 1) / ngrp;
+      for (int t = 0; t < trips; ++t) {
+        const int c = grp + t * ngrp;
+        const bool act = c < nc;
+        const int k = j + 1 + (act ? c : 0);
+        double v[RPL], x[RPL];
+        double w = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int i = j + 1 + l + QJ_G * u;
+          const bool in = act && i < M;
+          v[u] = in ? A[j * M + i] : 0.0;
+          x[u] = in ? A[k * M + i] : 0.0;
+          w = fma(v[u], x[u], w);
+        }
+        const double ajk = act ? A[k * M + j] : 0.0;
+        w += __shfl_xor_sync(0xffffffffu, w, 4);
+        w += __shfl_xor_sync(0xffffffffu, w, 2);
+        w += __shfl_xor_sync(0xffffffffu, w, 1);
+        w = tj * (w + ajk);
+        double nn = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          x[u] -= w * v[u];
+          nn = fma(x[u], x[u], nn);
+        }
+        nn += __shfl_xor_sync(0xffffffffu, nn, 4);
+        nn += __shfl_xor_sync(0xffffffffu, nn, 2);
+        nn += __shfl_xor_sync(0xffffffffu, nn, 1);
+        if (act) {
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            const int i = j + 1 + l + QJ_G * u;
+            if (i < M) A[k * M + i] = x[u];
+          }
+          if (l == 0) {
+            A[k * M + j] = ajk - w;
+            nrm[k] = nn;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // X = R^T (column j of X = row j of R), Vx = I
+  for (int idx = tid; idx < N * N2; idx += nthr) {
+    const int c = idx % N, j = idx / N;
+    X[idx] = (j < N && c >= j) ? A[c * M + j] : 0.0;
+  }
+  for (int idx = tid; idx < N2 * N2; idx += nthr) Vm[idx] = (idx % N2 == idx / N2) ? 1.0 : 0.0;
+  __syncthreads();
+  // ---- Hestenes sweeps on the columns of X (svd_kernel's rotation and stopping
+  // rule), round-robin pairs, one 8-lane group per pair
+  const int npair = N2 / 2;
+  for (int sweep = 0; sweep < 60 && N2 > 1; ++sweep) {
+    for (int t = 0; t < (N2 + ngrp - 1) / ngrp; ++t) {
+      const int j = grp + t * ngrp;
+      double x = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = l + QJ_G * u;
+        const double v = (j < N2 && i < N) ? X[j * N + i] : 0.0;
+        x = fma(v, v, x);
+      }
+      x += __shfl_xor_sync(0xffffffffu, x, 4);
+      x += __shfl_xor_sync(0xffffffffu, x, 2);
+      x += __shfl_xor_sync(0xffffffffu, x, 1);
+      if (l == 0 && j < N2) nrm[j] = x;
+    }
+    if (tid == 0) rotated = 0;
+    __syncthreads();
+    for (int round = 0; round < N2 - 1; ++round) {
+      const int k = grp;
+      if (k < npair || (grp * QJ_G < ((npair * QJ_G + 31) & ~31))) {
+        const bool act = k < npair;
+        int a = 0, b = 1;
+        if (act) {
+          if (k == 0) {
+            a = round;
+            b = N2 - 1;
+          } else {
+            a = round + k;
+            if (a >= N2 - 1) a -= N2 - 1;
+            b = round + N2 - 1 - k;
+            if (b >= N2 - 1) b -= N2 - 1;
+          }
+          if (a > b) { const int t = a; a = b; b = t; }
+        }
+        double x[RPL], y[RPL];
+        double ga = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int i = l + QJ_G * u;
+          const bool in = act && i < N;
+          x[u] = in ? X[a * N + i] : 0.0;
+          y[u] = in ? X[b * N + i] : 0.0;
+          ga = fma(x[u], y[u], ga);
+        }
+        ga += __shfl_xor_sync(0xffffffffu, ga, 4);
+        ga += __shfl_xor_sync(0xffffffffu, ga, 2);
+        ga += __shfl_xor_sync(0xffffffffu, ga, 1);
+        const double al = act ? nrm[a] : 0.0, be = act ? nrm[b] : 0.0;
+        if (act && ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = rsqrt(1.0 + t * t), sn = c * t;
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            const int i = l + QJ_G * u;
+            if (i < N) {
+              X[a * N + i] = c * x[u] - sn * y[u];
+              X[b * N + i] = sn * x[u] + c * y[u];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < RPL; ++u) {
+            const int i = l + QJ_G * u;
+            if (i < N2) {
+              const double vx = Vm[a * N2 + i], vy = Vm[b * N2 + i];
+              Vm[a * N2 + i] = c * vx - sn * vy;
+              Vm[b * N2 + i] = sn * vx + c * vy;
+            }
+          }
+          if (l == 0) {
+            nrm[a] = al - t * ga;
+            nrm[b] = be + t * ga;
+            rotated = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  // singular values and their order (rank by counting: descending, stable)
+  for (int j = warp; j < N; j += nw) {
+    double x = 0.0;
+    for (int i = lane; i < N; i += 32) x += X[j * N + i] * X[j * N + i];
+    x = warp_sum(x);
+    if (lane == 0) sg[j] = sqrt(x);
+  }
+  __syncthreads();
+  for (int j = tid; j < N; j += nthr) {
+    int rk = 0;
+    const double v = sg[j];
+    for (int k = 0; k < N; ++k) rk += (sg[k] > v) || (sg[k] == v && k < j);
+    order[rk] = j;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < N * N; idx += nthr) {
+    const int i = idx % N, j = idx / N;
+    const double sv = sg[order[j]];
+    U[idx] = sv > 0.0 ? X[order[j] * N + i] / sv : 0.0;
+  }
+  __syncthreads();
+  // complete the zero ones with canonical unit vectors (Gram-Schmidt x2)
+  if (warp == 0 && sg[order[N - 1]] == 0.0) {
+    int cand = 0;
+    for (int j = 0; j < N; ++j) {
+      if (sg[order[j]] > 0.0) continue;
+      for (; cand < N; ++cand) {
+        double v0 = lane == cand ? 1.0 : 0.0, v1 = lane + 32 == cand ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int k = 0; k < N; ++k) {
+            if (k == j || (sg[order[k]] == 0.0 && k > j)) continue;
+            const double u0 = lane < N ? U[k * N + lane] : 0.0;
+            const double u1 = lane + 32 < N ? U[k * N + lane + 32] : 0.0;
+            const double d = warp_sum(fma(u0, v0, u1 * v1));
+            v0 -= d * u0;
+            v1 -= d * u1;
+          }
+        }
+        const double nn = warp_sum(fma(v0, v0, v1 * v1));
+        if (nn > 0.25) {
+          const double inv = 1.0 / sqrt(nn);
+          if (lane < N) U[j * N + lane] = v0 * inv;
+          if (lane + 32 < N) U[j * N + lane + 32] = v1 * inv;
+          __syncwarp();
+          ++cand;
+          break;
+        }
+      }
+    }
+  }
+  // B = Q [Vx(:, order); 0]: the reflectors applied backwards
+  for (int idx = tid; idx < M * N; idx += nthr) {
+    const int i = idx % M, k = idx / M;
+    B[idx] = i < N ? Vm[order[k] * N2 + i] : 0.0;
+  }
+  __syncthreads();
+  for (int j = N - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    qj_apply<RPL>(A, B, M, j, 0, N, tj);
+    __syncthreads();
+  }
+  for (int j = tid; j < N; j += nthr) sig[j] = sg[order[j]];
+  // A = B Sigma (Pi U)^T
+  if (tall) {
+    for (int idx = tid; idx < p * N; idx += nthr) {
+      const int i = idx / N, k = idx % N;
+      P[idx] = B[k * M + i];
+    }
+    for (int idx = tid; idx < N * N; idx += nthr) {
+      const int i = idx % N, k = idx / N;
+      Qt[k * q + perm[i]] = U[k * N + i];
+    }
+  } else {
+    for (int idx = tid; idx < N * N; idx += nthr) {
+      const int i = idx % N, k = idx / N;
+      P[perm[i] * N + k] = U[k * N + i];
+    }
+    for (int idx = tid; idx < N * q; idx += nthr) {
+      const int k = idx / q, c = idx % q;
+      Qt[idx] = B[k * M + c];
+    }
+  }
+}
+
 __global__ void tail_kernel(const double* sig, int k, double theta, int rmin, int rmax, int* info,
                             double* tail) {
   __shared__ double tails[513];
@@ -551,6 +912,115 @@ __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const dou
   for (int i = tid; i < pq; i += nthr) S[i] = W[i];
 }
 
+// S[:, k0:k1] <- H_j S[:, k0:k1] for the reflector stored in column j of the
+// row-major S (v_j = 1, v_i = S[i][j] below): each column is one group of G
+// threads (8 up to 128 rows, else 32) that forms w = tau (S[j][k] + v^T
+// S[j+1:, k]) by a partial sum per thread and a G-lane xor reduction, then
+// updates its own column -- no block barrier between the dot product and the
+// update, and no redundant per-column scalar work across whole warps.
+__device__ void hh_apply_groups(double* S, int LDS, int rows, int j, int k0, int k1, double tj) {
+  const int nc = k1 - k0;
+  if (nc <= 0) return;
+  const int G = rows <= 128 ? 8 : 32;
+  const int tid = threadIdx.x, ngrp = blockDim.x / G, grp = tid / G, g = tid - grp * G;
+  const int trips = (nc + ngrp - 1) / ngrp;
+  if (((tid >> 5) << 5) / G >= nc) return;  // whole warp past the last column
+  for (int t = 0; t < trips; ++t) {
+    const int c = grp + t * ngrp;
+    const bool act = c < nc;
+    const int k = k0 + (act ? c : 0);
+    double w = 0.0;
+    const double sjk = act ? S[j * LDS + k] : 0.0;
+    if (act)
+      for (int i = j + 1 + g; i < rows; i += G) w = fma(S[i * LDS + j], S[i * LDS + k], w);
+    for (int o = G >> 1; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    if (act) {
+      w = tj * (w + sjk);
+      for (int i = j + 1 + g; i < rows; i += G) S[i * LDS + k] -= w * S[i * LDS + j];
+      if (g == 0) S[j * LDS + k] = sjk - w;
+    }
+  }
+}
+
+// The same RK4 over a cluster of SRK_CL CTAs: CTA c owns a block of rows of
+// the R x R iterate, forms its rows of G_s W (all of W needed) and of
+// (G_s W) F_s (its rows only), and broadcasts its rows of the next stage's W
+// into every CTA's shared memory (DSMEM stores; W double-buffered, so one
+// cluster barrier per stage). Same products, same summation order as
+// s_rk4_kernel, so the result is bit-identical; the work is spread over 8 SMs.
+constexpr int SRK_CL = 8;
+__global__ void __cluster_dims__(SRK_CL, 1, 1) __launch_bounds__(256)
+    s_rk4_cluster_kernel(double* S, int p, int q, const double* G, const double* F, int ns,
+                         double dt) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  const int per = (p + SRK_CL - 1) / SRK_CL;
+  const int r0 = cr * per;
+  const int nr = r0 < p ? (p - r0 < per ? p - r0 : per) : 0;
+  const int pq = p * q;
+  double* W0 = sm;                 // p x q, double-buffered across stages
+  double* W1 = W0 + pq;
+  double* S0 = W1 + pq;            // own rows (per x q)
+  double* T = S0 + per * q;        // per x q
+  double* Acc = T + per * q;       // per x q
+  double* sg = Acc + per * q;      // ns x per x p: own rows of every G_s
+  double* sf = sg + (size_t)ns * per * p;  // ns x q x q
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < ns * nr * p; i += nthr) {
+    const int s = i / (nr * p), rem = i - s * nr * p, a = rem / p, k = rem - a * p;
+    sg[(s * per + a) * p + k] = G[(size_t)s * p * p + (size_t)(r0 + a) * p + k];
+  }
+  for (int i = tid; i < ns * q * q; i += nthr) sf[i] = F[i];
+  for (int i = tid; i < pq; i += nthr) W0[i] = S[i];
+  for (int i = tid; i < nr * q; i += nthr) S0[i] = S[(size_t)r0 * q + i];
+  __syncthreads();
+  const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+  for (int st = 0; st < 4; ++st) {
+    const double* W = (st & 1) ? W1 : W0;
+    double* Wn = (st & 1) ? W0 : W1;
+    for (int i = tid; i < nr * q; i += nthr) Acc[i] = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const double* Gs = sg + (size_t)s * per * p;
+      const double* Fs = sf + (size_t)s * q * q;
+      __syncthreads();
+      for (int i = tid; i < nr * q; i += nthr) {
+        const int a = i / q, b = i % q;
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < p; k += 2) {
+          t0 = fma(Gs[a * p + k], W[k * q + b], t0);
+          t1 = fma(Gs[a * p + k + 1], W[(k + 1) * q + b], t1);
+        }
+        if (k < p) t0 = fma(Gs[a * p + k], W[k * q + b], t0);
+        T[i] = t0 + t1;
+      }
+      __syncthreads();
+      for (int i = tid; i < nr * q; i += nthr) {
+        const int a = i / q, b = i % q;
+        double t0 = 0.0, t1 = 0.0;
+        int k = 0;
+        for (; k + 1 < q; k += 2) {
+          t0 = fma(T[a * q + k], Fs[k * q + b], t0);
+          t1 = fma(T[a * q + k + 1], Fs[(k + 1) * q + b], t1);
+        }
+        if (k < q) t0 = fma(T[a * q + k], Fs[k * q + b], t0);
+        Acc[i] -= t0 + t1;
+      }
+    }
+    const double c = coef[st] * dt;
+    if (st < 3) {
+      for (int i = tid; i < nr * q; i += nthr) {
+        const double v = S0[i] + c * Acc[i];
+        for (int rr = 0; rr < SRK_CL; ++rr) cl.map_shared_rank(Wn, rr)[(size_t)r0 * q + i] = v;
+      }
+      cl.sync();  // the next stage's W complete in every CTA
+    } else {
+      for (int i = tid; i < nr * q; i += nthr) S[(size_t)r0 * q + i] = S0[i] + c * Acc[i];
+    }
+  }
+}
+
 // Householder QR of a whole (rows x cols) column-major matrix in one CTA
 // (the m-side factors: rows = m moments <= ~600): the matrix lives in shared
 // memory, the reflectors are those of hh_qr_kernel (beta = -sign(alpha) ||x||,
@@ -566,11 +1036,9 @@ __global__ void __launch_bounds__(512)
   extern __shared__ double sm[];
   const int LDS = cols | 1;  // odd row length: conflict-free column walks
   double* S = gw ? gw : sm;            // rows x LDS
-  double* red = gw ? sm : S + (size_t)rows * LDS;  // 32
-  double* wk = red + 32;               // cols
-  double* tau = wk + cols;             // cols
+  double* tau = (gw ? sm : S + (size_t)rows * LDS) + 32 + cols;  // cols
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < rows * cols; idx += nthr) {
     const int i = idx % rows, j = idx / rows;
     S[i * LDS + j] = A[(size_t)i + (size_t)j * lda];
@@ -578,36 +1046,25 @@ __global__ void __launch_bounds__(512)
   __syncthreads();
   const int kk = rows < cols ? rows : cols;
   for (int j = 0; j < kk; ++j) {
-    double part = 0.0;
-    for (int i = j + 1 + tid; i < rows; i += nthr) part += S[i * LDS + j] * S[i * LDS + j];
-    const double xnorm2 = block_sum(part, red);
-    double tj = 0.0;
-    if (xnorm2 > 0.0) {
-      const double alpha = S[j * LDS + j];
-      const double beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
-      tj = (beta - alpha) / beta;
-      const double scl = 1.0 / (alpha - beta);
-      for (int i = j + 1 + tid; i < rows; i += nthr) S[i * LDS + j] *= scl;
-      __syncthreads();
-      for (int k = j + 1 + warp; k < cols; k += nw) {
-        double sacc = 0.0;
-        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
-        sacc = warp_sum(sacc);
-        if (lane == 0) wk[k] = S[j * LDS + k] + sacc;
+    // the reflector of column j in one warp
+    if (warp == 0) {
+      double part = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) part += S[i * LDS + j] * S[i * LDS + j];
+      const double xnorm2 = warp_sum(part);
+      double tj = 0.0;
+      if (xnorm2 > 0.0) {
+        const double alpha = S[j * LDS + j];
+        const double beta = -copysign(sqrt(alpha * alpha + xnorm2), alpha);
+        tj = (beta - alpha) / beta;
+        const double scl = 1.0 / (alpha - beta);
+        for (int i = j + 1 + lane; i < rows; i += 32) S[i * LDS + j] *= scl;
+        __syncwarp();
+        if (lane == 0) S[j * LDS + j] = beta;
       }
-      __syncthreads();
-      const int w = cols - j - 1;
-      if (w > 0) {
-        for (int idx = tid; idx < (rows - j) * w; idx += nthr) {
-          const int i = j + idx / w, k = j + 1 + idx % w;
-          const double v = (i == j) ? 1.0 : S[i * LDS + j];
-          S[i * LDS + k] -= tj * v * wk[k];
-        }
-      }
-      __syncthreads();
-      if (tid == 0) S[j * LDS + j] = beta;
+      if (lane == 0) tau[j] = tj;
     }
-    if (tid == 0) tau[j] = tj;
+    __syncthreads();
+    if (tau[j] != 0.0) hh_apply_groups(S, LDS, rows, j, j + 1, cols, tau[j]);
     __syncthreads();
   }
   // triangular factor (kk x cols, row-major)
@@ -620,19 +1077,7 @@ __global__ void __launch_bounds__(512)
   for (int j = kk - 1; j >= 0; --j) {
     const double tj = tau[j];
     if (j < kk - 1 && tj != 0.0) {
-      for (int k = j + 1 + warp; k < kk; k += nw) {
-        double sacc = 0.0;
-        for (int i = j + 1 + lane; i < rows; i += 32) sacc += S[i * LDS + j] * S[i * LDS + k];
-        sacc = warp_sum(sacc);
-        if (lane == 0) wk[k] = S[j * LDS + k] + sacc;
-      }
-      __syncthreads();
-      const int w = kk - j - 1;
-      for (int idx = tid; idx < (rows - j) * w; idx += nthr) {
-        const int i = j + idx / w, k = j + 1 + idx % w;
-        const double v = (i == j) ? 1.0 : S[i * LDS + j];
-        S[i * LDS + k] -= tj * v * wk[k];
-      }
+      hh_apply_groups(S, LDS, rows, j, j + 1, kk, tj);
       __syncthreads();
     }
     for (int i = tid; i < rows; i += nthr) {
@@ -733,9 +1178,9 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
     if (sm + 1024 <= (size_t)kMaxDynSmem) {
-      // a block of 4 warps for the small m-side factors (its barriers are the
-      // cost at 64 rows), 16 warps from a few hundred rows
-      const int thr = rows <= 128 ? 128 : 512;
+      // one 8-lane group per column up to 128 rows, 16 warps from a few hundred rows
+      int thr = rows <= 128 ? 8 * cols : 512;  // one 8-lane group per column
+      thr = thr > 512 ? 512 : ((thr + 31) / 32) * 32;
       set_smem((const void*)qr_small_kernel, sm);
       qr_small_kernel<<<1, thr, sm, st>>>(a, rows, cols, lda, q, ldq, rfac, nullptr);
       launched();
@@ -878,7 +1323,27 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   int threads = 32 * (N2 / 2);
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
-  if (M <= 64) {
+  if (M <= 64 && !getenv("PND_SVD_PLAIN")) {
+    const size_t smq = ((size_t)2 * M * N + (size_t)N * N2 + (size_t)N2 * N2 + (size_t)N * N +
+                        N + 2 * N2) * sizeof(double) + 2 * N * sizeof(int);
+    // one 8-lane group per Jacobi pair; rows per lane = ceil(M / 8)
+    int thq = ((QJ_G * (N2 / 2) + 31) / 32) * 32;
+    if (thq < 64) thq = 64;
+    const int rpl = (M + QJ_G - 1) / QJ_G;
+    auto kq = svd_qrj_kernel<8>;
+    switch (rpl) {
+      case 1: kq = svd_qrj_kernel<1>; break;
+      case 2: kq = svd_qrj_kernel<2>; break;
+      case 3: kq = svd_qrj_kernel<3>; break;
+      case 4: kq = svd_qrj_kernel<4>; break;
+      case 5: kq = svd_qrj_kernel<5>; break;
+      case 6: kq = svd_qrj_kernel<6>; break;
+      case 7: kq = svd_qrj_kernel<7>; break;
+      default: break;
+    }
+    set_smem((const void*)kq, smq);
+    kq<<<1, thq, smq, st>>>(s, p, q, P, sig, Qt);
+  } else if (M <= 64) {
     set_smem((const void*)svd_kernel<2>, sm);
     svd_kernel<2><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);
   } else if (M <= 128) {
@@ -930,6 +1395,15 @@ void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, do
     s_rk4_kernel<<<1, 1024, 0, st>>>(S, p, q, G, F, ns, dt, 0, gw);
     launched();
     CK(cudaFreeAsync(gw, st));
+    return;
+  }
+  const int per = (p + SRK_CL - 1) / SRK_CL;
+  const size_t sm_cl = (2 * (size_t)p * q + 3 * (size_t)per * q + (size_t)ns * per * p +
+                        (size_t)ns * q * q) * sizeof(double);
+  if (sm_cl + 1024 <= (size_t)kMaxDynSmem && !getenv("PND_SRK4_ONE")) {
+    set_smem((const void*)s_rk4_cluster_kernel, sm_cl);
+    s_rk4_cluster_kernel<<<SRK_CL, 256, sm_cl, st>>>(S, p, q, G, F, ns, dt);
+    launched();
     return;
   }
   set_smem((const void*)s_rk4_kernel, staged ? sm_staged : sm);

@@ -106,6 +106,24 @@ struct Handle {
   TimerState timer;
   bool nvtx_open = false;  // an NVTX phase range is open
   bool singular_pending = false;  // scattering solve flag awaiting the next sync
+
+  // speculative steps (step.cu spec_*): the host predicts every shape the
+  // step's device-side decisions produce (the augmentation ranks, the
+  // truncation ranks), launches the whole step without a host round trip and
+  // the device flags any disagreement; one synchronisation at the end reads
+  // the flag, and a mismatch restores the snapshot taken at the step's start
+  // and recomputes the step on the synchronous path. Small grids only (the
+  // snapshot is a copy of the state), one device.
+  bool spec = false;              // inside a speculative step
+  int spec_pause = 0;             // steps to run synchronously after a mismatch
+  int spec_r1[2] = {-1, -1};      // truncation ranks of the last step (the predictions)
+  int spec_tr = 0;                // which substep of the step is running (0, 1)
+  bool spec_kfull[2] = {false, false};  // its last augmentation was full
+  IBuf spec_flag;                 // [mismatch, singular]
+  NBuf snap_u;
+  DBuf snap_s, snap_v, snap_dep, snap_prev;
+  int snap_ua = 0, snap_ru = 0, snap_rv = 0;
+  long long spec_hits = 0, spec_misses = 0;
 };
 
 // phase mark: when timing is on, records an event on the handle's stream;
@@ -187,6 +205,11 @@ void dose_accumulate_step(Handle& h, double dt, bool tally_steps);
 // have_ugram: U^T U is already in defect_gram_slot (from the last truncation)
 double orth_defect(Handle& h, bool have_ugram = false);
 double* defect_gram_slot(Handle& h, int ru, int rv);
+// speculative steps: eligibility, snapshot + flag reset, and the one
+// synchronisation (false: the prediction failed and the state is restored)
+bool spec_eligible(Handle& h, int truncate_after);
+void spec_begin(Handle& h);
+bool spec_end(Handle& h, bool abort);
 // Q (k columns) = orthonormal basis of (I - U U^T) X; C1 = U^T X (device, ua x b; null
 // when U is empty). Returns k; the result is installed as the state's Q.
 // rank_bound: an upper bound on rank(X) known from its construction (the

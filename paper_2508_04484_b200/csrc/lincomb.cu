@@ -570,9 +570,7 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
     if (PW) kern = lincomb_pw_kernel<NB8>;
   }
   allow_max_smem(kern);
-  int nblk = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nblk, kern, LTH, smem));
-  if (nblk < 1) nblk = 1;
+  const int nblk = occupancy_cached((const void*)kern, LTH, smem);
   const int nchunks = (g.n + LCH - 1) / LCH;
   int grid = sm_count() * nblk;
   if (grid > nchunks) grid = nchunks;

@@ -30,9 +30,7 @@ __global__ void reduce_blocks(const double* __restrict__ partial, int nblk, int 
 
 template <class Kern>
 int resident(Kern k, int threads, size_t smem) {
-  int nb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, threads, smem));
-  return nb < 1 ? 1 : nb;
+  return occupancy_cached((const void*)k, threads, smem);
 }
 
 // ===================================================================== pgram

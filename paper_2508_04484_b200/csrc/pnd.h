@@ -43,14 +43,21 @@ void check_cuda(cudaError_t e, const char* what);
 // under a larger one).
 constexpr int kMaxDynSmem = 227 * 1024;
 int max_smem_optin();  // cudaDevAttrMaxSharedMemoryPerBlockOptin of the current device
+// Both queries below are cached per kernel (and launch shape): the driver
+// calls cost microseconds each, paid on every launch of the launch-bound small
+// problems otherwise.
+bool smem_set_once(const void* fn);   // true the first time fn is seen
 template <class F>
 inline void allow_max_smem(F* fn) {
+  if (!smem_set_once((const void*)fn)) return;
   cudaFuncAttributes fa{};
   check_cuda(cudaFuncGetAttributes(&fa, (const void*)fn), "cudaFuncGetAttributes");
   check_cuda(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   max_smem_optin() - (int)fa.sharedSizeBytes),
              "cudaFuncSetAttribute");
 }
+// cudaOccupancyMaxActiveBlocksPerMultiprocessor, cached per (kernel, threads, smem); >= 1
+int occupancy_cached(const void* fn, int threads, size_t smem);
 // after every kernel launch: surface launch errors, count the launch
 void launched();
 long long launch_count();

@@ -214,9 +214,7 @@ StScale stencil_scale(const Geom& g) {
 
 template <class Kern>
 int resident(Kern k, int threads, size_t smem) {
-  int nb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, threads, smem));
-  return nb < 1 ? 1 : nb;
+  return occupancy_cached((const void*)k, threads, smem);
 }
 
 // ============================================================ pipeline roles

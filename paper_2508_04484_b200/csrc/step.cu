@@ -371,6 +371,57 @@ void check_singular(Handle& h) {
   }
 }
 
+// ------------------------------------------------------------ speculative steps
+namespace {
+// flag[0] |= the device-side decision differs from the host's prediction
+__global__ void spec_check_kernel(const int* got, int want, int* flag) {
+  if (threadIdx.x == 0 && got[0] != want) atomicOr(flag, 1);
+}
+__global__ void spec_check_trunc_kernel(const int* r1, const double* sig, int want, int* flag) {
+  if (threadIdx.x == 0 && (r1[0] != want || sig[0] == 0.0)) atomicOr(flag, 2);
+}
+// the re-orthogonalisation pass of orth_complement, predicated on the device:
+// when the block's defect is within the trigger the pass applies TA = I,
+// TB = 0 (Q TA - U0 TB = Q exactly)
+__global__ void spec_select_kernel(const double* defect, double trigger, int a, int k, double* TA,
+                                   double* TB) {
+  if (defect[0] > trigger) return;
+  for (int i = threadIdx.x; i < k * k; i += blockDim.x) TA[i] = (i / k == i % k) ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < a * k; i += blockDim.x) TB[i] = 0.0;
+}
+}  // namespace
+
+// orth_complement after its pass-2 pivoted Cholesky, without a host round
+// trip: the increment is predicted to be full (k = min(b, rank_bound): no
+// deflated column, so no second level), the device checks the prediction,
+// and the re-orthogonalisation pass always runs, predicated by its defect.
+static int orth_complement_spec(Handle& h, NMat Y, NMat U0, int a, int b, int rank_bound,
+                                double* grams, double* TA, double* TB, int* info,
+                                double* dinfo) {
+  const Geom& g = h.g;
+  cudaStream_t st = h.st;
+  const int k = b < rank_bound ? b : rank_bound;
+  spec_check_kernel<<<1, 32, 0, st>>>(info, k, h.spec_flag.p);
+  launched();
+  NMat Qv = h.Q.view(g, k, st);
+  lincomb(g, Y, NMat{}, U0, TA, TB, Qv, grams, h.part, st);
+  double* C3 = grams;
+  double* G3 = grams + (size_t)a * k;
+  defect_gc_kernel<<<1, 256, 0, st>>>(G3, C3, a, k, dinfo);
+  launched();
+  double* G3c = slot(h, S_M2, (size_t)k * k);
+  CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+  if (a > 0) gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
+  cholqr_build(G3c, C3, a, k, 1, 0.0, nullptr, TA, TB, info + 1, nullptr, h.cq_work, st);
+  spec_select_kernel<<<1, 256, 0, st>>>(dinfo, 1e-12, a, k, TA, TB);
+  launched();
+  NMat Q2 = h.Qa.view(g, k, st);
+  lincomb(g, Qv, NMat{}, U0, TA, TB, Q2, nullptr, h.part, st);
+  std::swap(h.Q, h.Qa);
+  h.uq = k;
+  return k;
+}
+
 int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound) {
   const int a = h.ua, b = X.cols + (X2.p ? X2.cols : 0);
   cudaStream_t st = h.st;
@@ -391,6 +442,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   // rank-revealing pivoted Cholesky of the projected Gram: columns whose
   // residual falls below 1e-7 of the largest are deflated (to level 2)
   cholqr_build(G2, C2, a, b, 0, 1e-14, nullptr, TA, TB, info, sig, h.cq_work, st);
+  if (h.spec) return orth_complement_spec(h, Y, U0, a, b, rank_bound, grams, TA, TB, info, dinfo);
   CK(cudaMemcpyAsync(h.pinned + 8, info, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h.pinned + 11, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -398,6 +450,7 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   int k = *(int*)(h.pinned + 8);
   const double lam0 = h.pinned[11];
   h.uq = 0;
+  h.spec_kfull[h.spec_tr] = k == (b < rank_bound ? b : rank_bound);
   // Level 2 (graded increments): the one-pass Gram resolves directions only
   // down to ~1e-7 of the largest column (its entries carry eps |Y|^2 absolute
   // error), where the reference's Householder QR keeps every direction. When
@@ -897,14 +950,30 @@ void truncate(Handle& h, double theta, int rmin, int rmax, double* tail_out, int
   double* dtail = slot(h, S_TAIL, 2);
   int* info = h.iflag.get(8);
   tail_rule(sig, k, theta, rmin, rmax, info + 1, dtail, st);
-  CK(cudaMemcpyAsync(h.pinned, dtail, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync((int*)(h.pinned + 1), info + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(h.pinned + 2, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  check_singular(h);
-  const int r1 = *(int*)(h.pinned + 1);
-  const double tail = h.pinned[0];
-  const bool all_zero = h.pinned[2] == 0.0;
+  int r1;
+  double tail;
+  bool all_zero;
+  if (h.spec) {
+    // predicted: the rank this truncation kept last step (the fixed rank in
+    // fixed-rank runs), a nonzero S^; the tail is read after the step
+    const int which = h.spec_tr;
+    r1 = h.spec_r1[which] < k ? h.spec_r1[which] : k;
+    spec_check_trunc_kernel<<<1, 32, 0, st>>>(info + 1, sig, r1, h.spec_flag.p);
+    launched();
+    CK(cudaMemcpyAsync(h.pinned + 20 + which, dtail, sizeof(double), cudaMemcpyDeviceToHost, st));
+    tail = 0.0;
+    all_zero = false;
+  } else {
+    CK(cudaMemcpyAsync(h.pinned, dtail, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync((int*)(h.pinned + 1), info + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h.pinned + 2, sig, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    check_singular(h);
+    r1 = *(int*)(h.pinned + 1);
+    tail = h.pinned[0];
+    all_zero = h.pinned[2] == 0.0;
+    if (r1 >= 0) h.spec_r1[h.spec_tr] = r1;
+  }
   if (r1 < 0) {
     fail(PND_ENUMERICAL, "adaptive rank " + std::to_string(-r1 - 1) + " exceeds rank_max=" +
                              std::to_string(rmax) + "; increase the truncation threshold");
@@ -1012,9 +1081,95 @@ double orth_defect(Handle& h, bool have_ugram) {
   defect_kernel<<<1, 256, 0, st>>>(GV, h.rv, out);
   launched();
   phase(h, -1);
+  if (h.spec) {  // read with the speculative step's one synchronisation
+    CK(cudaMemcpyAsync(h.pinned + 22, out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    return 0.0;
+  }
   CK(cudaMemcpyAsync(h.pinned + 2, out, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   return h.pinned[2];
+}
+
+// ------------------------------------------------------------ speculative step driver
+bool spec_eligible(Handle& h, int truncate_after) {
+  if (getenv("PND_NO_SPEC") || h.spec_pause > 0 || truncate_after != 3) return false;
+  // the last synchronous step's augmentations were full (the prediction)
+  if (!h.spec_kfull[0] || !h.spec_kfull[1]) return false;
+  if (h.blocked || h.ua > 64 || h.rv > 64 || h.ua <= 0 || h.rv <= 0) return false;
+  if (h.spec_r1[0] < 1 || h.spec_r1[1] < 1) return false;  // no prediction yet
+  if (comm_world(h.g) != 1) return false;
+  // the snapshot is a copy of the state: small grids only (the launch-bound regime)
+  return (size_t)h.g.n * (size_t)(h.ua + h.uq) <= ((size_t)1 << 22);
+}
+
+void spec_begin(Handle& h) {
+  consolidate(h);
+  cudaStream_t st = h.st;
+  const Geom& g = h.g;
+  const NMat u = state_u(h);
+  const size_t rows = (size_t)g.n + 2 * (size_t)g.halo;
+  double* su = h.snap_u.d.get(rows * u.rs);
+  CK(cudaMemcpyAsync(su, u.p - (size_t)g.halo * u.rs, rows * u.rs * sizeof(double),
+                     cudaMemcpyDeviceToDevice, st));
+  h.snap_u.rs = u.rs;
+  CK(cudaMemcpyAsync(h.snap_s.get((size_t)h.ru * h.rv), h.S.p, sizeof(double) * h.ru * h.rv,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.snap_v.get((size_t)h.m * h.rv), h.V.p, sizeof(double) * h.m * h.rv,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.snap_dep.get(g.ld), h.dep.get(g.ld), sizeof(double) * g.ld,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.snap_prev.get(g.ld), h.prev.get(g.ld), sizeof(double) * g.ld,
+                     cudaMemcpyDeviceToDevice, st));
+  h.snap_ua = h.ua;
+  h.snap_ru = h.ru;
+  h.snap_rv = h.rv;
+  int* f = h.spec_flag.get(2);
+  CK(cudaMemsetAsync(f, 0, 2 * sizeof(int), st));
+  h.spec = true;
+}
+
+bool spec_end(Handle& h, bool abort) {
+  cudaStream_t st = h.st;
+  h.spec = false;
+  CK(cudaMemcpyAsync((int*)(h.pinned + 24), h.spec_flag.p, sizeof(int), cudaMemcpyDeviceToHost,
+                     st));
+  CK(cudaStreamSynchronize(st));
+  const int flag = *(int*)(h.pinned + 24);
+  // the scattering solves' singular-column flag (the synchronous path raises)
+  const bool singular = h.singular_pending && *(int*)(h.pinned + 10) != (1 << 30);
+  h.singular_pending = false;
+  // test hook: PND_SPEC_TEST_MISS=k rejects every k-th speculative step (the
+  // restore-and-recompute path, which must reproduce the accepted result)
+  bool forced = false;
+  if (const char* e = getenv("PND_SPEC_TEST_MISS")) {
+    const long long k = atoll(e);
+    forced = k > 0 && (h.spec_hits + h.spec_misses) % k == 0;
+  }
+  if (flag == 0 && !singular && !abort && !forced) {
+    ++h.spec_hits;
+    return true;
+  }
+  ++h.spec_misses;
+  h.spec_pause = 2;
+  // restore the step's input state
+  const Geom& g = h.g;
+  h.ua = h.snap_ua;
+  h.uq = 0;
+  h.ru = h.snap_ru;
+  h.rv = h.snap_rv;
+  const NMat u = h.U.view(g, h.ua, st);
+  if (u.rs != h.snap_u.rs) fail(PND_ECONFIG, "speculative step: snapshot stride mismatch");
+  const size_t rows = (size_t)g.n + 2 * (size_t)g.halo;
+  CK(cudaMemcpyAsync(u.p - (size_t)g.halo * u.rs, h.snap_u.d.p, rows * u.rs * sizeof(double),
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.S.get((size_t)h.ru * h.rv), h.snap_s.p, sizeof(double) * h.ru * h.rv,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.V.get((size_t)h.m * h.rv), h.snap_v.p, sizeof(double) * h.m * h.rv,
+                     cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.dep.p, h.snap_dep.p, sizeof(double) * g.ld, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h.prev.p, h.snap_prev.p, sizeof(double) * g.ld, cudaMemcpyDeviceToDevice,
+                     st));
+  return false;
 }
 
 }  // namespace pnd

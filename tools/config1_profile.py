@@ -15,13 +15,15 @@ for k in range(5):
 h = s.h
 h.call("pnd_synchronize")
 h.call("pnd_timing", 1)
-t0 = time.perf_counter(); tc = 0.0
+t0 = time.perf_counter(); c0 = time.process_time(); tc = 0.0
 for k in range(5, 5 + STEPS):
     a = time.perf_counter(); s.set_coefficients(edges[k], edges[k+1]); tc += time.perf_counter() - a
     s.step(edges[k]-edges[k+1])
 h.call("pnd_synchronize")
 t = time.perf_counter() - t0
+cpu = time.process_time() - c0
 nph = len(_lib.PHASES); ms = np.zeros(nph); cnt = np.zeros(nph, dtype=np.int32)
 h.call("pnd_timing_get", nph, _lib.ptr(ms), _lib.ptr(cnt))
-print("per step ms", 1000*t/STEPS, "host coeff ms", 1000*tc/STEPS)
+print("per step ms", 1000*t/STEPS, "host coeff ms", 1000*tc/STEPS, "host cpu ms", 1000*cpu/STEPS)
+hm = np.zeros(2, dtype=np.int64); h.call("pnd_spec_stats", _lib.ptr(hm)); print("speculative steps accepted/recomputed", hm.tolist())
 for n, v in zip(_lib.PHASES, ms): print(n, round(v/STEPS, 4))
