@@ -453,19 +453,19 @@ __device__ __forceinline__ void qj_apply(const double* V, double* T, int M, int 
 }
 
 template <int RPL>
-__global__ void __launch_bounds__(256, 1)
-    svd_qrj_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt) {
+__global__ void __launch_bounds__(512, 1)
+    svd_qrj_kernel(const double* s, int p, int q, double* P, double* sig, double* Qt,
+                   int stop) {
   extern __shared__ double sm[];
   const bool tall = p >= q;
   const int M = tall ? p : q, N = tall ? q : p;
   const int N2 = N + (N & 1);
-  double* A = sm;                // M x N column-major: R on/above the diagonal, reflectors below
-  double* X = A + M * N;         // N x N2 column-major, X = R^T
+  double* V = sm;                // N x M: reflector j below row j (V[j M + i], i > j)
+  double* X = V + N * M;         // N x N2 column-major, X = R^T
   double* Vm = X + N * N2;       // N2 x N2 column-major
   double* U = Vm + N2 * N2;      // N x N: normalised X columns in singular value order
-  double* B = U + N * N;         // M x N: Q Vx (sorted)
-  double* tau = B + M * N;       // N
-  double* nrm = tau + N;         // N2
+  double* tau = U + N * N;       // N
+  double* nrm = tau + N;         // N2 (QR: trailing norms by position; Jacobi: column norms)
   double* sg = nrm + N2;         // N2
   int* perm = (int*)(sg + N2);   // N: column pivots (A Pi)[:, j] = A[:, perm[j]]
   int* order = perm + N;         // N: singular values, descending
@@ -473,114 +473,121 @@ __global__ void __launch_bounds__(256, 1)
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
   const int grp = tid / QJ_G, l = tid % QJ_G, ngrp = nthr / QJ_G;
-  for (int idx = tid; idx < M * N; idx += nthr) {
-    const int i = idx % M, j = idx / M;
-    A[idx] = tall ? s[i * q + j] : s[j * q + i];
+  const unsigned gm = 0xffu << (lane & ~7);
+  // ---- Householder QR with column pivoting, column c of A in the registers
+  // of 8-lane group c (rows l + 8u); pivoting renames positions (no data
+  // moves): group c sits at position `at` (initially c)
+  const bool own = grp < N;
+  double xa[RPL];
+  double nn = 0.0;
+#pragma unroll
+  for (int u = 0; u < RPL; ++u) {
+    const int i = l + QJ_G * u;
+    xa[u] = (own && i < M) ? (tall ? s[i * q + grp] : s[grp * q + i]) : 0.0;
+    nn = fma(xa[u], xa[u], nn);
   }
-  for (int j = tid; j < N; j += nthr) perm[j] = j;
+  nn += __shfl_xor_sync(0xffffffffu, nn, 4);
+  nn += __shfl_xor_sync(0xffffffffu, nn, 2);
+  nn += __shfl_xor_sync(0xffffffffu, nn, 1);
+  int at = grp;
+  bool done = !own;
+  if (own && l == 0) nrm[grp] = nn;
   __syncthreads();
-  for (int c = warp; c < N; c += nw) {
-    double x = 0.0;
-    for (int i = lane; i < M; i += 32) x += A[c * M + i] * A[c * M + i];
-    x = warp_sum(x);
-    if (lane == 0) nrm[c] = x;
-  }
-  __syncthreads();
-  // ---- Householder QR with column pivoting
   for (int j = 0; j < N; ++j) {
-    if (warp == 0) {
-      // pivot: the largest trailing column norm, the first on ties
-      double best = -1.0;
-      int bi = j;
-      for (int c = j + lane; c < N; c += 32)
-        if (nrm[c] > best) { best = nrm[c]; bi = c; }
+    // pivot (every group redundantly): the first position p >= j with the
+    // largest trailing norm
+    double best = -1.0;
+    int bp = j;
+    for (int pp = j + l; pp < N; pp += QJ_G)
+      if (nrm[pp] > best) { best = nrm[pp]; bp = pp; }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    for (int o = 4; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ob > best || (ob == best && op < bp)) { best = ob; bp = op; }
+    }
+    // the group at position bp moves to position j, the one at j to bp
+    if (!done) {
+      if (at == bp) at = j;
+      else if (at == j) at = bp;
+    }
+    if (!done && at == j) {
+      // owner: reflector of row j from its registers
+      double sq = 0.0, al = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = l + QJ_G * u;
+        if (i > j) sq = fma(xa[u], xa[u], sq);
+        if (i == j) al = xa[u];
       }
-      if (bi != j) {
-        for (int i = lane; i < M; i += 32) {
-          const double t = A[j * M + i];
-          A[j * M + i] = A[bi * M + i];
-          A[bi * M + i] = t;
-        }
-        if (lane == 0) {
-          const int t = perm[j]; perm[j] = perm[bi]; perm[bi] = t;
-        }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        sq += __shfl_xor_sync(gm, sq, o);
+        al += __shfl_xor_sync(gm, al, o);
       }
-      __syncwarp();
-      double x = 0.0;
-      for (int i = j + 1 + lane; i < M; i += 32) x += A[j * M + i] * A[j * M + i];
-      const double xn2 = warp_sum(x);
-      const double alpha = A[j * M + j];
       double tj = 0.0;
-      if (xn2 > 0.0) {
-        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        tj = (beta - alpha) / beta;
-        const double scl = 1.0 / (alpha - beta);
-        for (int i = j + 1 + lane; i < M; i += 32) A[j * M + i] *= scl;
-        __syncwarp();
-        if (lane == 0) A[j * M + j] = beta;
+      if (sq > 0.0) {
+        const double beta = -copysign(sqrt(al * al + sq), al);
+        tj = (beta - al) / beta;
+        const double scl = 1.0 / (al - beta);
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int i = l + QJ_G * u;
+          if (i > j && i < M) V[j * M + i] = xa[u] * scl;
+          if (i == j) xa[u] = beta;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < RPL; ++u) {
+          const int i = l + QJ_G * u;
+          if (i > j && i < M) V[j * M + i] = 0.0;
+        }
       }
-      if (lane == 0) tau[j] = tj;
+      // R column j -> row j of X = R^T (X[j + i N] = R[i][j], zero below the diagonal)
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = l + QJ_G * u;
+        if (i < N) X[j + i * N] = i <= j ? xa[u] : 0.0;
+      }
+      if (l == 0) {
+        tau[j] = tj;
+        perm[j] = grp;
+      }
+      done = true;
     }
     __syncthreads();
-    // apply H_j to the trailing columns (8-lane groups); refresh their norms
-    // over rows > j for the next pivot
-    {
+    if (!done) {
+      // H_j on this column, then its trailing norm (rows > j) at its position
       const double tj = tau[j];
-      const int nc = N - j - 1;
-      const int trips = (nc + ngrp - 1) / ngrp;
-      for (int t = 0; t < trips; ++t) {
-        const int c = grp + t * ngrp;
-        const bool act = c < nc;
-        const int k = j + 1 + (act ? c : 0);
-        double v[RPL], x[RPL];
-        double w = 0.0;
+      double v[RPL];
+      double w = 0.0;
 #pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          const int i = j + 1 + l + QJ_G * u;
-          const bool in = act && i < M;
-          v[u] = in ? A[j * M + i] : 0.0;
-          x[u] = in ? A[k * M + i] : 0.0;
-          w = fma(v[u], x[u], w);
-        }
-        const double ajk = act ? A[k * M + j] : 0.0;
-        w += __shfl_xor_sync(0xffffffffu, w, 4);
-        w += __shfl_xor_sync(0xffffffffu, w, 2);
-        w += __shfl_xor_sync(0xffffffffu, w, 1);
-        w = tj * (w + ajk);
-        double nn = 0.0;
-#pragma unroll
-        for (int u = 0; u < RPL; ++u) {
-          x[u] -= w * v[u];
-          nn = fma(x[u], x[u], nn);
-        }
-        nn += __shfl_xor_sync(0xffffffffu, nn, 4);
-        nn += __shfl_xor_sync(0xffffffffu, nn, 2);
-        nn += __shfl_xor_sync(0xffffffffu, nn, 1);
-        if (act) {
-#pragma unroll
-          for (int u = 0; u < RPL; ++u) {
-            const int i = j + 1 + l + QJ_G * u;
-            if (i < M) A[k * M + i] = x[u];
-          }
-          if (l == 0) {
-            A[k * M + j] = ajk - w;
-            nrm[k] = nn;
-          }
-        }
+      for (int u = 0; u < RPL; ++u) {
+        const int i = l + QJ_G * u;
+        v[u] = i == j ? 1.0 : (i > j && i < M) ? V[j * M + i] : 0.0;
+        w = fma(v[u], xa[u], w);
       }
+      w += __shfl_xor_sync(gm, w, 4);
+      w += __shfl_xor_sync(gm, w, 2);
+      w += __shfl_xor_sync(gm, w, 1);
+      w *= tj;
+      double t2 = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        xa[u] -= w * v[u];
+        const int i = l + QJ_G * u;
+        if (i > j) t2 = fma(xa[u], xa[u], t2);
+      }
+      t2 += __shfl_xor_sync(gm, t2, 4);
+      t2 += __shfl_xor_sync(gm, t2, 2);
+      t2 += __shfl_xor_sync(gm, t2, 1);
+      if (l == 0) nrm[at] = t2;
     }
     __syncthreads();
   }
-  // X = R^T (column j of X = row j of R), Vx = I
-  for (int idx = tid; idx < N * N2; idx += nthr) {
-    const int c = idx % N, j = idx / N;
-    X[idx] = (j < N && c >= j) ? A[c * M + j] : 0.0;
-  }
+  if (stop == 1) return;  // profiling: the QR phase alone
+  // X's pad column and Vx = I
+  for (int idx = tid; idx < N * (N2 - N); idx += nthr) X[N * N + idx] = 0.0;
   for (int idx = tid; idx < N2 * N2; idx += nthr) Vm[idx] = (idx % N2 == idx / N2) ? 1.0 : 0.0;
   __syncthreads();
   // ---- Hestenes sweeps on the columns of X (svd_kernel's rotation and stopping
@@ -620,24 +627,51 @@ __global__ void __launch_bounds__(256, 1)
           }
           if (a > b) { const int t = a; a = b; b = t; }
         }
-        double x[RPL], y[RPL];
+        // every load of the round first (the rotation's operands do not depend
+        // on it): the measured round was a chain of load, shuffle, rotation
+        // parameters and a load-after-store of V
+        double x[RPL], y[RPL], vx[RPL], vy[RPL];
         double ga = 0.0;
 #pragma unroll
         for (int u = 0; u < RPL; ++u) {
           const int i = l + QJ_G * u;
           const bool in = act && i < N;
+          const bool inv = act && i < N2;
           x[u] = in ? X[a * N + i] : 0.0;
           y[u] = in ? X[b * N + i] : 0.0;
+          vx[u] = inv ? Vm[a * N2 + i] : 0.0;
+          vy[u] = inv ? Vm[b * N2 + i] : 0.0;
           ga = fma(x[u], y[u], ga);
         }
+        const double al = act ? nrm[a] : 0.0, be = act ? nrm[b] : 0.0;
+        const double thr = 1e-15 * sqrt(al * be);  // off the shuffle chain (dsqrt: ~100 cycles)
         ga += __shfl_xor_sync(0xffffffffu, ga, 4);
         ga += __shfl_xor_sync(0xffffffffu, ga, 2);
         ga += __shfl_xor_sync(0xffffffffu, ga, 1);
-        const double al = act ? nrm[a] : 0.0, be = act ? nrm[b] : 0.0;
-        if (act && ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = rsqrt(1.0 + t * t), sn = c * t;
+        if (act && ga != 0.0 && fabs(ga) > thr) {
+          // tan(2 theta) = 2 ga / (al - be), the smaller rotation (|theta| <= pi/4):
+          // cos 2theta = |d| / h, sin 2theta = sgn(d) g / h (d = be - al, g = 2 ga,
+          // h = |(d, g)|), c = sqrt(q), s = sin 2theta / (2 c), t = s / c with
+          // q = (1 + cos 2theta) / 2 in [1/2, 1]: two reciprocal square roots
+          // instead of two divisions, a square root and a reciprocal square root
+          // (the same rotation as zeta = d / g, t = sgn(zeta) / (|zeta| + sqrt(1 + zeta^2)))
+          const double d = be - al, gg = 2.0 * ga;
+          const double h2 = fma(d, d, gg * gg);
+          double c, sn, t;
+          if (h2 > 1e-290 && h2 < 1e290) {
+            const double r = rsqrt(h2);
+            const double c2 = fabs(d) * r, s2 = (d >= 0.0 ? gg : -gg) * r;
+            const double q = fma(0.5, c2, 0.5);
+            const double rq = rsqrt(q);
+            c = q * rq;
+            sn = 0.5 * s2 * rq;
+            t = sn * rq;
+          } else {  // extreme magnitudes: the scale-free formula
+            const double zeta = d / gg;
+            t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = rsqrt(1.0 + t * t);
+            sn = c * t;
+          }
 #pragma unroll
           for (int u = 0; u < RPL; ++u) {
             const int i = l + QJ_G * u;
@@ -645,14 +679,9 @@ __global__ void __launch_bounds__(256, 1)
               X[a * N + i] = c * x[u] - sn * y[u];
               X[b * N + i] = sn * x[u] + c * y[u];
             }
-          }
-#pragma unroll
-          for (int u = 0; u < RPL; ++u) {
-            const int i = l + QJ_G * u;
             if (i < N2) {
-              const double vx = Vm[a * N2 + i], vy = Vm[b * N2 + i];
-              Vm[a * N2 + i] = c * vx - sn * vy;
-              Vm[b * N2 + i] = sn * vx + c * vy;
+              Vm[a * N2 + i] = c * vx[u] - sn * vy[u];
+              Vm[b * N2 + i] = sn * vx[u] + c * vy[u];
             }
           }
           if (l == 0) {
@@ -668,6 +697,7 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     if (!any) break;
   }
+  if (stop == 2) return;  // profiling: QR + Jacobi
   // singular values and their order (rank by counting: descending, stable)
   for (int j = warp; j < N; j += nw) {
     double x = 0.0;
@@ -718,25 +748,46 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   }
-  // B = Q [Vx(:, order); 0]: the reflectors applied backwards
-  for (int idx = tid; idx < M * N; idx += nthr) {
-    const int i = idx % M, k = idx / M;
-    B[idx] = i < N ? Vm[order[k] * N2 + i] : 0.0;
-  }
   __syncthreads();
-  for (int j = N - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    qj_apply<RPL>(A, B, M, j, 0, N, tj);
-    __syncthreads();
+  // left vectors of A: B = Q [Vx(:, order); 0], column k in the registers of
+  // group k, the reflectors applied backwards from shared memory (no barrier)
+  if (grp < N) {
+    const int k = grp;
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = l + QJ_G * u;
+      xa[u] = i < N ? Vm[order[k] * N2 + i] : 0.0;
+    }
+    for (int j = N - 1; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      double v[RPL];
+      double w = 0.0;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) {
+        const int i = l + QJ_G * u;
+        v[u] = i == j ? 1.0 : (i > j && i < M) ? V[j * M + i] : 0.0;
+        w = fma(v[u], xa[u], w);
+      }
+      w += __shfl_xor_sync(gm, w, 4);
+      w += __shfl_xor_sync(gm, w, 2);
+      w += __shfl_xor_sync(gm, w, 1);
+      w *= tj;
+#pragma unroll
+      for (int u = 0; u < RPL; ++u) xa[u] -= w * v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < RPL; ++u) {
+      const int i = l + QJ_G * u;
+      if (i < M) {
+        if (tall) P[i * N + k] = xa[u];
+        else Qt[k * q + i] = xa[u];
+      }
+    }
   }
   for (int j = tid; j < N; j += nthr) sig[j] = sg[order[j]];
-  // A = B Sigma (Pi U)^T
+  // right vectors of A: Pi U
   if (tall) {
-    for (int idx = tid; idx < p * N; idx += nthr) {
-      const int i = idx / N, k = idx % N;
-      P[idx] = B[k * M + i];
-    }
     for (int idx = tid; idx < N * N; idx += nthr) {
       const int i = idx % N, k = idx / N;
       Qt[k * q + perm[i]] = U[k * N + i];
@@ -745,10 +796,6 @@ __global__ void __launch_bounds__(256, 1)
     for (int idx = tid; idx < N * N; idx += nthr) {
       const int i = idx % N, k = idx / N;
       P[perm[i] * N + k] = U[k * N + i];
-    }
-    for (int idx = tid; idx < N * q; idx += nthr) {
-      const int k = idx / q, c = idx % q;
-      Qt[idx] = B[k * M + c];
     }
   }
 }
@@ -918,7 +965,11 @@ __global__ void s_rk4_kernel(double* S, int p, int q, const double* G, const dou
 // S[j+1:, k]) by a partial sum per thread and a G-lane xor reduction, then
 // updates its own column -- no block barrier between the dot product and the
 // update, and no redundant per-column scalar work across whole warps.
-__device__ void hh_apply_groups(double* S, int LDS, int rows, int j, int k0, int k1, double tj) {
+// tau_la: look-ahead -- the group of column k0 (= j + 1) then forms that
+// column's reflector (the same dlarfg conventions) and stores it with its tau
+// in tau_la[k0], so the next column step needs no serial reflector phase
+__device__ void hh_apply_groups(double* S, int LDS, int rows, int j, int k0, int k1, double tj,
+                                double* tau_la = nullptr) {
   const int nc = k1 - k0;
   if (nc <= 0) return;
   const int G = rows <= 128 ? 8 : 32;
@@ -938,6 +989,25 @@ __device__ void hh_apply_groups(double* S, int LDS, int rows, int j, int k0, int
       w = tj * (w + sjk);
       for (int i = j + 1 + g; i < rows; i += G) S[i * LDS + k] -= w * S[i * LDS + j];
       if (g == 0) S[j * LDS + k] = sjk - w;
+      if (tau_la && c == 0) {
+        const int lane = tid & 31;
+        const unsigned gm = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+        __syncwarp(gm);
+        double x = 0.0;
+        for (int i = k + 1 + g; i < rows; i += G) x = fma(S[i * LDS + k], S[i * LDS + k], x);
+        for (int o = G >> 1; o > 0; o >>= 1) x += __shfl_xor_sync(gm, x, o);
+        const double alpha = S[k * LDS + k];
+        double tk = 0.0;
+        if (x > 0.0) {
+          const double beta = -copysign(sqrt(alpha * alpha + x), alpha);
+          tk = (beta - alpha) / beta;
+          const double scl = 1.0 / (alpha - beta);
+          for (int i = k + 1 + g; i < rows; i += G) S[i * LDS + k] *= scl;
+          __syncwarp(gm);
+          if (g == 0) S[k * LDS + k] = beta;
+        }
+        if (g == 0) tau_la[k] = tk;
+      }
     }
   }
 }
@@ -1021,6 +1091,127 @@ __global__ void __cluster_dims__(SRK_CL, 1, 1) __launch_bounds__(256)
   }
 }
 
+// Householder QR with the columns held in registers (rows <= 8 MAXR, cols <= 64):
+// one 8-lane group per column for the whole factorisation. Step j: the owner
+// of column j forms its reflector from its registers (dlarfg conventions:
+// beta = -sign(alpha) |x|, tau = 0 for a zero sub-column) and publishes v_j
+// and tau_j in shared memory; after one barrier every later column applies
+// H_j from its registers (one group reduction). The explicit Q needs no
+// barrier at all: group c applies H_c ... H_0 to e_c from the stored
+// reflectors. One barrier per column instead of the shared-matrix kernel's
+// serial reflector phase and two barriers (the m-side QRs are latency-bound).
+template <int MAXR>
+__global__ void __launch_bounds__(512)
+    qr_reg_kernel(const double* __restrict__ A, int rows, int cols, int lda,
+                  double* __restrict__ Q, int ldq, double* __restrict__ rfac) {
+  extern __shared__ double sm[];
+  const int kk = rows < cols ? rows : cols;
+  double* V = sm;                       // kk x rows: v_j below row j
+  double* tau = V + (size_t)kk * rows;  // kk
+  const int tid = threadIdx.x, lane = tid & 31, c = tid >> 3, l = tid & 7;
+  const unsigned gm = 0xffu << (lane & ~7);
+  const bool act = c < cols;
+  double x[MAXR];
+#pragma unroll
+  for (int u = 0; u < MAXR; ++u) {
+    const int i = l + 8 * u;
+    x[u] = (act && i < rows) ? A[(size_t)i + (size_t)c * lda] : 0.0;
+  }
+  for (int j = 0; j < kk; ++j) {
+    if (c == j) {
+      double s = 0.0, al = 0.0;
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int i = l + 8 * u;
+        if (i > j) s = fma(x[u], x[u], s);
+        if (i == j) al = x[u];
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(gm, s, o);
+        al += __shfl_xor_sync(gm, al, o);
+      }
+      double tj = 0.0;
+      if (s > 0.0) {
+        const double beta = -copysign(sqrt(al * al + s), al);
+        tj = (beta - al) / beta;
+        const double scl = 1.0 / (al - beta);
+#pragma unroll
+        for (int u = 0; u < MAXR; ++u) {
+          const int i = l + 8 * u;
+          if (i > j && i < rows) {
+            V[(size_t)j * rows + i] = x[u] * scl;
+            x[u] = 0.0;
+          }
+          if (i == j) x[u] = beta;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < MAXR; ++u) {
+          const int i = l + 8 * u;
+          if (i > j && i < rows) V[(size_t)j * rows + i] = 0.0;
+        }
+      }
+      if (l == 0) tau[j] = tj;
+    }
+    __syncthreads();
+    if (act && c > j) {
+      const double tj = tau[j];
+      if (tj != 0.0) {
+        double v[MAXR];
+        double w = 0.0;
+#pragma unroll
+        for (int u = 0; u < MAXR; ++u) {
+          const int i = l + 8 * u;
+          v[u] = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+          w = fma(v[u], x[u], w);
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
+        w *= tj;
+#pragma unroll
+        for (int u = 0; u < MAXR; ++u) x[u] -= w * v[u];
+      }
+    }
+  }
+  // triangular factor (kk x cols, row-major): column c is final after step c
+  if (act) {
+#pragma unroll
+    for (int u = 0; u < MAXR; ++u) {
+      const int i = l + 8 * u;
+      if (i < kk) rfac[(size_t)i * cols + c] = i <= c ? x[u] : 0.0;
+    }
+  }
+  __syncthreads();
+  // explicit Q (rows x kk): column c = H_0 ... H_c e_c (H_j e_c = e_c for j > c)
+  if (c < kk) {
+#pragma unroll
+    for (int u = 0; u < MAXR; ++u) x[u] = (l + 8 * u == c) ? 1.0 : 0.0;
+    for (int j = c; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      double v[MAXR];
+      double w = 0.0;
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) {
+        const int i = l + 8 * u;
+        v[u] = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+        w = fma(v[u], x[u], w);
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
+      w *= tj;
+#pragma unroll
+      for (int u = 0; u < MAXR; ++u) x[u] -= w * v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < MAXR; ++u) {
+      const int i = l + 8 * u;
+      if (i < rows) Q[(size_t)i + (size_t)c * ldq] = x[u];
+    }
+  }
+}
+
 // Householder QR of a whole (rows x cols) column-major matrix in one CTA
 // (the m-side factors: rows = m moments <= ~600): the matrix lives in shared
 // memory, the reflectors are those of hh_qr_kernel (beta = -sign(alpha) ||x||,
@@ -1045,8 +1236,9 @@ __global__ void __launch_bounds__(512)
   }
   __syncthreads();
   const int kk = rows < cols ? rows : cols;
-  for (int j = 0; j < kk; ++j) {
-    // the reflector of column j in one warp
+  for (int j = 0; j < kk && j < 1; ++j) {
+    // the reflector of column 0 in one warp; the later ones are formed by the
+    // column groups one step ahead (hh_apply_groups look-ahead)
     if (warp == 0) {
       double part = 0.0;
       for (int i = j + 1 + lane; i < rows; i += 32) part += S[i * LDS + j] * S[i * LDS + j];
@@ -1064,7 +1256,12 @@ __global__ void __launch_bounds__(512)
       if (lane == 0) tau[j] = tj;
     }
     __syncthreads();
-    if (tau[j] != 0.0) hh_apply_groups(S, LDS, rows, j, j + 1, cols, tau[j]);
+  }
+  for (int j = 0; j < kk; ++j) {
+    // H_j on the trailing columns; with a next reflector to form, the apply
+    // runs even for tau_j = 0 (w = 0) so the look-ahead group forms it
+    if (tau[j] != 0.0 || j + 1 < kk)
+      hh_apply_groups(S, LDS, rows, j, j + 1, cols, tau[j], j + 1 < kk ? tau : nullptr);
     __syncthreads();
   }
   // triangular factor (kk x cols, row-major)
@@ -1177,6 +1374,20 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
   {
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
+    if (rows <= 128 && cols <= 64 && !getenv("PND_QR_SHARED")) {
+      // columns in registers, one 8-lane group per column
+      const size_t smr = ((size_t)kc * rows + kc) * sizeof(double);
+      const int thr = ((8 * cols + 31) / 32) * 32;
+      if (rows <= 64) {
+        set_smem((const void*)qr_reg_kernel<8>, smr);
+        qr_reg_kernel<8><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+      } else {
+        set_smem((const void*)qr_reg_kernel<16>, smr);
+        qr_reg_kernel<16><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+      }
+      launched();
+      return kc;
+    }
     if (sm + 1024 <= (size_t)kMaxDynSmem) {
       // one 8-lane group per column up to 128 rows, 16 warps from a few hundred rows
       int thr = rows <= 128 ? 8 * cols : 512;  // one 8-lane group per column
@@ -1324,10 +1535,11 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
   if (threads < 64) threads = 64;
   if (threads > 1024) threads = 1024;
   if (M <= 64 && !getenv("PND_SVD_PLAIN")) {
-    const size_t smq = ((size_t)2 * M * N + (size_t)N * N2 + (size_t)N2 * N2 + (size_t)N * N +
+    const size_t smq = ((size_t)M * N + (size_t)N * N2 + (size_t)N2 * N2 + (size_t)N * N +
                         N + 2 * N2) * sizeof(double) + 2 * N * sizeof(int);
     // one 8-lane group per Jacobi pair; rows per lane = ceil(M / 8)
-    int thq = ((QJ_G * (N2 / 2) + 31) / 32) * 32;
+    // one 8-lane group per column in the QR, per Jacobi pair in the sweeps
+    int thq = ((QJ_G * (N > N2 / 2 ? N : N2 / 2) + 31) / 32) * 32;
     if (thq < 64) thq = 64;
     const int rpl = (M + QJ_G - 1) / QJ_G;
     auto kq = svd_qrj_kernel<8>;
@@ -1342,7 +1554,9 @@ void svd_small(const double* s, int p, int q, double* P, double* sig, double* Qt
       default: break;
     }
     set_smem((const void*)kq, smq);
-    kq<<<1, thq, smq, st>>>(s, p, q, P, sig, Qt);
+    // PND_SVD_STOP=1/2: stop after the QR / the Jacobi sweeps (phase timing only)
+    const char* stop = getenv("PND_SVD_STOP");
+    kq<<<1, thq, smq, st>>>(s, p, q, P, sig, Qt, stop ? atoi(stop) : 0);
   } else if (M <= 64) {
     set_smem((const void*)svd_kernel<2>, sm);
     svd_kernel<2><<<1, threads, sm, st>>>(s, p, q, P, sig, Qt, gw);

@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(LTH, 2)
     double v = 0.0;
     if (j < in.cols[q] && col < nb && !copy_y) {
       if (q == in.xq) v = -TB[(size_t)j * nb + col];
-      else v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
+      else if (!in.ident) v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
     }
     sB[i] = v;
   }
@@ -369,7 +369,29 @@ __global__ void __launch_bounds__(LTH, 2)
       double acc[NB8][2];
 #pragma unroll
       for (int nt = 0; nt < NB8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-      for (int q = 0; q < in.nin; ++q) {
+      if (in.ident) {
+        // TA = I: start from the Y rows (accumulator layout: row m, columns
+        // 2 kq, 2 kq + 1), Y2's after Y1's columns
+        const double* y = sb + in.off[0] + (warp * 8 + m) * in.rs[0];
+        const int c1 = in.cols[0];
+#pragma unroll
+        for (int nt = 0; nt < NB8; ++nt) {
+          const int col = nt * 8 + 2 * kq;
+          if (col < c1) acc[nt][0] = y[col];
+          if (col + 1 < c1) acc[nt][1] = y[col + 1];
+        }
+        if (in.ident == 2) {
+          const int c2 = in.cols[1];
+          const double* y2 = sb + in.off[1] + (warp * 8 + m) * in.rs[1];
+#pragma unroll
+          for (int nt = 0; nt < NB8; ++nt) {
+            const int col = nt * 8 + 2 * kq;
+            if (col >= c1 && col < c1 + c2) acc[nt][0] = y2[col - c1];
+            if (col + 1 >= c1 && col + 1 < c1 + c2) acc[nt][1] = y2[col + 1 - c1];
+          }
+        }
+      }
+      for (int q = in.ident; q < in.nin; ++q) {
         const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
         const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
 #pragma unroll 2
@@ -543,7 +565,11 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   constexpr int TS = lpad4(NB8 * 8);
   // per-warp Grams (lincomb_pw_kernel) while the registers allow
   constexpr bool PWOK = NB8 <= 3;
-  const bool PW = PWOK && gram_only;
+  // (Gram-only passes; for contractions that also form Grams the per-warp
+  // variant -- 0.4 operand loads per Gram DMMA instead of 2, no CTA barrier
+  // per chunk -- measured the same time at 256^3 r = 20, kept opt-in:
+  // PND_LINCOMB_PW_GRAMS=1)
+  const bool PW = PWOK && (gram_only || (grams != nullptr && getenv("PND_LINCOMB_PW_GRAMS")));
   int tb = 2;  // out-tile buffers
   size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
   size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);

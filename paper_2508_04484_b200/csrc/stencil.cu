@@ -298,7 +298,7 @@ __device__ __forceinline__ void reg_inc() {
 template <int NA, int RB, bool PRE, int KC, int KHR = 0>
 __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
     kstage_kernel(Geom g, NMat X, NMat U0, NMat out, const double* __restrict__ Bcat, int K,
-                  int K4, Seg S, int nstg, const double* __restrict__ isp, int oscale) {
+                  int K4, Seg S, int nstg, const double* __restrict__ isp, int oscale, int dbg) {
   constexpr int NTH = KHR > 0 ? RPTH : PTH;
   constexpr int NS = 2 * NA;
   constexpr int NT = RB / 8;
@@ -354,6 +354,14 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
       const double* Xs = sb + S.xoff[0];
       double* Fb = F0 + f * K4 * KCS;
       double* base = Fb + NS * xc * KCS;
+      if (dbg & 1) {  // profiling (PND_KSTAGE_DBG): formers skip the features
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&pb->ffull[f]);
+          mbar_arrive(&pb->sempty[r.s]);
+        }
+        continue;
+      }
       // base rows = unscaled centre rows (rows past n are zero halo rows; their
       // results are not stored)
       if (sepc) {
@@ -411,7 +419,7 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
         for (int nt = 0; nt < NT; ++nt) acc[h][nt][0] = acc[h][nt][1] = 0.0;
       double* Fb = F0 + b * K4 * KCS;
       const double* pa = Fb + (lane & 3) * KCS + mt * 8 + (lane >> 2);
-      int ks = ks0;
+      int ks = (dbg & 2) ? ks1 : ks0;  // profiling: no DMMA (PND_KSTAGE_DBG & 2)
       if constexpr (KHR > 0) {
         const double* pak = pa + ks0 * 4 * KCS;
 #pragma unroll
@@ -525,8 +533,9 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const int nchunks = (g.n + KC - 1) / KC;
   int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem);
   if (grid > nchunks) grid = nchunks;
+  const char* dbg = getenv("PND_KSTAGE_DBG");
   kstage_kernel<NA, RB, PRE, KC, KHR><<<grid, nth, smem, st>>>(
-      g, a.X, a.U0, a.out, B, K, K4, S, nstg, a.inv_s, a.out_scaled ? 1 : 0);
+      g, a.X, a.U0, a.out, B, K, K4, S, nstg, a.inv_s, a.out_scaled ? 1 : 0, dbg ? atoi(dbg) : 0);
   launched();
   return true;
 }
