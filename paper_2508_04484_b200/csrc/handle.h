@@ -154,7 +154,7 @@ void stencil_grams_blocks(Handle& h, const std::vector<NMat>& B, const double* i
 // mode 0 deflate, 1 re-orthogonalise, 2 deflated residuals, 3 level-2 scaled
 void cholqr_build(const double* G, const double* C, int a, int b, int mode, double tol2,
                   const double* dinv, double* TA, double* TB, int* info, double* d0out,
-                  DBuf& work, cudaStream_t st);
+                  DBuf& work, cudaStream_t st, const double* gate = nullptr);
 
 // ranks above 64 (xwide.cu): column-blocked storage, every product a chain
 // over 32-column blocks

@@ -41,6 +41,7 @@ struct Seg {
   int total;       // doubles staged
   unsigned bytes;  // bytes per chunk
   int cpp, nz;     // chunk order: cpp > 0 -> z-fastest (cpp chunks per z-plane)
+  int plus_only;   // D+ stencils only: the +1 / +2 segments of the y and z axes are not staged
 };
 
 // first cell of the p-th processed chunk. With whole chunks per z-plane the
@@ -55,8 +56,9 @@ __device__ __forceinline__ int chunk_cell(const Seg& S, int p, int ch) {
 }
 
 template <int CH>
-Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre) {
+Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool plus_only = false) {
   Seg s{};
+  s.plus_only = plus_only ? 1 : 0;
   s.nbox = 1;
   s.off[0] = -2;
   const int nxy = g.nx * g.ny;
@@ -68,16 +70,18 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre) {
   s.nrows = CH + 4 + (s.nbox - 1) * CH;
   int o = 0;
   unsigned bytes = 0;
+  // staged rows per input: all segments, or without the +1 / +2 ones (plus_only)
+  const int srows = plus_only ? CH + 4 + (s.nbox - 1) / 2 * CH : s.nrows;
   for (int k = 0; k < 2; ++k) {
     s.xoff[k] = o;
     if (k < nin) {
       o += up16(s.nrows * in[k].rs);
-      bytes += s.nrows * in[k].rs * 8;
+      bytes += srows * in[k].rs * 8;
     }
   }
   s.ioff = o;
   o += up16(2 * s.nrows);
-  bytes += 2 * s.nrows * 8;
+  bytes += 2 * srows * 8;
   s.coff = -1;
   if (centre) {
     s.coff = o;
@@ -103,6 +107,8 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
   mbar_expect_tx(bar, S.bytes);
 #pragma unroll
   for (int q = 0; q < 1 + 4 * (NA - 1); ++q) {
+    // D+ only (the one-material S-Grams): the +1 / +2 neighbours are never read
+    if (S.plus_only && q > 0 && ((q - 1) & 3) >= 2) continue;
     const int rows = q == 0 ? CH + 4 : CH;
     const long row = (long)c0 + S.off[q];
     const int drow = box_row<CH>(q);
@@ -890,7 +896,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   constexpr int GTL = pad4(GC);
   constexpr int NSF = PO ? NA : 2 * NA;
   const NMat ins[2] = {X1, X2};
-  const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr);
+  const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr, PO && !getenv("PND_SGRAM_ALLSEG"));
   const int W = T8 * 8;
   const size_t ft = (size_t)NSF * W * GTL + (size_t)GC * pad4(W);
   const size_t fixed = 2 * ft * sizeof(double) + sizeof(PipeBars);

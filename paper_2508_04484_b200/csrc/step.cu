@@ -172,7 +172,12 @@ __global__ void xnorm_kernel(const double* G2, const double* C1, int a, int b, d
 __global__ void __launch_bounds__(256)
     cholqr_kernel(const double* __restrict__ G, const double* __restrict__ C, int a, int b,
                   int mode, double tol2, const double* __restrict__ dinv, double* TA,
-                  double* TB, int* info, double* d0out, double* work, int in_smem) {
+                  double* TB, int* info, double* d0out, double* work, int in_smem,
+                  const double* __restrict__ gate) {
+  // gate (speculative steps): the re-orthogonalisation is not needed when the
+  // block's defect is within the 1e-12 trigger -- spec_select_kernel then
+  // supplies TA = I, TB = 0
+  if (gate && gate[0] <= 1e-12) return;
   extern __shared__ double sm[];
   double* A = in_smem ? sm : work;               // b x b working copy (R in its upper part)
   double* Ri = A + (size_t)b * b;                // k x k inverse of R
@@ -304,7 +309,7 @@ __global__ void __launch_bounds__(256)
 
 void cholqr_build(const double* G, const double* C, int a, int b, int mode, double tol2,
                   const double* dinv, double* TA, double* TB, int* info, double* d0out,
-                  DBuf& work, cudaStream_t st) {
+                  DBuf& work, cudaStream_t st, const double* gate) {
   if (b > 512) fail(PND_ECONFIG, "augmentation block wider than 512 columns");
   const size_t need = 2 * (size_t)b * b * sizeof(double);
   const bool in_smem = need + 8192 <= (size_t)kMaxDynSmem;
@@ -319,7 +324,7 @@ void cholqr_build(const double* G, const double* C, int a, int b, int mode, doub
     w = work.get(2 * (size_t)b * b);
   }
   cholqr_kernel<<<1, 256, in_smem ? need : 0, st>>>(G, C, a, b, mode, tol2, dinv, TA, TB, info,
-                                                   d0out, w, in_smem ? 1 : 0);
+                                                   d0out, w, in_smem ? 1 : 0, gate);
   launched();
 }
 
@@ -412,7 +417,7 @@ static int orth_complement_spec(Handle& h, NMat Y, NMat U0, int a, int b, int ra
   double* G3c = slot(h, S_M2, (size_t)k * k);
   CK(cudaMemcpyAsync(G3c, G3, sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
   if (a > 0) gemm(k, k, a, -1.0, tr(rowm(C3, k)), 0, rowm(C3, k), 0, 1.0, rowm(G3c, k), 0, 1, st);
-  cholqr_build(G3c, C3, a, k, 1, 0.0, nullptr, TA, TB, info + 1, nullptr, h.cq_work, st);
+  cholqr_build(G3c, C3, a, k, 1, 0.0, nullptr, TA, TB, info + 1, nullptr, h.cq_work, st, dinfo);
   spec_select_kernel<<<1, 256, 0, st>>>(dinfo, 1e-12, a, k, TA, TB);
   launched();
   NMat Q2 = h.Qa.view(g, k, st);
