@@ -895,6 +895,89 @@ __global__ void scat_solve_kernel(const double* B, const double* coeffs, const d
   for (int a = tid; a < r; a += nthr) lnew[a * m + q] = x[a];
 }
 
+// The same m implicit solves with one warp per system for r <= 32: lane i
+// holds row i of [I + dt sum_i c_i B_i | l] in registers; partial pivoting by
+// a warp argmax (first maximum, as above), row interchange and pivot-row
+// broadcast by shuffles, back substitution with the unknowns broadcast as they
+// are found. Same operations in the same order as scat_solve_kernel (whose
+// serial pivot search and back substitution on one thread were the cost).
+__global__ void __launch_bounds__(256)
+    scat_solve_warp_kernel(const double* B, const double* coeffs, const double* lcols, int r,
+                           int m, double dt, double* lnew, int* singular) {
+  const int lane = threadIdx.x & 31;
+  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (q >= m) return;  // whole warps
+  double row[32];
+  double cf[12];
+#pragma unroll
+  for (int t = 0; t < 12; ++t) cf[t] = coeffs[t * m + q];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    double v = 0.0;
+    if (lane < r && k < r) {
+      double s = 0.0;
+      for (int t = 0; t < 12; ++t) s += cf[t] * B[(size_t)t * r * r + lane * r + k];
+      v = (lane == k ? 1.0 : 0.0) + dt * s;
+    }
+    row[k] = v;
+  }
+  double xv = lane < r ? lcols[lane * m + q] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    if (j < r) {
+      // pivot: the first row i >= j with the largest |M[i][j]|
+      double best = (lane >= j && lane < r) ? fabs(row[j]) : -1.0;
+      int bi = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (best == 0.0) {
+        if (lane == 0) atomicMin(singular, q);
+        return;
+      }
+      if (bi != j) {
+        const int src = lane == j ? bi : lane == bi ? j : lane;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < r) row[k] = __shfl_sync(0xffffffffu, row[k], src);
+        xv = __shfl_sync(0xffffffffu, xv, src);
+      }
+      const double inv = 1.0 / __shfl_sync(0xffffffffu, row[j], j);
+      const double xj = __shfl_sync(0xffffffffu, xv, j);
+      const bool below = lane > j && lane < r;
+      const double l = row[j] * inv;
+      if (below) row[j] = l;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if (k > j && k < r) {
+          const double rjk = __shfl_sync(0xffffffffu, row[k], j);
+          if (below) row[k] -= l * rjk;
+        }
+      }
+      if (below) xv -= l * xj;
+    }
+  }
+  // back substitution, the unknowns broadcast as they are found
+  double xs[32];
+#pragma unroll
+  for (int i = 31; i >= 0; --i) {
+    if (i < r) {
+      double s = xv;
+#pragma unroll
+      for (int k = i + 1; k < 32; ++k)
+        if (k < r) s -= row[k] * xs[k];
+      const double xi = s / row[i];
+      xs[i] = __shfl_sync(0xffffffffu, xi, i);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 32; ++a)
+    if (a < r && lane == a) lnew[a * m + q] = xs[a];
+}
+
 // RK4 (Horner form) of S' = -sum_s G_s S F_s on the R x R coefficient matrix in
 // one CTA; with `staged` the Grams and moment factors are copied to shared
 // memory first (the products then read only shared memory), and every
@@ -1209,6 +1292,98 @@ __global__ void __launch_bounds__(512)
       const int i = l + 8 * u;
       if (i < rows) Q[(size_t)i + (size_t)c * ldq] = x[u];
     }
+  }
+}
+
+// The streaming substep's L phase on the moment side (dlra.py:176-194) for
+// small moment counts, fused over a cluster of LRK_CL CTAs: L0 = V0 S0^T, then
+// the Horner RK4 of L' = -sum_s A_s L Q_s (Q_s^T = the leading a x a block of
+// the S-phase Gram G_s): CTA c owns a block of rows, forms its rows of
+// Z_s = L Q_s^T (broadcast into every CTA's shared memory: A_s L needs all of
+// Z) and its rows of the next iterate (broadcast as well). Writes L1 (m x a
+// row-major) and BV = [L1 | V0] column-major, the next orthonormalisation's
+// input. Replaces ~20 small launches per step (GEMMs, split-K reductions,
+// copies, transposes) by one.
+constexpr int LRK_CL = 8;
+__global__ void __cluster_dims__(LRK_CL, 1, 1) __launch_bounds__(256)
+    l_rk4_cluster_kernel(const double* __restrict__ V, const double* __restrict__ S,
+                         const double* __restrict__ G, int ru, const double* __restrict__ amat,
+                         int m, int a, int b, int ns, double dt, double* __restrict__ L1,
+                         double* __restrict__ BV) {
+  extern __shared__ double sm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int cr = (int)cl.block_rank();
+  const int per = (m + LRK_CL - 1) / LRK_CL;
+  const int r0 = cr * per;
+  const int nr = r0 < m ? (m - r0 < per ? m - r0 : per) : 0;
+  const int ma = m * a;
+  double* LW0 = sm;                          // m x a (all rows), double-buffered
+  double* LW1 = LW0 + ma;
+  double* Z = LW1 + ma;                      // ns x m x a
+  double* Ar = Z + (size_t)ns * ma;          // ns x per x m: own rows of every A_s
+  double* Gs = Ar + (size_t)ns * per * m;    // ns x a x a: Q_s^T blocks
+  double* L0r = Gs + (size_t)ns * a * a;     // per x a
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int i = tid; i < ns * nr * m; i += nthr) {
+    const int s = i / (nr * m), rem = i - s * nr * m, r = rem / m, p = rem - r * m;
+    Ar[(s * per + r) * m + p] = amat[((size_t)s * m + r0 + r) * m + p];
+  }
+  for (int i = tid; i < ns * a * a; i += nthr) {
+    const int s = i / (a * a), rem = i - s * a * a, j = rem / a, k = rem - j * a;
+    Gs[i] = G[(size_t)s * ru * ru + (size_t)j * ru + k];
+  }
+  // L0 = V S^T, own rows; broadcast as the first iterate
+  for (int i = tid; i < nr * a; i += nthr) {
+    const int r = i / a, j = i - r * a;
+    double acc = 0.0;
+    for (int k = 0; k < b; ++k) acc = fma(V[(size_t)(r0 + r) * b + k], S[(size_t)j * b + k], acc);
+    L0r[i] = acc;
+    for (int rr = 0; rr < LRK_CL; ++rr) cl.map_shared_rank(LW0, rr)[(r0 + r) * a + j] = acc;
+  }
+  // V0 into BV's last b columns (column-major)
+  for (int i = tid; i < nr * b; i += nthr) {
+    const int r = i / b, k = i - r * b;
+    BV[(size_t)a * m + (size_t)k * m + r0 + r] = V[(size_t)(r0 + r) * b + k];
+  }
+  cl.sync();
+  const double coef[4] = {0.25, 1.0 / 3.0, 0.5, 1.0};
+  for (int st = 0; st < 4; ++st) {
+    const double* W = (st & 1) ? LW1 : LW0;
+    double* Wn = (st & 1) ? LW0 : LW1;
+    // Z_s rows: Z_s[r][j] = sum_i W[r][i] Q_s^T[j][i]
+    for (int i = tid; i < ns * nr * a; i += nthr) {
+      const int s = i / (nr * a), rem = i - s * nr * a, r = rem / a, j = rem - r * a;
+      const double* w = W + (r0 + r) * a;
+      const double* g = Gs + (s * a + j) * a;
+      double acc = 0.0;
+      for (int k = 0; k < a; ++k) acc = fma(w[k], g[k], acc);
+      for (int rr = 0; rr < LRK_CL; ++rr)
+        cl.map_shared_rank(Z, rr)[(size_t)s * ma + (r0 + r) * a + j] = acc;
+    }
+    cl.sync();  // every row of every Z_s in every CTA
+    const double c = -coef[st] * dt;
+    for (int i = tid; i < nr * a; i += nthr) {
+      const int r = i / a, j = i - r * a;
+      double t0 = 0.0, t1 = 0.0;
+      for (int s = 0; s < ns; ++s) {
+        const double* ar = Ar + (s * per + r) * m;
+        const double* z = Z + (size_t)s * ma + j;
+        int p = 0;
+        for (; p + 1 < m; p += 2) {
+          t0 = fma(ar[p], z[p * a], t0);
+          t1 = fma(ar[p + 1], z[(p + 1) * a], t1);
+        }
+        if (p < m) t0 = fma(ar[p], z[p * a], t0);
+      }
+      const double v = fma(c, t0 + t1, L0r[i]);
+      if (st < 3) {
+        for (int rr = 0; rr < LRK_CL; ++rr) cl.map_shared_rank(Wn, rr)[(r0 + r) * a + j] = v;
+      } else {
+        L1[(size_t)(r0 + r) * a + j] = v;
+        BV[(size_t)j * m + r0 + r] = v;
+      }
+    }
+    if (st < 3) cl.sync();  // the next iterate complete (and Z free) in every CTA
   }
 }
 
@@ -1592,9 +1767,28 @@ void scat_solves(const double* B, const double* coeffs, const double* lcols, int
     CK(cudaFreeAsync(gw, st));
     return;
   }
+  if (r <= 32 && !getenv("PND_SCAT_SOLVE_CTA")) {
+    scat_solve_warp_kernel<<<(m + 7) / 8, 256, 0, st>>>(B, coeffs, lcols, r, m, dt, lnew,
+                                                          singular);
+    launched();
+    return;
+  }
   set_smem((const void*)scat_solve_kernel, sm);
   scat_solve_kernel<<<m, 64, sm, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular, nullptr);
   launched();
+}
+
+bool l_rk4(const double* V, const double* S, const double* G, int ru, const double* amat, int m,
+           int a, int b, int ns, double dt, double* L1, double* BV, cudaStream_t st) {
+  if (getenv("PND_LRK4_GEMM")) return false;
+  const int per = (m + LRK_CL - 1) / LRK_CL;
+  const size_t smem = (2 * (size_t)m * a + (size_t)ns * m * a + (size_t)ns * per * m +
+                       (size_t)ns * a * a + (size_t)per * a) * sizeof(double);
+  if (smem + 1024 > (size_t)kMaxDynSmem) return false;
+  set_smem((const void*)l_rk4_cluster_kernel, smem);
+  l_rk4_cluster_kernel<<<LRK_CL, 256, smem, st>>>(V, S, G, ru, amat, m, a, b, ns, dt, L1, BV);
+  launched();
+  return true;
 }
 
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt, double*,

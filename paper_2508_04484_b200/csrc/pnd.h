@@ -268,6 +268,11 @@ void scat_solves(const double* B /* 12 x r x r */, const double* coeffs /* 12 x 
                  const double* lcols /* r x m */, int r, int m, double dt, double* lnew /* r x m */,
                  int* singular_col, cudaStream_t st);
 
+// L-phase RK4 of the streaming substep, fused (one cluster launch) when the
+// moment count is small: L1 (m x a row-major) and BV = [L1 | V] column-major;
+// false = not applicable (the GEMM path is used)
+bool l_rk4(const double* V, const double* S, const double* G, int ru, const double* amat, int m,
+           int a, int b, int ns, double dt, double* L1, double* BV, cudaStream_t st);
 // S-phase RK4 on an (p x q) matrix: S' = -sum_s G_s S F_s (G: p x p, F: q x q)
 void s_rk4(double* S, int p, int q, const double* G, const double* F, int ns, double dt,
            double* work, cudaStream_t st);

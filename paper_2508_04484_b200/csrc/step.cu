@@ -625,12 +625,14 @@ void streaming_step(Handle& h, double dt) {
   // --- L phase: L' = -sum_s A_s L Q_s, Q_s^T = G_s[:a, :a], L0 = V0 S0^T
   phase(h, PH_LSIDE);
   const int cols = a + b;
+  double* BV = slot(h, S_BV, (size_t)m * cols);
+  if (!l_rk4(h.V.p, h.S.p, G, ru, h.amat.p, m, a, b, ns, dt, slot(h, S_M2, (size_t)m * a), BV,
+             st)) {
   double* L0 = slot(h, S_L0, (size_t)m * a);
   double* LW = slot(h, S_LW, (size_t)m * a);
   double* Z = slot(h, S_ZST, (size_t)ns * m * a);
   gemm(m, a, b, 1.0, rowm(h.V.p, b), 0, tr(rowm(h.S.p, b)), 0, 0.0, rowm(L0, a), 0, 1, st);
   CK(cudaMemcpyAsync(LW, L0, sizeof(double) * m * a, cudaMemcpyDeviceToDevice, st));
-  double* BV = slot(h, S_BV, (size_t)m * cols);
   for (int stage = 0; stage < 4; ++stage) {
     gemm(m, a, a, 1.0, rowm(LW, a), 0, tr(rowm(G, ru)), (long)ru * ru, 0.0, rowm(Z, a),
          (long)m * a, ns, st);
@@ -642,6 +644,7 @@ void streaming_step(Handle& h, double dt) {
     if (stage == 3) transpose_in(dst, m, a, BV, m, st);
   }
   transpose_in(h.V.p, m, b, BV + (size_t)a * m, m, st);
+  }
 
   // --- V augmentation: V^ = orth([L1, V0])
   double* Vhc = slot(h, S_VHC, (size_t)m * cols);
