@@ -145,8 +145,11 @@ struct KStageArgs {
   DBuf* bcat = nullptr;     // per-handle scratch for the fragment-ordered [M; S0]
   bool in_scaled = false;   // X holds S^-1 x (the Horner intermediates)
   bool out_scaled = false;  // store S^-1 out instead of out
+  int zpart = 0;            // 0: all cells; 1: planes 2 .. nz-3; 2: planes 0, 1, nz-2, nz-1
 };
 void kstage(const KStageArgs& a, cudaStream_t st);
+// the plane split of kstage applies (whole chunks per plane, nz >= 5)
+bool kstage_can_split(const Geom& g);
 
 // stencil Grams: out[s] = [X1 | X2]^T D_s S^-1 [X1 | X2]  (ns x w x w, w = X1.cols + X2.cols)
 void stencil_grams(const Geom& g, NMat X1, NMat X2, const double* inv_s, double* out,

@@ -42,6 +42,9 @@ struct Seg {
   unsigned bytes;  // bytes per chunk
   int cpp, nz;     // chunk order: cpp > 0 -> z-fastest (cpp chunks per z-plane)
   int plus_only;   // D+ stencils only: the +1 / +2 segments of the y and z axes are not staged
+  // the planes a launch covers (cpp > 0): zlo .. zlo + nzr - 1, or with zb the
+  // four boundary planes 0, 1, nz - 2, nz - 1; nchunks = nzr * cpp (all: nz planes)
+  int zlo, nzr, zb, nchunks;
 };
 
 // first cell of the p-th processed chunk. With whole chunks per z-plane the
@@ -51,7 +54,8 @@ struct Seg {
 // 2 planes apart in time (which falls out of L2 at 256^3).
 __device__ __forceinline__ int chunk_cell(const Seg& S, int p, int ch) {
   if (S.cpp == 0) return p * ch;
-  const int zq = p % S.nz, r = p / S.nz;
+  const int zi = p % S.nzr, r = p / S.nzr;
+  const int zq = S.zb ? (zi < 2 ? zi : S.nz - 4 + zi) : S.zlo + zi;
   return (zq * S.cpp + r) * ch;
 }
 
@@ -92,6 +96,10 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool pl
   s.bytes = bytes;
   s.cpp = (nxy % CH == 0 && g.nz > 1) ? nxy / CH : 0;
   s.nz = g.nz;
+  s.zlo = 0;
+  s.nzr = g.nz;
+  s.zb = 0;
+  s.nchunks = (g.n + CH - 1) / CH;
   return s;
 }
 
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
   }
   __syncthreads();
   const bool sepc = S.coff >= 0;
-  const int nchunks = (g.n + KC - 1) / KC;
+  const int nchunks = S.nchunks;
 
   if (warp >= FORMW + CONW) {
     if constexpr (KHR > 0) reg_dec<REG_PROD>();
@@ -528,7 +536,16 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
   const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
-  const Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
+  Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
+  if (a.zpart) {
+    // interior planes (no halo row read) / the four boundary planes: the
+    // halo exchange of X overlaps the interior launch (streaming_step)
+    if (S.cpp == 0 || g.nz < 5) fail(PND_ECONFIG, "kstage: plane split needs whole chunks per plane");
+    S.zlo = a.zpart == 1 ? 2 : 0;
+    S.nzr = a.zpart == 1 ? g.nz - 4 : 4;
+    S.zb = a.zpart == 2 ? 1 : 0;
+    S.nchunks = S.nzr * S.cpp;
+  }
   const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (size_t)K4 * RB) * sizeof(double) +
                        sizeof(PipeBars);
   const int nstg = stages_for(fixed, S.total);
@@ -536,7 +553,7 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
   constexpr int nth = KHR > 0 ? RPTH : PTH;
   allow_max_smem(kstage_kernel<NA, RB, PRE, KC, KHR>);
-  const int nchunks = (g.n + KC - 1) / KC;
+  const int nchunks = S.nchunks;
   int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem);
   if (grid > nchunks) grid = nchunks;
   const char* dbg = getenv("PND_KSTAGE_DBG");
@@ -620,7 +637,7 @@ __global__ void __launch_bounds__(gpth(T8), 1)
   pipe_init(pb, nstg, GCONW);
   for (int i = tid; i < 2 * FT; i += GPTH) F0[i] = 0.0;
   __syncthreads();
-  const int nchunks = (g.n + GC - 1) / GC;
+  const int nchunks = S.nchunks;
 
   if (warp == FORMW + GCONW) {
     if (lane == 0) {
@@ -768,7 +785,7 @@ __global__ void __launch_bounds__(gpth(T8B), 1)
   pipe_init(pb, nstg, GCONW);
   for (int i = tid; i < 2 * FT; i += GPTH) F0[i] = 0.0;
   __syncthreads();
-  const int nchunks = (g.n + GC - 1) / GC;
+  const int nchunks = S.nchunks;
 
   if (warp == FORMW + GCONW) {
     if (lane == 0) {
@@ -1004,6 +1021,11 @@ void sgram_na(const Geom& g, NMat X1, NMat X2, const double* isp, double* out, D
 
 
 }  // namespace
+
+bool kstage_can_split(const Geom& g) {
+  // whole 32- and 16-cell chunks per plane, an interior to overlap
+  return g.nz >= 5 && ((size_t)g.nx * g.ny) % 32 == 0 && g.axis[g.na - 1] == 2;
+}
 
 void kstage(const KStageArgs& a, cudaStream_t st) {
   if (!a.bcat) fail(PND_ECONFIG, "kstage: no [M; S0] scratch buffer");

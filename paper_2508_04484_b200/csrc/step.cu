@@ -521,6 +521,23 @@ int orth_complement(Handle& h, NMat X, const double* C1, NMat X2, int rank_bound
   return k;
 }
 
+// One K stage with the halo exchange of its input overlapped: the exchange
+// (NCCL send/recv of the two boundary planes each way) runs on the side
+// stream while the planes 2 .. nz-3 are computed; the four boundary planes
+// follow once it has landed. The split is over whole chunks, so the result is
+// the unsplit launch's, bit for bit.
+static void kstage_overlapped(Handle& h, KStageArgs ka, cudaStream_t st) {
+  CK(cudaEventRecord(h.ev_fork, st));
+  CK(cudaStreamWaitEvent(h.st2, h.ev_fork, 0));
+  comm_halo_rows(h.g, ka.X.p, ka.X.rs, h.st2);
+  CK(cudaEventRecord(h.ev_join, h.st2));
+  ka.zpart = 1;
+  kstage(ka, st);
+  CK(cudaStreamWaitEvent(st, h.ev_join, 0));
+  ka.zpart = 2;
+  kstage(ka, st);
+}
+
 void streaming_step(Handle& h, double dt) {
   h.singular_pending = false;
   if (!h.stencil_error.empty()) fail(PND_ECONFIG, h.stencil_error);
@@ -535,9 +552,13 @@ void streaming_step(Handle& h, double dt) {
   cudaStream_t st = h.st;
   const NMat U0 = state_u(h);
   const double* isp = isp_rows(h);
-  comm_halo_rows(g, U0.p, U0.rs, st);  // U0's neighbour planes (K stage 0, L- and S-Grams)
   // ranks above 32: the stencil kernels run on 32-column blocks (wide.cu)
   const bool wide = a > 32 || b > 32;
+  // z-slabs: overlap each K stage's halo exchange with its interior planes
+  const bool split =
+      !wide && kstage_can_split(g) && (comm_world(g) > 1 || getenv("PND_KSTAGE_SPLIT"));
+  // U0's neighbour planes (K stage 0, L- and S-Grams): with the split, inside K stage 0
+  if (!split) comm_halo_rows(g, U0.p, U0.rs, st);
   std::vector<NMat> u0b, w1b, w2b;
   if (wide) {
     u0b = split_blocks(h, U0, h.wide_u0b);
@@ -585,6 +606,10 @@ void streaming_step(Handle& h, double dt) {
       // the same buffer rotation as below: U0 -> W1 -> W2 -> W1 -> W2
       kstage_blocks(h, xin, ka.U0, h.S.p, M, stage == 0 || stage == 2 ? w1b : w2b,
                     ka.in_scaled, ka.out_scaled);
+    } else if (split) {
+      // the input's boundary planes go to the neighbours (side stream) while
+      // the interior planes -- which read no halo row -- run
+      kstage_overlapped(h, ka, st);
     } else {
       if (stage > 0) comm_halo_rows(g, ka.X.p, ka.X.rs, st);  // the previous stage's output
       kstage(ka, st);

@@ -119,3 +119,23 @@ def test_slab_solve_blocked_rank_and_footprint_flux():
         assert p.rank_history[-1][2] == 70
     ref = full.dose.deposited
     assert np.linalg.norm(dep - ref) / np.linalg.norm(ref) < 1e-10
+
+
+def test_kstage_plane_split_is_bit_identical():
+    """The K stage split into interior planes and the four boundary planes
+    (overlapping a slab's halo exchange with the interior, streaming_step)
+    computes every chunk exactly as the single launch does."""
+    import os
+
+    from paper_2508_04484_b200.driver import run_bundle
+    from paper_2508_04484_b200.problem import ProblemBundle
+
+    b = ProblemBundle.load(GOLDEN / "bundle_smoke.npz")
+    one = run_bundle(b)
+    os.environ["PND_KSTAGE_SPLIT"] = "1"
+    try:
+        split = run_bundle(b)
+    finally:
+        os.environ.pop("PND_KSTAGE_SPLIT", None)
+    np.testing.assert_array_equal(split.dose.deposited, one.dose.deposited)
+    assert [r for _, _, r in split.rank_history] == [r for _, _, r in one.rank_history]
