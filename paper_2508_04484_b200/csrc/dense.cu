@@ -1183,21 +1183,25 @@ __global__ void __cluster_dims__(SRK_CL, 1, 1) __launch_bounds__(256)
 // barrier at all: group c applies H_c ... H_0 to e_c from the stored
 // reflectors. One barrier per column instead of the shared-matrix kernel's
 // serial reflector phase and two barriers (the m-side QRs are latency-bound).
-template <int MAXR>
-__global__ void __launch_bounds__(512)
+template <int G, int MAXR>
+__global__ void __launch_bounds__(G == 8 ? 512 : 640)
     qr_reg_kernel(const double* __restrict__ A, int rows, int cols, int lda,
                   double* __restrict__ Q, int ldq, double* __restrict__ rfac) {
+  // G lanes per column (8 up to 128 rows, 16 for the P19 moment count, 400
+  // rows); with G = 16 the reflector is re-read from shared memory instead of
+  // being held twice in registers
+  constexpr bool VREG = MAXR <= 16;
   extern __shared__ double sm[];
   const int kk = rows < cols ? rows : cols;
   double* V = sm;                       // kk x rows: v_j below row j
   double* tau = V + (size_t)kk * rows;  // kk
-  const int tid = threadIdx.x, lane = tid & 31, c = tid >> 3, l = tid & 7;
-  const unsigned gm = 0xffu << (lane & ~7);
+  const int tid = threadIdx.x, lane = tid & 31, c = tid / G, l = tid % G;
+  const unsigned gm = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
   const bool act = c < cols;
   double x[MAXR];
 #pragma unroll
   for (int u = 0; u < MAXR; ++u) {
-    const int i = l + 8 * u;
+    const int i = l + G * u;
     x[u] = (act && i < rows) ? A[(size_t)i + (size_t)c * lda] : 0.0;
   }
   for (int j = 0; j < kk; ++j) {
@@ -1205,12 +1209,12 @@ __global__ void __launch_bounds__(512)
       double s = 0.0, al = 0.0;
 #pragma unroll
       for (int u = 0; u < MAXR; ++u) {
-        const int i = l + 8 * u;
+        const int i = l + G * u;
         if (i > j) s = fma(x[u], x[u], s);
         if (i == j) al = x[u];
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
+      for (int o = G / 2; o > 0; o >>= 1) {
         s += __shfl_xor_sync(gm, s, o);
         al += __shfl_xor_sync(gm, al, o);
       }
@@ -1221,7 +1225,7 @@ __global__ void __launch_bounds__(512)
         const double scl = 1.0 / (al - beta);
 #pragma unroll
         for (int u = 0; u < MAXR; ++u) {
-          const int i = l + 8 * u;
+          const int i = l + G * u;
           if (i > j && i < rows) {
             V[(size_t)j * rows + i] = x[u] * scl;
             x[u] = 0.0;
@@ -1231,7 +1235,7 @@ __global__ void __launch_bounds__(512)
       } else {
 #pragma unroll
         for (int u = 0; u < MAXR; ++u) {
-          const int i = l + 8 * u;
+          const int i = l + G * u;
           if (i > j && i < rows) V[(size_t)j * rows + i] = 0.0;
         }
       }
@@ -1241,19 +1245,29 @@ __global__ void __launch_bounds__(512)
     if (act && c > j) {
       const double tj = tau[j];
       if (tj != 0.0) {
-        double v[MAXR];
+        double v[VREG ? MAXR : 1];
         double w = 0.0;
 #pragma unroll
         for (int u = 0; u < MAXR; ++u) {
-          const int i = l + 8 * u;
-          v[u] = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
-          w = fma(v[u], x[u], w);
+          const int i = l + G * u;
+          const double vi = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+          if constexpr (VREG) v[u] = vi;
+          w = fma(vi, x[u], w);
         }
 #pragma unroll
-        for (int o = 4; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
+        for (int o = G / 2; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
         w *= tj;
 #pragma unroll
-        for (int u = 0; u < MAXR; ++u) x[u] -= w * v[u];
+        for (int u = 0; u < MAXR; ++u) {
+          double vi;
+          if constexpr (VREG) {
+            vi = v[u];
+          } else {
+            const int i = l + G * u;
+            vi = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+          }
+          x[u] -= w * vi;
+        }
       }
     }
   }
@@ -1261,7 +1275,7 @@ __global__ void __launch_bounds__(512)
   if (act) {
 #pragma unroll
     for (int u = 0; u < MAXR; ++u) {
-      const int i = l + 8 * u;
+      const int i = l + G * u;
       if (i < kk) rfac[(size_t)i * cols + c] = i <= c ? x[u] : 0.0;
     }
   }
@@ -1269,27 +1283,37 @@ __global__ void __launch_bounds__(512)
   // explicit Q (rows x kk): column c = H_0 ... H_c e_c (H_j e_c = e_c for j > c)
   if (c < kk) {
 #pragma unroll
-    for (int u = 0; u < MAXR; ++u) x[u] = (l + 8 * u == c) ? 1.0 : 0.0;
+    for (int u = 0; u < MAXR; ++u) x[u] = (l + G * u == c) ? 1.0 : 0.0;
     for (int j = c; j >= 0; --j) {
       const double tj = tau[j];
       if (tj == 0.0) continue;
-      double v[MAXR];
+      double v[VREG ? MAXR : 1];
       double w = 0.0;
 #pragma unroll
       for (int u = 0; u < MAXR; ++u) {
-        const int i = l + 8 * u;
-        v[u] = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
-        w = fma(v[u], x[u], w);
+        const int i = l + G * u;
+        const double vi = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+        if constexpr (VREG) v[u] = vi;
+        w = fma(vi, x[u], w);
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
+      for (int o = G / 2; o > 0; o >>= 1) w += __shfl_xor_sync(gm, w, o);
       w *= tj;
 #pragma unroll
-      for (int u = 0; u < MAXR; ++u) x[u] -= w * v[u];
+      for (int u = 0; u < MAXR; ++u) {
+        double vi;
+        if constexpr (VREG) {
+          vi = v[u];
+        } else {
+          const int i = l + G * u;
+          vi = i == j ? 1.0 : (i > j && i < rows) ? V[(size_t)j * rows + i] : 0.0;
+        }
+        x[u] -= w * vi;
+      }
     }
 #pragma unroll
     for (int u = 0; u < MAXR; ++u) {
-      const int i = l + 8 * u;
+      const int i = l + G * u;
       if (i < rows) Q[(size_t)i + (size_t)c * ldq] = x[u];
     }
   }
@@ -1549,16 +1573,24 @@ int tsqr(double* a, int rows, int cols, int lda, double* q, int ldq, double* rfa
   {
     // whole matrix in one CTA when it fits (the m-side QRs)
     const size_t sm = ((size_t)rows * (cols | 1) + 32 + 2 * (size_t)cols) * sizeof(double);
-    if (rows <= 128 && cols <= 64 && !getenv("PND_QR_SHARED")) {
-      // columns in registers, one 8-lane group per column
-      const size_t smr = ((size_t)kc * rows + kc) * sizeof(double);
-      const int thr = ((8 * cols + 31) / 32) * 32;
-      if (rows <= 64) {
-        set_smem((const void*)qr_reg_kernel<8>, smr);
-        qr_reg_kernel<8><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+    const size_t smr = ((size_t)kc * rows + kc) * sizeof(double);
+    if (!getenv("PND_QR_SHARED") && smr + 1024 <= (size_t)kMaxDynSmem &&
+        ((rows <= 128 && cols <= 64) || (rows <= 416 && cols <= 40))) {
+      // columns in registers: one 8-lane group per column up to 128 rows, 16 lanes
+      // up to 416 (the P19 moment count)
+      if (rows <= 128) {
+        const int thr = ((8 * cols + 31) / 32) * 32;
+        if (rows <= 64) {
+          set_smem((const void*)qr_reg_kernel<8, 8>, smr);
+          qr_reg_kernel<8, 8><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+        } else {
+          set_smem((const void*)qr_reg_kernel<8, 16>, smr);
+          qr_reg_kernel<8, 16><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+        }
       } else {
-        set_smem((const void*)qr_reg_kernel<16>, smr);
-        qr_reg_kernel<16><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
+        const int thr = ((16 * cols + 31) / 32) * 32;
+        set_smem((const void*)qr_reg_kernel<16, 26>, smr);
+        qr_reg_kernel<16, 26><<<1, thr, smr, st>>>(a, rows, cols, lda, q, ldq, rfac);
       }
       launched();
       return kc;
