@@ -445,8 +445,9 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
         }
         ks = ks1;
       }
-#pragma unroll 2
-      for (; ks + 1 < ks1; ks += 2) {
+      if (ks + 1 < ks1) {
+        // software-pipelined: the next k-step pair's fragments are loaded
+        // before this pair's DMMAs issue (the loads were the DMMAs' wait)
         double av[2], bv[2][NT];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -454,10 +455,28 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) bv[h][nt] = pb0[((ks + h) * NT + nt) * 32];
         }
+        for (; ks + 1 < ks1; ks += 2) {
+          double an[2], bn[2][NT];
+          const bool more = ks + 3 < ks1;
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+          for (int h = 0; h < 2; ++h) {
+            an[h] = more ? pa[(ks + 2 + h) * 4 * KCS] : 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[h][nt][0], acc[h][nt][1], av[h], bv[h][nt]);
+            for (int nt = 0; nt < NT; ++nt)
+              bn[h][nt] = more ? pb0[((ks + 2 + h) * NT + nt) * 32] : 0.0;
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              dmma884(acc[h][nt][0], acc[h][nt][1], av[h], bv[h][nt]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            av[h] = an[h];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) bv[h][nt] = bn[h][nt];
+          }
+        }
       }
       if (ks < ks1) {
         const double a0 = pa[ks * 4 * KCS];
@@ -719,19 +738,55 @@ __global__ void __launch_bounds__(gpth(T8), 1)
       mbar_wait(&pb->ffull[b], u & 1);
       const double* pa = F0 + b * FT + NS * W * GTL + kq * XS + m0;
       const double* pbt = F0 + b * FT + ((bt0 + m) * 8 + m0) * GTL + kq;
+      // software-pipelined over the chunk's GC / 4 k-steps (while the
+      // registers allow: UPW T8 <= 10 accumulator tiles): the next k-step's
+      // fragments are loaded before this one's DMMAs issue
+      if constexpr (UPW * T8 > 10) {
 #pragma unroll 1
-      for (int k0 = 0; k0 < GC; k0 += 4) {
-        double af[T8];
+        for (int k0 = 0; k0 < GC; k0 += 4) {
+          double af[T8];
 #pragma unroll
-        for (int ti = 0; ti < T8; ++ti) af[ti] = pa[k0 * XS + ti * 8];
+          for (int ti = 0; ti < T8; ++ti) af[ti] = pa[k0 * XS + ti * 8];
+#pragma unroll
+          for (int q = 0; q < UPW; ++q) {
+            if (m + GCONW * q < nbt) {
+              const double bf = pbt[q * GCONW * 8 * GTL + k0];
+#pragma unroll
+              for (int ti = 0; ti < T8; ++ti) dmma884(acc[q][ti][0], acc[q][ti][1], af[ti], bf);
+            }
+          }
+        }
+      } else {
+      double af[T8], bf[UPW];
+#pragma unroll
+      for (int ti = 0; ti < T8; ++ti) af[ti] = pa[ti * 8];
+#pragma unroll
+      for (int q = 0; q < UPW; ++q)
+        bf[q] = m + GCONW * q < nbt ? pbt[q * GCONW * 8 * GTL] : 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < GC; k0 += 4) {
+        double an[T8], bn[UPW];
+        if (k0 + 4 < GC) {
+#pragma unroll
+          for (int ti = 0; ti < T8; ++ti) an[ti] = pa[(k0 + 4) * XS + ti * 8];
+#pragma unroll
+          for (int q = 0; q < UPW; ++q)
+            bn[q] = m + GCONW * q < nbt ? pbt[q * GCONW * 8 * GTL + k0 + 4] : 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < UPW; ++q) {
           if (m + GCONW * q < nbt) {
-            const double bf = pbt[q * GCONW * 8 * GTL + k0];
 #pragma unroll
-            for (int ti = 0; ti < T8; ++ti) dmma884(acc[q][ti][0], acc[q][ti][1], af[ti], bf);
+            for (int ti = 0; ti < T8; ++ti) dmma884(acc[q][ti][0], acc[q][ti][1], af[ti], bf[q]);
           }
         }
+        if (k0 + 4 < GC) {
+#pragma unroll
+          for (int ti = 0; ti < T8; ++ti) af[ti] = an[ti];
+#pragma unroll
+          for (int q = 0; q < UPW; ++q) bf[q] = bn[q];
+        }
+      }
       }
       warp_arrive(&pb->fempty[b]);
     }
