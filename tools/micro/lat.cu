@@ -34,6 +34,33 @@ __global__ void lat(double* out, double seed, int n) {
   if (threadIdx.x == 0) out[0] = r;
 }
 
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// DMMA m8n8k4: dependent-chain latency (one chain) and issue interval with
+// NC independent chains per warp, W warps per SM sub-partition
+template <int NC>
+__global__ void dmma_lat(double* out, int n) {
+  double c[NC][2];
+  for (int k = 0; k < NC; ++k) c[k][0] = c[k][1] = threadIdx.x * 1e-9;
+  const double a = 1.0000001, b = 0.9999999;
+  __syncthreads();
+  const long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) dmma(c[k][0], c[k][1], a, b);
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0)
+    printf("dmma NC=%2d warps=%2d: %6.1f cycles per DMMA per warp (%6.1f per chain step)\n", NC,
+           blockDim.x / 32, (double)(t1 - t0) / (n * NC), (double)(t1 - t0) / n);
+  double s = 0;
+  for (int k = 0; k < NC; ++k) s += c[k][0] + c[k][1];
+  out[threadIdx.x] = s;
+}
+
 int main() {
   double* d;
   cudaMalloc(&d, 8);
@@ -43,5 +70,17 @@ int main() {
   cudaDeviceSynchronize();
   lat<<<1, 640>>>(d, 0.5, 1000);
   cudaDeviceSynchronize();
+  double* o;
+  cudaMalloc(&o, 1024 * 8);
+  for (int w : {1, 4, 8, 16}) {
+    dmma_lat<1><<<1, 32 * w>>>(o, 1000);
+    cudaDeviceSynchronize();
+    dmma_lat<3><<<1, 32 * w>>>(o, 1000);
+    cudaDeviceSynchronize();
+    dmma_lat<6><<<1, 32 * w>>>(o, 1000);
+    cudaDeviceSynchronize();
+    dmma_lat<12><<<1, 32 * w>>>(o, 1000);
+    cudaDeviceSynchronize();
+  }
   return 0;
 }
