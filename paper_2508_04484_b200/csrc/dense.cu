@@ -895,89 +895,6 @@ __global__ void scat_solve_kernel(const double* B, const double* coeffs, const d
   for (int a = tid; a < r; a += nthr) lnew[a * m + q] = x[a];
 }
 
-// The same m implicit solves with one warp per system for r <= 32: lane i
-// holds row i of [I + dt sum_i c_i B_i | l] in registers; partial pivoting by
-// a warp argmax (first maximum, as above), row interchange and pivot-row
-// broadcast by shuffles, back substitution with the unknowns broadcast as they
-// are found. Same operations in the same order as scat_solve_kernel (whose
-// serial pivot search and back substitution on one thread were the cost).
-__global__ void __launch_bounds__(256)
-    scat_solve_warp_kernel(const double* B, const double* coeffs, const double* lcols, int r,
-                           int m, double dt, double* lnew, int* singular) {
-  const int lane = threadIdx.x & 31;
-  const int q = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (q >= m) return;  // whole warps
-  double row[32];
-  double cf[12];
-#pragma unroll
-  for (int t = 0; t < 12; ++t) cf[t] = coeffs[t * m + q];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    double v = 0.0;
-    if (lane < r && k < r) {
-      double s = 0.0;
-      for (int t = 0; t < 12; ++t) s += cf[t] * B[(size_t)t * r * r + lane * r + k];
-      v = (lane == k ? 1.0 : 0.0) + dt * s;
-    }
-    row[k] = v;
-  }
-  double xv = lane < r ? lcols[lane * m + q] : 0.0;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (j < r) {
-      // pivot: the first row i >= j with the largest |M[i][j]|
-      double best = (lane >= j && lane < r) ? fabs(row[j]) : -1.0;
-      int bi = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (best == 0.0) {
-        if (lane == 0) atomicMin(singular, q);
-        return;
-      }
-      if (bi != j) {
-        const int src = lane == j ? bi : lane == bi ? j : lane;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < r) row[k] = __shfl_sync(0xffffffffu, row[k], src);
-        xv = __shfl_sync(0xffffffffu, xv, src);
-      }
-      const double inv = 1.0 / __shfl_sync(0xffffffffu, row[j], j);
-      const double xj = __shfl_sync(0xffffffffu, xv, j);
-      const bool below = lane > j && lane < r;
-      const double l = row[j] * inv;
-      if (below) row[j] = l;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        if (k > j && k < r) {
-          const double rjk = __shfl_sync(0xffffffffu, row[k], j);
-          if (below) row[k] -= l * rjk;
-        }
-      }
-      if (below) xv -= l * xj;
-    }
-  }
-  // back substitution, the unknowns broadcast as they are found
-  double xs[32];
-#pragma unroll
-  for (int i = 31; i >= 0; --i) {
-    if (i < r) {
-      double s = xv;
-#pragma unroll
-      for (int k = i + 1; k < 32; ++k)
-        if (k < r) s -= row[k] * xs[k];
-      const double xi = s / row[i];
-      xs[i] = __shfl_sync(0xffffffffu, xi, i);
-    }
-  }
-#pragma unroll
-  for (int a = 0; a < 32; ++a)
-    if (a < r && lane == a) lnew[a * m + q] = xs[a];
-}
-
 // RK4 (Horner form) of S' = -sum_s G_s S F_s on the R x R coefficient matrix in
 // one CTA; with `staged` the Grams and moment factors are copied to shared
 // memory first (the products then read only shared memory), and every
@@ -1797,12 +1714,6 @@ void scat_solves(const double* B, const double* coeffs, const double* lcols, int
     scat_solve_kernel<<<m, 128, 0, st>>>(B, coeffs, lcols, r, m, dt, lnew, singular, gw);
     launched();
     CK(cudaFreeAsync(gw, st));
-    return;
-  }
-  if (r <= 32 && !getenv("PND_SCAT_SOLVE_CTA")) {
-    scat_solve_warp_kernel<<<(m + 7) / 8, 256, 0, st>>>(B, coeffs, lcols, r, m, dt, lnew,
-                                                          singular);
-    launched();
     return;
   }
   set_smem((const void*)scat_solve_kernel, sm);

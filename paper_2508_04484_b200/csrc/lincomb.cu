@@ -64,6 +64,16 @@ struct LIn {
   int woff;         // smem offset of the staged weights
 };
 
+// element q of a per-input array of LIn. A runtime index into the kernel's
+// by-value parameter struct makes the compiler copy it to local memory
+// (LDL in the chunk loops -- 11 % of the stall samples of the CGS passes);
+// selects over constant indices keep every field in registers / the
+// constant bank
+template <class T>
+__device__ __forceinline__ T sel3(const T (&a)[3], int q) {
+  return q == 0 ? a[0] : q == 1 ? a[1] : a[2];
+}
+
 template <int NB8, int TBUF = 2>
 __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
     lincomb_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
@@ -76,7 +86,7 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
   double* const sT = sB + in.ks * NB8 * 32;     // tb x [LCH][TS] (tb = 1: 128 wide inputs)
   LBars* bars = reinterpret_cast<LBars*>(sT + tb * LCH * TS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
+  const int xcn = in.xq >= 0 ? sel3(in.cols, in.xq) : 0;
   const int XT = (xcn + 7) / 8;                  // X^T out row tiles
   // Gram tiles: X^T out (XT x NB8), then the upper triangle of the symmetric
   // out^T out (mirrored when stored)
@@ -92,15 +102,15 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
   for (int s = 0; s < nstg; ++s)
     for (int q = 0; q < in.nin; ++q)
       for (int i = tid; i < LZPAD; i += LTH)
-        sm[s * in.stage + in.off[q] + LCH * in.rs[q] + i] = 0.0;
+        sm[s * in.stage + sel3(in.off, q) + LCH * sel3(in.rs, q) + i] = 0.0;
   // B = [TA; -TB] in fragment order (zero rows past each input's columns)
   for (int i = tid; i < in.ks * NB8 * 32; i += LTH) {
     const int l = i & 31, f = i >> 5, ks = f / NB8, nt = f - ks * NB8;
     int q = 0;
-    while (q + 1 < in.nin && ks >= in.ks0[q + 1]) ++q;
-    const int j = 4 * (ks - in.ks0[q]) + (l & 3), col = nt * 8 + (l >> 2);
+    while (q + 1 < in.nin && ks >= sel3(in.ks0, q + 1)) ++q;
+    const int j = 4 * (ks - sel3(in.ks0, q)) + (l & 3), col = nt * 8 + (l >> 2);
     double v = 0.0;
-    if (j < in.cols[q] && col < nb && !copy_y) {
+    if (j < sel3(in.cols, q) && col < nb && !copy_y) {
       if (q == in.xq) v = -TB[(size_t)j * nb + col];
       else if (!in.ident) v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
     }
@@ -118,8 +128,8 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
         mbar_expect_tx(&bars->sfull[r.s], in.bytes);
         const long c0 = (long)chunk * LCH;
         for (int q = 0; q < in.nin; ++q)
-          bulk_load(sm + r.s * in.stage + in.off[q], in.p[q] + c0 * in.rs[q],
-                    LCH * in.rs[q] * 8, &bars->sfull[r.s]);
+          bulk_load(sm + r.s * in.stage + sel3(in.off, q), sel3(in.p, q) + c0 * sel3(in.rs, q),
+                    LCH * sel3(in.rs, q) * 8, &bars->sfull[r.s]);
         if (in.w) bulk_load(sm + r.s * in.stage + in.woff, in.w + c0, LCH * 8, &bars->sfull[r.s]);
       }
     }
@@ -143,14 +153,14 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
       const double* y = sb + in.off[0];
       const double* wv = in.w ? sb + in.woff : nullptr;
       const int y2 = in.nin > 1 && in.xq != 1 ? 1 : -1;  // second Y input, if any
-      const int c1 = in.cols[0], c2 = y2 >= 0 ? in.cols[y2] : 0;
+      const int c1 = in.cols[0], c2 = y2 >= 0 ? sel3(in.cols, y2) : 0;
       for (int e = lane; e < 8 * NB8 * 8; e += 32) {
         const int i = warp * 8 + e / (NB8 * 8), c = e % (NB8 * 8);
         // rows past n are halo rows (possibly a neighbour slab's): no Gram input
         double v = 0.0;
         if (c0 + i < n) {
           if (c < c1) v = y[i * in.rs[0] + c];
-          else if (c - c1 < c2) v = sb[in.off[y2] + i * in.rs[y2] + c - c1];
+          else if (c - c1 < c2) v = sb[sel3(in.off, y2) + i * sel3(in.rs, y2) + c - c1];
         }
         T[i * TS + c] = wv ? wv[i] * v : v;
       }
@@ -184,8 +194,8 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
       }
     }
     for (int q = in.ident; q < in.nin; ++q) {
-      const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
-      const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
+      const double* pa = sb + sel3(in.off, q) + (warp * 8 + m) * sel3(in.rs, q) + kq;
+      const int k0 = sel3(in.ks0, q), k1 = q + 1 < in.nin ? sel3(in.ks0, q + 1) : in.ks;
       int ks = k0;
       for (; ks + 1 < k1; ks += 2) {
         const double a0 = pa[4 * (ks - k0)], a1 = pa[4 * (ks + 1 - k0)];
@@ -220,8 +230,8 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
     }
     if (grams) {
       named_sync(1, 32 * LCW);  // out tile of this chunk complete
-      const double* sx = in.xq >= 0 ? sb + in.off[in.xq] : nullptr;
-      const int rsx = in.xq >= 0 ? in.rs[in.xq] : 0;
+      const double* sx = in.xq >= 0 ? sb + sel3(in.off, in.xq) : nullptr;
+      const int rsx = in.xq >= 0 ? sel3(in.rs, in.xq) : 0;
 #pragma unroll
       for (int t = 0; t < GPW_MAX; ++t) {
         const int tile = warp + LCW * t;
@@ -296,7 +306,7 @@ __global__ void __launch_bounds__(LTH, 2)
   double* const sT = sB + in.ks * NB8 * 32;     // per warp [8][TS]
   LBars* bars = reinterpret_cast<LBars*>(sT + LCW * 8 * TS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int xcn = in.xq >= 0 ? in.cols[in.xq] : 0;
+  const int xcn = in.xq >= 0 ? sel3(in.cols, in.xq) : 0;
   const int XT = (xcn + 7) / 8;
   if (tid == 0) {
     for (int b = 0; b < nstg; ++b) {
@@ -308,14 +318,14 @@ __global__ void __launch_bounds__(LTH, 2)
   for (int s = 0; s < nstg; ++s)
     for (int q = 0; q < in.nin; ++q)
       for (int i = tid; i < LZPAD; i += LTH)
-        sm[s * in.stage + in.off[q] + LCH * in.rs[q] + i] = 0.0;
+        sm[s * in.stage + sel3(in.off, q) + LCH * sel3(in.rs, q) + i] = 0.0;
   for (int i = tid; i < in.ks * NB8 * 32; i += LTH) {
     const int l = i & 31, f = i >> 5, ks = f / NB8, nt = f - ks * NB8;
     int q = 0;
-    while (q + 1 < in.nin && ks >= in.ks0[q + 1]) ++q;
-    const int j = 4 * (ks - in.ks0[q]) + (l & 3), col = nt * 8 + (l >> 2);
+    while (q + 1 < in.nin && ks >= sel3(in.ks0, q + 1)) ++q;
+    const int j = 4 * (ks - sel3(in.ks0, q)) + (l & 3), col = nt * 8 + (l >> 2);
     double v = 0.0;
-    if (j < in.cols[q] && col < nb && !copy_y) {
+    if (j < sel3(in.cols, q) && col < nb && !copy_y) {
       if (q == in.xq) v = -TB[(size_t)j * nb + col];
       else if (!in.ident) v = TA[(size_t)((q == 0 ? 0 : in.cols[0]) + j) * nb + col];
     }
@@ -333,8 +343,8 @@ __global__ void __launch_bounds__(LTH, 2)
         mbar_expect_tx(&bars->sfull[r.s], in.bytes);
         const long c0 = (long)chunk * LCH;
         for (int q = 0; q < in.nin; ++q)
-          bulk_load(sm + r.s * in.stage + in.off[q], in.p[q] + c0 * in.rs[q],
-                    LCH * in.rs[q] * 8, &bars->sfull[r.s]);
+          bulk_load(sm + r.s * in.stage + sel3(in.off, q), sel3(in.p, q) + c0 * sel3(in.rs, q),
+                    LCH * sel3(in.rs, q) * 8, &bars->sfull[r.s]);
         if (in.w) bulk_load(sm + r.s * in.stage + in.woff, in.w + c0, LCH * 8, &bars->sfull[r.s]);
       }
     }
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(LTH, 2)
 #pragma unroll
   for (int t = 0; t < NTT; ++t) gt[t][0] = gt[t][1] = 0.0;
   double* const T = sT + warp * 8 * TS;
-  const int rsx = in.xq >= 0 ? in.rs[in.xq] : 0;
+  const int rsx = in.xq >= 0 ? sel3(in.rs, in.xq) : 0;
   // Gram-only second Y input: staged at index 1 unless that is X
   const int y2 = copy_y && in.nin > 1 && in.xq != 1 ? 1 : -1;
   Ring r(nstg);
@@ -392,8 +402,8 @@ __global__ void __launch_bounds__(LTH, 2)
         }
       }
       for (int q = in.ident; q < in.nin; ++q) {
-        const double* pa = sb + in.off[q] + (warp * 8 + m) * in.rs[q] + kq;
-        const int k0 = in.ks0[q], k1 = q + 1 < in.nin ? in.ks0[q + 1] : in.ks;
+        const double* pa = sb + sel3(in.off, q) + (warp * 8 + m) * sel3(in.rs, q) + kq;
+        const int k0 = sel3(in.ks0, q), k1 = q + 1 < in.nin ? sel3(in.ks0, q + 1) : in.ks;
 #pragma unroll 2
         for (int ks = k0; ks < k1; ++ks) {
           const double a0 = pa[4 * (ks - k0)];
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(LTH, 2)
       rsy = TS;
     }
     if (grams) {
-      const double* sx = in.xq >= 0 ? sb + in.off[in.xq] + warp * 8 * rsx : nullptr;
+      const double* sx = in.xq >= 0 ? sb + sel3(in.off, in.xq) + warp * 8 * rsx : nullptr;
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int cl = 4 * s + kq;  // k index = this lane's cell
@@ -436,12 +446,12 @@ __global__ void __launch_bounds__(LTH, 2)
               bf[tj] = live ? wv * sy[cl * rsy + tj * 8 + m] : 0.0;
           } else {
             const int c1 = in.cols[0];
-            const double* s2 = sb + in.off[y2] + (warp * 8 + cl) * in.rs[y2];
+            const double* s2 = sb + sel3(in.off, y2) + (warp * 8 + cl) * sel3(in.rs, y2);
 #pragma unroll
             for (int tj = 0; tj < NB8; ++tj) {
               const int col = tj * 8 + m;
               const double v = col < c1 ? sy[cl * rsy + col]
-                               : col - c1 < in.cols[y2] ? s2[col - c1] : 0.0;
+                               : col - c1 < sel3(in.cols, y2) ? s2[col - c1] : 0.0;
               bf[tj] = live ? wv * v : 0.0;
             }
           }
