@@ -141,6 +141,14 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
   double gacc[GPW_MAX][2], gacc2[GPW_MAX][2];  // even / odd k-steps: two chains per tile
 #pragma unroll
   for (int t = 0; t < GPW_MAX; ++t) gacc[t][0] = gacc[t][1] = gacc2[t][0] = gacc2[t][1] = 0.0;
+  // this warp's Gram tiles, resolved once (the triangular index walk was a
+  // per-chunk loop of branches)
+  int g_ti[GPW_MAX], g_tj[GPW_MAX];
+#pragma unroll
+  for (int t = 0; t < GPW_MAX; ++t) {
+    g_ti[t] = g_tj[t] = -1;
+    if (warp + LCW * t < GT) gram_tile(warp + LCW * t, XT, NB8, g_ti[t], g_tj[t]);
+  }
   Ring r(nstg);
   int it = 0;
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, r.next(), ++it) {
@@ -234,16 +242,14 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
       const int rsx = in.xq >= 0 ? sel3(in.rs, in.xq) : 0;
 #pragma unroll
       for (int t = 0; t < GPW_MAX; ++t) {
-        const int tile = warp + LCW * t;
-        if (tile < GT) {
-          int ti, tj;
-          gram_tile(tile, XT, NB8, ti, tj);
+        if (g_ti[t] >= 0) {
+          const int ti = g_ti[t], tj = g_tj[t];
           const bool xg = ti < XT;
           const double* pa = xg ? sx + (ti * 8 + m) : T + ((ti - XT) * 8 + m);
           const int sa = xg ? rsx : TS;
           const double* pb = T + tj * 8 + m;
           // rows past n: zero staged rows and zero out rows -> no contribution
-#pragma unroll 4
+#pragma unroll
           for (int k0 = 0; k0 < LCH; k0 += 8) {
             dmma884(gacc[t][0], gacc[t][1], pa[(k0 + kq) * sa], pb[(k0 + kq) * TS]);
             dmma884(gacc2[t][0], gacc2[t][1], pa[(k0 + 4 + kq) * sa], pb[(k0 + 4 + kq) * TS]);
