@@ -327,7 +327,8 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
   // Bcat in DMMA B-fragment order: sB[(ks NT + nt) 32 + lane] =
   // Bcat[4 ks + (lane & 3)][8 nt + (lane >> 2)] (one contiguous 256-byte load each)
   double* const sB = F0 + 2 * K4 * KCS;
-  PipeBars* pb = reinterpret_cast<PipeBars*>(sB + K4 * RB);
+  double* const red = sB + K4 * RB;  // [k-part - 1][MT][NT][64] contraction partials
+  PipeBars* pb = reinterpret_cast<PipeBars*>(red + (KSPLIT - 1) * MT * NT * 64);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xc = X.cols, ra = U0.p ? U0.cols : 0;
   pipe_init(pb, nstg, CONW);
@@ -425,6 +426,10 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
       const int b = it & 1, u = it >> 1;
       const int c0 = chunk_cell(S, chunk, KC);
+      // the output row's 1/S, fetched before the wait (its latency was an
+      // epilogue stall)
+      const int prow = c0 + mt * 8 + (lane >> 2);
+      const double is_pre = (!kh && oscale && prow < g.n) ? __ldg(isp + 2 * (long)prow) : 1.0;
       mbar_wait(&pb->ffull[b], u & 1);
       double acc[2][NT][2];
 #pragma unroll
@@ -489,15 +494,19 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
         acc[0][nt][0] += acc[1][nt][0];
         acc[0][nt][1] += acc[1][nt][1];
       }
-      named_sync(2, 32 * CONW);  // every contraction warp is done reading F[b]
-      double* red = Fb;          // [k-part - 1][MT][NT][64] partials
+      // F[b] is free as soon as this warp's DMMAs have read it; the k-parts
+      // of an m-tile meet in their own partial buffer, synchronised pairwise
+      // (named barrier 3 + m-tile, KSPLIT warps) instead of across all
+      // contraction warps
+      __syncwarp();
+      warp_arrive(&pb->fempty[b]);
       if (kh) {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
           *reinterpret_cast<double2*>(red + (((kh - 1) * MT + mt) * NT + nt) * 64 + 2 * lane) =
               make_double2(acc[0][nt][0], acc[0][nt][1]);
       }
-      named_sync(2, 32 * CONW);
+      named_sync(3 + mt, 32 * KSPLIT);  // the m-tile's partials written
       if (!kh) {
         const int row = c0 + mt * 8 + (lane >> 2);
         double v[NT][2];
@@ -513,11 +522,10 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
             v[nt][1] += pv.y;
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pb->fempty[b]);
+        named_sync(3 + mt, 32 * KSPLIT);  // read before the next chunk's partials
         if (row < g.n) {
           double* o = out.p + (long)row * out.rs;
-          const double is = oscale ? __ldg(isp + 2 * (long)row) : 1.0;
+          const double is = is_pre;
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const int n = nt * 8 + 2 * (lane & 3);
@@ -531,7 +539,7 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
           }
         }
       } else {
-        warp_arrive(&pb->fempty[b]);
+        named_sync(3 + mt, 32 * KSPLIT);
       }
     }
   }
@@ -565,7 +573,9 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
     S.zb = a.zpart == 2 ? 1 : 0;
     S.nchunks = S.nzr * S.cpp;
   }
-  const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (size_t)K4 * RB) * sizeof(double) +
+  constexpr int KSP = CONW / (KC / 8);
+  const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (size_t)K4 * RB +
+                        (size_t)(KSP - 1) * (KC / 8) * (RB / 8) * 64) * sizeof(double) +
                        sizeof(PipeBars);
   const int nstg = stages_for(fixed, S.total);
   if (nstg < 2) return false;
