@@ -242,6 +242,9 @@ int pnd_create(pnd_handle** out, int nx, int ny, int nz, double dx, double dy, d
     g.ld = (int)((n + 31) / 32 * 32);
     g.inv_nx = 1.0 / nx;
     g.inv_nxy = 1.0 / ((double)nx * ny);
+    auto magic = [](unsigned long long d) { return d < 2 ? 0ULL : ~0ULL / d + 1; };
+    g.mnx = magic((unsigned long long)nx);
+    g.mnxy = magic((unsigned long long)nx * ny);
     g.halo = (int)halo;
     g.h[0] = dx;
     g.h[1] = dy;

@@ -80,6 +80,9 @@ struct Geom {
   int z0 = 0;
   int nzg = 0;    // 0: single device (nzg = nz)
   double inv_nx = 0.0, inv_nxy = 0.0;  // 1/nx, 1/(nx ny): cell -> (i, j, k) without division
+  // the same by integer reciprocals: q = umulhi64(c, m) for c < 2^32 with
+  // m = floor((2^64 - 1) / d) + 1 (d >= 2; m = 0 marks d = 1)
+  unsigned long long mnx = 0, mnxy = 0;
   void* comm = nullptr;
   // 1/S is the same in every cell (one material class): the stencil Grams then
   // form only the D+ stencils and take D- = -(D+)^T + boundary rows (stencil.cu)

@@ -149,14 +149,12 @@ struct Ctx {
   }
 
   __device__ __forceinline__ void init(const Geom& g, int c, int i, const double* I) {
-    // cell -> (i, j, k) by reciprocal multiply + one correction step (exact
-    // for c < 2^31: the double product is within one of the true quotient)
+    // cell -> (i, j, k) by exact integer reciprocals (the double-product
+    // version's int->double conversions were the formers' top stall)
     const int nxy = g.nx * g.ny;
-    int ck = __double2int_rz((double)c * g.inv_nxy);
-    ck += (c - ck * nxy >= nxy) - (c - ck * nxy < 0);
+    const int ck = g.mnxy ? (int)__umul64hi((unsigned long long)c, g.mnxy) : c;
     const int rem = c - ck * nxy;
-    int cj = __double2int_rz((double)rem * g.inv_nx);
-    cj += (rem - cj * g.nx >= g.nx) - (rem - cj * g.nx < 0);
+    const int cj = g.mnx ? (int)__umul64hi((unsigned long long)rem, g.mnx) : rem;
     const int ci = rem - cj * g.nx;
     inner = true;
     // z in global planes (a slab's faces are interior unless they are the grid's)
