@@ -695,7 +695,9 @@ __global__ void __launch_bounds__(gpth(T8), 1)
         Cb[ci * XS + j] = c0 + ci >= g.n ? 0.0  // past n: halo rows (maybe a neighbour's)
                           : j < a1 ? X1s[(ci + 2) * X1.rs + j]
                                    : X2s[(ci + 2) * X2.rs + j - a1];
-      Ctx<GC, NA> cx;
+      // PO (one material class): 1/S is one number, so the formers difference
+      // the raw rows and reduce_parts_po applies 1/S with 1/(2h)
+      Ctx<GC, NA, PO> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
       constexpr int TT = (W + JS - 1) / JS;
@@ -950,13 +952,15 @@ __global__ void __launch_bounds__(gpth(T8B), 1)
 
 // the D+ partials (NA x per) summed in fixed order into the even stencil slots
 __global__ void reduce_parts_po(const double* __restrict__ partial, int nblk, int count, int per,
-                                StScale sc, double* __restrict__ out) {
+                                StScale sc, const double* __restrict__ isp,
+                                double* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double s = 0.0;
   for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * count + i];
   const int a = i / per;
-  out[(size_t)(2 * a) * per + (i - a * per)] = s * sc.v[a];
+  // isp[0]: the one material's 1/S (the formers differenced the raw rows)
+  out[(size_t)(2 * a) * per + (i - a * per)] = s * sc.v[a] * isp[0];
 }
 
 // sums the per-CTA Gram partials in a fixed order and applies the stencil's
@@ -1002,7 +1006,7 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
     StScale sc = stencil_scale(g), sp{};
     for (int a = 0; a < NA; ++a) sp.v[a] = sc.v[2 * a];
     reduce_parts_po<<<(int)((count + 255) / 256), 256, 0, st>>>(part, grid, (int)count, w * w,
-                                                                sp, out);
+                                                                sp, isp, out);
     launched();
     minus_from_plus(g, X1, X2, isp, out, partial, st);
     comm_allreduce(g, out, (size_t)2 * NA * w * w, st);
