@@ -581,11 +581,13 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   constexpr int TS = lpad4(NB8 * 8);
   // per-warp Grams (lincomb_pw_kernel) while the registers allow
   constexpr bool PWOK = NB8 <= 3;
-  // (Gram-only passes; for contractions that also form Grams the per-warp
-  // variant -- 0.4 operand loads per Gram DMMA instead of 2, no CTA barrier
-  // per chunk -- measured the same time at 256^3 r = 20, kept opt-in:
-  // PND_LINCOMB_PW_GRAMS=1)
-  const bool PW = PWOK && (gram_only || (grams != nullptr && getenv("PND_LINCOMB_PW_GRAMS")));
+  // (Gram-only passes and the CGS passes' contraction + Grams: 0.4 operand
+  // loads per Gram DMMA instead of 2 and no CTA barrier per chunk -- the
+  // barrier was 7.7 % of the CTA variant's stall samples; at 256^3 r = 20 the
+  // two augmentations take 9.05 instead of 9.88 ms. The rotation's U^T U
+  // alone (no X) stays on the CTA variant, which is faster there.)
+  const bool PW = PWOK && (gram_only || (grams != nullptr && X.p != nullptr &&
+                                         !getenv("PND_LINCOMB_CTA_GRAMS")));
   int tb = 2;  // out-tile buffers
   size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
   size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
