@@ -7,7 +7,8 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fina
 timeout 900 python bench.py > gpurun_out/final_bench.json 2> gpurun_out/final_bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/final_bench_ref.json 2> gpurun_out/final_bench_ref.err
 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-config1 > /dev/null 2>&1
-/usr/local/cuda/bin/ncu --set full --clock-control none -k regex:"kstage_kernel|sgram_kernel|lincomb_kernel" -c 8 -o gpurun_out/final_stencil timeout 900 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config1 > /dev/null 2>&1
+/usr/local/cuda/bin/ncu --set full --clock-control none -k regex:"kstage_kernel" --launch-skip 4 -c 4 -o gpurun_out/final_kstage timeout 900 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config1 > /dev/null 2>&1
+/usr/local/cuda/bin/ncu --set full --clock-control none -k regex:"sgram_kernel|lincomb" --launch-skip 12 -c 10 -o gpurun_out/final_sgram_lincomb timeout 900 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-config1 > /dev/null 2>&1
 timeout 300 python tools/config1_profile.py 200 > gpurun_out/final_config1.txt 2>&1
 /usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_config1_launches.csv timeout 600 python tools/config1_profile.py 20 > /dev/null 2>&1
 echo done
