@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(512, 1)
   double* sg = nrm + N2;         // N2
   int* perm = (int*)(sg + N2);   // N: column pivots (A Pi)[:, j] = A[:, perm[j]]
   int* order = perm + N;         // N: singular values, descending
-  __shared__ int rotated;
+  __shared__ int rotated, large;
   const int tid = threadIdx.x, nthr = blockDim.x;
   const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
   const int grp = tid / QJ_G, l = tid % QJ_G, ngrp = nthr / QJ_G;
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(512, 1)
       x += __shfl_xor_sync(0xffffffffu, x, 1);
       if (l == 0 && j < N2) nrm[j] = x;
     }
-    if (tid == 0) rotated = 0;
+    if (tid == 0) rotated = large = 0;
     __syncthreads();
     for (int round = 0; round < N2 - 1; ++round) {
       const int k = grp;
@@ -688,12 +688,16 @@ __global__ void __launch_bounds__(512, 1)
             nrm[a] = al - t * ga;
             nrm[b] = be + t * ga;
             rotated = 1;
+            if (fabs(ga) > 1e7 * thr) large = 1;  // |cos angle| above 1e-8
           }
         }
       }
       __syncthreads();
     }
-    const int any = rotated;
+    // converged: no rotation, or every rotation of this sweep was below 1e-8
+    // relative -- the next sweep's (quadratically smaller, below 1e-15) would
+    // all be skipped, so it is not run
+    const int any = rotated && large;
     __syncthreads();
     if (!any) break;
   }
