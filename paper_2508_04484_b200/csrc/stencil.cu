@@ -42,6 +42,7 @@ struct Seg {
   unsigned bytes;  // bytes per chunk
   int cpp, nz;     // chunk order: cpp > 0 -> z-fastest (cpp chunks per z-plane)
   int plus_only;   // D+ stencils only: the +1 / +2 segments of the y and z axes are not staged
+  int no_isp;      // the [1/S, 0] rows are not staged (inputs already scaled by 1/S)
   // the planes a launch covers (cpp > 0): zlo .. zlo + nzr - 1, or with zb the
   // four boundary planes 0, 1, nz - 2, nz - 1; nchunks = nzr * cpp (all: nz planes)
   int zlo, nzr, zb, nchunks;
@@ -60,9 +61,11 @@ __device__ __forceinline__ int chunk_cell(const Seg& S, int p, int ch) {
 }
 
 template <int CH>
-Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool plus_only = false) {
+Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool plus_only = false,
+             bool no_isp = false) {
   Seg s{};
   s.plus_only = plus_only ? 1 : 0;
+  s.no_isp = no_isp ? 1 : 0;
   s.nbox = 1;
   s.off[0] = -2;
   const int nxy = g.nx * g.ny;
@@ -85,7 +88,7 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool pl
   }
   s.ioff = o;
   o += up16(2 * s.nrows);
-  bytes += 2 * srows * 8;
+  if (!no_isp) bytes += 2 * srows * 8;
   s.coff = -1;
   if (centre) {
     s.coff = o;
@@ -122,7 +125,7 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
     const int drow = box_row<CH>(q);
     bulk_load(dst + S.xoff[0] + drow * a.rs, a.p + row * a.rs, rows * a.rs * 8, bar);
     if (nin > 1) bulk_load(dst + S.xoff[1] + drow * b.rs, b.p + row * b.rs, rows * b.rs * 8, bar);
-    bulk_load(dst + S.ioff + 2 * drow, isp + 2 * row, rows * 16, bar);
+    if (!S.no_isp) bulk_load(dst + S.ioff + 2 * drow, isp + 2 * row, rows * 16, bar);
   }
   if (S.coff >= 0) bulk_load(dst + S.coff, c.p + (long)c0 * c.rs, CH * c.rs * 8, bar);
 }
@@ -561,7 +564,8 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
   const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
-  Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr);
+  // PRE: the staged rows already hold S^-1 x, the formers read no 1/S row
+  Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr, false, PRE);
   if (a.zpart) {
     // interior planes (no halo row read) / the four boundary planes: the
     // halo exchange of X overlaps the interior launch (streaming_step)
@@ -980,7 +984,8 @@ void sgram_launch(const Geom& g, NMat X1, NMat X2, const double* isp, double* ou
   constexpr int GTL = pad4(GC);
   constexpr int NSF = PO ? NA : 2 * NA;
   const NMat ins[2] = {X1, X2};
-  const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr, PO && !getenv("PND_SGRAM_ALLSEG"));
+  // PO: raw rows are differenced (1/S applied in the reduction): no 1/S rows staged
+  const Seg S = make_seg<GC>(g, ins, X2.p ? 2 : 1, nullptr, PO && !getenv("PND_SGRAM_ALLSEG"), PO);
   const int W = T8 * 8;
   const size_t ft = (size_t)NSF * W * GTL + (size_t)GC * pad4(W);
   const size_t fixed = 2 * ft * sizeof(double) + sizeof(PipeBars);
