@@ -87,8 +87,10 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool pl
     }
   }
   s.ioff = o;
-  o += up16(2 * s.nrows);
-  if (!no_isp) bytes += 2 * srows * 8;
+  if (!no_isp) {
+    o += up16(2 * s.nrows);
+    bytes += 2 * srows * 8;
+  }
   s.coff = -1;
   if (centre) {
     s.coff = o;
@@ -327,8 +329,10 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
   double* const F0 = sm + nstg * S.total;
   // Bcat in DMMA B-fragment order: sB[(ks NT + nt) 32 + lane] =
   // Bcat[4 ks + (lane & 3)][8 nt + (lane >> 2)] (one contiguous 256-byte load each)
+  // (KHR: the B fragments live in the contraction warps' registers, loaded
+  // from global memory once; no shared copy -- the room goes to a deeper ring)
   double* const sB = F0 + 2 * K4 * KCS;
-  double* const red = sB + K4 * RB;  // [k-part - 1][MT][NT][64] contraction partials
+  double* const red = sB + (KHR > 0 ? 0 : K4 * RB);  // [k-part - 1][MT][NT][64] partials
   PipeBars* pb = reinterpret_cast<PipeBars*>(red + (KSPLIT - 1) * MT * NT * 64);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xc = X.cols, ra = U0.p ? U0.cols : 0;
@@ -337,9 +341,11 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
     F0[K * KCS + i] = 0.0;
     F0[K4 * KCS + K * KCS + i] = 0.0;
   }
-  for (int i = tid; i < K4 * RB; i += NTH) {
-    const int l = i & 31, f = i >> 5, ks = f / NT, nt = f - ks * NT;
-    sB[i] = Bcat[(4 * ks + (l & 3)) * RB + 8 * nt + (l >> 2)];
+  if constexpr (KHR == 0) {
+    for (int i = tid; i < K4 * RB; i += NTH) {
+      const int l = i & 31, f = i >> 5, ks = f / NT, nt = f - ks * NT;
+      sB[i] = Bcat[(4 * ks + (l & 3)) * RB + 8 * nt + (l >> 2)];
+    }
   }
   __syncthreads();
   const bool sepc = S.coff >= 0;
@@ -382,6 +388,10 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
       // results are not stored)
       if (sepc) {
         for (int j = cj; j < ra; j += JS) base[j * KCS + ci] = sb[S.coff + ci * U0.rs + j];
+      } else if (ra > 0 && U0.p != X.p) {
+        // KHR: U0's centre rows are not staged (the ring is deeper instead)
+        const double* u0r = U0.p + (long)(c0 + ci) * U0.rs;
+        for (int j = cj; j < ra; j += JS) base[j * KCS + ci] = __ldg(u0r + j);
       } else {
         for (int j = cj; j < ra; j += JS) base[j * KCS + ci] = Xs[(ci + 2) * X.rs + j];
       }
@@ -421,7 +431,8 @@ __global__ void __launch_bounds__(KHR > 0 ? RPTH : PTH, 1)
 #pragma unroll
       for (int i = 0; i < KHR; ++i)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) breg[i][nt] = pb0[((ks0 + i) * NT + nt) * 32];
+        for (int nt = 0; nt < NT; ++nt)
+          breg[i][nt] = __ldg(Bcat + (4 * (ks0 + i) + (lane & 3)) * RB + 8 * nt + (lane >> 2));
     }
     int it = 0;
     for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
@@ -564,8 +575,9 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   const Geom& g = a.geo;
   const int ra = a.U0.p ? a.U0.cols : 0;
   const bool sepc = ra > 0 && !(a.U0.p == a.X.p && a.U0.rs == a.X.rs);
-  // PRE: the staged rows already hold S^-1 x, the formers read no 1/S row
-  Seg S = make_seg<KC>(g, &a.X, 1, sepc ? &a.U0 : nullptr, false, PRE);
+  // PRE: the staged rows already hold S^-1 x, the formers read no 1/S row;
+  // KHR: U0's centre rows are read from global memory instead of staged
+  Seg S = make_seg<KC>(g, &a.X, 1, (sepc && KHR == 0) ? &a.U0 : nullptr, false, PRE);
   if (a.zpart) {
     // interior planes (no halo row read) / the four boundary planes: the
     // halo exchange of X overlaps the interior launch (streaming_step)
@@ -576,11 +588,11 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
     S.nchunks = S.nzr * S.cpp;
   }
   constexpr int KSP = CONW / (KC / 8);
-  const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (size_t)K4 * RB +
+  const size_t fixed = (2 * (size_t)K4 * pad4(KC) + (KHR > 0 ? 0 : (size_t)K4 * RB) +
                         (size_t)(KSP - 1) * (KC / 8) * (RB / 8) * 64) * sizeof(double) +
                        sizeof(PipeBars);
   const int nstg = stages_for(fixed, S.total);
-  if (nstg < 2) return false;
+  if (nstg < (KHR > 0 ? 3 : 2)) return false;  // KHR only pays with a deeper ring
   const size_t smem = fixed + (size_t)nstg * S.total * sizeof(double);
   constexpr int nth = KHR > 0 ? RPTH : PTH;
   allow_max_smem(kstage_kernel<NA, RB, PRE, KC, KHR>);
@@ -607,7 +619,11 @@ void kstage_launch(const KStageArgs& a, DBuf& bcat, cudaStream_t st) {
   launched();
   // 32-cell chunks when the tiles fit, else 16-cell chunks (larger ranks);
   // the register-rebalanced variant for the bench's 3-D r = 20 tiles
-  if (NA == 3 && RB == 24 && getenv("PND_KSTAGE_REG_B")) {  // measured: no gain
+  // The B fragments in registers (setmaxnreg-rebalanced warpgroups) free the
+  // shared copy of [M; S0] for a third staging slot; measured a gain only for
+  // the last Horner stage (no U0 base rows: 5.74 -> 5.30 ms at 256^3) and a
+  // loss with them (the base rows then come from global memory: 6.21 -> 6.79)
+  if (NA == 3 && RB == 24 && ra == 0 && !getenv("PND_KSTAGE_SMEM_B")) {
     const int khr = K4 / 8;  // k-steps per contraction k-half (KC = 32: 4 m-tiles x 2)
     if (khr == 18 && kstage_try<NA, RB, PRE, 32, 18>(a, B, K, K4, st)) return;
     if (khr == 16 && kstage_try<NA, RB, PRE, 32, 16>(a, B, K, K4, st)) return;
