@@ -74,11 +74,11 @@ Seg make_seg(const Geom& g, const NMat* in, int nin, const NMat* centre, bool pl
     const int ds[4] = {-2, -1, 1, 2};
     for (int q = 0; q < 4; ++q) s.off[s.nbox++] = ds[q] * st;
   }
-  s.nrows = CH + 4 + (s.nbox - 1) * CH;
+  s.nrows = CH + 4 + (plus_only ? (s.nbox - 1) / 2 : s.nbox - 1) * CH;
   int o = 0;
   unsigned bytes = 0;
   // staged rows per input: all segments, or without the +1 / +2 ones (plus_only)
-  const int srows = plus_only ? CH + 4 + (s.nbox - 1) / 2 * CH : s.nrows;
+  const int srows = s.nrows;
   for (int k = 0; k < 2; ++k) {
     s.xoff[k] = o;
     if (k < nin) {
@@ -120,11 +120,12 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
   mbar_expect_tx(bar, S.bytes);
 #pragma unroll
   for (int q = 0; q < 1 + 4 * (NA - 1); ++q) {
-    // D+ only (the one-material S-Grams): the +1 / +2 neighbours are never read
+    // D+ only (the one-material S-Grams): the +1 / +2 neighbours are never
+    // read, and the staged segments are packed back to back
     if (S.plus_only && q > 0 && ((q - 1) & 3) >= 2) continue;
     const int rows = q == 0 ? CH + 4 : CH;
     const long row = (long)c0 + S.off[q];
-    const int drow = box_row<CH>(q);
+    const int drow = box_row<CH>(S.plus_only && q > 0 ? 1 + 2 * ((q - 1) >> 2) + ((q - 1) & 3) : q);
     bulk_load(dst + S.xoff[0] + drow * a.rs, a.p + row * a.rs, rows * a.rs * 8, bar);
     if (nin > 1) bulk_load(dst + S.xoff[1] + drow * b.rs, b.p + row * b.rs, rows * b.rs * 8, bar);
     if (!S.no_isp) bulk_load(dst + S.ioff + 2 * drow, isp + 2 * row, rows * 16, bar);
@@ -138,7 +139,10 @@ __device__ __forceinline__ void issue_seg(const Seg& S, double* dst, uint64_t* b
 // apply<FAST>() forms the 2 NA values D_s S^-1 x of column (col0 + off):
 // FAST = every cell of the warp is >= 2 cells from every face (branch-free
 // interior formula); otherwise the boundary closures of spatial.py:81-118.
-template <int CH, int NA, bool PRE = false>
+// CMP: the compact plus-only staging (only the -2 / -1 segments of the y and
+// z axes are staged, back to back); the +1 / +2 points then alias the -2 row
+// and are never read (D+ only)
+template <int CH, int NA, bool PRE = false, bool CMP = false>
 struct Ctx {
   static constexpr int NP = 1 + 4 * NA;
   const double* xr[NP];
@@ -150,6 +154,7 @@ struct Ctx {
     if (p == 0) return i + 2;
     const int ai = (p - 1) >> 2, q = (p - 1) & 3;
     if (ai == 0) return i + (q < 2 ? q : q + 1);
+    if (CMP) return box_row<CH>(1 + 2 * (ai - 1) + (q < 2 ? q : 0)) + i;
     return box_row<CH>(1 + 4 * (ai - 1) + q) + i;
   }
 
@@ -717,7 +722,7 @@ __global__ void __launch_bounds__(gpth(T8), 1)
                                    : X2s[(ci + 2) * X2.rs + j - a1];
       // PO (one material class): 1/S is one number, so the formers difference
       // the raw rows and reduce_parts_po applies 1/S with 1/(2h)
-      Ctx<GC, NA, PO> cx;
+      Ctx<GC, NA, PO, PO> cx;
       cx.init(g, c0 + ci, ci, sb + S.ioff);
       const bool fast = __all_sync(0xffffffffu, cx.inner);
       constexpr int TT = (W + JS - 1) / JS;
