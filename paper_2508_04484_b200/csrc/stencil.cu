@@ -603,6 +603,11 @@ bool kstage_try(const KStageArgs& a, const double* B, int K, int K4, cudaStream_
   allow_max_smem(kstage_kernel<NA, RB, PRE, KC, KHR>);
   const int nchunks = S.nchunks;
   int grid = sm_count() * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem);
+  // the interior launch of an overlapped halo exchange leaves two SMs to the
+  // exchange's NCCL kernels (the persistent CTAs would otherwise hold every
+  // SM and serialise the exchange behind them)
+  if (a.zpart == 1 && grid > 2 * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem))
+    grid -= 2 * resident(kstage_kernel<NA, RB, PRE, KC, KHR>, nth, smem);
   if (grid > nchunks) grid = nchunks;
   const char* dbg = getenv("PND_KSTAGE_DBG");
   kstage_kernel<NA, RB, PRE, KC, KHR><<<grid, nth, smem, st>>>(
