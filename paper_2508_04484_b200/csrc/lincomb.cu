@@ -300,16 +300,16 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
 // tile (only __syncwarp), and in Gram-only mode the staged Y rows are the B
 // operand directly. The out^T out A and B fragments are the same loads. Each
 // warp writes its own partial; lreduce sums grid x 8 partials in fixed order.
-template <int NB8>
+template <int NB8, int NO8 = NB8>
 __global__ void __launch_bounds__(LTH, 2)
     lincomb_pw_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
                       int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
                       double* __restrict__ partial, int) {
-  constexpr int TS = lpad4(NB8 * 8);            // out tile row length
-  constexpr int NTT = NB8 * (NB8 + 1) / 2;      // upper-triangle out^T out tiles
+  constexpr int TS = lpad4(NO8 * 8);            // out tile row length
+  constexpr int NTT = NO8 * (NO8 + 1) / 2;      // upper-triangle out^T out tiles
   extern __shared__ __align__(128) double sm[];
-  double* const sB = sm + nstg * in.stage;      // [ks][NB8][32] fragment order
-  double* const sT = sB + in.ks * NB8 * 32;     // per warp [8][TS]
+  double* const sB = sm + nstg * in.stage;      // [ks][NO8][32] fragment order
+  double* const sT = sB + in.ks * NO8 * 32;     // per warp [8][TS]
   LBars* bars = reinterpret_cast<LBars*>(sT + LCW * 8 * TS);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int xcn = in.xq >= 0 ? sel3(in.cols, in.xq) : 0;
@@ -325,8 +325,8 @@ __global__ void __launch_bounds__(LTH, 2)
     for (int q = 0; q < in.nin; ++q)
       for (int i = tid; i < LZPAD; i += LTH)
         sm[s * in.stage + sel3(in.off, q) + LCH * sel3(in.rs, q) + i] = 0.0;
-  for (int i = tid; i < in.ks * NB8 * 32; i += LTH) {
-    const int l = i & 31, f = i >> 5, ks = f / NB8, nt = f - ks * NB8;
+  for (int i = tid; i < in.ks * NO8 * 32; i += LTH) {
+    const int l = i & 31, f = i >> 5, ks = f / NO8, nt = f - ks * NO8;
     int q = 0;
     while (q + 1 < in.nin && ks >= sel3(in.ks0, q + 1)) ++q;
     const int j = 4 * (ks - sel3(in.ks0, q)) + (l & 3), col = nt * 8 + (l >> 2);
@@ -358,11 +358,11 @@ __global__ void __launch_bounds__(LTH, 2)
   }
 
   const int m = lane >> 2, kq = lane & 3;
-  double gx[NB8][NB8][2], gt[NTT][2];
+  double gx[NB8][NO8][2], gt[NTT][2];
 #pragma unroll
   for (int ti = 0; ti < NB8; ++ti)
 #pragma unroll
-    for (int tj = 0; tj < NB8; ++tj) gx[ti][tj][0] = gx[ti][tj][1] = 0.0;
+    for (int tj = 0; tj < NO8; ++tj) gx[ti][tj][0] = gx[ti][tj][1] = 0.0;
 #pragma unroll
   for (int t = 0; t < NTT; ++t) gt[t][0] = gt[t][1] = 0.0;
   double* const T = sT + warp * 8 * TS;
@@ -382,16 +382,16 @@ __global__ void __launch_bounds__(LTH, 2)
       rsy = in.rs[0];
     } else {
       // ---- out tile: m-tile `warp`, all n-tiles (NB8 independent chains)
-      double acc[NB8][2];
+      double acc[NO8][2];
 #pragma unroll
-      for (int nt = 0; nt < NB8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      for (int nt = 0; nt < NO8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
       if (in.ident) {
         // TA = I: start from the Y rows (accumulator layout: row m, columns
         // 2 kq, 2 kq + 1), Y2's after Y1's columns
         const double* y = sb + in.off[0] + (warp * 8 + m) * in.rs[0];
         const int c1 = in.cols[0];
 #pragma unroll
-        for (int nt = 0; nt < NB8; ++nt) {
+        for (int nt = 0; nt < NO8; ++nt) {
           const int col = nt * 8 + 2 * kq;
           if (col < c1) acc[nt][0] = y[col];
           if (col + 1 < c1) acc[nt][1] = y[col + 1];
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(LTH, 2)
           const int c2 = in.cols[1];
           const double* y2 = sb + in.off[1] + (warp * 8 + m) * in.rs[1];
 #pragma unroll
-          for (int nt = 0; nt < NB8; ++nt) {
+          for (int nt = 0; nt < NO8; ++nt) {
             const int col = nt * 8 + 2 * kq;
             if (col >= c1 && col < c1 + c2) acc[nt][0] = y2[col - c1];
             if (col + 1 >= c1 && col + 1 < c1 + c2) acc[nt][1] = y2[col + 1 - c1];
@@ -414,13 +414,13 @@ __global__ void __launch_bounds__(LTH, 2)
         for (int ks = k0; ks < k1; ++ks) {
           const double a0 = pa[4 * (ks - k0)];
 #pragma unroll
-          for (int nt = 0; nt < NB8; ++nt)
-            dmma884(acc[nt][0], acc[nt][1], a0, sB[(ks * NB8 + nt) * 32 + lane]);
+          for (int nt = 0; nt < NO8; ++nt)
+            dmma884(acc[nt][0], acc[nt][1], a0, sB[(ks * NO8 + nt) * 32 + lane]);
         }
       }
       const long row = w0 + m;
 #pragma unroll
-      for (int nt = 0; nt < NB8; ++nt) {
+      for (int nt = 0; nt < NO8; ++nt) {
         const double v0 = acc[nt][0], v1 = acc[nt][1];
         const int col = nt * 8 + 2 * kq;
         // rows past n (halo rows, possibly a neighbour slab's) stay out of the Grams
@@ -441,20 +441,20 @@ __global__ void __launch_bounds__(LTH, 2)
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int cl = 4 * s + kq;  // k index = this lane's cell
-        double bf[NB8];
+        double bf[NO8];
         if (copy_y) {
           // Gram-only: B = diag(w) [Y1 | Y2]; rows past n contribute nothing
           const bool live = w0 + cl < n;
           const double wv = in.w ? sb[in.woff + warp * 8 + cl] : 1.0;
           if (y2 < 0) {
 #pragma unroll
-            for (int tj = 0; tj < NB8; ++tj)
+            for (int tj = 0; tj < NO8; ++tj)
               bf[tj] = live ? wv * sy[cl * rsy + tj * 8 + m] : 0.0;
           } else {
             const int c1 = in.cols[0];
             const double* s2 = sb + sel3(in.off, y2) + (warp * 8 + cl) * sel3(in.rs, y2);
 #pragma unroll
-            for (int tj = 0; tj < NB8; ++tj) {
+            for (int tj = 0; tj < NO8; ++tj) {
               const int col = tj * 8 + m;
               const double v = col < c1 ? sy[cl * rsy + col]
                                : col - c1 < sel3(in.cols, y2) ? s2[col - c1] : 0.0;
@@ -463,22 +463,22 @@ __global__ void __launch_bounds__(LTH, 2)
           }
         } else {
 #pragma unroll
-          for (int tj = 0; tj < NB8; ++tj) bf[tj] = sy[cl * rsy + tj * 8 + m];
+          for (int tj = 0; tj < NO8; ++tj) bf[tj] = sy[cl * rsy + tj * 8 + m];
         }
 #pragma unroll
         for (int ti = 0; ti < NB8; ++ti) {
           if (ti < XT) {
             const double a = sx[cl * rsx + ti * 8 + m];
 #pragma unroll
-            for (int tj = 0; tj < NB8; ++tj) dmma884(gx[ti][tj][0], gx[ti][tj][1], a, bf[tj]);
+            for (int tj = 0; tj < NO8; ++tj) dmma884(gx[ti][tj][0], gx[ti][tj][1], a, bf[tj]);
           }
         }
         if (!skip_tt) {
           // out^T out: the A fragment of row tile ti is the B fragment of tile ti
 #pragma unroll
-          for (int ti = 0, t = 0; ti < NB8; ++ti)
+          for (int ti = 0, t = 0; ti < NO8; ++ti)
 #pragma unroll
-            for (int tj = ti; tj < NB8; ++tj, ++t) dmma884(gt[t][0], gt[t][1], bf[ti], bf[tj]);
+            for (int tj = ti; tj < NO8; ++tj, ++t) dmma884(gt[t][0], gt[t][1], bf[ti], bf[tj]);
         }
       }
     }
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(LTH, 2)
     for (int ti = 0; ti < NB8; ++ti) {
       const int rrow = ti * 8 + m;
 #pragma unroll
-      for (int tj = 0; tj < NB8; ++tj) {
+      for (int tj = 0; tj < NO8; ++tj) {
         const int c = tj * 8 + col;
         if (ti < XT && rrow < xcn) {
           if (c < nb) o[(size_t)rrow * nb + c] = gx[ti][tj][0];
@@ -503,9 +503,9 @@ __global__ void __launch_bounds__(LTH, 2)
     if (!skip_tt) {
       double* ot = o + (size_t)xcn * nb;
 #pragma unroll
-      for (int ti = 0, t = 0; ti < NB8; ++ti)
+      for (int ti = 0, t = 0; ti < NO8; ++ti)
 #pragma unroll
-        for (int tj = ti; tj < NB8; ++tj, ++t) {
+        for (int tj = ti; tj < NO8; ++tj, ++t) {
           const int rrow = ti * 8 + m, c = tj * 8 + col;
           if (rrow < nb) {
             if (c < nb) ot[(size_t)rrow * nb + c] = gt[t][0];
@@ -586,11 +586,16 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   // barrier was 7.7 % of the CTA variant's stall samples; at 256^3 r = 20 the
   // two augmentations take 9.05 instead of 9.88 ms. The rotation's U^T U
   // alone (no X) stays on the CTA variant, which is faster there.)
-  const bool PW = PWOK && (gram_only || (grams != nullptr && X.p != nullptr &&
-                                         !getenv("PND_LINCOMB_CTA_GRAMS")));
+  // one output tile against a wider X (the CGS passes of a one-column
+  // increment): the per-warp kernel with its out tile, B fragments and Grams
+  // sized for 8 columns, with or without Grams
+  const bool narrow = !gram_only && NB8 > 1 && nb <= 8 && X.p != nullptr;
+  const bool PW = narrow || (PWOK && (gram_only || (grams != nullptr && X.p != nullptr &&
+                                                   !getenv("PND_LINCOMB_CTA_GRAMS"))));
+  const int no8 = narrow ? 1 : NB8;
   int tb = 2;  // out-tile buffers
-  size_t tile = PW ? (size_t)LCW * 8 * TS : 2 * (size_t)LCH * TS;
-  size_t fixed = ((size_t)ks * NB8 * 32 + tile) * sizeof(double) + sizeof(LBars);
+  size_t tile = PW ? (size_t)LCW * 8 * (narrow ? lpad4(8) : TS) : 2 * (size_t)LCH * TS;
+  size_t fixed = ((size_t)ks * no8 * 32 + tile) * sizeof(double) + sizeof(LBars);
   // two CTAs per SM: keep the whole CTA under ~113 KB
   const size_t cap = 113 * 1024;
   int nstg = 0;
@@ -610,8 +615,9 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
   auto kern = lincomb_kernel<NB8>;
   if (tb == 1) kern = lincomb_kernel<NB8, 1>;
+  if (narrow) kern = lincomb_pw_kernel<NB8, 1>;
   if constexpr (PWOK) {
-    if (PW) kern = lincomb_pw_kernel<NB8>;
+    if (PW && !narrow) kern = lincomb_pw_kernel<NB8>;
   }
   allow_max_smem(kern);
   const int nblk = occupancy_cached((const void*)kern, LTH, smem);

@@ -720,6 +720,37 @@ __global__ void coeff_kernel(const double* g, const double* sig, int m, double* 
 
 __global__ void init_int(int* p, int v) { *p = v; }
 
+// One material class and one beam: dK = dt (psi/S) w^T with w = N^T rows (a
+// b-vector), so span((I - U0 U0^T) dK) = span((I - U0 U0^T) z) for the single
+// column z = dt |w| psi/S -- zero exactly when dK is. zscale: s = dt |w|_2.
+__global__ void zscale_kernel(const double* __restrict__ atomic, const double* __restrict__ rows,
+                              int b, double dt, double* s) {
+  double v = 0.0;
+  for (int j = threadIdx.x; j < b; j += 32) {
+    double w = 0.0;
+    for (int i = 0; i < 12; ++i) w = fma(atomic[i], rows[i * b + j], w);
+    v = fma(w, w, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x == 0) s[0] = dt * sqrt(v);
+}
+
+// z = s psi / S (column 0; the padding column of the even stride is zero)
+__global__ void zcol_kernel(int n, const double* __restrict__ s, const double* __restrict__ inv_s,
+                            const double* __restrict__ psi, NMat z) {
+  const double sc = s[0];
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const double2 v{sc * inv_s[c] * psi[c], 0.0};
+    *reinterpret_cast<double2*>(z.p + (size_t)c * 2) = v;
+  }
+}
+
+// U0^T z = s U0^T diag(1/S) psi (u: stride us)
+__global__ void zcoef_kernel(const double* __restrict__ s, const double* __restrict__ u, int us,
+                             int a, double* out) {
+  for (int i = threadIdx.x; i < a; i += blockDim.x) out[i] = s[0] * u[(size_t)i * us];
+}
+
 // per-cell weight of Gram i: [cls == i] / S (phase < 0) or wtab[cls][phase] / S;
 // zero past n (the chunked staging reads up to 64 rows beyond)
 __global__ void class_weight_kernel(const int* cls, const double* wtab, const double* inv_s, int n,
@@ -767,25 +798,33 @@ void scattering_step(Handle& h, double dt) {
 
   // substep 2 increment: dK = dt src_rows(V0) = dt Z rows  (dlra.py:303; K1 = U0 S0 + dK)
   // with the source rows Z[c][b*12 + i] = N_{cls,i} psi_b / S materialised once
-  const NMat dK = h.W2.view(g, b, st);
   phase(h, PH_SCATK1);
-  NMat Z{};
+  NMat Z{}, dK{};
   bool forked = false;
+  double* C1 = slot(h, S_C1, (size_t)a * b + 72);
+  double* zs = C1 + 64;  // rank one: the scale s of z (C1 holds U0^T z, a <= 64)
   if (rank1) {
-    // dK (memory-bound, on the side stream) overlaps the B_0 / projection Gram
-    // pass below (reads only U0 and psi); joined before dK is used
+    // the increment's one direction z (memory-bound, on the side stream)
+    // overlaps the B_0 / projection Gram pass below (reads only U0 and psi);
+    // joined before z is used
+    zscale_kernel<<<1, 32, 0, st>>>(h.cls_atomic.p, rows, b, dt, zs);
+    launched();
     CK(cudaEventRecord(h.ev_fork, st));
     CK(cudaStreamWaitEvent(h.st2, h.ev_fork, 0));
-    scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, 1, h.psi.p, 1, rows, dK, h.st2);
+    dK = h.Xs.view(g, 1, h.st2);
+    zcol_kernel<<<sm_count() * 8, 256, 0, h.st2>>>(g.n, zs, h.inv_s.p, h.psi.p, dK);
+    launched();
     CK(cudaEventRecord(h.ev_join, h.st2));
     forked = true;
   } else if (B > 0) {
+    dK = h.W2.view(g, b, st);
     Z = h.Xs.view(g, 12 * B, st);
     source_rows(g, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.psi.p, B, Z, st);
     double* TAz = slot(h, S_TAZ, (size_t)12 * B * b);
     axpby(12 * B * b, dt, rows, 0.0, TAz, st);
     lincomb(g, Z, NMat{}, NMat{}, TAz, nullptr, dK, nullptr, h.part, st);
   } else {
+    dK = h.W2.view(g, b, st);
     scat_dk(g, dt, h.inv_s.p, h.cls.p, h.cls_atomic.p, h.n_cls, nullptr, 0, rows, dK, st);
   }
 
@@ -803,12 +842,15 @@ void scattering_step(Handle& h, double dt) {
                            a * sizeof(double), a, cudaMemcpyDeviceToDevice, st));
       gemm(a, 12, 1, 1.0, Mat{Hu + a, a + 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0,
            rowm(left, 12), 0, 1, st);
+      zcoef_kernel<<<1, 64, 0, st>>>(zs, Hu + a, a + 1, a, C1);
     } else {  // 64 columns: the Gram-only pass takes at most 64
       gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);
       gram_xy(g, U0, psi_col, Hu, h.part, st, h.inv_s.p);
       gemm(a, 12, 1, 1.0, Mat{Hu, 1, 1}, 0, rowm(h.cls_atomic.p, 12), 0, 0.0, rowm(left, 12), 0,
            1, st);
+      zcoef_kernel<<<1, 64, 0, st>>>(zs, Hu, 1, a, C1);
     }
+    launched();
   } else if (h.n_cls == 1) {
     gram_xy(g, U0, U0, H, h.part, st, h.inv_s.p);  // one class: U0^T diag(1/S) U0
   } else if (a > 32) {
@@ -848,13 +890,12 @@ void scattering_step(Handle& h, double dt) {
   phase(h, PH_SCATGRAM);
   if (B > 0 && !rank1) gram_xy(g, U0, Z, left, h.part, st);
   phase(h, PH_SCATSMALL);
-  // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass)
-  double* C1 = slot(h, S_C1, (size_t)a * b);
-  if (B > 0) {
+  // C1 = U0^T dK = dt sum_b left_b rows_b  (no n-side pass; rank one: U0^T z above)
+  if (B > 0 && !rank1) {
     for (int beam = 0; beam < B; ++beam)
       gemm(a, b, 12, dt, Mat{left + beam * 12, 12 * B, 1}, 0, rowm(rows + (size_t)beam * 12 * b, b),
            0, beam == 0 ? 0.0 : 1.0, rowm(C1, b), 0, 1, st);
-  } else {
+  } else if (B == 0) {
     fill_zero(C1, (size_t)a * b, st);
   }
   double* coeffs = slot(h, S_COEF, (size_t)12 * m);
@@ -881,7 +922,8 @@ void scattering_step(Handle& h, double dt) {
   // substep 2: U^ = [U0 | orth((I - U0 U0^T) dK)]
   phase(h, PH_ORTH);
   if (forked) CK(cudaStreamWaitEvent(st, h.ev_join, 0));  // dK from the side stream
-  // rank(dK) <= rank of the source rows: one per (material class, beam)
+  // rank(dK) <= rank of the source rows: one per (material class, beam);
+  // rank one: the column z spans it
   const int bound = rank1 ? 1 : (long)h.n_cls * B < b ? h.n_cls * B : b;
   const int k = orth_complement(h, dK, C1, NMat{}, bound);
   const int ru = a + k;

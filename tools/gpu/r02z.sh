@@ -1,2 +1,5 @@
-timeout 1200 python tools/adaptive_run.py 128 6.4 3e-5 200 gpurun_out/r02z_adaptive_128_3e-5.json > gpurun_out/r02z_adaptive_128_3e-5.txt 2>&1
-timeout 1900 python tools/adaptive_run.py 256 6.4 1e-4 200 gpurun_out/r02z_adaptive_256_1e-4.json > gpurun_out/r02z_adaptive_256_1e-4.txt 2>&1
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/r02z_tests.txt 2>&1
+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/r02z_bench.json 2> gpurun_out/r02z_bench.err
+/usr/local/cuda/bin/ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02z_launches.csv timeout 600 python bench.py --steps 3 --warmup 1 --no-cpu-baseline --no-config1 > /dev/null 2>&1
+echo done
