@@ -540,6 +540,83 @@ __global__ void __launch_bounds__(256) lreduce(const double* __restrict__ partia
   }
 }
 
+// One output column (the CGS passes of a one-column increment):
+//   out = y ta - X tb  (ident: ta = 1), Grams [X^T out ; out^T out]
+// The contraction is a 1 x XC dot product per cell -- FP64 FMAs on the CUDA
+// cores, not tensor-core tiles padded to 8 output columns. One thread per
+// cell, its X row read straight from global memory (the warp's 32 rows are
+// one contiguous span, every sector used across the row's loads), two cells
+// per thread in flight; Gram partials reduced per warp, summed by lreduce.
+constexpr int L1TH = 256;
+template <int XCM>
+__global__ void __launch_bounds__(L1TH, 2)
+    lincomb1_kernel(int n, const double* __restrict__ y, int rsy, const double* __restrict__ X,
+                    int rsx, int xc, const double* __restrict__ TA, const double* __restrict__ TB,
+                    NMat out, double* __restrict__ partial) {
+  __shared__ double sc[XCM];
+  for (int j = threadIdx.x; j < XCM; j += blockDim.x) sc[j] = j < xc ? TB[j] : 0.0;
+  const double ta = TA ? TA[0] : 1.0;
+  __syncthreads();
+  double gx[XCM], gt = 0.0;
+#pragma unroll
+  for (int j = 0; j < XCM; ++j) gx[j] = 0.0;
+  const long stride = (long)gridDim.x * blockDim.x;
+  for (long c = (long)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += stride) {
+    const double* xr = X + c * rsx;
+    double x[XCM];
+#pragma unroll
+    for (int j = 0; j < XCM; j += 2) {
+      if (j < xc) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xr + j));
+        x[j] = v.x;
+        x[j + 1] = v.y;
+      } else {
+        x[j] = x[j + 1] = 0.0;
+      }
+    }
+    double v = ta * __ldg(y + c * rsy);
+#pragma unroll
+    for (int j = 0; j < XCM; ++j) v = fma(-sc[j], x[j], v);
+    if (out.p) *reinterpret_cast<double2*>(out.p + c * out.rs) = make_double2(v, 0.0);
+    if (partial) {
+#pragma unroll
+      for (int j = 0; j < XCM; ++j) gx[j] = fma(x[j], v, gx[j]);
+      gt = fma(v, v, gt);
+    }
+  }
+  if (!partial) return;
+  const int lane = threadIdx.x & 31;
+  double* o = partial + ((size_t)blockIdx.x * (L1TH / 32) + (threadIdx.x >> 5)) * (xc + 1);
+#pragma unroll
+  for (int j = 0; j < XCM; ++j) {
+    double t = gx[j];
+    for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
+    if (lane == 0 && j < xc) o[j] = t;
+  }
+  for (int s = 16; s > 0; s >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, s);
+  if (lane == 0) o[xc] = gt;
+}
+
+template <int XCM>
+void lincomb1_launch(const Geom& g, NMat Y1, NMat X, const double* TA, const double* TB, NMat out,
+                     double* grams, DBuf& partial, cudaStream_t st) {
+  auto kern = lincomb1_kernel<XCM>;
+  const int nblk = occupancy_cached((const void*)kern, L1TH, 0);
+  int grid = sm_count() * nblk;
+  const int need = (g.n + L1TH - 1) / L1TH;
+  if (grid > need) grid = need;
+  const size_t count = (size_t)X.cols + 1;
+  const int nparts = grid * (L1TH / 32);
+  double* part = grams ? partial.get(count * nparts) : nullptr;
+  kern<<<grid, L1TH, 0, st>>>(g.n, Y1.p, Y1.rs, X.p, X.rs, X.cols, TA, TB, out, part);
+  launched();
+  if (grams) {
+    lreduce<<<(int)((count + 31) / 32), dim3(32, 8), 0, st>>>(part, nparts, (int)count, grams);
+    launched();
+    comm_allreduce(g, grams, count, st);
+  }
+}
+
 template <int NB8>
 void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const double* TB,
                     NMat out, double* grams, DBuf& partial, cudaStream_t st, bool gram_only,
@@ -646,6 +723,13 @@ void lincomb(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, const do
   const int K = Y1.cols + (Y2.p ? Y2.cols : 0) + (X.p ? X.cols : 0);
   if (K > 128) fail(PND_ECONFIG, "lincomb supports at most 128 input columns");
   if (grams && X.p && X.cols > 64) fail(PND_ECONFIG, "lincomb Grams support at most 64 X columns");
+  if (out.cols == 1 && out.p && Y1.cols == 1 && !(Y2.p && Y2.cols > 0) && X.p && X.cols > 0 &&
+      X.cols <= 32 && X.rs % 2 == 0 && out.rs == 2 && !getenv("PND_LINCOMB1_OFF")) {
+    if (X.cols <= 8) return lincomb1_launch<8>(g, Y1, X, TA, TB, out, grams, partial, st);
+    if (X.cols <= 16) return lincomb1_launch<16>(g, Y1, X, TA, TB, out, grams, partial, st);
+    if (X.cols <= 24) return lincomb1_launch<24>(g, Y1, X, TA, TB, out, grams, partial, st);
+    return lincomb1_launch<32>(g, Y1, X, TA, TB, out, grams, partial, st);
+  }
   switch ((w + 7) / 8) {
     case 1: lincomb_launch<1>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
     case 2: lincomb_launch<2>(g, Y1, Y2, X, TA, TB, out, grams, partial, st, false); break;
