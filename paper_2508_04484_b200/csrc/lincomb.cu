@@ -547,14 +547,16 @@ __global__ void __launch_bounds__(256) lreduce(const double* __restrict__ partia
 // cell, its X row read straight from global memory (the warp's 32 rows are
 // one contiguous span, every sector used across the row's loads), two cells
 // per thread in flight; Gram partials reduced per warp, summed by lreduce.
+// Gram-only (out.p null, TB null): X^T diag(w) y.
 constexpr int L1TH = 256;
 template <int XCM>
 __global__ void __launch_bounds__(L1TH, 2)
     lincomb1_kernel(int n, const double* __restrict__ y, int rsy, const double* __restrict__ X,
                     int rsx, int xc, const double* __restrict__ TA, const double* __restrict__ TB,
-                    NMat out, double* __restrict__ partial) {
+                    NMat out, double* __restrict__ partial, const double* __restrict__ w,
+                    int gram_only) {
   __shared__ double sc[XCM];
-  for (int j = threadIdx.x; j < XCM; j += blockDim.x) sc[j] = j < xc ? TB[j] : 0.0;
+  for (int j = threadIdx.x; j < XCM; j += blockDim.x) sc[j] = TB && j < xc ? TB[j] : 0.0;
   const double ta = TA ? TA[0] : 1.0;
   __syncthreads();
   double gx[XCM], gt = 0.0;
@@ -579,36 +581,41 @@ __global__ void __launch_bounds__(L1TH, 2)
     for (int j = 0; j < XCM; ++j) v = fma(-sc[j], x[j], v);
     if (out.p) *reinterpret_cast<double2*>(out.p + c * out.rs) = make_double2(v, 0.0);
     if (partial) {
+      const double vg = w ? v * __ldg(w + c) : v;
 #pragma unroll
-      for (int j = 0; j < XCM; ++j) gx[j] = fma(x[j], v, gx[j]);
+      for (int j = 0; j < XCM; ++j) gx[j] = fma(x[j], vg, gx[j]);
       gt = fma(v, v, gt);
     }
   }
   if (!partial) return;
   const int lane = threadIdx.x & 31;
-  double* o = partial + ((size_t)blockIdx.x * (L1TH / 32) + (threadIdx.x >> 5)) * (xc + 1);
+  double* o = partial + ((size_t)blockIdx.x * (L1TH / 32) + (threadIdx.x >> 5)) *
+                             (xc + (gram_only ? 0 : 1));
 #pragma unroll
   for (int j = 0; j < XCM; ++j) {
     double t = gx[j];
     for (int s = 16; s > 0; s >>= 1) t += __shfl_xor_sync(0xffffffffu, t, s);
     if (lane == 0 && j < xc) o[j] = t;
   }
+  if (gram_only) return;
   for (int s = 16; s > 0; s >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, s);
   if (lane == 0) o[xc] = gt;
 }
 
 template <int XCM>
 void lincomb1_launch(const Geom& g, NMat Y1, NMat X, const double* TA, const double* TB, NMat out,
-                     double* grams, DBuf& partial, cudaStream_t st) {
+                     double* grams, DBuf& partial, cudaStream_t st, const double* w = nullptr) {
+  const bool gram_only = out.p == nullptr;
   auto kern = lincomb1_kernel<XCM>;
   const int nblk = occupancy_cached((const void*)kern, L1TH, 0);
   int grid = sm_count() * nblk;
   const int need = (g.n + L1TH - 1) / L1TH;
   if (grid > need) grid = need;
-  const size_t count = (size_t)X.cols + 1;
+  const size_t count = (size_t)X.cols + (gram_only ? 0 : 1);
   const int nparts = grid * (L1TH / 32);
   double* part = grams ? partial.get(count * nparts) : nullptr;
-  kern<<<grid, L1TH, 0, st>>>(g.n, Y1.p, Y1.rs, X.p, X.rs, X.cols, TA, TB, out, part);
+  kern<<<grid, L1TH, 0, st>>>(g.n, Y1.p, Y1.rs, X.p, X.rs, X.cols, TA, TB, out, part, w,
+                              gram_only ? 1 : 0);
   launched();
   if (grams) {
     lreduce<<<(int)((count + 31) / 32), dim3(32, 8), 0, st>>>(part, nparts, (int)count, grams);
@@ -769,6 +776,8 @@ void gram_xy(const Geom& g, NMat X, NMat Y, double* out, DBuf& partial, cudaStre
   const int w = Y.cols > X.cols ? Y.cols : X.cols;
   if (w > 64) fail(PND_ECONFIG, "Grams support at most 64 columns");
   const NMat none{}, o{nullptr, 0, Y.cols};
+  if (Y.cols == 1 && X.cols <= 8 && X.rs % 2 == 0 && !getenv("PND_LINCOMB1_OFF"))
+    return lincomb1_launch<8>(g, Y, X, nullptr, nullptr, o, out, partial, st, weight);
   switch ((w + 7) / 8) {
     case 1: lincomb_launch<1>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
     case 2: lincomb_launch<2>(g, Y, none, X, nullptr, nullptr, o, out, partial, st, true, weight); break;
