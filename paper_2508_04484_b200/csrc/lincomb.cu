@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(LTH, NB8 >= 7 ? 1 : 2)
 // tile (only __syncwarp), and in Gram-only mode the staged Y rows are the B
 // operand directly. The out^T out A and B fragments are the same loads. Each
 // warp writes its own partial; lreduce sums grid x 8 partials in fixed order.
-template <int NB8, int NO8 = NB8>
+// SYM (Gram-only, X = Y1, Y1 covering every out tile but the last): the
+// tiles below the diagonal are mirrors -- not formed (left zero), copied
+// after the reduction (mirror_tiles_kernel).
+template <int NB8, int NO8 = NB8, bool SYM = false>
 __global__ void __launch_bounds__(LTH, 2)
     lincomb_pw_kernel(int n, LIn in, const double* __restrict__ TA, const double* __restrict__ TB,
                       int ny, int nb, NMat out, int nstg, int grams, int copy_y, int skip_tt,
@@ -470,7 +473,8 @@ __global__ void __launch_bounds__(LTH, 2)
           if (ti < XT) {
             const double a = sx[cl * rsx + ti * 8 + m];
 #pragma unroll
-            for (int tj = 0; tj < NO8; ++tj) dmma884(gx[ti][tj][0], gx[ti][tj][1], a, bf[tj]);
+            for (int tj = 0; tj < NO8; ++tj)
+              if (!(SYM && tj < ti)) dmma884(gx[ti][tj][0], gx[ti][tj][1], a, bf[tj]);
           }
         }
         if (!skip_tt) {
@@ -517,6 +521,15 @@ __global__ void __launch_bounds__(LTH, 2)
           }
         }
     }
+  }
+}
+
+// the mirrored tiles of a symmetric Gram-only pass: rows r of X against
+// out columns c < r in an earlier tile
+__global__ void mirror_tiles_kernel(double* g, int xc, int nb) {
+  for (int e = threadIdx.x; e < xc * nb; e += blockDim.x) {
+    const int r = e / nb, c = e - r * nb;
+    if (c / 8 < r / 8) g[e] = g[(size_t)c * nb + r];
   }
 }
 
@@ -699,9 +712,12 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   const size_t smem = fixed + (size_t)nstg * in.stage * sizeof(double);
   auto kern = lincomb_kernel<NB8>;
   if (tb == 1) kern = lincomb_kernel<NB8, 1>;
+  // symmetric Gram-only pass: every out tile below the diagonal lies in Y1
+  const bool sym = PWOK && gram_only && same && NB8 > 1 && Y1.cols >= 8 * (NB8 - 1) &&
+                   !getenv("PND_LINCOMB_NOSYM");
   if (narrow) kern = lincomb_pw_kernel<NB8, 1>;
   if constexpr (PWOK) {
-    if (PW && !narrow) kern = lincomb_pw_kernel<NB8>;
+    if (PW && !narrow) kern = sym ? lincomb_pw_kernel<NB8, NB8, true> : lincomb_pw_kernel<NB8>;
   }
   allow_max_smem(kern);
   const int nblk = occupancy_cached((const void*)kern, LTH, smem);
@@ -718,6 +734,10 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   if (grams) {
     lreduce<<<(int)((count + 31) / 32), dim3(32, 8), 0, st>>>(part, nparts, (int)count, grams);
     launched();
+    if (sym) {
+      mirror_tiles_kernel<<<1, 256, 0, st>>>(grams, xcn, nb);
+      launched();
+    }
     comm_allreduce(g, grams, count, st);
   }
 }
