@@ -715,7 +715,8 @@ void lincomb_launch(const Geom& g, NMat Y1, NMat Y2, NMat X, const double* TA, c
   // symmetric Gram-only pass: every out tile below the diagonal lies in Y1
   // (large grids: on small ones the mirror launch costs more than it saves)
   const bool sym = PWOK && gram_only && same && NB8 > 1 && Y1.cols >= 8 * (NB8 - 1) &&
-                   g.n >= (1 << 18) && !getenv("PND_LINCOMB_NOSYM");
+                   (g.n >= (1 << 18) || getenv("PND_LINCOMB_SYM")) &&
+                   !getenv("PND_LINCOMB_NOSYM");
   if (narrow) kern = lincomb_pw_kernel<NB8, 1>;
   if constexpr (PWOK) {
     if (PW && !narrow) kern = sym ? lincomb_pw_kernel<NB8, NB8, true> : lincomb_pw_kernel<NB8>;
