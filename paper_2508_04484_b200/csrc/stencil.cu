@@ -1194,26 +1194,31 @@ ERows e_rows(int L) {
 }
 
 // boundary cells b of one axis -> Xb[b] = X[c], Zb[b] = sigma_c sum_d E[i][i+d] X[c + d s]
-__global__ void e_gather_kernel(int n, int L, long s, ERows er, NMat X1, NMat X2,
+// (one warp row per boundary cell, lanes over the columns; 32-bit cell
+// arithmetic: the 64-bit divisions of a flat element index dominated)
+__global__ void e_gather_kernel(int n, int L, int s, ERows er, NMat X1, NMat X2,
                                 const double* __restrict__ isp, NMat Xb, NMat Zb) {
-  const long M = n / L;
-  const long nb = er.nb * M;
+  const int M = n / L;
+  const int nb = er.nb * M;
   const int a1 = X1.cols, w = a1 + (X2.p ? X2.cols : 0);
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < nb * w;
-       e += (long)gridDim.x * blockDim.x) {
-    const long b = e / w;
-    const int col = (int)(e - b * w);
-    const int p = (int)(b / M);
-    const long q = b - (long)p * M;
-    const long c = (q / s) * (s * L) + er.row[p] * s + (q % s);
-    auto at = [&](long cc) {
-      return col < a1 ? X1.p[cc * X1.rs + col] : X2.p[cc * X2.rs + col - a1];
-    };
-    double z = 0.0;
-    for (int d = 0; d < 5; ++d)
-      if (er.e[p][d] != 0.0) z += er.e[p][d] * at(c + (d - 2) * s);
-    Xb.p[b * Xb.rs + col] = at(c);
-    Zb.p[b * Zb.rs + col] = isp[2 * c] * z;
+  for (int b = blockIdx.x * blockDim.y + threadIdx.y; b < nb; b += gridDim.x * blockDim.y) {
+    const int p = b / M;
+    const int q = b - p * M;
+    const long c = (long)(q / s) * ((long)s * L) + (long)er.row[p] * s + (q % s);
+    double e[5];
+#pragma unroll
+    for (int d = 0; d < 5; ++d) e[d] = er.e[p][d];
+    const double sc = isp[2 * c];
+    for (int col = threadIdx.x; col < w; col += 32) {
+      const double* base = col < a1 ? X1.p + col : X2.p + (col - a1);
+      const long rs = col < a1 ? X1.rs : X2.rs;
+      double z = 0.0;
+#pragma unroll
+      for (int d = 0; d < 5; ++d)
+        if (e[d] != 0.0) z += e[d] * base[(c + (d - 2) * (long)s) * rs];
+      Xb.p[(long)b * Xb.rs + col] = base[c * rs];
+      Zb.p[(long)b * Zb.rs + col] = sc * z;
+    }
   }
 }
 
@@ -1249,12 +1254,17 @@ void minus_from_plus(const Geom& g, NMat X1, NMat X2, const double* isp, double*
     const size_t rows = (size_t)nb + 2 * 64;
     double* buf = nullptr;
     CK(cudaMallocAsync((void**)&buf, 2 * rows * rs * sizeof(double), st));
-    fill_zero(buf, 2 * rows * rs, st);
+    if (rs > w) {
+      fill_zero(buf, 2 * rows * rs, st);  // the padding column too
+    } else {  // the gather writes every row: zero only the 64-row margins
+      for (size_t m0 : {(size_t)0, (size_t)nb + 64, rows, rows + (size_t)nb + 64})
+        fill_zero(buf + m0 * rs, 64 * (size_t)rs, st);
+    }
     NMat Xb{buf + 64 * (size_t)rs, rs, w}, Zb{buf + (rows + 64) * (size_t)rs, rs, w};
-    long tot = nb * w;
-    int grid = (int)((tot + 255) / 256);
+    int grid = (int)((nb + 7) / 8);
     if (grid > 148 * 16) grid = 148 * 16;
-    e_gather_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(g.n, L, s, er, X1, X2, isp, Xb, Zb);
+    e_gather_kernel<<<grid > 0 ? grid : 1, dim3(32, 8), 0, st>>>(g.n, L, (int)s, er, X1, X2, isp,
+                                                                 Xb, Zb);
     launched();
     gram_xy(gb, Xb, Zb, corr, partial, st);
     minus_assemble_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(out, w, ai, corr, g.i2h[axis]);
