@@ -1254,8 +1254,8 @@ void minus_from_plus(const Geom& g, NMat X1, NMat X2, const double* isp, double*
     const size_t rows = (size_t)nb + 2 * 64;
     double* buf = nullptr;
     CK(cudaMallocAsync((void**)&buf, 2 * rows * rs * sizeof(double), st));
-    if (rs > w) {
-      fill_zero(buf, 2 * rows * rs, st);  // the padding column too
+    if (rs > w || rows < (1 << 16)) {
+      fill_zero(buf, 2 * rows * rs, st);  // the padding column too / one launch on small grids
     } else {  // the gather writes every row: zero only the 64-row margins
       for (size_t m0 : {(size_t)0, (size_t)nb + 64, rows, rows + (size_t)nb + 64})
         fill_zero(buf + m0 * rs, 64 * (size_t)rs, st);
